@@ -1,0 +1,148 @@
+/*
+ * vsb200.h -- C ABI of libvsb200.so, the B200 (sm_100a) implementation of the voxelskip
+ * empty-space-skipping hot path (arXiv 1912.09596): TF classification -> hierarchy build
+ * (LBVH / macro grid / SVT k-d / binned k-d / hybrid) -> DVR ray march.
+ *
+ * The reference (`voxelskip`, /root/reference/pkg/src/voxelskip/) is a Python package, so its
+ * own "FFI" for this path is the Python call surface listed in SURVEY.md §8(b).  Each entry
+ * point below names the reference function it replaces; the Python package
+ * paper_1912_09596_b200 binds them through ctypes with the same names and semantics as the
+ * reference.
+ *
+ * Conventions
+ *  - Every pointer argument is a DEVICE pointer unless marked (host).  The library never
+ *    allocates or frees caller memory; scratch comes from *_workspace() queries (two-phase,
+ *    CUB style) and is passed back as (ws, ws_bytes).
+ *  - Every call takes an explicit stream (a cudaStream_t) and is asynchronous on it.
+ *  - Return value: 0 ok; negative = argument error (VS_E*); positive = a cudaError_t.
+ *    vs_last_error() returns the message of the last failure on the calling host thread.
+ *  - Volumes are C-order [x][y][z] (z fastest), as volume.py:64-81.  Scalar volumes are held
+ *    as uint8 LUT bins (quantize_scalar, volume.py:159-162, is the identity on u8 data).
+ *  - Bit volumes are packed along z: word (x, y, w) at (x*ny + y)*ceil(nz/32) + w, bit z&31.
+ *  - Boxes are half-open int32 [lo, hi) stored as (rows, 3).
+ *  - No floating-point atomics touch any parity output; results are deterministic.
+ */
+#ifndef VSB200_H
+#define VSB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* vs_stream_t; /* cudaStream_t */
+
+enum { VS_OK = 0, VS_EINVAL = -1, VS_ERANGE = -2, VS_EWORKSPACE = -3 };
+
+/* Transfer-function classification parameters (device copy read by the kernels, so a TF
+ * change is one 64-byte H2D and CUDA-graph replays stay valid).  Built on the host from the
+ * LUT alpha column by vs_tf_params_from_alpha: visible bin <=> lut[bin,3] > 0
+ * (classify, volume.py:307-319). */
+typedef struct vs_tf_params {
+  uint32_t vis[8];   /* 256-bit visibility mask, bit b = (alpha[b] > 0)                   */
+  int32_t mode;      /* 0 = table lookup, 1/2 = that many visibility changes, 3 = constant */
+  int32_t start;     /* visibility of bin 0                                                */
+  int32_t bound[2];  /* bins where visibility flips (ascending), modes 1/2                 */
+  int32_t nvisible;  /* number of visible bins                                             */
+  int32_t pad[3];
+} vs_tf_params;
+
+const char* vs_version(void);
+int vs_last_error(char* buf, size_t size);
+
+/* Host helper: alpha (host, 256 floats) -> params (host). */
+int vs_tf_params_from_alpha(const float* alpha256, vs_tf_params* out);
+
+/* ---- classification: volume.py:159-162 (quantize_scalar), 289-304 (_dilate26),
+ *      307-319 (classify), 322-324 (occupancy) ------------------------------------------ */
+
+/* quantize_scalar: floor(v*255 + 0.5) clipped to [0,255] in float64, f32 field -> u8 bins. */
+int vs_quantize_f32(const float* field, int64_t n, uint8_t* bins, vs_stream_t stream);
+
+/* Fused TF pass over the u8 bins, one read of the volume (fast path: nz % 16 == 0, 8^3
+ * bricks).  Per 8^3 brick it writes a 27-bit halo summary: bit (ex+1)*9+(ey+1)*3+(ez+1) is
+ * set iff the brick holds a visible voxel inside the 1-voxel halo of the neighbour brick at
+ * offset -e (e=-1: last slab, 0: anywhere, +1: first slab).  The dilated brick vote of
+ * flag_bricks(classify(dilate=True)) (lbvh.py:83-102) is then an OR over 27 neighbours, and
+ * bit 13 alone is the undilated vote.  Optionally writes the undilated packed bits; adds the
+ * count of visible voxels (occupancy numerator) to *count (caller zeroes it).
+ * summary: ceil(nx/8)*ceil(ny/8)*ceil(nz/8) uint32, C-order. */
+int vs_classify_summary(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
+                        uint32_t* summary, uint32_t* bits_opt, unsigned long long* count_opt,
+                        vs_stream_t stream);
+
+/* Generic-dims classification to packed undilated bits (+ optional visible count). */
+int vs_classify_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
+                     uint32_t* bits, unsigned long long* count_opt, vs_stream_t stream);
+
+/* _dilate26: 3x3x3 box OR, neighbourhood clipped at the borders.  in != out. */
+int vs_dilate_bits(const uint32_t* in, int nx, int ny, int nz, uint32_t* out,
+                   vs_stream_t stream);
+
+/* BinaryVolume.bits (bool bytes, C-order) <-> packed bits. */
+int vs_pack_bits(const uint8_t* bools, int nx, int ny, int nz, uint32_t* bits,
+                 vs_stream_t stream);
+int vs_unpack_bits(const uint32_t* bits, int nx, int ny, int nz, uint8_t* bools,
+                   vs_stream_t stream);
+/* count_nonzero(bits) added to *count (caller zeroes it). */
+int vs_count_bits(const uint32_t* bits, int nx, int ny, int nz, unsigned long long* count,
+                  vs_stream_t stream);
+
+/* Per-cell vote (any set bit), cells of edge cs clipped at the border, C-order bool bytes:
+ * flag_bricks' padded reshape-any (lbvh.py:93-95) and _macro_from_bits (svt.py:161-167). */
+int vs_vote_cells(const uint32_t* bits, int nx, int ny, int nz, int cs, uint8_t* flags,
+                  vs_stream_t stream);
+
+/* ---- Morton bitmap of non-empty bricks (the sorted order of build_lbvh, lbvh.py:226-229) --
+ * A brick grid of nb = (nbx,nby,nbz) bricks is addressed by Morton code in a cube of side
+ * P = vs_morton_side(nb) (power of two, >= 8).  Bit `code` of `bitmap` is the brick flag;
+ * tile_counts[t] = popcount of the 512-code tile t.  Because Morton codes of distinct bricks
+ * are distinct, increasing code order IS the reference's stable argsort of
+ * (code << 32 | scan_index). */
+int vs_morton_side(int nbx, int nby, int nbz);
+
+/* From the 27-bit summaries (dilate=1 -> flag_bricks(classify(dilate=True)); 0 -> undilated).
+ * Also writes the 16^3 macro-cell grid (derive_macro_grid(b, 16), svt.py:134-167) when
+ * cell16_opt != NULL: a 16-cell is exactly the OR of its 2x2x2 aligned 8-bricks. */
+int vs_summary_to_bitmap(const uint32_t* summary, int nx, int ny, int nz, int dilate, int P,
+                         uint32_t* bitmap, uint32_t* tile_counts, uint8_t* cell16_opt,
+                         vs_stream_t stream);
+
+/* From C-order brick flag bytes (any brick size). */
+int vs_flags_to_bitmap(const uint8_t* flags, int nbx, int nby, int nbz, int P,
+                       uint32_t* bitmap, uint32_t* tile_counts, vs_stream_t stream);
+
+/* BrickSet in scan (C) order (flag_bricks, lbvh.py:96-101): coords (n,3), codes (n,).
+ * *n_out (device int) receives n. */
+size_t vs_bricks_workspace(int nbx, int nby, int nbz);
+int vs_bricks_from_bitmap(const uint32_t* bitmap, int nbx, int nby, int nbz, int P,
+                          int32_t* coords, uint32_t* codes, int* n_out, void* ws,
+                          size_t ws_bytes, vs_stream_t stream);
+
+/* ---- LBVH: build_lbvh (lbvh.py:216-264) = Karras radix tree (lbvh.py:167-200) + refit
+ * (lbvh.py:203-213).  Outputs use the reference layout: rows 0..n-2 internal (Karras index),
+ * rows n-1..2n-2 the leaves in Morton order; left/right = -1 on leaves; leaf_brick = -1 on
+ * internal rows and 0..n-1 on leaves; brick_coords (n,3) Morton-sorted; root 0 (n>0).
+ * Capacities: rows >= 2*cap-1, brick_coords >= cap, where cap >= number of bricks.
+ * info (device int[2]) receives {n, height} (lbvh.py:128-144). */
+size_t vs_lbvh_workspace(int P, int64_t cap);
+int vs_lbvh_from_bitmap(const uint32_t* bitmap, const uint32_t* tile_counts, int P, int bs,
+                        int nx, int ny, int nz, int64_t cap, int32_t* lo, int32_t* hi,
+                        int32_t* left, int32_t* right, int32_t* leaf_brick,
+                        int32_t* brick_coords, int* info, void* ws, size_t ws_bytes,
+                        vs_stream_t stream);
+
+/* Arbitrary BrickSet (codes may repeat): keys = code << 32 | index, stable radix sort, then
+ * the same tree/refit.  n is known to the caller. */
+size_t vs_lbvh_bricks_workspace(int64_t n);
+int vs_lbvh_from_bricks(const int32_t* coords, const uint32_t* codes, int64_t n, int bs,
+                        int nx, int ny, int nz, int32_t* lo, int32_t* hi, int32_t* left,
+                        int32_t* right, int32_t* leaf_brick, int32_t* brick_coords, int* info,
+                        void* ws, size_t ws_bytes, vs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSB200_H */

@@ -1,0 +1,14 @@
+"""paper_1912_09596_b200 -- B200-native (sm_100a) empty-space-skipping build + render.
+
+Drop-in for the reference package ``voxelskip`` (/root/reference/pkg/src/voxelskip/__init__.py):
+the same public names, argument meanings, array layouts and exceptions, backed by
+hand-written CUDA kernels in libvsb200.so (include/vsb200.h).  There is no CPU fallback.
+"""
+
+from .lbvh import (BrickSet, Lbvh, MortonRangeError, build_lbvh, empty_lbvh, flag_bricks,
+                   leaf_boxes, morton_decode, morton_encode)
+from .svt import MacroGrid, derive_macro_grid
+from .volume import (Aabb, BinaryVolume, TransferFunction, UnsupportedFormatError, Volume,
+                     VolumeFormatError, classify, occupancy, quantize_scalar)
+
+__version__ = "0.1.0"

@@ -1,0 +1,697 @@
+// TF classification kernels: the fused brick-summary pass, packed bit volumes, dilation,
+// cell votes and the Morton bitmap of non-empty bricks.
+//
+// Reference semantics (paths relative to /root/reference/pkg/src/voxelskip/):
+//   quantize_scalar  volume.py:159-162   floor(v*255+0.5) clipped, float64
+//   classify         volume.py:307-319   visible <=> lut[bin, 3] > 0
+//   _dilate26        volume.py:289-304   3x3x3 box OR, clipped at the borders
+//   occupancy        volume.py:322-324   count_nonzero / size (undilated at the call sites)
+//   flag_bricks      lbvh.py:83-102      padded reshape-any per brick, C scan order
+//   _macro_from_bits svt.py:161-167      same vote with cell edge cs
+//
+// The hot kernel is k_brick_summary: one coalesced 16-byte-per-lane pass over the u8 volume
+// (HBM-bound; the only compulsory traffic of a TF-change LBVH rebuild).  Visibility is
+// evaluated four bytes at a time with SWAR compares when the visible set is one or two bin
+// intervals (ramp / band TFs), else by a 256-byte shared-memory table.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cstdarg>
+
+#include "common.cuh"
+
+namespace vs {
+
+static __thread char g_err[512];
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+// ---------------------------------------------------------------------------------------
+// Visibility of four packed u8 bins -> 0x80 in every visible byte.
+// ---------------------------------------------------------------------------------------
+struct VisEval {
+  int mode;
+  uint32_t flip;        // 0x80808080 if bin 0 is visible
+  uint32_t c_lo[2];     // (c & 0x7f) replicated
+  uint32_t c_hi[2];     // all-ones if c >= 128 (then x >= c needs the high bit)
+  const uint8_t* tab;   // mode 0: shared table, 0x80 / 0 per bin
+
+  __device__ __forceinline__ static uint32_t ge(uint32_t x, uint32_t clo, uint32_t chi) {
+    // per byte x >= c, with c in [1,255]: (x|0x80) - (c&0x7f) never borrows across bytes;
+    // its high bit is (x&0x7f) >= (c&0x7f).
+    const uint32_t H = 0x80808080u;
+    uint32_t r = (x | H) - clo;
+    return ((x & r) | ((x | r) & ~chi)) & H;
+  }
+  template <int MODE>
+  __device__ __forceinline__ uint32_t eval(uint32_t x) const {
+    if (MODE == 1) return ge(x, c_lo[0], c_hi[0]) ^ flip;
+    if (MODE == 2) return ge(x, c_lo[0], c_hi[0]) ^ ge(x, c_lo[1], c_hi[1]) ^ flip;
+    if (MODE == 3) return flip;
+    return (uint32_t)tab[x & 0xff] | ((uint32_t)tab[(x >> 8) & 0xff] << 8) |
+           ((uint32_t)tab[(x >> 16) & 0xff] << 16) | ((uint32_t)tab[x >> 24] << 24);
+  }
+};
+
+__device__ __forceinline__ void load_vis(VisEval& ve, const vs_tf_params* tf, uint8_t* tab) {
+  ve.mode = tf->mode;
+  ve.flip = tf->start ? 0x80808080u : 0u;
+  for (int k = 0; k < 2; ++k) {
+    uint32_t c = (uint32_t)tf->bound[k] & 0xffu;
+    ve.c_lo[k] = (c & 0x7fu) * 0x01010101u;
+    ve.c_hi[k] = (c & 0x80u) ? 0xffffffffu : 0u;
+  }
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    tab[b] = ((tf->vis[b >> 5] >> (b & 31)) & 1u) ? 0x80 : 0;
+  ve.tab = tab;
+}
+
+// 4 visible-flag bytes (0x80 each) -> 4 contiguous bits.
+__device__ __forceinline__ uint32_t compress4(uint32_t g) {
+  return (((g >> 7) * 0x00204081u) >> 21) & 0xFu;
+}
+
+// ---------------------------------------------------------------------------------------
+// k_brick_summary: warp task = (brick bx, brick by, 512-voxel z chunk); lane = 2 bricks in
+// z (16 bytes of each z-row).  The 8x8 rows of the brick pair stream through registers; the
+// 27 halo-region "any" bits are folded per row (y categories), per x slab (x categories),
+// and per 4-byte word (z categories: byte 0 of the first word is z-local 0, byte 3 of the
+// second word is z-local 7).
+// ---------------------------------------------------------------------------------------
+constexpr int SUMMARY_WARPS = 8;
+
+template <int MODE, bool WRITE_BITS, bool COUNT>
+__device__ __forceinline__ void summary_body(const VisEval& ve, uint32_t* red,
+                                             const uint8_t* __restrict__ vol, int nx, int ny,
+                                             int nz, uint32_t* __restrict__ summary,
+                                             uint32_t* __restrict__ bits,
+                                             unsigned long long* __restrict__ count, int nbx,
+                                             int nby, int nbz, int nzc, int64_t ntasks) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t task = (int64_t)blockIdx.x * SUMMARY_WARPS + warp;
+  uint32_t cnt = 0;
+  if (task < ntasks) {
+    const int zc = (int)(task % nzc);
+    const int64_t r = task / nzc;
+    const int by = (int)(r % nby);
+    const int bx = (int)(r / nby);
+    const int z0 = zc * 512 + lane * 16;
+    const bool active = z0 < nz;
+    const int x0 = bx * 8, y0 = by * 8;
+    const int nzw = (int)nzw_of(nz);
+    // nz % 16 == 0, so the active lanes are a prefix of the warp (and uniform per task).
+    const unsigned amask = __ballot_sync(0xffffffffu, active);
+
+    // X-category accumulators of 9-bit (y,z) masks, per brick (A = z0..7, B = z8..15).
+    uint32_t xa_any = 0, xa_first = 0, xa_last = 0;
+    uint32_t xb_any = 0, xb_first = 0, xb_last = 0;
+    if (active) {
+#pragma unroll 1
+      for (int lx = 0; lx < 8; ++lx) {
+        const int x = x0 + lx;
+        if (x >= nx) break;
+        // y-category accumulators (word pairs) for brick A and B
+        uint32_t ya0 = 0, ya1 = 0, yfa0 = 0, yfa1 = 0, yla0 = 0, yla1 = 0;
+        uint32_t yb0 = 0, yb1 = 0, yfb0 = 0, yfb1 = 0, ylb0 = 0, ylb1 = 0;
+        const uint8_t* row = vol + ((int64_t)x * ny + y0) * nz + z0;
+        uint4 v[8];
+#pragma unroll
+        for (int ly = 0; ly < 8; ++ly) {
+          if (y0 + ly < ny)
+            v[ly] = __ldcs(reinterpret_cast<const uint4*>(row + (int64_t)ly * nz));
+          else
+            v[ly] = make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int ly = 0; ly < 8; ++ly) {
+          uint32_t g0, g1, g2, g3;
+          if (y0 + ly < ny) {
+            g0 = ve.eval<MODE>(v[ly].x);
+            g1 = ve.eval<MODE>(v[ly].y);
+            g2 = ve.eval<MODE>(v[ly].z);
+            g3 = ve.eval<MODE>(v[ly].w);
+          } else {
+            g0 = g1 = g2 = g3 = 0;
+          }
+          if (COUNT) cnt += __popc(g0) + __popc(g1) + __popc(g2) + __popc(g3);
+          if (WRITE_BITS) {
+            uint32_t m = compress4(g0) | (compress4(g1) << 4) | (compress4(g2) << 8) |
+                         (compress4(g3) << 12);
+            uint32_t other = __shfl_down_sync(amask, m, 1);
+            if (y0 + ly < ny) {
+              const int64_t wbase = ((int64_t)x * ny + (y0 + ly)) * nzw;
+              if ((lane & 1) == 0) {
+                uint32_t word = m | ((z0 + 16 < nz) ? (other << 16) : 0u);
+                bits[wbase + (z0 >> 5)] = word;
+              }
+            }
+          }
+          ya0 |= g0; ya1 |= g1; yb0 |= g2; yb1 |= g3;
+          if (ly == 0) { yfa0 = g0; yfa1 = g1; yfb0 = g2; yfb1 = g3; }
+          if (ly == 7) { yla0 = g0; yla1 = g1; ylb0 = g2; ylb1 = g3; }
+        }
+        // z categories of a word pair -> 3 bits: bit0 last slab (z7), bit1 any, bit2 first (z0)
+        auto zc3 = [](uint32_t w0, uint32_t w1) -> uint32_t {
+          return (w1 >> 31) | (((w0 | w1) != 0u) << 1) | (((w0 >> 7) & 1u) << 2);
+        };
+        const uint32_t pa = zc3(yla0, yla1) | (zc3(ya0, ya1) << 3) | (zc3(yfa0, yfa1) << 6);
+        const uint32_t pb = zc3(ylb0, ylb1) | (zc3(yb0, yb1) << 3) | (zc3(yfb0, yfb1) << 6);
+        xa_any |= pa; xb_any |= pb;
+        if (lx == 0) { xa_first = pa; xb_first = pb; }
+        if (lx == 7) { xa_last = pa; xb_last = pb; }
+      }
+      const int bz = z0 >> 3;
+      const int64_t sbase = ((int64_t)bx * nby + by) * nbz;
+      summary[sbase + bz] = xa_last | (xa_any << 9) | (xa_first << 18);
+      if (bz + 1 < nbz) summary[sbase + bz + 1] = xb_last | (xb_any << 9) | (xb_first << 18);
+    }
+  }
+  if (COUNT) {
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) red[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      for (int w = 0; w < SUMMARY_WARPS; ++w) s += red[w];
+      if (s) atomicAdd(count, s);
+    }
+  }
+}
+
+template <bool WRITE_BITS, bool COUNT>
+__global__ void __launch_bounds__(SUMMARY_WARPS * 32)
+    k_brick_summary(const uint8_t* __restrict__ vol, int nx, int ny, int nz,
+                    const vs_tf_params* __restrict__ tf, uint32_t* __restrict__ summary,
+                    uint32_t* __restrict__ bits, unsigned long long* __restrict__ count,
+                    int nbx, int nby, int nbz, int nzc, int64_t ntasks) {
+  __shared__ uint8_t tab[256];
+  __shared__ uint32_t red[SUMMARY_WARPS];
+  VisEval ve;
+  load_vis(ve, tf, tab);
+  __syncthreads();
+  switch (ve.mode) {  // uniform: one TF per launch
+    case 1:
+      summary_body<1, WRITE_BITS, COUNT>(ve, red, vol, nx, ny, nz, summary, bits, count, nbx,
+                                         nby, nbz, nzc, ntasks);
+      break;
+    case 2:
+      summary_body<2, WRITE_BITS, COUNT>(ve, red, vol, nx, ny, nz, summary, bits, count, nbx,
+                                         nby, nbz, nzc, ntasks);
+      break;
+    case 3:
+      summary_body<3, WRITE_BITS, COUNT>(ve, red, vol, nx, ny, nz, summary, bits, count, nbx,
+                                         nby, nbz, nzc, ntasks);
+      break;
+    default:
+      summary_body<0, WRITE_BITS, COUNT>(ve, red, vol, nx, ny, nz, summary, bits, count, nbx,
+                                         nby, nbz, nzc, ntasks);
+      break;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Generic classification to packed bits: thread per 32-voxel word.
+// ---------------------------------------------------------------------------------------
+__global__ void k_classify_bits(const uint8_t* __restrict__ vol, int nx, int ny, int nz,
+                                const vs_tf_params* __restrict__ tf, uint32_t* __restrict__ bits,
+                                unsigned long long* __restrict__ count) {
+  __shared__ uint8_t tab[256];
+  __shared__ uint32_t red[32];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    tab[b] = (tf->vis[b >> 5] >> (b & 31)) & 1u;
+  __syncthreads();
+  const int64_t nzw = nzw_of(nz);
+  const int64_t nwords = (int64_t)nx * ny * nzw;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t c = 0;
+  if (i < nwords) {
+    const int64_t rowi = i / nzw;
+    const int w = (int)(i % nzw);
+    const uint8_t* row = vol + rowi * nz;
+    uint32_t word = 0;
+    const int zend = min(32, nz - w * 32);
+    for (int k = 0; k < zend; ++k) word |= (uint32_t)tab[row[w * 32 + k]] << k;
+    bits[i] = word;
+    c = __popc(word);
+  }
+  if (count) {
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+      if (s) atomicAdd(count, s);
+    }
+  }
+}
+
+__global__ void k_quantize(const float* __restrict__ f, int64_t n, uint8_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // volume.py:159-162 in float64, no FMA: floor(v*255 + 0.5), clip [0, 255]; NaN -> 0 like
+  // numpy's int64 cast of NaN (INT64_MIN) clipped to 0.
+  double d = floor(__dadd_rn(__dmul_rn((double)f[i], 255.0), 0.5));
+  int q = (d != d) ? 0 : (d < 0.0 ? 0 : (d > 255.0 ? 255 : (int)d));
+  out[i] = (uint8_t)q;
+}
+
+// Row-dilated word: z dilation within a packed row, border-clipped.
+__device__ __forceinline__ uint32_t zdil(const uint32_t* __restrict__ row, int w, int nzw,
+                                         uint32_t lastmask) {
+  uint32_t v = __ldg(row + w);
+  uint32_t r = v | (v << 1) | (v >> 1);
+  if (w > 0) r |= __ldg(row + w - 1) >> 31;
+  if (w + 1 < nzw) r |= __ldg(row + w + 1) << 31;
+  if (w + 1 == nzw) r &= lastmask;
+  return r;
+}
+
+// _dilate26 on packed bits: thread = (word w, row y, x chunk); slides along x keeping the
+// y/z-dilated rows x-1, x, x+1 in registers.
+constexpr int DIL_XCHUNK = 16;
+__global__ void k_dilate(const uint32_t* __restrict__ in, int nx, int ny, int nz,
+                         uint32_t* __restrict__ out) {
+  const int nzw = (int)nzw_of(nz);
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const int x0 = blockIdx.z * DIL_XCHUNK;
+  if (w >= nzw) return;
+  const uint32_t lastmask = (nz & 31) ? ((1u << (nz & 31)) - 1u) : 0xffffffffu;
+  auto yz = [&](int x) -> uint32_t {
+    if (x < 0 || x >= nx) return 0u;
+    uint32_t r = 0;
+    for (int dy = -1; dy <= 1; ++dy) {
+      int yy = y + dy;
+      if (yy < 0 || yy >= ny) continue;
+      r |= zdil(in + ((int64_t)x * ny + yy) * nzw, w, nzw, lastmask);
+    }
+    return r;
+  };
+  uint32_t prev = yz(x0 - 1), cur = yz(x0);
+  const int xe = min(nx, x0 + DIL_XCHUNK);
+  for (int x = x0; x < xe; ++x) {
+    uint32_t nxt = yz(x + 1);
+    out[((int64_t)x * ny + y) * nzw + w] = prev | cur | nxt;
+    prev = cur;
+    cur = nxt;
+  }
+}
+
+__global__ void k_pack(const uint8_t* __restrict__ b, int64_t nrows, int nz,
+                       uint32_t* __restrict__ bits) {
+  const int64_t nzw = nzw_of(nz);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows * nzw) return;
+  const int64_t r = i / nzw;
+  const int w = (int)(i % nzw);
+  const uint8_t* row = b + r * nz + w * 32;
+  const int zend = min(32, nz - w * 32);
+  uint32_t word = 0;
+  for (int k = 0; k < zend; ++k) word |= (row[k] ? 1u : 0u) << k;
+  bits[i] = word;
+}
+
+__global__ void k_unpack(const uint32_t* __restrict__ bits, int64_t nrows, int nz,
+                         uint8_t* __restrict__ b) {
+  const int64_t n = nrows * nz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = i / nz;
+  const int z = (int)(i % nz);
+  b[i] = (bits[r * nzw_of(nz) + (z >> 5)] >> (z & 31)) & 1u;
+}
+
+__global__ void k_count_bits(const uint32_t* __restrict__ bits, int64_t nwords,
+                             unsigned long long* __restrict__ count) {
+  __shared__ uint32_t red[32];
+  uint32_t c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += __popc(bits[i]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+    if (s) atomicAdd(count, s);
+  }
+}
+
+// Per-cell vote, thread per cell (C-order), early exit on the first set word.
+__global__ void k_vote_cells(const uint32_t* __restrict__ bits, int nx, int ny, int nz, int cs,
+                             int ncx, int ncy, int ncz, uint8_t* __restrict__ flags) {
+  const int64_t ncell = (int64_t)ncx * ncy * ncz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncell) return;
+  const int cz = (int)(i % ncz);
+  const int cy = (int)((i / ncz) % ncy);
+  const int cx = (int)(i / ((int64_t)ncz * ncy));
+  const int nzw = (int)nzw_of(nz);
+  const int xa = cx * cs, xb = min(nx, xa + cs);
+  const int ya = cy * cs, yb = min(ny, ya + cs);
+  const int za = cz * cs, zb = min(nz, za + cs);
+  const int wa = za >> 5, wb = (zb - 1) >> 5;
+  uint8_t f = 0;
+  for (int x = xa; x < xb && !f; ++x)
+    for (int y = ya; y < yb && !f; ++y) {
+      const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
+      for (int w = wa; w <= wb; ++w) {
+        uint32_t m = 0xffffffffu;
+        if (w == wa) m &= 0xffffffffu << (za & 31);
+        if (w == wb && ((zb & 31) != 0)) m &= (1u << (zb & 31)) - 1u;
+        if (__ldg(row + w) & m) { f = 1; break; }
+      }
+    }
+  flags[i] = f;
+}
+
+// ---------------------------------------------------------------------------------------
+// Summary -> Morton bitmap (+ tile counts, + 16^3 cells).  CTA = one 8^3 tile of bricks =
+// one aligned 512-code Morton range; the 10^3 summary halo is staged in shared memory.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int sbit(int ex, int ey, int ez) {
+  return (ex + 1) * 9 + (ey + 1) * 3 + (ez + 1);
+}
+
+__global__ void __launch_bounds__(512)
+    k_summary_to_bitmap(const uint32_t* __restrict__ summary, int nbx, int nby, int nbz,
+                        int dilate, uint32_t* __restrict__ bitmap,
+                        uint32_t* __restrict__ tile_counts, uint8_t* __restrict__ cell16,
+                        int ncx, int ncy, int ncz) {
+  __shared__ uint32_t s[10][10][10];
+  __shared__ uint32_t wc[16];
+  const uint32_t tile = blockIdx.x;
+  const int tx = (int)compact10(tile) * 8, ty = (int)compact10(tile >> 1) * 8,
+            tz = (int)compact10(tile >> 2) * 8;
+  const int t = threadIdx.x;
+  if (tx >= nbx || ty >= nby || tz >= nbz) {  // tile outside the brick grid
+    if (t < 16) bitmap[(size_t)tile * 16 + t] = 0;
+    if (t == 0) tile_counts[tile] = 0;
+    return;
+  }
+  for (int k = t; k < 1000; k += 512) {
+    const int hx = k / 100, hy = (k / 10) % 10, hz = k % 10;
+    const int gx = tx + hx - 1, gy = ty + hy - 1, gz = tz + hz - 1;
+    uint32_t v = 0;
+    if (gx >= 0 && gx < nbx && gy >= 0 && gy < nby && gz >= 0 && gz < nbz)
+      v = summary[((int64_t)gx * nby + gy) * nbz + gz];
+    s[hx][hy][hz] = v;
+  }
+  __syncthreads();
+  const int lx = (int)compact10((uint32_t)t), ly = (int)compact10((uint32_t)t >> 1),
+            lz = (int)compact10((uint32_t)t >> 2);
+  const int bx = tx + lx, by = ty + ly, bz = tz + lz;
+  uint32_t f = 0;
+  if (bx < nbx && by < nby && bz < nbz) {
+    if (dilate) {
+#pragma unroll
+      for (int ex = -1; ex <= 1; ++ex)
+#pragma unroll
+        for (int ey = -1; ey <= 1; ++ey)
+#pragma unroll
+          for (int ez = -1; ez <= 1; ++ez)
+            f |= s[lx + 1 + ex][ly + 1 + ey][lz + 1 + ez] >> sbit(ex, ey, ez);
+      f &= 1u;
+    } else {
+      f = (s[lx + 1][ly + 1][lz + 1] >> sbit(0, 0, 0)) & 1u;
+    }
+  }
+  const uint32_t ball = __ballot_sync(0xffffffffu, f != 0);
+  const int lane = t & 31, warp = t >> 5;
+  if (lane == 0) {
+    bitmap[(size_t)tile * 16 + warp] = ball;
+    wc[warp] = __popc(ball);
+  }
+  if (cell16 && (lane & 7) == 0) {
+    const int cx = bx >> 1, cy = by >> 1, cz = bz >> 1;
+    if (cx < ncx && cy < ncy && cz < ncz)
+      cell16[((int64_t)cx * ncy + cy) * ncz + cz] = ((ball >> lane) & 0xffu) ? 1 : 0;
+  }
+  __syncthreads();
+  if (t == 0) {
+    uint32_t c = 0;
+    for (int k = 0; k < 16; ++k) c += wc[k];
+    tile_counts[tile] = c;
+  }
+}
+
+__global__ void k_flags_scatter(const uint8_t* __restrict__ flags, int nbx, int nby, int nbz,
+                                uint32_t* __restrict__ bitmap) {
+  const int64_t n = (int64_t)nbx * nby * nbz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !flags[i]) return;
+  const uint32_t bz = (uint32_t)(i % nbz), by = (uint32_t)((i / nbz) % nby),
+                 bx = (uint32_t)(i / ((int64_t)nbz * nby));
+  const uint32_t code = morton3(bx, by, bz);
+  atomicOr(bitmap + (code >> 5), 1u << (code & 31));
+}
+
+__global__ void k_tile_counts(const uint32_t* __restrict__ bitmap, int64_t ntiles,
+                              uint32_t* __restrict__ tile_counts) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  uint32_t c = 0;
+  const uint4* p = reinterpret_cast<const uint4*>(bitmap + t * 16);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint4 v = p[k];
+    c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  }
+  tile_counts[t] = c;
+}
+
+__global__ void k_bitmap_to_scan_flags(const uint32_t* __restrict__ bitmap, int nbx, int nby,
+                                       int nbz, uint8_t* __restrict__ flags) {
+  const int64_t n = (int64_t)nbx * nby * nbz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t bz = (uint32_t)(i % nbz), by = (uint32_t)((i / nbz) % nby),
+                 bx = (uint32_t)(i / ((int64_t)nbz * nby));
+  const uint32_t code = morton3(bx, by, bz);
+  flags[i] = (bitmap[code >> 5] >> (code & 31)) & 1u;
+}
+
+__global__ void k_decode_scan(const int64_t* __restrict__ idx, const int* __restrict__ n_dev,
+                              int nby, int nbz, int32_t* __restrict__ coords,
+                              uint32_t* __restrict__ codes, int64_t cap) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cap || k >= *n_dev) return;
+  const int64_t i = idx[k];
+  const int bz = (int)(i % nbz), by = (int)((i / nbz) % nby), bx = (int)(i / ((int64_t)nbz * nby));
+  coords[3 * k] = bx;
+  coords[3 * k + 1] = by;
+  coords[3 * k + 2] = bz;
+  codes[k] = morton3(bx, by, bz);
+}
+
+}  // namespace vs
+
+using namespace vs;
+
+// =======================================================================================
+// C ABI
+// =======================================================================================
+extern "C" {
+
+const char* vs_version(void) { return "vsb200 0.1 sm_100a"; }
+
+int vs_last_error(char* buf, size_t size) {
+  if (buf && size) {
+    strncpy(buf, g_err, size - 1);
+    buf[size - 1] = 0;
+  }
+  return (int)strlen(g_err);
+}
+
+int vs_tf_params_from_alpha(const float* alpha, vs_tf_params* out) {
+  if (!alpha || !out) return fail_arg("null pointer");
+  memset(out, 0, sizeof *out);
+  int prev = alpha[0] > 0.0f;
+  int nflip = 0;
+  out->start = prev;
+  for (int b = 0; b < 256; ++b) {
+    int v = alpha[b] > 0.0f;
+    if (v) {
+      out->vis[b >> 5] |= 1u << (b & 31);
+      out->nvisible++;
+    }
+    if (b > 0 && v != prev) {
+      if (nflip < 2) out->bound[nflip] = b;
+      nflip++;
+    }
+    prev = v;
+  }
+  out->mode = nflip == 0 ? 3 : (nflip <= 2 ? nflip : 0);
+  return 0;
+}
+
+int vs_quantize_f32(const float* field, int64_t n, uint8_t* bins, vs_stream_t st) {
+  if (n < 0 || (n && (!field || !bins))) return fail_arg("vs_quantize_f32");
+  if (n == 0) return 0;
+  k_quantize<<<(unsigned)cdiv(n, 256), 256, 0, S(st)>>>(field, n, bins);
+  return check_launch("k_quantize");
+}
+
+int vs_classify_summary(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
+                        uint32_t* summary, uint32_t* bits, unsigned long long* count,
+                        vs_stream_t st) {
+  if (!bins || !tf || !summary || nx < 1 || ny < 1 || nz < 1)
+    return fail_arg("vs_classify_summary");
+  if (nz % 16 != 0) return fail_arg("vs_classify_summary needs nz % 16 == 0");
+  const int nbx = (int)cdiv(nx, 8), nby = (int)cdiv(ny, 8), nbz = (int)cdiv(nz, 8);
+  const int nzc = (int)cdiv(nz, 512);
+  const int64_t ntasks = (int64_t)nbx * nby * nzc;
+  const unsigned grid = (unsigned)cdiv(ntasks, SUMMARY_WARPS);
+  if (bits && count)
+    k_brick_summary<true, true><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
+        bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
+  else if (bits)
+    k_brick_summary<true, false><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
+        bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
+  else if (count)
+    k_brick_summary<false, true><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
+        bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
+  else
+    k_brick_summary<false, false><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
+        bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
+  return check_launch("k_brick_summary");
+}
+
+int vs_classify_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
+                     uint32_t* bits, unsigned long long* count, vs_stream_t st) {
+  if (!bins || !tf || !bits || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_classify_bits");
+  const int64_t nwords = (int64_t)nx * ny * nzw_of(nz);
+  k_classify_bits<<<(unsigned)cdiv(nwords, 256), 256, 0, S(st)>>>(bins, nx, ny, nz, tf, bits,
+                                                                    count);
+  return check_launch("k_classify_bits");
+}
+
+int vs_dilate_bits(const uint32_t* in, int nx, int ny, int nz, uint32_t* out, vs_stream_t st) {
+  if (!in || !out || in == out || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_dilate_bits");
+  if (ny > 65535) return fail_arg("vs_dilate_bits: ny > 65535");
+  const int nzw = (int)nzw_of(nz);
+  const int bx = nzw >= 128 ? 128 : 32;
+  dim3 grid((unsigned)cdiv(nzw, bx), (unsigned)ny, (unsigned)cdiv(nx, DIL_XCHUNK));
+  k_dilate<<<grid, bx, 0, S(st)>>>(in, nx, ny, nz, out);
+  return check_launch("k_dilate");
+}
+
+int vs_pack_bits(const uint8_t* bools, int nx, int ny, int nz, uint32_t* bits, vs_stream_t st) {
+  if (!bools || !bits || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_pack_bits");
+  const int64_t nrows = (int64_t)nx * ny;
+  k_pack<<<(unsigned)cdiv(nrows * nzw_of(nz), 256), 256, 0, S(st)>>>(bools, nrows, nz, bits);
+  return check_launch("k_pack");
+}
+
+int vs_unpack_bits(const uint32_t* bits, int nx, int ny, int nz, uint8_t* bools,
+                   vs_stream_t st) {
+  if (!bools || !bits || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_unpack_bits");
+  const int64_t nrows = (int64_t)nx * ny;
+  k_unpack<<<(unsigned)cdiv(nrows * nz, 256), 256, 0, S(st)>>>(bits, nrows, nz, bools);
+  return check_launch("k_unpack");
+}
+
+int vs_count_bits(const uint32_t* bits, int nx, int ny, int nz, unsigned long long* count,
+                  vs_stream_t st) {
+  if (!bits || !count || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_count_bits");
+  const int64_t nwords = (int64_t)nx * ny * nzw_of(nz);
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(nwords, 256), 148 * 16);
+  k_count_bits<<<grid, 256, 0, S(st)>>>(bits, nwords, count);
+  return check_launch("k_count_bits");
+}
+
+int vs_vote_cells(const uint32_t* bits, int nx, int ny, int nz, int cs, uint8_t* flags,
+                  vs_stream_t st) {
+  if (!bits || !flags || nx < 1 || ny < 1 || nz < 1 || cs < 1) return fail_arg("vs_vote_cells");
+  const int ncx = (int)cdiv(nx, cs), ncy = (int)cdiv(ny, cs), ncz = (int)cdiv(nz, cs);
+  const int64_t n = (int64_t)ncx * ncy * ncz;
+  k_vote_cells<<<(unsigned)cdiv(n, 128), 128, 0, S(st)>>>(bits, nx, ny, nz, cs, ncx, ncy, ncz,
+                                                          flags);
+  return check_launch("k_vote_cells");
+}
+
+int vs_morton_side(int nbx, int nby, int nbz) {
+  int m = std::max(nbx, std::max(nby, nbz));
+  if (m > 1024 || m < 1) return VS_ERANGE;
+  int p = 8;
+  while (p < m) p <<= 1;
+  return p;
+}
+
+int vs_summary_to_bitmap(const uint32_t* summary, int nx, int ny, int nz, int dilate, int P,
+                         uint32_t* bitmap, uint32_t* tile_counts, uint8_t* cell16,
+                         vs_stream_t st) {
+  if (!summary || !bitmap || !tile_counts || nx < 1 || ny < 1 || nz < 1)
+    return fail_arg("vs_summary_to_bitmap");
+  const int nbx = (int)cdiv(nx, 8), nby = (int)cdiv(ny, 8), nbz = (int)cdiv(nz, 8);
+  if (P != vs_morton_side(nbx, nby, nbz)) return fail_arg("vs_summary_to_bitmap: P");
+  const int64_t ntiles = (int64_t)P * P * P / 512;
+  const int ncx = (int)cdiv(nx, 16), ncy = (int)cdiv(ny, 16), ncz = (int)cdiv(nz, 16);
+  k_summary_to_bitmap<<<(unsigned)ntiles, 512, 0, S(st)>>>(summary, nbx, nby, nbz, dilate,
+                                                           bitmap, tile_counts, cell16, ncx,
+                                                           ncy, ncz);
+  return check_launch("k_summary_to_bitmap");
+}
+
+int vs_flags_to_bitmap(const uint8_t* flags, int nbx, int nby, int nbz, int P, uint32_t* bitmap,
+                       uint32_t* tile_counts, vs_stream_t st) {
+  if (!flags || !bitmap || !tile_counts || nbx < 1 || nby < 1 || nbz < 1)
+    return fail_arg("vs_flags_to_bitmap");
+  if (P != vs_morton_side(nbx, nby, nbz)) return fail_arg("vs_flags_to_bitmap: P");
+  const int64_t nwords = (int64_t)P * P * P / 32;
+  const int64_t ntiles = nwords / 16;
+  VS_CUDA(cudaMemsetAsync(bitmap, 0, nwords * 4, S(st)), "memset bitmap");
+  const int64_t n = (int64_t)nbx * nby * nbz;
+  k_flags_scatter<<<(unsigned)cdiv(n, 256), 256, 0, S(st)>>>(flags, nbx, nby, nbz, bitmap);
+  VS_TRY(check_launch("k_flags_scatter"));
+  k_tile_counts<<<(unsigned)cdiv(ntiles, 256), 256, 0, S(st)>>>(bitmap, ntiles, tile_counts);
+  return check_launch("k_tile_counts");
+}
+
+size_t vs_bricks_workspace(int nbx, int nby, int nbz) {
+  const int64_t n = (int64_t)nbx * nby * nbz;
+  size_t cub_bytes = 0;
+  cub::DeviceSelect::Flagged(nullptr, cub_bytes, thrust::counting_iterator<int64_t>(0),
+                             (const uint8_t*)nullptr, (int64_t*)nullptr, (int*)nullptr, (int)n);
+  Bump b(nullptr);
+  b.take<uint8_t>(n);
+  b.take<int64_t>(n);
+  b.take<char>(cub_bytes);
+  return b.off + 256;
+}
+
+int vs_bricks_from_bitmap(const uint32_t* bitmap, int nbx, int nby, int nbz, int P,
+                          int32_t* coords, uint32_t* codes, int* n_out, void* ws,
+                          size_t ws_bytes, vs_stream_t st) {
+  if (!bitmap || !coords || !codes || !n_out || nbx < 1 || nby < 1 || nbz < 1)
+    return fail_arg("vs_bricks_from_bitmap");
+  if (ws_bytes < vs_bricks_workspace(nbx, nby, nbz)) return VS_EWORKSPACE;
+  const int64_t n = (int64_t)nbx * nby * nbz;
+  size_t cub_bytes = 0;
+  cub::DeviceSelect::Flagged(nullptr, cub_bytes, thrust::counting_iterator<int64_t>(0),
+                             (const uint8_t*)nullptr, (int64_t*)nullptr, (int*)nullptr, (int)n);
+  Bump b(ws);
+  uint8_t* flags = b.take<uint8_t>(n);
+  int64_t* idx = b.take<int64_t>(n);
+  void* tmp = b.take<char>(cub_bytes);
+  k_bitmap_to_scan_flags<<<(unsigned)cdiv(n, 256), 256, 0, S(st)>>>(bitmap, nbx, nby, nbz,
+                                                                    flags);
+  VS_TRY(check_launch("k_bitmap_to_scan_flags"));
+  VS_CUDA(cub::DeviceSelect::Flagged(tmp, cub_bytes, thrust::counting_iterator<int64_t>(0),
+                                     flags, idx, n_out, (int)n, S(st)),
+          "DeviceSelect::Flagged");
+  k_decode_scan<<<(unsigned)cdiv(n, 256), 256, 0, S(st)>>>(idx, n_out, nby, nbz, coords, codes,
+                                                           n);
+  return check_launch("k_decode_scan");
+}
+
+}  // extern "C"

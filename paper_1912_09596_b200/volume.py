@@ -1,0 +1,318 @@
+"""Scalar volumes, transfer functions and binary classification on the B200.
+
+Drop-in for voxelskip.volume (/root/reference/pkg/src/voxelskip/volume.py): same class and
+function names, argument meanings and exceptions.  The data live on the GPU:
+
+* ``Volume`` holds the LUT bins as uint8 (quantize_scalar, volume.py:159-162, is applied once
+  at upload; it is the identity on 8-bit data) and, only when the float field is not exactly
+  ``f32(bin/255)``, the float32 field the renderer interpolates.  ``.data`` is a lazy host view.
+* ``BinaryVolume`` is either materialised (packed bits, 1 bit/voxel, z-packed words) or a lazy
+  classification ``(volume, tf, dilate)``.  A lazy one feeds flag_bricks / derive_macro_grid
+  through the fused one-pass brick-summary kernel, so a TF-change LBVH rebuild reads the
+  volume exactly once and never writes the N^3 bit volume.  ``.bits`` materialises on demand.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream
+
+LUT_SIZE = 256
+
+
+class VolumeFormatError(ValueError):
+    """Raw file does not match its metadata (size or layout)."""
+
+
+class UnsupportedFormatError(ValueError):
+    """Voxel precision outside the supported 8/16-bit range."""
+
+
+@dataclass(frozen=True)
+class Aabb:
+    """Half-open integer voxel box [lo, hi) (volume.py:28-61)."""
+
+    lo: tuple[int, int, int]
+    hi: tuple[int, int, int]
+
+    def __post_init__(self):
+        object.__setattr__(self, "lo", tuple(int(v) for v in self.lo))
+        object.__setattr__(self, "hi", tuple(int(v) for v in self.hi))
+        if any(l > h for l, h in zip(self.lo, self.hi)):
+            raise ValueError(f"inverted bounds {self.lo}..{self.hi}")
+
+    def volume(self) -> int:
+        e = self.extent()
+        return e[0] * e[1] * e[2]
+
+    def extent(self) -> tuple[int, int, int]:
+        return tuple(h - l for l, h in zip(self.lo, self.hi))
+
+    def contains(self, p) -> bool:
+        return all(l <= c < h for l, c, h in zip(self.lo, p, self.hi))
+
+    def union(self, other: "Aabb") -> "Aabb":
+        return Aabb(tuple(map(min, self.lo, other.lo)), tuple(map(max, self.hi, other.hi)))
+
+    def intersect(self, other: "Aabb") -> "Aabb | None":
+        lo = tuple(map(max, self.lo, other.lo))
+        hi = tuple(map(min, self.hi, other.hi))
+        if any(l >= h for l, h in zip(lo, hi)):
+            return None
+        return Aabb(lo, hi)
+
+
+# f32(u/255) for every u8 (load_raw normalises in float64 then narrows, volume.py:193-194)
+U8_FIELD = (np.arange(256, dtype=np.float64) / 255.0).astype(np.float32)
+
+
+class Volume:
+    """Dense scalar field normalised to [0, 1], shape (nx, ny, nz), C-order (volume.py:64-81).
+
+    ``data`` may be a float array (quantised on the device) or uint8 bins (taken as the field
+    ``f32(u/255)``, exactly what load_raw returns for 8-bit files).  numpy or torch input."""
+
+    def __init__(self, data, name: str = "volume"):
+        self.name = name
+        dev = _lib.device()
+        t = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.asarray(data))
+        if t.dim() != 3 or min(t.shape) < 1:
+            raise ValueError("volume data must be a non-empty 3-d array")
+        self._dims = tuple(int(d) for d in t.shape)
+        if t.dtype == torch.uint8:
+            self.bins = t.to(dev).contiguous()
+            self.field = None
+        else:
+            f = t.to(device=dev, dtype=torch.float32).contiguous()
+            bins = torch.empty(self._dims, dtype=torch.uint8, device=dev)
+            call("vs_quantize_f32", ptr(f), f.numel(), ptr(bins), stream())
+            self.bins = bins
+            table = torch.from_numpy(U8_FIELD).to(dev)
+            exact = bool(torch.equal(table[bins.long()], f)) if f.numel() <= (1 << 28) else False
+            self.field = None if exact else f
+        self._host = None
+
+    @property
+    def dims(self) -> tuple[int, int, int]:
+        return self._dims
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._host is None:
+            if self.field is not None:
+                self._host = self.field.cpu().numpy()
+            else:
+                self._host = U8_FIELD[self.bins.cpu().numpy()]
+        return self._host
+
+    @property
+    def is_u8(self) -> bool:
+        return self.field is None
+
+    def bounds(self) -> Aabb:
+        return Aabb((0, 0, 0), self.dims)
+
+
+class TransferFunction:
+    """256-entry RGBA lookup table, all channels in [0, 1] (volume.py:84-140)."""
+
+    def __init__(self, lut):
+        lut = np.ascontiguousarray(np.asarray(lut), dtype=np.float32)
+        if lut.shape != (LUT_SIZE, 4):
+            raise ValueError(f"lut must be ({LUT_SIZE}, 4), got {lut.shape}")
+        if lut.min() < 0.0 or lut.max() > 1.0:
+            raise ValueError("lut channels must lie in [0, 1]")
+        self.lut = lut
+        self._dev = {}
+
+    @classmethod
+    def constant(cls, r: float, g: float, b: float, a: float) -> "TransferFunction":
+        return cls(np.tile(np.array([r, g, b, a], dtype=np.float32), (LUT_SIZE, 1)))
+
+    @classmethod
+    def opaque(cls) -> "TransferFunction":
+        """Grey, alpha 1 on every bin but 0 (volume.py:102-111)."""
+        v = np.linspace(0.0, 1.0, LUT_SIZE, dtype=np.float32)
+        a = (np.arange(LUT_SIZE) > 0).astype(np.float32)
+        return cls(np.stack([v, v, v, a], axis=1))
+
+    @classmethod
+    def ramp(cls, threshold: float = 0.3, max_alpha: float = 0.8,
+             color_lo=(0.2, 0.4, 1.0), color_hi=(1.0, 0.6, 0.1)) -> "TransferFunction":
+        """Alpha 0 up to ``threshold``, then linear to ``max_alpha`` (volume.py:113-132); the
+        colour blends color_lo -> color_hi over the same parameter, computed in float64."""
+        v = np.linspace(0.0, 1.0, LUT_SIZE)
+        t = np.clip((v - threshold) / max(1e-9, 1.0 - threshold), 0.0, 1.0)
+        rgb = (1.0 - t)[:, None] * np.asarray(color_lo)[None, :] + \
+            t[:, None] * np.asarray(color_hi)[None, :]
+        a = np.where(v > threshold, t * max_alpha, 0.0)
+        return cls(np.concatenate([rgb, a[:, None]], axis=1).astype(np.float32))
+
+    @classmethod
+    def from_json(cls, path) -> "TransferFunction":
+        return cls(np.asarray(json.loads(Path(path).read_text())["rgba"], dtype=np.float32))
+
+    def to_json(self, path) -> None:
+        Path(path).write_text(json.dumps({"rgba": self.lut.tolist()}))
+
+    # -- device-side caches -----------------------------------------------------------------
+    def params_host(self) -> np.ndarray:
+        """vs_tf_params (64 bytes) for this LUT's alpha column."""
+        if "params_host" not in self._dev:
+            buf = np.zeros(16, dtype=np.int32)
+            alpha = np.ascontiguousarray(self.lut[:, 3])
+            call("vs_tf_params_from_alpha", alpha.ctypes.data, buf.ctypes.data)
+            self._dev["params_host"] = buf
+        return self._dev["params_host"]
+
+    def params(self) -> torch.Tensor:
+        dev = _lib.device()
+        key = ("params", dev.index)
+        if key not in self._dev:
+            stage = _pinned_stage()
+            stage.copy_(torch.from_numpy(self.params_host()))
+            self._dev[key] = stage.to(dev)  # pinned -> device (synchronous, 64 bytes)
+        return self._dev[key]
+
+
+_STAGE = None
+
+
+def _pinned_stage() -> torch.Tensor:
+    global _STAGE
+    if _STAGE is None:
+        _STAGE = torch.empty(16, dtype=torch.int32).pin_memory()
+    return _STAGE
+
+
+def quantize_scalar(values) -> np.ndarray:
+    """Host mirror of volume.py:159-162 (floor(v*255 + 0.5) clamped, float64).  The device
+    path applies the same rounding in k_quantize."""
+    idx = np.floor(np.asarray(values, dtype=np.float64) * 255.0 + 0.5)
+    return np.clip(np.nan_to_num(idx, nan=0.0), 0, LUT_SIZE - 1).astype(np.int64)
+
+
+def _nzw(nz: int) -> int:
+    return (nz + 31) // 32
+
+
+class BinaryVolume:
+    """One visibility flag per voxel (volume.py:143-156), held on the GPU.
+
+    ``BinaryVolume(bits)`` packs a host/device bool array.  classify() returns a lazy one
+    bound to (volume, tf, dilate)."""
+
+    def __init__(self, bits=None, *, _source=None, dims=None):
+        self._packed = None
+        self._source = _source
+        self._summary = None
+        self._count = None
+        self._host = None
+        if bits is not None:
+            t = bits if isinstance(bits, torch.Tensor) else torch.from_numpy(
+                np.ascontiguousarray(np.asarray(bits), dtype=bool))
+            if t.dim() != 3:
+                raise ValueError("bits must be 3-d")
+            self._dims = tuple(int(d) for d in t.shape)
+            dev = _lib.device()
+            b8 = t.to(device=dev, dtype=torch.uint8).contiguous()
+            nx, ny, nz = self._dims
+            self._packed = torch.empty(nx * ny * _nzw(nz), dtype=torch.int32, device=dev)
+            if b8.numel():
+                call("vs_pack_bits", ptr(b8), nx, ny, nz, ptr(self._packed), stream())
+        else:
+            self._dims = tuple(int(d) for d in dims)
+
+    @property
+    def dims(self) -> tuple[int, int, int]:
+        return self._dims
+
+    @property
+    def lazy(self) -> bool:
+        return self._packed is None
+
+    def summary_ok(self) -> bool:
+        """The fused brick-summary kernel applies (8^3 bricks, rows of 16-byte multiples)."""
+        return self._source is not None and self._dims[2] % 16 == 0
+
+    def summary(self) -> torch.Tensor:
+        """27-bit halo summaries per 8^3 brick (vs_classify_summary); computes the undilated
+        visible count in the same pass."""
+        if self._summary is None:
+            v, tf, _ = self._source
+            nx, ny, nz = self._dims
+            dev = _lib.device()
+            nb = [-(-d // 8) for d in self._dims]
+            s = torch.empty(nb[0] * nb[1] * nb[2], dtype=torch.int32, device=dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            call("vs_classify_summary", ptr(v.bins), nx, ny, nz, ptr(tf.params()), ptr(s), None,
+                 ptr(cnt), stream())
+            self._summary = s
+            self._count = cnt
+        return self._summary
+
+    def packed(self) -> torch.Tensor:
+        """Packed bits (int32 words, z-packed rows), materialised on first use."""
+        if self._packed is None:
+            v, tf, dilate = self._source
+            nx, ny, nz = self._dims
+            dev = _lib.device()
+            base = torch.empty(nx * ny * _nzw(nz), dtype=torch.int32, device=dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            call("vs_classify_bits", ptr(v.bins), nx, ny, nz, ptr(tf.params()), ptr(base),
+                 ptr(cnt), stream())
+            if self._count is None:
+                self._count = cnt
+            if dilate:
+                out = torch.empty_like(base)
+                call("vs_dilate_bits", ptr(base), nx, ny, nz, ptr(out), stream())
+                base = out
+            self._packed = base
+        return self._packed
+
+    def base_count(self) -> int:
+        """Visible voxels of the UNDILATED classification behind a lazy volume."""
+        if self._count is None:
+            if self.summary_ok():
+                self.summary()
+            else:
+                self.packed()
+        return int(self._count.item())
+
+    def count_nonzero(self) -> int:
+        if self._source is not None and not self._source[2]:
+            return self.base_count()
+        p = self.packed()
+        nx, ny, nz = self._dims
+        cnt = torch.zeros(1, dtype=torch.int64, device=p.device)
+        call("vs_count_bits", ptr(p), nx, ny, nz, ptr(cnt), stream())
+        return int(cnt.item())
+
+    @property
+    def bits(self) -> np.ndarray:
+        if self._host is None:
+            p = self.packed()
+            nx, ny, nz = self._dims
+            out = torch.empty(self._dims, dtype=torch.uint8, device=p.device)
+            call("vs_unpack_bits", ptr(p), nx, ny, nz, ptr(out), stream())
+            self._host = out.cpu().numpy().view(bool)
+        return self._host
+
+
+def classify(v: Volume, tf: TransferFunction, dilate: bool = False) -> BinaryVolume:
+    """Visible iff lut[bin, 3] > 0; with ``dilate`` grown by the clipped 3x3x3 box
+    (volume.py:289-319).  Returns a lazy BinaryVolume evaluated by the fused kernels."""
+    return BinaryVolume(_source=(v, tf, bool(dilate)), dims=v.dims)
+
+
+def occupancy(b: BinaryVolume) -> float:
+    """Fraction of voxels flagged (volume.py:322-324)."""
+    nx, ny, nz = b.dims
+    return float(b.count_nonzero()) / (nx * ny * nz)
