@@ -5,6 +5,7 @@ the same public names, argument meanings, array layouts and exceptions, backed b
 hand-written CUDA kernels in libvsb200.so (include/vsb200.h).  There is no CPU fallback.
 """
 
+from .bench import INDEX_KINDS, build_index, index_kind, report_stats
 from .lbvh import (BrickSet, Lbvh, MortonRangeError, build_lbvh, empty_lbvh, flag_bricks,
                    leaf_boxes, morton_decode, morton_encode)
 from .svt import MacroGrid, derive_macro_grid

@@ -33,43 +33,66 @@ void set_error(const char* fmt, ...) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Visibility of four packed u8 bins -> 0x80 in every visible byte.
+// Visibility of four packed u8 bins.  eval<V>(x) returns a word whose bit 7 of every byte is
+// that byte's visibility (other bits are don't-care unless clean<V>()).
+//
+//   V = 0            shared-memory table (clean)
+//   V = 16           constant TF (all or nothing visible; clean)
+//   V = 1 + ops      one visibility flip at bin c0        ops: bit0 c0 >= 128, bit2 bin 0 visible
+//   V = 8 + ops      two flips at c0 < c1                 ops: bit1 c1 >= 128 as well
+//
+// Per byte, x >= c (c in [1,255]) is the high bit of (x|0x80) - (c&0x7f) OR'ed (c < 128) or
+// AND'ed (c >= 128) with x; the subtraction never borrows across bytes.  So a ramp TF costs
+// three integer ops per four voxels, and the OR into the running brick accumulator fuses into
+// the last one (LOP3).
 // ---------------------------------------------------------------------------------------
-struct VisEval {
-  int mode;
-  uint32_t flip;        // 0x80808080 if bin 0 is visible
-  uint32_t c_lo[2];     // (c & 0x7f) replicated
-  uint32_t c_hi[2];     // all-ones if c >= 128 (then x >= c needs the high bit)
-  const uint8_t* tab;   // mode 0: shared table, 0x80 / 0 per bin
+constexpr uint32_t HB = 0x80808080u;
+constexpr int V_TABLE = 0, V_CONST = 16;
 
-  __device__ __forceinline__ static uint32_t ge(uint32_t x, uint32_t clo, uint32_t chi) {
-    // per byte x >= c, with c in [1,255]: (x|0x80) - (c&0x7f) never borrows across bytes;
-    // its high bit is (x&0x7f) >= (c&0x7f).
-    const uint32_t H = 0x80808080u;
-    uint32_t r = (x | H) - clo;
-    return ((x & r) | ((x | r) & ~chi)) & H;
-  }
-  template <int MODE>
+struct VisEval {
+  uint32_t clo0, clo1, flip;
+  const uint8_t* tab;  // V_TABLE: 0x80 / 0 per bin, shared memory
+
+  template <int V>
+  __device__ static constexpr bool clean() { return V == V_TABLE || V == V_CONST; }
+
+  template <int V>
   __device__ __forceinline__ uint32_t eval(uint32_t x) const {
-    if (MODE == 1) return ge(x, c_lo[0], c_hi[0]) ^ flip;
-    if (MODE == 2) return ge(x, c_lo[0], c_hi[0]) ^ ge(x, c_lo[1], c_hi[1]) ^ flip;
-    if (MODE == 3) return flip;
-    return (uint32_t)tab[x & 0xff] | ((uint32_t)tab[(x >> 8) & 0xff] << 8) |
-           ((uint32_t)tab[(x >> 16) & 0xff] << 16) | ((uint32_t)tab[x >> 24] << 24);
+    if constexpr (V == V_TABLE) {
+      return (uint32_t)tab[x & 0xff] | ((uint32_t)tab[(x >> 8) & 0xff] << 8) |
+             ((uint32_t)tab[(x >> 16) & 0xff] << 16) | ((uint32_t)tab[x >> 24] << 24);
+    } else if constexpr (V == V_CONST) {
+      return flip;
+    } else if constexpr (V < 8) {
+      constexpr int ops = V - 1;
+      const uint32_t r = (x | HB) - clo0;
+      const uint32_t a = (ops & 1) ? (x & r) : (x | r);
+      return (ops & 4) ? ~a : a;
+    } else {
+      constexpr int ops = V - 8;
+      const uint32_t xh = x | HB;
+      const uint32_t r0 = xh - clo0, r1 = xh - clo1;
+      const uint32_t a = ((ops & 1) ? (x & r0) : (x | r0)) ^ ((ops & 2) ? (x & r1) : (x | r1));
+      return (ops & 4) ? ~a : a;
+    }
   }
 };
 
-__device__ __forceinline__ void load_vis(VisEval& ve, const vs_tf_params* tf, uint8_t* tab) {
-  ve.mode = tf->mode;
-  ve.flip = tf->start ? 0x80808080u : 0u;
-  for (int k = 0; k < 2; ++k) {
-    uint32_t c = (uint32_t)tf->bound[k] & 0xffu;
-    ve.c_lo[k] = (c & 0x7fu) * 0x01010101u;
-    ve.c_hi[k] = (c & 0x80u) ? 0xffffffffu : 0u;
-  }
+__device__ __forceinline__ int load_vis(VisEval& ve, const vs_tf_params* tf, uint8_t* tab) {
+  const uint32_t c0 = (uint32_t)tf->bound[0] & 0xffu, c1 = (uint32_t)tf->bound[1] & 0xffu;
+  ve.clo0 = (c0 & 0x7fu) * 0x01010101u;
+  ve.clo1 = (c1 & 0x7fu) * 0x01010101u;
+  ve.flip = tf->start ? HB : 0u;
   for (int b = threadIdx.x; b < 256; b += blockDim.x)
     tab[b] = ((tf->vis[b >> 5] >> (b & 31)) & 1u) ? 0x80 : 0;
   ve.tab = tab;
+  const int start = tf->start ? 4 : 0;
+  switch (tf->mode) {
+    case 1: return 1 + ((c0 & 0x80u) ? 1 : 0) + start;
+    case 2: return 8 + ((c0 & 0x80u) ? 1 : 0) + ((c1 & 0x80u) ? 2 : 0) + start;
+    case 3: return V_CONST;
+    default: return V_TABLE;
+  }
 }
 
 // 4 visible-flag bytes (0x80 each) -> 4 contiguous bits.
@@ -86,7 +109,60 @@ __device__ __forceinline__ uint32_t compress4(uint32_t g) {
 // ---------------------------------------------------------------------------------------
 constexpr int SUMMARY_WARPS = 8;
 
-template <int MODE, bool WRITE_BITS, bool COUNT>
+// One x slab (8 rows in y) of a lane's brick pair -> 9-bit (y,z) category masks pa, pb.
+template <int V, bool WRITE_BITS, bool COUNT, bool FULL>
+__device__ __forceinline__ void summary_slab(const VisEval& ve, const uint8_t* __restrict__ vol,
+                                             int x, int y0, int ny, int nz, int z0, int nzw,
+                                             int lane, unsigned amask,
+                                             uint32_t* __restrict__ bits, uint32_t& cnt,
+                                             uint32_t& pa, uint32_t& pb) {
+  // y-category accumulators (word pairs) for brick A and B
+  uint32_t ya0 = 0, ya1 = 0, yfa0 = 0, yfa1 = 0, yla0 = 0, yla1 = 0;
+  uint32_t yb0 = 0, yb1 = 0, yfb0 = 0, yfb1 = 0, ylb0 = 0, ylb1 = 0;
+  const uint8_t* row = vol + ((int64_t)x * ny + y0) * nz + z0;
+  uint4 v[8];
+#pragma unroll
+  for (int ly = 0; ly < 8; ++ly) {
+    if (FULL || y0 + ly < ny)
+      v[ly] = __ldcs(reinterpret_cast<const uint4*>(row + (int64_t)ly * nz));
+  }
+#pragma unroll
+  for (int ly = 0; ly < 8; ++ly) {
+    if (!(FULL || y0 + ly < ny)) continue;  // rows past ny: not part of the volume
+    uint32_t g0 = ve.eval<V>(v[ly].x), g1 = ve.eval<V>(v[ly].y);
+    uint32_t g2 = ve.eval<V>(v[ly].z), g3 = ve.eval<V>(v[ly].w);
+    if (COUNT || WRITE_BITS) {
+      if (!VisEval::clean<V>()) { g0 &= HB; g1 &= HB; g2 &= HB; g3 &= HB; }
+    }
+    if (COUNT) cnt += __popc(g0 | (g1 >> 1) | (g2 >> 2) | (g3 >> 3));
+    if (WRITE_BITS) {
+      uint32_t m = compress4(g0) | (compress4(g1) << 4) | (compress4(g2) << 8) |
+                   (compress4(g3) << 12);
+      uint32_t other = __shfl_down_sync(amask, m, 1);
+      const int64_t wbase = ((int64_t)x * ny + (y0 + ly)) * nzw;
+      if ((lane & 1) == 0) {
+        uint32_t word = m | ((z0 + 16 < nz) ? (other << 16) : 0u);
+        bits[wbase + (z0 >> 5)] = word;
+      }
+    }
+    ya0 |= g0; ya1 |= g1; yb0 |= g2; yb1 |= g3;
+    if (ly == 0) { yfa0 = g0; yfa1 = g1; yfb0 = g2; yfb1 = g3; }
+    if (ly == 7) { yla0 = g0; yla1 = g1; ylb0 = g2; ylb1 = g3; }
+  }
+  if (!VisEval::clean<V>() && !(COUNT || WRITE_BITS)) {
+    ya0 &= HB; ya1 &= HB; yb0 &= HB; yb1 &= HB;
+    yfa0 &= HB; yfa1 &= HB; yfb0 &= HB; yfb1 &= HB;
+    yla0 &= HB; yla1 &= HB; ylb0 &= HB; ylb1 &= HB;
+  }
+  // z categories of a word pair -> 3 bits: bit0 last slab (z7), bit1 any, bit2 first (z0)
+  auto zc3 = [](uint32_t w0, uint32_t w1) -> uint32_t {
+    return (w1 >> 31) | (((w0 | w1) != 0u) << 1) | (((w0 >> 7) & 1u) << 2);
+  };
+  pa = zc3(yla0, yla1) | (zc3(ya0, ya1) << 3) | (zc3(yfa0, yfa1) << 6);
+  pb = zc3(ylb0, ylb1) | (zc3(yb0, yb1) << 3) | (zc3(yfb0, yfb1) << 6);
+}
+
+template <int V, bool WRITE_BITS, bool COUNT>
 __device__ __forceinline__ void summary_body(const VisEval& ve, uint32_t* red,
                                              const uint8_t* __restrict__ vol, int nx, int ny,
                                              int nz, uint32_t* __restrict__ summary,
@@ -113,56 +189,18 @@ __device__ __forceinline__ void summary_body(const VisEval& ve, uint32_t* red,
     uint32_t xa_any = 0, xa_first = 0, xa_last = 0;
     uint32_t xb_any = 0, xb_first = 0, xb_last = 0;
     if (active) {
+      const bool full_y = y0 + 8 <= ny;  // warp-uniform
 #pragma unroll 1
       for (int lx = 0; lx < 8; ++lx) {
         const int x = x0 + lx;
         if (x >= nx) break;
-        // y-category accumulators (word pairs) for brick A and B
-        uint32_t ya0 = 0, ya1 = 0, yfa0 = 0, yfa1 = 0, yla0 = 0, yla1 = 0;
-        uint32_t yb0 = 0, yb1 = 0, yfb0 = 0, yfb1 = 0, ylb0 = 0, ylb1 = 0;
-        const uint8_t* row = vol + ((int64_t)x * ny + y0) * nz + z0;
-        uint4 v[8];
-#pragma unroll
-        for (int ly = 0; ly < 8; ++ly) {
-          if (y0 + ly < ny)
-            v[ly] = __ldcs(reinterpret_cast<const uint4*>(row + (int64_t)ly * nz));
-          else
-            v[ly] = make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int ly = 0; ly < 8; ++ly) {
-          uint32_t g0, g1, g2, g3;
-          if (y0 + ly < ny) {
-            g0 = ve.eval<MODE>(v[ly].x);
-            g1 = ve.eval<MODE>(v[ly].y);
-            g2 = ve.eval<MODE>(v[ly].z);
-            g3 = ve.eval<MODE>(v[ly].w);
-          } else {
-            g0 = g1 = g2 = g3 = 0;
-          }
-          if (COUNT) cnt += __popc(g0) + __popc(g1) + __popc(g2) + __popc(g3);
-          if (WRITE_BITS) {
-            uint32_t m = compress4(g0) | (compress4(g1) << 4) | (compress4(g2) << 8) |
-                         (compress4(g3) << 12);
-            uint32_t other = __shfl_down_sync(amask, m, 1);
-            if (y0 + ly < ny) {
-              const int64_t wbase = ((int64_t)x * ny + (y0 + ly)) * nzw;
-              if ((lane & 1) == 0) {
-                uint32_t word = m | ((z0 + 16 < nz) ? (other << 16) : 0u);
-                bits[wbase + (z0 >> 5)] = word;
-              }
-            }
-          }
-          ya0 |= g0; ya1 |= g1; yb0 |= g2; yb1 |= g3;
-          if (ly == 0) { yfa0 = g0; yfa1 = g1; yfb0 = g2; yfb1 = g3; }
-          if (ly == 7) { yla0 = g0; yla1 = g1; ylb0 = g2; ylb1 = g3; }
-        }
-        // z categories of a word pair -> 3 bits: bit0 last slab (z7), bit1 any, bit2 first (z0)
-        auto zc3 = [](uint32_t w0, uint32_t w1) -> uint32_t {
-          return (w1 >> 31) | (((w0 | w1) != 0u) << 1) | (((w0 >> 7) & 1u) << 2);
-        };
-        const uint32_t pa = zc3(yla0, yla1) | (zc3(ya0, ya1) << 3) | (zc3(yfa0, yfa1) << 6);
-        const uint32_t pb = zc3(ylb0, ylb1) | (zc3(yb0, yb1) << 3) | (zc3(yfb0, yfb1) << 6);
+        uint32_t pa, pb;
+        if (full_y)
+          summary_slab<V, WRITE_BITS, COUNT, true>(ve, vol, x, y0, ny, nz, z0, nzw, lane,
+                                                   amask, bits, cnt, pa, pb);
+        else
+          summary_slab<V, WRITE_BITS, COUNT, false>(ve, vol, x, y0, ny, nz, z0, nzw, lane,
+                                                    amask, bits, cnt, pa, pb);
         xa_any |= pa; xb_any |= pb;
         if (lx == 0) { xa_first = pa; xb_first = pb; }
         if (lx == 7) { xa_last = pa; xb_last = pb; }
@@ -185,35 +223,52 @@ __device__ __forceinline__ void summary_body(const VisEval& ve, uint32_t* red,
   }
 }
 
-template <bool WRITE_BITS, bool COUNT>
+#define VS_SUMMARY_ARGS ve, red, vol, nx, ny, nz, summary, bits, count, nbx, nby, nbz, nzc, ntasks
+
+// Fast kernel (summary only): one instantiation per visibility shape, chosen per launch from
+// the device parameter block (uniform branch), so CUDA-graph replays follow TF changes.
 __global__ void __launch_bounds__(SUMMARY_WARPS * 32)
     k_brick_summary(const uint8_t* __restrict__ vol, int nx, int ny, int nz,
                     const vs_tf_params* __restrict__ tf, uint32_t* __restrict__ summary,
-                    uint32_t* __restrict__ bits, unsigned long long* __restrict__ count,
                     int nbx, int nby, int nbz, int nzc, int64_t ntasks) {
+  __shared__ uint8_t tab[256];
+  __shared__ uint32_t red[SUMMARY_WARPS];
+  uint32_t* bits = nullptr;
+  unsigned long long* count = nullptr;
+  VisEval ve;
+  const int v = load_vis(ve, tf, tab);
+  __syncthreads();
+  switch (v) {
+    case 1: summary_body<1, false, false>(VS_SUMMARY_ARGS); break;
+    case 2: summary_body<2, false, false>(VS_SUMMARY_ARGS); break;
+    case 5: summary_body<5, false, false>(VS_SUMMARY_ARGS); break;
+    case 6: summary_body<6, false, false>(VS_SUMMARY_ARGS); break;
+    case 8: summary_body<8, false, false>(VS_SUMMARY_ARGS); break;
+    case 9: summary_body<9, false, false>(VS_SUMMARY_ARGS); break;
+    case 10: summary_body<10, false, false>(VS_SUMMARY_ARGS); break;
+    case 11: summary_body<11, false, false>(VS_SUMMARY_ARGS); break;
+    case 12: summary_body<12, false, false>(VS_SUMMARY_ARGS); break;
+    case 13: summary_body<13, false, false>(VS_SUMMARY_ARGS); break;
+    case 14: summary_body<14, false, false>(VS_SUMMARY_ARGS); break;
+    case 15: summary_body<15, false, false>(VS_SUMMARY_ARGS); break;
+    case V_CONST: summary_body<V_CONST, false, false>(VS_SUMMARY_ARGS); break;
+    default: summary_body<V_TABLE, false, false>(VS_SUMMARY_ARGS); break;
+  }
+}
+
+// Side-output kernel (packed undilated bits and/or the visible count): table lookup.
+template <bool WRITE_BITS, bool COUNT>
+__global__ void __launch_bounds__(SUMMARY_WARPS * 32)
+    k_brick_summary_out(const uint8_t* __restrict__ vol, int nx, int ny, int nz,
+                        const vs_tf_params* __restrict__ tf, uint32_t* __restrict__ summary,
+                        uint32_t* __restrict__ bits, unsigned long long* __restrict__ count,
+                        int nbx, int nby, int nbz, int nzc, int64_t ntasks) {
   __shared__ uint8_t tab[256];
   __shared__ uint32_t red[SUMMARY_WARPS];
   VisEval ve;
   load_vis(ve, tf, tab);
   __syncthreads();
-  switch (ve.mode) {  // uniform: one TF per launch
-    case 1:
-      summary_body<1, WRITE_BITS, COUNT>(ve, red, vol, nx, ny, nz, summary, bits, count, nbx,
-                                         nby, nbz, nzc, ntasks);
-      break;
-    case 2:
-      summary_body<2, WRITE_BITS, COUNT>(ve, red, vol, nx, ny, nz, summary, bits, count, nbx,
-                                         nby, nbz, nzc, ntasks);
-      break;
-    case 3:
-      summary_body<3, WRITE_BITS, COUNT>(ve, red, vol, nx, ny, nz, summary, bits, count, nbx,
-                                         nby, nbz, nzc, ntasks);
-      break;
-    default:
-      summary_body<0, WRITE_BITS, COUNT>(ve, red, vol, nx, ny, nz, summary, bits, count, nbx,
-                                         nby, nbz, nzc, ntasks);
-      break;
-  }
+  summary_body<V_TABLE, WRITE_BITS, COUNT>(VS_SUMMARY_ARGS);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -552,17 +607,17 @@ int vs_classify_summary(const uint8_t* bins, int nx, int ny, int nz, const vs_tf
   const int64_t ntasks = (int64_t)nbx * nby * nzc;
   const unsigned grid = (unsigned)cdiv(ntasks, SUMMARY_WARPS);
   if (bits && count)
-    k_brick_summary<true, true><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
+    k_brick_summary_out<true, true><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
         bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
   else if (bits)
-    k_brick_summary<true, false><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
+    k_brick_summary_out<true, false><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
         bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
   else if (count)
-    k_brick_summary<false, true><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
+    k_brick_summary_out<false, true><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
         bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
   else
-    k_brick_summary<false, false><<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(
-        bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
+    k_brick_summary<<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(bins, nx, ny, nz, tf, summary,
+                                                            nbx, nby, nbz, nzc, ntasks);
   return check_launch("k_brick_summary");
 }
 

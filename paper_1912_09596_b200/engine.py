@@ -24,7 +24,7 @@ from .volume import TransferFunction, Volume
 
 class LbvhRebuilder:
     def __init__(self, v: Volume, brick_size: int = 8, with_grid: bool = False,
-                 count: bool = True):
+                 count: bool = False):
         if brick_size != 8 or v.dims[2] % 16 != 0:
             raise ValueError("LbvhRebuilder needs 8^3 bricks and nz % 16 == 0")
         self.v = v

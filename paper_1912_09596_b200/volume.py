@@ -242,20 +242,21 @@ class BinaryVolume:
         """The fused brick-summary kernel applies (8^3 bricks, rows of 16-byte multiples)."""
         return self._source is not None and self._dims[2] % 16 == 0
 
-    def summary(self) -> torch.Tensor:
-        """27-bit halo summaries per 8^3 brick (vs_classify_summary); computes the undilated
-        visible count in the same pass."""
-        if self._summary is None:
+    def summary(self, count: bool = False) -> torch.Tensor:
+        """27-bit halo summaries per 8^3 brick (vs_classify_summary); with ``count`` the
+        undilated visible-voxel count is taken in the same pass."""
+        if self._summary is None or (count and self._count is None):
             v, tf, _ = self._source
             nx, ny, nz = self._dims
             dev = _lib.device()
             nb = [-(-d // 8) for d in self._dims]
             s = torch.empty(nb[0] * nb[1] * nb[2], dtype=torch.int32, device=dev)
-            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev) if count else None
             call("vs_classify_summary", ptr(v.bins), nx, ny, nz, ptr(tf.params()), ptr(s), None,
                  ptr(cnt), stream())
             self._summary = s
-            self._count = cnt
+            if count:
+                self._count = cnt
         return self._summary
 
     def packed(self) -> torch.Tensor:
@@ -281,7 +282,7 @@ class BinaryVolume:
         """Visible voxels of the UNDILATED classification behind a lazy volume."""
         if self._count is None:
             if self.summary_ok():
-                self.summary()
+                self.summary(count=True)
             else:
                 self.packed()
         return int(self._count.item())

@@ -106,7 +106,8 @@ def _band_lut(lo, hi):
 
 
 @pytest.mark.parametrize("dims", [(48, 40, 64), (64, 64, 32), (33, 17, 48), (24, 24, 528)])
-@pytest.mark.parametrize("tfkind", ["ramp", "band", "twoband", "comb", "all", "none"])
+@pytest.mark.parametrize("tfkind", ["ramp", "ramp_lo", "band", "band_mid", "band_lo", "low", "lowhi",
+                                    "twoband", "comb", "all", "none"])
 def test_random_volumes_vs_oracle(vs, rng, dims, tfkind):
     """Fused summary path (all four visibility modes) vs the oracle on blocky random u8."""
     nx, ny, nz = dims
@@ -117,8 +118,18 @@ def test_random_volumes_vs_oracle(vs, rng, dims, tfkind):
     u8[mask] = noise[mask]
     if tfkind == "ramp":
         lut = vs.TransferFunction.ramp(0.8).lut
+    elif tfkind == "ramp_lo":
+        lut = vs.TransferFunction.ramp(0.2).lut
     elif tfkind == "band":
         lut = _band_lut(200, 203)
+    elif tfkind == "band_mid":
+        lut = _band_lut(100, 150)
+    elif tfkind == "band_lo":
+        lut = _band_lut(10, 12)
+    elif tfkind == "low":
+        lut = _band_lut(0, 99)
+    elif tfkind == "lowhi":
+        lut = _band_lut(0, 199)
     elif tfkind == "twoband":
         lut = _band_lut(10, 12)
         lut[250:, 3] = 0.25
