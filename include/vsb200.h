@@ -142,6 +142,74 @@ int vs_lbvh_from_bricks(const int32_t* coords, const uint32_t* codes, int64_t n,
                         int32_t* right, int32_t* leaf_brick, int32_t* brick_coords, int* info,
                         void* ws, size_t ws_bytes, vs_stream_t stream);
 
+
+/* ---- renderer: render_frame (render.py:869-911) and the single-ray API (:917-1015) ------ */
+enum { VS_KIND_NAIVE = 0, VS_KIND_GRID = 1, VS_KIND_LBVH = 2, VS_KIND_KD = 3, VS_KIND_HYBRID = 4 };
+enum { VS_RF_OVERFLOW = 1, VS_RF_ORDER = 2 }; /* render flags */
+
+typedef struct vs_volume_desc {
+  const uint8_t* bins;   /* u8 LUT bins, C-order                                      */
+  const float* field;    /* float32 field, or NULL when the field is f32(bin/255) exactly */
+  int nx, ny, nz, pad;
+} vs_volume_desc;
+
+/* An index for traversal (render.py:41, index_kind :44-55).
+ * grid / hybrid: occ (ncx,ncy,ncz) bool bytes, cell size cs (svt.py:29-37).
+ * lbvh: lo/hi (m,3), left/right (m,); root = 0 if lbvh_info[0] (device n_bricks) > 0 else -1
+ *       (lbvh_info may be NULL, then `root` is used).
+ * kd / hybrid: lo/hi (m,3), axis (m,) int8, plane/left/right (m,), root (kdtree.py:85-127). */
+typedef struct vs_index_desc {
+  int kind;
+  int root;
+  const uint8_t* occ;
+  int ncx, ncy, ncz, cs;
+  const int32_t* lo;
+  const int32_t* hi;
+  const int32_t* left;
+  const int32_t* right;
+  const int32_t* plane;
+  const int8_t* axis;
+  const int* lbvh_info;
+} vs_index_desc;
+
+/* Orthographic camera with the host-normalised frame of Camera.ray_origins (render.py:134-149):
+ * pixel (i, j) starts at (eye + ys*up) + xs*right, xs = ((i + 0.5) - w/2)*scale,
+ * ys = ((h/2 - j) - 0.5)*scale, and marches along dir. */
+typedef struct vs_camera_desc {
+  double eye[3], up[3], right[3], dir[3];
+  double scale;
+  int width, height;
+} vs_camera_desc;
+
+/* Which image rows this launch renders: local row l -> stripe s = l / stripe, image row
+ * (s*nparts + part)*stripe + l % stripe (interleaved row stripes for multi-GPU tiles). */
+typedef struct vs_rows_desc {
+  int nrows, stripe, nparts, part;
+} vs_rows_desc;
+
+/* Render rows of a frame.  lut: (256,4) float32 device; corr: 256 float64 device holding
+ * 1 - (1 - lut[b,3])^dt computed with libm pow (render.py:752).  Outputs per local row-major
+ * pixel: rgba8 (quantised), optional float64 premultiplied rgba, optional per-pixel sample
+ * counts; *total_opt += sum of samples (caller zeroes).  *flags |= VS_RF_* on stack overflow
+ * or non-monotone interval emission (the host raises).  rows_opt NULL = the full frame. */
+int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camera_desc* cam,
+              const float* lut, const double* corr, double dt, int nearest,
+              const vs_rows_desc* rows_opt, uint8_t* rgba8, double* rgba64_opt,
+              int32_t* samples_opt, unsigned long long* total_opt, int* flags,
+              vs_stream_t stream);
+
+/* traverse_* (render.py:928-961) for a batch of rays: out (nrays, cap, 2) merged intervals,
+ * counts[q] = total intervals of ray q (may exceed cap; then out holds the first cap). */
+int vs_traverse_rays(const vs_index_desc* ix, int nx, int ny, int nz, const double* origins,
+                     const double* dir, int nrays, double* out, int cap, int* counts, int* flags,
+                     vs_stream_t stream);
+
+/* integrate (render.py:964-1001) for a batch of rays over given segments. */
+int vs_integrate_rays(const vs_volume_desc* vol, const double* origins, const double* dir,
+                      const double* segs, const int* counts, int cap, int nrays,
+                      const float* lut, const double* corr, double dt, int nearest,
+                      double* rgba, long long* samples, vs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,9 @@ SIGNATURES: dict[str, tuple] = {
     "vs_lbvh_from_bitmap": (i32, [P, P, i32, i32, i32, i32, i32, i64, P, P, P, P, P, P, P, P,
                                   SZ, P]),
     "vs_lbvh_bricks_workspace": (SZ, [i64]),
+    "vs_render": (i32, [P, P, P, P, P, C.c_double, i32, P, P, P, P, P, P, P]),
+    "vs_traverse_rays": (i32, [P, i32, i32, i32, P, P, i32, P, i32, P, P, P]),
+    "vs_integrate_rays": (i32, [P, P, P, P, P, i32, i32, P, P, C.c_double, i32, P, P, P]),
     "vs_lbvh_from_bricks": (i32, [P, P, i64, i32, i32, i32, i32, P, P, P, P, P, P, P, P, SZ,
                                   P]),
 }

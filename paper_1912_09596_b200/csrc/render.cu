@@ -1,0 +1,609 @@
+// DVR ray marcher: one thread per pixel ray, index traversal streamed straight into the
+// lattice-locked front-to-back integrator.
+//
+// Reference semantics (paths relative to /root/reference/pkg/src/voxelskip/render.py):
+//   Camera.ray_origins :134-149  origin = (eye + ys*up) + xs*right, top row first
+//   _ray_setup :273-287, _slab :196-240 (half-open boxes, zero-direction containment)
+//   _k_naive :290-302, _dda_runs/_k_grid :305-401, _k_bvh :404-504, _kd_leaves/_k_kd
+//   :507-590, _k_hybrid :593-630, _sort_merge :243-270, _k_integrate :633-765,
+//   render_frame :869-911 (quantise floor(x*255 + 0.5) clipped).
+//
+// The reference collects every leaf interval of a ray, sorts and merges them, then
+// integrates.  Here the traversals emit intervals already in increasing t (siblings of the
+// LBVH and k-d trees are separated by an axis plane and visited near-first; DDA runs are
+// monotone), so a one-interval merge window reproduces _sort_merge exactly and the
+// integrator consumes intervals as they appear: no per-ray buffers, no overflow re-run.  A
+// non-monotone emission (which would make the streaming result differ) raises a flag the
+// host turns into an error.
+//
+// Arithmetic is the reference's: IEEE double, no FMA (the library is built -fmad=false),
+// trilinear first-level differences in float32 (numba types f32 - f32 as f32), opacity
+// correction 1 - (1 - a)^dt from a host table computed with libm pow (== numba's **).
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace vs {
+
+constexpr double R_FAR = 1e300;
+constexpr int RENDER_TX = 16, RENDER_TY = 8;  // 128-thread pixel tiles
+constexpr int STACK_CAP = 128;
+
+enum RenderFlags { RF_OVERFLOW = 1, RF_ORDER = 2 };
+
+struct Ray {
+  double ox, oy, oz, dx, dy, dz, ix, iy, iz;
+  bool zx, zy, zz;
+};
+
+__device__ __forceinline__ void ray_setup(Ray& r, double ox, double oy, double oz,
+                                          const vs_camera_desc& c) {
+  r.ox = ox; r.oy = oy; r.oz = oz;
+  r.dx = c.dir[0]; r.dy = c.dir[1]; r.dz = c.dir[2];
+  r.zx = r.dx == 0.0; r.zy = r.dy == 0.0; r.zz = r.dz == 0.0;
+  r.ix = r.zx ? 0.0 : 1.0 / r.dx;
+  r.iy = r.zy ? 0.0 : 1.0 / r.dy;
+  r.iz = r.zz ? 0.0 : 1.0 / r.dz;
+}
+
+// _slab: [l, h) box; returns hit and (t0, t1) with t1 > t0.
+__device__ __forceinline__ bool slab(const Ray& r, double lx, double ly, double lz, double hx,
+                                     double hy, double hz, double& t0, double& t1) {
+  double tmin = -R_FAR, tmax = R_FAR;
+  if (r.zx) {
+    if (r.ox < lx || r.ox >= hx) return false;
+  } else {
+    double ta = __dmul_rn(lx - r.ox, r.ix), tb = __dmul_rn(hx - r.ox, r.ix);
+    if (ta > tb) { double t = ta; ta = tb; tb = t; }
+    if (ta > tmin) tmin = ta;
+    if (tb < tmax) tmax = tb;
+  }
+  if (r.zy) {
+    if (r.oy < ly || r.oy >= hy) return false;
+  } else {
+    double ta = __dmul_rn(ly - r.oy, r.iy), tb = __dmul_rn(hy - r.oy, r.iy);
+    if (ta > tb) { double t = ta; ta = tb; tb = t; }
+    if (ta > tmin) tmin = ta;
+    if (tb < tmax) tmax = tb;
+  }
+  if (r.zz) {
+    if (r.oz < lz || r.oz >= hz) return false;
+  } else {
+    double ta = __dmul_rn(lz - r.oz, r.iz), tb = __dmul_rn(hz - r.oz, r.iz);
+    if (ta > tb) { double t = ta; ta = tb; tb = t; }
+    if (ta > tmin) tmin = ta;
+    if (tb < tmax) tmax = tb;
+  }
+  if (tmax <= tmin) return false;
+  t0 = tmin;
+  t1 = tmax;
+  return true;
+}
+
+__device__ __forceinline__ bool node_slab(const Ray& r, const int32_t* __restrict__ lo,
+                                          const int32_t* __restrict__ hi, int i, double& a,
+                                          double& b) {
+  const int32_t* l = lo + 3 * i;
+  const int32_t* h = hi + 3 * i;
+  return slab(r, (double)__ldg(l), (double)__ldg(l + 1), (double)__ldg(l + 2),
+              (double)__ldg(h), (double)__ldg(h + 1), (double)__ldg(h + 2), a, b);
+}
+
+// Shared per-CTA tables.
+struct RenderSmem {
+  float4 lut[256];
+  double corr[256];
+  float u8f[256];
+};
+
+// ---- integrator (_k_integrate for one ray, fed segment by segment) -------------------------
+struct Integrator {
+  const Ray* r;
+  const RenderSmem* sm;
+  const uint8_t* __restrict__ bins;
+  const float* __restrict__ field;  // null: u8 field f32(u/255)
+  int nx, ny, nz;
+  double entry, dt;
+  bool nearest;
+  double accr, accg, accb, acca;
+  int64_t taken;
+
+  __device__ __forceinline__ float fetch(int64_t idx) const {
+    if (field) return __ldg(field + idx);
+    return sm->u8f[__ldg(bins + idx)];
+  }
+
+  __device__ __forceinline__ void segment(double t0, double t1) {
+    int64_t k = (int64_t)ceil(__ddiv_rn(t0 - entry, dt));
+    if (k < 0) k = 0;
+    while (k > 0 && __dadd_rn(entry, __dmul_rn((double)(k - 1), dt)) >= t0) k--;
+    while (__dadd_rn(entry, __dmul_rn((double)k, dt)) < t0) k++;
+    double t = __dadd_rn(entry, __dmul_rn((double)k, dt));
+    const int64_t sy = nz, sx = (int64_t)ny * nz;
+    while (t < t1) {
+      const double px = __dadd_rn(r->ox, __dmul_rn(t, r->dx));
+      const double py = __dadd_rn(r->oy, __dmul_rn(t, r->dy));
+      const double pz = __dadd_rn(r->oz, __dmul_rn(t, r->dz));
+      double value;
+      if (nearest) {
+        int64_t xi = (int64_t)floor(px), yi = (int64_t)floor(py), zi = (int64_t)floor(pz);
+        xi = xi < 0 ? 0 : (xi > nx - 1 ? nx - 1 : xi);
+        yi = yi < 0 ? 0 : (yi > ny - 1 ? ny - 1 : yi);
+        zi = zi < 0 ? 0 : (zi > nz - 1 ? nz - 1 : zi);
+        value = (double)fetch(xi * sx + yi * sy + zi);
+      } else {
+        const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
+        int64_t x0 = (int64_t)floor(qx), y0 = (int64_t)floor(qy), z0 = (int64_t)floor(qz);
+        const double fx = qx - (double)x0, fy = qy - (double)y0, fz = qz - (double)z0;
+        int64_t x1 = x0 + 1, y1 = y0 + 1, z1 = z0 + 1;
+        x0 = x0 < 0 ? 0 : (x0 > nx - 1 ? nx - 1 : x0);
+        y0 = y0 < 0 ? 0 : (y0 > ny - 1 ? ny - 1 : y0);
+        z0 = z0 < 0 ? 0 : (z0 > nz - 1 ? nz - 1 : z0);
+        x1 = x1 < 0 ? 0 : (x1 > nx - 1 ? nx - 1 : x1);
+        y1 = y1 < 0 ? 0 : (y1 > ny - 1 ? ny - 1 : y1);
+        z1 = z1 < 0 ? 0 : (z1 > nz - 1 ? nz - 1 : z1);
+        const int64_t b00 = x0 * sx + y0 * sy, b10 = x1 * sx + y0 * sy;
+        const int64_t b01 = x0 * sx + y1 * sy, b11 = x1 * sx + y1 * sy;
+        const float c000 = fetch(b00 + z0), c100 = fetch(b10 + z0);
+        const float c010 = fetch(b01 + z0), c110 = fetch(b11 + z0);
+        const float c001 = fetch(b00 + z1), c101 = fetch(b10 + z1);
+        const float c011 = fetch(b01 + z1), c111 = fetch(b11 + z1);
+        const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
+        const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
+        const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, fx));
+        const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, fx));
+        const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, fx));
+        const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, fx));
+        const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, fy));
+        const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, fy));
+        value = __dadd_rn(c0, __dmul_rn(c1 - c0, fz));
+      }
+      const double bd = floor(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
+      const int bin = bd < 0.0 ? 0 : (bd > 255.0 ? 255 : (int)bd);
+      const float4 c = sm->lut[bin];
+      if (c.w > 0.0f) {
+        const double w = __dmul_rn(1.0 - acca, sm->corr[bin]);
+        accr = __dadd_rn(accr, __dmul_rn(w, (double)c.x));
+        accg = __dadd_rn(accg, __dmul_rn(w, (double)c.y));
+        accb = __dadd_rn(accb, __dmul_rn(w, (double)c.z));
+        acca = __dadd_rn(acca, w);
+      }
+      ++taken;
+      ++k;
+      t = __dadd_rn(entry, __dmul_rn((double)k, dt));
+    }
+  }
+};
+
+// One-interval merge window (= _sort_merge on a t-sorted stream).
+template <class Sink>
+struct Merger {
+  Sink* sink;
+  double a, b, last_t0;
+  bool open;
+  int* flags;
+  __device__ __forceinline__ void push(double t0, double t1) {
+    if (t0 < last_t0) *flags |= RF_ORDER;
+    last_t0 = t0;
+    if (t1 <= t0) return;
+    if (open && t0 <= b) {
+      if (t1 > b) b = t1;
+    } else {
+      if (open) sink->segment(a, b);
+      a = t0;
+      b = t1;
+      open = true;
+    }
+  }
+  __device__ __forceinline__ void flush() {
+    if (open) sink->segment(a, b);
+    open = false;
+  }
+};
+
+template <class Sink>
+__device__ __forceinline__ Merger<Sink> make_merger(Sink* s, int* flags) {
+  Merger<Sink> m;
+  m.sink = s;
+  m.a = m.b = 0.0;
+  m.last_t0 = -DBL_MAX;
+  m.open = false;
+  m.flags = flags;
+  return m;
+}
+
+// _dda_runs over the macro grid between t_in and t_out, runs pushed into `out`.
+template <class Out>
+__device__ void dda_runs(const Ray& r, const vs_index_desc& ix, double t_in, double t_out,
+                         Out& out) {
+  const int ncx = ix.ncx, ncy = ix.ncy, ncz = ix.ncz;
+  const double cs = (double)ix.cs;
+  const double px = __dadd_rn(r.ox, __dmul_rn(t_in, r.dx));
+  const double py = __dadd_rn(r.oy, __dmul_rn(t_in, r.dy));
+  const double pz = __dadd_rn(r.oz, __dmul_rn(t_in, r.dz));
+  int64_t cx = (int64_t)floor(__ddiv_rn(px, cs)), cy = (int64_t)floor(__ddiv_rn(py, cs)),
+          cz = (int64_t)floor(__ddiv_rn(pz, cs));
+  cx = cx < 0 ? 0 : (cx > ncx - 1 ? ncx - 1 : cx);
+  cy = cy < 0 ? 0 : (cy > ncy - 1 ? ncy - 1 : cy);
+  cz = cz < 0 ? 0 : (cz > ncz - 1 ? ncz - 1 : cz);
+  const int sx = r.zx ? 0 : (r.ix > 0.0 ? 1 : -1);
+  const int sy = r.zy ? 0 : (r.iy > 0.0 ? 1 : -1);
+  const int sz = r.zz ? 0 : (r.iz > 0.0 ? 1 : -1);
+  auto cross = [&](int64_t c, int s, double o, double inv) -> double {
+    return __dmul_rn(__dmul_rn((double)(c + (s > 0)), cs) - o, inv);
+  };
+  double tnx = sx == 0 ? R_FAR : cross(cx, sx, r.ox, r.ix);
+  double tny = sy == 0 ? R_FAR : cross(cy, sy, r.oy, r.iy);
+  double tnz = sz == 0 ? R_FAR : cross(cz, sz, r.oz, r.iz);
+  bool open_run = false;
+  double run_t0 = 0.0, tcur = t_in;
+  const int64_t max_steps = (int64_t)ncx + ncy + ncz + 3;
+  for (int64_t step = 0; step < max_steps; ++step) {
+    double tn = tnx;
+    if (tny < tn) tn = tny;
+    if (tnz < tn) tn = tnz;
+    if (__ldg(ix.occ + (cx * ncy + cy) * ncz + cz)) {
+      if (!open_run) { open_run = true; run_t0 = tcur; }
+    } else if (open_run) {
+      out.push(run_t0, tcur);
+      open_run = false;
+    }
+    if (tn >= t_out) break;
+    if (tnx == tn) { cx += sx; tnx = cross(cx, sx, r.ox, r.ix); }
+    if (tny == tn) { cy += sy; tny = cross(cy, sy, r.oy, r.iy); }
+    if (tnz == tn) { cz += sz; tnz = cross(cz, sz, r.oz, r.iz); }
+    tcur = tn;
+    if (cx < 0 || cy < 0 || cz < 0 || cx >= ncx || cy >= ncy || cz >= ncz) break;
+  }
+  if (open_run) out.push(run_t0, t_out);
+}
+
+// _k_bvh leaf intervals, near-first DFS; the stack holds node ids (a popped node's clipped
+// interval is recomputed: same inputs, same doubles).
+template <class Out>
+__device__ void bvh_leaves(const Ray& r, const vs_index_desc& ix, int root, double tmin,
+                           double tmax, Out& out, int* flags) {
+  int stk[STACK_CAP];
+  int sp = 0;
+  double a, b;
+  if (root < 0) return;
+  if (node_slab(r, ix.lo, ix.hi, root, a, b)) {
+    a = a > tmin ? a : tmin;
+    b = b < tmax ? b : tmax;
+    if (b > a) stk[sp++] = root;
+  }
+  while (sp > 0) {
+    const int i = stk[--sp];
+    const int li = __ldg(ix.left + i);
+    if (li < 0) {
+      node_slab(r, ix.lo, ix.hi, i, a, b);
+      a = a > tmin ? a : tmin;
+      b = b < tmax ? b : tmax;
+      out.push(a, b);
+      continue;
+    }
+    const int ri = __ldg(ix.right + i);
+    double la, lb, ra, rb;
+    bool hl = node_slab(r, ix.lo, ix.hi, li, la, lb);
+    if (hl) { la = la > tmin ? la : tmin; lb = lb < tmax ? lb : tmax; if (lb <= la) hl = false; }
+    bool hr = node_slab(r, ix.lo, ix.hi, ri, ra, rb);
+    if (hr) { ra = ra > tmin ? ra : tmin; rb = rb < tmax ? rb : tmax; if (rb <= ra) hr = false; }
+    if (sp + 2 > STACK_CAP) { *flags |= RF_OVERFLOW; return; }
+    if (hl && hr) {
+      if (la <= ra) { stk[sp++] = ri; stk[sp++] = li; }
+      else { stk[sp++] = li; stk[sp++] = ri; }
+    } else if (hl) {
+      stk[sp++] = li;
+    } else if (hr) {
+      stk[sp++] = ri;
+    }
+  }
+}
+
+// _kd_leaves: pop, slab-test clipped to [tmin, tmax], leaf -> interval, inner -> far, near.
+template <class Out>
+__device__ void kd_leaves(const Ray& r, const vs_index_desc& ix, int root, double tmin,
+                          double tmax, Out& out, int* flags) {
+  int stk[STACK_CAP];
+  int sp = 0;
+  if (root < 0) return;
+  stk[sp++] = root;
+  while (sp > 0) {
+    const int i = stk[--sp];
+    double a, b;
+    if (!node_slab(r, ix.lo, ix.hi, i, a, b)) continue;
+    a = a > tmin ? a : tmin;
+    b = b < tmax ? b : tmax;
+    if (b <= a) continue;
+    const int ax = __ldg(ix.axis + i);
+    if (ax < 0) { out.push(a, b); continue; }
+    const double pl = (double)__ldg(ix.plane + i);
+    bool front_left;
+    const bool zero = ax == 0 ? r.zx : (ax == 1 ? r.zy : r.zz);
+    if (zero)
+      front_left = (ax == 0 ? r.ox : (ax == 1 ? r.oy : r.oz)) < pl;
+    else
+      front_left = (ax == 0 ? r.ix : (ax == 1 ? r.iy : r.iz)) > 0.0;
+    const int lc = __ldg(ix.left + i), rc = __ldg(ix.right + i);
+    const int nr = front_left ? lc : rc, fr = front_left ? rc : lc;
+    if (sp + 2 > STACK_CAP) { *flags |= RF_OVERFLOW; return; }
+    if (fr >= 0) stk[sp++] = fr;
+    if (nr >= 0) stk[sp++] = nr;
+  }
+}
+
+// Hybrid: merged k-d leaf intervals -> DDA runs inside each -> merged runs.
+template <class Sink>
+struct LeafToGrid {
+  const Ray* r;
+  const vs_index_desc* ix;
+  Merger<Sink>* runs;
+  __device__ __forceinline__ void segment(double t0, double t1) { dda_runs(*r, *ix, t0, t1, *runs); }
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
+    k_render(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, const float* __restrict__ lut,
+             const double* __restrict__ corr, double dt, int nearest, vs_rows_desc rows,
+             uint8_t* __restrict__ rgba8, double* __restrict__ rgba64, int32_t* __restrict__ samples,
+             unsigned long long* __restrict__ total, int* __restrict__ flags_out) {
+  __shared__ RenderSmem sm;
+  __shared__ unsigned long long red[RENDER_TX * RENDER_TY / 32];
+  const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
+  for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
+    sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
+    sm.corr[k] = corr[k];
+    sm.u8f[k] = (float)((double)k / 255.0);
+  }
+  __syncthreads();
+  const int i = blockIdx.x * RENDER_TX + threadIdx.x;  // pixel column
+  const int l = blockIdx.y * RENDER_TY + threadIdx.y;  // local row
+  int64_t taken = 0;
+  int flags = 0;
+  if (i < cam.width && l < rows.nrows) {
+    // local row -> image row: stripes of rows.stripe rows dealt round-robin over rows.nparts
+    const int s = l / rows.stripe, w = l % rows.stripe;
+    const int j = (s * rows.nparts + rows.part) * rows.stripe + w;
+    const double xs = __dmul_rn(((double)i + 0.5) - (double)cam.width / 2.0, cam.scale);
+    const double ys = __dmul_rn(((double)cam.height / 2.0 - (double)j) - 0.5, cam.scale);
+    const double ox = __dadd_rn(__dadd_rn(cam.eye[0], __dmul_rn(ys, cam.up[0])), __dmul_rn(xs, cam.right[0]));
+    const double oy = __dadd_rn(__dadd_rn(cam.eye[1], __dmul_rn(ys, cam.up[1])), __dmul_rn(xs, cam.right[1]));
+    const double oz = __dadd_rn(__dadd_rn(cam.eye[2], __dmul_rn(ys, cam.up[2])), __dmul_rn(xs, cam.right[2]));
+    Ray r;
+    ray_setup(r, ox, oy, oz, cam);
+    Integrator I;
+    I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
+    I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
+    I.accr = I.accg = I.accb = I.acca = 0.0;
+    I.taken = 0;
+    double tmin, tmax;
+    if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+      I.entry = tmin;  // _k_integrate's own slab of the full volume gives the same entry
+      auto m = make_merger(&I, &flags);
+      if (KIND == VS_KIND_NAIVE) {
+        m.push(tmin, tmax);
+      } else if (KIND == VS_KIND_GRID) {
+        dda_runs(r, ix, tmin, tmax, m);
+      } else if (KIND == VS_KIND_LBVH) {
+        const int n = ix.lbvh_info ? __ldg(ix.lbvh_info) : ix.root + 1;
+        bvh_leaves(r, ix, n > 0 ? 0 : -1, tmin, tmax, m, &flags);
+      } else if (KIND == VS_KIND_KD) {
+        kd_leaves(r, ix, ix.root, tmin, tmax, m, &flags);
+      } else {
+        LeafToGrid<Integrator> g;
+        g.r = &r; g.ix = &ix; g.runs = &m;
+        auto leaves = make_merger(&g, &flags);
+        kd_leaves(r, ix, ix.root, tmin, tmax, leaves, &flags);
+        leaves.flush();
+      }
+      m.flush();
+    }
+    taken = I.taken;
+    const int64_t pix = (int64_t)l * cam.width + i;
+    const double acc[4] = {I.accr, I.accg, I.accb, I.acca};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double q = floor(__dadd_rn(__dmul_rn(acc[c], 255.0), 0.5));
+      rgba8[4 * pix + c] = (uint8_t)(q < 0.0 ? 0 : (q > 255.0 ? 255 : (int)q));
+      if (rgba64) rgba64[4 * pix + c] = acc[c];
+    }
+    if (samples) samples[pix] = (int32_t)taken;
+  }
+  if (flags) atomicOr(flags_out, flags);
+  if (total) {
+    unsigned long long t = (unsigned long long)taken;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((tid & 31) == 0) red[tid >> 5] = t;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long s = 0;
+      for (int k = 0; k < RENDER_TX * RENDER_TY / 32; ++k) s += red[k];
+      if (s) atomicAdd(total, s);
+    }
+  }
+}
+
+// Single-ray traversal (render.py:917-961): the merged interval list of one ray.
+struct ListSink {
+  double* out;
+  int cap, n;
+  __device__ void segment(double t0, double t1) {
+    if (n < cap) { out[2 * n] = t0; out[2 * n + 1] = t1; }
+    ++n;
+  }
+};
+
+__global__ void k_traverse_rays(vs_index_desc ix, int nx, int ny, int nz,
+                                const double* __restrict__ origins, const double* __restrict__ dir,
+                                int nrays, double* __restrict__ out, int cap,
+                                int* __restrict__ counts, int* __restrict__ flags_out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nrays) return;
+  vs_camera_desc c;
+  c.dir[0] = dir[0]; c.dir[1] = dir[1]; c.dir[2] = dir[2];
+  Ray r;
+  ray_setup(r, origins[3 * q], origins[3 * q + 1], origins[3 * q + 2], c);
+  ListSink L{out + (int64_t)q * cap * 2, cap, 0};
+  int flags = 0;
+  double tmin, tmax;
+  if (slab(r, 0.0, 0.0, 0.0, (double)nx, (double)ny, (double)nz, tmin, tmax)) {
+    auto m = make_merger(&L, &flags);
+    switch (ix.kind) {
+      case VS_KIND_NAIVE: m.push(tmin, tmax); break;
+      case VS_KIND_GRID: dda_runs(r, ix, tmin, tmax, m); break;
+      case VS_KIND_LBVH: {
+        const int n = ix.lbvh_info ? ix.lbvh_info[0] : ix.root + 1;
+        bvh_leaves(r, ix, n > 0 ? 0 : -1, tmin, tmax, m, &flags);
+        break;
+      }
+      case VS_KIND_KD: kd_leaves(r, ix, ix.root, tmin, tmax, m, &flags); break;
+      default: {
+        LeafToGrid<ListSink> g;
+        g.r = &r; g.ix = &ix; g.runs = &m;
+        auto leaves = make_merger(&g, &flags);
+        kd_leaves(r, ix, ix.root, tmin, tmax, leaves, &flags);
+        leaves.flush();
+      }
+    }
+    m.flush();
+  }
+  counts[q] = L.n;
+  if (flags) atomicOr(flags_out, flags);
+}
+
+// Single-ray integration over given segments (render.py:964-1015).
+__global__ void k_integrate_rays(vs_volume_desc vol, const double* __restrict__ origins,
+                                 const double* __restrict__ dir, const double* __restrict__ segs,
+                                 const int* __restrict__ counts, int cap, int nrays,
+                                 const float* __restrict__ lut, const double* __restrict__ corr,
+                                 double dt, int nearest, double* __restrict__ rgba,
+                                 long long* __restrict__ samples) {
+  __shared__ RenderSmem sm;
+  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
+    sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
+    sm.corr[k] = corr[k];
+    sm.u8f[k] = (float)((double)k / 255.0);
+  }
+  __syncthreads();
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nrays) return;
+  vs_camera_desc c;
+  c.dir[0] = dir[0]; c.dir[1] = dir[1]; c.dir[2] = dir[2];
+  Ray r;
+  ray_setup(r, origins[3 * q], origins[3 * q + 1], origins[3 * q + 2], c);
+  Integrator I;
+  I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
+  I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
+  I.accr = I.accg = I.accb = I.acca = 0.0;
+  I.taken = 0;
+  const int m = counts[q];
+  double entry, ex;
+  if (m > 0 && slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, entry, ex)) {
+    I.entry = entry;
+    for (int s = 0; s < m && s < cap; ++s)
+      I.segment(segs[((int64_t)q * cap + s) * 2], segs[((int64_t)q * cap + s) * 2 + 1]);
+  }
+  rgba[4 * q] = I.accr;
+  rgba[4 * q + 1] = I.accg;
+  rgba[4 * q + 2] = I.accb;
+  rgba[4 * q + 3] = I.acca;
+  samples[q] = I.taken;
+}
+
+template <int K>
+static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
+                          const vs_index_desc& ix, const vs_camera_desc& c, const float* lut,
+                          const double* corr, double dt, int nearest, const vs_rows_desc& rows,
+                          uint8_t* rgba8, double* rgba64, int32_t* samples,
+                          unsigned long long* total, int* flags) {
+  k_render<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
+                                                          rgba8, rgba64, samples, total, flags);
+}
+
+}  // namespace vs
+
+using namespace vs;
+
+extern "C" {
+
+int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camera_desc* cam,
+              const float* lut, const double* corr, double dt, int nearest,
+              const vs_rows_desc* rows_opt, uint8_t* rgba8, double* rgba64_opt,
+              int32_t* samples_opt, unsigned long long* total_opt, int* flags,
+              vs_stream_t stream) {
+  if (!vol || !ix || !cam || !lut || !corr || !rgba8 || !flags || !(dt > 0.0))
+    return fail_arg("vs_render");
+  if (!vol->bins || vol->nx < 1 || vol->ny < 1 || vol->nz < 1) return fail_arg("vs_render: volume");
+  if (cam->width < 1 || cam->height < 1) return fail_arg("vs_render: viewport");
+  vs_rows_desc rows;
+  if (rows_opt) {
+    rows = *rows_opt;
+  } else {
+    rows.nrows = cam->height; rows.stripe = cam->height > 0 ? cam->height : 1;
+    rows.nparts = 1; rows.part = 0;
+  }
+  if (rows.stripe < 1 || rows.nparts < 1 || rows.part < 0 || rows.part >= rows.nparts)
+    return fail_arg("vs_render: rows");
+  if (rows.nrows <= 0) return 0;
+  const int kind = ix->kind;
+  if ((kind == VS_KIND_GRID || kind == VS_KIND_HYBRID) && (!ix->occ || ix->cs < 1))
+    return fail_arg("vs_render: grid");
+  if ((kind == VS_KIND_LBVH || kind == VS_KIND_KD || kind == VS_KIND_HYBRID) &&
+      (!ix->lo || !ix->hi || !ix->left || !ix->right))
+    return fail_arg("vs_render: tree");
+  if ((kind == VS_KIND_KD || kind == VS_KIND_HYBRID) && (!ix->axis || !ix->plane))
+    return fail_arg("vs_render: kd");
+  dim3 grid((unsigned)cdiv(cam->width, RENDER_TX), (unsigned)cdiv(rows.nrows, RENDER_TY));
+  cudaStream_t st = S(stream);
+  switch (kind) {
+    case VS_KIND_NAIVE:
+      launch_render<VS_KIND_NAIVE>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
+                                   rgba64_opt, samples_opt, total_opt, flags);
+      break;
+    case VS_KIND_GRID:
+      launch_render<VS_KIND_GRID>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
+                                  rgba64_opt, samples_opt, total_opt, flags);
+      break;
+    case VS_KIND_LBVH:
+      launch_render<VS_KIND_LBVH>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
+                                  rgba64_opt, samples_opt, total_opt, flags);
+      break;
+    case VS_KIND_KD:
+      launch_render<VS_KIND_KD>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
+                                rgba64_opt, samples_opt, total_opt, flags);
+      break;
+    case VS_KIND_HYBRID:
+      launch_render<VS_KIND_HYBRID>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
+                                    rgba64_opt, samples_opt, total_opt, flags);
+      break;
+    default:
+      return fail_arg("vs_render: kind");
+  }
+  return check_launch("k_render");
+}
+
+int vs_traverse_rays(const vs_index_desc* ix, int nx, int ny, int nz, const double* origins,
+                     const double* dir, int nrays, double* out, int cap, int* counts, int* flags,
+                     vs_stream_t stream) {
+  if (!ix || !origins || !dir || !out || !counts || !flags || nrays < 0 || cap < 1)
+    return fail_arg("vs_traverse_rays");
+  if (nrays == 0) return 0;
+  k_traverse_rays<<<(unsigned)cdiv(nrays, 64), 64, 0, S(stream)>>>(*ix, nx, ny, nz, origins, dir,
+                                                                    nrays, out, cap, counts, flags);
+  return check_launch("k_traverse_rays");
+}
+
+int vs_integrate_rays(const vs_volume_desc* vol, const double* origins, const double* dir,
+                      const double* segs, const int* counts, int cap, int nrays, const float* lut,
+                      const double* corr, double dt, int nearest, double* rgba,
+                      long long* samples, vs_stream_t stream) {
+  if (!vol || !origins || !dir || !segs || !counts || !lut || !corr || !rgba || !samples ||
+      nrays < 0 || cap < 1 || !(dt > 0.0))
+    return fail_arg("vs_integrate_rays");
+  if (nrays == 0) return 0;
+  k_integrate_rays<<<(unsigned)cdiv(nrays, 64), 64, 0, S(stream)>>>(
+      *vol, origins, dir, segs, counts, cap, nrays, lut, corr, dt, nearest, rgba, samples);
+  return check_launch("k_integrate_rays");
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+"""k-d trees over occupancy classifications on the B200, drop-in for voxelskip.kdtree
+(/root/reference/pkg/src/voxelskip/kdtree.py).
+
+KdTree keeps the reference's flat row layout (DFS preorder, row 0 = root): lo/hi (m,3) int32,
+axis (m,) int8 (-1 = leaf), plane/left/right (m,) int32 (-1 = dropped child).  Device copies
+feed the renderer; host arrays are materialised lazily.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .volume import Aabb
+
+DEFAULT_CELL_SIZE = 8
+DEFAULT_BINS = 4
+
+
+@dataclass(frozen=True)
+class BuildParams:
+    """Knobs for build_kdtree (kdtree.py:43-73)."""
+
+    mode: str = "shallow"
+    max_leaf_size: int | None = None
+    builder: str = "sweep"
+    bins: int = DEFAULT_BINS
+    cell_size: int = DEFAULT_CELL_SIZE
+
+    def __post_init__(self):
+        if self.mode not in ("shallow", "deep"):
+            raise ValueError(f"unknown mode: {self.mode!r}")
+        if self.builder not in ("sweep", "binned"):
+            raise ValueError(f"unknown builder: {self.builder!r}")
+        if self.max_leaf_size is not None:
+            if self.mode != "deep":
+                raise ValueError("max_leaf_size only applies to deep trees")
+            if self.max_leaf_size < 1:
+                raise ValueError("max_leaf_size must be positive")
+        if self.bins < 2:
+            raise ValueError("bins must be >= 2")
+        if self.cell_size < 1:
+            raise ValueError("cell_size must be positive")
+
+
+@dataclass(frozen=True)
+class SplitPlane:
+    """An axis-aligned cut: voxels with coordinate < position go left (kdtree.py:76-82)."""
+
+    axis: int
+    position: int
+    cost: int
+
+
+class KdTree:
+    """Flat node arrays, row 0 the root unless empty (kdtree.py:85-127)."""
+
+    _FIELDS = ("lo", "hi", "axis", "plane", "left", "right")
+
+    def __init__(self, lo=None, hi=None, axis=None, plane=None, left=None, right=None,
+                 root: int = -1, dims=(0, 0, 0), *, dev: dict | None = None,
+                 height: int | None = None):
+        self.root = int(root)
+        self.dims = tuple(int(d) for d in dims)
+        self._host = {}
+        if dev is None:
+            self._host = {
+                "lo": np.asarray(lo, np.int32).reshape(-1, 3),
+                "hi": np.asarray(hi, np.int32).reshape(-1, 3),
+                "axis": np.asarray(axis, np.int8).reshape(-1),
+                "plane": np.asarray(plane, np.int32).reshape(-1),
+                "left": np.asarray(left, np.int32).reshape(-1),
+                "right": np.asarray(right, np.int32).reshape(-1),
+            }
+            self._m = len(self._host["axis"])
+        else:
+            self._m = int(dev["axis"].shape[0])
+        self._dev = dev
+        self._height = height
+
+    def __getattr__(self, name):
+        if name in KdTree._FIELDS:
+            h = self.__dict__["_host"]
+            if name not in h:
+                h[name] = self.__dict__["_dev"][name].cpu().numpy()
+            return h[name]
+        raise AttributeError(name)
+
+    def device_arrays(self) -> dict:
+        if self._dev is None:
+            dev = _lib.device()
+            self._dev = {k: torch.from_numpy(np.ascontiguousarray(self._host[k])).to(dev)
+                         for k in KdTree._FIELDS}
+        return self._dev
+
+    @property
+    def node_count(self) -> int:
+        return self._m
+
+    def is_leaf(self, i: int) -> bool:
+        return bool(self.axis[i] < 0)
+
+    def node_box(self, i: int) -> Aabb:
+        return Aabb(tuple(int(v) for v in self.lo[i]), tuple(int(v) for v in self.hi[i]))
+
+    def leaf_mask(self) -> np.ndarray:
+        return self.axis < 0
+
+    def height(self) -> int:
+        """Nodes on the longest root-to-leaf path (kdtree.py:115-127)."""
+        if self._height is None:
+            if self.node_count == 0:
+                self._height = 0
+            else:
+                left, right = self.left, self.right
+                best, stack = 0, [(self.root, 1)]
+                while stack:
+                    i, d = stack.pop()
+                    best = max(best, d)
+                    for c in (int(left[i]), int(right[i])):
+                        if c >= 0:
+                            stack.append((c, d + 1))
+                self._height = best
+        return self._height
+
+
+def empty_kdtree(dims) -> KdTree:
+    z3 = np.zeros((0, 3), np.int32)
+    z = np.zeros(0, np.int32)
+    return KdTree(z3, z3, np.zeros(0, np.int8), z, z, z, -1, dims)
+
+
+def build_index_kind(kind: str, b):
+    raise NotImplementedError(f"{kind}: SVT k-d builders are not built yet")

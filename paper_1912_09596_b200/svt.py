@@ -34,7 +34,7 @@ class MacroGrid:
         return self._host
 
     def storage_bytes(self) -> int:
-        return int(np.prod(self.cells_dims))
+        return (int(np.prod(self.cells_dims)) + 7) // 8  # packbits size, as svt.py:36-37
 
 
 def derive_macro_grid(source, cell_size: int) -> MacroGrid:
