@@ -210,6 +210,29 @@ int vs_integrate_rays(const vs_volume_desc* vol, const double* origins, const do
                       const float* lut, const double* corr, double dt, int nearest,
                       double* rgba, long long* samples, vs_stream_t stream);
 
+/* ---- summed-volume tables (svt.py:40-131) ------------------------------------------------ */
+/* build_svt_grid: tables (nbx,nby,nbz,bs+1,bs+1,bs+1) uint32, bs in [2, 32]. */
+int vs_svt_build(const uint32_t* bits, int nx, int ny, int nz, int bs, uint32_t* tables,
+                 vs_stream_t stream);
+/* box_count for nbox boxes (lo3, hi3 int32 each, clipped to dims) -> counts (int64). */
+int vs_box_count(const uint32_t* tables, int nx, int ny, int nz, int bs, const int32_t* boxes,
+                 int nbox, long long* counts, vs_stream_t stream);
+/* shrink_to_occupied of one box: out = lo3, hi3 of the set flags inside (hi[0] < 0 = None). */
+int vs_tight_box(const uint32_t* bits, int nx, int ny, int nz, const int32_t* box, int* out,
+                 vs_stream_t stream);
+
+/* ---- k-d trees: build_kdtree (kdtree.py:387-498) -------------------------------------------
+ * Level-synchronous on the device, rows renumbered to the reference's DFS preorder.
+ * deep: 0 shallow / 1 deep; mls: max_leaf_size or -1; binned: 0 sweep / 1 binned (bins, cs).
+ * Synchronous (one host sync per tree level); scratch is stream-ordered device memory.
+ * The result handle is read with vs_kd_result_info / _copy and released with _free. */
+int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, int binned,
+                int bins, int cs, void** handle, vs_stream_t stream);
+int vs_kd_result_info(void* handle, int64_t* m, int* root, int* height);
+int vs_kd_result_copy(void* handle, int32_t* lo, int32_t* hi, int8_t* axis, int32_t* plane,
+                      int32_t* left, int32_t* right, vs_stream_t stream);
+void vs_kd_result_free(void* handle);
+
 #ifdef __cplusplus
 }
 #endif

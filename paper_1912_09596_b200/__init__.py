@@ -6,14 +6,15 @@ hand-written CUDA kernels in libvsb200.so (include/vsb200.h).  There is no CPU f
 """
 
 from .bench import INDEX_KINDS, build_index, index_kind, report_stats
-from .hybrid import HybridGrid
-from .kdtree import BuildParams, KdTree, SplitPlane, empty_kdtree
+from .hybrid import HybridGrid, build_hybrid
+from .kdtree import BuildParams, KdTree, SplitPlane, build_kdtree, empty_kdtree
 from .lbvh import (BrickSet, Lbvh, MortonRangeError, build_lbvh, empty_lbvh, flag_bricks,
                    leaf_boxes, morton_decode, morton_encode)
 from .render import (DEFAULT_DT, Camera, Frame, Ray, RaySegmentList, integrate, render_float,
                      render_frame, sample_count_of, traverse_grid, traverse_hybrid, traverse_kd,
                      traverse_lbvh, traverse_naive)
-from .svt import MacroGrid, derive_macro_grid
+from .svt import (MacroGrid, SvtGrid, box_count, build_svt_grid, derive_macro_grid,
+                  shrink_to_occupied)
 from .volume import (Aabb, BinaryVolume, TransferFunction, UnsupportedFormatError, Volume,
                      VolumeFormatError, classify, occupancy, quantize_scalar)
 

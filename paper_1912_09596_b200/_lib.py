@@ -39,6 +39,13 @@ SIGNATURES: dict[str, tuple] = {
     "vs_lbvh_from_bitmap": (i32, [P, P, i32, i32, i32, i32, i32, i64, P, P, P, P, P, P, P, P,
                                   SZ, P]),
     "vs_lbvh_bricks_workspace": (SZ, [i64]),
+    "vs_svt_build": (i32, [P, i32, i32, i32, i32, P, P]),
+    "vs_box_count": (i32, [P, i32, i32, i32, i32, P, i32, P, P]),
+    "vs_tight_box": (i32, [P, i32, i32, i32, P, P, P]),
+    "vs_kd_build": (i32, [P, i32, i32, i32, i32, i32, i32, i32, i32, P, P]),
+    "vs_kd_result_info": (i32, [P, P, P, P]),
+    "vs_kd_result_copy": (i32, [P, P, P, P, P, P, P, P]),
+    "vs_kd_result_free": (None, [P]),
     "vs_render": (i32, [P, P, P, P, P, C.c_double, i32, P, P, P, P, P, P, P]),
     "vs_traverse_rays": (i32, [P, i32, i32, i32, P, P, i32, P, i32, P, P, P]),
     "vs_integrate_rays": (i32, [P, P, P, P, P, i32, i32, P, P, C.c_double, i32, P, P, P]),

@@ -1,0 +1,1137 @@
+// Level-synchronous k-d tree construction over the packed bit volume: build_kdtree
+// (/root/reference/pkg/src/voxelskip/kdtree.py:387-498) with both plane searches.
+//
+// The reference recursion is depth-first; its decisions for a node depend only on the node's
+// box (and the root volume), so every node of one tree level is decided in parallel here and
+// the rows are renumbered to the reference's DFS preorder at the end (emit-before-recurse,
+// left subtree first; kdtree.py:412-419, 479-484).
+//
+// Per level:
+//   sweep builder (kdtree.py:148-230): for every node that may split, per-slab spans along
+//     each axis (k_spans_x / k_spans_y own an x- or y-slab per warp and also OR the region's
+//     (x,z) / (y,z) projections; k_spans_z derives the z-slab spans from those projections),
+//     then one warp per node runs _axis_sweep's prefix/suffix min/max scans, the cost argmin
+//     (first minimum; strict < across axes), the acceptance test cost < box volume, the
+//     halting rule and the forced middle split; children are exact tight boxes.
+//   binned builder (kdtree.py:268-381): per-cell tight boxes once (precompute_cell_boxes),
+//     per level the same slab decomposition over cells with box unions (the coordinate
+//     filter that _cells_reduce's Morton range accelerates), _snapped_positions in IEEE
+//     double, first strict minimum; binned leaves get the exact shrink from k_spans_x.
+//   compaction of children into the next level (left then right), parent links.
+// Finalisation: subtree sizes bottom-up, preorder numbers top-down, scatter rows.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cfloat>
+#include <vector>
+
+#include "common.cuh"
+
+namespace vs {
+
+constexpr int KD_FAR = 0x3fffffff;  // "no coordinate" sentinel for minima (kdtree.py:40 _FAR)
+
+struct Box {
+  int lo[3], hi[3];
+};
+
+__host__ __device__ inline int64_t box_vol(const Box& b) {
+  return (int64_t)(b.hi[0] - b.lo[0]) * (b.hi[1] - b.lo[1]) * (b.hi[2] - b.lo[2]);
+}
+
+// Slab span: coordinates local to the node box, min = KD_FAR / max = -1 when empty.
+struct Span {
+  int mn1, mx1, mn2, mx2;
+};
+
+struct KdLevel {
+  int n;                 // nodes on this level
+  Box* box;              // node boxes
+  int* need;             // bit0 spans needed (sweep search / forced / binned leaf shrink)
+  int64_t* off_x;        // n+1 exclusive prefix of x extents (of nodes needing spans)
+  int64_t* off_y;
+  int64_t* off_z;
+  int64_t* off_pxz;      // n+1 prefix of ex * wz words
+  int64_t* off_pyz;      // n+1 prefix of ey * wz words
+  int64_t* off_zw;       // n+1 prefix of wz
+};
+
+__device__ __forceinline__ int wz_of(const Box& b) { return (b.hi[2] - b.lo[2] + 31) >> 5; }
+
+// Local z word w of row `row` for a node spanning global z [z0, z1): bits z0+32w .. (masked).
+__device__ __forceinline__ uint32_t local_word(const uint32_t* __restrict__ row, int z0, int z1,
+                                               int w) {
+  const int gz = z0 + 32 * w;
+  const int gw = gz >> 5, sh = gz & 31;
+  uint32_t v = __ldg(row + gw) >> sh;
+  if (sh && gz + 32 - sh < z1) v |= __ldg(row + gw + 1) << (32 - sh);
+  const int rem = z1 - gz;
+  if (rem < 32) v &= (1u << rem) - 1u;
+  return v;
+}
+
+__device__ __forceinline__ int find_node(const int64_t* __restrict__ off, int n, int64_t item) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---- spans along x (and the (x,z) projection): warp per (node, x-slab) --------------------
+__global__ void k_spans_x(const uint32_t* __restrict__ bits, int ny, int nzw, KdLevel L,
+                          const int64_t* __restrict__ total, Span* __restrict__ span_x,
+                          uint32_t* __restrict__ pxz) {
+  __shared__ uint32_t acc[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t items = *total;
+  for (int64_t it = (int64_t)blockIdx.x * 8 + wib; it < items; it += (int64_t)gridDim.x * 8) {
+    const int i = find_node(L.off_x, L.n, it);
+    const Box b = L.box[i];
+    const int s = (int)(it - L.off_x[i]);
+    const int x = b.lo[0] + s;
+    const int wz = wz_of(b);
+    for (int w = lane; w < wz; w += 32) acc[wib][w] = 0;
+    __syncwarp();
+    int mny = KD_FAR, mxy = -1, mnz = KD_FAR, mxz = -1;
+    for (int y = b.lo[1] + lane; y < b.hi[1]; y += 32) {
+      const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
+      int zf = KD_FAR, zl = -1;
+      for (int w = 0; w < wz; ++w) {
+        const uint32_t v = local_word(row, b.lo[2], b.hi[2], w);
+        if (v) {
+          if (zf == KD_FAR) zf = 32 * w + __ffs(v) - 1;
+          zl = 32 * w + 31 - __clz(v);
+          atomicOr(&acc[wib][w], v);
+        }
+      }
+      if (zl >= 0) {
+        const int ly = y - b.lo[1];
+        mny = min(mny, ly);
+        mxy = max(mxy, ly);
+        mnz = min(mnz, zf);
+        mxz = max(mxz, zl);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      mny = min(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+      mxy = max(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+      mnz = min(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
+      mxz = max(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
+    }
+    __syncwarp();
+    if (lane == 0) span_x[it] = Span{mny, mxy, mnz, mxz};
+    uint32_t* dst = pxz + L.off_pxz[i] + (int64_t)s * wz;
+    for (int w = lane; w < wz; w += 32) dst[w] = acc[wib][w];
+    __syncwarp();
+  }
+}
+
+// ---- spans along y (and the (y,z) projection): warp per (node, y-slab) --------------------
+__global__ void k_spans_y(const uint32_t* __restrict__ bits, int ny, int nzw, KdLevel L,
+                          const int64_t* __restrict__ total, Span* __restrict__ span_y,
+                          uint32_t* __restrict__ pyz) {
+  __shared__ uint32_t acc[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t items = *total;
+  for (int64_t it = (int64_t)blockIdx.x * 8 + wib; it < items; it += (int64_t)gridDim.x * 8) {
+    const int i = find_node(L.off_y, L.n, it);
+    const Box b = L.box[i];
+    const int s = (int)(it - L.off_y[i]);
+    const int y = b.lo[1] + s;
+    const int wz = wz_of(b);
+    for (int w = lane; w < wz; w += 32) acc[wib][w] = 0;
+    __syncwarp();
+    int mnx = KD_FAR, mxx = -1, mnz = KD_FAR, mxz = -1;
+    for (int x = b.lo[0] + lane; x < b.hi[0]; x += 32) {
+      const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
+      int zf = KD_FAR, zl = -1;
+      for (int w = 0; w < wz; ++w) {
+        const uint32_t v = local_word(row, b.lo[2], b.hi[2], w);
+        if (v) {
+          if (zf == KD_FAR) zf = 32 * w + __ffs(v) - 1;
+          zl = 32 * w + 31 - __clz(v);
+          atomicOr(&acc[wib][w], v);
+        }
+      }
+      if (zl >= 0) {
+        const int lx = x - b.lo[0];
+        mnx = min(mnx, lx);
+        mxx = max(mxx, lx);
+        mnz = min(mnz, zf);
+        mxz = max(mxz, zl);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      mnx = min(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+      mxx = max(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+      mnz = min(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
+      mxz = max(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
+    }
+    __syncwarp();
+    if (lane == 0) span_y[it] = Span{mnx, mxx, mnz, mxz};
+    uint32_t* dst = pyz + L.off_pyz[i] + (int64_t)s * wz;
+    for (int w = lane; w < wz; w += 32) dst[w] = acc[wib][w];
+    __syncwarp();
+  }
+}
+
+// ---- spans along z from the projections: thread per (node, local z word) ------------------
+__global__ void k_spans_z(KdLevel L, const int64_t* __restrict__ total,
+                          const uint32_t* __restrict__ pxz, const uint32_t* __restrict__ pyz,
+                          Span* __restrict__ span_z) {
+  const int64_t items = *total;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int i = find_node(L.off_zw, L.n, it);
+    const Box b = L.box[i];
+    const int w = (int)(it - L.off_zw[i]);
+    const int wz = wz_of(b);
+    const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
+    const int nzb = min(32, ez - 32 * w);
+    int mnx[32], mxx[32];
+    // first / last x per z bit
+    uint32_t seen = 0;
+    const uint32_t* px = pxz + L.off_pxz[i] + w;
+    for (int x = 0; x < ex && seen != 0xffffffffu; ++x) {
+      uint32_t nw = px[(int64_t)x * wz] & ~seen;
+      seen |= nw;
+      while (nw) { int k = __ffs(nw) - 1; nw &= nw - 1; mnx[k] = x; }
+    }
+    const uint32_t any = seen;
+    seen = 0;
+    for (int x = ex - 1; x >= 0 && seen != any; --x) {
+      uint32_t nw = px[(int64_t)x * wz] & ~seen;
+      seen |= nw;
+      while (nw) { int k = __ffs(nw) - 1; nw &= nw - 1; mxx[k] = x; }
+    }
+    Span* out = span_z + L.off_z[i] + 32 * w;
+    for (int k = 0; k < nzb; ++k) {
+      const bool ok = (any >> k) & 1u;
+      out[k].mn1 = ok ? mnx[k] : KD_FAR;
+      out[k].mx1 = ok ? mxx[k] : -1;
+    }
+    const uint32_t* py = pyz + L.off_pyz[i] + w;
+    seen = 0;
+    for (int y = 0; y < ey && seen != any; ++y) {
+      uint32_t nw = py[(int64_t)y * wz] & ~seen;
+      seen |= nw;
+      while (nw) { int k = __ffs(nw) - 1; nw &= nw - 1; mnx[k] = y; }
+    }
+    seen = 0;
+    for (int y = ey - 1; y >= 0 && seen != any; --y) {
+      uint32_t nw = py[(int64_t)y * wz] & ~seen;
+      seen |= nw;
+      while (nw) { int k = __ffs(nw) - 1; nw &= nw - 1; mxx[k] = y; }
+    }
+    for (int k = 0; k < nzb; ++k) {
+      const bool ok = (any >> k) & 1u;
+      out[k].mn2 = ok ? mnx[k] : KD_FAR;
+      out[k].mx2 = ok ? mxx[k] : -1;
+    }
+  }
+}
+
+// ---- per-node decision ------------------------------------------------------------------
+struct KdParams {
+  int deep;          // 0 shallow, 1 deep
+  int mls;           // max_leaf_size, -1 none
+  int binned;
+  int bins, cs;
+  int64_t root_vol;
+};
+
+struct KdDecision {
+  int axis;          // -1 leaf
+  int plane;
+  int nchild;        // bit0 left present, bit1 right present
+  int dropped;       // binned leaf whose shrink is empty (no row)
+  Box left, right;   // global boxes
+  Box leaf;          // leaf row box (binned: shrunk)
+};
+
+__device__ __forceinline__ bool halted(const KdParams& P, int64_t vol) {
+  return P.deep ? vol <= 512 : vol * 10 <= P.root_vol;  // kdtree.py:421-424
+}
+
+// Warp scan helpers (inclusive min / max).
+__device__ __forceinline__ int wmin_incl(int v, int lane) {
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = min(v, u);
+  }
+  return v;
+}
+__device__ __forceinline__ int wmax_incl(int v, int lane) {
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = max(v, u);
+  }
+  return v;
+}
+
+// Row-order tight box (axis row, other1, other2) in local coordinates; empty if hi0 < 0.
+struct RBox {
+  int lo0, lo1, lo2, hi0, hi1, hi2;
+};
+
+__device__ __forceinline__ int64_t rvol(const RBox& r) {
+  if (r.hi0 < 0) return 0;
+  return (int64_t)(r.hi0 - r.lo0 + 1) * (r.hi1 - r.lo1 + 1) * (r.hi2 - r.lo2 + 1);
+}
+
+// Sweep one axis: (first-minimum cut k in 1..e-1, its cost).  suf scratch holds e RBoxes.
+__device__ void sweep_axis(const Span* __restrict__ sp, int e, RBox* __restrict__ suf,
+                           int lane, int& best_k, int64_t& best_cost) {
+  // suffix pass (from the end): suf[s] = tight box of slabs [s, e)
+  RBox carry{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
+  for (int base = ((e - 1) / 32) * 32; base >= 0; base -= 32) {
+    const int s = base + (31 - lane);  // lane 0 handles the highest slab of the chunk
+    RBox r{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
+    if (s < e) {
+      const Span v = sp[s];
+      if (v.mx1 >= 0) r = RBox{s, v.mn1, v.mn2, s, v.mx1, v.mx2};
+    }
+    r.lo0 = min(wmin_incl(r.lo0, lane), carry.lo0);
+    r.lo1 = min(wmin_incl(r.lo1, lane), carry.lo1);
+    r.lo2 = min(wmin_incl(r.lo2, lane), carry.lo2);
+    r.hi0 = max(wmax_incl(r.hi0, lane), carry.hi0);
+    r.hi1 = max(wmax_incl(r.hi1, lane), carry.hi1);
+    r.hi2 = max(wmax_incl(r.hi2, lane), carry.hi2);
+    if (s < e) suf[s] = r;
+    carry.lo0 = __shfl_sync(0xffffffffu, r.lo0, 31);
+    carry.lo1 = __shfl_sync(0xffffffffu, r.lo1, 31);
+    carry.lo2 = __shfl_sync(0xffffffffu, r.lo2, 31);
+    carry.hi0 = __shfl_sync(0xffffffffu, r.hi0, 31);
+    carry.hi1 = __shfl_sync(0xffffffffu, r.hi1, 31);
+    carry.hi2 = __shfl_sync(0xffffffffu, r.hi2, 31);
+  }
+  __syncwarp();
+  // prefix pass with costs: cost(k) = vol(pre[k-1]) + vol(suf[k]), k = 1..e-1
+  RBox pc{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
+  int64_t bc = INT64_MAX;
+  int bk = 0;
+  for (int base = 0; base < e; base += 32) {
+    const int s = base + lane;
+    RBox r{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
+    if (s < e) {
+      const Span v = sp[s];
+      if (v.mx1 >= 0) r = RBox{s, v.mn1, v.mn2, s, v.mx1, v.mx2};
+    }
+    r.lo0 = min(wmin_incl(r.lo0, lane), pc.lo0);
+    r.lo1 = min(wmin_incl(r.lo1, lane), pc.lo1);
+    r.lo2 = min(wmin_incl(r.lo2, lane), pc.lo2);
+    r.hi0 = max(wmax_incl(r.hi0, lane), pc.hi0);
+    r.hi1 = max(wmax_incl(r.hi1, lane), pc.hi1);
+    r.hi2 = max(wmax_incl(r.hi2, lane), pc.hi2);
+    // candidate k = s + 1 uses pre[s] and suf[s + 1]
+    int64_t c = INT64_MAX;
+    if (s + 1 < e) c = rvol(r) + rvol(suf[s + 1]);
+    // first minimum across the chunk
+    int64_t cm = c;
+    int km = s + 1;
+    for (int o = 16; o; o >>= 1) {
+      int64_t c2 = __shfl_xor_sync(0xffffffffu, cm, o);
+      int k2 = __shfl_xor_sync(0xffffffffu, km, o);
+      if (c2 < cm || (c2 == cm && k2 < km)) { cm = c2; km = k2; }
+    }
+    if (cm < bc) { bc = cm; bk = km; }
+    pc.lo0 = __shfl_sync(0xffffffffu, r.lo0, 31);
+    pc.lo1 = __shfl_sync(0xffffffffu, r.lo1, 31);
+    pc.lo2 = __shfl_sync(0xffffffffu, r.lo2, 31);
+    pc.hi0 = __shfl_sync(0xffffffffu, r.hi0, 31);
+    pc.hi1 = __shfl_sync(0xffffffffu, r.hi1, 31);
+    pc.hi2 = __shfl_sync(0xffffffffu, r.hi2, 31);
+  }
+  best_k = bk;
+  best_cost = bc;
+}
+
+// Tight row-order box of slabs [s0, s1) (warp reduction).
+__device__ RBox range_box(const Span* __restrict__ sp, int s0, int s1, int lane) {
+  RBox r{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
+  for (int s = s0 + lane; s < s1; s += 32) {
+    const Span v = sp[s];
+    if (v.mx1 >= 0) {
+      r.lo0 = min(r.lo0, s); r.hi0 = max(r.hi0, s);
+      r.lo1 = min(r.lo1, v.mn1); r.hi1 = max(r.hi1, v.mx1);
+      r.lo2 = min(r.lo2, v.mn2); r.hi2 = max(r.hi2, v.mx2);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    r.lo0 = min(r.lo0, __shfl_xor_sync(0xffffffffu, r.lo0, o));
+    r.lo1 = min(r.lo1, __shfl_xor_sync(0xffffffffu, r.lo1, o));
+    r.lo2 = min(r.lo2, __shfl_xor_sync(0xffffffffu, r.lo2, o));
+    r.hi0 = max(r.hi0, __shfl_xor_sync(0xffffffffu, r.hi0, o));
+    r.hi1 = max(r.hi1, __shfl_xor_sync(0xffffffffu, r.hi1, o));
+    r.hi2 = max(r.hi2, __shfl_xor_sync(0xffffffffu, r.hi2, o));
+  }
+  return r;
+}
+
+// Row order -> xyz (kdtree.py:38 _ROWS_TO_XYZ): axis a rows are (a, o1, o2).
+__device__ __forceinline__ void others(int a, int& o1, int& o2) {
+  o1 = a == 0 ? 1 : 0;
+  o2 = a == 2 ? 1 : 2;
+}
+
+__device__ __forceinline__ Box to_global(const Box& node, int a, const RBox& r) {
+  int o1, o2;
+  others(a, o1, o2);
+  Box g;
+  g.lo[a] = node.lo[a] + r.lo0; g.hi[a] = node.lo[a] + r.hi0 + 1;
+  g.lo[o1] = node.lo[o1] + r.lo1; g.hi[o1] = node.lo[o1] + r.hi1 + 1;
+  g.lo[o2] = node.lo[o2] + r.lo2; g.hi[o2] = node.lo[o2] + r.hi2 + 1;
+  return g;
+}
+
+// ---- binned search helpers ---------------------------------------------------------------
+// Per cell-slab union of occupied cells' tight boxes (global voxel coords), lo = KD_FAR empty.
+struct CBox {
+  int lo[3], hi[3];
+};
+
+// _snapped_positions (kdtree.py:346-350) in IEEE double, no FMA.
+__device__ int snapped_positions(int lo, int hi, int bins, int cs, int* out) {
+  const double extent = (double)(hi - lo);
+  const double step = __ddiv_rn(extent, (double)bins);
+  int n = 0;
+  for (int j = 1; j < bins; ++j) {
+    const double raw = __dadd_rn((double)lo, __dmul_rn((double)j, step));
+    const int64_t p = (int64_t)floor(__dadd_rn(__ddiv_rn(raw, (double)cs), 0.5)) * cs;
+    if (lo < p && p < hi) {
+      bool dup = false;
+      for (int q = 0; q < n; ++q) dup |= out[q] == (int)p;
+      if (!dup) out[n++] = (int)p;
+    }
+  }
+  for (int a = 1; a < n; ++a)  // sort ascending
+    for (int b = a; b > 0 && out[b - 1] > out[b]; --b) { int t = out[b]; out[b] = out[b - 1]; out[b - 1] = t; }
+  return n;
+}
+
+// _cells_reduce of a region through the node's cell-slab unions along axis a: cells with
+// coordinate c in [c0, c1] along a (other axes: the node's cell range), union clipped to
+// the region.  Returns false for None.
+__device__ bool cells_reduce_axis(const CBox* __restrict__ cslab, int node_c0, int c0, int c1,
+                                  const Box& region, int lane, Box& out) {
+  Box u;
+  for (int k = 0; k < 3; ++k) { u.lo[k] = KD_FAR; u.hi[k] = -1; }
+  for (int c = c0 + lane; c <= c1; c += 32) {
+    const CBox v = cslab[c - node_c0];
+    if (v.lo[0] != KD_FAR) {
+      for (int k = 0; k < 3; ++k) { u.lo[k] = min(u.lo[k], v.lo[k]); u.hi[k] = max(u.hi[k], v.hi[k]); }
+    }
+  }
+  for (int o = 16; o; o >>= 1)
+    for (int k = 0; k < 3; ++k) {
+      u.lo[k] = min(u.lo[k], __shfl_xor_sync(0xffffffffu, u.lo[k], o));
+      u.hi[k] = max(u.hi[k], __shfl_xor_sync(0xffffffffu, u.hi[k], o));
+    }
+  if (u.lo[0] == KD_FAR) return false;
+  for (int k = 0; k < 3; ++k) {
+    out.lo[k] = max(u.lo[k], region.lo[k]);
+    out.hi[k] = min(u.hi[k], region.hi[k]);
+    if (out.lo[k] >= out.hi[k]) return false;
+  }
+  return true;
+}
+
+struct BinnedCtx {
+  const CBox* cslab[3];      // per-level cell-slab unions, per axis
+  const int64_t* coff[3];    // per-node offsets into cslab
+  int nc[3];
+};
+
+__device__ __forceinline__ void node_cell_range(const Box& b, int cs, const int* nc, int a,
+                                                int& c0, int& c1) {
+  c0 = max(b.lo[a] / cs, 0);
+  c1 = min((b.hi[a] - 1) / cs, nc[a] - 1);
+}
+
+// _cells_reduce(region) for a region inside node box b (uses the axis-a slab unions).
+__device__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a, const Box& region,
+                             int cs, int lane, Box& out) {
+  int n0, n1;
+  node_cell_range(node, cs, B.nc, a, n0, n1);
+  // region's cell range along a (kdtree.py:329-331), clamped like the reference
+  const int c0 = max(region.lo[a] / cs, 0);
+  const int c1 = min((region.hi[a] - 1) / cs, B.nc[a] - 1);
+  for (int k = 0; k < 3; ++k) {
+    int r0 = max(region.lo[k] / cs, 0), r1 = min((region.hi[k] - 1) / cs, B.nc[k] - 1);
+    if (r0 > r1) return false;
+  }
+  return cells_reduce_axis(B.cslab[a] + B.coff[a][i], n0, max(c0, n0), min(c1, n1), region,
+                           lane, out);
+}
+
+// ---- the decision kernel: one warp per node ------------------------------------------------
+__global__ void k_decide(KdLevel L, KdParams P, const Span* __restrict__ span_x,
+                         const Span* __restrict__ span_y, const Span* __restrict__ span_z,
+                         RBox* __restrict__ scratch, const int64_t* __restrict__ off_scr,
+                         BinnedCtx B, KdDecision* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= L.n) return;
+  const Box b = L.box[i];
+  int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
+  const int64_t vol = box_vol(b);
+  const Span* sp[3] = {span_x + L.off_x[i], span_y + L.off_y[i], span_z + L.off_z[i]};
+  KdDecision d;
+  d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.leaf = b;
+  bool split = false;
+  if (!halted(P, vol)) {
+    if (!P.binned) {
+      // _sweep_search + acceptance (kdtree.py:191-221, 431-439)
+      int ba = -1, bk = 0;
+      int64_t bc = 0;
+      for (int a = 0; a < 3; ++a) {
+        if (ext[a] < 2) continue;
+        int k;
+        int64_t c;
+        sweep_axis(sp[a], ext[a], scratch + off_scr[i], lane, k, c);
+        if (ba >= 0 && c >= bc) continue;
+        ba = a; bk = k; bc = c;
+      }
+      if (ba >= 0 && bc < vol) {
+        const RBox l = range_box(sp[ba], 0, bk, lane), r = range_box(sp[ba], bk, ext[ba], lane);
+        d.axis = ba; d.plane = b.lo[ba] + bk;
+        if (l.hi0 >= 0) { d.left = to_global(b, ba, l); d.nchild |= 1; }
+        if (r.hi0 >= 0) { d.right = to_global(b, ba, r); d.nchild |= 2; }
+        split = true;
+      }
+    } else {
+      // _binned_search (kdtree.py:353-368): first strict minimum over (axis, position)
+      int ba = -1, bp = 0;
+      int64_t bc = 0;
+      Box bl, br;
+      bool hl = false, hr = false;
+      for (int a = 0; a < 3; ++a) {
+        int pos[64];
+        const int np = snapped_positions(b.lo[a], b.hi[a], P.bins, P.cs, pos);
+        for (int q = 0; q < np; ++q) {
+          Box lreg = b, rreg = b, lb, rb;
+          lreg.hi[a] = pos[q];
+          rreg.lo[a] = pos[q];
+          const bool l = cells_reduce(B, i, b, a, lreg, P.cs, lane, lb);
+          const bool r = cells_reduce(B, i, b, a, rreg, P.cs, lane, rb);
+          const int64_t c = (l ? box_vol(lb) : 0) + (r ? box_vol(rb) : 0);
+          if (ba < 0 || c < bc) { ba = a; bp = pos[q]; bc = c; bl = lb; br = rb; hl = l; hr = r; }
+        }
+      }
+      if (ba >= 0 && bc < vol) {
+        d.axis = ba; d.plane = bp;
+        if (hl) { d.left = bl; d.nchild |= 1; }
+        if (hr) { d.right = br; d.nchild |= 2; }
+        split = true;
+      }
+    }
+  }
+  if (!split && P.mls >= 0) {
+    // forced_split (kdtree.py:441-467)
+    int a = 0;
+    if (ext[1] > ext[a]) a = 1;
+    if (ext[2] > ext[a]) a = 2;
+    if (ext[a] > P.mls) {
+      const int lo = b.lo[a], hi = b.hi[a];
+      int pos = lo + ext[a] / 2;
+      if (P.binned) {
+        const int cs = P.cs;
+        const int first = (lo / cs + 1) * cs, last = ((hi - 1) / cs) * cs;
+        if (first <= last) {
+          const int64_t snap =
+              (int64_t)floor(__dadd_rn(__ddiv_rn((double)pos, (double)cs), 0.5)) * cs;
+          {
+            int64_t q = snap < first ? (int64_t)first : snap;
+            pos = (int)(q > last ? (int64_t)last : q);
+          }
+        }
+        Box lreg = b, rreg = b, lb, rb;
+        lreg.hi[a] = pos;
+        rreg.lo[a] = pos;
+        const bool l = cells_reduce(B, i, b, a, lreg, cs, lane, lb);
+        const bool r = cells_reduce(B, i, b, a, rreg, cs, lane, rb);
+        d.axis = a; d.plane = pos;
+        if (l) { d.left = lb; d.nchild |= 1; }
+        if (r) { d.right = rb; d.nchild |= 2; }
+      } else {
+        const int k = pos - lo;
+        const RBox l = range_box(sp[a], 0, k, lane), r = range_box(sp[a], k, ext[a], lane);
+        d.axis = a; d.plane = pos;
+        if (l.hi0 >= 0) { d.left = to_global(b, a, l); d.nchild |= 1; }
+        if (r.hi0 >= 0) { d.right = to_global(b, a, r); d.nchild |= 2; }
+      }
+      split = true;
+    }
+  }
+  if (lane == 0) out[i] = d;
+}
+
+// Which nodes need bit spans this level (sweep: any node that may search or force-split;
+// binned: only nodes that will be leaves -> decided after the binned pass, so all
+// candidates here; the host runs the spans for binned leaves in a second pass).
+__global__ void k_need(KdLevel L, KdParams P, int binned_pass2,
+                       const KdDecision* __restrict__ dec) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.n) return;
+  const Box b = L.box[i];
+  const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
+  int need;
+  if (!P.binned) {
+    const int mx = max(ext[0], max(ext[1], ext[2]));
+    need = (!halted(P, box_vol(b)) || (P.mls >= 0 && mx > P.mls)) ? 1 : 0;
+  } else {
+    need = binned_pass2 ? (dec[i].axis < 0 ? 1 : 0) : 0;
+  }
+  L.need[i] = need;
+  const int wz = (ext[2] + 31) >> 5;
+  // per-node sizes (scanned by the host afterwards)
+  L.off_x[i] = need ? ext[0] : 0;
+  L.off_y[i] = (need && !P.binned) ? ext[1] : 0;
+  L.off_z[i] = (need && !P.binned) ? ext[2] : 0;
+  L.off_pxz[i] = need ? (int64_t)ext[0] * wz : 0;
+  L.off_pyz[i] = (need && !P.binned) ? (int64_t)ext[1] * wz : 0;
+  L.off_zw[i] = (need && !P.binned) ? wz : 0;
+}
+
+// Scratch for the suffix boxes: max extent of the node (any axis).
+__global__ void k_scratch_sizes(KdLevel L, int64_t* __restrict__ sz) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.n) return;
+  const Box b = L.box[i];
+  const int m = max(b.hi[0] - b.lo[0], max(b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]));
+  sz[i] = (L.need[i] & 1) ? m : 0;
+}
+
+// ---- cell boxes (precompute_cell_boxes, kdtree.py:285-320) ---------------------------------
+__global__ void k_cell_boxes(const uint32_t* __restrict__ bits, int nx, int ny, int nz, int cs,
+                             int ncx, int ncy, int ncz, CBox* __restrict__ cells) {
+  const int64_t n = (int64_t)ncx * ncy * ncz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cz = (int)(i % ncz), cy = (int)((i / ncz) % ncy), cx = (int)(i / ((int64_t)ncz * ncy));
+  const int nzw = (int)nzw_of(nz);
+  const int x0 = cx * cs, x1 = min(nx, x0 + cs), y0 = cy * cs, y1 = min(ny, y0 + cs);
+  const int z0 = cz * cs, z1 = min(nz, z0 + cs);
+  CBox c;
+  for (int k = 0; k < 3; ++k) { c.lo[k] = KD_FAR; c.hi[k] = -1; }
+  for (int x = x0; x < x1; ++x)
+    for (int y = y0; y < y1; ++y) {
+      const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
+      for (int w = z0 >> 5; w <= (z1 - 1) >> 5; ++w) {
+        uint32_t v = __ldg(row + w);
+        const int wb = w * 32;
+        if (wb < z0) v &= 0xffffffffu << (z0 - wb);
+        if (z1 - wb < 32) v &= (1u << (z1 - wb)) - 1u;
+        if (!v) continue;
+        c.lo[0] = min(c.lo[0], x); c.hi[0] = max(c.hi[0], x + 1);
+        c.lo[1] = min(c.lo[1], y); c.hi[1] = max(c.hi[1], y + 1);
+        c.lo[2] = min(c.lo[2], wb + __ffs(v) - 1);
+        c.hi[2] = max(c.hi[2], wb + 32 - __clz(v));
+      }
+    }
+  if (c.hi[0] < 0) c.lo[0] = KD_FAR;
+  cells[i] = c;
+}
+
+// Cell-slab unions along axis A: warp per (node, cell slab c in the node's cell range).
+__global__ void k_cell_slabs(const CBox* __restrict__ cells, int ncx, int ncy, int ncz, int cs,
+                             int A, KdLevel L, const int64_t* __restrict__ off,
+                             const int64_t* __restrict__ total, CBox* __restrict__ out) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nc[3] = {ncx, ncy, ncz};
+  const int64_t items = *total;
+  for (int64_t it = (int64_t)blockIdx.x * 8 + wib; it < items; it += (int64_t)gridDim.x * 8) {
+    const int i = find_node(off, L.n, it);
+    const Box b = L.box[i];
+    int c0[3], c1[3];
+    for (int k = 0; k < 3; ++k) node_cell_range(b, cs, nc, k, c0[k], c1[k]);
+    const int c = c0[A] + (int)(it - off[i]);
+    int o1, o2;
+    others(A, o1, o2);
+    const int n1 = c1[o1] - c0[o1] + 1, n2 = c1[o2] - c0[o2] + 1;
+    CBox u;
+    for (int k = 0; k < 3; ++k) { u.lo[k] = KD_FAR; u.hi[k] = -1; }
+    for (int q = lane; q < n1 * n2; q += 32) {
+      int cc[3];
+      cc[A] = c;
+      cc[o1] = c0[o1] + q / n2;
+      cc[o2] = c0[o2] + q % n2;
+      const CBox v = cells[((int64_t)cc[0] * ncy + cc[1]) * ncz + cc[2]];
+      if (v.lo[0] != KD_FAR)
+        for (int k = 0; k < 3; ++k) { u.lo[k] = min(u.lo[k], v.lo[k]); u.hi[k] = max(u.hi[k], v.hi[k]); }
+    }
+    for (int o = 16; o; o >>= 1)
+      for (int k = 0; k < 3; ++k) {
+        u.lo[k] = min(u.lo[k], __shfl_xor_sync(0xffffffffu, u.lo[k], o));
+        u.hi[k] = max(u.hi[k], __shfl_xor_sync(0xffffffffu, u.hi[k], o));
+      }
+    if (lane == 0) out[it] = u;
+  }
+}
+
+__global__ void k_cell_slab_sizes(KdLevel L, int cs, int ncx, int ncy, int ncz, int A,
+                                  int64_t* __restrict__ sz) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.n) return;
+  const int nc[3] = {ncx, ncy, ncz};
+  int c0, c1;
+  node_cell_range(L.box[i], cs, nc, A, c0, c1);
+  sz[i] = c1 - c0 + 1;
+}
+
+// ---- next level + bookkeeping ---------------------------------------------------------------
+__global__ void k_child_counts(const KdDecision* __restrict__ dec, int n, int64_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  cnt[i] = __popc(dec[i].nchild);
+}
+
+struct NodeRec {   // per node, global BFS id
+  Box box;
+  int axis, plane, left, right, dropped, level;
+};
+
+__global__ void k_emit_level(const KdDecision* __restrict__ dec, const int64_t* __restrict__ coff,
+                             int n, int64_t base, int64_t next_base, int level,
+                             NodeRec* __restrict__ rec, Box* __restrict__ next_box) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const KdDecision d = dec[i];
+  NodeRec r;
+  r.box = d.leaf;  // internal rows keep the node box; binned leaves the shrunk box
+  r.axis = d.axis;
+  r.plane = d.plane;
+  r.left = r.right = -1;
+  r.dropped = d.dropped;
+  r.level = level;
+  int64_t o = coff[i];
+  if (d.nchild & 1) { next_box[o] = d.left; r.left = (int)(next_base + o); ++o; }
+  if (d.nchild & 2) { next_box[o] = d.right; r.right = (int)(next_base + o); }
+  rec[base + i] = r;
+}
+
+
+// Binned leaves: exact shrink_to_occupied(box) from the x spans; empty -> dropped.
+__global__ void k_leaf_shrink(KdLevel L, const Span* __restrict__ span_x,
+                              KdDecision* __restrict__ dec) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= L.n || !(L.need[i] & 1)) return;
+  const Box b = L.box[i];
+  const RBox t = range_box(span_x + L.off_x[i], 0, b.hi[0] - b.lo[0], lane);
+  if (lane == 0) {
+    if (t.hi0 < 0) dec[i].dropped = 1;
+    else dec[i].leaf = to_global(b, 0, t);
+  }
+}
+
+// Single-CTA exclusive scan of K int64 arrays of n+1 entries each (entry n = total).
+struct ScanSet {
+  int64_t* a[12];
+  int k;
+};
+
+__global__ void k_multi_scan(ScanSet S, int n) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int64_t len = (int64_t)n + 1;
+  const int64_t chunk = (len + T - 1) / T;
+  for (int k = 0; k < S.k; ++k) {
+    int64_t* a = S.a[k];
+    const int64_t b0 = t * chunk, b1 = min(len, b0 + chunk);
+    int64_t sum = 0;
+    for (int64_t j = b0; j < b1; ++j) sum += (j < n) ? a[j] : 0;
+    part[t] = sum;
+    __syncthreads();
+    for (int o = 1; o < T; o <<= 1) {
+      int64_t v = t >= o ? part[t - o] : 0;
+      __syncthreads();
+      part[t] += v;
+      __syncthreads();
+    }
+    int64_t run = part[t] - sum;  // exclusive prefix of this chunk
+    for (int64_t j = b0; j < b1; ++j) {
+      const int64_t v = (j < n) ? a[j] : 0;
+      a[j] = run;
+      run += v;
+    }
+    __syncthreads();
+  }
+}
+
+// Root box: tight box of every set bit (shrink_to_occupied of the full volume).
+__global__ void k_bits_bbox(const uint32_t* __restrict__ bits, int nx, int ny, int nz,
+                            int* __restrict__ bb) {
+  const int nzw = (int)nzw_of(nz);
+  const int64_t nrows = (int64_t)nx * ny;
+  int lo[3] = {KD_FAR, KD_FAR, KD_FAR}, hi[3] = {-1, -1, -1};
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(r / ny), y = (int)(r % ny);
+    const uint32_t* row = bits + r * nzw;
+    int zf = -1, zl = -1;
+    for (int w = 0; w < nzw; ++w) {
+      const uint32_t v = row[w];
+      if (v) {
+        if (zf < 0) zf = 32 * w + __ffs(v) - 1;
+        zl = 32 * w + 31 - __clz(v);
+      }
+    }
+    if (zf >= 0) {
+      lo[0] = min(lo[0], x); hi[0] = max(hi[0], x);
+      lo[1] = min(lo[1], y); hi[1] = max(hi[1], y);
+      lo[2] = min(lo[2], zf); hi[2] = max(hi[2], zl);
+    }
+  }
+  for (int k = 0; k < 3; ++k) {
+    for (int o = 16; o; o >>= 1) {
+      lo[k] = min(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = max(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0 && hi[0] >= 0)
+    for (int k = 0; k < 3; ++k) { atomicMin(bb + k, lo[k]); atomicMax(bb + 3 + k, hi[k] + 1); }
+}
+
+// Finalisation: subtree sizes (bottom-up per level), preorder (top-down per level), rows.
+__global__ void k_sizes(const NodeRec* __restrict__ rec, int64_t b0, int64_t b1,
+                        int* __restrict__ size) {
+  const int64_t i = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b1) return;
+  const NodeRec r = rec[i];
+  int s = 0;
+  if (!r.dropped) {
+    s = 1;
+    if (r.left >= 0) s += size[r.left];
+    if (r.right >= 0) s += size[r.right];
+  }
+  size[i] = s;
+}
+
+__global__ void k_preorder(const NodeRec* __restrict__ rec, int64_t b0, int64_t b1,
+                           const int* __restrict__ size, int* __restrict__ pre) {
+  const int64_t i = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b1) return;
+  const NodeRec r = rec[i];
+  if (r.dropped) return;
+  const int p = pre[i];
+  int nxt = p + 1;
+  if (r.left >= 0 && size[r.left] > 0) { pre[r.left] = nxt; nxt += size[r.left]; }
+  if (r.right >= 0 && size[r.right] > 0) pre[r.right] = nxt;
+}
+
+__global__ void k_scatter_rows(const NodeRec* __restrict__ rec, int64_t total,
+                               const int* __restrict__ size, const int* __restrict__ pre,
+                               int32_t* __restrict__ lo, int32_t* __restrict__ hi,
+                               int8_t* __restrict__ axis, int32_t* __restrict__ plane,
+                               int32_t* __restrict__ left, int32_t* __restrict__ right,
+                               int* __restrict__ height) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const NodeRec r = rec[i];
+  if (r.dropped) return;
+  const int p = pre[i];
+  for (int k = 0; k < 3; ++k) { lo[3 * p + k] = r.box.lo[k]; hi[3 * p + k] = r.box.hi[k]; }
+  axis[p] = (int8_t)r.axis;
+  plane[p] = r.plane;
+  left[p] = (r.left >= 0 && size[r.left] > 0) ? pre[r.left] : -1;
+  right[p] = (r.right >= 0 && size[r.right] > 0) ? pre[r.right] : -1;
+  atomicMax(height, r.level + 1);
+}
+
+}  // namespace vs
+
+using namespace vs;
+
+namespace {
+
+// Grow-only stream-ordered scratch buffer (data-dependent sizes: the k-d tree's level widths
+// are only known as it is built).
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaStream_t st = nullptr;
+  int ensure(size_t bytes, const char* what) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFreeAsync(p, st);
+    size_t nb = std::max(bytes, cap * 3 / 2 + 256);
+    cudaError_t e = cudaMallocAsync(&p, nb, st);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cap = 0;
+      set_error("%s: cudaMallocAsync(%zu): %s", what, nb, cudaGetErrorString(e));
+      return (int)e;
+    }
+    cap = nb;
+    return 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  ~DBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+struct KdResultImpl {
+  int64_t m = 0;
+  int root = -1;
+  int height = 0;
+  DBuf lo, hi, axis, plane, left, right;
+};
+
+int d2h(void* dst, const void* src, size_t n, cudaStream_t st) {
+  VS_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st), "d2h");
+  VS_CUDA(cudaStreamSynchronize(st), "sync");
+  return 0;
+}
+
+constexpr int SPAN_BLOCKS = 148 * 8;
+
+}  // namespace
+
+extern "C" {
+
+int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, int binned,
+                int bins, int cs, void** handle, vs_stream_t stream) {
+  if (!bits || !handle || nx < 1 || ny < 1 || nz < 1 || bins < 2 || cs < 1)
+    return fail_arg("vs_kd_build");
+  if (bins > 65) return fail_arg("vs_kd_build: bins > 65");
+  if (nz > 1024) return fail_arg("vs_kd_build: nz > 1024");
+  cudaStream_t st = S(stream);
+  auto* R = new KdResultImpl();
+  *handle = R;
+  for (DBuf* b : {&R->lo, &R->hi, &R->axis, &R->plane, &R->left, &R->right}) b->st = st;
+  const int nzw = (int)nzw_of(nz);
+
+  DBuf bb, cur, nxt, need, offs, dec, cnt, spx, spy, spz, pxz, pyz, scr, rec, cellb, cslab,
+      coff, sizes, pre, tot;
+  for (DBuf* b : {&bb, &cur, &nxt, &need, &offs, &dec, &cnt, &spx, &spy, &spz, &pxz, &pyz, &scr,
+                  &rec, &cellb, &cslab, &coff, &sizes, &pre, &tot})
+    b->st = st;
+
+  // root box (kdtree.py:398): tight box of every flag
+  VS_TRY(bb.ensure(6 * sizeof(int), "bbox"));
+  const int init[6] = {KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
+  VS_CUDA(cudaMemcpyAsync(bb.p, init, sizeof init, cudaMemcpyHostToDevice, st), "bbox init");
+  k_bits_bbox<<<SPAN_BLOCKS, 256, 0, st>>>(bits, nx, ny, nz, bb.as<int>());
+  VS_TRY(check_launch("k_bits_bbox"));
+  int rb[6];
+  VS_TRY(d2h(rb, bb.p, sizeof rb, st));
+  if (rb[3] < 0) return 0;  // empty tree
+  Box root;
+  for (int k = 0; k < 3; ++k) { root.lo[k] = rb[k]; root.hi[k] = rb[3 + k]; }
+
+  KdParams P;
+  P.deep = deep; P.mls = mls; P.binned = binned; P.bins = bins; P.cs = cs;
+  P.root_vol = box_vol(root);
+
+  const int ncx = (int)cdiv(nx, cs), ncy = (int)cdiv(ny, cs), ncz = (int)cdiv(nz, cs);
+  if (binned) {
+    const int64_t ncell = (int64_t)ncx * ncy * ncz;
+    VS_TRY(cellb.ensure(ncell * sizeof(CBox), "cells"));
+    k_cell_boxes<<<(unsigned)cdiv(ncell, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy,
+                                                             ncz, cellb.as<CBox>());
+    VS_TRY(check_launch("k_cell_boxes"));
+  }
+
+  VS_TRY(cur.ensure(sizeof(Box), "level"));
+  VS_CUDA(cudaMemcpyAsync(cur.p, &root, sizeof root, cudaMemcpyHostToDevice, st), "root");
+  int64_t n = 1, base = 0;
+  std::vector<int64_t> level_base;
+  int level = 0;
+  while (n > 0) {
+    level_base.push_back(base);
+    // per-level arrays: need (n ints), 12 offset arrays (n+1 int64), decisions, counts
+    VS_TRY(need.ensure(n * sizeof(int), "need"));
+    VS_TRY(offs.ensure(12 * (n + 1) * sizeof(int64_t), "offsets"));
+    VS_TRY(dec.ensure(n * sizeof(KdDecision), "decisions"));
+    VS_TRY(cnt.ensure((n + 1) * sizeof(int64_t), "counts"));
+    VS_TRY(tot.ensure(16 * sizeof(int64_t), "totals"));
+    int64_t* O = offs.as<int64_t>();
+    auto arr = [&](int k) { return O + (int64_t)k * (n + 1); };
+    KdLevel L;
+    L.n = (int)n; L.box = cur.as<Box>(); L.need = need.as<int>();
+    L.off_x = arr(0); L.off_y = arr(1); L.off_z = arr(2);
+    L.off_pxz = arr(3); L.off_pyz = arr(4); L.off_zw = arr(5);
+    int64_t* scr_off = arr(6);
+    BinnedCtx B;
+    B.nc[0] = ncx; B.nc[1] = ncy; B.nc[2] = ncz;
+    const unsigned gn = (unsigned)cdiv(n, 128);
+    const unsigned gw = (unsigned)cdiv(n, 4);  // warp per node, 128-thread blocks
+    auto scan = [&](std::initializer_list<int64_t*> lst) -> int {
+      ScanSet S;
+      S.k = 0;
+      for (int64_t* a : lst) S.a[S.k++] = a;
+      k_multi_scan<<<1, 1024, 0, st>>>(S, (int)n);
+      return check_launch("k_multi_scan");
+    };
+    auto totals = [&](std::initializer_list<int64_t*> lst, int64_t* out) -> int {
+      int k = 0;
+      for (int64_t* a : lst) {
+        VS_CUDA(cudaMemcpyAsync(tot.as<int64_t>() + k, a + n, sizeof(int64_t),
+                                cudaMemcpyDeviceToDevice, st), "tot");
+        ++k;
+      }
+      return d2h(out, tot.p, k * sizeof(int64_t), st);
+    };
+    if (!binned) {
+      k_need<<<gn, 128, 0, st>>>(L, P, 0, nullptr);
+      VS_TRY(check_launch("k_need"));
+      k_scratch_sizes<<<gn, 128, 0, st>>>(L, scr_off);
+      VS_TRY(check_launch("k_scratch_sizes"));
+      VS_TRY(scan({L.off_x, L.off_y, L.off_z, L.off_pxz, L.off_pyz, L.off_zw, scr_off}));
+      int64_t t[7];
+      VS_TRY(totals({L.off_x, L.off_y, L.off_z, L.off_pxz, L.off_pyz, L.off_zw, scr_off}, t));
+      VS_TRY(spx.ensure((t[0] + 1) * sizeof(Span), "span_x"));
+      VS_TRY(spy.ensure((t[1] + 1) * sizeof(Span), "span_y"));
+      VS_TRY(spz.ensure((t[2] + 32) * sizeof(Span), "span_z"));
+      VS_TRY(pxz.ensure((t[3] + 1) * 4, "pxz"));
+      VS_TRY(pyz.ensure((t[4] + 1) * 4, "pyz"));
+      VS_TRY(scr.ensure((t[6] + 1) * sizeof(RBox), "scratch"));
+      if (t[0] > 0) {
+        k_spans_x<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_x + n, spx.as<Span>(),
+                                               pxz.as<uint32_t>());
+        VS_TRY(check_launch("k_spans_x"));
+        k_spans_y<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_y + n, spy.as<Span>(),
+                                               pyz.as<uint32_t>());
+        VS_TRY(check_launch("k_spans_y"));
+        k_spans_z<<<SPAN_BLOCKS, 128, 0, st>>>(L, L.off_zw + n, pxz.as<uint32_t>(),
+                                               pyz.as<uint32_t>(), spz.as<Span>());
+        VS_TRY(check_launch("k_spans_z"));
+      }
+      k_decide<<<gw, 128, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(), spz.as<Span>(),
+                                   scr.as<RBox>(), scr_off, B, dec.as<KdDecision>());
+      VS_TRY(check_launch("k_decide"));
+    } else {
+      int64_t* co[3] = {arr(7), arr(8), arr(9)};
+      for (int a = 0; a < 3; ++a) {
+        k_cell_slab_sizes<<<gn, 128, 0, st>>>(L, cs, ncx, ncy, ncz, a, co[a]);
+        VS_TRY(check_launch("k_cell_slab_sizes"));
+      }
+      VS_TRY(scan({co[0], co[1], co[2]}));
+      int64_t t[3];
+      VS_TRY(totals({co[0], co[1], co[2]}, t));
+      VS_TRY(cslab.ensure((t[0] + t[1] + t[2] + 3) * sizeof(CBox), "cell slabs"));
+      CBox* cbase = cslab.as<CBox>();
+      CBox* cs3[3] = {cbase, cbase + t[0] + 1, cbase + t[0] + t[1] + 2};
+      for (int a = 0; a < 3; ++a) {
+        k_cell_slabs<<<SPAN_BLOCKS, 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
+                                                  co[a], co[a] + n, cs3[a]);
+        VS_TRY(check_launch("k_cell_slabs"));
+        B.cslab[a] = cs3[a];
+        B.coff[a] = co[a];
+      }
+      k_decide<<<gw, 128, 0, st>>>(L, P, nullptr, nullptr, nullptr, nullptr, nullptr, B,
+                                   dec.as<KdDecision>());
+      VS_TRY(check_launch("k_decide"));
+      // exact shrink for the binned leaves (kdtree.py:474)
+      k_need<<<gn, 128, 0, st>>>(L, P, 1, dec.as<KdDecision>());
+      VS_TRY(check_launch("k_need"));
+      VS_TRY(scan({L.off_x, L.off_pxz}));
+      int64_t t2[2];
+      VS_TRY(totals({L.off_x, L.off_pxz}, t2));
+      if (t2[0] > 0) {
+        VS_TRY(spx.ensure((t2[0] + 1) * sizeof(Span), "span_x"));
+        VS_TRY(pxz.ensure((t2[1] + 1) * 4, "pxz"));
+        k_spans_x<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_x + n, spx.as<Span>(),
+                                               pxz.as<uint32_t>());
+        VS_TRY(check_launch("k_spans_x"));
+        k_leaf_shrink<<<gw, 128, 0, st>>>(L, spx.as<Span>(), dec.as<KdDecision>());
+        VS_TRY(check_launch("k_leaf_shrink"));
+      }
+    }
+    // next level
+    k_child_counts<<<gn, 128, 0, st>>>(dec.as<KdDecision>(), (int)n, cnt.as<int64_t>());
+    VS_TRY(check_launch("k_child_counts"));
+    VS_TRY(scan({cnt.as<int64_t>()}));
+    int64_t next_n;
+    VS_TRY(d2h(&next_n, cnt.as<int64_t>() + n, sizeof next_n, st));
+    // grow the record array (copy-preserving)
+    if ((size_t)(base + n) * sizeof(NodeRec) > rec.cap) {
+      DBuf bigger;
+      bigger.st = st;
+      VS_TRY(bigger.ensure(std::max<size_t>((base + n) * sizeof(NodeRec) * 2, 4096), "records"));
+      if (base) VS_CUDA(cudaMemcpyAsync(bigger.p, rec.p, base * sizeof(NodeRec),
+                                        cudaMemcpyDeviceToDevice, st), "records copy");
+      std::swap(rec.p, bigger.p);
+      std::swap(rec.cap, bigger.cap);
+    }
+    VS_TRY(nxt.ensure(std::max<int64_t>(next_n, 1) * sizeof(Box), "next level"));
+    k_emit_level<<<gn, 128, 0, st>>>(dec.as<KdDecision>(), cnt.as<int64_t>(), (int)n, base,
+                                     base + n, level, rec.as<NodeRec>(), nxt.as<Box>());
+    VS_TRY(check_launch("k_emit_level"));
+    std::swap(cur.p, nxt.p);
+    std::swap(cur.cap, nxt.cap);
+    base += n;
+    n = next_n;
+    ++level;
+  }
+  const int64_t total = base;
+  level_base.push_back(total);
+  VS_TRY(sizes.ensure(total * sizeof(int), "sizes"));
+  VS_TRY(pre.ensure(total * sizeof(int), "preorder"));
+  for (int l = (int)level_base.size() - 2; l >= 0; --l) {
+    const int64_t b0 = level_base[l], b1 = level_base[l + 1];
+    k_sizes<<<(unsigned)cdiv(b1 - b0, 128), 128, 0, st>>>(rec.as<NodeRec>(), b0, b1,
+                                                          sizes.as<int>());
+    VS_TRY(check_launch("k_sizes"));
+  }
+  int m = 0;
+  VS_TRY(d2h(&m, sizes.p, sizeof m, st));
+  R->m = m;
+  if (m == 0) return 0;
+  VS_CUDA(cudaMemsetAsync(pre.p, 0, sizeof(int), st), "pre root");
+  for (size_t l = 0; l + 1 < level_base.size(); ++l) {
+    const int64_t b0 = level_base[l], b1 = level_base[l + 1];
+    k_preorder<<<(unsigned)cdiv(b1 - b0, 128), 128, 0, st>>>(rec.as<NodeRec>(), b0, b1,
+                                                             sizes.as<int>(), pre.as<int>());
+    VS_TRY(check_launch("k_preorder"));
+  }
+  VS_TRY(R->lo.ensure(3 * m * 4, "lo"));
+  VS_TRY(R->hi.ensure(3 * m * 4, "hi"));
+  VS_TRY(R->axis.ensure(m, "axis"));
+  VS_TRY(R->plane.ensure(m * 4, "plane"));
+  VS_TRY(R->left.ensure(m * 4, "left"));
+  VS_TRY(R->right.ensure(m * 4, "right"));
+  VS_TRY(tot.ensure(sizeof(int) * 2, "height"));
+  VS_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(int), st), "height init");
+  k_scatter_rows<<<(unsigned)cdiv(total, 128), 128, 0, st>>>(
+      rec.as<NodeRec>(), total, sizes.as<int>(), pre.as<int>(), R->lo.as<int32_t>(),
+      R->hi.as<int32_t>(), R->axis.as<int8_t>(), R->plane.as<int32_t>(), R->left.as<int32_t>(),
+      R->right.as<int32_t>(), tot.as<int>());
+  VS_TRY(check_launch("k_scatter_rows"));
+  VS_TRY(d2h(&R->height, tot.p, sizeof(int), st));
+  R->root = 0;
+  return 0;
+}
+
+int vs_kd_result_info(void* handle, int64_t* m, int* root, int* height) {
+  auto* R = static_cast<KdResultImpl*>(handle);
+  if (!R) return fail_arg("vs_kd_result_info");
+  if (m) *m = R->m;
+  if (root) *root = R->root;
+  if (height) *height = R->height;
+  return 0;
+}
+
+int vs_kd_result_copy(void* handle, int32_t* lo, int32_t* hi, int8_t* axis, int32_t* plane,
+                      int32_t* left, int32_t* right, vs_stream_t stream) {
+  auto* R = static_cast<KdResultImpl*>(handle);
+  if (!R) return fail_arg("vs_kd_result_copy");
+  if (R->m == 0) return 0;
+  cudaStream_t st = S(stream);
+  const int64_t m = R->m;
+  VS_CUDA(cudaMemcpyAsync(lo, R->lo.p, 12 * m, cudaMemcpyDeviceToDevice, st), "copy lo");
+  VS_CUDA(cudaMemcpyAsync(hi, R->hi.p, 12 * m, cudaMemcpyDeviceToDevice, st), "copy hi");
+  VS_CUDA(cudaMemcpyAsync(axis, R->axis.p, m, cudaMemcpyDeviceToDevice, st), "copy axis");
+  VS_CUDA(cudaMemcpyAsync(plane, R->plane.p, 4 * m, cudaMemcpyDeviceToDevice, st), "copy plane");
+  VS_CUDA(cudaMemcpyAsync(left, R->left.p, 4 * m, cudaMemcpyDeviceToDevice, st), "copy left");
+  VS_CUDA(cudaMemcpyAsync(right, R->right.p, 4 * m, cudaMemcpyDeviceToDevice, st), "copy right");
+  return 0;
+}
+
+void vs_kd_result_free(void* handle) { delete static_cast<KdResultImpl*>(handle); }
+
+}  // extern "C"

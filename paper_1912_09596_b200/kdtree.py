@@ -133,5 +133,56 @@ def empty_kdtree(dims) -> KdTree:
     return KdTree(z3, z3, np.zeros(0, np.int8), z, z, z, -1, dims)
 
 
+def build_kdtree(g, params: BuildParams | None = None) -> KdTree:
+    """Top-down build over a table grid (kdtree.py:387-498) on the device: level-synchronous
+    split search (vs_kd_build), rows in the reference's DFS preorder."""
+    import ctypes as C
+
+    from ._lib import call, ptr, query, stream
+
+    params = params or BuildParams()
+    b = g.binary
+    nx, ny, nz = g.dims
+    h = C.c_void_p()
+    try:
+        call("vs_kd_build", ptr(b.packed()), nx, ny, nz, int(params.mode == "deep"),
+             -1 if params.max_leaf_size is None else int(params.max_leaf_size),
+             int(params.builder == "binned"), int(params.bins), int(params.cell_size),
+             C.byref(h), stream())
+        m, root, height = C.c_int64(), C.c_int(), C.c_int()
+        call("vs_kd_result_info", h, C.byref(m), C.byref(root), C.byref(height))
+        m = int(m.value)
+        if m == 0:
+            return empty_kdtree(g.dims)
+        dev = _lib.device()
+        d = {"lo": torch.empty((m, 3), dtype=torch.int32, device=dev),
+             "hi": torch.empty((m, 3), dtype=torch.int32, device=dev),
+             "axis": torch.empty(m, dtype=torch.int8, device=dev),
+             "plane": torch.empty(m, dtype=torch.int32, device=dev),
+             "left": torch.empty(m, dtype=torch.int32, device=dev),
+             "right": torch.empty(m, dtype=torch.int32, device=dev)}
+        call("vs_kd_result_copy", h, ptr(d["lo"]), ptr(d["hi"]), ptr(d["axis"]), ptr(d["plane"]),
+             ptr(d["left"]), ptr(d["right"]), stream())
+        torch.cuda.current_stream().synchronize()
+    finally:
+        if h.value:
+            _lib.lib().vs_kd_result_free(h)
+    return KdTree(root=int(root.value), dims=g.dims, dev=d, height=int(height.value))
+
+
+_KD_PARAMS = {
+    "kd-shallow": BuildParams(mode="shallow"),
+    "kd-deep-mls32": BuildParams(mode="deep", max_leaf_size=32),
+    "kd-deep-mls128": BuildParams(mode="deep", max_leaf_size=128),
+    "kd-binned-mls32": BuildParams(mode="deep", max_leaf_size=32, builder="binned"),
+}
+
+
 def build_index_kind(kind: str, b):
-    raise NotImplementedError(f"{kind}: SVT k-d builders are not built yet")
+    """bench.py:166-172 for the table-based kinds."""
+    from .hybrid import build_hybrid
+    from .svt import build_svt_grid
+
+    if kind == "hybrid":
+        return build_hybrid(build_svt_grid(b), b)
+    return build_kdtree(build_svt_grid(b), _KD_PARAMS[kind])

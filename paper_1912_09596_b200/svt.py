@@ -60,3 +60,79 @@ def derive_macro_grid(source, cell_size: int) -> MacroGrid:
     else:
         call("vs_vote_cells", ptr(b.packed()), nx, ny, nz, cs, ptr(occ), stream())
     return MacroGrid(cs, nc, dims, occ)
+
+
+class SvtGrid:
+    """Per-brick summed-volume tables (svt.py:20-26) over a classification.
+
+    ``tables`` (nbx, nby, nbz, bs+1, bs+1, bs+1) uint32 is built on the device on first use
+    (vs_svt_build); the k-d builders read the packed bits directly, so a TF-change k-d
+    rebuild never pays for the tables unless they are asked for."""
+
+    def __init__(self, b: BinaryVolume, brick_size: int):
+        self.binary = b
+        self.brick_size = int(brick_size)
+        self.dims = b.dims
+        self.bricks_dims = tuple(-(-d // self.brick_size) for d in self.dims)
+        self._tables_dev = None
+        self._tables = None
+
+    @property
+    def bits(self) -> np.ndarray:
+        return self.binary.bits
+
+    def tables_dev(self) -> torch.Tensor:
+        if self._tables_dev is None:
+            nb, e = self.bricks_dims, self.brick_size + 1
+            t = torch.empty((*nb, e, e, e), dtype=torch.int32, device=_lib.device())
+            nx, ny, nz = self.dims
+            call("vs_svt_build", ptr(self.binary.packed()), nx, ny, nz, self.brick_size, ptr(t),
+                 stream())
+            self._tables_dev = t
+        return self._tables_dev
+
+    @property
+    def tables(self) -> np.ndarray:
+        if self._tables is None:
+            self._tables = self.tables_dev().cpu().numpy().view(np.uint32)
+        return self._tables
+
+
+def build_svt_grid(b: BinaryVolume, brick_size: int = DEFAULT_BRICK_SIZE) -> SvtGrid:
+    """Cumulative-count tables for every brick (svt.py:40-57); built lazily on the device."""
+    if brick_size < 2:
+        raise ValueError("brick_size must be >= 2")
+    if brick_size > 32:
+        raise ValueError("brick_size > 32 is not supported by the device table builder")
+    return SvtGrid(b, brick_size)
+
+
+def box_count(g: SvtGrid, box) -> int:
+    """Exact number of set flags inside ``box`` (svt.py:65-90), from the tables."""
+    t = g.tables_dev()
+    dev = t.device
+    b = torch.tensor([list(box.lo) + list(box.hi)], dtype=torch.int32, device=dev)
+    out = torch.zeros(1, dtype=torch.int64, device=dev)
+    nx, ny, nz = g.dims
+    call("vs_box_count", ptr(t), nx, ny, nz, g.brick_size, ptr(b), 1, ptr(out), stream())
+    return int(out.item())
+
+
+def tight_box(b: BinaryVolume, box):
+    """Minimal box holding every flag of ``box`` (None when empty), from the packed bits."""
+    from .volume import Aabb
+
+    dev = _lib.device()
+    bx = torch.tensor(list(box.lo) + list(box.hi), dtype=torch.int32, device=dev)
+    out = torch.empty(6, dtype=torch.int32, device=dev)
+    nx, ny, nz = b.dims
+    call("vs_tight_box", ptr(b.packed()), nx, ny, nz, ptr(bx), ptr(out), stream())
+    r = out.cpu().tolist()
+    if r[3] < 0:
+        return None
+    return Aabb(tuple(r[:3]), tuple(r[3:]))
+
+
+def shrink_to_occupied(g: SvtGrid, box):
+    """Minimal box containing every set flag inside ``box``, or None (svt.py:100-131)."""
+    return tight_box(g.binary, box)

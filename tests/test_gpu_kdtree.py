@@ -1,0 +1,143 @@
+"""GPU parity of the summed-volume tables, box queries, k-d trees (sweep and binned) and the
+hybrid index (csrc/svt.cu, csrc/kdtree.cu) against the reference's golden vectors and the
+CPU oracle: every array bit for bit, rows in the reference's DFS preorder."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import unpack_bits
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+KD_PARAMS = {
+    "kd-shallow": dict(mode="shallow"),
+    "kd-deep": dict(mode="deep"),
+    "kd-deep-mls8": dict(mode="deep", max_leaf_size=8),
+    "kd-deep-mls32": dict(mode="deep", max_leaf_size=32),
+    "kd-deep-mls128": dict(mode="deep", max_leaf_size=128),
+    "kd-binned-mls32": dict(mode="deep", max_leaf_size=32, builder="binned"),
+    "kd-binned": dict(mode="deep", builder="binned"),
+    "kd-binned-mls8": dict(mode="deep", max_leaf_size=8, builder="binned"),
+}
+
+
+@pytest.fixture(scope="module")
+def vs():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1912_09596_b200 as vs
+
+    return vs
+
+
+def _check_tree(t, want: dict, msg=""):
+    for f in ("lo", "hi", "axis", "plane", "left", "right"):
+        np.testing.assert_array_equal(getattr(t, f), want[f], err_msg=f"{msg}.{f}")
+    assert t.root == want["root"], msg
+    assert t.height() == want["height"], msg
+
+
+def _gold_tree(g, p):
+    return {f: g[f"{p}_{f}"] for f in ("lo", "hi", "axis", "plane", "left", "right")} | {
+        "root": int(g[f"{p}_root"]), "height": int(g[f"{p}_height"])}
+
+
+def _structures(vs, g, prefix, b):
+    g_svt = None
+    for key in g:
+        if key.startswith(prefix + "svt") and key[len(prefix) + 3:].isdigit():
+            bs = int(key[len(prefix) + 3:])
+            svt = vs.build_svt_grid(b, bs)
+            np.testing.assert_array_equal(svt.tables, g[key], err_msg=key)
+            if bs == 32:
+                g_svt = svt
+    svt = g_svt or vs.build_svt_grid(b, 32)
+    for name, kw in KD_PARAMS.items():
+        if prefix + name + "_lo" in g:
+            t = vs.build_kdtree(svt, vs.BuildParams(**kw))
+            _check_tree(t, _gold_tree(g, prefix + name), prefix + name)
+
+
+@pytest.mark.parametrize("tname", ["ramp03", "ramp06", "ramp00", "opaque", "band"])
+def test_blobs64(vs, blobs64, tname):
+    v = vs.Volume(blobs64["u8"])
+    b = vs.classify(v, vs.TransferFunction(blobs64[f"{tname}_lut"]), dilate=True)
+    _structures(vs, blobs64, f"{tname}_", b)
+
+
+@pytest.mark.parametrize("case", ["rand_64x48x40", "rand_20x17x9", "blocky48", "blocky_37x45x50",
+                                  "sparse64"])
+def test_bit_cases(vs, bitcases, case):
+    dims = tuple(int(d) for d in bitcases[f"{case}_dims"])
+    b = vs.BinaryVolume(unpack_bits(bitcases[f"{case}_bits"], dims))
+    _structures(vs, bitcases, f"{case}_", b)
+
+
+@pytest.mark.parametrize("scene", ["shell", "menger"])
+@pytest.mark.parametrize("tname", ["opaque", "ramp"])
+def test_scenes(vs, scenes, scene, tname):
+    v = vs.Volume(scenes[f"{scene}_u8"])
+    b = vs.classify(v, vs.TransferFunction(scenes[f"{scene}_{tname}_lut"]), dilate=True)
+    _structures(vs, scenes, f"{scene}_{tname}_", b)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("name", list(KD_PARAMS))
+def test_random_vs_oracle(vs, seed, name):
+    rng = np.random.default_rng(seed)
+    dims = tuple(int(d) for d in rng.integers(20, 70, size=3))
+    coarse = rng.random((dims[0] // 6 + 1, dims[1] // 6 + 1, dims[2] // 6 + 1)) < 0.15
+    bits = np.repeat(np.repeat(np.repeat(coarse, 6, 0), 6, 1), 6, 2)[:dims[0], :dims[1], :dims[2]]
+    bits = bits & (rng.random(dims) < 0.6)
+    b = vs.BinaryVolume(bits)
+    t = vs.build_kdtree(vs.build_svt_grid(b), vs.BuildParams(**KD_PARAMS[name]))
+    _check_tree(t, O.kd_build(bits, **KD_PARAMS[name]), name)
+
+
+def test_box_queries(vs, rng):
+    bits = rng.random((40, 33, 29)) < 0.01
+    b = vs.BinaryVolume(bits)
+    for bs in (8, 32):
+        g = vs.build_svt_grid(b, bs)
+        t = O.svt_build(bits, bs)
+        for _ in range(25):
+            lo = rng.integers(0, 30, size=3)
+            hi = lo + rng.integers(1, 20, size=3)
+            box = vs.Aabb(tuple(lo), tuple(hi))
+            assert vs.box_count(g, box) == O.box_count(t, bits.shape, bs, lo, hi)
+            got = vs.shrink_to_occupied(g, box)
+            want = O.shrink_svt(t, bits.shape, bs, lo, hi)
+            assert (got is None and want is None) or (got.lo, got.hi) == want
+
+
+def test_index_kinds_and_render(vs, blobs64):
+    """build_index for the table kinds == golden; frames through them == golden pixels."""
+    v = vs.Volume(blobs64["u8"])
+    tf = vs.TransferFunction(blobs64["ramp03_lut"])
+    b = vs.classify(v, tf, dilate=True)
+    cam = vs.Camera(eye=tuple(blobs64["cam_eye"]), direction=tuple(blobs64["cam_dir"]),
+                    up=tuple(blobs64["cam_up"]), extent=float(blobs64["cam_extent"]), width=96,
+                    height=64)
+    for kind in ("kd-shallow", "kd-deep-mls32", "kd-binned-mls32", "hybrid"):
+        idx = vs.build_index(kind, b)
+        tree = idx.tree if kind == "hybrid" else idx
+        _check_tree(tree, _gold_tree(blobs64, "ramp03_" + ("kd-shallow" if kind == "hybrid" else kind)), kind)
+        st = vs.report_stats(idx)
+        assert st == {"node_count": tree.node_count, "height": tree.height()}
+        rgba, samples = vs.render_float(v, tf, idx, cam)
+        np.testing.assert_array_equal(samples, blobs64[f"ramp03_render_{kind}_samples"])
+        np.testing.assert_array_equal(rgba, blobs64[f"ramp03_render_{kind}_rgba"])
+
+
+def test_empty_and_dense(vs):
+    z = vs.BinaryVolume(np.zeros((16, 16, 16), bool))
+    t = vs.build_kdtree(vs.build_svt_grid(z))
+    assert t.node_count == 0 and t.root == -1 and t.height() == 0
+    d = vs.BinaryVolume(np.ones((24, 24, 24), bool))  # test_acceptance.py:116-124
+    t = vs.build_kdtree(vs.build_svt_grid(d), vs.BuildParams(mode="deep"))
+    assert t.node_count == 1 and t.height() == 1
