@@ -170,6 +170,10 @@ typedef struct vs_index_desc {
   const int32_t* plane;
   const int8_t* axis;
   const int* lbvh_info;
+  /* lbvh: optional C-order bit grid of the leaf bricks (nbx,nby,nbz) with edge bs; when set,
+   * the leaves are enumerated by a brick DDA instead of the tree walk (same intervals). */
+  const uint32_t* brick_bits;
+  int nbx, nby, nbz, bs;
 } vs_index_desc;
 
 /* Orthographic camera with the host-normalised frame of Camera.ray_origins (render.py:134-149):
@@ -197,6 +201,10 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
               const vs_rows_desc* rows_opt, uint8_t* rgba8, double* rgba64_opt,
               int32_t* samples_opt, unsigned long long* total_opt, int* flags,
               vs_stream_t stream);
+
+/* Leaf-brick bit grid of an LBVH from its brick_coords (n from n_dev, or cap if NULL). */
+int vs_lbvh_brick_grid(const int32_t* brick_coords, const int* n_dev, int64_t cap, int nbx,
+                       int nby, int nbz, uint32_t* bits, vs_stream_t stream);
 
 /* traverse_* (render.py:928-961) for a batch of rays: out (nrays, cap, 2) merged intervals,
  * counts[q] = total intervals of ray q (may exceed cap; then out holds the first cap). */

@@ -258,6 +258,77 @@ __device__ void dda_runs(const Ray& r, const vs_index_desc& ix, double t_in, dou
   if (open_run) out.push(run_t0, t_out);
 }
 
+// LBVH leaf intervals without walking the tree.  A leaf's interval is reported by _k_bvh
+// iff its own slab interval clipped to [tmin, tmax] is non-empty (ancestor boxes contain it
+// and slab intervals are monotone in the box bounds, in floating point too), so the merged
+// union equals the merged union of every occupied brick's clipped slab interval.  A 3-D DDA
+// over the brick grid visits exactly the bricks whose interval along the ray is non-empty,
+// in increasing t: its per-axis crossings are the same expressions slab() evaluates for a
+// brick's faces, and simultaneous crossings skip only bricks touched in a single point.  The
+// start brick is the one whose per-axis crossing window contains tmin.  Each occupied brick
+// then gets the reference's exact clipped slab interval (box hi clipped to dims).
+template <class Out>
+__device__ void brick_dda(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz,
+                          double tmin, double tmax, Out& out) {
+  const int bs = ix.bs;
+  const double cs = (double)bs;
+  const int nb[3] = {ix.nbx, ix.nby, ix.nbz};
+  const int dims[3] = {nx, ny, nz};
+  const double o[3] = {r.ox, r.oy, r.oz}, d[3] = {r.dx, r.dy, r.dz}, inv[3] = {r.ix, r.iy, r.iz};
+  const bool zero[3] = {r.zx, r.zy, r.zz};
+  int c[3], s[3];
+  double tn[3];
+  for (int a = 0; a < 3; ++a) {
+    s[a] = zero[a] ? 0 : (inv[a] > 0.0 ? 1 : -1);
+    const double p = __dadd_rn(o[a], __dmul_rn(tmin, d[a]));
+    int ca = (int)floor(__ddiv_rn(p, cs));
+    ca = ca < 0 ? 0 : (ca > nb[a] - 1 ? nb[a] - 1 : ca);
+    auto plane_t = [&](int k) { return __dmul_rn((double)(k * bs) - o[a], inv[a]); };
+    if (s[a] > 0) {
+      while (ca > 0 && plane_t(ca) > tmin) --ca;
+      while (ca + 1 < nb[a] && plane_t(ca + 1) <= tmin) ++ca;
+      tn[a] = plane_t(ca + 1);
+    } else if (s[a] < 0) {
+      while (ca + 1 < nb[a] && plane_t(ca + 1) > tmin) ++ca;
+      while (ca > 0 && plane_t(ca) <= tmin) --ca;
+      tn[a] = plane_t(ca);
+    } else {
+      ca = (int)floor(__ddiv_rn(o[a], cs));
+      if (ca < 0 || ca >= nb[a]) return;
+      tn[a] = R_FAR;
+    }
+    c[a] = ca;
+  }
+  const uint32_t* __restrict__ bits = ix.brick_bits;
+  const int64_t maxsteps = (int64_t)nb[0] + nb[1] + nb[2] + 3;
+  for (int64_t step = 0; step < maxsteps; ++step) {
+    const int64_t lin = ((int64_t)c[0] * nb[1] + c[1]) * nb[2] + c[2];
+    if ((__ldg(bits + (lin >> 5)) >> (lin & 31)) & 1u) {
+      double a, b;
+      const int l0 = c[0] * bs, l1 = c[1] * bs, l2 = c[2] * bs;
+      if (slab(r, (double)l0, (double)l1, (double)l2, (double)min(l0 + bs, dims[0]),
+               (double)min(l1 + bs, dims[1]), (double)min(l2 + bs, dims[2]), a, b)) {
+        a = a > tmin ? a : tmin;
+        b = b < tmax ? b : tmax;
+        if (b > a) out.push(a, b);
+      }
+    }
+    double t = tn[0];
+    if (tn[1] < t) t = tn[1];
+    if (tn[2] < t) t = tn[2];
+    if (t >= tmax) break;
+    bool outside = false;
+    for (int a2 = 0; a2 < 3; ++a2) {
+      if (tn[a2] == t) {
+        c[a2] += s[a2];
+        if (c[a2] < 0 || c[a2] >= nb[a2]) outside = true;
+        tn[a2] = __dmul_rn((double)((c[a2] + (s[a2] > 0)) * bs) - o[a2], inv[a2]);
+      }
+    }
+    if (outside) break;
+  }
+}
+
 // _k_bvh leaf intervals, near-first DFS; the stack holds node ids (a popped node's clipped
 // interval is recomputed: same inputs, same doubles).
 template <class Out>
@@ -386,7 +457,11 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
         dda_runs(r, ix, tmin, tmax, m);
       } else if (KIND == VS_KIND_LBVH) {
         const int n = ix.lbvh_info ? __ldg(ix.lbvh_info) : ix.root + 1;
-        bvh_leaves(r, ix, n > 0 ? 0 : -1, tmin, tmax, m, &flags);
+        if (ix.brick_bits) {
+          if (n > 0) brick_dda(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax, m);
+        } else {
+          bvh_leaves(r, ix, n > 0 ? 0 : -1, tmin, tmax, m, &flags);
+        }
       } else if (KIND == VS_KIND_KD) {
         kd_leaves(r, ix, ix.root, tmin, tmax, m, &flags);
       } else {
@@ -453,7 +528,11 @@ __global__ void k_traverse_rays(vs_index_desc ix, int nx, int ny, int nz,
       case VS_KIND_GRID: dda_runs(r, ix, tmin, tmax, m); break;
       case VS_KIND_LBVH: {
         const int n = ix.lbvh_info ? ix.lbvh_info[0] : ix.root + 1;
-        bvh_leaves(r, ix, n > 0 ? 0 : -1, tmin, tmax, m, &flags);
+        if (ix.brick_bits) {
+          if (n > 0) brick_dda(r, ix, nx, ny, nz, tmin, tmax, m);
+        } else {
+          bvh_leaves(r, ix, n > 0 ? 0 : -1, tmin, tmax, m, &flags);
+        }
         break;
       }
       case VS_KIND_KD: kd_leaves(r, ix, ix.root, tmin, tmax, m, &flags); break;
@@ -508,6 +587,15 @@ __global__ void k_integrate_rays(vs_volume_desc vol, const double* __restrict__ 
   rgba[4 * q + 2] = I.accb;
   rgba[4 * q + 3] = I.acca;
   samples[q] = I.taken;
+}
+
+__global__ void k_brick_grid(const int32_t* __restrict__ coords, const int* __restrict__ n_dev,
+                             int64_t n_host, int nby, int nbz, uint32_t* __restrict__ bits) {
+  const int64_t n = n_dev ? (int64_t)*n_dev : n_host;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t lin = ((int64_t)coords[3 * i] * nby + coords[3 * i + 1]) * nbz + coords[3 * i + 2];
+  atomicOr(bits + (lin >> 5), 1u << (lin & 31));
 }
 
 template <int K>
@@ -580,6 +668,18 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
       return fail_arg("vs_render: kind");
   }
   return check_launch("k_render");
+}
+
+int vs_lbvh_brick_grid(const int32_t* brick_coords, const int* n_dev, int64_t cap, int nbx,
+                       int nby, int nbz, uint32_t* bits, vs_stream_t stream) {
+  if (!brick_coords || !bits || nbx < 1 || nby < 1 || nbz < 1 || cap < 0)
+    return fail_arg("vs_lbvh_brick_grid");
+  const int64_t nwords = ((int64_t)nbx * nby * nbz + 31) / 32;
+  VS_CUDA(cudaMemsetAsync(bits, 0, nwords * 4, S(stream)), "memset brick grid");
+  if (cap == 0) return 0;
+  k_brick_grid<<<(unsigned)cdiv(cap, 256), 256, 0, S(stream)>>>(brick_coords, n_dev, cap, nby,
+                                                                 nbz, bits);
+  return check_launch("k_brick_grid");
 }
 
 int vs_traverse_rays(const vs_index_desc* ix, int nx, int ny, int nz, const double* origins,

@@ -200,6 +200,22 @@ class Lbvh:
     def is_leaf(self, i: int) -> bool:
         return self.left[i] < 0
 
+    def brick_grid_dims(self):
+        return tuple(-(-d // self.brick_size) for d in self.dims)
+
+    def brick_grid(self) -> torch.Tensor:
+        """C-order bit grid of the leaf bricks (renderer's brick DDA), built on first use."""
+        g = self.__dict__.get("_brick_grid")
+        if g is None:
+            nb = self.brick_grid_dims()
+            words = (nb[0] * nb[1] * nb[2] + 31) // 32
+            g = torch.empty(max(words, 1), dtype=torch.int32, device=self.info.device)
+            cap = self.dev["brick_coords"].shape[0]
+            call("vs_lbvh_brick_grid", ptr(self.dev["brick_coords"]), ptr(self.info), cap, *nb,
+                 ptr(g), stream())
+            self.__dict__["_brick_grid"] = g
+        return g
+
 
 def empty_lbvh(brick_size: int, dims) -> Lbvh:
     dev = _lib.device()

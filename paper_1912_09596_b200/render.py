@@ -149,7 +149,9 @@ class IndexDesc(C.Structure):
     _fields_ = [("kind", C.c_int), ("root", C.c_int), ("occ", C.c_void_p), ("ncx", C.c_int),
                 ("ncy", C.c_int), ("ncz", C.c_int), ("cs", C.c_int), ("lo", C.c_void_p),
                 ("hi", C.c_void_p), ("left", C.c_void_p), ("right", C.c_void_p),
-                ("plane", C.c_void_p), ("axis", C.c_void_p), ("lbvh_info", C.c_void_p)]
+                ("plane", C.c_void_p), ("axis", C.c_void_p), ("lbvh_info", C.c_void_p),
+                ("brick_bits", C.c_void_p), ("nbx", C.c_int), ("nby", C.c_int), ("nbz", C.c_int),
+                ("bs", C.c_int)]
 
 
 class CameraDesc(C.Structure):
@@ -178,7 +180,7 @@ def camera_desc(cam: Camera) -> CameraDesc:
     return c
 
 
-def index_desc(index) -> IndexDesc:
+def index_desc(index, use_brick_dda: bool = True) -> IndexDesc:
     """Descriptor + the tensors it points at (keep them alive for the launch)."""
     kind = index_kind(index)
     d = IndexDesc()
@@ -194,6 +196,10 @@ def index_desc(index) -> IndexDesc:
         d.lo, d.hi = ptr(t.dev["lo"]), ptr(t.dev["hi"])
         d.left, d.right = ptr(t.dev["left"]), ptr(t.dev["right"])
         d.lbvh_info = ptr(t.info)
+        if use_brick_dda:
+            d.brick_bits = ptr(t.brick_grid())
+            d.nbx, d.nby, d.nbz = t.brick_grid_dims()
+            d.bs = t.brick_size
     if kind in ("kd", "hybrid"):
         t = index if kind == "kd" else index.tree
         dv = t.device_arrays()

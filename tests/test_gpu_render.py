@@ -192,3 +192,33 @@ def test_render_errors(vs, blobs64):
     assert fr.pixels.max() == 0 and fr.sample_count > 0
     lb = vs.build_index("lbvh", vs.classify(v, empty, dilate=True))
     assert vs.render_frame(v, empty, lb, cam).sample_count == 0
+
+
+@pytest.mark.parametrize("az,el", [(30.0, 15.0), (0.0, 0.0), (90.0, 0.0), (200.0, -35.0),
+                                   (45.0, 45.0)])
+def test_lbvh_brick_dda_equals_tree_walk(vs, az, el):
+    """The brick-DDA leaf enumeration and the reference's tree walk give identical frames,
+    on a volume whose dims are not brick multiples (clipped border bricks)."""
+    from paper_1912_09596_b200.render import RenderTarget, index_desc, render_rows
+
+    rng = np.random.default_rng(7)
+    dims = (45, 38, 52)
+    coarse = rng.integers(0, 256, size=(10, 10, 11), dtype=np.uint8)
+    u8 = np.repeat(np.repeat(np.repeat(coarse, 5, 0), 4, 1), 5, 2)[:dims[0], :dims[1], :dims[2]].copy()
+    v = vs.Volume(u8)
+    tf = vs.TransferFunction.ramp(0.7)
+    idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
+    cam = vs.Camera.orbit(dims, az, el, width=57, height=43)
+    outs = []
+    for dda in (False, True):
+        tgt = RenderTarget(cam.width, cam.height, want_rgba64=True, want_samples=True)
+        render_rows(v, tf, idx, cam, tgt, idx_desc=index_desc(idx, use_brick_dda=dda))
+        outs.append((tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy(), int(tgt.flags.item())))
+    assert outs[0][2] == 0 and outs[1][2] == 0
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    lb = {"lo": idx.lo, "hi": idx.hi, "left": idx.left, "right": idx.right, "root": idx.root,
+          "height": idx.height()}
+    orgba, osamples = O.render("lbvh", u8, tf.lut, lb, cam, nthreads=4)
+    np.testing.assert_array_equal(outs[1][1], osamples)
+    np.testing.assert_array_equal(outs[1][0], orgba)
