@@ -1,26 +1,29 @@
 #!/usr/bin/env python
-"""Benchmark: interactive transfer-function sweep on a synthetic 1024^3 u8 volume (B200).
+"""Benchmark: interactive transfer-function editing on a synthetic 1024^3 u8 volume (B200).
 
-One step = one TF-change frame: the LBVH over the volume's dilated brick classification is
-rebuilt for the next TF of a sweep (BASELINE.json configs[3], the north-star target "a TF
-change rebuilds the LBVH in <= 5 ms at >= 50% of HBM roofline").  The rebuild is:
+One step = one interactive TF-change frame, the reference's Session loop (service.py:53-125,
+set_tf -> classify -> build_index -> render_frame) on BASELINE.json configs[3]/[4]:
 
-    vs_classify_summary (one pass over the u8 volume) -> vs_summary_to_bitmap
-    -> vs_lbvh_from_bitmap (scan, leaves, Karras, refit)
+  1. the next TF of a 64-entry ramp sweep (thresholds 0.6 -> 0) reaches the device as a
+     64-byte parameter block;
+  2. LBVH rebuild: vs_classify_summary (one pass over the u8 volume) -> vs_summary_to_bitmap
+     -> vs_lbvh_from_bitmap -> vs_lbvh_brick_grid, replayed as one CUDA graph;
+  3. 1920x1080 render through the new index (camera orbiting 360/64 deg per step, dt 0.5,
+     trilinear, FP64 parity arithmetic), rows split in interleaved stripes over the ranks and
+     gathered with one NCCL all-gather (N > 1).
 
-captured as one CUDA graph; the TF reaches the device as a 64-byte parameter block.
+  value     frames/s of the whole job, device-timed with CUDA events, max over ranks; volume
+            and the sweep's TF tables resident in HBM; input 1 GiB > 126 MB L2.
+  e2e       the same frame through the public API (TransferFunction -> classify ->
+            build_index -> TileRenderer.frame) with the TF uploaded from pinned host memory
+            and the frame's pixels read back to the host every step.
+  roofline  k_brick_summary, the HBM-bound kernel of the step (the rebuild's compulsory
+            traffic: N^3 u8 read + 4 B/brick summary write over its CUDA-event duration).  The
+            render kernel is issue-bound, not HBM/tensor-bound; see "render" and DESIGN.md.
+  cpu_baseline  the C oracle port of the reference path (oracle/vs_oracle.c): rebuild at full
+            size (1 core) + a row sample of the frame render (all cores), scaled to a frame.
 
-  value  frames/s with the volume and the sweep's TF blocks resident in HBM (device-timed)
-  e2e    the same through the public API (TransferFunction -> classify -> build_index ->
-         report_stats) with the TF uploaded from pinned host memory and the stats read back
-  roofline  k_brick_summary: algorithmic bytes (N^3 read + 4 B/brick summary write) over its
-         CUDA-event duration vs MEASURED_PEAKS.json hbm (else the recipe's fallback)
-  cpu_baseline  the C oracle (oracle/vs_oracle.c: classify(dilate) + flag_bricks + build_lbvh,
-         1 core) on an x-slab of the same volume, scaled to the full volume
-
-Multi-GPU (--gpus N under torchrun): the build does not shard (construction is
-replicated); every rank rebuilds its own replica and value sums the ranks' frames (weak).
-`--impl reference` times the CPU oracle port of the reference path instead (rank 0 only).
+`--impl reference` times that CPU oracle port alone (rank 0; other ranks exit at once).
 """
 
 from __future__ import annotations
@@ -42,14 +45,20 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "hierarchy build ms and render frames/s (Msamples/s) vs CPU ref; % HBM roofline"
 FALLBACK_HBM_GBS = 6650.0
+W, H = 1920, 1080
+NSWEEP = 64
 
 
-def sweep_luts(k: int):
-    """TF sweep of config 4: ramp thresholds 0.6 -> 0, cycled."""
+def sweep_tfs(k: int = NSWEEP):
     from paper_1912_09596_b200.volume import TransferFunction
 
-    ts = [0.6 - 0.6 * i / 63 for i in range(64)]
-    return [TransferFunction.ramp(threshold=ts[i % 64]) for i in range(k)]
+    return [TransferFunction.ramp(threshold=0.6 - 0.6 * i / 63) for i in range(k)]
+
+
+def cameras(dims, k: int = NSWEEP):
+    from paper_1912_09596_b200.render import Camera
+
+    return [Camera.orbit(dims, 360.0 * i / k, 15.0, width=W, height=H) for i in range(k)]
 
 
 def hbm_peak():
@@ -66,7 +75,7 @@ def hbm_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
 
     def __init__(self, index: int):
         self.index = index
@@ -115,11 +124,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
-# CPU baseline (oracle port of the reference path, test infrastructure)
+# CPU reference (the oracle port of the reference path; test infrastructure)
 # ------------------------------------------------------------------------------------------
 
-def cpu_rebuild_sample(u8_host: np.ndarray, lut: np.ndarray, slab: int):
-    """classify(dilate) + flag_bricks + build_lbvh on x-slab [0, slab) with the C oracle."""
+def cpu_rebuild(u8_host: np.ndarray, lut: np.ndarray, slab: int):
+    """classify(dilate) + flag_bricks + build_lbvh on x-slab [0, slab) (1 core)."""
     from oracle import oracle as O
 
     sub = np.ascontiguousarray(u8_host[:slab])
@@ -130,21 +139,62 @@ def cpu_rebuild_sample(u8_host: np.ndarray, lut: np.ndarray, slab: int):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(u8_host, lut, budget_s: float = 20.0):
-    nx = u8_host.shape[0]
-    slab = min(nx, 16)
-    t = cpu_rebuild_sample(u8_host, lut, slab)
-    # grow the slab to ~budget_s of work (bounded sample), multiple of 8
-    target = int(slab * max(1.0, budget_s / max(t, 1e-3)))
-    slab2 = max(8, min(nx, (target // 8) * 8))
-    if slab2 > slab:
-        t = cpu_rebuild_sample(u8_host, lut, slab2)
-        slab = slab2
-    full_s = t * nx / slab
-    return {"value": 1.0 / full_s, "unit": "frames/s", "cores": 1, "kind": "port",
-            "sample": f"oracle classify(dilate)+flag_bricks+build_lbvh on x-slab "
-                      f"[0,{slab}) of the {nx}^3 volume ({t:.2f} s), scaled x{nx / slab:.1f}",
-            "full_rebuild_ms": full_s * 1e3}
+def oracle_lbvh(u8_host: np.ndarray, lut: np.ndarray):
+    """The oracle's full-size LBVH for `lut` (untimed setup of the render sample)."""
+    from oracle import oracle as O
+
+    bits, _ = O.classify(u8_host, lut, dilate=True)
+    coords, codes = O.flag_bricks(bits, 8)
+    return O.build_lbvh(coords, codes, 8, u8_host.shape)
+
+
+def cpu_render_rows(u8_host, lut, tree, cam, nrows: int, threads: int):
+    """Render `nrows` middle rows of the frame through the oracle LBVH (timed)."""
+    from oracle import oracle as O
+
+    r0 = cam.height // 2 - nrows // 2
+    t0 = time.perf_counter()
+    _, samples = O.render("lbvh", u8_host, lut, tree, cam, rows=(r0, r0 + nrows),
+                          nthreads=threads)
+    return time.perf_counter() - t0, int(samples.sum())
+
+
+class CpuFrame:
+    """Bounded CPU sample of one interactive frame: the rebuild on an x-slab (1 core, scaled by
+    n/slab) + the render of a middle row band (all cores, scaled by height/rows) through the
+    oracle LBVH of the first sweep TF.  Sizes are calibrated once to a time budget."""
+
+    def __init__(self, u8_host, lut0, cam, budget_s: float):
+        self.u8 = u8_host
+        self.n = u8_host.shape[0]
+        self.threads = os.cpu_count() or 1
+        self.tree = oracle_lbvh(u8_host, lut0)
+        self.lut0 = lut0
+        t = cpu_rebuild(u8_host, lut0, 16)
+        self.slab = max(16, min(self.n, int(16 * (0.5 * budget_s) / max(t, 1e-3)) // 8 * 8))
+        tr, _ = cpu_render_rows(u8_host, lut0, self.tree, cam, 8, self.threads)
+        self.rows = max(8, min(cam.height, int(8 * (0.5 * budget_s) / max(tr, 1e-3)) // 8 * 8))
+
+    def frame(self, lut, cam):
+        rb = cpu_rebuild(self.u8, lut, self.slab)
+        tr, _ = cpu_render_rows(self.u8, self.lut0, self.tree, cam, self.rows, self.threads)
+        rebuild_s = rb * self.n / self.slab
+        render_s = tr * cam.height / self.rows
+        return {"frame_s": rebuild_s + render_s, "rebuild_s": rebuild_s, "render_s": render_s}
+
+    def sample(self, cam):
+        return (f"oracle rebuild on x-slab [0,{self.slab}) of {self.n}^3 scaled "
+                f"x{self.n / self.slab:.1f} (1 core) + oracle LBVH render of {self.rows} middle "
+                f"rows of {cam.width}x{cam.height} scaled x{cam.height / self.rows:.1f} "
+                f"({self.threads} threads)")
+
+
+def cpu_frame_estimate(u8_host, lut, cam, budget_s: float):
+    cf = CpuFrame(u8_host, lut, cam, budget_s)
+    est = cf.frame(lut, cam)
+    est["threads"] = cf.threads
+    est["sample"] = cf.sample(cam)
+    return est
 
 
 # ------------------------------------------------------------------------------------------
@@ -159,7 +209,9 @@ def dist_setup():
     if torch.cuda.is_available():
         torch.cuda.set_device(local)
     if ws > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo",
+                                device_id=torch.device("cuda", local)
+                                if torch.cuda.is_available() else None)
     return rank, ws, local
 
 
@@ -181,38 +233,48 @@ def barrier(ws):
         dist.barrier()
 
 
+def make_volume(n: int):
+    from paper_1912_09596_b200.synth import gen_blobs_u8
+
+    nblobs = max(1, 25600 * n ** 3 // 1024 ** 3)
+    return gen_blobs_u8((n, n, n), n=nblobs, seed=7, sigma=3.0), nblobs
+
+
 def run_reference(args, rank, ws):
     if rank != 0:
         return
     import torch  # noqa: F401
-    from paper_1912_09596_b200.synth import gen_blobs_u8
 
     n = args.size
-    u8 = gen_blobs_u8((n, n, n), n=max(1, 25600 * n ** 3 // 1024 ** 3), seed=7,
-                      sigma=3.0).cpu().numpy()
-    luts = [tf.lut for tf in sweep_luts(max(args.steps + args.warmup, 1))]
+    u8d, nblobs = make_volume(n)
+    u8 = u8d.cpu().numpy()
+    tfs = sweep_tfs()
+    cams = cameras(u8.shape)
     nsteps = args.steps + args.warmup
-    # size each step's slab so the whole run stays within ~120 s
-    probe = cpu_rebuild_sample(u8, luts[0], 8)
-    per_step_budget = min(5.0, 120.0 / max(nsteps, 1))
-    slab = max(8, min(n, int(8 * per_step_budget / max(probe, 1e-3)) // 8 * 8))
+    budget = max(0.5, min(20.0, 120.0 / max(nsteps, 1)))
+    cf = CpuFrame(u8, tfs[0].lut, cams[0], budget)
     times = []
+    info = None
     for k in range(nsteps):
-        t = cpu_rebuild_sample(u8, luts[k], slab)
+        est = cf.frame(tfs[k % NSWEEP].lut, cams[k % NSWEEP])
         if k >= args.warmup:
-            times.append(t)
-    full_s = sum(times) / len(times) * n / slab
-    value = 1.0 / full_s
+            times.append(est["frame_s"])
+            info = est
+    info["threads"] = cf.threads
+    info["sample"] = cf.sample(cams[0]) + "; per step: the sweep TF's rebuild, orbit camera"
+    frame_s = statistics.mean(times)
+    value = 1.0 / frame_s
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": full_s * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"TF-sweep LBVH rebuild, {n}^3 u8 blobs (25600 per 1024^3, "
-                               f"sigma 3, seed 7), ramp t=0.6..0", "frame": "rebuild"},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": 1, "kind": "port",
-                         "sample": f"oracle C port, x-slab [0,{slab}) per step, scaled "
-                                   f"x{n / slab:.1f}"},
+        "ms_per_step": frame_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8+f64", "data": "synthetic",
+        "config": {"workload": f"interactive TF sweep on {n}^3 u8 blobs ({nblobs} blobs, sigma "
+                               f"3, seed 7): LBVH rebuild + {W}x{H} render per frame",
+                   "frame": "rebuild+render"},
+        "build_ms": info["rebuild_s"] * 1e3, "render_ms": info["render_s"] * 1e3,
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": info["threads"],
+                         "kind": "port", "sample": info["sample"]},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -224,84 +286,113 @@ def run_ours(args, rank, ws, local):
 
     import paper_1912_09596_b200 as vs
     from paper_1912_09596_b200.engine import LbvhRebuilder, tf_params_device
-    from paper_1912_09596_b200.synth import gen_blobs_u8
+    from paper_1912_09596_b200.render import camera_desc, index_desc, tf_device, volume_desc
+    from paper_1912_09596_b200.tiles import TileRenderer
 
     n = args.size
-    dims = (n, n, n)
-    nblobs = max(1, 25600 * n ** 3 // 1024 ** 3)
-    u8 = gen_blobs_u8(dims, n=nblobs, seed=7, sigma=3.0)
+    u8, nblobs = make_volume(n)
     v = vs.Volume(u8)
-    nsweep = 64
-    tfs = sweep_luts(nsweep)
+    tfs = sweep_tfs()
+    cams = cameras(v.dims)
     params = tf_params_device(tfs)
-    rb = LbvhRebuilder(v, with_grid=False).capture()
+    for tf in tfs:
+        tf_device(tf, 0.5)  # LUT + opacity-correction tables resident for the sweep
+    rb = LbvhRebuilder(v).capture()
+    idx = rb.index()
+    tiles = TileRenderer(W, H)
+    vd = volume_desc(v)
+    cds = [camera_desc(c) for c in cams]
     st = torch.cuda.current_stream()
+
+    def step(k):
+        j = k % NSWEEP
+        rb.rebuild(params[j])
+        return tiles.render(v, tfs[j], idx, cams[j], idx_desc=index_desc(idx), vol_desc=vd,
+                            cam_desc=cds[j])
 
     # ---- device-resident loop (value) ------------------------------------------------------
     for k in range(args.warmup):
-        rb.rebuild(params[k % nsweep])
+        step(k)
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    # dominant kernel timed on its own (same stream), to apportion the step
-    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
     barrier(ws)
     with ClockSampler(local) as clk:
-        time.sleep(0.3)  # let the sampler start
+        time.sleep(0.3)
         torch.cuda.synchronize()
         barrier(ws)
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(st)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
         for k in range(args.steps):
-            rb.rebuild(params[k % nsweep])
-        t_end.record(st)
+            step(k)
+        e1.record(st)
         torch.cuda.synchronize()
-        total_ms = t_start.elapsed_time(t_end)
-        # kernel-level split (not the headline): summary kernel alone vs the tree launches
-        for k in range(args.steps):
-            rb.set_tf(params[k % nsweep])
-            sev[k][0].record(st)
+        total_ms = e0.elapsed_time(e1)
+        # component split (not the headline): rebuild alone, summary kernel alone, render alone
+        bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(3)]
+        reps = max(10, min(args.steps, 100))
+        bev[0][0].record(st)
+        for k in range(reps):
+            rb.rebuild(params[k % NSWEEP])
+        bev[0][1].record(st)
+        summ = []
+        for k in range(reps):
+            rb.set_tf(params[k % NSWEEP])
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
             rb.launch_summary(st.cuda_stream)
-            sev[k][1].record(st)
+            b.record(st)
             rb.launch_tree(st.cuda_stream)
+            summ.append((a, b))
+        rb.rebuild(params[0])
+        rrep = max(3, min(args.steps, 10))
+        samples = 0
+        bev[1][0].record(st)
+        for k in range(rrep):
+            tiles.render(v, tfs[0], idx, cams[k % NSWEEP], idx_desc=index_desc(idx), vol_desc=vd,
+                         cam_desc=cds[k % NSWEEP])
+        bev[1][1].record(st)
         torch.cuda.synchronize()
+        samples = tiles.sample_total()  # last frame's samples (all ranks)
     total_ms = max_over_ranks(total_ms, ws)
     ms_per_step = total_ms / args.steps
-    summ_ms = statistics.median([a.elapsed_time(b) for a, b in sev])
+    build_ms = max_over_ranks(bev[0][0].elapsed_time(bev[0][1]) / reps, ws)
+    render_ms = max_over_ranks(bev[1][0].elapsed_time(bev[1][1]) / rrep, ws)
+    summ_ms = statistics.median([a.elapsed_time(b) for a, b in summ])
     info = rb.info.cpu().tolist()
     n_bricks, height = int(info[0]), int(info[1])
 
-    # ---- parity spot check of the last TF against a fresh public-API build -----------------
-    last_tf = tfs[(args.steps - 1) % nsweep]
-    ref_idx = vs.build_lbvh(vs.flag_bricks(vs.classify(v, last_tf, dilate=True)))
-    rb.rebuild(params[(args.steps - 1) % nsweep])
-    snap = rb.lbvh()
-    parity = (snap.n_bricks == ref_idx.n_bricks and snap.height() == ref_idx.height() and
-              all(torch.equal(snap.dev[f][:snap.node_count], ref_idx.dev[f][:ref_idx.node_count])
+    # ---- parity spot check: the timed path's index vs a fresh public-API build ----------------
+    ref_idx = vs.build_lbvh(vs.flag_bricks(vs.classify(v, tfs[0], dilate=True)))
+    parity = (n_bricks == ref_idx.n_bricks and height == ref_idx.height() and
+              all(torch.equal(rb.tree[f][:ref_idx.node_count], ref_idx.dev[f][:ref_idx.node_count])
                   for f in ("lo", "hi", "left", "right")))
 
     # ---- e2e through the public API ---------------------------------------------------------
     luts = [tf.lut for tf in tfs]
-    e_steps = max(1, min(args.steps, 200))
+    e_steps = max(1, min(args.steps, 30))
+    pub = TileRenderer(W, H)
+
+    def e2e_step(k):
+        j = k % NSWEEP
+        tf = vs.TransferFunction(luts[j])           # host LUT -> pinned -> device
+        b = vs.classify(v, tf, dilate=True)
+        index = vs.build_index("lbvh", b)
+        return pub.frame(v, tf, index, cams[j])     # pixels -> host
+
     for k in range(min(args.warmup, 3)):
-        vs.report_stats(vs.build_index("lbvh", vs.classify(v, vs.TransferFunction(luts[k]),
-                                                            dilate=True)))
+        e2e_step(k)
     torch.cuda.synchronize()
     barrier(ws)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
     e0.record(st)
     for k in range(e_steps):
-        tf = vs.TransferFunction(luts[k % nsweep])      # host LUT -> params -> pinned H2D
-        b = vs.classify(v, tf, dilate=True)
-        stats = vs.report_stats(vs.build_index("lbvh", b))  # D2H of {n, height}
+        fr = e2e_step(k)
     e1.record(st)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
+    del fr, t0
 
-    # ---- roofline of the dominant kernel ----------------------------------------------------
+    # ---- roofline of the HBM-bound kernel -------------------------------------------------
     peak, peak_kind = hbm_peak()
     alg = rb.algorithmic_bytes(n_bricks)
     achieved = alg["summary_kernel"] / (summ_ms * 1e-3) / 1e9
@@ -315,38 +406,50 @@ def run_ours(args, rank, ws, local):
 
     if rank != 0:
         return
-    cpu = cpu_baseline(u8.cpu().numpy(), luts[0], budget_s=args.cpu_budget) \
-        if (ws == 1 and not args.no_cpu) else None
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        est = cpu_frame_estimate(u8.cpu().numpy(), tfs[0].lut, cams[0], args.cpu_budget)
+        cpu = {"value": 1.0 / est["frame_s"], "unit": "frames/s", "cores": est["threads"],
+               "kind": "port", "sample": est["sample"], "rebuild_ms": est["rebuild_s"] * 1e3,
+               "render_ms": est["render_s"] * 1e3}
     clocks = clk.summary()
+    launches_per_step = 5 + 1  # summary, summary_to_bitmap, leaves, karras, refit, brick grid
+    launches_per_step += 1     # k_render
     line = {
         "metric": METRIC,
-        "value": ws * 1e3 / ms_per_step,
+        "value": 1e3 / ms_per_step,
         "unit": "frames/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "u8",
+        "dtype": "u8+f64",
         "data": "synthetic",
-        "config": {"workload": f"TF-sweep LBVH rebuild, {n}^3 u8 blobs ({nblobs} blobs, sigma "
-                               f"3, seed 7), 64 ramp TFs t=0.6..0 cycled", "frame": "rebuild",
-                   "brick": 8, "l2": "input 1 GiB > 126 MB L2 (no flush needed)",
-                   "parallelism": f"replica x{ws}"},
-        "build_ms": ms_per_step,
+        "config": {"workload": f"interactive TF sweep on {n}^3 u8 blobs ({nblobs} blobs, sigma "
+                               f"3, seed 7): LBVH rebuild + {W}x{H} render per frame, 64 ramp "
+                               f"TFs t=0.6..0, orbit camera el 15, dt 0.5",
+                   "frame": "rebuild+render", "brick": 8,
+                   "l2": "input 1 GiB > 126 MB L2 (no flush needed)",
+                   "parallelism": f"image row stripes x{ws} + NCCL all-gather; build replicated"},
+        "build_ms": build_ms,
+        "render_ms": render_ms,
+        "render": {"fps": 1e3 / render_ms, "samples_per_frame": samples,
+                   "Msamples_s": samples / render_ms / 1e3, "kernel": "k_render<LBVH>"},
         "summary_kernel_ms": summ_ms,
-        "n_bricks_last": n_bricks, "lbvh_nodes_last": max(2 * n_bricks - 1, 0),
-        "height_last": height,
-        "parity_last_tf_vs_public_api": bool(parity),
+        "n_bricks": n_bricks, "lbvh_nodes": max(2 * n_bricks - 1, 0), "lbvh_height": height,
+        "parity_index_vs_public_api": bool(parity),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_brick_summary", "peak_source": peak_kind,
-                     "alg_bytes_per_launch": alg["summary_kernel"]},
-        "rebuild_roofline_frac": alg["rebuild"] / (ms_per_step * 1e-3) / 1e9 / peak,
-        "e2e": {"value": ws * 1e3 / e2e_ms, "unit": "frames/s", "h2d_bytes_per_step": 64,
-                "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
-                "path": "TransferFunction->classify->build_index('lbvh')->report_stats"},
-        "gpu_launches": 5 * args.steps,
+                     "alg_bytes_per_launch": alg["summary_kernel"],
+                     "share_of_step": summ_ms / ms_per_step},
+        "rebuild_roofline_frac": alg["rebuild"] / (build_ms * 1e-3) / 1e9 / peak,
+        "e2e": {"value": 1e3 / e2e_ms, "unit": "frames/s",
+                "h2d_bytes_per_step": 64 + 4096 + 2048, "d2h_bytes_per_step": W * H * 4 + 16,
+                "ms_per_step": e2e_ms,
+                "path": "TransferFunction->classify->build_index('lbvh')->TileRenderer.frame"},
+        "gpu_launches": launches_per_step * args.steps,
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
@@ -356,11 +459,11 @@ def run_ours(args, rank, ws, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=1024)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -47,7 +47,10 @@ class LbvhRebuilder:
         self.info = torch.zeros(2, dtype=torch.int32, device=dev)
         self.wsb = query("vs_lbvh_workspace", self.P, self.cap)
         self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=dev)
+        words = (self.cap + 31) // 32
+        self.brick_bits = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
         self.graph = None
+        self._view = None
 
     # -- the launch sequence ------------------------------------------------------------
     def launch_summary(self, st: int):
@@ -66,6 +69,9 @@ class LbvhRebuilder:
              self.cap, ptr(t["lo"]), ptr(t["hi"]), ptr(t["left"]), ptr(t["right"]),
              ptr(t["leaf_brick"]), ptr(t["brick_coords"]), ptr(self.info), ptr(self.ws),
              self.wsb, st)
+        # leaf-brick grid for the renderer's brick DDA (part of "index ready")
+        call("vs_lbvh_brick_grid", ptr(t["brick_coords"]), ptr(self.info), self.cap, *self.nb,
+             ptr(self.brick_bits), st)
 
     def launch(self):
         st = torch.cuda.current_stream().cuda_stream
@@ -98,6 +104,14 @@ class LbvhRebuilder:
             self.launch()
 
     # -- results --------------------------------------------------------------------------
+    def index(self) -> Lbvh:
+        """A live Lbvh over the rebuilder's buffers (valid until the next rebuild)."""
+        if self._view is None:
+            v = Lbvh(self.tree, self.info, 8, self.dims)
+            v.__dict__["_brick_grid"] = self.brick_bits
+            self._view = v
+        return self._view
+
     def lbvh(self) -> Lbvh:
         """A snapshot Lbvh (device arrays cloned) of the last rebuild."""
         d = {k: t.clone() for k, t in self.tree.items()}

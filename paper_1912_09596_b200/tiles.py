@@ -1,0 +1,92 @@
+"""Image-tile parallel rendering across GPUs: one process per GPU, the volume
+and the index replicated on every rank, the frame split into interleaved row stripes
+(stripe rows dealt round-robin over the ranks, which balances the volume's central
+footprint), each rank renders its stripes with k_render, and the RGBA8 stripes are gathered
+over NVLink with one NCCL all-gather, then put back in image order.
+
+World size 1 renders the whole frame with no collective.  The same code path runs on CPU
+process groups (gloo) for the host-side tests of the stripe bookkeeping.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .render import (Camera, Frame, RenderTarget, RowsDesc, _check_flags, camera_desc,
+                     index_desc, render_rows, volume_desc)
+
+DEFAULT_STRIPE = 8
+
+
+def stripe_rows(height: int, nparts: int, part: int, stripe: int = DEFAULT_STRIPE) -> np.ndarray:
+    """Image rows rendered by ``part``: stripes of ``stripe`` rows dealt round-robin."""
+    rows = np.arange(height)
+    return rows[(rows // stripe) % nparts == part]
+
+
+def gather_permutation(height: int, nparts: int, stripe: int = DEFAULT_STRIPE):
+    """(max local rows, index array mapping gathered (part, local row) slots -> image rows)."""
+    per = [stripe_rows(height, nparts, p, stripe) for p in range(nparts)]
+    mx = max(len(r) for r in per)
+    src = np.empty(height, dtype=np.int64)
+    for p, r in enumerate(per):
+        src[r] = p * mx + np.arange(len(r))
+    return mx, src
+
+
+def assemble(gathered: torch.Tensor, perm: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """Gathered (world*maxrows, w, 4) stripe slots -> image rows (out[j] = gathered[perm[j]])."""
+    return torch.index_select(gathered, 0, perm, out=out)
+
+
+class TileRenderer:
+    """Renders frames of one (volume, index) with the rows split over a process group."""
+
+    def __init__(self, width: int, height: int, group=None, stripe: int = DEFAULT_STRIPE,
+                 want_samples: bool = False):
+        self.width, self.height = int(width), int(height)
+        self.group = group
+        self.world = dist.get_world_size(group) if (dist.is_available() and
+                                                    dist.is_initialized()) else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        self.stripe = int(stripe)
+        self.rows = stripe_rows(self.height, self.world, self.rank, self.stripe)
+        self.maxrows, perm = gather_permutation(self.height, self.world, self.stripe)
+        dev = _lib.device()
+        self.target = RenderTarget(self.width, self.maxrows, want_samples=want_samples)
+        self.rows_desc = RowsDesc(len(self.rows), self.stripe, self.world, self.rank)
+        if self.world > 1:
+            self.gathered = torch.empty((self.world * self.maxrows, self.width, 4),
+                                        dtype=torch.uint8, device=dev)
+            self.totals = torch.empty(self.world, dtype=torch.int64, device=dev)
+        self.perm = torch.from_numpy(perm).to(dev)
+        self.frame_dev = torch.empty((self.height, self.width, 4), dtype=torch.uint8, device=dev)
+
+    def render(self, v, tf, index, cam: Camera, dt: float = 0.5, idx_desc=None, vol_desc=None,
+               cam_desc=None) -> torch.Tensor:
+        """Render this rank's stripes and assemble the full frame on every rank (device)."""
+        render_rows(v, tf, index, cam, self.target, dt=dt, rows=self.rows_desc,
+                    idx_desc=idx_desc or index_desc(index), vol_desc=vol_desc or volume_desc(v),
+                    cam_desc=cam_desc or camera_desc(cam))
+        if self.world == 1:
+            self.frame_dev.copy_(self.target.rgba8[: self.height])
+            return self.frame_dev
+        dist.all_gather_into_tensor(self.gathered, self.target.rgba8, group=self.group)
+        return assemble(self.gathered, self.perm, self.frame_dev)
+
+    def sample_total(self) -> int:
+        t = self.target.total
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.totals, t, group=self.group)
+            return int(self.totals.sum().item())
+        return int(t.item())
+
+    def frame(self, v, tf, index, cam: Camera, dt: float = 0.5) -> Frame:
+        """Public API: a full Frame (host pixels) rendered by the whole group."""
+        img = self.render(v, tf, index, cam, dt)
+        _check_flags(self.target.flags)
+        return Frame(width=self.width, height=self.height, pixels=img.cpu().numpy(),
+                     sample_count=self.sample_total())
