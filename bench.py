@@ -369,7 +369,7 @@ def run_ours(args, rank, ws, local):
 
     # ---- e2e through the public API ---------------------------------------------------------
     luts = [tf.lut for tf in tfs]
-    e_steps = max(1, min(args.steps, 30))
+    e_steps = args.steps  # the same TF sweep / camera orbit as the device-timed loop
     pub = TileRenderer(W, H)
 
     def e2e_step(k):
