@@ -20,6 +20,7 @@
 // trilinear first-level differences in float32 (numba types f32 - f32 as f32), opacity
 // correction 1 - (1 - a)^dt from a host table computed with libm pow (== numba's **).
 #include <cfloat>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -96,7 +97,9 @@ struct RenderSmem {
   float u8f[256];
 };
 
-// ---- integrator (_k_integrate for one ray, fed segment by segment) -------------------------
+// ---- integrator (_k_integrate for one ray), resumable ----------------------------------------
+// begin(t0, t1) positions the lattice index k exactly as render.py:664-671; run(S) takes at
+// most S samples so the render loop can interleave traversal and sampling across a warp.
 struct Integrator {
   const Ray* r;
   const RenderSmem* sm;
@@ -107,310 +110,497 @@ struct Integrator {
   bool nearest;
   double accr, accg, accb, acca;
   int64_t taken;
+  // active segment
+  double t, t1;
+  int64_t k;
+  bool active;
 
+  // f32(u / 255) exactly (load_raw normalises in float64 then narrows): u/255 in binary is
+  // u's 8 bits repeated, so rounding the 64-bit repetition to float and scaling by 2^-64 is
+  // the correctly rounded value (checked for all 256 codes) -- no table, no MIO traffic.
+  __device__ __forceinline__ static float u8f(uint32_t u) {
+    const uint32_t w = u * 0x01010101u;
+    const unsigned long long q = ((unsigned long long)w << 32) | w;
+    return __fmul_rn(__ull2float_rn(q), __int_as_float(0x1f800000));  // x 2^-64
+  }
   __device__ __forceinline__ float fetch(int64_t idx) const {
     if (field) return __ldg(field + idx);
-    return sm->u8f[__ldg(bins + idx)];
+    return u8f(__ldg(bins + idx));
   }
 
-  __device__ __forceinline__ void segment(double t0, double t1) {
-    int64_t k = (int64_t)ceil(__ddiv_rn(t0 - entry, dt));
-    if (k < 0) k = 0;
-    while (k > 0 && __dadd_rn(entry, __dmul_rn((double)(k - 1), dt)) >= t0) k--;
-    while (__dadd_rn(entry, __dmul_rn((double)k, dt)) < t0) k++;
-    double t = __dadd_rn(entry, __dmul_rn((double)k, dt));
+  __device__ __forceinline__ void begin(double t0, double t1_) {
+    int64_t kk = (int64_t)ceil(__ddiv_rn(t0 - entry, dt));
+    if (kk < 0) kk = 0;
+    while (kk > 0 && __dadd_rn(entry, __dmul_rn((double)(kk - 1), dt)) >= t0) kk--;
+    while (__dadd_rn(entry, __dmul_rn((double)kk, dt)) < t0) kk++;
+    k = kk;
+    t = __dadd_rn(entry, __dmul_rn((double)kk, dt));
+    t1 = t1_;
+    active = t < t1;
+  }
+
+  __device__ __forceinline__ void sample() {
     const int64_t sy = nz, sx = (int64_t)ny * nz;
-    while (t < t1) {
-      const double px = __dadd_rn(r->ox, __dmul_rn(t, r->dx));
-      const double py = __dadd_rn(r->oy, __dmul_rn(t, r->dy));
-      const double pz = __dadd_rn(r->oz, __dmul_rn(t, r->dz));
-      double value;
-      if (nearest) {
-        int64_t xi = (int64_t)floor(px), yi = (int64_t)floor(py), zi = (int64_t)floor(pz);
-        xi = xi < 0 ? 0 : (xi > nx - 1 ? nx - 1 : xi);
-        yi = yi < 0 ? 0 : (yi > ny - 1 ? ny - 1 : yi);
-        zi = zi < 0 ? 0 : (zi > nz - 1 ? nz - 1 : zi);
-        value = (double)fetch(xi * sx + yi * sy + zi);
-      } else {
-        const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
-        int64_t x0 = (int64_t)floor(qx), y0 = (int64_t)floor(qy), z0 = (int64_t)floor(qz);
-        const double fx = qx - (double)x0, fy = qy - (double)y0, fz = qz - (double)z0;
-        int64_t x1 = x0 + 1, y1 = y0 + 1, z1 = z0 + 1;
-        x0 = x0 < 0 ? 0 : (x0 > nx - 1 ? nx - 1 : x0);
-        y0 = y0 < 0 ? 0 : (y0 > ny - 1 ? ny - 1 : y0);
-        z0 = z0 < 0 ? 0 : (z0 > nz - 1 ? nz - 1 : z0);
-        x1 = x1 < 0 ? 0 : (x1 > nx - 1 ? nx - 1 : x1);
-        y1 = y1 < 0 ? 0 : (y1 > ny - 1 ? ny - 1 : y1);
-        z1 = z1 < 0 ? 0 : (z1 > nz - 1 ? nz - 1 : z1);
-        const int64_t b00 = x0 * sx + y0 * sy, b10 = x1 * sx + y0 * sy;
-        const int64_t b01 = x0 * sx + y1 * sy, b11 = x1 * sx + y1 * sy;
-        const float c000 = fetch(b00 + z0), c100 = fetch(b10 + z0);
-        const float c010 = fetch(b01 + z0), c110 = fetch(b11 + z0);
-        const float c001 = fetch(b00 + z1), c101 = fetch(b10 + z1);
-        const float c011 = fetch(b01 + z1), c111 = fetch(b11 + z1);
-        const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
-        const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
-        const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, fx));
-        const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, fx));
-        const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, fx));
-        const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, fx));
-        const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, fy));
-        const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, fy));
-        value = __dadd_rn(c0, __dmul_rn(c1 - c0, fz));
-      }
-      const double bd = floor(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
-      const int bin = bd < 0.0 ? 0 : (bd > 255.0 ? 255 : (int)bd);
-      const float4 c = sm->lut[bin];
-      if (c.w > 0.0f) {
-        const double w = __dmul_rn(1.0 - acca, sm->corr[bin]);
-        accr = __dadd_rn(accr, __dmul_rn(w, (double)c.x));
-        accg = __dadd_rn(accg, __dmul_rn(w, (double)c.y));
-        accb = __dadd_rn(accb, __dmul_rn(w, (double)c.z));
-        acca = __dadd_rn(acca, w);
-      }
-      ++taken;
-      ++k;
-      t = __dadd_rn(entry, __dmul_rn((double)k, dt));
-    }
-  }
-};
-
-// One-interval merge window (= _sort_merge on a t-sorted stream).
-template <class Sink>
-struct Merger {
-  Sink* sink;
-  double a, b, last_t0;
-  bool open;
-  int* flags;
-  __device__ __forceinline__ void push(double t0, double t1) {
-    if (t0 < last_t0) *flags |= RF_ORDER;
-    last_t0 = t0;
-    if (t1 <= t0) return;
-    if (open && t0 <= b) {
-      if (t1 > b) b = t1;
+    const double px = __dadd_rn(r->ox, __dmul_rn(t, r->dx));
+    const double py = __dadd_rn(r->oy, __dmul_rn(t, r->dy));
+    const double pz = __dadd_rn(r->oz, __dmul_rn(t, r->dz));
+    double value;
+    if (nearest) {
+      int64_t xi = (int64_t)floor(px), yi = (int64_t)floor(py), zi = (int64_t)floor(pz);
+      xi = xi < 0 ? 0 : (xi > nx - 1 ? nx - 1 : xi);
+      yi = yi < 0 ? 0 : (yi > ny - 1 ? ny - 1 : yi);
+      zi = zi < 0 ? 0 : (zi > nz - 1 ? nz - 1 : zi);
+      value = (double)fetch(xi * sx + yi * sy + zi);
     } else {
-      if (open) sink->segment(a, b);
-      a = t0;
-      b = t1;
-      open = true;
+      const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
+      int64_t x0 = (int64_t)floor(qx), y0 = (int64_t)floor(qy), z0 = (int64_t)floor(qz);
+      const double fx = qx - (double)x0, fy = qy - (double)y0, fz = qz - (double)z0;
+      int64_t x1 = x0 + 1, y1 = y0 + 1, z1 = z0 + 1;
+      x0 = x0 < 0 ? 0 : (x0 > nx - 1 ? nx - 1 : x0);
+      y0 = y0 < 0 ? 0 : (y0 > ny - 1 ? ny - 1 : y0);
+      z0 = z0 < 0 ? 0 : (z0 > nz - 1 ? nz - 1 : z0);
+      x1 = x1 < 0 ? 0 : (x1 > nx - 1 ? nx - 1 : x1);
+      y1 = y1 < 0 ? 0 : (y1 > ny - 1 ? ny - 1 : y1);
+      z1 = z1 < 0 ? 0 : (z1 > nz - 1 ? nz - 1 : z1);
+      const int64_t b00 = x0 * sx + y0 * sy, b10 = x1 * sx + y0 * sy;
+      const int64_t b01 = x0 * sx + y1 * sy, b11 = x1 * sx + y1 * sy;
+      const float c000 = fetch(b00 + z0), c100 = fetch(b10 + z0);
+      const float c010 = fetch(b01 + z0), c110 = fetch(b11 + z0);
+      const float c001 = fetch(b00 + z1), c101 = fetch(b10 + z1);
+      const float c011 = fetch(b01 + z1), c111 = fetch(b11 + z1);
+      const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
+      const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
+      const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, fx));
+      const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, fx));
+      const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, fx));
+      const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, fx));
+      const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, fy));
+      const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, fy));
+      value = __dadd_rn(c0, __dmul_rn(c1 - c0, fz));
     }
+    const double bd = floor(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
+    const int bin = bd < 0.0 ? 0 : (bd > 255.0 ? 255 : (int)bd);
+    const float4 c = sm->lut[bin];
+    if (c.w > 0.0f) {
+      const double w = __dmul_rn(1.0 - acca, sm->corr[bin]);
+      accr = __dadd_rn(accr, __dmul_rn(w, (double)c.x));
+      accg = __dadd_rn(accg, __dmul_rn(w, (double)c.y));
+      accb = __dadd_rn(accb, __dmul_rn(w, (double)c.z));
+      acca = __dadd_rn(acca, w);
+    }
+    ++taken;
+    ++k;
+    t = __dadd_rn(entry, __dmul_rn((double)k, dt));
   }
-  __device__ __forceinline__ void flush() {
-    if (open) sink->segment(a, b);
-    open = false;
+
+  __device__ __forceinline__ void run(int smax) {
+    for (int q = 0; q < smax && t < t1; ++q) sample();
+    active = t < t1;
+  }
+
+  __device__ __forceinline__ void segment(double t0, double t1_) {  // whole segment at once
+    begin(t0, t1_);
+    while (t < t1) sample();
+    active = false;
   }
 };
 
-template <class Sink>
-__device__ __forceinline__ Merger<Sink> make_merger(Sink* s, int* flags) {
-  Merger<Sink> m;
-  m.sink = s;
-  m.a = m.b = 0.0;
-  m.last_t0 = -DBL_MAX;
-  m.open = false;
-  m.flags = flags;
-  return m;
-}
+// ---- interval generators -----------------------------------------------------------------
+// next(a, b, budget): 1 = produced [a, b), 0 = exhausted, 2 = budget (traversal steps) spent.
 
-// _dda_runs over the macro grid between t_in and t_out, runs pushed into `out`.
-template <class Out>
-__device__ void dda_runs(const Ray& r, const vs_index_desc& ix, double t_in, double t_out,
-                         Out& out) {
-  const int ncx = ix.ncx, ncy = ix.ncy, ncz = ix.ncz;
-  const double cs = (double)ix.cs;
-  const double px = __dadd_rn(r.ox, __dmul_rn(t_in, r.dx));
-  const double py = __dadd_rn(r.oy, __dmul_rn(t_in, r.dy));
-  const double pz = __dadd_rn(r.oz, __dmul_rn(t_in, r.dz));
-  int64_t cx = (int64_t)floor(__ddiv_rn(px, cs)), cy = (int64_t)floor(__ddiv_rn(py, cs)),
-          cz = (int64_t)floor(__ddiv_rn(pz, cs));
-  cx = cx < 0 ? 0 : (cx > ncx - 1 ? ncx - 1 : cx);
-  cy = cy < 0 ? 0 : (cy > ncy - 1 ? ncy - 1 : cy);
-  cz = cz < 0 ? 0 : (cz > ncz - 1 ? ncz - 1 : cz);
-  const int sx = r.zx ? 0 : (r.ix > 0.0 ? 1 : -1);
-  const int sy = r.zy ? 0 : (r.iy > 0.0 ? 1 : -1);
-  const int sz = r.zz ? 0 : (r.iz > 0.0 ? 1 : -1);
-  auto cross = [&](int64_t c, int s, double o, double inv) -> double {
+// Single interval (_k_naive).
+struct NaiveGen {
+  double a, b;
+  bool done;
+  __device__ __forceinline__ int next(double& x, double& y, int&) {
+    if (done) return 0;
+    done = true;
+    x = a; y = b;
+    return 1;
+  }
+};
+
+// _dda_runs (render.py:305-378) over [t_in, t_out), resumable.
+struct GridDDA {
+  const uint8_t* __restrict__ occ;
+  int ncx, ncy, ncz;
+  double cs, t_out, run_t0, tcur, tnx, tny, tnz;
+  int64_t cx, cy, cz, step, max_steps;
+  int sx, sy, sz;
+  bool open_run, done, fin;
+
+  __device__ __forceinline__ double cross(int64_t c, int s, double o, double inv) const {
     return __dmul_rn(__dmul_rn((double)(c + (s > 0)), cs) - o, inv);
-  };
-  double tnx = sx == 0 ? R_FAR : cross(cx, sx, r.ox, r.ix);
-  double tny = sy == 0 ? R_FAR : cross(cy, sy, r.oy, r.iy);
-  double tnz = sz == 0 ? R_FAR : cross(cz, sz, r.oz, r.iz);
-  bool open_run = false;
-  double run_t0 = 0.0, tcur = t_in;
-  const int64_t max_steps = (int64_t)ncx + ncy + ncz + 3;
-  for (int64_t step = 0; step < max_steps; ++step) {
-    double tn = tnx;
-    if (tny < tn) tn = tny;
-    if (tnz < tn) tn = tnz;
-    if (__ldg(ix.occ + (cx * ncy + cy) * ncz + cz)) {
-      if (!open_run) { open_run = true; run_t0 = tcur; }
-    } else if (open_run) {
-      out.push(run_t0, tcur);
-      open_run = false;
-    }
-    if (tn >= t_out) break;
-    if (tnx == tn) { cx += sx; tnx = cross(cx, sx, r.ox, r.ix); }
-    if (tny == tn) { cy += sy; tny = cross(cy, sy, r.oy, r.iy); }
-    if (tnz == tn) { cz += sz; tnz = cross(cz, sz, r.oz, r.iz); }
-    tcur = tn;
-    if (cx < 0 || cy < 0 || cz < 0 || cx >= ncx || cy >= ncy || cz >= ncz) break;
   }
-  if (open_run) out.push(run_t0, t_out);
-}
+  __device__ void init(const Ray& r, const vs_index_desc& ix, double t_in, double t_out_) {
+    occ = ix.occ;
+    ncx = ix.ncx; ncy = ix.ncy; ncz = ix.ncz;
+    cs = (double)ix.cs;
+    t_out = t_out_;
+    const double px = __dadd_rn(r.ox, __dmul_rn(t_in, r.dx));
+    const double py = __dadd_rn(r.oy, __dmul_rn(t_in, r.dy));
+    const double pz = __dadd_rn(r.oz, __dmul_rn(t_in, r.dz));
+    cx = (int64_t)floor(__ddiv_rn(px, cs));
+    cy = (int64_t)floor(__ddiv_rn(py, cs));
+    cz = (int64_t)floor(__ddiv_rn(pz, cs));
+    cx = cx < 0 ? 0 : (cx > ncx - 1 ? ncx - 1 : cx);
+    cy = cy < 0 ? 0 : (cy > ncy - 1 ? ncy - 1 : cy);
+    cz = cz < 0 ? 0 : (cz > ncz - 1 ? ncz - 1 : cz);
+    sx = r.zx ? 0 : (r.ix > 0.0 ? 1 : -1);
+    sy = r.zy ? 0 : (r.iy > 0.0 ? 1 : -1);
+    sz = r.zz ? 0 : (r.iz > 0.0 ? 1 : -1);
+    tnx = sx == 0 ? R_FAR : cross(cx, sx, r.ox, r.ix);
+    tny = sy == 0 ? R_FAR : cross(cy, sy, r.oy, r.iy);
+    tnz = sz == 0 ? R_FAR : cross(cz, sz, r.oz, r.iz);
+    open_run = false;
+    run_t0 = 0.0;
+    tcur = t_in;
+    step = 0;
+    max_steps = (int64_t)ncx + ncy + ncz + 3;
+    done = false;
+    fin = false;
+  }
+  __device__ __forceinline__ int next(const Ray& r, double& x, double& y, int& budget) {
+    while (!done) {
+      if (budget <= 0) return 2;
+      --budget;
+      if (step >= max_steps) { done = true; break; }
+      double tn = tnx;
+      if (tny < tn) tn = tny;
+      if (tnz < tn) tn = tnz;
+      bool emit = false;
+      if (__ldg(occ + (cx * ncy + cy) * ncz + cz)) {
+        if (!open_run) { open_run = true; run_t0 = tcur; }
+      } else if (open_run) {
+        x = run_t0; y = tcur; open_run = false; emit = true;
+      }
+      ++step;
+      if (tn >= t_out) {
+        done = true;
+      } else {
+        if (tnx == tn) { cx += sx; tnx = cross(cx, sx, r.ox, r.ix); }
+        if (tny == tn) { cy += sy; tny = cross(cy, sy, r.oy, r.iy); }
+        if (tnz == tn) { cz += sz; tnz = cross(cz, sz, r.oz, r.iz); }
+        tcur = tn;
+        if (cx < 0 || cy < 0 || cz < 0 || cx >= ncx || cy >= ncy || cz >= ncz) done = true;
+      }
+      if (emit) return 1;
+    }
+    if (!fin) {
+      fin = true;
+      if (open_run) { open_run = false; x = run_t0; y = t_out; return 1; }
+    }
+    return 0;
+  }
+};
 
-// LBVH leaf intervals without walking the tree.  A leaf's interval is reported by _k_bvh
-// iff its own slab interval clipped to [tmin, tmax] is non-empty (ancestor boxes contain it
-// and slab intervals are monotone in the box bounds, in floating point too), so the merged
-// union equals the merged union of every occupied brick's clipped slab interval.  A 3-D DDA
-// over the brick grid visits exactly the bricks whose interval along the ray is non-empty,
-// in increasing t: its per-axis crossings are the same expressions slab() evaluates for a
-// brick's faces, and simultaneous crossings skip only bricks touched in a single point.  The
-// start brick is the one whose per-axis crossing window contains tmin.  Each occupied brick
-// then gets the reference's exact clipped slab interval (box hi clipped to dims).
-template <class Out>
-__device__ void brick_dda(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz,
-                          double tmin, double tmax, Out& out) {
-  const int bs = ix.bs;
-  const double cs = (double)bs;
-  const int nb[3] = {ix.nbx, ix.nby, ix.nbz};
-  const int dims[3] = {nx, ny, nz};
-  const double o[3] = {r.ox, r.oy, r.oz}, d[3] = {r.dx, r.dy, r.dz}, inv[3] = {r.ix, r.iy, r.iz};
-  const bool zero[3] = {r.zx, r.zy, r.zz};
+// LBVH leaves without walking the tree.  A leaf's interval is reported by _k_bvh iff its own
+// slab interval clipped to [tmin, tmax] is non-empty (ancestor boxes contain it and slab
+// intervals are monotone in the box bounds, in floating point too), so the merged union equals
+// the merged union of every occupied brick's clipped slab interval.  A 3-D DDA over the brick
+// grid visits exactly the bricks whose interval along the ray is non-empty, in increasing t:
+// its per-axis crossings are the same expressions slab() evaluates for a brick's faces, and
+// simultaneous crossings skip only bricks touched in a single point.  The start brick is the
+// one whose per-axis crossing window contains tmin.  Each occupied brick then gets the
+// reference's exact clipped slab interval (box hi clipped to dims).
+struct BrickDDA {
+  const uint32_t* __restrict__ bits;
+  int nb[3], dims[3], bs;
   int c[3], s[3];
-  double tn[3];
-  for (int a = 0; a < 3; ++a) {
-    s[a] = zero[a] ? 0 : (inv[a] > 0.0 ? 1 : -1);
-    const double p = __dadd_rn(o[a], __dmul_rn(tmin, d[a]));
-    int ca = (int)floor(__ddiv_rn(p, cs));
-    ca = ca < 0 ? 0 : (ca > nb[a] - 1 ? nb[a] - 1 : ca);
-    auto plane_t = [&](int k) { return __dmul_rn((double)(k * bs) - o[a], inv[a]); };
-    if (s[a] > 0) {
-      while (ca > 0 && plane_t(ca) > tmin) --ca;
-      while (ca + 1 < nb[a] && plane_t(ca + 1) <= tmin) ++ca;
-      tn[a] = plane_t(ca + 1);
-    } else if (s[a] < 0) {
-      while (ca + 1 < nb[a] && plane_t(ca + 1) > tmin) ++ca;
-      while (ca > 0 && plane_t(ca) <= tmin) --ca;
-      tn[a] = plane_t(ca);
-    } else {
-      ca = (int)floor(__ddiv_rn(o[a], cs));
-      if (ca < 0 || ca >= nb[a]) return;
-      tn[a] = R_FAR;
-    }
-    c[a] = ca;
+  double tn[3], tmin, tmax;
+  int64_t step, maxsteps;
+  bool done;
+
+  __device__ __forceinline__ double plane_t(const Ray& r, int a, int k) const {
+    const double o = a == 0 ? r.ox : (a == 1 ? r.oy : r.oz);
+    const double inv = a == 0 ? r.ix : (a == 1 ? r.iy : r.iz);
+    return __dmul_rn((double)(k * bs) - o, inv);
   }
-  const uint32_t* __restrict__ bits = ix.brick_bits;
-  const int64_t maxsteps = (int64_t)nb[0] + nb[1] + nb[2] + 3;
-  for (int64_t step = 0; step < maxsteps; ++step) {
-    const int64_t lin = ((int64_t)c[0] * nb[1] + c[1]) * nb[2] + c[2];
-    if ((__ldg(bits + (lin >> 5)) >> (lin & 31)) & 1u) {
-      double a, b;
-      const int l0 = c[0] * bs, l1 = c[1] * bs, l2 = c[2] * bs;
-      if (slab(r, (double)l0, (double)l1, (double)l2, (double)min(l0 + bs, dims[0]),
-               (double)min(l1 + bs, dims[1]), (double)min(l2 + bs, dims[2]), a, b)) {
-        a = a > tmin ? a : tmin;
-        b = b < tmax ? b : tmax;
-        if (b > a) out.push(a, b);
+  __device__ void init(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz,
+                       double tmin_, double tmax_, bool nonempty) {
+    bits = ix.brick_bits;
+    bs = ix.bs;
+    nb[0] = ix.nbx; nb[1] = ix.nby; nb[2] = ix.nbz;
+    dims[0] = nx; dims[1] = ny; dims[2] = nz;
+    tmin = tmin_; tmax = tmax_;
+    done = !nonempty;
+    step = 0;
+    maxsteps = (int64_t)nb[0] + nb[1] + nb[2] + 3;
+    const double cs = (double)bs;
+    for (int a = 0; a < 3; ++a) {
+      const double o = a == 0 ? r.ox : (a == 1 ? r.oy : r.oz);
+      const double d = a == 0 ? r.dx : (a == 1 ? r.dy : r.dz);
+      const double inv = a == 0 ? r.ix : (a == 1 ? r.iy : r.iz);
+      const bool zero = a == 0 ? r.zx : (a == 1 ? r.zy : r.zz);
+      s[a] = zero ? 0 : (inv > 0.0 ? 1 : -1);
+      const double p = __dadd_rn(o, __dmul_rn(tmin, d));
+      int ca = (int)floor(__ddiv_rn(p, cs));
+      ca = ca < 0 ? 0 : (ca > nb[a] - 1 ? nb[a] - 1 : ca);
+      if (s[a] > 0) {
+        while (ca > 0 && plane_t(r, a, ca) > tmin) --ca;
+        while (ca + 1 < nb[a] && plane_t(r, a, ca + 1) <= tmin) ++ca;
+        tn[a] = plane_t(r, a, ca + 1);
+      } else if (s[a] < 0) {
+        while (ca + 1 < nb[a] && plane_t(r, a, ca + 1) > tmin) ++ca;
+        while (ca > 0 && plane_t(r, a, ca) <= tmin) --ca;
+        tn[a] = plane_t(r, a, ca);
+      } else {
+        ca = (int)floor(__ddiv_rn(o, cs));
+        if (ca < 0 || ca >= nb[a]) done = true;
+        tn[a] = R_FAR;
       }
+      c[a] = ca;
     }
-    double t = tn[0];
-    if (tn[1] < t) t = tn[1];
-    if (tn[2] < t) t = tn[2];
-    if (t >= tmax) break;
-    bool outside = false;
-    for (int a2 = 0; a2 < 3; ++a2) {
-      if (tn[a2] == t) {
-        c[a2] += s[a2];
-        if (c[a2] < 0 || c[a2] >= nb[a2]) outside = true;
-        tn[a2] = __dmul_rn((double)((c[a2] + (s[a2] > 0)) * bs) - o[a2], inv[a2]);
-      }
-    }
-    if (outside) break;
   }
-}
+  __device__ __forceinline__ int next(const Ray& r, double& x, double& y, int& budget) {
+    while (!done) {
+      if (budget <= 0) return 2;
+      --budget;
+      if (step++ >= maxsteps) { done = true; break; }
+      const int64_t lin = ((int64_t)c[0] * nb[1] + c[1]) * nb[2] + c[2];
+      bool emit = false;
+      if ((__ldg(bits + (lin >> 5)) >> (lin & 31)) & 1u) {
+        double a, b;
+        const int l0 = c[0] * bs, l1 = c[1] * bs, l2 = c[2] * bs;
+        if (slab(r, (double)l0, (double)l1, (double)l2, (double)min(l0 + bs, dims[0]),
+                 (double)min(l1 + bs, dims[1]), (double)min(l2 + bs, dims[2]), a, b)) {
+          a = a > tmin ? a : tmin;
+          b = b < tmax ? b : tmax;
+          if (b > a) { x = a; y = b; emit = true; }
+        }
+      }
+      double tt = tn[0];
+      if (tn[1] < tt) tt = tn[1];
+      if (tn[2] < tt) tt = tn[2];
+      if (tt >= tmax) {
+        done = true;
+      } else {
+        for (int a2 = 0; a2 < 3; ++a2) {
+          if (tn[a2] == tt) {
+            c[a2] += s[a2];
+            if (c[a2] < 0 || c[a2] >= nb[a2]) done = true;
+            tn[a2] = plane_t(r, a2, c[a2] + (s[a2] > 0));
+          }
+        }
+      }
+      if (emit) return 1;
+    }
+    return 0;
+  }
+};
 
 // _k_bvh leaf intervals, near-first DFS; the stack holds node ids (a popped node's clipped
 // interval is recomputed: same inputs, same doubles).
-template <class Out>
-__device__ void bvh_leaves(const Ray& r, const vs_index_desc& ix, int root, double tmin,
-                           double tmax, Out& out, int* flags) {
+struct BvhWalk {
+  const int32_t *lo, *hi, *left, *right;
+  double tmin, tmax;
+  int sp;
   int stk[STACK_CAP];
-  int sp = 0;
-  double a, b;
-  if (root < 0) return;
-  if (node_slab(r, ix.lo, ix.hi, root, a, b)) {
-    a = a > tmin ? a : tmin;
-    b = b < tmax ? b : tmax;
-    if (b > a) stk[sp++] = root;
-  }
-  while (sp > 0) {
-    const int i = stk[--sp];
-    const int li = __ldg(ix.left + i);
-    if (li < 0) {
-      node_slab(r, ix.lo, ix.hi, i, a, b);
+
+  __device__ void init(const Ray& r, const vs_index_desc& ix, int root, double tmin_,
+                       double tmax_) {
+    lo = ix.lo; hi = ix.hi; left = ix.left; right = ix.right;
+    tmin = tmin_; tmax = tmax_;
+    sp = 0;
+    double a, b;
+    if (root >= 0 && node_slab(r, lo, hi, root, a, b)) {
       a = a > tmin ? a : tmin;
       b = b < tmax ? b : tmax;
-      out.push(a, b);
-      continue;
-    }
-    const int ri = __ldg(ix.right + i);
-    double la, lb, ra, rb;
-    bool hl = node_slab(r, ix.lo, ix.hi, li, la, lb);
-    if (hl) { la = la > tmin ? la : tmin; lb = lb < tmax ? lb : tmax; if (lb <= la) hl = false; }
-    bool hr = node_slab(r, ix.lo, ix.hi, ri, ra, rb);
-    if (hr) { ra = ra > tmin ? ra : tmin; rb = rb < tmax ? rb : tmax; if (rb <= ra) hr = false; }
-    if (sp + 2 > STACK_CAP) { *flags |= RF_OVERFLOW; return; }
-    if (hl && hr) {
-      if (la <= ra) { stk[sp++] = ri; stk[sp++] = li; }
-      else { stk[sp++] = li; stk[sp++] = ri; }
-    } else if (hl) {
-      stk[sp++] = li;
-    } else if (hr) {
-      stk[sp++] = ri;
+      if (b > a) stk[sp++] = root;
     }
   }
-}
+  __device__ __forceinline__ int next(const Ray& r, double& x, double& y, int& budget, int* flags) {
+    while (sp > 0) {
+      if (budget <= 0) return 2;
+      --budget;
+      const int i = stk[--sp];
+      const int li = __ldg(left + i);
+      double a, b;
+      if (li < 0) {
+        node_slab(r, lo, hi, i, a, b);
+        x = a > tmin ? a : tmin;
+        y = b < tmax ? b : tmax;
+        return 1;
+      }
+      const int ri = __ldg(right + i);
+      double la, lb, ra, rb;
+      bool hl = node_slab(r, lo, hi, li, la, lb);
+      if (hl) { la = la > tmin ? la : tmin; lb = lb < tmax ? lb : tmax; if (lb <= la) hl = false; }
+      bool hr = node_slab(r, lo, hi, ri, ra, rb);
+      if (hr) { ra = ra > tmin ? ra : tmin; rb = rb < tmax ? rb : tmax; if (rb <= ra) hr = false; }
+      if (sp + 2 > STACK_CAP) { *flags |= RF_OVERFLOW; sp = 0; return 0; }
+      if (hl && hr) {
+        if (la <= ra) { stk[sp++] = ri; stk[sp++] = li; }
+        else { stk[sp++] = li; stk[sp++] = ri; }
+      } else if (hl) {
+        stk[sp++] = li;
+      } else if (hr) {
+        stk[sp++] = ri;
+      }
+    }
+    return 0;
+  }
+};
 
 // _kd_leaves: pop, slab-test clipped to [tmin, tmax], leaf -> interval, inner -> far, near.
-template <class Out>
-__device__ void kd_leaves(const Ray& r, const vs_index_desc& ix, int root, double tmin,
-                          double tmax, Out& out, int* flags) {
+struct KdWalk {
+  const int32_t *lo, *hi, *left, *right, *plane;
+  const int8_t* axis;
+  double tmin, tmax;
+  int sp;
   int stk[STACK_CAP];
-  int sp = 0;
-  if (root < 0) return;
-  stk[sp++] = root;
-  while (sp > 0) {
-    const int i = stk[--sp];
-    double a, b;
-    if (!node_slab(r, ix.lo, ix.hi, i, a, b)) continue;
-    a = a > tmin ? a : tmin;
-    b = b < tmax ? b : tmax;
-    if (b <= a) continue;
-    const int ax = __ldg(ix.axis + i);
-    if (ax < 0) { out.push(a, b); continue; }
-    const double pl = (double)__ldg(ix.plane + i);
-    bool front_left;
-    const bool zero = ax == 0 ? r.zx : (ax == 1 ? r.zy : r.zz);
-    if (zero)
-      front_left = (ax == 0 ? r.ox : (ax == 1 ? r.oy : r.oz)) < pl;
-    else
-      front_left = (ax == 0 ? r.ix : (ax == 1 ? r.iy : r.iz)) > 0.0;
-    const int lc = __ldg(ix.left + i), rc = __ldg(ix.right + i);
-    const int nr = front_left ? lc : rc, fr = front_left ? rc : lc;
-    if (sp + 2 > STACK_CAP) { *flags |= RF_OVERFLOW; return; }
-    if (fr >= 0) stk[sp++] = fr;
-    if (nr >= 0) stk[sp++] = nr;
-  }
-}
 
-// Hybrid: merged k-d leaf intervals -> DDA runs inside each -> merged runs.
-template <class Sink>
-struct LeafToGrid {
-  const Ray* r;
-  const vs_index_desc* ix;
-  Merger<Sink>* runs;
-  __device__ __forceinline__ void segment(double t0, double t1) { dda_runs(*r, *ix, t0, t1, *runs); }
+  __device__ void init(const vs_index_desc& ix, double tmin_, double tmax_) {
+    lo = ix.lo; hi = ix.hi; left = ix.left; right = ix.right; plane = ix.plane; axis = ix.axis;
+    tmin = tmin_; tmax = tmax_;
+    sp = 0;
+    if (ix.root >= 0) stk[sp++] = ix.root;
+  }
+  __device__ __forceinline__ int next(const Ray& r, double& x, double& y, int& budget, int* flags) {
+    while (sp > 0) {
+      if (budget <= 0) return 2;
+      --budget;
+      const int i = stk[--sp];
+      double a, b;
+      if (!node_slab(r, lo, hi, i, a, b)) continue;
+      a = a > tmin ? a : tmin;
+      b = b < tmax ? b : tmax;
+      if (b <= a) continue;
+      const int ax = __ldg(axis + i);
+      if (ax < 0) { x = a; y = b; return 1; }
+      const double pl = (double)__ldg(plane + i);
+      bool front_left;
+      const bool zero = ax == 0 ? r.zx : (ax == 1 ? r.zy : r.zz);
+      if (zero)
+        front_left = (ax == 0 ? r.ox : (ax == 1 ? r.oy : r.oz)) < pl;
+      else
+        front_left = (ax == 0 ? r.ix : (ax == 1 ? r.iy : r.iz)) > 0.0;
+      const int lc = __ldg(left + i), rc = __ldg(right + i);
+      const int nr = front_left ? lc : rc, fr = front_left ? rc : lc;
+      if (sp + 2 > STACK_CAP) { *flags |= RF_OVERFLOW; sp = 0; return 0; }
+      if (fr >= 0) stk[sp++] = fr;
+      if (nr >= 0) stk[sp++] = nr;
+    }
+    return 0;
+  }
 };
+
+// One-interval merge window over a t-sorted raw stream (= _sort_merge): drop t1 <= t0, merge
+// when t0 <= previous t1.  Produces merged segments.
+struct MergeState {
+  double a, b, last_t0;
+  bool open, src_done;
+  __device__ __forceinline__ void init() { open = false; src_done = false; last_t0 = -DBL_MAX; a = b = 0.0; }
+  // feed one raw interval; returns true and (x, y) when a merged segment is complete
+  __device__ __forceinline__ bool feed(double t0, double t1, double& x, double& y, int* flags) {
+    if (t0 < last_t0) *flags |= RF_ORDER;
+    last_t0 = t0;
+    if (t1 <= t0) return false;
+    if (open && t0 <= b) {
+      if (t1 > b) b = t1;
+      return false;
+    }
+    const bool out = open;
+    if (out) { x = a; y = b; }
+    a = t0; b = t1; open = true;
+    return out;
+  }
+  __device__ __forceinline__ bool drain(double& x, double& y) {
+    if (!open) return false;
+    open = false;
+    x = a; y = b;
+    return true;
+  }
+};
+
+struct NoGen {};
+
+// Per-kind source of merged segments (members only for the kinds that use them, so the
+// brick-DDA path carries no traversal stack).
+template <int KIND>
+struct SegmentSource {
+  typename std::conditional<KIND == VS_KIND_NAIVE, NaiveGen, NoGen>::type naive;
+  typename std::conditional<KIND == VS_KIND_GRID || KIND == VS_KIND_HYBRID, GridDDA, NoGen>::type grid;
+  typename std::conditional<KIND == VS_KIND_LBVH, BrickDDA, NoGen>::type brick;
+  typename std::conditional<KIND == VS_KIND_LBVH, BvhWalk, NoGen>::type bvh;
+  typename std::conditional<KIND == VS_KIND_KD || KIND == VS_KIND_HYBRID, KdWalk, NoGen>::type kd;
+  MergeState m, leaves;
+  bool use_brick, inner_active;
+
+  __device__ void init(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz, double tmin,
+                       double tmax) {
+    m.init();
+    if constexpr (KIND == VS_KIND_NAIVE) {
+      naive.a = tmin; naive.b = tmax; naive.done = false;
+    } else if constexpr (KIND == VS_KIND_GRID) {
+      grid.init(r, ix, tmin, tmax);
+    } else if constexpr (KIND == VS_KIND_LBVH) {
+      const int n = ix.lbvh_info ? __ldg(ix.lbvh_info) : ix.root + 1;
+      use_brick = ix.brick_bits != nullptr;
+      if (use_brick) brick.init(r, ix, nx, ny, nz, tmin, tmax, n > 0);
+      else bvh.init(r, ix, n > 0 ? 0 : -1, tmin, tmax);
+    } else {
+      kd.init(ix, tmin, tmax);
+      if constexpr (KIND == VS_KIND_HYBRID) { leaves.init(); inner_active = false; }
+    }
+  }
+
+  // raw intervals of the kind (before the final merge); 1 / 0 / 2 as the generators
+  __device__ __forceinline__ int raw(const Ray& r, const vs_index_desc& ix, double& x, double& y,
+                                     int& budget, int* flags) {
+    if constexpr (KIND == VS_KIND_NAIVE) {
+      return naive.next(x, y, budget);
+    } else if constexpr (KIND == VS_KIND_GRID) {
+      return grid.next(r, x, y, budget);
+    } else if constexpr (KIND == VS_KIND_LBVH) {
+      if (use_brick) return brick.next(r, x, y, budget);
+      return bvh.next(r, x, y, budget, flags);
+    } else if constexpr (KIND == VS_KIND_KD) {
+      return kd.next(r, x, y, budget, flags);
+    } else {
+    // hybrid: merged k-d leaf intervals, each walked by the grid DDA
+    while (true) {
+      if (inner_active) {
+        const int g = grid.next(r, x, y, budget);
+        if (g != 0) return g;
+        inner_active = false;
+      }
+      double la, lb;
+      bool got = false;
+      while (!got) {
+        if (leaves.src_done) {
+          if (!leaves.drain(la, lb)) return 0;
+          got = true;
+          break;
+        }
+        double ka, kb;
+        const int k = kd.next(r, ka, kb, budget, flags);
+        if (k == 2) return 2;
+        if (k == 0) { leaves.src_done = true; continue; }
+        got = leaves.feed(ka, kb, la, lb, flags);
+      }
+      grid.init(r, ix, la, lb);
+      inner_active = true;
+    }
+    }
+  }
+
+  // next merged segment: 1 = (x, y), 0 = exhausted, 2 = budget spent
+  __device__ __forceinline__ int next(const Ray& r, const vs_index_desc& ix, double& x, double& y,
+                                      int& budget, int* flags) {
+    while (true) {
+      if (m.src_done) return m.drain(x, y) ? 1 : 0;
+      double a, b;
+      const int k = raw(r, ix, a, b, budget, flags);
+      if (k == 2) return 2;
+      if (k == 0) { m.src_done = true; continue; }
+      if (m.feed(a, b, x, y, flags)) return 1;
+    }
+  }
+};
+
+constexpr int TRAV_BUDGET = 16;   // traversal steps per loop turn
+constexpr int SAMPLE_BUDGET = 8;  // lattice samples per loop turn
 
 template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
@@ -419,7 +609,6 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
              uint8_t* __restrict__ rgba8, double* __restrict__ rgba64, int32_t* __restrict__ samples,
              unsigned long long* __restrict__ total, int* __restrict__ flags_out) {
   __shared__ RenderSmem sm;
-  __shared__ unsigned long long red[RENDER_TX * RENDER_TY / 32];
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
   for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
     sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
@@ -447,31 +636,25 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
     I.accr = I.accg = I.accb = I.acca = 0.0;
     I.taken = 0;
+    I.active = false;
     double tmin, tmax;
     if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
       I.entry = tmin;  // _k_integrate's own slab of the full volume gives the same entry
-      auto m = make_merger(&I, &flags);
-      if (KIND == VS_KIND_NAIVE) {
-        m.push(tmin, tmax);
-      } else if (KIND == VS_KIND_GRID) {
-        dda_runs(r, ix, tmin, tmax, m);
-      } else if (KIND == VS_KIND_LBVH) {
-        const int n = ix.lbvh_info ? __ldg(ix.lbvh_info) : ix.root + 1;
-        if (ix.brick_bits) {
-          if (n > 0) brick_dda(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax, m);
-        } else {
-          bvh_leaves(r, ix, n > 0 ? 0 : -1, tmin, tmax, m, &flags);
+      SegmentSource<KIND> src;
+      src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
+      // while-while: each turn does a bounded amount of traversal (lanes without a segment)
+      // and a bounded number of samples (lanes with one), so lanes in the same phase share
+      // instructions instead of serialising whole traversals against whole sample loops.
+      while (true) {
+        if (!I.active) {
+          int budget = TRAV_BUDGET;
+          double a, b;
+          const int g = src.next(r, ix, a, b, budget, &flags);
+          if (g == 0) break;
+          if (g == 1) I.begin(a, b);
         }
-      } else if (KIND == VS_KIND_KD) {
-        kd_leaves(r, ix, ix.root, tmin, tmax, m, &flags);
-      } else {
-        LeafToGrid<Integrator> g;
-        g.r = &r; g.ix = &ix; g.runs = &m;
-        auto leaves = make_merger(&g, &flags);
-        kd_leaves(r, ix, ix.root, tmin, tmax, leaves, &flags);
-        leaves.flush();
+        if (I.active) I.run(SAMPLE_BUDGET);
       }
-      m.flush();
     }
     taken = I.taken;
     const int64_t pix = (int64_t)l * cam.width + i;
@@ -485,28 +668,30 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     if (samples) samples[pix] = (int32_t)taken;
   }
   if (flags) atomicOr(flags_out, flags);
-  if (total) {
+  if (total) {  // warp-level: no block barrier behind the slowest warp of the tile
     unsigned long long t = (unsigned long long)taken;
     for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if ((tid & 31) == 0) red[tid >> 5] = t;
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long s = 0;
-      for (int k = 0; k < RENDER_TX * RENDER_TY / 32; ++k) s += red[k];
-      if (s) atomicAdd(total, s);
-    }
+    if ((tid & 31) == 0 && t) atomicAdd(total, t);
   }
 }
 
-// Single-ray traversal (render.py:917-961): the merged interval list of one ray.
-struct ListSink {
-  double* out;
-  int cap, n;
-  __device__ void segment(double t0, double t1) {
-    if (n < cap) { out[2 * n] = t0; out[2 * n + 1] = t1; }
-    ++n;
+// Single-ray traversal (render.py:917-961): the merged interval list of each ray.
+template <int KIND>
+__device__ void traverse_one(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz,
+                             double tmin, double tmax, double* out, int cap, int& n, int* flags) {
+  SegmentSource<KIND> src;
+  src.init(r, ix, nx, ny, nz, tmin, tmax);
+  while (true) {
+    int budget = 1 << 30;
+    double a, b;
+    const int g = src.next(r, ix, a, b, budget, flags);
+    if (g == 0) break;
+    if (g == 1) {
+      if (n < cap) { out[2 * n] = a; out[2 * n + 1] = b; }
+      ++n;
+    }
   }
-};
+}
 
 __global__ void k_traverse_rays(vs_index_desc ix, int nx, int ny, int nz,
                                 const double* __restrict__ origins, const double* __restrict__ dir,
@@ -518,35 +703,19 @@ __global__ void k_traverse_rays(vs_index_desc ix, int nx, int ny, int nz,
   c.dir[0] = dir[0]; c.dir[1] = dir[1]; c.dir[2] = dir[2];
   Ray r;
   ray_setup(r, origins[3 * q], origins[3 * q + 1], origins[3 * q + 2], c);
-  ListSink L{out + (int64_t)q * cap * 2, cap, 0};
-  int flags = 0;
+  int flags = 0, n = 0;
+  double* o = out + (int64_t)q * cap * 2;
   double tmin, tmax;
   if (slab(r, 0.0, 0.0, 0.0, (double)nx, (double)ny, (double)nz, tmin, tmax)) {
-    auto m = make_merger(&L, &flags);
     switch (ix.kind) {
-      case VS_KIND_NAIVE: m.push(tmin, tmax); break;
-      case VS_KIND_GRID: dda_runs(r, ix, tmin, tmax, m); break;
-      case VS_KIND_LBVH: {
-        const int n = ix.lbvh_info ? ix.lbvh_info[0] : ix.root + 1;
-        if (ix.brick_bits) {
-          if (n > 0) brick_dda(r, ix, nx, ny, nz, tmin, tmax, m);
-        } else {
-          bvh_leaves(r, ix, n > 0 ? 0 : -1, tmin, tmax, m, &flags);
-        }
-        break;
-      }
-      case VS_KIND_KD: kd_leaves(r, ix, ix.root, tmin, tmax, m, &flags); break;
-      default: {
-        LeafToGrid<ListSink> g;
-        g.r = &r; g.ix = &ix; g.runs = &m;
-        auto leaves = make_merger(&g, &flags);
-        kd_leaves(r, ix, ix.root, tmin, tmax, leaves, &flags);
-        leaves.flush();
-      }
+      case VS_KIND_NAIVE: traverse_one<VS_KIND_NAIVE>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
+      case VS_KIND_GRID: traverse_one<VS_KIND_GRID>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
+      case VS_KIND_LBVH: traverse_one<VS_KIND_LBVH>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
+      case VS_KIND_KD: traverse_one<VS_KIND_KD>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
+      default: traverse_one<VS_KIND_HYBRID>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
     }
-    m.flush();
   }
-  counts[q] = L.n;
+  counts[q] = n;
   if (flags) atomicOr(flags_out, flags);
 }
 
