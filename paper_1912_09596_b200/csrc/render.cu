@@ -29,6 +29,7 @@ namespace vs {
 constexpr double R_FAR = 1e300;
 constexpr int RENDER_TX = 16, RENDER_TY = 8;  // 128-thread pixel tiles
 constexpr int STACK_CAP = 128;
+constexpr int KIND_LBVH_BRICK = 5;  // internal: LBVH leaves by brick DDA
 
 enum RenderFlags { RF_OVERFLOW = 1, RF_ORDER = 2 };
 
@@ -327,6 +328,7 @@ struct BrickDDA {
     step = 0;
     maxsteps = (int64_t)nb[0] + nb[1] + nb[2] + 3;
     const double cs = (double)bs;
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
       const double o = a == 0 ? r.ox : (a == 1 ? r.oy : r.oz);
       const double d = a == 0 ? r.dx : (a == 1 ? r.dy : r.dz);
@@ -375,6 +377,7 @@ struct BrickDDA {
       if (tt >= tmax) {
         done = true;
       } else {
+#pragma unroll
         for (int a2 = 0; a2 < 3; ++a2) {
           if (tn[a2] == tt) {
             c[a2] += s[a2];
@@ -521,11 +524,11 @@ template <int KIND>
 struct SegmentSource {
   typename std::conditional<KIND == VS_KIND_NAIVE, NaiveGen, NoGen>::type naive;
   typename std::conditional<KIND == VS_KIND_GRID || KIND == VS_KIND_HYBRID, GridDDA, NoGen>::type grid;
-  typename std::conditional<KIND == VS_KIND_LBVH, BrickDDA, NoGen>::type brick;
+  typename std::conditional<KIND == KIND_LBVH_BRICK, BrickDDA, NoGen>::type brick;
   typename std::conditional<KIND == VS_KIND_LBVH, BvhWalk, NoGen>::type bvh;
   typename std::conditional<KIND == VS_KIND_KD || KIND == VS_KIND_HYBRID, KdWalk, NoGen>::type kd;
   MergeState m, leaves;
-  bool use_brick, inner_active;
+  bool inner_active;
 
   __device__ void init(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz, double tmin,
                        double tmax) {
@@ -534,11 +537,12 @@ struct SegmentSource {
       naive.a = tmin; naive.b = tmax; naive.done = false;
     } else if constexpr (KIND == VS_KIND_GRID) {
       grid.init(r, ix, tmin, tmax);
+    } else if constexpr (KIND == KIND_LBVH_BRICK) {
+      const int n = ix.lbvh_info ? __ldg(ix.lbvh_info) : ix.root + 1;
+      brick.init(r, ix, nx, ny, nz, tmin, tmax, n > 0);
     } else if constexpr (KIND == VS_KIND_LBVH) {
       const int n = ix.lbvh_info ? __ldg(ix.lbvh_info) : ix.root + 1;
-      use_brick = ix.brick_bits != nullptr;
-      if (use_brick) brick.init(r, ix, nx, ny, nz, tmin, tmax, n > 0);
-      else bvh.init(r, ix, n > 0 ? 0 : -1, tmin, tmax);
+      bvh.init(r, ix, n > 0 ? 0 : -1, tmin, tmax);
     } else {
       kd.init(ix, tmin, tmax);
       if constexpr (KIND == VS_KIND_HYBRID) { leaves.init(); inner_active = false; }
@@ -552,8 +556,9 @@ struct SegmentSource {
       return naive.next(x, y, budget);
     } else if constexpr (KIND == VS_KIND_GRID) {
       return grid.next(r, x, y, budget);
+    } else if constexpr (KIND == KIND_LBVH_BRICK) {
+      return brick.next(r, x, y, budget);
     } else if constexpr (KIND == VS_KIND_LBVH) {
-      if (use_brick) return brick.next(r, x, y, budget);
       return bvh.next(r, x, y, budget, flags);
     } else if constexpr (KIND == VS_KIND_KD) {
       return kd.next(r, x, y, budget, flags);
@@ -710,7 +715,12 @@ __global__ void k_traverse_rays(vs_index_desc ix, int nx, int ny, int nz,
     switch (ix.kind) {
       case VS_KIND_NAIVE: traverse_one<VS_KIND_NAIVE>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
       case VS_KIND_GRID: traverse_one<VS_KIND_GRID>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
-      case VS_KIND_LBVH: traverse_one<VS_KIND_LBVH>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
+      case VS_KIND_LBVH:
+        if (ix.brick_bits)
+          traverse_one<KIND_LBVH_BRICK>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags);
+        else
+          traverse_one<VS_KIND_LBVH>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags);
+        break;
       case VS_KIND_KD: traverse_one<VS_KIND_KD>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
       default: traverse_one<VS_KIND_HYBRID>(r, ix, nx, ny, nz, tmin, tmax, o, cap, n, &flags); break;
     }
@@ -822,6 +832,10 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
                                   rgba64_opt, samples_opt, total_opt, flags);
       break;
     case VS_KIND_LBVH:
+      if (ix->brick_bits)
+        launch_render<KIND_LBVH_BRICK>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows,
+                                       rgba8, rgba64_opt, samples_opt, total_opt, flags);
+      else
       launch_render<VS_KIND_LBVH>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
                                   rgba64_opt, samples_opt, total_opt, flags);
       break;
