@@ -202,6 +202,9 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
               int32_t* samples_opt, unsigned long long* total_opt, int* flags,
               vs_stream_t stream);
 
+/* Renderer turn sizes of the traversal / sampling interleave (<= 0: unbounded). */
+void vs_set_render_tuning(int trav_steps, int samples);
+
 /* Leaf-brick bit grid of an LBVH from its brick_coords (n from n_dev, or cap if NULL). */
 int vs_lbvh_brick_grid(const int32_t* brick_coords, const int* n_dev, int64_t cap, int nbx,
                        int nby, int nbz, uint32_t* bits, vs_stream_t stream);

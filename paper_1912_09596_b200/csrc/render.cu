@@ -604,15 +604,16 @@ struct SegmentSource {
   }
 };
 
-constexpr int TRAV_BUDGET = 16;   // traversal steps per loop turn
-constexpr int SAMPLE_BUDGET = 8;  // lattice samples per loop turn
+// while-while turn sizes (vs_set_render_tuning): traversal steps / lattice samples per turn
+static int g_trav_budget = 16, g_sample_budget = 8;
 
 template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     k_render(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, const float* __restrict__ lut,
              const double* __restrict__ corr, double dt, int nearest, vs_rows_desc rows,
              uint8_t* __restrict__ rgba8, double* __restrict__ rgba64, int32_t* __restrict__ samples,
-             unsigned long long* __restrict__ total, int* __restrict__ flags_out) {
+             unsigned long long* __restrict__ total, int* __restrict__ flags_out, int trav_budget,
+             int sample_budget) {
   __shared__ RenderSmem sm;
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
   for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
@@ -652,13 +653,13 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
       // instructions instead of serialising whole traversals against whole sample loops.
       while (true) {
         if (!I.active) {
-          int budget = TRAV_BUDGET;
+          int budget = trav_budget;
           double a, b;
           const int g = src.next(r, ix, a, b, budget, &flags);
           if (g == 0) break;
           if (g == 1) I.begin(a, b);
         }
-        if (I.active) I.run(SAMPLE_BUDGET);
+        if (I.active) I.run(sample_budget);
       }
     }
     taken = I.taken;
@@ -784,7 +785,8 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                           uint8_t* rgba8, double* rgba64, int32_t* samples,
                           unsigned long long* total, int* flags) {
   k_render<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
-                                                          rgba8, rgba64, samples, total, flags);
+                                                          rgba8, rgba64, samples, total, flags,
+                                                          g_trav_budget, g_sample_budget);
 }
 
 }  // namespace vs
@@ -851,6 +853,11 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
       return fail_arg("vs_render: kind");
   }
   return check_launch("k_render");
+}
+
+void vs_set_render_tuning(int trav_steps, int samples) {
+  g_trav_budget = trav_steps > 0 ? trav_steps : (1 << 30);
+  g_sample_budget = samples > 0 ? samples : (1 << 30);
 }
 
 int vs_lbvh_brick_grid(const int32_t* brick_coords, const int* n_dev, int64_t cap, int nbx,

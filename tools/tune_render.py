@@ -1,0 +1,34 @@
+"""Sweep the renderer's traversal/sampling turn sizes on a 1080p frame (dev tool)."""
+import sys, json
+sys.path.insert(0, ".")
+import torch
+import paper_1912_09596_b200 as vs
+from paper_1912_09596_b200 import _lib
+from paper_1912_09596_b200.synth import gen_blobs_u8
+from paper_1912_09596_b200.render import RenderTarget, render_rows, index_desc, volume_desc, camera_desc
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+kinds = sys.argv[2].split(",") if len(sys.argv) > 2 else ["lbvh", "grid", "naive"]
+u8 = gen_blobs_u8((n, n, n), n=max(1, 25600 * n**3 // 1024**3), seed=7, sigma=3.0)
+v = vs.Volume(u8)
+tf = vs.TransferFunction.ramp(0.3)
+b = vs.classify(v, tf, dilate=True)
+cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=1920, height=1080)
+res = {}
+for kind in kinds:
+    idx = vs.build_index(kind, b)
+    tgt = RenderTarget(1920, 1080)
+    d = index_desc(idx); vd = volume_desc(v); cd = camera_desc(cam)
+    for tb, sb in [(0, 0), (4, 4), (8, 8), (16, 8), (32, 16), (64, 32), (16, 64), (128, 128), (0, 16)]:
+        _lib.lib().vs_set_render_tuning(tb, sb)
+        render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        res[f"{kind} {tb}/{sb}"] = ms
+        print(kind, tb, sb, round(ms, 2), flush=True)
+print(json.dumps(res))
