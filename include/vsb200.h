@@ -151,7 +151,15 @@ typedef struct vs_volume_desc {
   const uint8_t* bins;   /* u8 LUT bins, C-order                                      */
   const float* field;    /* float32 field, or NULL when the field is f32(bin/255) exactly */
   int nx, ny, nz, pad;
+  /* optional trilinear gather volume (u8 volumes): per voxel the 2x2 (y, z) neighbourhood
+   * {(y,z), (y,z+1), (y+1,z), (y+1,z+1)} (+1 clamped) packed in one uint32, so a trilinear
+   * sample is two 32-bit loads instead of eight byte loads.  Built by vs_build_quads. */
+  const uint32_t* quads;
 } vs_volume_desc;
+
+/* Trilinear gather volume for vs_volume_desc.quads: quads[(x*ny + y)*nz + z] (4 B / voxel). */
+int vs_build_quads(const uint8_t* bins, int nx, int ny, int nz, uint32_t* quads,
+                   vs_stream_t stream);
 
 /* An index for traversal (render.py:41, index_kind :44-55).
  * grid / hybrid: occ (ncx,ncy,ncz) bool bytes, cell size cs (svt.py:29-37).

@@ -106,6 +106,7 @@ struct Integrator {
   const RenderSmem* sm;
   const uint8_t* __restrict__ bins;
   const float* __restrict__ field;  // null: u8 field f32(u/255)
+  const uint32_t* __restrict__ quads;  // optional packed (y,z) 2x2 neighbourhoods
   int nx, ny, nz;
   double entry, dt;
   bool nearest;
@@ -152,6 +153,34 @@ struct Integrator {
       yi = yi < 0 ? 0 : (yi > ny - 1 ? ny - 1 : yi);
       zi = zi < 0 ? 0 : (zi > nz - 1 ? nz - 1 : zi);
       value = (double)fetch(xi * sx + yi * sy + zi);
+    } else if (quads) {
+      // trilinear at p - 0.5 (render.py:694-744) from two packed 2x2 (y, z) neighbourhoods
+      const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
+      const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
+      const double fx = qx - flx, fy = qy - fly, fz = qz - flz;
+      const int x0r = (int)flx, y0r = (int)fly, z0r = (int)flz;
+      const int x0 = x0r < 0 ? 0 : (x0r > nx - 1 ? nx - 1 : x0r);
+      const int x1 = x0r + 1 < 0 ? 0 : (x0r + 1 > nx - 1 ? nx - 1 : x0r + 1);
+      const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
+      const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
+      const int64_t yz = (int64_t)y0 * nz + z0, sxq = (int64_t)ny * nz;
+      uint32_t w0 = __ldg(quads + (int64_t)x0 * sxq + yz);
+      uint32_t w1 = __ldg(quads + (int64_t)x1 * sxq + yz);
+      if (y0r < 0) { w0 = __byte_perm(w0, 0, 0x1010); w1 = __byte_perm(w1, 0, 0x1010); }
+      if (z0r < 0) { w0 = __byte_perm(w0, 0, 0x2200); w1 = __byte_perm(w1, 0, 0x2200); }
+      const float c000 = u8f(w0 & 0xffu), c001 = u8f((w0 >> 8) & 0xffu);
+      const float c010 = u8f((w0 >> 16) & 0xffu), c011 = u8f(w0 >> 24);
+      const float c100 = u8f(w1 & 0xffu), c101 = u8f((w1 >> 8) & 0xffu);
+      const float c110 = u8f((w1 >> 16) & 0xffu), c111 = u8f(w1 >> 24);
+      const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
+      const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
+      const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, fx));
+      const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, fx));
+      const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, fx));
+      const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, fx));
+      const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, fy));
+      const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, fy));
+      value = __dadd_rn(c0, __dmul_rn(c1 - c0, fz));
     } else {
       const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
       int64_t x0 = (int64_t)floor(qx), y0 = (int64_t)floor(qy), z0 = (int64_t)floor(qz);
@@ -605,7 +634,7 @@ struct SegmentSource {
 };
 
 // while-while turn sizes (vs_set_render_tuning): traversal steps / lattice samples per turn
-static int g_trav_budget = 16, g_sample_budget = 8;
+static int g_trav_budget = 1, g_sample_budget = 1;
 
 template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
@@ -639,6 +668,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     ray_setup(r, ox, oy, oz, cam);
     Integrator I;
     I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
+    I.quads = vol.field ? nullptr : vol.quads;
     I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
     I.accr = I.accg = I.accb = I.acca = 0.0;
     I.taken = 0;
@@ -752,6 +782,7 @@ __global__ void k_integrate_rays(vs_volume_desc vol, const double* __restrict__ 
   ray_setup(r, origins[3 * q], origins[3 * q + 1], origins[3 * q + 2], c);
   Integrator I;
   I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
+  I.quads = vol.field ? nullptr : vol.quads;
   I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
   I.accr = I.accg = I.accb = I.acca = 0.0;
   I.taken = 0;
@@ -767,6 +798,18 @@ __global__ void k_integrate_rays(vs_volume_desc vol, const double* __restrict__ 
   rgba[4 * q + 2] = I.accb;
   rgba[4 * q + 3] = I.acca;
   samples[q] = I.taken;
+}
+
+__global__ void k_build_quads(const uint8_t* __restrict__ b, int nx, int ny, int nz,
+                              uint32_t* __restrict__ q) {
+  const int64_t n = (int64_t)nx * ny * nz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int z = (int)(i % nz);
+  const int y = (int)((i / nz) % ny);
+  const int64_t dz = z + 1 < nz ? 1 : 0, dy = y + 1 < ny ? nz : 0;
+  const uint32_t v0 = b[i], v1 = b[i + dz], v2 = b[i + dy], v3 = b[i + dy + dz];
+  q[i] = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
 }
 
 __global__ void k_brick_grid(const int32_t* __restrict__ coords, const int* __restrict__ n_dev,
@@ -853,6 +896,14 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
       return fail_arg("vs_render: kind");
   }
   return check_launch("k_render");
+}
+
+int vs_build_quads(const uint8_t* bins, int nx, int ny, int nz, uint32_t* quads,
+                   vs_stream_t stream) {
+  if (!bins || !quads || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_build_quads");
+  const int64_t n = (int64_t)nx * ny * nz;
+  k_build_quads<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(bins, nx, ny, nz, quads);
+  return check_launch("k_build_quads");
 }
 
 void vs_set_render_tuning(int trav_steps, int samples) {

@@ -142,7 +142,7 @@ class Frame:
 # -- C structs (include/vsb200.h) --------------------------------------------------------------
 class VolumeDesc(C.Structure):
     _fields_ = [("bins", C.c_void_p), ("field", C.c_void_p), ("nx", C.c_int), ("ny", C.c_int),
-                ("nz", C.c_int), ("pad", C.c_int)]
+                ("nz", C.c_int), ("pad", C.c_int), ("quads", C.c_void_p)]
 
 
 class IndexDesc(C.Structure):
@@ -164,9 +164,10 @@ class RowsDesc(C.Structure):
     _fields_ = [("nrows", C.c_int), ("stripe", C.c_int), ("nparts", C.c_int), ("part", C.c_int)]
 
 
-def volume_desc(v: Volume) -> VolumeDesc:
+def volume_desc(v: Volume, quads: bool = True) -> VolumeDesc:
     nx, ny, nz = v.dims
-    return VolumeDesc(ptr(v.bins), ptr(v.field), nx, ny, nz, 0)
+    q = v.quads() if (quads and v.field is None) else None
+    return VolumeDesc(ptr(v.bins), ptr(v.field), nx, ny, nz, 0, ptr(q))
 
 
 def camera_desc(cam: Camera) -> CameraDesc:

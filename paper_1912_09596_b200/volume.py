@@ -116,6 +116,16 @@ class Volume:
     def is_u8(self) -> bool:
         return self.field is None
 
+    def quads(self) -> torch.Tensor:
+        """Trilinear gather volume (4 B/voxel, TF-independent; vs_build_quads), built once."""
+        q = self.__dict__.get("_quads")
+        if q is None:
+            nx, ny, nz = self._dims
+            q = torch.empty(self._dims, dtype=torch.int32, device=self.bins.device)
+            call("vs_build_quads", ptr(self.bins), nx, ny, nz, ptr(q), stream())
+            self.__dict__["_quads"] = q
+        return q
+
     def bounds(self) -> Aabb:
         return Aabb((0, 0, 0), self.dims)
 

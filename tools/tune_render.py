@@ -19,7 +19,7 @@ for kind in kinds:
     idx = vs.build_index(kind, b)
     tgt = RenderTarget(1920, 1080)
     d = index_desc(idx); vd = volume_desc(v); cd = camera_desc(cam)
-    for tb, sb in [(0, 0), (4, 4), (8, 8), (16, 8), (32, 16), (64, 32), (16, 64), (128, 128), (0, 16)]:
+    for tb, sb in [(1, 1), (2, 2), (1, 2), (2, 1), (1, 4), (4, 1), (2, 4), (4, 2), (3, 3), (4, 4)]:
         _lib.lib().vs_set_render_tuning(tb, sb)
         render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
         torch.cuda.synchronize()
