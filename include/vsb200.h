@@ -207,8 +207,12 @@ typedef struct vs_rows_desc {
 int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camera_desc* cam,
               const float* lut, const double* corr, double dt, int nearest,
               const vs_rows_desc* rows_opt, uint8_t* rgba8, double* rgba64_opt,
-              int32_t* samples_opt, unsigned long long* total_opt, int* flags,
-              vs_stream_t stream);
+              int32_t* samples_opt, unsigned long long* total_opt, int* flags, void* ws,
+              size_t ws_bytes, int seg_cap, vs_stream_t stream);
+/* Two-phase rendering (ws != NULL, seg_cap > 0): a traversal kernel stores each ray's merged
+ * segments (up to seg_cap; rays with more are re-traversed inside the integration kernel),
+ * then an integration kernel consumes them.  Workspace bytes for npix pixels: */
+size_t vs_render_workspace(int64_t npix, int seg_cap);
 
 /* Renderer turn sizes of the traversal / sampling interleave (<= 0: unbounded). */
 void vs_set_render_tuning(int trav_steps, int samples);

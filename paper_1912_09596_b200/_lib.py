@@ -49,7 +49,8 @@ SIGNATURES: dict[str, tuple] = {
     "vs_set_render_tuning": (None, [i32, i32]),
     "vs_build_quads": (i32, [P, i32, i32, i32, P, P]),
     "vs_lbvh_brick_grid": (i32, [P, P, i64, i32, i32, i32, P, P]),
-    "vs_render": (i32, [P, P, P, P, P, C.c_double, i32, P, P, P, P, P, P, P]),
+    "vs_render": (i32, [P, P, P, P, P, C.c_double, i32, P, P, P, P, P, P, P, SZ, i32, P]),
+    "vs_render_workspace": (SZ, [i64, i32]),
     "vs_traverse_rays": (i32, [P, i32, i32, i32, P, P, i32, P, i32, P, P, P]),
     "vs_integrate_rays": (i32, [P, P, P, P, P, i32, i32, P, P, C.c_double, i32, P, P, P]),
     "vs_lbvh_from_bricks": (i32, [P, P, i64, i32, i32, i32, i32, P, P, P, P, P, P, P, P, SZ,

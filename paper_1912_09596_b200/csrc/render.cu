@@ -711,6 +711,122 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
   }
 }
 
+// ---- two-phase render: traversal kernel writes each ray's merged segments, the integration
+// kernel consumes them (no traversal/sampling divergence inside one warp).  Rays with more
+// than `cap` segments are re-traversed by the fused path inside the integration kernel.
+__device__ __forceinline__ void pixel_ray(const vs_camera_desc& cam, const vs_rows_desc& rows,
+                                          int i, int l, Ray& r) {
+  const int s = l / rows.stripe, w = l % rows.stripe;
+  const int j = (s * rows.nparts + rows.part) * rows.stripe + w;
+  const double xs = __dmul_rn(((double)i + 0.5) - (double)cam.width / 2.0, cam.scale);
+  const double ys = __dmul_rn(((double)cam.height / 2.0 - (double)j) - 0.5, cam.scale);
+  const double ox = __dadd_rn(__dadd_rn(cam.eye[0], __dmul_rn(ys, cam.up[0])), __dmul_rn(xs, cam.right[0]));
+  const double oy = __dadd_rn(__dadd_rn(cam.eye[1], __dmul_rn(ys, cam.up[1])), __dmul_rn(xs, cam.right[1]));
+  const double oz = __dadd_rn(__dadd_rn(cam.eye[2], __dmul_rn(ys, cam.up[2])), __dmul_rn(xs, cam.right[2]));
+  ray_setup(r, ox, oy, oz, cam);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
+    k_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
+               double2* __restrict__ segs, int* __restrict__ counts, int cap,
+               int* __restrict__ flags_out) {
+  const int i = blockIdx.x * RENDER_TX + threadIdx.x;
+  const int l = blockIdx.y * RENDER_TY + threadIdx.y;
+  if (i >= cam.width || l >= rows.nrows) return;
+  const int64_t pix = (int64_t)l * cam.width + i;
+  const int64_t npix = (int64_t)rows.nrows * cam.width;
+  Ray r;
+  pixel_ray(cam, rows, i, l, r);
+  int n = 0, flags = 0;
+  double tmin, tmax;
+  if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+    SegmentSource<KIND> src;
+    src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
+    while (true) {
+      int budget = 1 << 30;
+      double a, b;
+      const int g = src.next(r, ix, a, b, budget, &flags);
+      if (g == 0) break;
+      if (n < cap) segs[(int64_t)n * npix + pix] = make_double2(a, b);
+      ++n;
+    }
+  }
+  counts[pix] = n;
+  if (flags) atomicOr(flags_out, flags);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
+    k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
+                         const float* __restrict__ lut, const double* __restrict__ corr, double dt,
+                         int nearest, vs_rows_desc rows, const double2* __restrict__ segs,
+                         const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
+                         double* __restrict__ rgba64, int32_t* __restrict__ samples,
+                         unsigned long long* __restrict__ total, int* __restrict__ flags_out) {
+  __shared__ RenderSmem sm;
+  const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
+  for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
+    sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
+    sm.corr[k] = corr[k];
+    sm.u8f[k] = 0.0f;
+  }
+  __syncthreads();
+  const int i = blockIdx.x * RENDER_TX + threadIdx.x;
+  const int l = blockIdx.y * RENDER_TY + threadIdx.y;
+  int64_t taken = 0;
+  int flags = 0;
+  if (i < cam.width && l < rows.nrows) {
+    const int64_t pix = (int64_t)l * cam.width + i;
+    const int64_t npix = (int64_t)rows.nrows * cam.width;
+    Ray r;
+    pixel_ray(cam, rows, i, l, r);
+    Integrator I;
+    I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
+    I.quads = vol.field ? nullptr : vol.quads;
+    I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
+    I.accr = I.accg = I.accb = I.acca = 0.0;
+    I.taken = 0;
+    I.active = false;
+    const int n = counts[pix];
+    double tmin, tmax;
+    if (n > 0 && slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+      I.entry = tmin;
+      if (n <= cap) {
+        for (int q = 0; q < n; ++q) {
+          const double2 sg = segs[(int64_t)q * npix + pix];
+          I.segment(sg.x, sg.y);
+        }
+      } else {  // overflow: fused traversal + integration for this ray
+        SegmentSource<KIND> src;
+        src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
+        while (true) {
+          int budget = 1 << 30;
+          double a, b;
+          const int g = src.next(r, ix, a, b, budget, &flags);
+          if (g == 0) break;
+          I.segment(a, b);
+        }
+      }
+    }
+    taken = I.taken;
+    const double acc[4] = {I.accr, I.accg, I.accb, I.acca};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double q = floor(__dadd_rn(__dmul_rn(acc[c], 255.0), 0.5));
+      rgba8[4 * pix + c] = (uint8_t)(q < 0.0 ? 0 : (q > 255.0 ? 255 : (int)q));
+      if (rgba64) rgba64[4 * pix + c] = acc[c];
+    }
+    if (samples) samples[pix] = (int32_t)taken;
+  }
+  if (flags) atomicOr(flags_out, flags);
+  if (total) {
+    unsigned long long t = (unsigned long long)taken;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((tid & 31) == 0 && t) atomicAdd(total, t);
+  }
+}
+
 // Single-ray traversal (render.py:917-961): the merged interval list of each ray.
 template <int KIND>
 __device__ void traverse_one(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz,
@@ -821,12 +937,26 @@ __global__ void k_brick_grid(const int32_t* __restrict__ coords, const int* __re
   atomicOr(bits + (lin >> 5), 1u << (lin & 31));
 }
 
+static thread_local void* g_seg_ws = nullptr;  // set by vs_render for its own launches
+static thread_local int g_seg_cap = 0;
+
 template <int K>
 static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                           const vs_index_desc& ix, const vs_camera_desc& c, const float* lut,
                           const double* corr, double dt, int nearest, const vs_rows_desc& rows,
                           uint8_t* rgba8, double* rgba64, int32_t* samples,
                           unsigned long long* total, int* flags) {
+  if (g_seg_ws && g_seg_cap > 0) {
+    const int64_t npix = (int64_t)rows.nrows * c.width;
+    double2* segs = static_cast<double2*>(g_seg_ws);
+    int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
+    k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, segs, counts,
+                                                               g_seg_cap, flags);
+    k_integrate_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+        v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
+        total, flags);
+    return;
+  }
   k_render<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
                                                           rgba8, rgba64, samples, total, flags,
                                                           g_trav_budget, g_sample_budget);
@@ -838,11 +968,16 @@ using namespace vs;
 
 extern "C" {
 
+size_t vs_render_workspace(int64_t npix, int seg_cap) {
+  if (npix <= 0 || seg_cap <= 0) return 0;
+  return (size_t)npix * seg_cap * 16 + (size_t)npix * 4 + 256;
+}
+
 int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camera_desc* cam,
               const float* lut, const double* corr, double dt, int nearest,
               const vs_rows_desc* rows_opt, uint8_t* rgba8, double* rgba64_opt,
-              int32_t* samples_opt, unsigned long long* total_opt, int* flags,
-              vs_stream_t stream) {
+              int32_t* samples_opt, unsigned long long* total_opt, int* flags, void* ws,
+              size_t ws_bytes, int seg_cap, vs_stream_t stream) {
   if (!vol || !ix || !cam || !lut || !corr || !rgba8 || !flags || !(dt > 0.0))
     return fail_arg("vs_render");
   if (!vol->bins || vol->nx < 1 || vol->ny < 1 || vol->nz < 1) return fail_arg("vs_render: volume");
@@ -867,6 +1002,16 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
     return fail_arg("vs_render: kd");
   dim3 grid((unsigned)cdiv(cam->width, RENDER_TX), (unsigned)cdiv(rows.nrows, RENDER_TY));
   cudaStream_t st = S(stream);
+  const int64_t npix = (int64_t)rows.nrows * cam->width;
+  if (ws && seg_cap > 0) {
+    if (ws_bytes < vs_render_workspace(npix, seg_cap)) return VS_EWORKSPACE;
+    if ((reinterpret_cast<uintptr_t>(ws) & 15) != 0) return fail_arg("vs_render: ws alignment");
+    g_seg_ws = ws;
+    g_seg_cap = seg_cap;
+  } else {
+    g_seg_ws = nullptr;
+    g_seg_cap = 0;
+  }
   switch (kind) {
     case VS_KIND_NAIVE:
       launch_render<VS_KIND_NAIVE>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,

@@ -233,11 +233,19 @@ def _check_flags(flags: torch.Tensor):
         raise RuntimeError("non-monotone interval emission (streaming merge would differ)")
 
 
-class RenderTarget:
-    """Device output buffers for render_rows (reused across frames)."""
+SEG_CAP = 16  # segments per ray kept between the traversal and integration kernels
 
-    def __init__(self, width: int, nrows: int, want_rgba64=False, want_samples=False):
+
+class RenderTarget:
+    """Device output buffers for render_rows (reused across frames), plus the two-phase
+    segment workspace (``seg_cap`` = 0 selects the fused single-kernel path)."""
+
+    def __init__(self, width: int, nrows: int, want_rgba64=False, want_samples=False,
+                 seg_cap: int = SEG_CAP):
         dev = _lib.device()
+        self.seg_cap = int(seg_cap)
+        wsb = _lib.query("vs_render_workspace", width * nrows, self.seg_cap)
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
         self.rgba8 = torch.empty((nrows, width, 4), dtype=torch.uint8, device=dev)
         self.rgba64 = torch.empty((nrows, width, 4), dtype=torch.float64, device=dev) \
             if want_rgba64 else None
@@ -262,7 +270,8 @@ def render_rows(v: Volume, tf: TransferFunction, index, cam: Camera, target: Ren
     call("vs_render", C.addressof(vol_desc), C.addressof(idx_desc), C.addressof(cam_desc),
          ptr(lut), ptr(corr), float(dt), int(nearest),
          None if rows is None else C.addressof(rows), ptr(target.rgba8), ptr(target.rgba64),
-         ptr(target.samples), ptr(target.total), ptr(target.flags), stream())
+         ptr(target.samples), ptr(target.total), ptr(target.flags), ptr(target.ws),
+         0 if target.ws is None else target.ws.numel(), target.seg_cap, stream())
 
 
 def render_frame(v: Volume, tf: TransferFunction, index, cam: Camera, dt: float = DEFAULT_DT,

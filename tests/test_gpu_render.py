@@ -244,3 +244,23 @@ def test_quad_gather_equals_byte_gather(vs, az, el):
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     orgba, osamples = O.render("naive", u8, tf.lut, None, cam, nthreads=4)
     np.testing.assert_array_equal(outs[1][0], orgba)
+
+
+@pytest.mark.parametrize("kind", ["naive", "grid", "lbvh", "kd-deep-mls32", "hybrid"])
+def test_two_phase_equals_fused(vs, blobs64, kind):
+    """Two-phase rendering (segment buffer, incl. overflow re-traversal at cap 1) == fused."""
+    from paper_1912_09596_b200.render import RenderTarget, render_rows
+
+    v = vs.Volume(blobs64["u8"])
+    tf = vs.TransferFunction(blobs64["ramp03_lut"])
+    idx = _index(vs, kind, blobs64, "ramp03_", v, tf)
+    cam = _cam_from(vs, blobs64, 96, 64)
+    outs = []
+    for cap in (0, 1, 16):
+        tgt = RenderTarget(cam.width, cam.height, want_rgba64=True, want_samples=True, seg_cap=cap)
+        render_rows(v, tf, idx, cam, tgt)
+        outs.append((tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy()))
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o[1], outs[0][1])
+        np.testing.assert_array_equal(o[0], outs[0][0])
+    np.testing.assert_array_equal(outs[0][1], blobs64[f"ramp03_render_{kind}_samples"])
