@@ -216,6 +216,8 @@ size_t vs_render_workspace(int64_t npix, int seg_cap);
 
 /* Renderer turn sizes of the traversal / sampling interleave (<= 0: unbounded). */
 void vs_set_render_tuning(int trav_steps, int samples);
+/* Renderer code-path options (bit 0: u8 -> f32 via a shared-memory table); same results. */
+void vs_set_render_options(int opts);
 
 /* Leaf-brick bit grid of an LBVH from its brick_coords (n from n_dev, or cap if NULL). */
 int vs_lbvh_brick_grid(const int32_t* brick_coords, const int* n_dev, int64_t cap, int nbx,

@@ -107,6 +107,7 @@ struct Integrator {
   const uint8_t* __restrict__ bins;
   const float* __restrict__ field;  // null: u8 field f32(u/255)
   const uint32_t* __restrict__ quads;  // optional packed (y,z) 2x2 neighbourhoods
+  bool idx32, use_tab;
   int nx, ny, nz;
   double entry, dt;
   bool nearest;
@@ -163,15 +164,32 @@ struct Integrator {
       const int x1 = x0r + 1 < 0 ? 0 : (x0r + 1 > nx - 1 ? nx - 1 : x0r + 1);
       const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
       const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
-      const int64_t yz = (int64_t)y0 * nz + z0, sxq = (int64_t)ny * nz;
-      uint32_t w0 = __ldg(quads + (int64_t)x0 * sxq + yz);
-      uint32_t w1 = __ldg(quads + (int64_t)x1 * sxq + yz);
+      uint32_t w0, w1;
+      if (idx32) {  // < 2^32 voxels: 32-bit offsets
+        const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
+        const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
+        w0 = __ldg(quads + ((uint32_t)x0 * sxq + yz));
+        w1 = __ldg(quads + ((uint32_t)x1 * sxq + yz));
+      } else {
+        const int64_t yz = (int64_t)y0 * nz + z0, sxq = (int64_t)ny * nz;
+        w0 = __ldg(quads + (int64_t)x0 * sxq + yz);
+        w1 = __ldg(quads + (int64_t)x1 * sxq + yz);
+      }
       if (y0r < 0) { w0 = __byte_perm(w0, 0, 0x1010); w1 = __byte_perm(w1, 0, 0x1010); }
       if (z0r < 0) { w0 = __byte_perm(w0, 0, 0x2200); w1 = __byte_perm(w1, 0, 0x2200); }
-      const float c000 = u8f(w0 & 0xffu), c001 = u8f((w0 >> 8) & 0xffu);
-      const float c010 = u8f((w0 >> 16) & 0xffu), c011 = u8f(w0 >> 24);
-      const float c100 = u8f(w1 & 0xffu), c101 = u8f((w1 >> 8) & 0xffu);
-      const float c110 = u8f((w1 >> 16) & 0xffu), c111 = u8f(w1 >> 24);
+      float c000, c001, c010, c011, c100, c101, c110, c111;
+      if (use_tab) {  // shared-memory table of f32(u/255) (same values, MIO instead of XU)
+        const float* tb = sm->u8f;
+        c000 = tb[w0 & 0xffu]; c001 = tb[(w0 >> 8) & 0xffu];
+        c010 = tb[(w0 >> 16) & 0xffu]; c011 = tb[w0 >> 24];
+        c100 = tb[w1 & 0xffu]; c101 = tb[(w1 >> 8) & 0xffu];
+        c110 = tb[(w1 >> 16) & 0xffu]; c111 = tb[w1 >> 24];
+      } else {
+        c000 = u8f(w0 & 0xffu); c001 = u8f((w0 >> 8) & 0xffu);
+        c010 = u8f((w0 >> 16) & 0xffu); c011 = u8f(w0 >> 24);
+        c100 = u8f(w1 & 0xffu); c101 = u8f((w1 >> 8) & 0xffu);
+        c110 = u8f((w1 >> 16) & 0xffu); c111 = u8f(w1 >> 24);
+      }
       const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
       const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
       const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, fx));
@@ -635,6 +653,7 @@ struct SegmentSource {
 
 // while-while turn sizes (vs_set_render_tuning): traversal steps / lattice samples per turn
 static int g_trav_budget = 1, g_sample_budget = 1;
+static int g_render_opts = 0;  // bit0: u8 -> f32 by shared-memory table
 
 template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
@@ -642,7 +661,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
              const double* __restrict__ corr, double dt, int nearest, vs_rows_desc rows,
              uint8_t* __restrict__ rgba8, double* __restrict__ rgba64, int32_t* __restrict__ samples,
              unsigned long long* __restrict__ total, int* __restrict__ flags_out, int trav_budget,
-             int sample_budget) {
+             int sample_budget, int render_opts) {
   __shared__ RenderSmem sm;
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
   for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
@@ -669,6 +688,8 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     Integrator I;
     I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
     I.quads = vol.field ? nullptr : vol.quads;
+    I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
+    I.use_tab = (render_opts & 1) != 0;
     I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
     I.accr = I.accg = I.accb = I.acca = 0.0;
     I.taken = 0;
@@ -763,13 +784,14 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
                          int nearest, vs_rows_desc rows, const double2* __restrict__ segs,
                          const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
                          double* __restrict__ rgba64, int32_t* __restrict__ samples,
-                         unsigned long long* __restrict__ total, int* __restrict__ flags_out) {
+                         unsigned long long* __restrict__ total, int* __restrict__ flags_out,
+                         int render_opts) {
   __shared__ RenderSmem sm;
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
   for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
     sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
     sm.corr[k] = corr[k];
-    sm.u8f[k] = 0.0f;
+    sm.u8f[k] = (float)((double)k / 255.0);
   }
   __syncthreads();
   const int i = blockIdx.x * RENDER_TX + threadIdx.x;
@@ -784,6 +806,8 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     Integrator I;
     I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
     I.quads = vol.field ? nullptr : vol.quads;
+    I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
+    I.use_tab = (render_opts & 1) != 0;
     I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
     I.accr = I.accg = I.accb = I.acca = 0.0;
     I.taken = 0;
@@ -883,6 +907,7 @@ __global__ void k_integrate_rays(vs_volume_desc vol, const double* __restrict__ 
                                  const float* __restrict__ lut, const double* __restrict__ corr,
                                  double dt, int nearest, double* __restrict__ rgba,
                                  long long* __restrict__ samples) {
+  const int render_opts = 0;
   __shared__ RenderSmem sm;
   for (int k = threadIdx.x; k < 256; k += blockDim.x) {
     sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
@@ -899,6 +924,8 @@ __global__ void k_integrate_rays(vs_volume_desc vol, const double* __restrict__ 
   Integrator I;
   I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
   I.quads = vol.field ? nullptr : vol.quads;
+    I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
+    I.use_tab = (render_opts & 1) != 0;
   I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
   I.accr = I.accg = I.accb = I.acca = 0.0;
   I.taken = 0;
@@ -954,12 +981,13 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                                                                g_seg_cap, flags);
     k_integrate_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
         v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
-        total, flags);
+        total, flags, g_render_opts);
     return;
   }
   k_render<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
                                                           rgba8, rgba64, samples, total, flags,
-                                                          g_trav_budget, g_sample_budget);
+                                                          g_trav_budget, g_sample_budget,
+                                                          g_render_opts);
 }
 
 }  // namespace vs
@@ -1050,6 +1078,8 @@ int vs_build_quads(const uint8_t* bins, int nx, int ny, int nz, uint32_t* quads,
   k_build_quads<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(bins, nx, ny, nz, quads);
   return check_launch("k_build_quads");
 }
+
+void vs_set_render_options(int opts) { g_render_opts = opts; }
 
 void vs_set_render_tuning(int trav_steps, int samples) {
   g_trav_budget = trav_steps > 0 ? trav_steps : (1 << 30);

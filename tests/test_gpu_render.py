@@ -264,3 +264,20 @@ def test_two_phase_equals_fused(vs, blobs64, kind):
         np.testing.assert_array_equal(o[1], outs[0][1])
         np.testing.assert_array_equal(o[0], outs[0][0])
     np.testing.assert_array_equal(outs[0][1], blobs64[f"ramp03_render_{kind}_samples"])
+
+
+def test_u8_table_option_equal(vs, blobs64):
+    from paper_1912_09596_b200 import _lib
+
+    v = vs.Volume(blobs64["u8"])
+    tf = vs.TransferFunction(blobs64["ramp03_lut"])
+    cam = _cam_from(vs, blobs64, 96, 64)
+    outs = []
+    try:
+        for opts in (0, 1):
+            _lib.lib().vs_set_render_options(opts)
+            outs.append(vs.render_float(v, tf, None, cam))
+    finally:
+        _lib.lib().vs_set_render_options(0)
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[1][0], blobs64["ramp03_render_naive_rgba"])

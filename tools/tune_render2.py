@@ -20,7 +20,8 @@ for t in ts:
     for kind in kinds:
         idx = vs.build_index(kind, b)
         d = index_desc(idx); vd = volume_desc(v); cd = camera_desc(cam)
-        for cap in (0, 8, 16, 32):
+        for opts, cap in [(o, c) for o in (0, 1) for c in (0, 32)]:
+            _lib.lib().vs_set_render_options(opts)
             tgt = RenderTarget(1920, 1080, seg_cap=cap)
             render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
             torch.cuda.synchronize()
@@ -30,6 +31,6 @@ for t in ts:
                 render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
             e1.record(); torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 3
-            res[f"{kind} t={t} cap={cap}"] = (ms, int(tgt.total.item()))
-            print(kind, t, cap, round(ms, 2), int(tgt.total.item()), flush=True)
+            res[f"{kind} t={t} opts={opts} cap={cap}"] = (ms, int(tgt.total.item()))
+            print(kind, t, "opts", opts, "cap", cap, round(ms, 2), int(tgt.total.item()), flush=True)
 print(json.dumps(res))
