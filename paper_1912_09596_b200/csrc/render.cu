@@ -142,7 +142,23 @@ struct Integrator {
     active = t < t1;
   }
 
+  // first lattice index with entry + k*dt >= t0 (render.py:664-671)
+  __device__ __forceinline__ int64_t first_k(double t0) const {
+    int64_t kk = (int64_t)ceil(__ddiv_rn(t0 - entry, dt));
+    if (kk < 0) kk = 0;
+    while (kk > 0 && __dadd_rn(entry, __dmul_rn((double)(kk - 1), dt)) >= t0) kk--;
+    while (__dadd_rn(entry, __dmul_rn((double)kk, dt)) < t0) kk++;
+    return kk;
+  }
+
   __device__ __forceinline__ void sample() {
+    sample_at();
+    ++k;
+    t = __dadd_rn(entry, __dmul_rn((double)k, dt));
+  }
+
+  // one lattice sample at the current t (no lattice advance)
+  __device__ __forceinline__ void sample_at() {
     const int64_t sy = nz, sx = (int64_t)ny * nz;
     const double px = __dadd_rn(r->ox, __dmul_rn(t, r->dx));
     const double py = __dadd_rn(r->oy, __dmul_rn(t, r->dy));
@@ -237,8 +253,6 @@ struct Integrator {
       acca = __dadd_rn(acca, w);
     }
     ++taken;
-    ++k;
-    t = __dadd_rn(entry, __dmul_rn((double)k, dt));
   }
 
   __device__ __forceinline__ void run(int smax) {
@@ -653,7 +667,7 @@ struct SegmentSource {
 
 // while-while turn sizes (vs_set_render_tuning): traversal steps / lattice samples per turn
 static int g_trav_budget = 1, g_sample_budget = 1;
-static int g_render_opts = 0;  // bit0: u8 -> f32 by shared-memory table
+static int g_render_opts = 1;  // bit0: u8 -> f32 by shared-memory table
 
 template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
@@ -750,7 +764,7 @@ __device__ __forceinline__ void pixel_ray(const vs_camera_desc& cam, const vs_ro
 template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     k_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
-               double2* __restrict__ segs, int* __restrict__ counts, int cap,
+               double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
                int* __restrict__ flags_out) {
   const int i = blockIdx.x * RENDER_TX + threadIdx.x;
   const int l = blockIdx.y * RENDER_TY + threadIdx.y;
@@ -764,13 +778,26 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
   if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
     SegmentSource<KIND> src;
     src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
+    Integrator L;  // lattice only: k ranges of the merged segments
+    L.entry = tmin;
+    L.dt = dt;
+    int kprev = -1;
     while (true) {
       int budget = 1 << 30;
       double a, b;
       const int g = src.next(r, ix, a, b, budget, &flags);
       if (g == 0) break;
-      if (n < cap) segs[(int64_t)n * npix + pix] = make_double2(a, b);
-      ++n;
+      // samples of [a, b) are lattice indices [first_k(a), first_k(b)); ranges are disjoint
+      // and increasing, so abutting ones are joined
+      const int k0 = (int)L.first_k(a), k1 = (int)L.first_k(b);
+      if (k1 <= k0) continue;
+      if (n > 0 && k0 == kprev && n <= cap) {
+        segs[(int64_t)(n - 1) * npix + pix].y = k1;
+      } else {
+        if (n < cap) segs[(int64_t)n * npix + pix] = make_int2(k0, k1);
+        ++n;
+      }
+      kprev = k1;
     }
   }
   counts[pix] = n;
@@ -781,7 +808,7 @@ template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
                          const float* __restrict__ lut, const double* __restrict__ corr, double dt,
-                         int nearest, vs_rows_desc rows, const double2* __restrict__ segs,
+                         int nearest, vs_rows_desc rows, const int2* __restrict__ segs,
                          const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
                          double* __restrict__ rgba64, int32_t* __restrict__ samples,
                          unsigned long long* __restrict__ total, int* __restrict__ flags_out,
@@ -817,9 +844,20 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     if (n > 0 && slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
       I.entry = tmin;
       if (n <= cap) {
-        for (int q = 0; q < n; ++q) {
-          const double2 sg = segs[(int64_t)q * npix + pix];
-          I.segment(sg.x, sg.y);
+        // flat sample loop: each turn either samples or switches to the next lattice range
+        int q = 0;
+        int2 kr = segs[pix];
+        int k = kr.x;
+        while (true) {
+          if (k < kr.y) {
+            I.t = __dadd_rn(I.entry, __dmul_rn((double)k, dt));
+            I.sample_at();
+            ++k;
+          } else {
+            if (++q >= n) break;
+            kr = segs[(int64_t)q * npix + pix];
+            k = kr.x;
+          }
         }
       } else {  // overflow: fused traversal + integration for this ray
         SegmentSource<KIND> src;
@@ -975,9 +1013,9 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                           unsigned long long* total, int* flags) {
   if (g_seg_ws && g_seg_cap > 0) {
     const int64_t npix = (int64_t)rows.nrows * c.width;
-    double2* segs = static_cast<double2*>(g_seg_ws);
+    int2* segs = static_cast<int2*>(g_seg_ws);
     int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
-    k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, segs, counts,
+    k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs, counts,
                                                                g_seg_cap, flags);
     k_integrate_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
         v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
@@ -998,7 +1036,7 @@ extern "C" {
 
 size_t vs_render_workspace(int64_t npix, int seg_cap) {
   if (npix <= 0 || seg_cap <= 0) return 0;
-  return (size_t)npix * seg_cap * 16 + (size_t)npix * 4 + 256;
+  return (size_t)npix * seg_cap * 8 + (size_t)npix * 4 + 256;
 }
 
 int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camera_desc* cam,

@@ -233,7 +233,7 @@ def _check_flags(flags: torch.Tensor):
         raise RuntimeError("non-monotone interval emission (streaming merge would differ)")
 
 
-SEG_CAP = 16  # segments per ray kept between the traversal and integration kernels
+SEG_CAP = 32  # lattice ranges per ray kept between the traversal and integration kernels
 
 
 class RenderTarget:
