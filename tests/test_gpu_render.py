@@ -281,3 +281,30 @@ def test_u8_table_option_equal(vs, blobs64):
         _lib.lib().vs_set_render_options(0)
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     np.testing.assert_array_equal(outs[1][0], blobs64["ramp03_render_naive_rgba"])
+
+
+@pytest.mark.parametrize("kind", ["naive", "grid", "lbvh", "kd-deep-mls32", "hybrid"])
+def test_persistent_two_phase_equal(vs, blobs64, kind):
+    """Persistent-lane two-phase rendering (render option bit 1) == fused, incl. overflow."""
+    from paper_1912_09596_b200 import _lib
+    from paper_1912_09596_b200.render import RenderTarget, render_rows
+
+    v = vs.Volume(blobs64["u8"])
+    tf = vs.TransferFunction(blobs64["ramp03_lut"])
+    idx = _index(vs, kind, blobs64, "ramp03_", v, tf)
+    cam = _cam_from(vs, blobs64, 96, 64)
+    outs = []
+    try:
+        for opts, cap in ((1, 0), (3, 1), (3, 32)):
+            _lib.lib().vs_set_render_options(opts)
+            tgt = RenderTarget(cam.width, cam.height, want_rgba64=True, want_samples=True,
+                               seg_cap=cap)
+            render_rows(v, tf, idx, cam, tgt)
+            outs.append((tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy(),
+                         int(tgt.total.item())))
+    finally:
+        _lib.lib().vs_set_render_options(1)
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o[1], outs[0][1])
+        np.testing.assert_array_equal(o[0], outs[0][0])
+        assert o[2] == outs[0][2]
