@@ -157,6 +157,81 @@ struct Integrator {
     t = __dadd_rn(entry, __dmul_rn((double)k, dt));
   }
 
+  // ---- quad-gather trilinear split in two halves so the next sample's loads can be issued
+  // before the current sample's arithmetic (render.py:694-744) ----
+  struct Gather {
+    uint32_t w0, w1;
+    double fx, fy, fz;
+  };
+  __device__ __forceinline__ void gather(double tt, Gather& g) const {
+    const double px = __dadd_rn(r->ox, __dmul_rn(tt, r->dx));
+    const double py = __dadd_rn(r->oy, __dmul_rn(tt, r->dy));
+    const double pz = __dadd_rn(r->oz, __dmul_rn(tt, r->dz));
+    const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
+    const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
+    g.fx = qx - flx; g.fy = qy - fly; g.fz = qz - flz;
+    const int x0r = (int)flx, y0r = (int)fly, z0r = (int)flz;
+    const int x0 = x0r < 0 ? 0 : (x0r > nx - 1 ? nx - 1 : x0r);
+    const int x1 = x0r + 1 < 0 ? 0 : (x0r + 1 > nx - 1 ? nx - 1 : x0r + 1);
+    const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
+    const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
+    uint32_t w0, w1;
+    if (idx32) {  // < 2^32 voxels: 32-bit offsets
+      const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
+      const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
+      w0 = __ldg(quads + ((uint32_t)x0 * sxq + yz));
+      w1 = __ldg(quads + ((uint32_t)x1 * sxq + yz));
+    } else {
+      const int64_t yz = (int64_t)y0 * nz + z0, sxq = (int64_t)ny * nz;
+      w0 = __ldg(quads + (int64_t)x0 * sxq + yz);
+      w1 = __ldg(quads + (int64_t)x1 * sxq + yz);
+    }
+    // clamped low borders: the +1 neighbour is the voxel itself
+    if (y0r < 0) { w0 = __byte_perm(w0, 0, 0x1010); w1 = __byte_perm(w1, 0, 0x1010); }
+    if (z0r < 0) { w0 = __byte_perm(w0, 0, 0x2200); w1 = __byte_perm(w1, 0, 0x2200); }
+    g.w0 = w0;
+    g.w1 = w1;
+  }
+  __device__ __forceinline__ double interp(const Gather& g) const {
+    const uint32_t w0 = g.w0, w1 = g.w1;
+    float c000, c001, c010, c011, c100, c101, c110, c111;
+    if (use_tab) {  // shared-memory table of f32(u/255) (same values, MIO instead of XU)
+      const float* tb = sm->u8f;
+      c000 = tb[w0 & 0xffu]; c001 = tb[(w0 >> 8) & 0xffu];
+      c010 = tb[(w0 >> 16) & 0xffu]; c011 = tb[w0 >> 24];
+      c100 = tb[w1 & 0xffu]; c101 = tb[(w1 >> 8) & 0xffu];
+      c110 = tb[(w1 >> 16) & 0xffu]; c111 = tb[w1 >> 24];
+    } else {
+      c000 = u8f(w0 & 0xffu); c001 = u8f((w0 >> 8) & 0xffu);
+      c010 = u8f((w0 >> 16) & 0xffu); c011 = u8f(w0 >> 24);
+      c100 = u8f(w1 & 0xffu); c101 = u8f((w1 >> 8) & 0xffu);
+      c110 = u8f((w1 >> 16) & 0xffu); c111 = u8f(w1 >> 24);
+    }
+    const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
+    const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
+    const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, g.fx));
+    const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, g.fx));
+    const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, g.fx));
+    const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, g.fx));
+    const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, g.fy));
+    const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, g.fy));
+    return __dadd_rn(c0, __dmul_rn(c1 - c0, g.fz));
+  }
+  // classification + front-to-back compositing of one interpolated value (render.py:745-758)
+  __device__ __forceinline__ void shade(double value) {
+    const double bd = floor(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
+    const int bin = bd < 0.0 ? 0 : (bd > 255.0 ? 255 : (int)bd);
+    const float4 c = sm->lut[bin];
+    if (c.w > 0.0f) {
+      const double w = __dmul_rn(1.0 - acca, sm->corr[bin]);
+      accr = __dadd_rn(accr, __dmul_rn(w, (double)c.x));
+      accg = __dadd_rn(accg, __dmul_rn(w, (double)c.y));
+      accb = __dadd_rn(accb, __dmul_rn(w, (double)c.z));
+      acca = __dadd_rn(acca, w);
+    }
+    ++taken;
+  }
+
   // one lattice sample at the current t (no lattice advance)
   __device__ __forceinline__ void sample_at() {
     const int64_t sy = nz, sx = (int64_t)ny * nz;
@@ -171,50 +246,9 @@ struct Integrator {
       zi = zi < 0 ? 0 : (zi > nz - 1 ? nz - 1 : zi);
       value = (double)fetch(xi * sx + yi * sy + zi);
     } else if (quads) {
-      // trilinear at p - 0.5 (render.py:694-744) from two packed 2x2 (y, z) neighbourhoods
-      const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
-      const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
-      const double fx = qx - flx, fy = qy - fly, fz = qz - flz;
-      const int x0r = (int)flx, y0r = (int)fly, z0r = (int)flz;
-      const int x0 = x0r < 0 ? 0 : (x0r > nx - 1 ? nx - 1 : x0r);
-      const int x1 = x0r + 1 < 0 ? 0 : (x0r + 1 > nx - 1 ? nx - 1 : x0r + 1);
-      const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
-      const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
-      uint32_t w0, w1;
-      if (idx32) {  // < 2^32 voxels: 32-bit offsets
-        const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
-        const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
-        w0 = __ldg(quads + ((uint32_t)x0 * sxq + yz));
-        w1 = __ldg(quads + ((uint32_t)x1 * sxq + yz));
-      } else {
-        const int64_t yz = (int64_t)y0 * nz + z0, sxq = (int64_t)ny * nz;
-        w0 = __ldg(quads + (int64_t)x0 * sxq + yz);
-        w1 = __ldg(quads + (int64_t)x1 * sxq + yz);
-      }
-      if (y0r < 0) { w0 = __byte_perm(w0, 0, 0x1010); w1 = __byte_perm(w1, 0, 0x1010); }
-      if (z0r < 0) { w0 = __byte_perm(w0, 0, 0x2200); w1 = __byte_perm(w1, 0, 0x2200); }
-      float c000, c001, c010, c011, c100, c101, c110, c111;
-      if (use_tab) {  // shared-memory table of f32(u/255) (same values, MIO instead of XU)
-        const float* tb = sm->u8f;
-        c000 = tb[w0 & 0xffu]; c001 = tb[(w0 >> 8) & 0xffu];
-        c010 = tb[(w0 >> 16) & 0xffu]; c011 = tb[w0 >> 24];
-        c100 = tb[w1 & 0xffu]; c101 = tb[(w1 >> 8) & 0xffu];
-        c110 = tb[(w1 >> 16) & 0xffu]; c111 = tb[w1 >> 24];
-      } else {
-        c000 = u8f(w0 & 0xffu); c001 = u8f((w0 >> 8) & 0xffu);
-        c010 = u8f((w0 >> 16) & 0xffu); c011 = u8f(w0 >> 24);
-        c100 = u8f(w1 & 0xffu); c101 = u8f((w1 >> 8) & 0xffu);
-        c110 = u8f((w1 >> 16) & 0xffu); c111 = u8f(w1 >> 24);
-      }
-      const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
-      const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
-      const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, fx));
-      const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, fx));
-      const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, fx));
-      const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, fx));
-      const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, fy));
-      const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, fy));
-      value = __dadd_rn(c0, __dmul_rn(c1 - c0, fz));
+      Gather g;
+      gather(t, g);
+      value = interp(g);
     } else {
       const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
       int64_t x0 = (int64_t)floor(qx), y0 = (int64_t)floor(qy), z0 = (int64_t)floor(qz);
@@ -242,17 +276,7 @@ struct Integrator {
       const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, fy));
       value = __dadd_rn(c0, __dmul_rn(c1 - c0, fz));
     }
-    const double bd = floor(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
-    const int bin = bd < 0.0 ? 0 : (bd > 255.0 ? 255 : (int)bd);
-    const float4 c = sm->lut[bin];
-    if (c.w > 0.0f) {
-      const double w = __dmul_rn(1.0 - acca, sm->corr[bin]);
-      accr = __dadd_rn(accr, __dmul_rn(w, (double)c.x));
-      accg = __dadd_rn(accg, __dmul_rn(w, (double)c.y));
-      accb = __dadd_rn(accb, __dmul_rn(w, (double)c.z));
-      acca = __dadd_rn(acca, w);
-    }
-    ++taken;
+    shade(value);
   }
 
   __device__ __forceinline__ void run(int smax) {
@@ -843,7 +867,33 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     double tmin, tmax;
     if (n > 0 && slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
       I.entry = tmin;
-      if (n <= cap) {
+      if (n <= cap && I.quads && !I.nearest) {
+        // flat sample loop, software-pipelined: the next sample's gather loads are issued
+        // before the current sample's interpolation and compositing
+        int q = 0;
+        int2 kr = segs[pix];
+        int k = kr.x;
+        Integrator::Gather g;
+        bool have = k < kr.y;
+        if (have) I.gather(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
+        while (true) {
+          if (have) {
+            Integrator::Gather gn;
+            const bool hn = k + 1 < kr.y;
+            if (hn) I.gather(__dadd_rn(I.entry, __dmul_rn((double)(k + 1), dt)), gn);
+            I.shade(I.interp(g));
+            ++k;
+            if (hn) g = gn;
+            have = hn;
+          } else {
+            if (++q >= n) break;
+            kr = segs[(int64_t)q * npix + pix];
+            k = kr.x;
+            have = k < kr.y;
+            if (have) I.gather(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
+          }
+        }
+      } else if (n <= cap) {
         // flat sample loop: each turn either samples or switches to the next lattice range
         int q = 0;
         int2 kr = segs[pix];
