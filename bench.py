@@ -414,7 +414,7 @@ def run_ours(args, rank, ws, local):
                "render_ms": est["render_s"] * 1e3}
     clocks = clk.summary()
     launches_per_step = 5 + 1  # summary, summary_to_bitmap, leaves, karras, refit, brick grid
-    launches_per_step += 1     # k_render
+    launches_per_step += 2     # k_segments (traversal), k_integrate_segments (sampling)
     line = {
         "metric": METRIC,
         "value": 1e3 / ms_per_step,
@@ -435,7 +435,8 @@ def run_ours(args, rank, ws, local):
         "build_ms": build_ms,
         "render_ms": render_ms,
         "render": {"fps": 1e3 / render_ms, "samples_per_frame": samples,
-                   "Msamples_s": samples / render_ms / 1e3, "kernel": "k_render<LBVH>"},
+                   "Msamples_s": samples / render_ms / 1e3,
+                   "kernels": "k_segments<LBVH brick DDA> + k_integrate_segments"},
         "summary_kernel_ms": summ_ms,
         "n_bricks": n_bricks, "lbvh_nodes": max(2 * n_bricks - 1, 0), "lbvh_height": height,
         "parity_index_vs_public_api": bool(parity),
