@@ -109,7 +109,7 @@ struct Integrator {
   const uint32_t* __restrict__ quads;  // optional packed (y,z) 2x2 neighbourhoods
   bool idx32, use_tab;
   int nx, ny, nz;
-  double entry, dt;
+  double entry, dt, inv_dt;
   bool nearest;
   double accr, accg, accb, acca;
   int64_t taken;
@@ -132,19 +132,18 @@ struct Integrator {
   }
 
   __device__ __forceinline__ void begin(double t0, double t1_) {
-    int64_t kk = (int64_t)ceil(__ddiv_rn(t0 - entry, dt));
-    if (kk < 0) kk = 0;
-    while (kk > 0 && __dadd_rn(entry, __dmul_rn((double)(kk - 1), dt)) >= t0) kk--;
-    while (__dadd_rn(entry, __dmul_rn((double)kk, dt)) < t0) kk++;
+    const int64_t kk = first_k(t0);
     k = kk;
     t = __dadd_rn(entry, __dmul_rn((double)kk, dt));
     t1 = t1_;
     active = t < t1;
   }
 
-  // first lattice index with entry + k*dt >= t0 (render.py:664-671)
+  // first lattice index with entry + k*dt >= t0 (render.py:664-671).  The reference's
+  // fix-up loops make the result the smallest k >= 0 with t_k >= t0 whatever the initial
+  // guess, so the guess uses a multiply by 1/dt instead of the division.
   __device__ __forceinline__ int64_t first_k(double t0) const {
-    int64_t kk = (int64_t)ceil(__ddiv_rn(t0 - entry, dt));
+    int64_t kk = (int64_t)ceil(__dmul_rn(t0 - entry, inv_dt));
     if (kk < 0) kk = 0;
     while (kk > 0 && __dadd_rn(entry, __dmul_rn((double)(kk - 1), dt)) >= t0) kk--;
     while (__dadd_rn(entry, __dmul_rn((double)kk, dt)) < t0) kk++;
@@ -691,7 +690,9 @@ struct SegmentSource {
 
 // while-while turn sizes (vs_set_render_tuning): traversal steps / lattice samples per turn
 static int g_trav_budget = 1, g_sample_budget = 1;
-static int g_render_opts = 1;  // bit0: u8 -> f32 by shared-memory table
+// bit0: u8 -> f32 by shared-memory table; bit1: persistent traversal lanes;
+// bit2: persistent traversal + integration lanes
+static int g_render_opts = 1;
 
 template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
@@ -728,7 +729,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     I.quads = vol.field ? nullptr : vol.quads;
     I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
     I.use_tab = (render_opts & 1) != 0;
-    I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
+    I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
     I.accr = I.accg = I.accb = I.acca = 0.0;
     I.taken = 0;
     I.active = false;
@@ -805,6 +806,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     Integrator L;  // lattice only: k ranges of the merged segments
     L.entry = tmin;
     L.dt = dt;
+    L.inv_dt = 1.0 / dt;
     int kprev = -1;
     while (true) {
       int budget = 1 << 30;
@@ -859,7 +861,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     I.quads = vol.field ? nullptr : vol.quads;
     I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
     I.use_tab = (render_opts & 1) != 0;
-    I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
+    I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
     I.accr = I.accg = I.accb = I.acca = 0.0;
     I.taken = 0;
     I.active = false;
@@ -974,6 +976,7 @@ __global__ void __launch_bounds__(128)
       Integrator L;
       L.entry = tmin;
       L.dt = dt;
+      L.inv_dt = 1.0 / dt;
       int kprev = -1;
       while (true) {
         int budget = 1 << 30;
@@ -1021,7 +1024,7 @@ __global__ void __launch_bounds__(128)
   I.quads = vol.field ? nullptr : vol.quads;
   I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
   I.use_tab = (render_opts & 1) != 0;
-  I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
+  I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
   int64_t pix = -1;
   int n = 0, q = 0, k = 0;
   int2 kr = make_int2(0, 0);
@@ -1163,7 +1166,7 @@ __global__ void k_integrate_rays(vs_volume_desc vol, const double* __restrict__ 
   I.quads = vol.field ? nullptr : vol.quads;
     I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
     I.use_tab = (render_opts & 1) != 0;
-  I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.nearest = nearest != 0;
+  I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
   I.accr = I.accg = I.accb = I.acca = 0.0;
   I.taken = 0;
   const int m = counts[q];
@@ -1210,7 +1213,7 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                           const double* corr, double dt, int nearest, const vs_rows_desc& rows,
                           uint8_t* rgba8, double* rgba64, int32_t* samples,
                           unsigned long long* total, int* flags) {
-  if (g_seg_ws && g_seg_cap > 0 && (g_render_opts & 2)) {  // persistent two-phase
+  if (g_seg_ws && g_seg_cap > 0 && (g_render_opts & 4)) {  // persistent two-phase
     const int64_t npix = (int64_t)rows.nrows * c.width;
     int2* segs = static_cast<int2*>(g_seg_ws);
     int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
@@ -1230,8 +1233,17 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     const int64_t npix = (int64_t)rows.nrows * c.width;
     int2* segs = static_cast<int2*>(g_seg_ws);
     int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
-    k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs, counts,
-                                                               g_seg_cap, flags);
+    if (g_render_opts & 2) {  // persistent traversal lanes
+      unsigned long long* queues = reinterpret_cast<unsigned long long*>(
+          (reinterpret_cast<uintptr_t>(counts + npix) + 15) & ~uintptr_t(15));
+      cudaMemsetAsync(queues, 0, sizeof(unsigned long long), st);
+      const int64_t nids = (int64_t)grid.x * grid.y * RENDER_TX * RENDER_TY;
+      k_segments_p<K><<<148 * 8, 128, 0, st>>>(v, ix, c, rows, dt, segs, counts, g_seg_cap,
+                                               queues, nids, flags);
+    } else {
+      k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
+                                                                 counts, g_seg_cap, flags);
+    }
     k_integrate_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
         v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
         total, flags, g_render_opts);

@@ -20,7 +20,7 @@ for t in ts:
     for kind in kinds:
         idx = vs.build_index(kind, b)
         d = index_desc(idx); vd = volume_desc(v); cd = camera_desc(cam)
-        for opts, cap in [(1, 0), (1, 32)]:
+        for opts, cap in [(1, 32), (3, 32)]:
             _lib.lib().vs_set_render_options(opts)  # noqa
             tgt = RenderTarget(1920, 1080, seg_cap=cap)
             render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
