@@ -790,7 +790,7 @@ template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     k_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
                double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
-               int* __restrict__ flags_out) {
+               int* __restrict__ flags_out, int step_budget) {
   const int i = blockIdx.x * RENDER_TX + threadIdx.x;
   const int l = blockIdx.y * RENDER_TY + threadIdx.y;
   if (i >= cam.width || l >= rows.nrows) return;
@@ -809,10 +809,12 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     L.inv_dt = 1.0 / dt;
     int kprev = -1;
     while (true) {
-      int budget = 1 << 30;
+      // a bounded number of traversal steps per turn keeps the warp's lanes in one flat loop
+      int budget = step_budget;
       double a, b;
       const int g = src.next(r, ix, a, b, budget, &flags);
       if (g == 0) break;
+      if (g == 2) continue;
       // samples of [a, b) are lattice indices [first_k(a), first_k(b)); ranges are disjoint
       // and increasing, so abutting ones are joined
       const int k0 = (int)L.first_k(a), k1 = (int)L.first_k(b);
@@ -1242,7 +1244,8 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                                                queues, nids, flags);
     } else {
       k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                 counts, g_seg_cap, flags);
+                                                                 counts, g_seg_cap, flags,
+                                                                 g_trav_budget);
     }
     k_integrate_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
         v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,

@@ -20,8 +20,9 @@ for t in ts:
     for kind in kinds:
         idx = vs.build_index(kind, b)
         d = index_desc(idx); vd = volume_desc(v); cd = camera_desc(cam)
-        for opts, cap in [(1, 32), (3, 32)]:
+        for opts, cap, tb in [(1, 32, 1), (1, 32, 2), (1, 32, 4), (1, 32, 1 << 30)]:
             _lib.lib().vs_set_render_options(opts)  # noqa
+            _lib.lib().vs_set_render_tuning(tb, 1)
             tgt = RenderTarget(1920, 1080, seg_cap=cap)
             render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
             torch.cuda.synchronize()
@@ -31,6 +32,6 @@ for t in ts:
                 render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
             e1.record(); torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 3
-            res[f"{kind} t={t} opts={opts} cap={cap}"] = (ms, int(tgt.total.item()))
-            print(kind, t, "opts", opts, "cap", cap, round(ms, 2), int(tgt.total.item()), flush=True)
+            res[f"{kind} t={t} opts={opts} cap={cap} tb={tb}"] = (ms, int(tgt.total.item()))
+            print(kind, t, "opts", opts, "cap", cap, "tb", tb, round(ms, 2), int(tgt.total.item()), flush=True)
 print(json.dumps(res))
