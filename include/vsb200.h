@@ -258,6 +258,17 @@ int vs_kd_result_copy(void* handle, int32_t* lo, int32_t* hi, int8_t* axis, int3
                       int32_t* left, int32_t* right, vs_stream_t stream);
 void vs_kd_result_free(void* handle);
 
+/* precompute_cell_boxes (kdtree.py:285-320) in C order: per cell of edge cs, the tight box of
+ * its flags (lo, hi (n,3) int32, global voxel coords; empty cells get the reference's
+ * placeholders lo = c*cs, hi = (c+1)*cs) and occupied (n,) bool bytes.  Synchronous. */
+int vs_cell_boxes(const uint32_t* bits, int nx, int ny, int nz, int cs, int32_t* lo, int32_t* hi,
+                  uint8_t* occupied, vs_stream_t stream);
+/* sweep_best_plane (binned = 0; kdtree.py:244-262) or binned_best_plane (binned = 1;
+ * kdtree.py:371-381) for one box (host int[6] lo3 hi3).  out (host long long[4]) =
+ * {found, axis, position, cost}.  Synchronous. */
+int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* box_host,
+                     int binned, int bins, int cs, long long* out_host, vs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

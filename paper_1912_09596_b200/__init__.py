@@ -7,7 +7,8 @@ hand-written CUDA kernels in libvsb200.so (include/vsb200.h).  There is no CPU f
 
 from .bench import INDEX_KINDS, build_index, index_kind, report_stats
 from .hybrid import HybridGrid, build_hybrid
-from .kdtree import BuildParams, KdTree, SplitPlane, build_kdtree, empty_kdtree
+from .kdtree import (BuildParams, CellBoxList, KdTree, SplitPlane, binned_best_plane, build_kdtree,
+                     empty_kdtree, precompute_cell_boxes, sweep_best_plane)
 from .lbvh import (BrickSet, Lbvh, MortonRangeError, build_lbvh, empty_lbvh, flag_bricks,
                    leaf_boxes, morton_decode, morton_encode)
 from .render import (DEFAULT_DT, Camera, Frame, Ray, RaySegmentList, integrate, render_float,

@@ -46,6 +46,8 @@ SIGNATURES: dict[str, tuple] = {
     "vs_kd_result_info": (i32, [P, P, P, P]),
     "vs_kd_result_copy": (i32, [P, P, P, P, P, P, P, P]),
     "vs_kd_result_free": (None, [P]),
+    "vs_cell_boxes": (i32, [P, i32, i32, i32, i32, P, P, P, P]),
+    "vs_kd_best_plane": (i32, [P, i32, i32, i32, P, i32, i32, i32, P, P]),
     "vs_set_render_tuning": (None, [i32, i32]),
     "vs_set_render_options": (None, [i32]),
     "vs_build_quads": (i32, [P, i32, i32, i32, P, P]),

@@ -1135,3 +1135,195 @@ int vs_kd_result_copy(void* handle, int32_t* lo, int32_t* hi, int8_t* axis, int3
 void vs_kd_result_free(void* handle) { delete static_cast<KdResultImpl*>(handle); }
 
 }  // extern "C"
+
+// ---- single-box plane searches (sweep_best_plane kdtree.py:244-262, binned_best_plane
+//      kdtree.py:371-381): the level machinery on a one-node level ----------------------------
+namespace vs {
+
+__global__ void k_best_plane(KdLevel L, KdParams P, const Span* __restrict__ span_x,
+                             const Span* __restrict__ span_y, const Span* __restrict__ span_z,
+                             RBox* __restrict__ scratch, BinnedCtx B, long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  const Box b = L.box[0];
+  const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
+  long long found = 0, axis = -1, pos = 0, cost = 0;
+  if (!P.binned) {
+    const Span* sp[3] = {span_x, span_y, span_z};
+    const RBox t = range_box(span_x, 0, ext[0], lane);
+    if (t.hi0 >= 0) {
+      const int64_t tv = rvol(t);  // _region_tight_volume
+      int ba = -1, bk = 0;
+      int64_t bc = 0;
+      for (int a = 0; a < 3; ++a) {
+        if (ext[a] < 2) continue;
+        int k;
+        int64_t c;
+        sweep_axis(sp[a], ext[a], scratch, lane, k, c);
+        if (ba >= 0 && c >= bc) continue;
+        ba = a; bk = k; bc = c;
+      }
+      if (ba >= 0 && bc < tv) { found = 1; axis = ba; pos = b.lo[ba] + bk; cost = bc; }
+    }
+  } else {
+    Box target;
+    if (cells_reduce(B, 0, b, 0, b, P.cs, lane, target)) {
+      int ba = -1, bp = 0;
+      int64_t bc = 0;
+      for (int a = 0; a < 3; ++a) {
+        int ps[64];
+        const int np = snapped_positions(b.lo[a], b.hi[a], P.bins, P.cs, ps);
+        for (int q = 0; q < np; ++q) {
+          Box lreg = b, rreg = b, lb, rb;
+          lreg.hi[a] = ps[q];
+          rreg.lo[a] = ps[q];
+          const bool l = cells_reduce(B, 0, b, a, lreg, P.cs, lane, lb);
+          const bool r = cells_reduce(B, 0, b, a, rreg, P.cs, lane, rb);
+          const int64_t c = (l ? box_vol(lb) : 0) + (r ? box_vol(rb) : 0);
+          if (ba < 0 || c < bc) { ba = a; bp = ps[q]; bc = c; }
+        }
+      }
+      if (ba >= 0 && bc < box_vol(target)) { found = 1; axis = ba; pos = bp; cost = bc; }
+    }
+  }
+  if (lane == 0) { out[0] = found; out[1] = axis; out[2] = pos; out[3] = cost; }
+}
+
+// precompute_cell_boxes layout (kdtree.py:285-320): C-order lo/hi with the reference's
+// placeholders for empty cells (lo = c*cs, hi = (c+1)*cs, unclipped).
+__global__ void k_cell_box_rows(const CBox* __restrict__ cells, int ncx, int ncy, int ncz, int cs,
+                                int32_t* __restrict__ lo, int32_t* __restrict__ hi,
+                                uint8_t* __restrict__ occ) {
+  const int64_t n = (int64_t)ncx * ncy * ncz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cz = (int)(i % ncz), cy = (int)((i / ncz) % ncy), cx = (int)(i / ((int64_t)ncz * ncy));
+  const int c[3] = {cx, cy, cz};
+  const CBox v = cells[i];
+  const bool o = v.lo[0] != KD_FAR;
+  occ[i] = o;
+  for (int k = 0; k < 3; ++k) {
+    lo[3 * i + k] = o ? v.lo[k] : c[k] * cs;
+    hi[3 * i + k] = o ? v.hi[k] : (c[k] + 1) * cs;
+  }
+}
+
+}  // namespace vs
+
+extern "C" {
+
+int vs_cell_boxes(const uint32_t* bits, int nx, int ny, int nz, int cs, int32_t* lo, int32_t* hi,
+                  uint8_t* occupied, vs_stream_t stream) {
+  if (!bits || !lo || !hi || !occupied || nx < 1 || ny < 1 || nz < 1 || cs < 1)
+    return fail_arg("vs_cell_boxes");
+  cudaStream_t st = S(stream);
+  const int ncx = (int)cdiv(nx, cs), ncy = (int)cdiv(ny, cs), ncz = (int)cdiv(nz, cs);
+  const int64_t n = (int64_t)ncx * ncy * ncz;
+  DBuf cells;
+  cells.st = st;
+  VS_TRY(cells.ensure(n * sizeof(CBox), "cells"));
+  k_cell_boxes<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy, ncz,
+                                                       cells.as<CBox>());
+  VS_TRY(check_launch("k_cell_boxes"));
+  k_cell_box_rows<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(cells.as<CBox>(), ncx, ncy, ncz, cs, lo,
+                                                          hi, occupied);
+  VS_TRY(check_launch("k_cell_box_rows"));
+  VS_CUDA(cudaStreamSynchronize(st), "sync");
+  return 0;
+}
+
+int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* box_host,
+                     int binned, int bins, int cs, long long* out_host, vs_stream_t stream) {
+  if (!bits || !box_host || !out_host || nx < 1 || ny < 1 || nz < 1 || bins < 2 || bins > 65 ||
+      cs < 1)
+    return fail_arg("vs_kd_best_plane");
+  if (nz > 1024) return fail_arg("vs_kd_best_plane: nz > 1024");
+  cudaStream_t st = S(stream);
+  out_host[0] = 0; out_host[1] = -1; out_host[2] = 0; out_host[3] = 0;
+  Box b;
+  const int dims[3] = {nx, ny, nz};
+  for (int k = 0; k < 3; ++k) { b.lo[k] = box_host[k]; b.hi[k] = box_host[3 + k]; }
+  if (!binned) {  // sweep_best_plane clips the box to the volume first
+    for (int k = 0; k < 3; ++k) {
+      b.lo[k] = std::max(b.lo[k], 0);
+      b.hi[k] = std::min(b.hi[k], dims[k]);
+      if (b.lo[k] >= b.hi[k]) return 0;
+    }
+  }
+  const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
+  for (int k = 0; k < 3; ++k)
+    if (ext[k] <= 0) return 0;
+  const int wz = (ext[2] + 31) / 32;
+  const int ncx = (int)cdiv(nx, cs), ncy = (int)cdiv(ny, cs), ncz = (int)cdiv(nz, cs);
+  const int nc[3] = {ncx, ncy, ncz};
+  DBuf lev, spx, spy, spz, pxz, pyz, scr, cellb, cslab, res;
+  for (DBuf* d : {&lev, &spx, &spy, &spz, &pxz, &pyz, &scr, &cellb, &cslab, &res}) d->st = st;
+  // one-node level: box, need, 12 offset arrays of 2 entries
+  struct Host {
+    Box box;
+    int need;
+    int pad;
+    int64_t off[12][2];
+  } h;
+  memset(&h, 0, sizeof h);
+  h.box = b;
+  h.need = 1;
+  const int64_t sizes[6] = {ext[0], ext[1], ext[2], (int64_t)ext[0] * wz, (int64_t)ext[1] * wz, wz};
+  for (int k = 0; k < 6; ++k) h.off[k][1] = sizes[k];
+  int64_t csz[3];
+  for (int a = 0; a < 3; ++a) {
+    int c0 = std::max(b.lo[a] / cs, 0), c1 = std::min((b.hi[a] - 1) / cs, nc[a] - 1);
+    csz[a] = std::max(c1 - c0 + 1, 0);
+    h.off[7 + a][1] = csz[a];
+  }
+  VS_TRY(lev.ensure(sizeof h, "level"));
+  VS_CUDA(cudaMemcpyAsync(lev.p, &h, sizeof h, cudaMemcpyHostToDevice, st), "level copy");
+  Host* d = lev.as<Host>();
+  KdLevel L;
+  L.n = 1; L.box = &d->box; L.need = &d->need;
+  L.off_x = d->off[0]; L.off_y = d->off[1]; L.off_z = d->off[2];
+  L.off_pxz = d->off[3]; L.off_pyz = d->off[4]; L.off_zw = d->off[5];
+  KdParams P;
+  P.deep = 1; P.mls = -1; P.binned = binned; P.bins = bins; P.cs = cs; P.root_vol = 0;
+  BinnedCtx B;
+  B.nc[0] = ncx; B.nc[1] = ncy; B.nc[2] = ncz;
+  const int nzw = (int)nzw_of(nz);
+  VS_TRY(res.ensure(4 * sizeof(long long), "result"));
+  VS_TRY(scr.ensure((std::max(ext[0], std::max(ext[1], ext[2])) + 1) * sizeof(RBox), "scratch"));
+  if (!binned) {
+    VS_TRY(spx.ensure((ext[0] + 1) * sizeof(Span), "span_x"));
+    VS_TRY(spy.ensure((ext[1] + 1) * sizeof(Span), "span_y"));
+    VS_TRY(spz.ensure((ext[2] + 32) * sizeof(Span), "span_z"));
+    VS_TRY(pxz.ensure((sizes[3] + 1) * 4, "pxz"));
+    VS_TRY(pyz.ensure((sizes[4] + 1) * 4, "pyz"));
+    k_spans_x<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_x + 1, spx.as<Span>(),
+                                           pxz.as<uint32_t>());
+    k_spans_y<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_y + 1, spy.as<Span>(),
+                                           pyz.as<uint32_t>());
+    k_spans_z<<<SPAN_BLOCKS, 128, 0, st>>>(L, L.off_zw + 1, pxz.as<uint32_t>(), pyz.as<uint32_t>(),
+                                           spz.as<Span>());
+    VS_TRY(check_launch("spans"));
+  } else {
+    const int64_t ncell = (int64_t)ncx * ncy * ncz;
+    VS_TRY(cellb.ensure(ncell * sizeof(CBox), "cells"));
+    k_cell_boxes<<<(unsigned)cdiv(ncell, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy, ncz,
+                                                             cellb.as<CBox>());
+    VS_TRY(cslab.ensure((csz[0] + csz[1] + csz[2] + 3) * sizeof(CBox), "cell slabs"));
+    CBox* cs3[3] = {cslab.as<CBox>(), cslab.as<CBox>() + csz[0] + 1,
+                    cslab.as<CBox>() + csz[0] + csz[1] + 2};
+    for (int a = 0; a < 3; ++a) {
+      k_cell_slabs<<<SPAN_BLOCKS, 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
+                                                d->off[7 + a], d->off[7 + a] + 1, cs3[a]);
+      B.cslab[a] = cs3[a];
+      B.coff[a] = d->off[7 + a];
+    }
+    VS_TRY(check_launch("cell slabs"));
+  }
+  k_best_plane<<<1, 32, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(), spz.as<Span>(),
+                                 scr.as<RBox>(), B, res.as<long long>());
+  VS_TRY(check_launch("k_best_plane"));
+  VS_TRY(d2h(out_host, res.p, 4 * sizeof(long long), st));
+  return 0;
+}
+
+}  // extern "C"

@@ -186,3 +186,73 @@ def build_index_kind(kind: str, b):
     if kind == "hybrid":
         return build_hybrid(build_svt_grid(b), b)
     return build_kdtree(build_svt_grid(b), _KD_PARAMS[kind])
+
+
+@dataclass
+class CellBoxList:
+    """Tight flag bounds of every coarse cell, sorted by cell Morton code (kdtree.py:268-282).
+    Rows for unoccupied cells are placeholders; consult ``occupied`` first."""
+
+    cell_size: int
+    cells_dims: tuple
+    dims: tuple
+    codes: np.ndarray
+    coords: np.ndarray
+    lo: np.ndarray
+    hi: np.ndarray
+    occupied: np.ndarray
+    binary: object = None  # the classification the boxes came from (device bits)
+
+
+def precompute_cell_boxes(b, cell_size: int = DEFAULT_CELL_SIZE) -> CellBoxList:
+    """Per-cell tight boxes in one device pass (vs_cell_boxes), rows in Morton order."""
+    from ._lib import call, ptr, stream
+    from .lbvh import morton_encode
+
+    cs = int(cell_size)
+    dims = b.dims
+    nc = tuple(-(-d // cs) for d in dims)
+    n = nc[0] * nc[1] * nc[2]
+    dev = _lib.device()
+    lo = torch.empty((n, 3), dtype=torch.int32, device=dev)
+    hi = torch.empty((n, 3), dtype=torch.int32, device=dev)
+    occ = torch.empty(n, dtype=torch.uint8, device=dev)
+    call("vs_cell_boxes", ptr(b.packed()), *dims, cs, ptr(lo), ptr(hi), ptr(occ), stream())
+    cx, cy, cz = np.indices(nc)
+    coords = np.stack([cx, cy, cz], axis=-1).reshape(-1, 3)
+    codes = np.asarray(morton_encode(coords[:, 0], coords[:, 1], coords[:, 2]), np.uint32)
+    order = np.argsort(codes, kind="stable")
+    return CellBoxList(cell_size=cs, cells_dims=nc, dims=dims, codes=codes[order],
+                       coords=coords[order].astype(np.int32), lo=lo.cpu().numpy()[order],
+                       hi=hi.cpu().numpy()[order], occupied=occ.cpu().numpy().view(bool)[order],
+                       binary=b)
+
+
+def _best_plane(b, box, binned: int, bins: int, cs: int):
+    import ctypes as C
+
+    from ._lib import call, ptr, stream
+
+    bx = (C.c_int * 6)(*[int(v) for v in list(box.lo) + list(box.hi)])
+    out = (C.c_longlong * 4)()
+    nx, ny, nz = b.dims
+    call("vs_kd_best_plane", ptr(b.packed()), nx, ny, nz, C.addressof(bx), int(binned),
+         int(bins), int(cs), C.addressof(out), stream())
+    if not out[0]:
+        return None
+    return SplitPlane(axis=int(out[1]), position=int(out[2]), cost=int(out[3]))
+
+
+def sweep_best_plane(g, box) -> SplitPlane | None:
+    """Exhaustive search for the cut minimising vol(tight left) + vol(tight right); None when
+    no cut strictly beats the box's own tight volume; ties to the lower axis then position
+    (kdtree.py:244-262)."""
+    return _best_plane(g.binary, box, 0, DEFAULT_BINS, DEFAULT_CELL_SIZE)
+
+
+def binned_best_plane(cells: CellBoxList, box, bins: int = DEFAULT_BINS) -> SplitPlane | None:
+    """bins-1 snapped candidate cuts per axis with child bounds from the per-cell boxes
+    (kdtree.py:371-381)."""
+    if cells.binary is None:
+        raise ValueError("CellBoxList was not built by precompute_cell_boxes")
+    return _best_plane(cells.binary, box, 1, bins, cells.cell_size)

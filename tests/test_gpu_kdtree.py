@@ -141,3 +141,43 @@ def test_empty_and_dense(vs):
     d = vs.BinaryVolume(np.ones((24, 24, 24), bool))  # test_acceptance.py:116-124
     t = vs.build_kdtree(vs.build_svt_grid(d), vs.BuildParams(mode="deep"))
     assert t.node_count == 1 and t.height() == 1
+
+
+@pytest.mark.parametrize("case", ["rand_64x48x40", "blocky48", "sparse64"])
+def test_precompute_cell_boxes(vs, bitcases, case):
+    dims = tuple(int(d) for d in bitcases[f"{case}_dims"])
+    b = vs.BinaryVolume(unpack_bits(bitcases[f"{case}_bits"], dims))
+    cells = vs.precompute_cell_boxes(b, 8)
+    for f in ("codes", "coords", "lo", "hi", "occupied"):
+        np.testing.assert_array_equal(getattr(cells, f), bitcases[f"{case}_cells8_{f}"], err_msg=f)
+
+
+def test_best_plane_apis_vs_reference_semantics(vs, rng):
+    """sweep_best_plane / binned_best_plane on random boxes: the split the k-d builder takes
+    at a root equals the single-box search, and the two-cluster known answer
+    (test_kdtree.py:112-122, 217-231) holds."""
+    bits = np.zeros((64, 24, 24), bool)
+    bits[8:16, 8:16, 8:16] = True
+    bits[40:48, 8:16, 8:16] = True
+    b = vs.BinaryVolume(bits)
+    g = vs.build_svt_grid(b)
+    full = vs.Aabb((0, 0, 0), bits.shape)
+    p = vs.sweep_best_plane(g, full)
+    assert p is not None and p.axis == 0 and 16 <= p.position <= 40 and p.cost == 2 * 512
+    cells = vs.precompute_cell_boxes(b, 8)
+    pb = vs.binned_best_plane(cells, full)
+    assert pb is not None and pb.axis == 0 and pb.cost == 2 * 512
+    assert vs.sweep_best_plane(g, vs.Aabb((0, 0, 0), (4, 4, 4))) is None
+    # a box inside one cluster: no cut beats its tight volume
+    assert vs.sweep_best_plane(g, vs.Aabb((8, 8, 8), (16, 16, 16))) is None
+    # random: the root decision of a deep sweep tree equals the single-box search
+    for seed in range(4):
+        r = np.random.default_rng(seed)
+        bb = r.random((30, 26, 22)) < 0.03
+        bv = vs.BinaryVolume(bb)
+        gg = vs.build_svt_grid(bv)
+        t = vs.build_kdtree(gg, vs.BuildParams(mode="deep"))
+        if t.node_count > 1 and t.axis[0] >= 0:
+            root = vs.Aabb(tuple(t.lo[0]), tuple(t.hi[0]))
+            sp = vs.sweep_best_plane(gg, root)
+            assert sp is not None and (sp.axis, sp.position) == (int(t.axis[0]), int(t.plane[0]))
