@@ -27,6 +27,8 @@ __device__ __forceinline__ int delta(const uint64_t* __restrict__ k, int64_t i, 
   return x == 0 ? 64 : __clzll((long long)x);
 }
 
+// Thread per 32-code bitmap word: rank = tile offset + popcounts of the earlier words of the
+// tile (16-lane segmented warp scan) + bits below in the word; each set bit emits its leaf.
 __global__ void k_leaves_from_bitmap(const uint32_t* __restrict__ bitmap,
                                      const uint32_t* __restrict__ tile_off, int bs, int nx,
                                      int ny, int nz, int64_t ntiles, uint64_t* __restrict__ keys,
@@ -34,38 +36,43 @@ __global__ void k_leaves_from_bitmap(const uint32_t* __restrict__ bitmap,
                                      int32_t* __restrict__ left, int32_t* __restrict__ right,
                                      int32_t* __restrict__ leaf_brick,
                                      int32_t* __restrict__ brick_coords, int* __restrict__ info) {
-  const int64_t tile = blockIdx.x;
-  const uint32_t base = tile_off[tile];
-  const uint32_t cnt = tile_off[tile + 1] - base;
-  if (tile == 0 && threadIdx.x == 0) info[0] = (int)tile_off[ntiles];
-  if (cnt == 0) return;
-  __shared__ uint32_t wpre[16];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const uint32_t word = bitmap[tile * 16 + w];
-  if (lane == 0) wpre[w] = __popc(word);
-  __syncthreads();
-  if (!((word >> lane) & 1u)) return;
-  uint32_t r = __popc(word & ((1u << lane) - 1u));
-  for (int k = 0; k < w; ++k) r += wpre[k];
+  const int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // word index
+  const int64_t nwords = ntiles * 16;
   const int64_t n = tile_off[ntiles];
-  const int64_t p = base + r;
-  const uint32_t code = (uint32_t)(tile * 512 + t);
-  const int bx = (int)compact10(code), by = (int)compact10(code >> 1),
-            bz = (int)compact10(code >> 2);
-  keys[p] = (uint64_t)code << 32;  // low word irrelevant: codes are distinct
-  brick_coords[3 * p] = bx;
-  brick_coords[3 * p + 1] = by;
-  brick_coords[3 * p + 2] = bz;
-  const int64_t row = n - 1 + p;
-  lo[3 * row] = bx * bs;
-  lo[3 * row + 1] = by * bs;
-  lo[3 * row + 2] = bz * bs;
-  hi[3 * row] = min(bx * bs + bs, nx);
-  hi[3 * row + 1] = min(by * bs + bs, ny);
-  hi[3 * row + 2] = min(bz * bs + bs, nz);
-  left[row] = -1;
-  right[row] = -1;
-  leaf_brick[row] = (int32_t)p;
+  if (wi == 0) info[0] = (int)n;
+  uint32_t word = wi < nwords ? __ldg(bitmap + wi) : 0u;
+  const uint32_t c = __popc(word);
+  uint32_t incl = c;
+  const int seg = threadIdx.x & 15;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o, 16);
+    if (seg >= o) incl += u;
+  }
+  if (wi >= nwords || !word) return;
+  int64_t p = (int64_t)tile_off[wi >> 4] + (incl - c);
+  while (word) {
+    const int bit = __ffs(word) - 1;
+    word &= word - 1;
+    const uint32_t code = (uint32_t)(wi * 32 + bit);
+    const int bx = (int)compact10(code), by = (int)compact10(code >> 1),
+              bz = (int)compact10(code >> 2);
+    keys[p] = (uint64_t)code << 32;  // low word irrelevant: codes are distinct
+    brick_coords[3 * p] = bx;
+    brick_coords[3 * p + 1] = by;
+    brick_coords[3 * p + 2] = bz;
+    const int64_t row = n - 1 + p;
+    lo[3 * row] = bx * bs;
+    lo[3 * row + 1] = by * bs;
+    lo[3 * row + 2] = bz * bs;
+    hi[3 * row] = min(bx * bs + bs, nx);
+    hi[3 * row + 1] = min(by * bs + bs, ny);
+    hi[3 * row + 2] = min(bz * bs + bs, nz);
+    left[row] = -1;
+    right[row] = -1;
+    leaf_brick[row] = (int32_t)p;
+    ++p;
+  }
 }
 
 __global__ void k_make_keys(const uint32_t* __restrict__ codes, int64_t n,
@@ -258,9 +265,9 @@ int vs_lbvh_from_bitmap(const uint32_t* bitmap, const uint32_t* tile_counts, int
   VS_CUDA(cudaMemcpyAsync(off, tile_counts, ntiles * 4, cudaMemcpyDeviceToDevice, st), "copy");
   VS_CUDA(cudaMemsetAsync(off + ntiles, 0, 4, st), "memset");
   VS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, sb, off, off, (int)(ntiles + 1), st), "scan");
-  k_leaves_from_bitmap<<<(unsigned)ntiles, 512, 0, st>>>(bitmap, off, bs, nx, ny, nz, ntiles,
-                                                         w.keys, lo, hi, left, right,
-                                                         leaf_brick, brick_coords, info);
+  k_leaves_from_bitmap<<<(unsigned)cdiv(ntiles * 16, 256), 256, 0, st>>>(
+      bitmap, off, bs, nx, ny, nz, ntiles, w.keys, lo, hi, left, right, leaf_brick, brick_coords,
+      info);
   VS_TRY(check_launch("k_leaves_from_bitmap"));
   return tree_and_refit(w, cap, lo, hi, left, right, leaf_brick, info, st);
 }
