@@ -6,9 +6,8 @@ set_tf -> classify -> build_index -> render_frame) on BASELINE.json configs[3]/[
 
   1. the next TF of a 64-entry ramp sweep (thresholds 0.6 -> 0) reaches the device as a
      64-byte parameter block;
-  2. LBVH rebuild: vs_classify_bricks (one pass over the u8 volume, dilated brick votes
-     scattered into a Morton bitmap) -> vs_lbvh_from_bitmap -> vs_lbvh_brick_grid, replayed
-     as one CUDA graph;
+  2. LBVH rebuild: vs_classify_summary (one pass over the u8 volume) -> vs_summary_to_bitmap
+     -> vs_lbvh_from_bitmap -> vs_lbvh_brick_grid, replayed as one CUDA graph;
   3. 1920x1080 render through the new index (camera orbiting 360/64 deg per step, dt 0.5,
      trilinear, FP64 parity arithmetic), rows split in interleaved stripes over the ranks and
      gathered with one NCCL all-gather (N > 1).
@@ -19,8 +18,7 @@ set_tf -> classify -> build_index -> render_frame) on BASELINE.json configs[3]/[
             build_index -> TileRenderer.frame) with the TF uploaded from pinned host memory
             and the frame's pixels read back to the host every step.
   roofline  k_brick_summary, the HBM-bound kernel of the step (the rebuild's compulsory
-            traffic: N^3 u8 read + the Morton brick bitmap written, over its CUDA-event
-            duration).  The
+            traffic: N^3 u8 read + 4 B/brick summary write over its CUDA-event duration).  The
             render kernel is issue-bound, not HBM/tensor-bound; see "render" and DESIGN.md.
   cpu_baseline  the C oracle port of the reference path (oracle/vs_oracle.c): rebuild at full
             size (1 core) + a row sample of the frame render (all cores), scaled to a frame.
@@ -415,7 +413,7 @@ def run_ours(args, rank, ws, local):
                "kind": "port", "sample": est["sample"], "rebuild_ms": est["rebuild_s"] * 1e3,
                "render_ms": est["render_s"] * 1e3}
     clocks = clk.summary()
-    launches_per_step = 4 + 1  # classify_bricks, leaves, karras, refit, brick grid
+    launches_per_step = 5 + 1  # summary, summary_to_bitmap, leaves, karras, refit, brick grid
     launches_per_step += 2     # k_segments (traversal), k_integrate_segments (sampling)
     line = {
         "metric": METRIC,

@@ -73,14 +73,6 @@ int vs_classify_summary(const uint8_t* bins, int nx, int ny, int nz, const vs_tf
                         uint32_t* summary, uint32_t* bits_opt, unsigned long long* count_opt,
                         vs_stream_t stream);
 
-/* The same pass fused with the brick vote: every non-empty brick ORs its 27-bit halo summary
- * straight into the Morton bitmap of the bricks it flags (dilate=1) or itself (dilate=0), and
- * newly set bits bump the tile counts; bitmap/tile_counts are zeroed here.  This is the LBVH
- * rebuild's only pass over the volume (vs_summary_to_bitmap is not needed after it). */
-int vs_classify_bricks(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
-                       int dilate, int P, uint32_t* bitmap, uint32_t* tile_counts,
-                       vs_stream_t stream);
-
 /* Generic-dims classification to packed undilated bits (+ optional visible count). */
 int vs_classify_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
                      uint32_t* bits, unsigned long long* count_opt, vs_stream_t stream);

@@ -162,47 +162,13 @@ __device__ __forceinline__ void summary_slab(const VisEval& ve, const uint8_t* _
   pb = zc3(ylb0, ylb1) | (zc3(yb0, yb1) << 3) | (zc3(yfb0, yfb1) << 6);
 }
 
-// Dilated brick votes straight into the Morton bitmap: brick n with summary S flags every
-// brick n - e whose halo its bit e covers (flag[b] = OR_e S[b+e] bit e); newly set bits bump
-// the 512-code tile counts.  OR is idempotent, so the result is order-independent.
-struct BitmapOut {
-  uint32_t* bitmap;
-  uint32_t* tiles;
-  int dilate;
-};
-
-__device__ __forceinline__ void set_brick(const BitmapOut& o, uint32_t bx, uint32_t by,
-                                          uint32_t bz) {
-  const uint32_t code = morton3(bx, by, bz);
-  const uint32_t bit = 1u << (code & 31);
-  const uint32_t old = atomicOr(o.bitmap + (code >> 5), bit);
-  if (!(old & bit)) atomicAdd(o.tiles + (code >> 9), 1u);
-}
-
-__device__ __forceinline__ void scatter_brick(const BitmapOut& o, uint32_t S, int bx, int by,
-                                              int bz, int nbx, int nby, int nbz) {
-  if (!S) return;
-  if (!o.dilate) {
-    if ((S >> 13) & 1u) set_brick(o, bx, by, bz);
-    return;
-  }
-  while (S) {
-    const int e = __ffs(S) - 1;
-    S &= S - 1;
-    const int tx = bx - (e / 9 - 1), ty = by - ((e / 3) % 3 - 1), tz = bz - (e % 3 - 1);
-    if (tx >= 0 && ty >= 0 && tz >= 0 && tx < nbx && ty < nby && tz < nbz)
-      set_brick(o, (uint32_t)tx, (uint32_t)ty, (uint32_t)tz);
-  }
-}
-
 template <int V, bool WRITE_BITS, bool COUNT>
 __device__ __forceinline__ void summary_body(const VisEval& ve, uint32_t* red,
                                              const uint8_t* __restrict__ vol, int nx, int ny,
                                              int nz, uint32_t* __restrict__ summary,
                                              uint32_t* __restrict__ bits,
                                              unsigned long long* __restrict__ count, int nbx,
-                                             int nby, int nbz, int nzc, int64_t ntasks,
-                                             const BitmapOut& bo) {
+                                             int nby, int nbz, int nzc, int64_t ntasks) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t task = (int64_t)blockIdx.x * SUMMARY_WARPS + warp;
@@ -240,17 +206,9 @@ __device__ __forceinline__ void summary_body(const VisEval& ve, uint32_t* red,
         if (lx == 7) { xa_last = pa; xb_last = pb; }
       }
       const int bz = z0 >> 3;
-      const uint32_t sa = xa_last | (xa_any << 9) | (xa_first << 18);
-      const uint32_t sb = xb_last | (xb_any << 9) | (xb_first << 18);
-      if (summary) {
-        const int64_t sbase = ((int64_t)bx * nby + by) * nbz;
-        summary[sbase + bz] = sa;
-        if (bz + 1 < nbz) summary[sbase + bz + 1] = sb;
-      }
-      if (bo.bitmap) {
-        scatter_brick(bo, sa, bx, by, bz, nbx, nby, nbz);
-        if (bz + 1 < nbz) scatter_brick(bo, sb, bx, by, bz + 1, nbx, nby, nbz);
-      }
+      const int64_t sbase = ((int64_t)bx * nby + by) * nbz;
+      summary[sbase + bz] = xa_last | (xa_any << 9) | (xa_first << 18);
+      if (bz + 1 < nbz) summary[sbase + bz + 1] = xb_last | (xb_any << 9) | (xb_first << 18);
     }
   }
   if (COUNT) {
@@ -265,14 +223,14 @@ __device__ __forceinline__ void summary_body(const VisEval& ve, uint32_t* red,
   }
 }
 
-#define VS_SUMMARY_ARGS ve, red, vol, nx, ny, nz, summary, bits, count, nbx, nby, nbz, nzc, ntasks, bo
+#define VS_SUMMARY_ARGS ve, red, vol, nx, ny, nz, summary, bits, count, nbx, nby, nbz, nzc, ntasks
 
 // Fast kernel (summary only): one instantiation per visibility shape, chosen per launch from
 // the device parameter block (uniform branch), so CUDA-graph replays follow TF changes.
 __global__ void __launch_bounds__(SUMMARY_WARPS * 32)
     k_brick_summary(const uint8_t* __restrict__ vol, int nx, int ny, int nz,
                     const vs_tf_params* __restrict__ tf, uint32_t* __restrict__ summary,
-                    int nbx, int nby, int nbz, int nzc, int64_t ntasks, BitmapOut bo) {
+                    int nbx, int nby, int nbz, int nzc, int64_t ntasks) {
   __shared__ uint8_t tab[256];
   __shared__ uint32_t red[SUMMARY_WARPS];
   uint32_t* bits = nullptr;
@@ -310,7 +268,6 @@ __global__ void __launch_bounds__(SUMMARY_WARPS * 32)
   VisEval ve;
   load_vis(ve, tf, tab);
   __syncthreads();
-  const BitmapOut bo{nullptr, nullptr, 0};
   summary_body<V_TABLE, WRITE_BITS, COUNT>(VS_SUMMARY_ARGS);
 }
 
@@ -660,28 +617,7 @@ int vs_classify_summary(const uint8_t* bins, int nx, int ny, int nz, const vs_tf
         bins, nx, ny, nz, tf, summary, bits, count, nbx, nby, nbz, nzc, ntasks);
   else
     k_brick_summary<<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(bins, nx, ny, nz, tf, summary,
-                                                            nbx, nby, nbz, nzc, ntasks,
-                                                            BitmapOut{nullptr, nullptr, 0});
-  return check_launch("k_brick_summary");
-}
-
-int vs_classify_bricks(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
-                       int dilate, int P, uint32_t* bitmap, uint32_t* tile_counts,
-                       vs_stream_t st) {
-  if (!bins || !tf || !bitmap || !tile_counts || nx < 1 || ny < 1 || nz < 1)
-    return fail_arg("vs_classify_bricks");
-  if (nz % 16 != 0) return fail_arg("vs_classify_bricks needs nz % 16 == 0");
-  const int nbx = (int)cdiv(nx, 8), nby = (int)cdiv(ny, 8), nbz = (int)cdiv(nz, 8);
-  if (P != vs_morton_side(nbx, nby, nbz)) return fail_arg("vs_classify_bricks: P");
-  const int64_t nwords = (int64_t)P * P * P / 32;
-  VS_CUDA(cudaMemsetAsync(bitmap, 0, nwords * 4, S(st)), "memset bitmap");
-  VS_CUDA(cudaMemsetAsync(tile_counts, 0, nwords / 16 * 4, S(st)), "memset tiles");
-  const int nzc = (int)cdiv(nz, 512);
-  const int64_t ntasks = (int64_t)nbx * nby * nzc;
-  const unsigned grid = (unsigned)cdiv(ntasks, SUMMARY_WARPS);
-  k_brick_summary<<<grid, SUMMARY_WARPS * 32, 0, S(st)>>>(bins, nx, ny, nz, tf, nullptr, nbx, nby,
-                                                          nbz, nzc, ntasks,
-                                                          BitmapOut{bitmap, tile_counts, dilate});
+                                                            nbx, nby, nbz, nzc, ntasks);
   return check_launch("k_brick_summary");
 }
 

@@ -54,21 +54,16 @@ class LbvhRebuilder:
 
     # -- the launch sequence ------------------------------------------------------------
     def launch_summary(self, st: int):
-        """The volume pass: TF classification + dilated brick vote into the Morton bitmap."""
         nx, ny, nz = self.dims
-        if self.grid is not None or self.count is not None:  # summary-array variant
-            if self.count is not None:
-                self.count.zero_()
-            call("vs_classify_summary", ptr(self.v.bins), nx, ny, nz, ptr(self.params),
-                 ptr(self.summary), None, ptr(self.count), st)
-            call("vs_summary_to_bitmap", ptr(self.summary), nx, ny, nz, 1, self.P,
-                 ptr(self.bitmap), ptr(self.tiles), ptr(self.grid), st)
-        else:
-            call("vs_classify_bricks", ptr(self.v.bins), nx, ny, nz, ptr(self.params), 1, self.P,
-                 ptr(self.bitmap), ptr(self.tiles), st)
+        if self.count is not None:
+            self.count.zero_()
+        call("vs_classify_summary", ptr(self.v.bins), nx, ny, nz, ptr(self.params),
+             ptr(self.summary), None, ptr(self.count), st)
 
     def launch_tree(self, st: int):
         nx, ny, nz = self.dims
+        call("vs_summary_to_bitmap", ptr(self.summary), nx, ny, nz, 1, self.P, ptr(self.bitmap),
+             ptr(self.tiles), ptr(self.grid), st)
         t = self.tree
         call("vs_lbvh_from_bitmap", ptr(self.bitmap), ptr(self.tiles), self.P, 8, nx, ny, nz,
              self.cap, ptr(t["lo"]), ptr(t["hi"]), ptr(t["left"]), ptr(t["right"]),
@@ -130,9 +125,8 @@ class LbvhRebuilder:
         """SURVEY.md §8(d) B_lbvh terms for one rebuild (compulsory traffic only)."""
         nx, ny, nz = self.dims
         vol = nx * ny * nz
-        bitmap = self.P ** 3 // 8 + self.P ** 3 // 512 * 4
         return {
-            "summary_kernel": vol + bitmap,  # u8 read + Morton bitmap / tile counts written
+            "summary_kernel": vol + 4 * self.cap,           # u8 read + 27-bit summary write
             "rebuild": vol + 16 * n_bricks + 36 * (2 * n_bricks - 1) + 12 * n_bricks,
         }
 

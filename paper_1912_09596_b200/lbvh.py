@@ -139,10 +139,9 @@ def flag_bricks(b: BinaryVolume, brick_size: int = DEFAULT_BRICK_SIZE) -> BrickS
     tiles = torch.empty(P * P * P // 512, dtype=torch.int32, device=dev)
     nx, ny, nz = dims
     if bs == 8 and b.lazy and b.summary_ok():
-        v, tf, dilate = b._source
-        # one pass over the u8 volume, votes scattered straight into the Morton bitmap
-        call("vs_classify_bricks", ptr(v.bins), nx, ny, nz, ptr(tf.params()), int(dilate), P,
-             ptr(bitmap), ptr(tiles), stream())
+        dilate = b._source[2]
+        call("vs_summary_to_bitmap", ptr(b.summary()), nx, ny, nz, int(dilate), P, ptr(bitmap),
+             ptr(tiles), None, stream())
     else:
         flags = torch.empty(nb, dtype=torch.uint8, device=dev)
         call("vs_vote_cells", ptr(b.packed()), nx, ny, nz, bs, ptr(flags), stream())
