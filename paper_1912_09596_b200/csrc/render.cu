@@ -112,7 +112,7 @@ struct Integrator {
   double entry, dt, inv_dt;
   bool nearest;
   double accr, accg, accb, acca;
-  int64_t taken;
+  int taken;  // per-ray lattice samples (< 2^31)
   // active segment
   double t, t1;
   int64_t k;
@@ -163,6 +163,11 @@ struct Integrator {
     double fx, fy, fz;
   };
   __device__ __forceinline__ void gather(double tt, Gather& g) const {
+    if (idx32) gather_t<true>(tt, g);
+    else gather_t<false>(tt, g);
+  }
+  template <bool IDX32>
+  __device__ __forceinline__ void gather_t(double tt, Gather& g) const {
     const double px = __dadd_rn(r->ox, __dmul_rn(tt, r->dx));
     const double py = __dadd_rn(r->oy, __dmul_rn(tt, r->dy));
     const double pz = __dadd_rn(r->oz, __dmul_rn(tt, r->dz));
@@ -175,7 +180,7 @@ struct Integrator {
     const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
     const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
     uint32_t w0, w1;
-    if (idx32) {  // < 2^32 voxels: 32-bit offsets
+    if (IDX32) {  // < 2^32 voxels: 32-bit offsets
       const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
       const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
       w0 = __ldg(quads + ((uint32_t)x0 * sxq + yz));
@@ -192,9 +197,14 @@ struct Integrator {
     g.w1 = w1;
   }
   __device__ __forceinline__ double interp(const Gather& g) const {
+    if (use_tab) return interp_t<true>(g);
+    return interp_t<false>(g);
+  }
+  template <bool TAB>
+  __device__ __forceinline__ double interp_t(const Gather& g) const {
     const uint32_t w0 = g.w0, w1 = g.w1;
     float c000, c001, c010, c011, c100, c101, c110, c111;
-    if (use_tab) {  // shared-memory table of f32(u/255) (same values, MIO instead of XU)
+    if (TAB) {  // shared-memory table of f32(u/255) (same values, MIO instead of XU)
       const float* tb = sm->u8f;
       c000 = tb[w0 & 0xffu]; c001 = tb[(w0 >> 8) & 0xffu];
       c010 = tb[(w0 >> 16) & 0xffu]; c011 = tb[w0 >> 24];
@@ -218,8 +228,9 @@ struct Integrator {
   }
   // classification + front-to-back compositing of one interpolated value (render.py:745-758)
   __device__ __forceinline__ void shade(double value) {
-    const double bd = floor(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
-    const int bin = bd < 0.0 ? 0 : (bd > 255.0 ? 255 : (int)bd);
+    // floor(v*255 + 0.5) clipped to [0, 255]: one floor-converting F2I + integer clamp
+    const int bi = __double2int_rd(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
+    const int bin = bi < 0 ? 0 : (bi > 255 ? 255 : bi);
     const float4 c = sm->lut[bin];
     if (c.w > 0.0f) {
       const double w = __dmul_rn(1.0 - acca, sm->corr[bin]);
@@ -832,7 +843,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
   if (flags) atomicOr(flags_out, flags);
 }
 
-template <int KIND>
+template <int KIND, bool IDX32>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
                          const float* __restrict__ lut, const double* __restrict__ corr, double dt,
@@ -879,13 +890,13 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
         int k = kr.x;
         Integrator::Gather g;
         bool have = k < kr.y;
-        if (have) I.gather(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
+        if (have) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
         while (true) {
           if (have) {
             Integrator::Gather gn;
             const bool hn = k + 1 < kr.y;
-            if (hn) I.gather(__dadd_rn(I.entry, __dmul_rn((double)(k + 1), dt)), gn);
-            I.shade(I.interp(g));
+            if (hn) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)(k + 1), dt)), gn);
+            I.shade(I.use_tab ? I.interp_t<true>(g) : I.interp_t<false>(g));
             ++k;
             if (hn) g = gn;
             have = hn;
@@ -894,7 +905,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
             kr = segs[(int64_t)q * npix + pix];
             k = kr.x;
             have = k < kr.y;
-            if (have) I.gather(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
+            if (have) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
           }
         }
       } else if (n <= cap) {
@@ -1247,9 +1258,14 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                                                                  counts, g_seg_cap, flags,
                                                                  g_trav_budget);
     }
-    k_integrate_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-        v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
-        total, flags, g_render_opts);
+    if ((int64_t)v.nx * v.ny * v.nz < (1LL << 32))
+      k_integrate_segments<K, true><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
+          total, flags, g_render_opts);
+    else
+      k_integrate_segments<K, false><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
+          total, flags, g_render_opts);
     return;
   }
   k_render<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
