@@ -219,6 +219,27 @@ void vs_set_render_tuning(int trav_steps, int samples);
 /* Renderer code-path options (bit 0: u8 -> f32 via a shared-memory table); same results. */
 void vs_set_render_options(int opts);
 
+/* ---- multi-channel volumes (configs[4]; no reference equivalent, see multichannel.cu) ---- */
+typedef struct vs_int2 { int32_t x, y; } int2_t;
+typedef struct vs_multi_desc {
+  int nch, nx, ny, nz;              /* channels (<= 4) and dims                            */
+  const uint32_t* quads[4];         /* per channel trilinear gather volume (vs_build_quads) */
+  const float* lut[4];              /* per channel (256,4) float32 LUT                     */
+  const double* corr[4];            /* per channel opacity correction table (libm pow)     */
+} vs_multi_desc;
+/* dst[i] |= src[i] (OR of per-channel brick summaries). */
+int vs_or_words(uint32_t* dst, const uint32_t* src, int64_t n, vs_stream_t stream);
+/* Integration of all channels over lattice ranges produced by vs_render_segments. */
+int vs_render_multi_integrate(const vs_multi_desc* md, const vs_camera_desc* cam, double dt,
+                              const vs_rows_desc* rows_opt, const int2_t* segs, const int* counts,
+                              int cap, uint8_t* rgba8, double* rgba64_opt, int32_t* samples_opt,
+                              unsigned long long* total_opt, int* flags, vs_stream_t stream);
+/* Traversal half of the two-phase renderer alone: per ray lattice ranges (segs: cap x npix
+ * int2, ray-minor) and counts (npix). */
+int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
+                       const vs_camera_desc* cam, double dt, const vs_rows_desc* rows_opt,
+                       int2_t* segs, int* counts, int cap, int* flags, vs_stream_t stream);
+
 /* Leaf-brick bit grid of an LBVH from its brick_coords (n from n_dev, or cap if NULL). */
 int vs_lbvh_brick_grid(const int32_t* brick_coords, const int* n_dev, int64_t cap, int nbx,
                        int nby, int nbz, uint32_t* bits, vs_stream_t stream);

@@ -370,3 +370,27 @@ def math_pow_corr(lut, dt: float) -> np.ndarray:
     """Same table with Python's math.pow (== numba's ** on glibc)."""
     lut = _lut(lut)
     return np.array([1.0 - math.pow(1.0 - float(a), dt) for a in lut[:, 3]], np.float64)
+
+
+def render_multi(kind: str, fields, luts, index: dict | None, cam, dt: float = 0.5):
+    """Multi-channel frame (or_render_multi): u8 channels, one LUT each."""
+    L = lib()
+    if not hasattr(L, "_multi_bound"):
+        L.or_render_multi.restype = None
+        L.or_render_multi.argtypes = [C.c_int, P, C.c_int, i64, i64, i64, P, P, i64, i64, i64, i64,
+                                      P, P, P, P, P, P, i64, i64, P, P, i64, i64, C.c_double, P, P]
+        L._multi_bound = True
+    fs = [np.ascontiguousarray(f, dtype=np.uint8) for f in fields]
+    ls = [_lut(l) for l in luts]
+    fp = (C.c_void_p * len(fs))(*[f.ctypes.data for f in fs])
+    lp = (C.c_void_p * len(ls))(*[l.ctypes.data for l in ls])
+    packed, direction = camera_vectors(cam)
+    w, h = cam.width, cam.height
+    rgba = np.zeros((w * h, 4), np.float64)
+    samples = np.zeros(w * h, np.int64)
+    args, keep = _index_args(kind, index, fs[0].shape)
+    L.or_render_multi(_KIND[kind], C.cast(fp, C.c_void_p), len(fs), *fs[0].shape,
+                      C.cast(lp, C.c_void_p), *args, _p(packed), _p(direction), w, h, float(dt),
+                      _p(rgba), _p(samples))
+    del keep
+    return rgba.reshape(h, w, 4), samples.reshape(h, w)

@@ -1186,3 +1186,109 @@ void or_integrate(const double* origin, const double* dir, const double* seg, i6
     ray_setup(&r, origin, dir);
     integrate_ray(&r, seg, m, field, is_f32, tab, nx, ny, nz, lut, corr, dt, nearest, rgba, samples);
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* Multi-channel integration (BASELINE configs[4]; no reference equivalent -- "parity       */
+/* unpinned" except when all channels but one have zero alpha, where it IS _k_integrate,    */
+/* render.py:633-765).  Channels are composited in channel order at each lattice sample     */
+/* with the reference's update.  u8 channels only.                                          */
+/* ------------------------------------------------------------------------------------ */
+static double trilinear_u8(const uint8_t* f, const float* tab, i64 nx, i64 ny, i64 nz, double px,
+                           double py, double pz) {
+    double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
+    i64 x0 = (i64)floor(qx), y0 = (i64)floor(qy), z0 = (i64)floor(qz);
+    double fx = qx - (double)x0, fy = qy - (double)y0, fz = qz - (double)z0;
+    i64 x1 = x0 + 1, y1 = y0 + 1, z1 = z0 + 1;
+    x0 = x0 < 0 ? 0 : (x0 > nx - 1 ? nx - 1 : x0);
+    y0 = y0 < 0 ? 0 : (y0 > ny - 1 ? ny - 1 : y0);
+    z0 = z0 < 0 ? 0 : (z0 > nz - 1 ? nz - 1 : z0);
+    x1 = x1 < 0 ? 0 : (x1 > nx - 1 ? nx - 1 : x1);
+    y1 = y1 < 0 ? 0 : (y1 > ny - 1 ? ny - 1 : y1);
+    z1 = z1 < 0 ? 0 : (z1 > nz - 1 ? nz - 1 : z1);
+    float c000 = tab[f[IDX3(x0, y0, z0, ny, nz)]], c100 = tab[f[IDX3(x1, y0, z0, ny, nz)]];
+    float c010 = tab[f[IDX3(x0, y1, z0, ny, nz)]], c110 = tab[f[IDX3(x1, y1, z0, ny, nz)]];
+    float c001 = tab[f[IDX3(x0, y0, z1, ny, nz)]], c101 = tab[f[IDX3(x1, y0, z1, ny, nz)]];
+    float c011 = tab[f[IDX3(x0, y1, z1, ny, nz)]], c111 = tab[f[IDX3(x1, y1, z1, ny, nz)]];
+    float d00 = c100 - c000, d10 = c110 - c010, d01 = c101 - c001, d11 = c111 - c011;
+    double c00 = (double)c000 + (double)d00 * fx;
+    double c10 = (double)c010 + (double)d10 * fx;
+    double c01 = (double)c001 + (double)d01 * fx;
+    double c11 = (double)c011 + (double)d11 * fx;
+    double c0 = c00 + (c10 - c00) * fy;
+    double c1 = c01 + (c11 - c01) * fy;
+    return c0 + (c1 - c0) * fz;
+}
+
+static void integrate_ray_multi(const RaySt* r, const double* seg, i64 m, const uint8_t** fields,
+                                int nch, const float* u8tab, i64 nx, i64 ny, i64 nz,
+                                const float** luts, const double** corrs, double dt,
+                                double* rgba, i64* samples) {
+    rgba[0] = rgba[1] = rgba[2] = rgba[3] = 0.0;
+    *samples = 0;
+    if (m == 0) return;
+    double entry, ex;
+    if (!slab(r, 0.0, 0.0, 0.0, (double)nx, (double)ny, (double)nz, &entry, &ex)) return;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    i64 taken = 0;
+    for (i64 s = 0; s < m; ++s) {
+        double t0 = seg[2 * s], t1 = seg[2 * s + 1];
+        i64 k = (i64)ceil((t0 - entry) / dt);
+        if (k < 0) k = 0;
+        while (k > 0 && entry + (double)(k - 1) * dt >= t0) k--;
+        while (entry + (double)k * dt < t0) k++;
+        double t = entry + (double)k * dt;
+        while (t < t1) {
+            double px = r->ox + t * r->dx, py = r->oy + t * r->dy, pz = r->oz + t * r->dz;
+            for (int c = 0; c < nch; ++c) {
+                double value = trilinear_u8(fields[c], u8tab, nx, ny, nz, px, py, pz);
+                double bd = floor(value * 255.0 + 0.5);
+                int bin = bd < 0.0 ? 0 : (bd > 255.0 ? 255 : (int)bd);
+                const float* lut = luts[c];
+                if (lut[4 * bin + 3] > 0.0f) {
+                    double w = (1.0 - acc[3]) * corrs[c][bin];
+                    acc[0] += w * (double)lut[4 * bin + 0];
+                    acc[1] += w * (double)lut[4 * bin + 1];
+                    acc[2] += w * (double)lut[4 * bin + 2];
+                    acc[3] += w;
+                }
+            }
+            taken++;
+            k++;
+            t = entry + (double)k * dt;
+        }
+    }
+    rgba[0] = acc[0]; rgba[1] = acc[1]; rgba[2] = acc[2]; rgba[3] = acc[3];
+    *samples = taken;
+}
+
+/* Multi-channel frame (single thread per call; small test frames). */
+void or_render_multi(int kind, const uint8_t** fields, int nch, i64 nx, i64 ny, i64 nz,
+                     const float** luts, const uint8_t* occ, i64 ncx, i64 ncy, i64 ncz, i64 cs,
+                     const int32_t* lo, const int32_t* hi, const int32_t* left,
+                     const int32_t* right, const int8_t* axis, const int32_t* plane, i64 root,
+                     i64 stack_cap, const double* cam, const double* dir, i64 w, i64 h,
+                     double dt, double* rgba, i64* samples) {
+    Index ix = {kind, nx, ny, nz, occ, ncx, ncy, ncz, (double)cs, lo, hi, left, right, plane, axis, root};
+    float tab[256];
+    or_u8_field_table(tab);
+    double corr_store[4][256];
+    const double* corrs[4];
+    for (int c = 0; c < nch; ++c) {
+        or_corr_table(luts[c], dt, corr_store[c]);
+        corrs[c] = corr_store[c];
+    }
+    SegBuf seg = {0, 0, 0}, tmp = {0, 0, 0};
+    i64* stk = (i64*)malloc(sizeof(i64) * (size_t)(stack_cap + 4));
+    double* sa = (double*)malloc(sizeof(double) * (size_t)(stack_cap + 4));
+    double* sb = (double*)malloc(sizeof(double) * (size_t)(stack_cap + 4));
+    for (i64 q = 0; q < w * h; ++q) {
+        double o[3];
+        pixel_origin(cam, w, h, q % w, q / w, o);
+        RaySt r;
+        ray_setup(&r, o, dir);
+        i64 m = traverse_ray(&ix, &r, &seg, &tmp, stk, sa, sb);
+        integrate_ray_multi(&r, seg.t, m, fields, nch, tab, nx, ny, nz, luts, corrs, dt,
+                            rgba + 4 * q, samples + q);
+    }
+    free(seg.t); free(tmp.t); free(stk); free(sa); free(sb);
+}

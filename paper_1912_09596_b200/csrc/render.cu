@@ -1370,6 +1370,49 @@ void vs_set_render_tuning(int trav_steps, int samples) {
   g_sample_budget = samples > 0 ? samples : (1 << 30);
 }
 
+int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
+                       const vs_camera_desc* cam, double dt, const vs_rows_desc* rows_opt,
+                       int2_t* segs, int* counts, int cap, int* flags, vs_stream_t stream) {
+  if (!vol || !ix || !cam || !segs || !counts || !flags || cap < 1 || !(dt > 0.0))
+    return fail_arg("vs_render_segments");
+  vs_rows_desc rows;
+  if (rows_opt) rows = *rows_opt;
+  else { rows.nrows = cam->height; rows.stripe = cam->height; rows.nparts = 1; rows.part = 0; }
+  if (rows.nrows <= 0) return 0;
+  dim3 grid((unsigned)cdiv(cam->width, RENDER_TX), (unsigned)cdiv(rows.nrows, RENDER_TY));
+  cudaStream_t st = S(stream);
+  int2* sg = reinterpret_cast<int2*>(segs);
+  switch (ix->kind) {
+    case VS_KIND_NAIVE:
+      k_segments<VS_KIND_NAIVE><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      break;
+    case VS_KIND_GRID:
+      k_segments<VS_KIND_GRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      break;
+    case VS_KIND_LBVH:
+      if (ix->brick_bits)
+        k_segments<KIND_LBVH_BRICK><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      else
+        k_segments<VS_KIND_LBVH><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      break;
+    case VS_KIND_KD:
+      k_segments<VS_KIND_KD><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      break;
+    case VS_KIND_HYBRID:
+      k_segments<VS_KIND_HYBRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      break;
+    default:
+      return fail_arg("vs_render_segments: kind");
+  }
+  return check_launch("k_segments");
+}
+
 int vs_lbvh_brick_grid(const int32_t* brick_coords, const int* n_dev, int64_t cap, int nbx,
                        int nby, int nbz, uint32_t* bits, vs_stream_t stream) {
   if (!brick_coords || !bits || nbx < 1 || nby < 1 || nbz < 1 || cap < 0)

@@ -1,0 +1,80 @@
+"""Multi-channel volumes (configs[4]) on the GPU: exact reduction to the reference's
+single-channel frames, and 4-channel frames vs the C restatement (oracle.render_multi)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vs():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1912_09596_b200 as vs
+
+    return vs
+
+
+def _cam(vs, g, w, h):
+    return vs.Camera(eye=tuple(g["cam_eye"]), direction=tuple(g["cam_dir"]), up=tuple(g["cam_up"]),
+                     extent=float(g["cam_extent"]), width=w, height=h)
+
+
+def test_reduces_to_single_channel(vs, blobs64):
+    from paper_1912_09596_b200.multichannel import classify_multi, render_float_multi
+
+    u8 = blobs64["u8"]
+    vols = [vs.Volume(u8), vs.Volume(u8[::-1].copy()), vs.Volume(u8.T.copy())]
+    zero = vs.TransferFunction(np.zeros((256, 4), np.float32))
+    tfs = [vs.TransferFunction(blobs64["ramp03_lut"]), zero, zero]
+    b = classify_multi(vols, tfs, dilate=True)
+    idx = vs.build_index("lbvh", b)
+    single = vs.build_index("lbvh", vs.classify(vols[0], tfs[0], dilate=True))
+    np.testing.assert_array_equal(idx.lo, single.lo)
+    cam = _cam(vs, blobs64, 96, 64)
+    rgba, samples = render_float_multi(vols, tfs, idx, cam)
+    np.testing.assert_array_equal(samples, blobs64["ramp03_render_lbvh_samples"])
+    np.testing.assert_array_equal(rgba, blobs64["ramp03_render_lbvh_rgba"])
+
+
+@pytest.mark.parametrize("kind", ["naive", "grid", "lbvh"])
+def test_four_channels_vs_restatement(vs, blobs64, kind):
+    from paper_1912_09596_b200.multichannel import classify_multi, render_float_multi
+
+    u8 = blobs64["u8"]
+    chans = [u8, np.ascontiguousarray(u8[::-1]), np.ascontiguousarray(u8.transpose(1, 0, 2)),
+             np.ascontiguousarray(u8[:, ::-1])]
+    luts = []
+    for c, t in enumerate((0.3, 0.4, 0.5, 0.6)):
+        lut = vs.TransferFunction.ramp(t).lut.copy()
+        lut[:, c % 3] = 0.9
+        luts.append(lut)
+    vols = [vs.Volume(c) for c in chans]
+    tfs = [vs.TransferFunction(l) for l in luts]
+    b = classify_multi(vols, tfs, dilate=True)
+    # union classification == OR of the per-channel oracle classifications, dilated
+    plain = np.zeros(u8.shape, bool)
+    for c, l in zip(chans, luts):
+        plain |= O.classify(c, l, dilate=False)[0]
+    np.testing.assert_array_equal(classify_multi(vols, tfs, dilate=False).bits, plain)
+    idx = vs.build_index(kind, b)
+    cam = _cam(vs, blobs64, 96, 64)
+    rgba, samples = render_float_multi(vols, tfs, idx, cam)
+    if kind == "naive":
+        oidx = None
+    elif kind == "grid":
+        oidx = {"occupied": idx.occupied, "cell_size": 16}
+    else:
+        oidx = {"lo": idx.lo, "hi": idx.hi, "left": idx.left, "right": idx.right,
+                "root": idx.root, "height": idx.height()}
+    orgba, osamples = O.render_multi(kind, chans, luts, oidx, cam)
+    np.testing.assert_array_equal(samples, osamples)
+    assert float(np.max(np.abs(rgba - orgba))) <= 1e-3
+    np.testing.assert_array_equal(rgba, orgba)

@@ -232,3 +232,17 @@ def test_shrink_direct_equals_svt(rng):
             assert O.shrink_svt(t, bits.shape, bs, lo, hi) == O.tight_box(bits, lo, hi)
             want = int(bits[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]].sum())
             assert O.box_count(t, bits.shape, bs, lo, hi) == want
+
+
+@pytest.mark.parametrize("kind", ["naive", "lbvh"])
+def test_multichannel_oracle_reduces_to_reference(blobs64, kind):
+    """With channels 1..3 at zero alpha the multi-channel restatement IS the reference frame
+    (the only pinned case of the multi-channel semantics, which the reference lacks)."""
+    cam = _Cam(blobs64, 96, 64)
+    u8 = blobs64["u8"]
+    zero = np.zeros((256, 4), np.float32)
+    k, idx = _index(kind, blobs64, "ramp03_", (64, 64, 64))
+    rgba, samples = O.render_multi(k, [u8, u8[::-1].copy(), u8, u8.T.copy()],
+                                   [blobs64["ramp03_lut"], zero, zero, zero], idx, cam)
+    np.testing.assert_array_equal(samples, blobs64[f"ramp03_render_{kind}_samples"])
+    np.testing.assert_array_equal(rgba, blobs64[f"ramp03_render_{kind}_rgba"])
