@@ -457,6 +457,136 @@ def run_ours(args, rank, ws, local):
     print(json.dumps(line), flush=True)
 
 
+def channel_tfs(nch: int, k: int = NSWEEP):
+    """Per-channel tinted ramps; the sweep moves every channel's threshold together."""
+    from paper_1912_09596_b200.volume import TransferFunction
+
+    tints = [(1.0, 0.3, 0.2), (0.2, 1.0, 0.3), (0.3, 0.4, 1.0), (1.0, 0.9, 0.2)]
+    out = []
+    for i in range(k):
+        t = 0.6 - 0.6 * i / 63
+        out.append([TransferFunction.ramp(threshold=t, color_lo=(0.1, 0.1, 0.1),
+                                          color_hi=tints[c]) for c in range(nch)])
+    return out
+
+
+def run_multi(args, rank, ws, local):
+    """BASELINE.json configs[4]: 4-channel 1024^3, 1080p, row-stripe tiles + NCCL gather."""
+    import torch
+
+    import paper_1912_09596_b200 as vs
+    from paper_1912_09596_b200.engine import LbvhRebuilder
+    from paper_1912_09596_b200.multichannel import classify_multi
+    from paper_1912_09596_b200.render import tf_device
+    from paper_1912_09596_b200.synth import gen_blobs_u8
+    from paper_1912_09596_b200.tiles import TileRenderer
+
+    n, nch = args.size, args.channels
+    nblobs = max(1, 25600 * n ** 3 // 1024 ** 3)
+    u8s = [gen_blobs_u8((n, n, n), n=nblobs, seed=7 + c, sigma=3.0) for c in range(nch)]
+    vols = [vs.Volume(u) for u in u8s]
+    for v in vols:
+        v.quads()
+    tfs = channel_tfs(nch)
+    cams = cameras(vols[0].dims)
+    params = torch.stack([torch.stack([tf.params() for tf in tl]) for tl in tfs])
+    for tl in tfs:
+        for tf in tl:
+            tf_device(tf, 0.5)
+    rb = LbvhRebuilder(vols).capture()
+    idx = rb.index()
+    tiles = TileRenderer(W, H)
+    st = torch.cuda.current_stream()
+
+    def step(k):
+        j = k % NSWEEP
+        rb.rebuild(params[j])
+        return tiles.render_multi(vols, tfs[j], idx, cams[j])
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    barrier(ws)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for k in range(args.steps):
+            step(k)
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    samples = tiles.sample_total()
+    # e2e through the public API: per-step host LUTs -> classify_multi -> build_index -> frame
+    luts = [[tf.lut for tf in tl] for tl in tfs]
+    e_steps = max(1, min(args.steps, 16))
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0.record(st)
+    for k in range(e_steps):
+        j = k % NSWEEP
+        tl = [vs.TransferFunction(l) for l in luts[j]]
+        b = classify_multi(vols, tl, dilate=True)
+        index = vs.build_index("lbvh", b)
+        frame = tiles.render_multi(vols, tl, index, cams[j]).cpu()
+    e1.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
+    del frame
+    if rank != 0:
+        return
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        from oracle import oracle as O
+
+        hosts = [u.cpu().numpy() for u in u8s]
+        t0 = time.perf_counter()
+        slab = 64
+        for h_, tf in zip(hosts, tfs[0]):
+            O.classify(np.ascontiguousarray(h_[:slab]), tf.lut, dilate=True)
+        rebuild_s = (time.perf_counter() - t0) * n / slab
+        import types
+        cam = cams[0]
+        nrows = 4
+        sub = types.SimpleNamespace(eye=cam.eye, direction=cam.direction, up=cam.up,
+                                    extent=cam.extent, width=cam.width, height=nrows)
+        # a band of rows through the image centre: shift the eye down to row H/2
+        b = classify_multi(vols, tfs[0], dilate=True)
+        index = vs.build_index("lbvh", b)
+        eye, up, right, scale = cam.frame_vectors()
+        shift = (H / 2.0 - nrows / 2.0) * scale
+        sub.eye = tuple(np.asarray(eye) - shift * np.asarray(up))
+        oidx = {"lo": index.lo, "hi": index.hi, "left": index.left, "right": index.right,
+                "root": index.root, "height": index.height()}
+        t0 = time.perf_counter()
+        O.render_multi("lbvh", hosts, [tf.lut for tf in tfs[0]], oidx, sub)
+        render_s = (time.perf_counter() - t0) * H / nrows
+        cpu = {"value": 1.0 / (rebuild_s + render_s), "unit": "frames/s", "cores": 1,
+               "kind": "port", "sample": f"oracle: {nch}-channel classify on x-slab [0,{slab}) "
+               f"scaled x{n / slab:.0f} + multi-channel LBVH render of {nrows} centre rows "
+               f"scaled x{H / nrows:.0f} (1 thread)",
+               "rebuild_ms": rebuild_s * 1e3, "render_ms": render_s * 1e3}
+    line = {
+        "metric": METRIC, "value": 1e3 / ms, "unit": "frames/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8+f64",
+        "data": "synthetic",
+        "config": {"workload": f"{nch}-channel {n}^3 u8 blobs (seeds 7..{6 + nch}), union "
+                               f"LBVH rebuild + {W}x{H} render per frame, TF sweep",
+                   "frame": "rebuild+render", "channels": nch,
+                   "parallelism": f"image row stripes x{ws} + NCCL all-gather"},
+        "render": {"samples_per_frame": samples},
+        "e2e": {"value": 1e3 / e2e_ms, "unit": "frames/s",
+                "h2d_bytes_per_step": nch * (64 + 4096 + 2048),
+                "d2h_bytes_per_step": W * H * 4, "ms_per_step": e2e_ms},
+        "gpu_launches": (nch + (nch - 1) + 5 + 1 + 2) * args.steps,
+        "cpu_baseline": cpu, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -466,11 +596,15 @@ def main():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--channels", type=int, default=1,
+                    help="> 1: BASELINE configs[4] multi-channel frames")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, ws, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, rank, ws)
+    elif args.channels > 1:
+        run_multi(args, rank, ws, local)
     else:
         run_ours(args, rank, ws, local)
     if ws > 1:

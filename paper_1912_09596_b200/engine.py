@@ -23,10 +23,17 @@ from .volume import TransferFunction, Volume
 
 
 class LbvhRebuilder:
-    def __init__(self, v: Volume, brick_size: int = 8, with_grid: bool = False,
-                 count: bool = False):
+    """``v`` is one Volume or a list of up to 4 channels (multichannel.py semantics: the
+    hierarchy covers the union of the channels' visible voxels; one 64-byte TF block per
+    channel, stacked)."""
+
+    def __init__(self, v, brick_size: int = 8, with_grid: bool = False, count: bool = False):
+        self.channels = list(v) if isinstance(v, (list, tuple)) else [v]
+        v = self.channels[0]
         if brick_size != 8 or v.dims[2] % 16 != 0:
             raise ValueError("LbvhRebuilder needs 8^3 bricks and nz % 16 == 0")
+        if len(self.channels) > 1 and count:
+            raise ValueError("count is single-channel only")
         self.v = v
         self.dims = v.dims
         nx, ny, nz = v.dims
@@ -34,7 +41,9 @@ class LbvhRebuilder:
         self.nb = tuple(-(-d // 8) for d in v.dims)
         self.P = query("vs_morton_side", *self.nb)
         self.cap = self.nb[0] * self.nb[1] * self.nb[2]
-        self.params = torch.zeros(16, dtype=torch.int32, device=dev)
+        self.params = torch.zeros(16 * len(self.channels), dtype=torch.int32, device=dev)
+        self.summary_tmp = torch.empty(self.cap, dtype=torch.int32, device=dev) \
+            if len(self.channels) > 1 else None
         self.summary = torch.empty(self.cap, dtype=torch.int32, device=dev)
         self.bitmap = torch.empty(self.P ** 3 // 32, dtype=torch.int32, device=dev)
         self.tiles = torch.empty(self.P ** 3 // 512, dtype=torch.int32, device=dev)
@@ -57,8 +66,16 @@ class LbvhRebuilder:
         nx, ny, nz = self.dims
         if self.count is not None:
             self.count.zero_()
-        call("vs_classify_summary", ptr(self.v.bins), nx, ny, nz, ptr(self.params),
-             ptr(self.summary), None, ptr(self.count), st)
+        if self.summary_tmp is None:
+            call("vs_classify_summary", ptr(self.v.bins), nx, ny, nz, ptr(self.params),
+                 ptr(self.summary), None, ptr(self.count), st)
+            return
+        for c, ch in enumerate(self.channels):  # union of the channels' classifications
+            out = self.summary if c == 0 else self.summary_tmp
+            call("vs_classify_summary", ptr(ch.bins), nx, ny, nz, ptr(self.params[16 * c:]),
+                 ptr(out), None, None, st)
+            if c:
+                call("vs_or_words", ptr(self.summary), ptr(out), self.cap, st)
 
     def launch_tree(self, st: int):
         nx, ny, nz = self.dims
@@ -92,8 +109,8 @@ class LbvhRebuilder:
         return self
 
     def set_tf(self, tf_params: torch.Tensor):
-        """tf_params: a device int32[16] vs_tf_params block (e.g. TransferFunction.params())."""
-        self.params.copy_(tf_params, non_blocking=True)
+        """tf_params: device int32[16 * channels] vs_tf_params block(s)."""
+        self.params.copy_(tf_params.reshape(-1), non_blocking=True)
 
     def rebuild(self, tf_params: torch.Tensor | None = None):
         if tf_params is not None:

@@ -68,6 +68,7 @@ class TileRenderer:
     def render(self, v, tf, index, cam: Camera, dt: float = 0.5, idx_desc=None, vol_desc=None,
                cam_desc=None) -> torch.Tensor:
         """Render this rank's stripes and assemble the full frame on every rank (device)."""
+        self._last_total = self.target.total
         render_rows(v, tf, index, cam, self.target, dt=dt, rows=self.rows_desc,
                     idx_desc=idx_desc or index_desc(index), vol_desc=vol_desc or volume_desc(v),
                     cam_desc=cam_desc or camera_desc(cam))
@@ -77,8 +78,24 @@ class TileRenderer:
         dist.all_gather_into_tensor(self.gathered, self.target.rgba8, group=self.group)
         return assemble(self.gathered, self.perm, self.frame_dev)
 
+    def render_multi(self, volumes, tfs, index, cam: Camera, dt: float = 0.5) -> torch.Tensor:
+        """Multi-channel frame (multichannel.py), same stripe split and gather."""
+        from .multichannel import MultiTarget, render_multi_rows
+
+        mt = self.__dict__.get("_multi_target")
+        if mt is None:
+            mt = MultiTarget(self.width, self.maxrows)
+            self._multi_target = mt
+        render_multi_rows(volumes, tfs, index, cam, mt, dt, rows=self.rows_desc)
+        self._last_total = mt.total
+        if self.world == 1:
+            self.frame_dev.copy_(mt.rgba8[: self.height])
+            return self.frame_dev
+        dist.all_gather_into_tensor(self.gathered, mt.rgba8, group=self.group)
+        return assemble(self.gathered, self.perm, self.frame_dev)
+
     def sample_total(self) -> int:
-        t = self.target.total
+        t = self.__dict__.get("_last_total", self.target.total)
         if self.world > 1:
             dist.all_gather_into_tensor(self.totals, t, group=self.group)
             return int(self.totals.sum().item())
