@@ -14,6 +14,7 @@ from .lbvh import (BrickSet, Lbvh, MortonRangeError, build_lbvh, empty_lbvh, fla
 from .render import (DEFAULT_DT, Camera, Frame, Ray, RaySegmentList, integrate, render_float,
                      render_frame, sample_count_of, traverse_grid, traverse_hybrid, traverse_kd,
                      traverse_lbvh, traverse_naive)
+from .service import Reply, Session, handle_message
 from .svt import (MacroGrid, SvtGrid, box_count, build_svt_grid, derive_macro_grid,
                   shrink_to_occupied)
 from .volume import (Aabb, BinaryVolume, TransferFunction, UnsupportedFormatError, Volume,
