@@ -5,7 +5,8 @@ the same public names, argument meanings, array layouts and exceptions, backed b
 hand-written CUDA kernels in libvsb200.so (include/vsb200.h).  There is no CPU fallback.
 """
 
-from .bench import INDEX_KINDS, build_index, index_kind, report_stats
+from .bench import (CSV_HEADER, INDEX_KINDS, BenchConfig, BenchRecord, build_index, index_kind,
+                    load_dataset, load_tf, report_stats, run_benchmark, to_csv)
 from .hybrid import HybridGrid, build_hybrid
 from .kdtree import (BuildParams, CellBoxList, KdTree, SplitPlane, binned_best_plane, build_kdtree,
                      empty_kdtree, precompute_cell_boxes, sweep_best_plane)
@@ -18,6 +19,7 @@ from .service import Reply, Session, handle_message
 from .svt import (MacroGrid, SvtGrid, box_count, build_svt_grid, derive_macro_grid,
                   shrink_to_occupied)
 from .volume import (Aabb, BinaryVolume, TransferFunction, UnsupportedFormatError, Volume,
-                     VolumeFormatError, classify, occupancy, quantize_scalar)
+                     VolumeFormatError, classify, gen_blobs, gen_menger, gen_shell, load_raw,
+                     occupancy, quantize_scalar, save_raw)
 
 __version__ = "0.1.0"

@@ -327,3 +327,102 @@ def occupancy(b: BinaryVolume) -> float:
     """Fraction of voxels flagged (volume.py:322-324)."""
     nx, ny, nz = b.dims
     return float(b.count_nonzero()) / (nx * ny * nz)
+
+
+# -- raw I/O and generators (fixtures/harness; SURVEY §8f ranks 2-3) -----------------------------
+
+def load_raw(path, meta: dict | None = None) -> Volume:
+    """A .raw scalar volume (volume.py:165-194): x-fastest on disk.  8-bit files go straight to
+    device u8 bins (the field f32(u/255) is implied, no float32 host copy); 16-bit files are
+    normalised on the device in float64 and narrowed to float32 like the reference."""
+    from pathlib import Path as _P
+
+    path = _P(path)
+    if meta is None:
+        meta = json.loads(path.with_suffix(path.suffix + ".json").read_text())
+    dims = tuple(int(d) for d in meta["dims"])
+    bits = int(meta.get("bits", meta.get("bits_per_voxel", 8)))
+    endian = meta.get("endian", meta.get("endianness", "little"))
+    if bits == 8:
+        dtype = np.dtype(np.uint8)
+    elif bits == 16:
+        dtype = np.dtype(np.uint16).newbyteorder("<" if endian == "little" else ">")
+    else:
+        raise UnsupportedFormatError(f"unsupported bit depth {bits}")
+    raw = path.read_bytes()
+    expected = dims[0] * dims[1] * dims[2] * dtype.itemsize
+    if len(raw) != expected:
+        raise VolumeFormatError(
+            f"{path}: file is {len(raw)} bytes, dims {dims} at {bits} bit need {expected}")
+    dev = _lib.device()
+    flat = np.frombuffer(raw, dtype=dtype)
+    if bits == 8:
+        t = torch.from_numpy(flat.copy()).to(dev)
+        # on disk x fastest: (nz, ny, nx) C-order == (nx, ny, nz) F-order -> permute on device
+        vol = t.reshape(dims[2], dims[1], dims[0]).permute(2, 1, 0).contiguous()
+        return Volume(vol, name=path.stem)
+    t = torch.from_numpy(flat.astype(np.int32)).to(dev)
+    f64 = t.reshape(dims[2], dims[1], dims[0]).permute(2, 1, 0).double() / float(2 ** bits - 1)
+    return Volume(f64.float().contiguous(), name=path.stem)
+
+
+def save_raw(v: Volume, path, bits: int = 8) -> None:
+    """Write .raw + JSON sidecar, x fastest, rint(v * peak) (volume.py:197-206)."""
+    from pathlib import Path as _P
+
+    if bits not in (8, 16):
+        raise UnsupportedFormatError(f"unsupported bit depth {bits}")
+    path = _P(path)
+    if bits == 8 and v.field is None:
+        q = v.bins  # rint(f32(u/255) * 255) == u
+    else:
+        src = v.field if v.field is not None else torch.from_numpy(U8_FIELD).to(
+            v.bins.device)[v.bins.long()]
+        q = torch.round(src.double() * float(2 ** bits - 1))
+        q = q.to(torch.uint8) if bits == 8 else q.to(torch.int32)
+    arr = q.permute(2, 1, 0).contiguous().cpu().numpy()
+    arr = arr.astype(np.uint8 if bits == 8 else "<u2")
+    path.write_bytes(arr.tobytes())
+    path.with_suffix(path.suffix + ".json").write_text(
+        json.dumps({"dims": list(v.dims), "bits": bits, "endian": "little"}))
+
+
+def gen_menger(level: int) -> Volume:
+    """Menger sponge of side 3^level, values 0/1 (volume.py:209-227), built on the device."""
+    if level < 0 or level > 6:
+        raise ValueError("level must be in [0, 6]")
+    dev = _lib.device()
+    n = 3 ** level
+    c = torch.arange(n, device=dev)
+    solid = torch.ones((n, n, n), dtype=torch.bool, device=dev)
+    for d in range(level):
+        digit = (c // 3 ** d) % 3 == 1
+        x, y, z = digit[:, None, None], digit[None, :, None], digit[None, None, :]
+        solid &= ~((x & y) | (x & z) | (y & z))
+    return Volume(solid.to(torch.uint8) * 255, name=f"menger{level}")
+
+
+def gen_shell(dims, center=None, radius: float = 0.0, thickness: float = 1.0) -> Volume:
+    """Spherical shell |(|p - c| - r)| <= t/2 at voxel centres (volume.py:230-248)."""
+    if thickness <= 0:
+        raise ValueError("thickness must be positive")
+    dims = tuple(int(d) for d in dims)
+    if center is None:
+        center = tuple(d / 2.0 for d in dims)
+    dev = _lib.device()
+    ax = [torch.arange(d, device=dev, dtype=torch.float64) + 0.5 - c for d, c in zip(dims, center)]
+    dist = torch.sqrt(ax[0][:, None, None] ** 2 + ax[1][None, :, None] ** 2 +
+                      ax[2][None, None, :] ** 2)
+    solid = torch.abs(dist - radius) <= thickness / 2.0
+    return Volume(solid.to(torch.uint8) * 255, name="shell")
+
+
+def gen_blobs(dims, n: int, seed: int, sigma: float = 1.5, centers=None) -> Volume:
+    """Sum of n Gaussian splats, clamped to [0, 1] (volume.py:251-286), accumulated on the
+    device in float64 (summation order differs from numpy's, so the float32 field can differ
+    in the last ulp; synth.gen_blobs_u8 gives the 8-bit benchmark volumes)."""
+    if n < 1:
+        raise ValueError("need at least one blob")
+    from .synth import blob_field
+
+    return Volume(blob_field(dims, n, seed, sigma, centers), name="blobs")
