@@ -1104,135 +1104,6 @@ __global__ void __launch_bounds__(128)
   if (total && my_total) atomicAdd(total, my_total);
 }
 
-// ---- tile-local lane refill: a warp owns a 32x8 pixel sub-tile and its lanes pull the next
-// ray of that sub-tile (shared-memory counter) whenever they finish one, so per-ray sample
-// imbalance is amortised over ~8 rays per lane while the warp's rays stay neighbours.
-constexpr int ITILE_W = 32, ITILE_H = 32, ISUB_H = 8;
-
-template <int KIND, bool IDX32>
-__global__ void __launch_bounds__(128)
-    k_integrate_tiles(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
-                      const float* __restrict__ lut, const double* __restrict__ corr, double dt,
-                      int nearest, vs_rows_desc rows, const int2* __restrict__ segs,
-                      const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
-                      double* __restrict__ rgba64, int32_t* __restrict__ samples,
-                      unsigned long long* __restrict__ total, int* __restrict__ flags_out,
-                      int render_opts) {
-  __shared__ RenderSmem sm;
-  __shared__ int ctr[4];
-  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
-    sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
-    sm.corr[k] = corr[k];
-    sm.u8f[k] = (float)((double)k / 255.0);
-  }
-  if (threadIdx.x < 4) ctr[threadIdx.x] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t npix = (int64_t)rows.nrows * cam.width;
-  const int i0 = blockIdx.x * ITILE_W, l0 = blockIdx.y * ITILE_H + wid * ISUB_H;
-  int flags = 0;
-  unsigned long long my_total = 0;
-  Ray r;
-  Integrator I;
-  I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
-  I.quads = vol.field ? nullptr : vol.quads;
-  I.idx32 = IDX32;
-  I.use_tab = (render_opts & 1) != 0;
-  I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt;
-  I.nearest = nearest != 0;
-  const bool fast = I.quads && !I.nearest && I.use_tab;
-  int64_t pix = -1;
-  int n = 0, q = 0, k = 0;
-  int2 kr = make_int2(0, 0);
-  Integrator::Gather g;
-  bool have = false;
-  while (true) {
-    if (pix >= 0) {
-      if (have) {  // one sample, next sample's gather issued first
-        Integrator::Gather gn;
-        const bool hn = k + 1 < kr.y;
-        if (hn) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)(k + 1), dt)), gn);
-        I.shade(I.interp_t<true>(g));
-        ++k;
-        if (hn) g = gn;
-        have = hn;
-        continue;
-      }
-      if (q + 1 < n) {  // next lattice range of this ray
-        ++q;
-        kr = segs[(int64_t)q * npix + pix];
-        k = kr.x;
-        have = k < kr.y;
-        if (have) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
-        continue;
-      }
-      // ray done
-      const double acc[4] = {I.accr, I.accg, I.accb, I.acca};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double qq = floor(__dadd_rn(__dmul_rn(acc[c], 255.0), 0.5));
-        rgba8[4 * pix + c] = (uint8_t)(qq < 0.0 ? 0 : (qq > 255.0 ? 255 : (int)qq));
-        if (rgba64) rgba64[4 * pix + c] = acc[c];
-      }
-      if (samples) samples[pix] = I.taken;
-      my_total += (unsigned long long)I.taken;
-      pix = -1;
-    }
-    const int id = atomicAdd(&ctr[wid], 1);
-    if (id >= ITILE_W * ISUB_H) break;
-    const int i = i0 + (id % ITILE_W), l = l0 + id / ITILE_W;
-    if (i >= cam.width || l >= rows.nrows) continue;
-    pix = (int64_t)l * cam.width + i;
-    pixel_ray(cam, rows, i, l, r);
-    I.accr = I.accg = I.accb = I.acca = 0.0;
-    I.taken = 0;
-    n = counts[pix];
-    q = 0;
-    kr = make_int2(0, 0);
-    k = 0;
-    have = false;
-    double tmin, tmax;
-    if (n <= 0 || !slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin,
-                        tmax)) {
-      n = 0;
-      continue;
-    }
-    I.entry = tmin;
-    if (n <= cap && fast) {
-      kr = segs[pix];
-      k = kr.x;
-      have = k < kr.y;
-      if (have) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
-    } else if (n <= cap) {  // nearest / float field: unpipelined samples
-      for (int qq = 0; qq < n; ++qq) {
-        const int2 rr = segs[(int64_t)qq * npix + pix];
-        for (int kk = rr.x; kk < rr.y; ++kk) {
-          I.t = __dadd_rn(I.entry, __dmul_rn((double)kk, dt));
-          I.sample_at();
-        }
-      }
-      n = 0;
-    } else {  // overflow: fused traversal + integration for this ray
-      SegmentSource<KIND> src;
-      src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
-      while (true) {
-        int budget = 1 << 30;
-        double a, b;
-        const int gg = src.next(r, ix, a, b, budget, &flags);
-        if (gg == 0) break;
-        I.segment(a, b);
-      }
-      n = 0;
-    }
-  }
-  if (flags) atomicOr(flags_out, flags);
-  if (total) {
-    unsigned long long t = my_total;
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0 && t) atomicAdd(total, t);
-  }
-}
-
 // Single-ray traversal (render.py:917-961): the merged interval list of each ray.
 template <int KIND>
 __device__ void traverse_one(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz,
@@ -1386,18 +1257,6 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
       k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                  counts, g_seg_cap, flags,
                                                                  g_trav_budget);
-    }
-    if (g_render_opts & 8) {  // tile-local lane refill
-      dim3 tg((unsigned)cdiv(c.width, ITILE_W), (unsigned)cdiv(rows.nrows, ITILE_H));
-      if ((int64_t)v.nx * v.ny * v.nz < (1LL << 32))
-        k_integrate_tiles<K, true><<<tg, 128, 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
-                                                       segs, counts, g_seg_cap, rgba8, rgba64,
-                                                       samples, total, flags, g_render_opts);
-      else
-        k_integrate_tiles<K, false><<<tg, 128, 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
-                                                        segs, counts, g_seg_cap, rgba8, rgba64,
-                                                        samples, total, flags, g_render_opts);
-      return;
     }
     if ((int64_t)v.nx * v.ny * v.nz < (1LL << 32))
       k_integrate_segments<K, true><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
