@@ -115,7 +115,8 @@ __global__ void k_leaves_from_sorted(const int32_t* __restrict__ coords,
 // Karras 2012 over sorted keys; n read from info[0] (device) so the launch needs no host sync.
 __global__ void k_karras(const uint64_t* __restrict__ keys, const int* __restrict__ info,
                          int64_t cap, int32_t* __restrict__ left, int32_t* __restrict__ right,
-                         int32_t* __restrict__ leaf_brick, int32_t* __restrict__ parent) {
+                         int32_t* __restrict__ leaf_brick, int32_t* __restrict__ parent,
+                         int2* __restrict__ range) {
   const int64_t n = info[0];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0 && n >= 1) parent[0] = -1;  // root (the single leaf when n == 1)
@@ -142,6 +143,7 @@ __global__ void k_karras(const uint64_t* __restrict__ keys, const int* __restric
   left[i] = (int32_t)lc;
   right[i] = (int32_t)rc;
   leaf_brick[i] = -1;
+  range[i] = make_int2((int)lo_i, (int)hi_i);
   parent[lc] = (int32_t)i;
   parent[rc] = (int32_t)i;
 }
@@ -202,11 +204,97 @@ static size_t sort_temp_bytes(int64_t n) {
   return b;
 }
 
+// Refit with the lower levels in shared memory: a CTA owns RC consecutive leaves; every
+// internal node whose leaf range lies inside the CTA's chunk is refit with shared-memory
+// arrival counters (no global fences), and only the nodes whose range crosses chunks -- about
+// log2(n / RC) levels -- climb with the global protocol.  Unions are order-independent, so the
+// boxes and heights equal k_refit's (and the reference's sweep).
+constexpr int RC = 1024;
+
+__global__ void __launch_bounds__(RC)
+    k_refit_chunked(int32_t* __restrict__ lo, int32_t* __restrict__ hi,
+                    const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+                    const int32_t* __restrict__ parent, const int2* __restrict__ range,
+                    int32_t* __restrict__ visit, int32_t* __restrict__ hgt, int* info) {
+  __shared__ int s_box[RC][6];
+  __shared__ int s_cnt[RC];
+  __shared__ int s_h[RC];
+  const int64_t n = info[0];
+  const int t = threadIdx.x;
+  if (blockIdx.x == 0 && t == 0) {
+    if (n == 0) info[1] = 0;
+    if (n == 1) info[1] = 1;
+  }
+  if (n < 2) return;
+  const int64_t c0 = (int64_t)blockIdx.x * RC;
+  if (c0 >= n) return;
+  const int64_t c1 = c0 + RC < n ? c0 + RC : n;
+  s_cnt[t] = 0;
+  __syncthreads();
+  const int64_t p = c0 + t;
+  if (p >= c1) return;
+  int64_t node = parent[n - 1 + p];
+  while (node >= 0) {
+    const int2 rg = range[node];
+    const int32_t l = left[node], r = right[node];
+    int b[6], hl, hr;
+    if (rg.x >= c0 && rg.y < c1) {  // inside the chunk: shared-memory protocol
+      __threadfence_block();
+      if (atomicAdd(&s_cnt[node - c0], 1) == 0) return;
+      __threadfence_block();
+      int bl[6], br[6];
+      if (l >= n - 1) {
+        for (int a = 0; a < 3; ++a) { bl[a] = lo[3 * l + a]; bl[3 + a] = hi[3 * l + a]; }
+        hl = 1;
+      } else {
+        for (int a = 0; a < 6; ++a) bl[a] = s_box[l - c0][a];
+        hl = s_h[l - c0];
+      }
+      if (r >= n - 1) {
+        for (int a = 0; a < 3; ++a) { br[a] = lo[3 * r + a]; br[3 + a] = hi[3 * r + a]; }
+        hr = 1;
+      } else {
+        for (int a = 0; a < 6; ++a) br[a] = s_box[r - c0][a];
+        hr = s_h[r - c0];
+      }
+      for (int a = 0; a < 3; ++a) {
+        b[a] = min(bl[a], br[a]);
+        b[3 + a] = max(bl[3 + a], br[3 + a]);
+      }
+      const int h = 1 + max(hl, hr);
+      for (int a = 0; a < 6; ++a) s_box[node - c0][a] = b[a];
+      s_h[node - c0] = h;
+      for (int a = 0; a < 3; ++a) { lo[3 * node + a] = b[a]; hi[3 * node + a] = b[3 + a]; }
+      hgt[node] = h;
+      if (node == 0) { info[1] = h; return; }
+    } else {  // crossing chunks: global protocol
+      __threadfence();
+      if (atomicAdd(&visit[node], 1) == 0) return;
+      __threadfence();
+      for (int a = 0; a < 3; ++a) {
+        b[a] = min(__ldcg(lo + 3 * l + a), __ldcg(lo + 3 * r + a));
+        b[3 + a] = max(__ldcg(hi + 3 * l + a), __ldcg(hi + 3 * r + a));
+      }
+      hl = (l >= n - 1) ? 1 : __ldcg(hgt + l);
+      hr = (r >= n - 1) ? 1 : __ldcg(hgt + r);
+      const int h = 1 + max(hl, hr);
+      for (int a = 0; a < 3; ++a) {
+        __stcg(lo + 3 * node + a, b[a]);
+        __stcg(hi + 3 * node + a, b[3 + a]);
+      }
+      __stcg(hgt + node, h);
+      if (node == 0) { info[1] = h; return; }
+    }
+    node = parent[node];
+  }
+}
+
 struct TreeWs {
   uint64_t* keys;
   int32_t* parent;
   int32_t* visit;
   int32_t* hgt;
+  int2* range;
 };
 
 static TreeWs take_tree(Bump& b, int64_t cap) {
@@ -215,6 +303,7 @@ static TreeWs take_tree(Bump& b, int64_t cap) {
   t.parent = b.take<int32_t>(std::max<int64_t>(2 * cap - 1, 1));
   t.visit = b.take<int32_t>(std::max<int64_t>(cap, 1));
   t.hgt = b.take<int32_t>(std::max<int64_t>(cap, 1));
+  t.range = b.take<int2>(std::max<int64_t>(cap, 1));
   return t;
 }
 
@@ -224,10 +313,11 @@ static int tree_and_refit(const TreeWs& w, int64_t cap, int32_t* lo, int32_t* hi
   VS_CUDA(cudaMemsetAsync(w.visit, 0, std::max<int64_t>(cap, 1) * sizeof(int32_t), st),
           "memset visit");
   const unsigned g = (unsigned)std::max<int64_t>(cdiv(cap, 256), 1);
-  k_karras<<<g, 256, 0, st>>>(w.keys, info, cap, left, right, leaf_brick, w.parent);
+  k_karras<<<g, 256, 0, st>>>(w.keys, info, cap, left, right, leaf_brick, w.parent, w.range);
   VS_TRY(check_launch("k_karras"));
-  k_refit<<<g, 256, 0, st>>>(lo, hi, left, right, w.parent, w.visit, w.hgt, info);
-  return check_launch("k_refit");
+  k_refit_chunked<<<(unsigned)std::max<int64_t>(cdiv(cap, RC), 1), RC, 0, st>>>(
+      lo, hi, left, right, w.parent, w.range, w.visit, w.hgt, info);
+  return check_launch("k_refit_chunked");
 }
 
 }  // namespace vs
