@@ -75,8 +75,18 @@ class TileRenderer:
         if self.world == 1:
             self.frame_dev.copy_(self.target.rgba8[: self.height])
             return self.frame_dev
-        dist.all_gather_into_tensor(self.gathered, self.target.rgba8, group=self.group)
+        self._gather(self.target.rgba8)
         return assemble(self.gathered, self.perm, self.frame_dev)
+
+    def _gather(self, local: torch.Tensor):
+        """All-gather of the equal-size stripe sets: NCCL over NVLink on device buffers; a gloo
+        group (CPU-side tests of the split) goes through host copies."""
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(self.gathered, local, group=self.group)
+        else:
+            host = torch.empty(self.gathered.shape, dtype=self.gathered.dtype)
+            dist.all_gather_into_tensor(host, local.cpu(), group=self.group)
+            self.gathered.copy_(host)
 
     def render_multi(self, volumes, tfs, index, cam: Camera, dt: float = 0.5) -> torch.Tensor:
         """Multi-channel frame (multichannel.py), same stripe split and gather."""
@@ -91,14 +101,18 @@ class TileRenderer:
         if self.world == 1:
             self.frame_dev.copy_(mt.rgba8[: self.height])
             return self.frame_dev
-        dist.all_gather_into_tensor(self.gathered, mt.rgba8, group=self.group)
+        self._gather(mt.rgba8)
         return assemble(self.gathered, self.perm, self.frame_dev)
 
     def sample_total(self) -> int:
         t = self.__dict__.get("_last_total", self.target.total)
         if self.world > 1:
-            dist.all_gather_into_tensor(self.totals, t, group=self.group)
-            return int(self.totals.sum().item())
+            if dist.get_backend(self.group) == "nccl":
+                dist.all_gather_into_tensor(self.totals, t, group=self.group)
+                return int(self.totals.sum().item())
+            host = torch.empty(self.world, dtype=torch.int64)
+            dist.all_gather_into_tensor(host, t.cpu(), group=self.group)
+            return int(host.sum())
         return int(t.item())
 
     def frame(self, v, tf, index, cam: Camera, dt: float = 0.5) -> Frame:
