@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
 }
 
 template <int KIND, bool IDX32>
-__global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, 5)
     k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
                          const float* __restrict__ lut, const double* __restrict__ corr, double dt,
                          int nearest, vs_rows_desc rows, const int2* __restrict__ segs,

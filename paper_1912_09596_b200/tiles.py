@@ -116,8 +116,14 @@ class TileRenderer:
         return int(t.item())
 
     def frame(self, v, tf, index, cam: Camera, dt: float = 0.5) -> Frame:
-        """Public API: a full Frame (host pixels) rendered by the whole group."""
+        """Public API: a full Frame (host pixels) rendered by the whole group; the pixels come
+        back through a pinned staging buffer."""
         img = self.render(v, tf, index, cam, dt)
         _check_flags(self.target.flags)
-        return Frame(width=self.width, height=self.height, pixels=img.cpu().numpy(),
+        host = self.__dict__.get("_pinned")
+        if host is None:
+            host = torch.empty(img.shape, dtype=img.dtype).pin_memory()
+            self._pinned = host
+        host.copy_(img)
+        return Frame(width=self.width, height=self.height, pixels=host.numpy().copy(),
                      sample_count=self.sample_total())

@@ -20,7 +20,7 @@ for t in ts:
     for kind in kinds:
         idx = vs.build_index(kind, b)
         d = index_desc(idx); vd = volume_desc(v); cd = camera_desc(cam)
-        for opts, cap, tb in [(1, 32, 1), (9, 32, 1)]:
+        for opts, cap, tb in [(1, 32, 1)]:
             _lib.lib().vs_set_render_options(opts)  # noqa
             _lib.lib().vs_set_render_tuning(tb, 1)
             tgt = RenderTarget(1920, 1080, seg_cap=cap)
