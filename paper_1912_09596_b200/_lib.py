@@ -8,12 +8,13 @@ errors, positive cudaError_t; failures raise with the library's thread-local mes
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libvsb200.so"
+LIB_PATH = Path(os.environ.get("VSB200_LIB", str(_PKG / "libvsb200.so")))  # override: dev tuning
 
 i32, i64, u64, P, SZ = C.c_int, C.c_int64, C.c_uint64, C.c_void_p, C.c_size_t
 

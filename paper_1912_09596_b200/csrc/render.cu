@@ -798,7 +798,7 @@ __device__ __forceinline__ void pixel_ray(const vs_camera_desc& cam, const vs_ro
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
     k_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
                double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
                int* __restrict__ flags_out, int step_budget) {
@@ -843,8 +843,14 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
   if (flags) atomicOr(flags_out, flags);
 }
 
+#ifndef VS_INTEGRATE_MINB
+#define VS_INTEGRATE_MINB 5
+#endif
+#ifndef VS_SEGMENTS_MINB
+#define VS_SEGMENTS_MINB 1
+#endif
 template <int KIND, bool IDX32>
-__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, 5)
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
     k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
                          const float* __restrict__ lut, const double* __restrict__ corr, double dt,
                          int nearest, vs_rows_desc rows, const int2* __restrict__ segs,
