@@ -844,10 +844,10 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
 }
 
 #ifndef VS_INTEGRATE_MINB
-#define VS_INTEGRATE_MINB 5
+#define VS_INTEGRATE_MINB 6
 #endif
 #ifndef VS_SEGMENTS_MINB
-#define VS_SEGMENTS_MINB 1
+#define VS_SEGMENTS_MINB 8
 #endif
 template <int KIND, bool IDX32>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
