@@ -24,6 +24,14 @@
 
 #include "common.cuh"
 
+// Minimum resident blocks per SM for the two render kernels (register caps; tuned on B200).
+#ifndef VS_INTEGRATE_MINB
+#define VS_INTEGRATE_MINB 6
+#endif
+#ifndef VS_SEGMENTS_MINB
+#define VS_SEGMENTS_MINB 8
+#endif
+
 namespace vs {
 
 constexpr double R_FAR = 1e300;
@@ -843,12 +851,6 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
   if (flags) atomicOr(flags_out, flags);
 }
 
-#ifndef VS_INTEGRATE_MINB
-#define VS_INTEGRATE_MINB 6
-#endif
-#ifndef VS_SEGMENTS_MINB
-#define VS_SEGMENTS_MINB 8
-#endif
 template <int KIND, bool IDX32>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
     k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
