@@ -709,8 +709,7 @@ struct SegmentSource {
 
 // while-while turn sizes (vs_set_render_tuning): traversal steps / lattice samples per turn
 static int g_trav_budget = 1, g_sample_budget = 1;
-// bit0: u8 -> f32 by shared-memory table; bit1: persistent traversal lanes;
-// bit2: persistent traversal + integration lanes
+// bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float conversion)
 static int g_render_opts = 1;
 
 template <int KIND>
@@ -962,156 +961,6 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
   }
 }
 
-// ---- persistent variants: lanes pull rays from a global queue as they finish, so a warp's
-// lanes stay busy regardless of how unequal its rays' traversal / sample counts are.  Ray ids
-// run through 16x8 pixel tiles so rays fetched together are spatial neighbours.
-__device__ __forceinline__ bool ray_pixel(int64_t id, int width, int nrows, int& i, int& l) {
-  const int64_t tile = id / (RENDER_TX * RENDER_TY);
-  const int w = (int)(id % (RENDER_TX * RENDER_TY));
-  const int tiles_x = (width + RENDER_TX - 1) / RENDER_TX;
-  i = (int)(tile % tiles_x) * RENDER_TX + (w % RENDER_TX);
-  l = (int)(tile / tiles_x) * RENDER_TY + (w / RENDER_TX);
-  return i < width && l < nrows;
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(128)
-    k_segments_p(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
-                 double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
-                 unsigned long long* __restrict__ queue, int64_t nids, int* __restrict__ flags_out) {
-  const int64_t npix = (int64_t)rows.nrows * cam.width;
-  int flags = 0;
-  while (true) {
-    const int64_t id = (int64_t)atomicAdd(queue, 1ull);
-    if (id >= nids) break;
-    int i, l;
-    if (!ray_pixel(id, cam.width, rows.nrows, i, l)) continue;
-    const int64_t pix = (int64_t)l * cam.width + i;
-    Ray r;
-    pixel_ray(cam, rows, i, l, r);
-    int n = 0;
-    double tmin, tmax;
-    if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
-      SegmentSource<KIND> src;
-      src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
-      Integrator L;
-      L.entry = tmin;
-      L.dt = dt;
-      L.inv_dt = 1.0 / dt;
-      int kprev = -1;
-      while (true) {
-        int budget = 1 << 30;
-        double a, b;
-        const int g = src.next(r, ix, a, b, budget, &flags);
-        if (g == 0) break;
-        const int k0 = (int)L.first_k(a), k1 = (int)L.first_k(b);
-        if (k1 <= k0) continue;
-        if (n > 0 && k0 == kprev && n <= cap) {
-          segs[(int64_t)(n - 1) * npix + pix].y = k1;
-        } else {
-          if (n < cap) segs[(int64_t)n * npix + pix] = make_int2(k0, k1);
-          ++n;
-        }
-        kprev = k1;
-      }
-    }
-    counts[pix] = n;
-  }
-  if (flags) atomicOr(flags_out, flags);
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(128)
-    k_integrate_p(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
-                  const float* __restrict__ lut, const double* __restrict__ corr, double dt,
-                  int nearest, vs_rows_desc rows, const int2* __restrict__ segs,
-                  const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
-                  double* __restrict__ rgba64, int32_t* __restrict__ samples,
-                  unsigned long long* __restrict__ total, unsigned long long* __restrict__ queue,
-                  int64_t nids, int* __restrict__ flags_out, int render_opts) {
-  __shared__ RenderSmem sm;
-  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
-    sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
-    sm.corr[k] = corr[k];
-    sm.u8f[k] = (float)((double)k / 255.0);
-  }
-  __syncthreads();
-  const int64_t npix = (int64_t)rows.nrows * cam.width;
-  int flags = 0;
-  unsigned long long my_total = 0;
-  Ray r;
-  Integrator I;
-  I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
-  I.quads = vol.field ? nullptr : vol.quads;
-  I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
-  I.use_tab = (render_opts & 1) != 0;
-  I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
-  int64_t pix = -1;
-  int n = 0, q = 0, k = 0;
-  int2 kr = make_int2(0, 0);
-  while (true) {
-    if (k < kr.y) {  // one lattice sample of the current range
-      I.t = __dadd_rn(I.entry, __dmul_rn((double)k, dt));
-      I.sample_at();
-      ++k;
-      continue;
-    }
-    if (q + 1 < n) {  // next range of the current ray
-      ++q;
-      kr = segs[(int64_t)q * npix + pix];
-      k = kr.x;
-      continue;
-    }
-    if (pix >= 0) {  // ray finished: write it out
-      const double acc[4] = {I.accr, I.accg, I.accb, I.acca};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double qq = floor(__dadd_rn(__dmul_rn(acc[c], 255.0), 0.5));
-        rgba8[4 * pix + c] = (uint8_t)(qq < 0.0 ? 0 : (qq > 255.0 ? 255 : (int)qq));
-        if (rgba64) rgba64[4 * pix + c] = acc[c];
-      }
-      if (samples) samples[pix] = (int32_t)I.taken;
-      my_total += (unsigned long long)I.taken;
-      pix = -1;
-    }
-    const int64_t id = (int64_t)atomicAdd(queue, 1ull);
-    if (id >= nids) break;
-    int i, l;
-    if (!ray_pixel(id, cam.width, rows.nrows, i, l)) continue;
-    pix = (int64_t)l * cam.width + i;
-    pixel_ray(cam, rows, i, l, r);
-    I.accr = I.accg = I.accb = I.acca = 0.0;
-    I.taken = 0;
-    n = counts[pix];
-    q = 0;
-    k = 0;
-    kr = make_int2(0, 0);
-    double tmin, tmax;
-    if (n > 0 && slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
-      I.entry = tmin;
-      if (n <= cap) {
-        kr = segs[pix];
-        k = kr.x;
-      } else {  // overflow: fused traversal + integration for this ray
-        SegmentSource<KIND> src;
-        src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
-        while (true) {
-          int budget = 1 << 30;
-          double a, b;
-          const int g = src.next(r, ix, a, b, budget, &flags);
-          if (g == 0) break;
-          I.segment(a, b);
-        }
-        n = 0;
-      }
-    } else {
-      n = 0;
-    }
-  }
-  if (flags) atomicOr(flags_out, flags);
-  if (total && my_total) atomicAdd(total, my_total);
-}
-
 // Single-ray traversal (render.py:917-961): the merged interval list of each ray.
 template <int KIND>
 __device__ void traverse_one(const Ray& r, const vs_index_desc& ix, int nx, int ny, int nz,
@@ -1234,38 +1083,13 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                           const double* corr, double dt, int nearest, const vs_rows_desc& rows,
                           uint8_t* rgba8, double* rgba64, int32_t* samples,
                           unsigned long long* total, int* flags) {
-  if (g_seg_ws && g_seg_cap > 0 && (g_render_opts & 4)) {  // persistent two-phase
-    const int64_t npix = (int64_t)rows.nrows * c.width;
-    int2* segs = static_cast<int2*>(g_seg_ws);
-    int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
-    unsigned long long* queues = reinterpret_cast<unsigned long long*>(
-        (reinterpret_cast<uintptr_t>(counts + npix) + 15) & ~uintptr_t(15));
-    cudaMemsetAsync(queues, 0, 2 * sizeof(unsigned long long), st);
-    const int64_t nids = (int64_t)grid.x * grid.y * RENDER_TX * RENDER_TY;
-    const int blocks = 148 * 8;
-    k_segments_p<K><<<blocks, 128, 0, st>>>(v, ix, c, rows, dt, segs, counts, g_seg_cap, queues,
-                                            nids, flags);
-    k_integrate_p<K><<<blocks, 128, 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows, segs, counts,
-                                             g_seg_cap, rgba8, rgba64, samples, total, queues + 1,
-                                             nids, flags, g_render_opts);
-    return;
-  }
   if (g_seg_ws && g_seg_cap > 0) {
     const int64_t npix = (int64_t)rows.nrows * c.width;
     int2* segs = static_cast<int2*>(g_seg_ws);
     int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
-    if (g_render_opts & 2) {  // persistent traversal lanes
-      unsigned long long* queues = reinterpret_cast<unsigned long long*>(
-          (reinterpret_cast<uintptr_t>(counts + npix) + 15) & ~uintptr_t(15));
-      cudaMemsetAsync(queues, 0, sizeof(unsigned long long), st);
-      const int64_t nids = (int64_t)grid.x * grid.y * RENDER_TX * RENDER_TY;
-      k_segments_p<K><<<148 * 8, 128, 0, st>>>(v, ix, c, rows, dt, segs, counts, g_seg_cap,
-                                               queues, nids, flags);
-    } else {
-      k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                 counts, g_seg_cap, flags,
-                                                                 g_trav_budget);
-    }
+    k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
+                                                               counts, g_seg_cap, flags,
+                                                               g_trav_budget);
     if ((int64_t)v.nx * v.ny * v.nz < (1LL << 32))
       k_integrate_segments<K, true><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
           v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,

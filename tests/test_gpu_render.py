@@ -283,6 +283,23 @@ def test_u8_table_option_equal(vs, blobs64):
     np.testing.assert_array_equal(outs[1][0], blobs64["ramp03_render_naive_rgba"])
 
 
+def test_u8_table_option_equal(vs, blobs64):
+    from paper_1912_09596_b200 import _lib
+
+    v = vs.Volume(blobs64["u8"])
+    tf = vs.TransferFunction(blobs64["ramp03_lut"])
+    cam = _cam_from(vs, blobs64, 96, 64)
+    outs = []
+    try:
+        for opts in (0, 1):
+            _lib.lib().vs_set_render_options(opts)
+            outs.append(vs.render_float(v, tf, None, cam))
+    finally:
+        _lib.lib().vs_set_render_options(0)
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[1][0], blobs64["ramp03_render_naive_rgba"])
+
+
 @pytest.mark.parametrize("kind", ["naive", "grid", "lbvh", "kd-deep-mls32", "hybrid"])
 def test_persistent_two_phase_equal(vs, blobs64, kind):
     """Persistent-lane two-phase rendering (render option bit 1) == fused, incl. overflow."""
