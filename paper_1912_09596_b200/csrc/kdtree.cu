@@ -23,6 +23,8 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -44,16 +46,32 @@ struct Span {
   int mn1, mx1, mn2, mx2;
 };
 
+// Per-level offset arrays (exclusive prefixes over the level's nodes, entry n = total), all
+// computed by prep_node when the level's boxes are emitted and scanned on the device.
+enum {
+  A_X = 0,   // x-slab spans (ext x) of nodes that search / force-split
+  A_Y,       // y-slab spans
+  A_Z,       // z-slab spans
+  A_PXZ,     // (x, z-word) projection words: ex * wz
+  A_PYZ,     // (y, z-word) projection words: ey * wz
+  A_ZW,      // z-span work items: wz
+  A_SCR,     // suffix-box scratch: max extent
+  A_IX,      // x-pass work items: ex * chunks(ey)
+  A_IY,      // y-pass work items: ey * chunks(ex)
+  A_C0,      // binned: cell slabs along x, y, z
+  A_C1,
+  A_C2,
+  KA
+};
+
+// Rows one x/y-pass work item covers (a node's slab is split into chunks of this many rows so
+// the top levels of a big volume still spread over every SM; chunks merge with atomics).
+constexpr int SPAN_CHUNK = 64;
+
 struct KdLevel {
-  int n;                 // nodes on this level
-  Box* box;              // node boxes
-  int* need;             // bit0 spans needed (sweep search / forced / binned leaf shrink)
-  int64_t* off_x;        // n+1 exclusive prefix of x extents (of nodes needing spans)
-  int64_t* off_y;
-  int64_t* off_z;
-  int64_t* off_pxz;      // n+1 prefix of ex * wz words
-  int64_t* off_pyz;      // n+1 prefix of ey * wz words
-  int64_t* off_zw;       // n+1 prefix of wz
+  int n;                      // nodes on this level
+  const Box* box;             // node boxes
+  const int64_t* off[KA];     // n+1 exclusive prefixes
 };
 
 __device__ __forceinline__ int wz_of(const Box& b) { return (b.hi[2] - b.lo[2] + 31) >> 5; }
@@ -79,157 +97,152 @@ __device__ __forceinline__ int find_node(const int64_t* __restrict__ off, int n,
   return lo;
 }
 
-// ---- spans along x (and the (x,z) projection): warp per (node, x-slab) --------------------
-__global__ void k_spans_x(const uint32_t* __restrict__ bits, int ny, int nzw, KdLevel L,
-                          const int64_t* __restrict__ total, Span* __restrict__ span_x,
-                          uint32_t* __restrict__ pxz) {
-  __shared__ uint32_t acc[8][32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t items = *total;
-  for (int64_t it = (int64_t)blockIdx.x * 8 + wib; it < items; it += (int64_t)gridDim.x * 8) {
-    const int i = find_node(L.off_x, L.n, it);
+// Lanes per row: the smallest power of two >= the node's z word count.
+__device__ __forceinline__ int group_width(int wz) {
+  return wz <= 1 ? 1 : 1 << (32 - __clz(wz - 1));
+}
+
+// ---- slab spans along x (AX = 0, rows = y) or y (AX = 1, rows = x), and the matching
+//      (slab, z-word) OR projection ------------------------------------------------------
+// Warp per (node, slab, chunk of SPAN_CHUNK rows).  A row's z words are read by one group of
+// lanes (coalesced: the row's bits are contiguous), 32 / width rows per warp step, four steps
+// in flight.  Single-chunk slabs store their span; chunked slabs merge into the initialised
+// span / projection with atomics.
+template <int AX>
+__global__ void __launch_bounds__(256) k_spans_rows(const uint32_t* __restrict__ bits, int ny,
+                                                    int nzw, KdLevel L, int64_t items,
+                                                    Span* __restrict__ span,
+                                                    uint32_t* __restrict__ proj) {
+  constexpr int AI = AX == 0 ? A_IX : A_IY, AS = AX == 0 ? A_X : A_Y,
+                AP = AX == 0 ? A_PXZ : A_PYZ;
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
+       it += (int64_t)gridDim.x * wpb) {
+    const int i = find_node(L.off[AI], L.n, it);
     const Box b = L.box[i];
-    const int s = (int)(it - L.off_x[i]);
-    const int x = b.lo[0] + s;
+    const int er = b.hi[1 - AX] - b.lo[1 - AX];
+    const int nch = (er + SPAN_CHUNK - 1) / SPAN_CHUNK;
+    const int local = (int)(it - L.off[AI][i]);
+    const int s = local / nch, c = local - s * nch;
+    const int r0 = c * SPAN_CHUNK, r1 = min(er, r0 + SPAN_CHUNK);
     const int wz = wz_of(b);
-    for (int w = lane; w < wz; w += 32) acc[wib][w] = 0;
-    __syncwarp();
-    int mny = KD_FAR, mxy = -1, mnz = KD_FAR, mxz = -1;
-    for (int y = b.lo[1] + lane; y < b.hi[1]; y += 32) {
-      const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
-      int zf = KD_FAR, zl = -1;
-      for (int w = 0; w < wz; ++w) {
-        const uint32_t v = local_word(row, b.lo[2], b.hi[2], w);
-        if (v) {
-          if (zf == KD_FAR) zf = 32 * w + __ffs(v) - 1;
-          zl = 32 * w + 31 - __clz(v);
-          atomicOr(&acc[wib][w], v);
+    const int gw = group_width(wz), G = 32 / gw;
+    const int g = lane / gw, wl = lane & (gw - 1);
+    const uint32_t gmask = gw == 32 ? 0xffffffffu : ((1u << gw) - 1u);
+    const int slab = b.lo[AX] + s;
+    uint32_t acc = 0;
+    int rmin = KD_FAR, rmax = -1;
+    for (int rb = r0; rb < r1; rb += G * U) {
+      uint32_t v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = rb + u * G + g;
+        v[u] = 0;
+        if (r < r1 && wl < wz) {
+          const int x = AX == 0 ? slab : b.lo[0] + r;
+          const int y = AX == 0 ? b.lo[1] + r : slab;
+          v[u] = local_word(bits + ((int64_t)x * ny + y) * nzw, b.lo[2], b.hi[2], wl);
         }
       }
-      if (zl >= 0) {
-        const int ly = y - b.lo[1];
-        mny = min(mny, ly);
-        mxy = max(mxy, ly);
-        mnz = min(mnz, zf);
-        mxz = max(mxz, zl);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t m = __ballot_sync(0xffffffffu, v[u] != 0);
+        if ((m >> (g * gw)) & gmask) {
+          const int r = rb + u * G + g;
+          rmin = min(rmin, r);
+          rmax = max(rmax, r);
+        }
+        acc |= v[u];
       }
     }
-    for (int o = 16; o; o >>= 1) {
-      mny = min(mny, __shfl_xor_sync(0xffffffffu, mny, o));
-      mxy = max(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
-      mnz = min(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
-      mxz = max(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
+    for (int o = gw; o < 32; o <<= 1) {
+      acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+      rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
     }
-    __syncwarp();
-    if (lane == 0) span_x[it] = Span{mny, mxy, mnz, mxz};
-    uint32_t* dst = pxz + L.off_pxz[i] + (int64_t)s * wz;
-    for (int w = lane; w < wz; w += 32) dst[w] = acc[wib][w];
-    __syncwarp();
+    const uint32_t mz = __ballot_sync(0xffffffffu, acc != 0) & gmask;
+    const int wf = mz ? __ffs(mz) - 1 : 0, wlst = mz ? 31 - __clz(mz) : 0;
+    const uint32_t af = __shfl_sync(0xffffffffu, acc, wf), al = __shfl_sync(0xffffffffu, acc, wlst);
+    Span sp{rmin, rmax, KD_FAR, -1};
+    if (mz) {
+      sp.mn2 = 32 * wf + __ffs(af) - 1;
+      sp.mx2 = 32 * wlst + 31 - __clz(al);
+    }
+    Span* dst = span + L.off[AS][i] + s;
+    uint32_t* pdst = proj + L.off[AP][i] + (int64_t)s * wz;
+    if (nch == 1) {
+      if (lane == 0) *dst = sp;
+      if (lane < wz) pdst[lane] = acc;
+    } else if (rmax >= 0) {
+      if (lane == 0) {
+        atomicMin(&dst->mn1, sp.mn1);
+        atomicMax(&dst->mx1, sp.mx1);
+        atomicMin(&dst->mn2, sp.mn2);
+        atomicMax(&dst->mx2, sp.mx2);
+      }
+      if (lane < wz && acc) atomicOr(pdst + lane, acc);
+    }
   }
 }
 
-// ---- spans along y (and the (y,z) projection): warp per (node, y-slab) --------------------
-__global__ void k_spans_y(const uint32_t* __restrict__ bits, int ny, int nzw, KdLevel L,
-                          const int64_t* __restrict__ total, Span* __restrict__ span_y,
-                          uint32_t* __restrict__ pyz) {
-  __shared__ uint32_t acc[8][32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t items = *total;
-  for (int64_t it = (int64_t)blockIdx.x * 8 + wib; it < items; it += (int64_t)gridDim.x * 8) {
-    const int i = find_node(L.off_y, L.n, it);
-    const Box b = L.box[i];
-    const int s = (int)(it - L.off_y[i]);
-    const int y = b.lo[1] + s;
-    const int wz = wz_of(b);
-    for (int w = lane; w < wz; w += 32) acc[wib][w] = 0;
-    __syncwarp();
-    int mnx = KD_FAR, mxx = -1, mnz = KD_FAR, mxz = -1;
-    for (int x = b.lo[0] + lane; x < b.hi[0]; x += 32) {
-      const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
-      int zf = KD_FAR, zl = -1;
-      for (int w = 0; w < wz; ++w) {
-        const uint32_t v = local_word(row, b.lo[2], b.hi[2], w);
-        if (v) {
-          if (zf == KD_FAR) zf = 32 * w + __ffs(v) - 1;
-          zl = 32 * w + 31 - __clz(v);
-          atomicOr(&acc[wib][w], v);
-        }
-      }
-      if (zl >= 0) {
-        const int lx = x - b.lo[0];
-        mnx = min(mnx, lx);
-        mxx = max(mxx, lx);
-        mnz = min(mnz, zf);
-        mxz = max(mxz, zl);
-      }
-    }
-    for (int o = 16; o; o >>= 1) {
-      mnx = min(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
-      mxx = max(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
-      mnz = min(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
-      mxz = max(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
-    }
-    __syncwarp();
-    if (lane == 0) span_y[it] = Span{mnx, mxx, mnz, mxz};
-    uint32_t* dst = pyz + L.off_pyz[i] + (int64_t)s * wz;
-    for (int w = lane; w < wz; w += 32) dst[w] = acc[wib][w];
-    __syncwarp();
+// Empty spans / projections for the chunked merge.
+__global__ void k_span_init(Span* __restrict__ sx, int64_t nx_, Span* __restrict__ sy, int64_t ny_,
+                            uint32_t* __restrict__ px, int64_t npx, uint32_t* __restrict__ py,
+                            int64_t npy) {
+  const Span e{KD_FAR, -1, KD_FAR, -1};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+       j < max(max(nx_, ny_), max(npx, npy)); j += stride) {
+    if (j < nx_) sx[j] = e;
+    if (j < ny_) sy[j] = e;
+    if (j < npx) px[j] = 0;
+    if (j < npy) py[j] = 0;
   }
 }
 
-// ---- spans along z from the projections: thread per (node, local z word) ------------------
-__global__ void k_spans_z(KdLevel L, const int64_t* __restrict__ total,
-                          const uint32_t* __restrict__ pxz, const uint32_t* __restrict__ pyz,
-                          Span* __restrict__ span_z) {
-  const int64_t items = *total;
-  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    const int i = find_node(L.off_zw, L.n, it);
+// ---- z-slab spans from the two projections: warp per (node, z word) ------------------------
+// Lane k owns local z bit 32w + k.  Per 32 projection rows, one ballot per z bit present in
+// the chunk gives every bit's first / last row.
+__device__ __forceinline__ void proj_minmax(const uint32_t* __restrict__ p, int wz, int e,
+                                            int lane, int& mn, int& mx) {
+  mn = KD_FAR;
+  mx = -1;
+  for (int base = 0; base < e; base += 32) {
+    const int r = base + lane;
+    const uint32_t v = r < e ? p[(int64_t)r * wz] : 0u;
+    uint32_t cor = __reduce_or_sync(0xffffffffu, v);
+    while (cor) {
+      const int k = __ffs(cor) - 1;
+      cor &= cor - 1;
+      const uint32_t bal = __ballot_sync(0xffffffffu, (v >> k) & 1u);
+      if (lane == k) {
+        if (mn == KD_FAR) mn = base + __ffs(bal) - 1;
+        mx = base + 31 - __clz(bal);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_spans_z(KdLevel L, int64_t items,
+                                                 const uint32_t* __restrict__ pxz,
+                                                 const uint32_t* __restrict__ pyz,
+                                                 Span* __restrict__ span_z) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
+       it += (int64_t)gridDim.x * wpb) {
+    const int i = find_node(L.off[A_ZW], L.n, it);
     const Box b = L.box[i];
-    const int w = (int)(it - L.off_zw[i]);
+    const int w = (int)(it - L.off[A_ZW][i]);
     const int wz = wz_of(b);
     const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
     const int nzb = min(32, ez - 32 * w);
-    int mnx[32], mxx[32];
-    // first / last x per z bit
-    uint32_t seen = 0;
-    const uint32_t* px = pxz + L.off_pxz[i] + w;
-    for (int x = 0; x < ex && seen != 0xffffffffu; ++x) {
-      uint32_t nw = px[(int64_t)x * wz] & ~seen;
-      seen |= nw;
-      while (nw) { int k = __ffs(nw) - 1; nw &= nw - 1; mnx[k] = x; }
-    }
-    const uint32_t any = seen;
-    seen = 0;
-    for (int x = ex - 1; x >= 0 && seen != any; --x) {
-      uint32_t nw = px[(int64_t)x * wz] & ~seen;
-      seen |= nw;
-      while (nw) { int k = __ffs(nw) - 1; nw &= nw - 1; mxx[k] = x; }
-    }
-    Span* out = span_z + L.off_z[i] + 32 * w;
-    for (int k = 0; k < nzb; ++k) {
-      const bool ok = (any >> k) & 1u;
-      out[k].mn1 = ok ? mnx[k] : KD_FAR;
-      out[k].mx1 = ok ? mxx[k] : -1;
-    }
-    const uint32_t* py = pyz + L.off_pyz[i] + w;
-    seen = 0;
-    for (int y = 0; y < ey && seen != any; ++y) {
-      uint32_t nw = py[(int64_t)y * wz] & ~seen;
-      seen |= nw;
-      while (nw) { int k = __ffs(nw) - 1; nw &= nw - 1; mnx[k] = y; }
-    }
-    seen = 0;
-    for (int y = ey - 1; y >= 0 && seen != any; --y) {
-      uint32_t nw = py[(int64_t)y * wz] & ~seen;
-      seen |= nw;
-      while (nw) { int k = __ffs(nw) - 1; nw &= nw - 1; mxx[k] = y; }
-    }
-    for (int k = 0; k < nzb; ++k) {
-      const bool ok = (any >> k) & 1u;
-      out[k].mn2 = ok ? mnx[k] : KD_FAR;
-      out[k].mx2 = ok ? mxx[k] : -1;
-    }
+    Span sp;
+    proj_minmax(pxz + L.off[A_PXZ][i] + w, wz, ex, lane, sp.mn1, sp.mx1);
+    proj_minmax(pyz + L.off[A_PYZ][i] + w, wz, ey, lane, sp.mn2, sp.mx2);
+    if (lane < nzb) span_z[L.off[A_Z][i] + 32 * w + lane] = sp;
   }
 }
 
@@ -469,15 +482,15 @@ __device__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a, 
 // ---- the decision kernel: one warp per node ------------------------------------------------
 __global__ void k_decide(KdLevel L, KdParams P, const Span* __restrict__ span_x,
                          const Span* __restrict__ span_y, const Span* __restrict__ span_z,
-                         RBox* __restrict__ scratch, const int64_t* __restrict__ off_scr,
-                         BinnedCtx B, KdDecision* __restrict__ out) {
+                         RBox* __restrict__ scratch, BinnedCtx B, KdDecision* __restrict__ out,
+                         int64_t* __restrict__ child_count) {
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= L.n) return;
   const Box b = L.box[i];
   int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
   const int64_t vol = box_vol(b);
-  const Span* sp[3] = {span_x + L.off_x[i], span_y + L.off_y[i], span_z + L.off_z[i]};
+  const Span* sp[3] = {span_x + L.off[A_X][i], span_y + L.off[A_Y][i], span_z + L.off[A_Z][i]};
   KdDecision d;
   d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.leaf = b;
   bool split = false;
@@ -490,7 +503,7 @@ __global__ void k_decide(KdLevel L, KdParams P, const Span* __restrict__ span_x,
         if (ext[a] < 2) continue;
         int k;
         int64_t c;
-        sweep_axis(sp[a], ext[a], scratch + off_scr[i], lane, k, c);
+        sweep_axis(sp[a], ext[a], scratch + L.off[A_SCR][i], lane, k, c);
         if (ba >= 0 && c >= bc) continue;
         ba = a; bk = k; bc = c;
       }
@@ -565,43 +578,10 @@ __global__ void k_decide(KdLevel L, KdParams P, const Span* __restrict__ span_x,
       split = true;
     }
   }
-  if (lane == 0) out[i] = d;
-}
-
-// Which nodes need bit spans this level (sweep: any node that may search or force-split;
-// binned: only nodes that will be leaves -> decided after the binned pass, so all
-// candidates here; the host runs the spans for binned leaves in a second pass).
-__global__ void k_need(KdLevel L, KdParams P, int binned_pass2,
-                       const KdDecision* __restrict__ dec) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= L.n) return;
-  const Box b = L.box[i];
-  const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
-  int need;
-  if (!P.binned) {
-    const int mx = max(ext[0], max(ext[1], ext[2]));
-    need = (!halted(P, box_vol(b)) || (P.mls >= 0 && mx > P.mls)) ? 1 : 0;
-  } else {
-    need = binned_pass2 ? (dec[i].axis < 0 ? 1 : 0) : 0;
+  if (lane == 0) {
+    out[i] = d;
+    child_count[i] = __popc(d.nchild);
   }
-  L.need[i] = need;
-  const int wz = (ext[2] + 31) >> 5;
-  // per-node sizes (scanned by the host afterwards)
-  L.off_x[i] = need ? ext[0] : 0;
-  L.off_y[i] = (need && !P.binned) ? ext[1] : 0;
-  L.off_z[i] = (need && !P.binned) ? ext[2] : 0;
-  L.off_pxz[i] = need ? (int64_t)ext[0] * wz : 0;
-  L.off_pyz[i] = (need && !P.binned) ? (int64_t)ext[1] * wz : 0;
-  L.off_zw[i] = (need && !P.binned) ? wz : 0;
-}
-
-// Scratch for the suffix boxes: max extent of the node (any axis).
-__global__ void k_scratch_sizes(KdLevel L, int64_t* __restrict__ sz) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= L.n) return;
-  const Box b = L.box[i];
-  const int m = max(b.hi[0] - b.lo[0], max(b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]));
-  sz[i] = (L.need[i] & 1) ? m : 0;
 }
 
 // ---- cell boxes (precompute_cell_boxes, kdtree.py:285-320) ---------------------------------
@@ -637,12 +617,13 @@ __global__ void k_cell_boxes(const uint32_t* __restrict__ bits, int nx, int ny, 
 
 // Cell-slab unions along axis A: warp per (node, cell slab c in the node's cell range).
 __global__ void k_cell_slabs(const CBox* __restrict__ cells, int ncx, int ncy, int ncz, int cs,
-                             int A, KdLevel L, const int64_t* __restrict__ off,
-                             const int64_t* __restrict__ total, CBox* __restrict__ out) {
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+                             int A, KdLevel L, int64_t items, CBox* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
   const int nc[3] = {ncx, ncy, ncz};
-  const int64_t items = *total;
-  for (int64_t it = (int64_t)blockIdx.x * 8 + wib; it < items; it += (int64_t)gridDim.x * 8) {
+  const int64_t* off = L.off[A_C0 + A];
+  for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
+       it += (int64_t)gridDim.x * wpb) {
     const int i = find_node(off, L.n, it);
     const Box b = L.box[i];
     int c0[3], c1[3];
@@ -671,31 +652,68 @@ __global__ void k_cell_slabs(const CBox* __restrict__ cells, int ncx, int ncy, i
   }
 }
 
-__global__ void k_cell_slab_sizes(KdLevel L, int cs, int ncx, int ncy, int ncz, int A,
-                                  int64_t* __restrict__ sz) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= L.n) return;
-  const int nc[3] = {ncx, ncy, ncz};
-  int c0, c1;
-  node_cell_range(L.box[i], cs, nc, A, c0, c1);
-  sz[i] = c1 - c0 + 1;
-}
-
-// ---- next level + bookkeeping ---------------------------------------------------------------
-__global__ void k_child_counts(const KdDecision* __restrict__ dec, int n, int64_t* __restrict__ cnt) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  cnt[i] = __popc(dec[i].nchild);
-}
-
+// ---- level bookkeeping ----------------------------------------------------------------------
 struct NodeRec {   // per node, global BFS id
   Box box;
   int axis, plane, left, right, dropped, level;
 };
 
+// Per-node work sizes of a level (written where the node's box is emitted).
+struct PrepCtx {
+  KdParams P;
+  int nc[3];
+  int64_t* arr[KA];   // per-node sizes, scanned in place afterwards
+};
+
+__device__ __forceinline__ void prep_node(const PrepCtx& C, const Box& b, int64_t i) {
+  const KdParams& P = C.P;
+  const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
+  int64_t v[KA];
+  for (int k = 0; k < KA; ++k) v[k] = 0;
+  if (!P.binned) {
+    const int mx = max(ext[0], max(ext[1], ext[2]));
+    const bool need = !halted(P, box_vol(b)) || (P.mls >= 0 && mx > P.mls);
+    if (need) {
+      const int wz = (ext[2] + 31) >> 5;
+      v[A_X] = ext[0];
+      v[A_Y] = ext[1];
+      v[A_Z] = ext[2];
+      v[A_PXZ] = (int64_t)ext[0] * wz;
+      v[A_PYZ] = (int64_t)ext[1] * wz;
+      v[A_ZW] = wz;
+      v[A_SCR] = mx;
+      v[A_IX] = (int64_t)ext[0] * ((ext[1] + SPAN_CHUNK - 1) / SPAN_CHUNK);
+      v[A_IY] = (int64_t)ext[1] * ((ext[0] + SPAN_CHUNK - 1) / SPAN_CHUNK);
+    }
+  } else {
+    for (int a = 0; a < 3; ++a) {
+      int c0, c1;
+      node_cell_range(b, P.cs, C.nc, a, c0, c1);
+      v[A_C0 + a] = c1 - c0 + 1;
+    }
+  }
+  for (int k = 0; k < KA; ++k) C.arr[k][i] = v[k];
+}
+
+// Root level: one box from the device bbox (empty volume -> zero nodes).
+__global__ void k_root_level(const int* __restrict__ bb, Box* __restrict__ box, PrepCtx C,
+                             int64_t* __restrict__ hdr) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Box r;
+  for (int k = 0; k < 3; ++k) { r.lo[k] = bb[k]; r.hi[k] = bb[3 + k]; }
+  const bool any = bb[3] >= 0;
+  hdr[0] = any ? 1 : 0;
+  if (any) {
+    box[0] = r;
+    C.P.root_vol = box_vol(r);
+    prep_node(C, r, 0);
+  }
+}
+
+// Rows of this level's nodes + the next level's boxes (left child first) and work sizes.
 __global__ void k_emit_level(const KdDecision* __restrict__ dec, const int64_t* __restrict__ coff,
                              int n, int64_t base, int64_t next_base, int level,
-                             NodeRec* __restrict__ rec, Box* __restrict__ next_box) {
+                             NodeRec* __restrict__ rec, Box* __restrict__ next_box, PrepCtx C) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const KdDecision d = dec[i];
@@ -707,92 +725,194 @@ __global__ void k_emit_level(const KdDecision* __restrict__ dec, const int64_t* 
   r.dropped = d.dropped;
   r.level = level;
   int64_t o = coff[i];
-  if (d.nchild & 1) { next_box[o] = d.left; r.left = (int)(next_base + o); ++o; }
-  if (d.nchild & 2) { next_box[o] = d.right; r.right = (int)(next_base + o); }
+  if (d.nchild & 1) {
+    next_box[o] = d.left;
+    prep_node(C, d.left, o);
+    r.left = (int)(next_base + o);
+    ++o;
+  }
+  if (d.nchild & 2) {
+    next_box[o] = d.right;
+    prep_node(C, d.right, o);
+    r.right = (int)(next_base + o);
+  }
   rec[base + i] = r;
 }
 
-
-// Binned leaves: exact shrink_to_occupied(box) from the x spans; empty -> dropped.
-__global__ void k_leaf_shrink(KdLevel L, const Span* __restrict__ span_x,
-                              KdDecision* __restrict__ dec) {
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= L.n || !(L.need[i] & 1)) return;
+// Binned leaves: exact shrink_to_occupied(box) (kdtree.py:474) read straight from the bits;
+// empty -> dropped (no row).  Block per node; non-leaves exit at once.
+__global__ void __launch_bounds__(128) k_leaf_shrink(const uint32_t* __restrict__ bits, int ny,
+                                                     int nzw, KdLevel L,
+                                                     KdDecision* __restrict__ dec) {
+  const int i = blockIdx.x;
+  if (i >= L.n || dec[i].axis >= 0) return;
+  __shared__ int red[6];
   const Box b = L.box[i];
-  const RBox t = range_box(span_x + L.off_x[i], 0, b.hi[0] - b.lo[0], lane);
-  if (lane == 0) {
-    if (t.hi0 < 0) dec[i].dropped = 1;
-    else dec[i].leaf = to_global(b, 0, t);
-  }
-}
-
-// Single-CTA exclusive scan of K int64 arrays of n+1 entries each (entry n = total).
-struct ScanSet {
-  int64_t* a[12];
-  int k;
-};
-
-__global__ void k_multi_scan(ScanSet S, int n) {
-  __shared__ int64_t part[1024];
-  const int t = threadIdx.x, T = blockDim.x;
-  const int64_t len = (int64_t)n + 1;
-  const int64_t chunk = (len + T - 1) / T;
-  for (int k = 0; k < S.k; ++k) {
-    int64_t* a = S.a[k];
-    const int64_t b0 = t * chunk, b1 = min(len, b0 + chunk);
-    int64_t sum = 0;
-    for (int64_t j = b0; j < b1; ++j) sum += (j < n) ? a[j] : 0;
-    part[t] = sum;
-    __syncthreads();
-    for (int o = 1; o < T; o <<= 1) {
-      int64_t v = t >= o ? part[t - o] : 0;
-      __syncthreads();
-      part[t] += v;
-      __syncthreads();
-    }
-    int64_t run = part[t] - sum;  // exclusive prefix of this chunk
-    for (int64_t j = b0; j < b1; ++j) {
-      const int64_t v = (j < n) ? a[j] : 0;
-      a[j] = run;
-      run += v;
-    }
-    __syncthreads();
-  }
-}
-
-// Root box: tight box of every set bit (shrink_to_occupied of the full volume).
-__global__ void k_bits_bbox(const uint32_t* __restrict__ bits, int nx, int ny, int nz,
-                            int* __restrict__ bb) {
-  const int nzw = (int)nzw_of(nz);
-  const int64_t nrows = (int64_t)nx * ny;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x < 6) red[threadIdx.x] = threadIdx.x < 3 ? KD_FAR : -1;
+  __syncthreads();
+  const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1];
+  const int wz = wz_of(b), gw = group_width(wz), G = 32 / gw;
+  const int g = lane / gw, wl = lane & (gw - 1);
+  const uint32_t gmask = gw == 32 ? 0xffffffffu : ((1u << gw) - 1u);
+  const int64_t rows = (int64_t)ex * ey;
   int lo[3] = {KD_FAR, KD_FAR, KD_FAR}, hi[3] = {-1, -1, -1};
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(r / ny), y = (int)(r % ny);
-    const uint32_t* row = bits + r * nzw;
-    int zf = -1, zl = -1;
-    for (int w = 0; w < nzw; ++w) {
-      const uint32_t v = row[w];
-      if (v) {
-        if (zf < 0) zf = 32 * w + __ffs(v) - 1;
-        zl = 32 * w + 31 - __clz(v);
-      }
+  uint32_t acc = 0;
+  for (int64_t rb = (int64_t)warp * G; rb < rows; rb += (int64_t)nw * G) {
+    const int64_t q = rb + g;
+    uint32_t v = 0;
+    int x = 0, y = 0;
+    if (q < rows && wl < wz) {
+      x = (int)(q / ey);
+      y = (int)(q - (int64_t)x * ey);
+      v = local_word(bits + ((int64_t)(b.lo[0] + x) * ny + b.lo[1] + y) * nzw, b.lo[2], b.hi[2], wl);
     }
-    if (zf >= 0) {
+    const uint32_t m = __ballot_sync(0xffffffffu, v != 0);
+    if (wl == 0 && ((m >> (g * gw)) & gmask)) {
       lo[0] = min(lo[0], x); hi[0] = max(hi[0], x);
       lo[1] = min(lo[1], y); hi[1] = max(hi[1], y);
-      lo[2] = min(lo[2], zf); hi[2] = max(hi[2], zl);
     }
+    acc |= v;
   }
-  for (int k = 0; k < 3; ++k) {
-    for (int o = 16; o; o >>= 1) {
+  // z extent from the per-lane OR words
+  for (int o = gw; o < 32; o <<= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+  const uint32_t mz = __ballot_sync(0xffffffffu, acc != 0) & gmask;
+  const int wf = mz ? __ffs(mz) - 1 : 0, wlst = mz ? 31 - __clz(mz) : 0;
+  const uint32_t af = __shfl_sync(0xffffffffu, acc, wf), al = __shfl_sync(0xffffffffu, acc, wlst);
+  if (mz) {
+    lo[2] = 32 * wf + __ffs(af) - 1;
+    hi[2] = 32 * wlst + 31 - __clz(al);
+  }
+  for (int o = 16; o; o >>= 1)
+    for (int k = 0; k < 3; ++k) {
       lo[k] = min(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
       hi[k] = max(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
     }
+  if (lane == 0 && hi[0] >= 0)
+    for (int k = 0; k < 3; ++k) { atomicMin(&red[k], lo[k]); atomicMax(&red[3 + k], hi[k]); }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (red[3] < 0) {
+      dec[i].dropped = 1;
+    } else {
+      Box t;
+      for (int k = 0; k < 3; ++k) { t.lo[k] = b.lo[k] + red[k]; t.hi[k] = b.lo[k] + red[3 + k] + 1; }
+      dec[i].leaf = t;
+    }
   }
-  if ((threadIdx.x & 31) == 0 && hi[0] >= 0)
-    for (int k = 0; k < 3; ++k) { atomicMin(bb + k, lo[k]); atomicMax(bb + 3 + k, hi[k] + 1); }
+}
+
+// Exclusive scans of up to KA int64 arrays of n entries in place (entry n = total, also copied
+// to totals[j]); n read from the device.  Block per array, 1024 threads, 4 items per thread.
+struct ScanSet {
+  int64_t* a[KA + 1];
+  int64_t* totals[KA + 1];
+  int k;
+};
+
+__global__ void __launch_bounds__(1024) k_multi_scan(ScanSet S, const int64_t* __restrict__ n_ptr,
+                                                    int64_t n_host) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry_s;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t n = n_ptr ? *n_ptr : n_host;
+  int64_t* a = S.a[blockIdx.x];
+  if (t == 0) carry_s = 0;
+  __syncthreads();
+  constexpr int PER = 4, TILE = 1024 * PER;
+  for (int64_t base = 0; base < n; base += TILE) {
+    int64_t v[PER], s = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int64_t j = base + (int64_t)t * PER + k;
+      v[k] = j < n ? a[j] : 0;
+      s += v[k];
+    }
+    int64_t incl = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = wsum[lane], wi = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += u;
+      }
+      wsum[lane] = wi - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    int64_t run = carry_s + wsum[warp] + incl - s;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int64_t j = base + (int64_t)t * PER + k;
+      if (j < n) a[j] = run;
+      run += v[k];
+    }
+    __syncthreads();
+    if (t == 1023) carry_s = run;
+    __syncthreads();
+  }
+  if (t == 0) {
+    a[n] = carry_s;
+    if (S.totals[blockIdx.x]) *S.totals[blockIdx.x] = carry_s;
+  }
+}
+
+// Root box: tight box of every set bit (shrink_to_occupied of the full volume).  Warp per
+// chunk of rows, lanes over a row's words (coalesced).
+__global__ void __launch_bounds__(256) k_bits_bbox(const uint32_t* __restrict__ bits, int nx,
+                                                   int ny, int nz, int* __restrict__ bb) {
+  const int nzw = (int)nzw_of(nz);
+  const int lane = threadIdx.x & 31;
+  const int gw = group_width(nzw), G = 32 / gw;
+  const int g = lane / gw, wl = lane & (gw - 1);
+  const uint32_t gmask = gw == 32 ? 0xffffffffu : ((1u << gw) - 1u);
+  const int64_t nrows = (int64_t)nx * ny;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int lo[2] = {KD_FAR, KD_FAR}, hi[2] = {-1, -1};
+  uint32_t acc = 0;
+  for (int64_t rb = wid * G; rb < nrows; rb += nwarps * G * 4) {
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t r = rb + (int64_t)u * nwarps * G + g;
+      v[u] = (r < nrows && wl < nzw) ? __ldg(bits + r * nzw + wl) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t r = rb + (int64_t)u * nwarps * G + g;
+      const uint32_t m = __ballot_sync(0xffffffffu, v[u] != 0);
+      if ((m >> (g * gw)) & gmask) {
+        const int x = (int)(r / ny), y = (int)(r - (int64_t)x * ny);
+        lo[0] = min(lo[0], x); hi[0] = max(hi[0], x);
+        lo[1] = min(lo[1], y); hi[1] = max(hi[1], y);
+      }
+      acc |= v[u];
+    }
+  }
+  for (int o = gw; o < 32; o <<= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+  const uint32_t mz = __ballot_sync(0xffffffffu, acc != 0) & gmask;
+  const int wf = mz ? __ffs(mz) - 1 : 0, wlst = mz ? 31 - __clz(mz) : 0;
+  const uint32_t af = __shfl_sync(0xffffffffu, acc, wf), al = __shfl_sync(0xffffffffu, acc, wlst);
+  int zlo = KD_FAR, zhi = -1;
+  if (mz) {
+    zlo = 32 * wf + __ffs(af) - 1;
+    zhi = 32 * wlst + 31 - __clz(al);
+  }
+  for (int o = 16; o; o >>= 1)
+    for (int k = 0; k < 2; ++k) {
+      lo[k] = min(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = max(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  if (lane == 0 && hi[0] >= 0) {
+    atomicMin(bb + 0, lo[0]); atomicMax(bb + 3, hi[0] + 1);
+    atomicMin(bb + 1, lo[1]); atomicMax(bb + 4, hi[1] + 1);
+    atomicMin(bb + 2, zlo); atomicMax(bb + 5, zhi + 1);
+  }
 }
 
 // Finalisation: subtree sizes (bottom-up per level), preorder (top-down per level), rows.
@@ -847,6 +967,30 @@ using namespace vs;
 
 namespace {
 
+// The library's stream-ordered pool: freed scratch stays mapped (release threshold = max), so
+// a build's per-level buffers and the next build's reuse them without remapping memory.
+cudaMemPool_t lib_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    cudaDeviceGetDefaultMemPool(&pool, dev);
+  }
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  pools[dev] = pool;
+  return pool;
+}
+
 // Grow-only stream-ordered scratch buffer (data-dependent sizes: the k-d tree's level widths
 // are only known as it is built).
 struct DBuf {
@@ -857,11 +1001,13 @@ struct DBuf {
     if (bytes <= cap) return 0;
     if (p) cudaFreeAsync(p, st);
     size_t nb = std::max(bytes, cap * 3 / 2 + 256);
-    cudaError_t e = cudaMallocAsync(&p, nb, st);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaMallocFromPoolAsync(&p, nb, lib_pool(dev), st);
     if (e != cudaSuccess) {
       p = nullptr;
       cap = 0;
-      set_error("%s: cudaMallocAsync(%zu): %s", what, nb, cudaGetErrorString(e));
+      set_error("%s: cudaMallocFromPoolAsync(%zu): %s", what, nb, cudaGetErrorString(e));
       return (int)e;
     }
     cap = nb;
@@ -889,10 +1035,18 @@ int d2h(void* dst, const void* src, size_t n, cudaStream_t st) {
 
 constexpr int SPAN_BLOCKS = 148 * 8;
 
+unsigned grid_for(int64_t items, int per_block, int cap = 148 * 64) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(items, per_block), cap));
+}
+
 }  // namespace
 
 extern "C" {
 
+// Level-synchronous build with one host synchronisation per level: the level's work sizes
+// are computed where its boxes are emitted (prep_node) and scanned on the device; the host
+// reads {node count, totals} once, sizes the level's buffers and launches the span passes,
+// the decisions and the next level's emission.
 int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, int binned,
                 int bins, int cs, void** handle, vs_stream_t stream) {
   if (!bits || !handle || nx < 1 || ny < 1 || nz < 1 || bins < 2 || cs < 1)
@@ -905,151 +1059,155 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
   for (DBuf* b : {&R->lo, &R->hi, &R->axis, &R->plane, &R->left, &R->right}) b->st = st;
   const int nzw = (int)nzw_of(nz);
 
-  DBuf bb, cur, nxt, need, offs, dec, cnt, spx, spy, spz, pxz, pyz, scr, rec, cellb, cslab,
-      coff, sizes, pre, tot;
-  for (DBuf* b : {&bb, &cur, &nxt, &need, &offs, &dec, &cnt, &spx, &spy, &spz, &pxz, &pyz, &scr,
-                  &rec, &cellb, &cslab, &coff, &sizes, &pre, &tot})
+  DBuf bb, cur, nxt, offs, dec, cnt, spx, spy, spz, pxz, pyz, scr, rec, cellb, cslab, sizes, pre,
+      hdr;
+  for (DBuf* b : {&bb, &cur, &nxt, &offs, &dec, &cnt, &spx, &spy, &spz, &pxz, &pyz, &scr, &rec,
+                  &cellb, &cslab, &sizes, &pre, &hdr})
     b->st = st;
 
-  // root box (kdtree.py:398): tight box of every flag
-  VS_TRY(bb.ensure(6 * sizeof(int), "bbox"));
-  const int init[6] = {KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
-  VS_CUDA(cudaMemcpyAsync(bb.p, init, sizeof init, cudaMemcpyHostToDevice, st), "bbox init");
-  k_bits_bbox<<<SPAN_BLOCKS, 256, 0, st>>>(bits, nx, ny, nz, bb.as<int>());
-  VS_TRY(check_launch("k_bits_bbox"));
-  int rb[6];
-  VS_TRY(d2h(rb, bb.p, sizeof rb, st));
-  if (rb[3] < 0) return 0;  // empty tree
-  Box root;
-  for (int k = 0; k < 3; ++k) { root.lo[k] = rb[k]; root.hi[k] = rb[3 + k]; }
-
   KdParams P;
-  P.deep = deep; P.mls = mls; P.binned = binned; P.bins = bins; P.cs = cs;
-  P.root_vol = box_vol(root);
-
+  P.deep = deep; P.mls = mls; P.binned = binned; P.bins = bins; P.cs = cs; P.root_vol = 0;
   const int ncx = (int)cdiv(nx, cs), ncy = (int)cdiv(ny, cs), ncz = (int)cdiv(nz, cs);
-  if (binned) {
-    const int64_t ncell = (int64_t)ncx * ncy * ncz;
-    VS_TRY(cellb.ensure(ncell * sizeof(CBox), "cells"));
-    k_cell_boxes<<<(unsigned)cdiv(ncell, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy,
-                                                             ncz, cellb.as<CBox>());
-    VS_TRY(check_launch("k_cell_boxes"));
+
+  // header: [0] node count of the level being prepared, [1 + k] total of offset array k,
+  // [KA + 1] child total (next level's node count), [KA + 2 ..] root bbox ints
+  constexpr int H = KA + 4;
+  VS_TRY(hdr.ensure(H * sizeof(int64_t) + 8 * sizeof(int), "header"));
+  int64_t* dh = hdr.as<int64_t>();
+  int* dbb = reinterpret_cast<int*>(dh + H);
+  int64_t hh[H];
+
+  // per-level offset arrays: KA arrays of stride cap + 1
+  int64_t cap = 0;
+  auto arrays = [&](int64_t need_cap) -> int {
+    if (need_cap > cap) {
+      cap = std::max<int64_t>(need_cap, cap * 2);
+      VS_TRY(offs.ensure((size_t)KA * (cap + 1) * sizeof(int64_t), "offsets"));
+    }
+    return 0;
+  };
+  auto arr = [&](int k) { return offs.as<int64_t>() + (int64_t)k * (cap + 1); };
+  auto prep_ctx = [&]() {
+    PrepCtx C;
+    C.P = P;
+    C.nc[0] = ncx; C.nc[1] = ncy; C.nc[2] = ncz;
+    for (int k = 0; k < KA; ++k) C.arr[k] = arr(k);
+    return C;
+  };
+  const int nscan = binned ? 3 : 9;
+  const int scan0 = binned ? A_C0 : 0;
+  auto scan_level = [&](const int64_t* n_dev) -> int {
+    ScanSet S;
+    S.k = nscan;
+    for (int j = 0; j < nscan; ++j) {
+      S.a[j] = arr(scan0 + j);
+      S.totals[j] = dh + 1 + scan0 + j;
+    }
+    k_multi_scan<<<nscan, 1024, 0, st>>>(S, n_dev, 0);
+    return check_launch("k_multi_scan");
+  };
+
+  // root box (kdtree.py:398): tight box of every flag
+  const int init[8] = {KD_FAR, KD_FAR, KD_FAR, -1, -1, -1, 0, 0};
+  VS_CUDA(cudaMemcpyAsync(dbb, init, sizeof init, cudaMemcpyHostToDevice, st), "bbox init");
+  VS_CUDA(cudaMemsetAsync(dh, 0, H * sizeof(int64_t), st), "header init");
+  k_bits_bbox<<<SPAN_BLOCKS, 256, 0, st>>>(bits, nx, ny, nz, dbb);
+  VS_TRY(check_launch("k_bits_bbox"));
+  VS_TRY(arrays(1));
+  VS_TRY(cur.ensure(sizeof(Box), "level"));
+  {
+    // root_vol is needed by every level's halting rule: read the bbox with the header
+    k_root_level<<<1, 32, 0, st>>>(dbb, cur.as<Box>(), prep_ctx(), dh);
+    VS_TRY(check_launch("k_root_level"));
+    VS_TRY(scan_level(dh));
+    int rb[6];
+    VS_CUDA(cudaMemcpyAsync(rb, dbb, sizeof rb, cudaMemcpyDeviceToHost, st), "bbox d2h");
+    VS_TRY(d2h(hh, dh, sizeof hh, st));
+    if (rb[3] < 0) return 0;  // empty tree
+    P.root_vol = (int64_t)(rb[3] - rb[0]) * (rb[4] - rb[1]) * (rb[5] - rb[2]);
   }
 
-  VS_TRY(cur.ensure(sizeof(Box), "level"));
-  VS_CUDA(cudaMemcpyAsync(cur.p, &root, sizeof root, cudaMemcpyHostToDevice, st), "root");
-  int64_t n = 1, base = 0;
+  int64_t n = hh[0], base = 0;
   std::vector<int64_t> level_base;
   int level = 0;
   while (n > 0) {
     level_base.push_back(base);
-    // per-level arrays: need (n ints), 12 offset arrays (n+1 int64), decisions, counts
-    VS_TRY(need.ensure(n * sizeof(int), "need"));
-    VS_TRY(offs.ensure(12 * (n + 1) * sizeof(int64_t), "offsets"));
+    KdLevel L;
+    L.n = (int)n;
+    L.box = cur.as<Box>();
+    for (int k = 0; k < KA; ++k) L.off[k] = arr(k);
+    const int64_t* tot = hh + 1;
     VS_TRY(dec.ensure(n * sizeof(KdDecision), "decisions"));
     VS_TRY(cnt.ensure((n + 1) * sizeof(int64_t), "counts"));
-    VS_TRY(tot.ensure(16 * sizeof(int64_t), "totals"));
-    int64_t* O = offs.as<int64_t>();
-    auto arr = [&](int k) { return O + (int64_t)k * (n + 1); };
-    KdLevel L;
-    L.n = (int)n; L.box = cur.as<Box>(); L.need = need.as<int>();
-    L.off_x = arr(0); L.off_y = arr(1); L.off_z = arr(2);
-    L.off_pxz = arr(3); L.off_pyz = arr(4); L.off_zw = arr(5);
-    int64_t* scr_off = arr(6);
     BinnedCtx B;
     B.nc[0] = ncx; B.nc[1] = ncy; B.nc[2] = ncz;
-    const unsigned gn = (unsigned)cdiv(n, 128);
     const unsigned gw = (unsigned)cdiv(n, 4);  // warp per node, 128-thread blocks
-    auto scan = [&](std::initializer_list<int64_t*> lst) -> int {
-      ScanSet S;
-      S.k = 0;
-      for (int64_t* a : lst) S.a[S.k++] = a;
-      k_multi_scan<<<1, 1024, 0, st>>>(S, (int)n);
-      return check_launch("k_multi_scan");
-    };
-    auto totals = [&](std::initializer_list<int64_t*> lst, int64_t* out) -> int {
-      int k = 0;
-      for (int64_t* a : lst) {
-        VS_CUDA(cudaMemcpyAsync(tot.as<int64_t>() + k, a + n, sizeof(int64_t),
-                                cudaMemcpyDeviceToDevice, st), "tot");
-        ++k;
-      }
-      return d2h(out, tot.p, k * sizeof(int64_t), st);
-    };
     if (!binned) {
-      k_need<<<gn, 128, 0, st>>>(L, P, 0, nullptr);
-      VS_TRY(check_launch("k_need"));
-      k_scratch_sizes<<<gn, 128, 0, st>>>(L, scr_off);
-      VS_TRY(check_launch("k_scratch_sizes"));
-      VS_TRY(scan({L.off_x, L.off_y, L.off_z, L.off_pxz, L.off_pyz, L.off_zw, scr_off}));
-      int64_t t[7];
-      VS_TRY(totals({L.off_x, L.off_y, L.off_z, L.off_pxz, L.off_pyz, L.off_zw, scr_off}, t));
-      VS_TRY(spx.ensure((t[0] + 1) * sizeof(Span), "span_x"));
-      VS_TRY(spy.ensure((t[1] + 1) * sizeof(Span), "span_y"));
-      VS_TRY(spz.ensure((t[2] + 32) * sizeof(Span), "span_z"));
-      VS_TRY(pxz.ensure((t[3] + 1) * 4, "pxz"));
-      VS_TRY(pyz.ensure((t[4] + 1) * 4, "pyz"));
-      VS_TRY(scr.ensure((t[6] + 1) * sizeof(RBox), "scratch"));
-      if (t[0] > 0) {
-        k_spans_x<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_x + n, spx.as<Span>(),
-                                               pxz.as<uint32_t>());
-        VS_TRY(check_launch("k_spans_x"));
-        k_spans_y<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_y + n, spy.as<Span>(),
-                                               pyz.as<uint32_t>());
-        VS_TRY(check_launch("k_spans_y"));
-        k_spans_z<<<SPAN_BLOCKS, 128, 0, st>>>(L, L.off_zw + n, pxz.as<uint32_t>(),
-                                               pyz.as<uint32_t>(), spz.as<Span>());
+      VS_TRY(spx.ensure((tot[A_X] + 1) * sizeof(Span), "span_x"));
+      VS_TRY(spy.ensure((tot[A_Y] + 1) * sizeof(Span), "span_y"));
+      VS_TRY(spz.ensure((tot[A_Z] + 32) * sizeof(Span), "span_z"));
+      VS_TRY(pxz.ensure((tot[A_PXZ] + 1) * 4, "pxz"));
+      VS_TRY(pyz.ensure((tot[A_PYZ] + 1) * 4, "pyz"));
+      VS_TRY(scr.ensure((tot[A_SCR] + 1) * sizeof(RBox), "scratch"));
+      if (tot[A_X] > 0) {
+        if (tot[A_IX] > tot[A_X] || tot[A_IY] > tot[A_Y]) {  // some slab is chunked
+          const int64_t mx = std::max(std::max(tot[A_X], tot[A_Y]),
+                                      std::max(tot[A_PXZ], tot[A_PYZ]));
+          k_span_init<<<grid_for(mx, 256), 256, 0, st>>>(spx.as<Span>(), tot[A_X], spy.as<Span>(),
+                                                         tot[A_Y], pxz.as<uint32_t>(), tot[A_PXZ],
+                                                         pyz.as<uint32_t>(), tot[A_PYZ]);
+          VS_TRY(check_launch("k_span_init"));
+        }
+        k_spans_rows<0><<<grid_for(tot[A_IX], 8), 256, 0, st>>>(bits, ny, nzw, L, tot[A_IX],
+                                                                spx.as<Span>(), pxz.as<uint32_t>());
+        VS_TRY(check_launch("k_spans_rows<x>"));
+        k_spans_rows<1><<<grid_for(tot[A_IY], 8), 256, 0, st>>>(bits, ny, nzw, L, tot[A_IY],
+                                                                spy.as<Span>(), pyz.as<uint32_t>());
+        VS_TRY(check_launch("k_spans_rows<y>"));
+        k_spans_z<<<grid_for(tot[A_ZW], 8), 256, 0, st>>>(L, tot[A_ZW], pxz.as<uint32_t>(),
+                                                          pyz.as<uint32_t>(), spz.as<Span>());
         VS_TRY(check_launch("k_spans_z"));
       }
       k_decide<<<gw, 128, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(), spz.as<Span>(),
-                                   scr.as<RBox>(), scr_off, B, dec.as<KdDecision>());
+                                   scr.as<RBox>(), B, dec.as<KdDecision>(), cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
     } else {
-      int64_t* co[3] = {arr(7), arr(8), arr(9)};
-      for (int a = 0; a < 3; ++a) {
-        k_cell_slab_sizes<<<gn, 128, 0, st>>>(L, cs, ncx, ncy, ncz, a, co[a]);
-        VS_TRY(check_launch("k_cell_slab_sizes"));
+      if (level == 0) {
+        const int64_t ncell = (int64_t)ncx * ncy * ncz;
+        VS_TRY(cellb.ensure(ncell * sizeof(CBox), "cells"));
+        k_cell_boxes<<<(unsigned)cdiv(ncell, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy,
+                                                                 ncz, cellb.as<CBox>());
+        VS_TRY(check_launch("k_cell_boxes"));
       }
-      VS_TRY(scan({co[0], co[1], co[2]}));
-      int64_t t[3];
-      VS_TRY(totals({co[0], co[1], co[2]}, t));
-      VS_TRY(cslab.ensure((t[0] + t[1] + t[2] + 3) * sizeof(CBox), "cell slabs"));
+      const int64_t t0 = tot[A_C0], t1 = tot[A_C1], t2 = tot[A_C2];
+      VS_TRY(cslab.ensure((t0 + t1 + t2 + 3) * sizeof(CBox), "cell slabs"));
       CBox* cbase = cslab.as<CBox>();
-      CBox* cs3[3] = {cbase, cbase + t[0] + 1, cbase + t[0] + t[1] + 2};
+      CBox* cs3[3] = {cbase, cbase + t0 + 1, cbase + t0 + t1 + 2};
+      const int64_t ta[3] = {t0, t1, t2};
       for (int a = 0; a < 3; ++a) {
-        k_cell_slabs<<<SPAN_BLOCKS, 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
-                                                  co[a], co[a] + n, cs3[a]);
+        k_cell_slabs<<<grid_for(ta[a], 8), 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
+                                                         ta[a], cs3[a]);
         VS_TRY(check_launch("k_cell_slabs"));
         B.cslab[a] = cs3[a];
-        B.coff[a] = co[a];
+        B.coff[a] = L.off[A_C0 + a];
       }
-      k_decide<<<gw, 128, 0, st>>>(L, P, nullptr, nullptr, nullptr, nullptr, nullptr, B,
-                                   dec.as<KdDecision>());
+      k_decide<<<gw, 128, 0, st>>>(L, P, nullptr, nullptr, nullptr, nullptr, B,
+                                   dec.as<KdDecision>(), cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
       // exact shrink for the binned leaves (kdtree.py:474)
-      k_need<<<gn, 128, 0, st>>>(L, P, 1, dec.as<KdDecision>());
-      VS_TRY(check_launch("k_need"));
-      VS_TRY(scan({L.off_x, L.off_pxz}));
-      int64_t t2[2];
-      VS_TRY(totals({L.off_x, L.off_pxz}, t2));
-      if (t2[0] > 0) {
-        VS_TRY(spx.ensure((t2[0] + 1) * sizeof(Span), "span_x"));
-        VS_TRY(pxz.ensure((t2[1] + 1) * 4, "pxz"));
-        k_spans_x<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_x + n, spx.as<Span>(),
-                                               pxz.as<uint32_t>());
-        VS_TRY(check_launch("k_spans_x"));
-        k_leaf_shrink<<<gw, 128, 0, st>>>(L, spx.as<Span>(), dec.as<KdDecision>());
-        VS_TRY(check_launch("k_leaf_shrink"));
-      }
+      k_leaf_shrink<<<(unsigned)n, 128, 0, st>>>(bits, ny, nzw, L, dec.as<KdDecision>());
+      VS_TRY(check_launch("k_leaf_shrink"));
     }
-    // next level
-    k_child_counts<<<gn, 128, 0, st>>>(dec.as<KdDecision>(), (int)n, cnt.as<int64_t>());
-    VS_TRY(check_launch("k_child_counts"));
-    VS_TRY(scan({cnt.as<int64_t>()}));
-    int64_t next_n;
-    VS_TRY(d2h(&next_n, cnt.as<int64_t>() + n, sizeof next_n, st));
-    // grow the record array (copy-preserving)
-    if ((size_t)(base + n) * sizeof(NodeRec) > rec.cap) {
+    // next level: child offsets, rows of this level, next boxes and their work sizes
+    {
+      ScanSet S;
+      S.k = 1;
+      S.a[0] = cnt.as<int64_t>();
+      S.totals[0] = dh + KA + 1;
+      k_multi_scan<<<1, 1024, 0, st>>>(S, nullptr, n);
+      VS_TRY(check_launch("k_multi_scan"));
+    }
+    if ((size_t)(base + n) * sizeof(NodeRec) > rec.cap) {  // grow the records (copy-preserving)
       DBuf bigger;
       bigger.st = st;
       VS_TRY(bigger.ensure(std::max<size_t>((base + n) * sizeof(NodeRec) * 2, 4096), "records"));
@@ -1058,14 +1216,21 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
       std::swap(rec.p, bigger.p);
       std::swap(rec.cap, bigger.cap);
     }
-    VS_TRY(nxt.ensure(std::max<int64_t>(next_n, 1) * sizeof(Box), "next level"));
-    k_emit_level<<<gn, 128, 0, st>>>(dec.as<KdDecision>(), cnt.as<int64_t>(), (int)n, base,
-                                     base + n, level, rec.as<NodeRec>(), nxt.as<Box>());
+    VS_TRY(nxt.ensure(2 * n * sizeof(Box), "next level"));
+    VS_TRY(arrays(2 * n));  // this level's arrays are dead from here on
+    k_emit_level<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(dec.as<KdDecision>(), cnt.as<int64_t>(),
+                                                         (int)n, base, base + n, level,
+                                                         rec.as<NodeRec>(), nxt.as<Box>(),
+                                                         prep_ctx());
     VS_TRY(check_launch("k_emit_level"));
+    VS_TRY(scan_level(dh + KA + 1));
+    VS_CUDA(cudaMemcpyAsync(dh, dh + KA + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, st),
+            "count");
+    VS_TRY(d2h(hh, dh, sizeof hh, st));
     std::swap(cur.p, nxt.p);
     std::swap(cur.cap, nxt.cap);
     base += n;
-    n = next_n;
+    n = hh[0];
     ++level;
   }
   const int64_t total = base;
@@ -1095,14 +1260,13 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
   VS_TRY(R->plane.ensure(m * 4, "plane"));
   VS_TRY(R->left.ensure(m * 4, "left"));
   VS_TRY(R->right.ensure(m * 4, "right"));
-  VS_TRY(tot.ensure(sizeof(int) * 2, "height"));
-  VS_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(int), st), "height init");
+  VS_CUDA(cudaMemsetAsync(dbb, 0, sizeof(int), st), "height init");
   k_scatter_rows<<<(unsigned)cdiv(total, 128), 128, 0, st>>>(
       rec.as<NodeRec>(), total, sizes.as<int>(), pre.as<int>(), R->lo.as<int32_t>(),
       R->hi.as<int32_t>(), R->axis.as<int8_t>(), R->plane.as<int32_t>(), R->left.as<int32_t>(),
-      R->right.as<int32_t>(), tot.as<int>());
+      R->right.as<int32_t>(), dbb);
   VS_TRY(check_launch("k_scatter_rows"));
-  VS_TRY(d2h(&R->height, tot.p, sizeof(int), st));
+  VS_TRY(d2h(&R->height, dbb, sizeof(int), st));
   R->root = 0;
   return 0;
 }
@@ -1258,31 +1422,32 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
   const int nc[3] = {ncx, ncy, ncz};
   DBuf lev, spx, spy, spz, pxz, pyz, scr, cellb, cslab, res;
   for (DBuf* d : {&lev, &spx, &spy, &spz, &pxz, &pyz, &scr, &cellb, &cslab, &res}) d->st = st;
-  // one-node level: box, need, 12 offset arrays of 2 entries
+  // one-node level: box + KA offset arrays of 2 entries
   struct Host {
     Box box;
-    int need;
-    int pad;
-    int64_t off[12][2];
+    int64_t off[KA][2];
   } h;
   memset(&h, 0, sizeof h);
   h.box = b;
-  h.need = 1;
-  const int64_t sizes[6] = {ext[0], ext[1], ext[2], (int64_t)ext[0] * wz, (int64_t)ext[1] * wz, wz};
-  for (int k = 0; k < 6; ++k) h.off[k][1] = sizes[k];
+  const int64_t sizes[A_IY + 1] = {ext[0], ext[1], ext[2], (int64_t)ext[0] * wz,
+                                   (int64_t)ext[1] * wz, wz,
+                                   std::max(ext[0], std::max(ext[1], ext[2])),
+                                   (int64_t)ext[0] * cdiv(ext[1], SPAN_CHUNK),
+                                   (int64_t)ext[1] * cdiv(ext[0], SPAN_CHUNK)};
+  for (int k = 0; k <= A_IY; ++k) h.off[k][1] = sizes[k];
   int64_t csz[3];
   for (int a = 0; a < 3; ++a) {
     int c0 = std::max(b.lo[a] / cs, 0), c1 = std::min((b.hi[a] - 1) / cs, nc[a] - 1);
     csz[a] = std::max(c1 - c0 + 1, 0);
-    h.off[7 + a][1] = csz[a];
+    h.off[A_C0 + a][1] = csz[a];
   }
   VS_TRY(lev.ensure(sizeof h, "level"));
   VS_CUDA(cudaMemcpyAsync(lev.p, &h, sizeof h, cudaMemcpyHostToDevice, st), "level copy");
   Host* d = lev.as<Host>();
   KdLevel L;
-  L.n = 1; L.box = &d->box; L.need = &d->need;
-  L.off_x = d->off[0]; L.off_y = d->off[1]; L.off_z = d->off[2];
-  L.off_pxz = d->off[3]; L.off_pyz = d->off[4]; L.off_zw = d->off[5];
+  L.n = 1;
+  L.box = &d->box;
+  for (int k = 0; k < KA; ++k) L.off[k] = d->off[k];
   KdParams P;
   P.deep = 1; P.mls = -1; P.binned = binned; P.bins = bins; P.cs = cs; P.root_vol = 0;
   BinnedCtx B;
@@ -1294,14 +1459,19 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
     VS_TRY(spx.ensure((ext[0] + 1) * sizeof(Span), "span_x"));
     VS_TRY(spy.ensure((ext[1] + 1) * sizeof(Span), "span_y"));
     VS_TRY(spz.ensure((ext[2] + 32) * sizeof(Span), "span_z"));
-    VS_TRY(pxz.ensure((sizes[3] + 1) * 4, "pxz"));
-    VS_TRY(pyz.ensure((sizes[4] + 1) * 4, "pyz"));
-    k_spans_x<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_x + 1, spx.as<Span>(),
-                                           pxz.as<uint32_t>());
-    k_spans_y<<<SPAN_BLOCKS, 256, 0, st>>>(bits, ny, nzw, L, L.off_y + 1, spy.as<Span>(),
-                                           pyz.as<uint32_t>());
-    k_spans_z<<<SPAN_BLOCKS, 128, 0, st>>>(L, L.off_zw + 1, pxz.as<uint32_t>(), pyz.as<uint32_t>(),
-                                           spz.as<Span>());
+    VS_TRY(pxz.ensure((sizes[A_PXZ] + 1) * 4, "pxz"));
+    VS_TRY(pyz.ensure((sizes[A_PYZ] + 1) * 4, "pyz"));
+    const int64_t mx = std::max(std::max(sizes[A_X], sizes[A_Y]),
+                                std::max(sizes[A_PXZ], sizes[A_PYZ]));
+    k_span_init<<<grid_for(mx, 256), 256, 0, st>>>(spx.as<Span>(), sizes[A_X], spy.as<Span>(),
+                                                   sizes[A_Y], pxz.as<uint32_t>(), sizes[A_PXZ],
+                                                   pyz.as<uint32_t>(), sizes[A_PYZ]);
+    k_spans_rows<0><<<grid_for(sizes[A_IX], 8), 256, 0, st>>>(bits, ny, nzw, L, sizes[A_IX],
+                                                              spx.as<Span>(), pxz.as<uint32_t>());
+    k_spans_rows<1><<<grid_for(sizes[A_IY], 8), 256, 0, st>>>(bits, ny, nzw, L, sizes[A_IY],
+                                                              spy.as<Span>(), pyz.as<uint32_t>());
+    k_spans_z<<<grid_for(sizes[A_ZW], 8), 256, 0, st>>>(L, sizes[A_ZW], pxz.as<uint32_t>(),
+                                                        pyz.as<uint32_t>(), spz.as<Span>());
     VS_TRY(check_launch("spans"));
   } else {
     const int64_t ncell = (int64_t)ncx * ncy * ncz;
@@ -1312,10 +1482,10 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
     CBox* cs3[3] = {cslab.as<CBox>(), cslab.as<CBox>() + csz[0] + 1,
                     cslab.as<CBox>() + csz[0] + csz[1] + 2};
     for (int a = 0; a < 3; ++a) {
-      k_cell_slabs<<<SPAN_BLOCKS, 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
-                                                d->off[7 + a], d->off[7 + a] + 1, cs3[a]);
+      k_cell_slabs<<<grid_for(csz[a], 8), 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
+                                                        csz[a], cs3[a]);
       B.cslab[a] = cs3[a];
-      B.coff[a] = d->off[7 + a];
+      B.coff[a] = d->off[A_C0 + a];
     }
     VS_TRY(check_launch("cell slabs"));
   }
