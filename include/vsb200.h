@@ -77,6 +77,12 @@ int vs_classify_summary(const uint8_t* bins, int nx, int ny, int nz, const vs_tf
 int vs_classify_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
                      uint32_t* bits, unsigned long long* count_opt, vs_stream_t stream);
 
+/* classify + _dilate26 fused into one pass over the volume (volume.py:307-319 with
+ * dilate=True): packed dilated bits + optional visible count of the UNDILATED classification.
+ * Needs nz % 32 == 0, nz <= 1024 and a 16-byte aligned volume (VS_EINVAL otherwise). */
+int vs_classify_dilate_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
+                            uint32_t* bits, unsigned long long* count_opt, vs_stream_t stream);
+
 /* _dilate26: 3x3x3 box OR, neighbourhood clipped at the borders.  in != out. */
 int vs_dilate_bits(const uint32_t* in, int nx, int ny, int nz, uint32_t* out,
                    vs_stream_t stream);

@@ -26,6 +26,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_quantize_f32": (i32, [P, i64, P, P]),
     "vs_classify_summary": (i32, [P, i32, i32, i32, P, P, P, P, P]),
     "vs_classify_bits": (i32, [P, i32, i32, i32, P, P, P, P]),
+    "vs_classify_dilate_bits": (i32, [P, i32, i32, i32, P, P, P, P]),
     "vs_dilate_bits": (i32, [P, i32, i32, i32, P, P]),
     "vs_pack_bits": (i32, [P, i32, i32, i32, P, P]),
     "vs_unpack_bits": (i32, [P, i32, i32, i32, P, P]),

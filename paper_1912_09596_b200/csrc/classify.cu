@@ -308,6 +308,141 @@ __global__ void k_classify_bits(const uint8_t* __restrict__ vol, int nx, int ny,
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// k_classify_pack<V, DIL>: classification to packed bits for rows of whole 32-voxel words
+// (nz % 32 == 0, nz <= 1024), optionally fused with _dilate26 (volume.py:289-304) so the
+// dilated bit volume costs one pass over the u8 volume.  Block = CP_TY output rows (+2 halo
+// rows when dilating) x one CP_XC run of x slabs; warp = one row, lane = one 32-voxel word
+// (two 16-byte loads, SWAR visibility).  Per x step: classify the next slab's rows, z-dilate
+// with lane shuffles, y-dilate through shared memory, x-dilate with a 3-slab register ring.
+// The next slab's loads are issued before the current slab is processed.
+// ---------------------------------------------------------------------------------------
+constexpr int CP_TY = 30, CP_XC = 32;
+
+template <int V>
+__device__ __forceinline__ uint32_t classify_word(const VisEval& ve, const uint4& a,
+                                                  const uint4& b) {
+  uint32_t g[8] = {ve.eval<V>(a.x), ve.eval<V>(a.y), ve.eval<V>(a.z), ve.eval<V>(a.w),
+                   ve.eval<V>(b.x), ve.eval<V>(b.y), ve.eval<V>(b.z), ve.eval<V>(b.w)};
+  uint32_t w = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w |= compress4(g[k] & HB) << (4 * k);
+  return w;
+}
+
+template <int V, bool DIL>
+__device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* zs,
+                                                   uint32_t* red, const uint8_t* __restrict__ vol,
+                                                   int nx, int ny, int nz,
+                                                   uint32_t* __restrict__ out,
+                                                   unsigned long long* __restrict__ count) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nzw = nz >> 5;
+  const int ty = DIL ? CP_TY : (int)(blockDim.x >> 5);
+  const int y0 = blockIdx.x * ty, x0 = blockIdx.y * CP_XC;
+  const int xe = min(nx, x0 + CP_XC);
+  const int y = y0 + warp - (DIL ? 1 : 0);
+  const bool rowok = y >= 0 && y < ny && lane < nzw;
+  const bool outrow = rowok && (!DIL || (warp >= 1 && warp <= CP_TY));
+  const uint8_t* rowp = vol + (int64_t)y * nz + lane * 32;
+  const int64_t xstride = (int64_t)ny * nz;
+  auto load = [&](int x, uint4& a, uint4& b) {
+    if (rowok && x >= 0 && x < nx) {
+      const uint4* q = reinterpret_cast<const uint4*>(rowp + (int64_t)x * xstride);
+      a = __ldcs(q);
+      b = __ldcs(q + 1);
+    }
+  };
+  uint32_t cnt = 0;
+  uint4 a = make_uint4(0, 0, 0, 0), b = a, na = a, nb = a;
+  if (!DIL) {
+    load(x0, a, b);
+    for (int x = x0; x < xe; ++x) {
+      if (x + 1 < xe) load(x + 1, na, nb);
+      if (outrow) {
+        const uint32_t w = classify_word<V>(ve, a, b);
+        out[((int64_t)x * ny + y) * nzw + lane] = w;
+        cnt += __popc(w);
+      }
+      a = na;
+      b = nb;
+    }
+  } else {
+    // y/z-dilated words of slabs x-1, x (ring), output row = warp
+    uint32_t prev = 0, cur = 0;
+    load(x0 - 1, a, b);
+    for (int xs = x0 - 1; xs <= xe; ++xs) {
+      // slab xs: classify, count, z-dilate, y-dilate
+      if (xs + 1 <= xe) {
+        na = make_uint4(0, 0, 0, 0);
+        nb = na;
+        load(xs + 1, na, nb);
+      }
+      uint32_t w = 0;
+      if (rowok && xs >= 0 && xs < nx) w = classify_word<V>(ve, a, b);
+      if (outrow && xs >= x0 && xs < xe) cnt += __popc(w);
+      const uint32_t up = __shfl_up_sync(0xffffffffu, w, 1);
+      const uint32_t dn = __shfl_down_sync(0xffffffffu, w, 1);
+      uint32_t zd = w | (w << 1) | (w >> 1);
+      if (lane > 0) zd |= up >> 31;
+      if (lane + 1 < nzw) zd |= dn << 31;
+      __syncthreads();
+      zs[warp * 32 + lane] = zd;
+      __syncthreads();
+      uint32_t yd = 0;
+      if (warp >= 1 && warp <= CP_TY) yd = zs[(warp - 1) * 32 + lane] | zd | zs[(warp + 1) * 32 + lane];
+      // slab xs - 1 is complete: prev (xs-2) | cur (xs-1) | yd (xs)
+      if (outrow && xs - 1 >= x0) out[((int64_t)(xs - 1) * ny + y) * nzw + lane] = prev | cur | yd;
+      prev = cur;
+      cur = yd;
+      a = na;
+      b = nb;
+    }
+  }
+  if (count) {
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) red[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+      if (s) atomicAdd(count, s);
+    }
+  }
+}
+
+#define VS_CP_ARGS ve, zs, red, vol, nx, ny, nz, out, count
+
+template <bool DIL>
+__global__ void __launch_bounds__(1024) k_classify_pack(const uint8_t* __restrict__ vol, int nx,
+                                                        int ny, int nz,
+                                                        const vs_tf_params* __restrict__ tf,
+                                                        uint32_t* __restrict__ out,
+                                                        unsigned long long* __restrict__ count) {
+  __shared__ uint8_t tab[256];
+  __shared__ uint32_t zs[(CP_TY + 2) * 32];
+  __shared__ uint32_t red[32];
+  VisEval ve;
+  const int v = load_vis(ve, tf, tab);
+  __syncthreads();
+  switch (v) {
+    case 1: classify_pack_body<1, DIL>(VS_CP_ARGS); break;
+    case 2: classify_pack_body<2, DIL>(VS_CP_ARGS); break;
+    case 5: classify_pack_body<5, DIL>(VS_CP_ARGS); break;
+    case 6: classify_pack_body<6, DIL>(VS_CP_ARGS); break;
+    case 8: classify_pack_body<8, DIL>(VS_CP_ARGS); break;
+    case 9: classify_pack_body<9, DIL>(VS_CP_ARGS); break;
+    case 10: classify_pack_body<10, DIL>(VS_CP_ARGS); break;
+    case 11: classify_pack_body<11, DIL>(VS_CP_ARGS); break;
+    case 12: classify_pack_body<12, DIL>(VS_CP_ARGS); break;
+    case 13: classify_pack_body<13, DIL>(VS_CP_ARGS); break;
+    case 14: classify_pack_body<14, DIL>(VS_CP_ARGS); break;
+    case 15: classify_pack_body<15, DIL>(VS_CP_ARGS); break;
+    case V_CONST: classify_pack_body<V_CONST, DIL>(VS_CP_ARGS); break;
+    default: classify_pack_body<V_TABLE, DIL>(VS_CP_ARGS); break;
+  }
+}
+
 __global__ void k_quantize(const float* __restrict__ f, int64_t n, uint8_t* __restrict__ out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -624,10 +759,26 @@ int vs_classify_summary(const uint8_t* bins, int nx, int ny, int nz, const vs_tf
 int vs_classify_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
                      uint32_t* bits, unsigned long long* count, vs_stream_t st) {
   if (!bins || !tf || !bits || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_classify_bits");
+  if (nz % 32 == 0 && nz <= 1024 && (reinterpret_cast<uintptr_t>(bins) & 15) == 0) {
+    dim3 grid((unsigned)cdiv(ny, 32), (unsigned)cdiv(nx, CP_XC));
+    k_classify_pack<false><<<grid, 1024, 0, S(st)>>>(bins, nx, ny, nz, tf, bits, count);
+    return check_launch("k_classify_pack");
+  }
   const int64_t nwords = (int64_t)nx * ny * nzw_of(nz);
   k_classify_bits<<<(unsigned)cdiv(nwords, 256), 256, 0, S(st)>>>(bins, nx, ny, nz, tf, bits,
                                                                     count);
   return check_launch("k_classify_bits");
+}
+
+int vs_classify_dilate_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
+                            uint32_t* bits, unsigned long long* count, vs_stream_t st) {
+  if (!bins || !tf || !bits || nx < 1 || ny < 1 || nz < 1)
+    return fail_arg("vs_classify_dilate_bits");
+  if (nz % 32 != 0 || nz > 1024 || (reinterpret_cast<uintptr_t>(bins) & 15) != 0)
+    return fail_arg("vs_classify_dilate_bits: needs nz % 32 == 0, nz <= 1024, 16-byte aligned");
+  dim3 grid((unsigned)cdiv(ny, CP_TY), (unsigned)cdiv(nx, CP_XC));
+  k_classify_pack<true><<<grid, 32 * (CP_TY + 2), 0, S(st)>>>(bins, nx, ny, nz, tf, bits, count);
+  return check_launch("k_classify_pack<dilate>");
 }
 
 int vs_dilate_bits(const uint32_t* in, int nx, int ny, int nz, uint32_t* out, vs_stream_t st) {

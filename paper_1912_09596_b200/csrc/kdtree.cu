@@ -58,11 +58,18 @@ enum {
   A_SCR,     // suffix-box scratch: max extent
   A_IX,      // x-pass work items: ex * chunks(ey)
   A_IY,      // y-pass work items: ey * chunks(ex)
+  A_IZ,      // z-pass work items: wz * chunks of 32 projection rows
   A_C0,      // binned: cell slabs along x, y, z
   A_C1,
   A_C2,
+  A_IC0,     // binned: cell-slab work items (slab x chunks of CELL_CHUNK cells), per axis
+  A_IC1,
+  A_IC2,
   KA
 };
+
+// Cells one cell-slab work item reduces (chunks of a big slab merge with atomics).
+constexpr int CELL_CHUNK = 1024;
 
 // Rows one x/y-pass work item covers (a node's slab is split into chunks of this many rows so
 // the top levels of a big volume still spread over every SM; chunks merge with atomics).
@@ -189,38 +196,37 @@ __global__ void __launch_bounds__(256) k_spans_rows(const uint32_t* __restrict__
 
 // Empty spans / projections for the chunked merge.
 __global__ void k_span_init(Span* __restrict__ sx, int64_t nx_, Span* __restrict__ sy, int64_t ny_,
-                            uint32_t* __restrict__ px, int64_t npx, uint32_t* __restrict__ py,
-                            int64_t npy) {
+                            Span* __restrict__ sz, int64_t nz_, uint32_t* __restrict__ px,
+                            int64_t npx, uint32_t* __restrict__ py, int64_t npy) {
   const Span e{KD_FAR, -1, KD_FAR, -1};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-       j < max(max(nx_, ny_), max(npx, npy)); j += stride) {
+       j < max(max(max(nx_, ny_), nz_), max(npx, npy)); j += stride) {
     if (j < nx_) sx[j] = e;
     if (j < ny_) sy[j] = e;
+    if (j < nz_) sz[j] = e;
     if (j < npx) px[j] = 0;
     if (j < npy) py[j] = 0;
   }
 }
 
-// ---- z-slab spans from the two projections: warp per (node, z word) ------------------------
-// Lane k owns local z bit 32w + k.  Per 32 projection rows, one ballot per z bit present in
-// the chunk gives every bit's first / last row.
-__device__ __forceinline__ void proj_minmax(const uint32_t* __restrict__ p, int wz, int e,
-                                            int lane, int& mn, int& mx) {
+// ---- z-slab spans from the two projections: warp per (node, z word, 32 projection rows) ----
+// Lane k owns local z bit 32w + k; one ballot per z bit present in the chunk gives the bit's
+// first / last row.  Single-chunk nodes store, chunked nodes merge with atomics.
+__device__ __forceinline__ void proj_chunk(const uint32_t* __restrict__ p, int wz, int e,
+                                           int base, int lane, int& mn, int& mx) {
   mn = KD_FAR;
   mx = -1;
-  for (int base = 0; base < e; base += 32) {
-    const int r = base + lane;
-    const uint32_t v = r < e ? p[(int64_t)r * wz] : 0u;
-    uint32_t cor = __reduce_or_sync(0xffffffffu, v);
-    while (cor) {
-      const int k = __ffs(cor) - 1;
-      cor &= cor - 1;
-      const uint32_t bal = __ballot_sync(0xffffffffu, (v >> k) & 1u);
-      if (lane == k) {
-        if (mn == KD_FAR) mn = base + __ffs(bal) - 1;
-        mx = base + 31 - __clz(bal);
-      }
+  const int r = base + lane;
+  const uint32_t v = r < e ? p[(int64_t)r * wz] : 0u;
+  uint32_t cor = __reduce_or_sync(0xffffffffu, v);
+  while (cor) {
+    const int k = __ffs(cor) - 1;
+    cor &= cor - 1;
+    const uint32_t bal = __ballot_sync(0xffffffffu, (v >> k) & 1u);
+    if (lane == k) {
+      mn = base + __ffs(bal) - 1;
+      mx = base + 31 - __clz(bal);
     }
   }
 }
@@ -233,16 +239,24 @@ __global__ void __launch_bounds__(256) k_spans_z(KdLevel L, int64_t items,
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
        it += (int64_t)gridDim.x * wpb) {
-    const int i = find_node(L.off[A_ZW], L.n, it);
+    const int i = find_node(L.off[A_IZ], L.n, it);
     const Box b = L.box[i];
-    const int w = (int)(it - L.off[A_ZW][i]);
     const int wz = wz_of(b);
     const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
+    const int nch = (max(ex, ey) + 31) >> 5;
+    const int local = (int)(it - L.off[A_IZ][i]);
+    const int w = local / nch, base = (local - w * nch) * 32;
     const int nzb = min(32, ez - 32 * w);
     Span sp;
-    proj_minmax(pxz + L.off[A_PXZ][i] + w, wz, ex, lane, sp.mn1, sp.mx1);
-    proj_minmax(pyz + L.off[A_PYZ][i] + w, wz, ey, lane, sp.mn2, sp.mx2);
-    if (lane < nzb) span_z[L.off[A_Z][i] + 32 * w + lane] = sp;
+    proj_chunk(pxz + L.off[A_PXZ][i] + w, wz, ex, base, lane, sp.mn1, sp.mx1);
+    proj_chunk(pyz + L.off[A_PYZ][i] + w, wz, ey, base, lane, sp.mn2, sp.mx2);
+    Span* dst = span_z + L.off[A_Z][i] + 32 * w + lane;
+    if (nch == 1) {
+      if (lane < nzb) *dst = sp;
+    } else if (lane < nzb) {
+      if (sp.mx1 >= 0) { atomicMin(&dst->mn1, sp.mn1); atomicMax(&dst->mx1, sp.mx1); }
+      if (sp.mx2 >= 0) { atomicMin(&dst->mn2, sp.mn2); atomicMax(&dst->mx2, sp.mx2); }
+    }
   }
 }
 
@@ -268,22 +282,6 @@ __device__ __forceinline__ bool halted(const KdParams& P, int64_t vol) {
   return P.deep ? vol <= 512 : vol * 10 <= P.root_vol;  // kdtree.py:421-424
 }
 
-// Warp scan helpers (inclusive min / max).
-__device__ __forceinline__ int wmin_incl(int v, int lane) {
-  for (int o = 1; o < 32; o <<= 1) {
-    int u = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v = min(v, u);
-  }
-  return v;
-}
-__device__ __forceinline__ int wmax_incl(int v, int lane) {
-  for (int o = 1; o < 32; o <<= 1) {
-    int u = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v = max(v, u);
-  }
-  return v;
-}
-
 // Row-order tight box (axis row, other1, other2) in local coordinates; empty if hi0 < 0.
 struct RBox {
   int lo0, lo1, lo2, hi0, hi1, hi2;
@@ -294,93 +292,117 @@ __device__ __forceinline__ int64_t rvol(const RBox& r) {
   return (int64_t)(r.hi0 - r.lo0 + 1) * (r.hi1 - r.lo1 + 1) * (r.hi2 - r.lo2 + 1);
 }
 
-// Sweep one axis: (first-minimum cut k in 1..e-1, its cost).  suf scratch holds e RBoxes.
-__device__ void sweep_axis(const Span* __restrict__ sp, int e, RBox* __restrict__ suf,
-                           int lane, int& best_k, int64_t& best_cost) {
-  // suffix pass (from the end): suf[s] = tight box of slabs [s, e)
-  RBox carry{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
-  for (int base = ((e - 1) / 32) * 32; base >= 0; base -= 32) {
-    const int s = base + (31 - lane);  // lane 0 handles the highest slab of the chunk
-    RBox r{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
-    if (s < e) {
-      const Span v = sp[s];
-      if (v.mx1 >= 0) r = RBox{s, v.mn1, v.mn2, s, v.mx1, v.mx2};
-    }
-    r.lo0 = min(wmin_incl(r.lo0, lane), carry.lo0);
-    r.lo1 = min(wmin_incl(r.lo1, lane), carry.lo1);
-    r.lo2 = min(wmin_incl(r.lo2, lane), carry.lo2);
-    r.hi0 = max(wmax_incl(r.hi0, lane), carry.hi0);
-    r.hi1 = max(wmax_incl(r.hi1, lane), carry.hi1);
-    r.hi2 = max(wmax_incl(r.hi2, lane), carry.hi2);
-    if (s < e) suf[s] = r;
-    carry.lo0 = __shfl_sync(0xffffffffu, r.lo0, 31);
-    carry.lo1 = __shfl_sync(0xffffffffu, r.lo1, 31);
-    carry.lo2 = __shfl_sync(0xffffffffu, r.lo2, 31);
-    carry.hi0 = __shfl_sync(0xffffffffu, r.hi0, 31);
-    carry.hi1 = __shfl_sync(0xffffffffu, r.hi1, 31);
-    carry.hi2 = __shfl_sync(0xffffffffu, r.hi2, 31);
-  }
-  __syncwarp();
-  // prefix pass with costs: cost(k) = vol(pre[k-1]) + vol(suf[k]), k = 1..e-1
-  RBox pc{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
-  int64_t bc = INT64_MAX;
-  int bk = 0;
-  for (int base = 0; base < e; base += 32) {
-    const int s = base + lane;
-    RBox r{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
-    if (s < e) {
-      const Span v = sp[s];
-      if (v.mx1 >= 0) r = RBox{s, v.mn1, v.mn2, s, v.mx1, v.mx2};
-    }
-    r.lo0 = min(wmin_incl(r.lo0, lane), pc.lo0);
-    r.lo1 = min(wmin_incl(r.lo1, lane), pc.lo1);
-    r.lo2 = min(wmin_incl(r.lo2, lane), pc.lo2);
-    r.hi0 = max(wmax_incl(r.hi0, lane), pc.hi0);
-    r.hi1 = max(wmax_incl(r.hi1, lane), pc.hi1);
-    r.hi2 = max(wmax_incl(r.hi2, lane), pc.hi2);
-    // candidate k = s + 1 uses pre[s] and suf[s + 1]
-    int64_t c = INT64_MAX;
-    if (s + 1 < e) c = rvol(r) + rvol(suf[s + 1]);
-    // first minimum across the chunk
-    int64_t cm = c;
-    int km = s + 1;
-    for (int o = 16; o; o >>= 1) {
-      int64_t c2 = __shfl_xor_sync(0xffffffffu, cm, o);
-      int k2 = __shfl_xor_sync(0xffffffffu, km, o);
-      if (c2 < cm || (c2 == cm && k2 < km)) { cm = c2; km = k2; }
-    }
-    if (cm < bc) { bc = cm; bk = km; }
-    pc.lo0 = __shfl_sync(0xffffffffu, r.lo0, 31);
-    pc.lo1 = __shfl_sync(0xffffffffu, r.lo1, 31);
-    pc.lo2 = __shfl_sync(0xffffffffu, r.lo2, 31);
-    pc.hi0 = __shfl_sync(0xffffffffu, r.hi0, 31);
-    pc.hi1 = __shfl_sync(0xffffffffu, r.hi1, 31);
-    pc.hi2 = __shfl_sync(0xffffffffu, r.hi2, 31);
-  }
-  best_k = bk;
-  best_cost = bc;
+__device__ __forceinline__ RBox rb_empty() { return RBox{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1}; }
+
+__device__ __forceinline__ RBox rb_join(const RBox& a, const RBox& b) {
+  return RBox{min(a.lo0, b.lo0), min(a.lo1, b.lo1), min(a.lo2, b.lo2),
+              max(a.hi0, b.hi0), max(a.hi1, b.hi1), max(a.hi2, b.hi2)};
 }
 
-// Tight row-order box of slabs [s0, s1) (warp reduction).
-__device__ RBox range_box(const Span* __restrict__ sp, int s0, int s1, int lane) {
-  RBox r{KD_FAR, KD_FAR, KD_FAR, -1, -1, -1};
-  for (int s = s0 + lane; s < s1; s += 32) {
-    const Span v = sp[s];
-    if (v.mx1 >= 0) {
-      r.lo0 = min(r.lo0, s); r.hi0 = max(r.hi0, s);
-      r.lo1 = min(r.lo1, v.mn1); r.hi1 = max(r.hi1, v.mx1);
-      r.lo2 = min(r.lo2, v.mn2); r.hi2 = max(r.hi2, v.mx2);
+__device__ __forceinline__ RBox slab_box(const Span* __restrict__ sp, int s) {
+  const Span v = sp[s];
+  return v.mx1 >= 0 ? RBox{s, v.mn1, v.mn2, s, v.mx1, v.mx2} : rb_empty();
+}
+
+__device__ __forceinline__ RBox rb_shfl(const RBox& r, int src_lane) {
+  return RBox{__shfl_sync(0xffffffffu, r.lo0, src_lane), __shfl_sync(0xffffffffu, r.lo1, src_lane),
+              __shfl_sync(0xffffffffu, r.lo2, src_lane), __shfl_sync(0xffffffffu, r.hi0, src_lane),
+              __shfl_sync(0xffffffffu, r.hi1, src_lane), __shfl_sync(0xffffffffu, r.hi2, src_lane)};
+}
+
+// Block of DT threads cooperates on one node (k_decide / k_best_plane).
+constexpr int DT = 128;
+constexpr int DW = DT / 32;
+
+struct DecideSmem {
+  RBox wbox[DW];
+  int64_t wcost[DW];
+  int wk[DW];
+};
+
+// Exclusive block scan (join) of one box per thread in thread order (rev = false) or in
+// reverse thread order (rev = true).
+__device__ RBox block_excl_scan(RBox x, bool rev, DecideSmem& sm) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  RBox inc = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    RBox u;
+    u.lo0 = rev ? __shfl_down_sync(0xffffffffu, inc.lo0, o) : __shfl_up_sync(0xffffffffu, inc.lo0, o);
+    u.lo1 = rev ? __shfl_down_sync(0xffffffffu, inc.lo1, o) : __shfl_up_sync(0xffffffffu, inc.lo1, o);
+    u.lo2 = rev ? __shfl_down_sync(0xffffffffu, inc.lo2, o) : __shfl_up_sync(0xffffffffu, inc.lo2, o);
+    u.hi0 = rev ? __shfl_down_sync(0xffffffffu, inc.hi0, o) : __shfl_up_sync(0xffffffffu, inc.hi0, o);
+    u.hi1 = rev ? __shfl_down_sync(0xffffffffu, inc.hi1, o) : __shfl_up_sync(0xffffffffu, inc.hi1, o);
+    u.hi2 = rev ? __shfl_down_sync(0xffffffffu, inc.hi2, o) : __shfl_up_sync(0xffffffffu, inc.hi2, o);
+    if (rev ? lane + o < 32 : lane >= o) inc = rb_join(inc, u);
+  }
+  // exclusive within the warp: the neighbour's inclusive value
+  RBox ex = rb_shfl(inc, rev ? min(lane + 1, 31) : max(lane - 1, 0));
+  if (rev ? lane == 31 : lane == 0) ex = rb_empty();
+  __syncthreads();
+  if (rev ? lane == 0 : lane == 31) sm.wbox[warp] = inc;  // warp total
+  __syncthreads();
+  for (int w = 0; w < DW; ++w)
+    if (rev ? w > warp : w < warp) ex = rb_join(ex, sm.wbox[w]);
+  return ex;
+}
+
+__device__ RBox block_reduce(RBox r, DecideSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) r = rb_join(r, rb_shfl(r, lane ^ o));
+  __syncthreads();
+  if (lane == 0) sm.wbox[warp] = r;
+  __syncthreads();
+  RBox t = rb_empty();
+  for (int w = 0; w < DW; ++w) t = rb_join(t, sm.wbox[w]);
+  return t;
+}
+
+// Tight row-order box of slabs [s0, s1).
+__device__ RBox range_box(const Span* __restrict__ sp, int s0, int s1, DecideSmem& sm) {
+  RBox r = rb_empty();
+  for (int s = s0 + (int)threadIdx.x; s < s1; s += DT) r = rb_join(r, slab_box(sp, s));
+  return block_reduce(r, sm);
+}
+
+// Sweep one axis (kdtree.py:156-188): first-minimum cut k in 1..e-1 and its cost
+// vol(tight [0,k)) + vol(tight [k,e)).  Thread t owns a contiguous run of slabs; suffix boxes
+// go to `suf` (e entries), prefix boxes stay in registers.
+__device__ void sweep_axis(const Span* __restrict__ sp, int e, RBox* __restrict__ suf,
+                           DecideSmem& sm, int& best_k, int64_t& best_cost) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int per = (e + DT - 1) / DT;
+  const int s0 = min(e, t * per), s1 = min(e, s0 + per);
+  RBox loc = rb_empty();
+  for (int s = s0; s < s1; ++s) loc = rb_join(loc, slab_box(sp, s));
+  RBox r = block_excl_scan(loc, true, sm);  // slabs after my run
+  for (int s = s1 - 1; s >= s0; --s) {
+    r = rb_join(r, slab_box(sp, s));
+    suf[s] = r;
+  }
+  RBox pre = block_excl_scan(loc, false, sm);  // slabs before my run (syncs: suf visible)
+  int64_t bc = INT64_MAX;
+  int bk = 0;
+  for (int s = s0; s < s1; ++s) {
+    pre = rb_join(pre, slab_box(sp, s));
+    if (s + 1 < e) {
+      const int64_t c = rvol(pre) + rvol(suf[s + 1]);
+      if (c < bc) { bc = c; bk = s + 1; }
     }
   }
   for (int o = 16; o; o >>= 1) {
-    r.lo0 = min(r.lo0, __shfl_xor_sync(0xffffffffu, r.lo0, o));
-    r.lo1 = min(r.lo1, __shfl_xor_sync(0xffffffffu, r.lo1, o));
-    r.lo2 = min(r.lo2, __shfl_xor_sync(0xffffffffu, r.lo2, o));
-    r.hi0 = max(r.hi0, __shfl_xor_sync(0xffffffffu, r.hi0, o));
-    r.hi1 = max(r.hi1, __shfl_xor_sync(0xffffffffu, r.hi1, o));
-    r.hi2 = max(r.hi2, __shfl_xor_sync(0xffffffffu, r.hi2, o));
+    const int64_t c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+    const int k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+    if (c2 < bc || (c2 == bc && k2 < bk)) { bc = c2; bk = k2; }
   }
-  return r;
+  __syncthreads();
+  if (lane == 0) { sm.wcost[warp] = bc; sm.wk[warp] = bk; }
+  __syncthreads();
+  bc = sm.wcost[0];
+  bk = sm.wk[0];
+  for (int w = 1; w < DW; ++w)
+    if (sm.wcost[w] < bc || (sm.wcost[w] == bc && sm.wk[w] < bk)) { bc = sm.wcost[w]; bk = sm.wk[w]; }
+  best_k = bk;
+  best_cost = bc;
 }
 
 // Row order -> xyz (kdtree.py:38 _ROWS_TO_XYZ): axis a rows are (a, o1, o2).
@@ -479,23 +501,28 @@ __device__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a, 
                            lane, out);
 }
 
-// ---- the decision kernel: one warp per node ------------------------------------------------
-__global__ void k_decide(KdLevel L, KdParams P, const Span* __restrict__ span_x,
-                         const Span* __restrict__ span_y, const Span* __restrict__ span_z,
-                         RBox* __restrict__ scratch, BinnedCtx B, KdDecision* __restrict__ out,
-                         int64_t* __restrict__ child_count) {
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// ---- the decision kernel: one block of DT threads per node ----------------------------------
+__global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
+                                               const Span* __restrict__ span_x,
+                                               const Span* __restrict__ span_y,
+                                               const Span* __restrict__ span_z,
+                                               RBox* __restrict__ scratch, BinnedCtx B,
+                                               KdDecision* __restrict__ out,
+                                               int64_t* __restrict__ child_count) {
+  __shared__ DecideSmem sm;
+  const int t = threadIdx.x;
+  const int i = blockIdx.x;
   if (i >= L.n) return;
   const Box b = L.box[i];
   int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
   const int64_t vol = box_vol(b);
-  const Span* sp[3] = {span_x + L.off[A_X][i], span_y + L.off[A_Y][i], span_z + L.off[A_Z][i]};
   KdDecision d;
   d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.leaf = b;
   bool split = false;
-  if (!halted(P, vol)) {
-    if (!P.binned) {
+  {
+    const Span* sp[3] = {span_x + L.off[A_X][i], span_y + L.off[A_Y][i],
+                         span_z + L.off[A_Z][i]};
+    if (!halted(P, vol)) {
       // _sweep_search + acceptance (kdtree.py:191-221, 431-439)
       int ba = -1, bk = 0;
       int64_t bc = 0;
@@ -503,79 +530,104 @@ __global__ void k_decide(KdLevel L, KdParams P, const Span* __restrict__ span_x,
         if (ext[a] < 2) continue;
         int k;
         int64_t c;
-        sweep_axis(sp[a], ext[a], scratch + L.off[A_SCR][i], lane, k, c);
+        sweep_axis(sp[a], ext[a], scratch + L.off[A_SCR][i], sm, k, c);
         if (ba >= 0 && c >= bc) continue;
         ba = a; bk = k; bc = c;
       }
       if (ba >= 0 && bc < vol) {
-        const RBox l = range_box(sp[ba], 0, bk, lane), r = range_box(sp[ba], bk, ext[ba], lane);
+        const RBox l = range_box(sp[ba], 0, bk, sm);
+        const RBox r = range_box(sp[ba], bk, ext[ba], sm);
         d.axis = ba; d.plane = b.lo[ba] + bk;
         if (l.hi0 >= 0) { d.left = to_global(b, ba, l); d.nchild |= 1; }
         if (r.hi0 >= 0) { d.right = to_global(b, ba, r); d.nchild |= 2; }
         split = true;
       }
-    } else {
-      // _binned_search (kdtree.py:353-368): first strict minimum over (axis, position)
-      int ba = -1, bp = 0;
-      int64_t bc = 0;
-      Box bl, br;
-      bool hl = false, hr = false;
-      for (int a = 0; a < 3; ++a) {
-        int pos[64];
-        const int np = snapped_positions(b.lo[a], b.hi[a], P.bins, P.cs, pos);
-        for (int q = 0; q < np; ++q) {
-          Box lreg = b, rreg = b, lb, rb;
-          lreg.hi[a] = pos[q];
-          rreg.lo[a] = pos[q];
-          const bool l = cells_reduce(B, i, b, a, lreg, P.cs, lane, lb);
-          const bool r = cells_reduce(B, i, b, a, rreg, P.cs, lane, rb);
-          const int64_t c = (l ? box_vol(lb) : 0) + (r ? box_vol(rb) : 0);
-          if (ba < 0 || c < bc) { ba = a; bp = pos[q]; bc = c; bl = lb; br = rb; hl = l; hr = r; }
-        }
-      }
-      if (ba >= 0 && bc < vol) {
-        d.axis = ba; d.plane = bp;
-        if (hl) { d.left = bl; d.nchild |= 1; }
-        if (hr) { d.right = br; d.nchild |= 2; }
+    }
+    if (!split && P.mls >= 0) {
+      // forced_split (kdtree.py:441-467): middle of the longest axis, exact children
+      int a = 0;
+      if (ext[1] > ext[a]) a = 1;
+      if (ext[2] > ext[a]) a = 2;
+      if (ext[a] > P.mls) {
+        const int k = ext[a] / 2;
+        const RBox l = range_box(sp[a], 0, k, sm);
+        const RBox r = range_box(sp[a], k, ext[a], sm);
+        d.axis = a; d.plane = b.lo[a] + k;
+        if (l.hi0 >= 0) { d.left = to_global(b, a, l); d.nchild |= 1; }
+        if (r.hi0 >= 0) { d.right = to_global(b, a, r); d.nchild |= 2; }
         split = true;
       }
     }
   }
+  if (t == 0) {
+    out[i] = d;
+    child_count[i] = __popc(d.nchild);
+  }
+}
+
+// ---- binned decisions: one warp per node (kdtree.py:353-368, 441-467) ----------------------
+__global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, BinnedCtx B,
+                                                       KdDecision* __restrict__ out,
+                                                       int64_t* __restrict__ child_count) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= L.n) return;
+  const Box b = L.box[i];
+  const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
+  const int64_t vol = box_vol(b);
+  KdDecision d;
+  d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.leaf = b;
+  bool split = false;
+  if (!halted(P, vol)) {
+    // first strict minimum over (axis, position)
+    int ba = -1, bp = 0;
+    int64_t bc = 0;
+    Box bl, br;
+    bool hl = false, hr = false;
+    for (int a = 0; a < 3; ++a) {
+      int pos[64];
+      const int np = snapped_positions(b.lo[a], b.hi[a], P.bins, P.cs, pos);
+      for (int q = 0; q < np; ++q) {
+        Box lreg = b, rreg = b, lb, rb;
+        lreg.hi[a] = pos[q];
+        rreg.lo[a] = pos[q];
+        const bool l = cells_reduce(B, i, b, a, lreg, P.cs, lane, lb);
+        const bool r = cells_reduce(B, i, b, a, rreg, P.cs, lane, rb);
+        const int64_t c = (l ? box_vol(lb) : 0) + (r ? box_vol(rb) : 0);
+        if (ba < 0 || c < bc) { ba = a; bp = pos[q]; bc = c; bl = lb; br = rb; hl = l; hr = r; }
+      }
+    }
+    if (ba >= 0 && bc < vol) {
+      d.axis = ba; d.plane = bp;
+      if (hl) { d.left = bl; d.nchild |= 1; }
+      if (hr) { d.right = br; d.nchild |= 2; }
+      split = true;
+    }
+  }
   if (!split && P.mls >= 0) {
-    // forced_split (kdtree.py:441-467)
+    // forced_split snapped to the interior raster
     int a = 0;
     if (ext[1] > ext[a]) a = 1;
     if (ext[2] > ext[a]) a = 2;
     if (ext[a] > P.mls) {
       const int lo = b.lo[a], hi = b.hi[a];
       int pos = lo + ext[a] / 2;
-      if (P.binned) {
-        const int cs = P.cs;
-        const int first = (lo / cs + 1) * cs, last = ((hi - 1) / cs) * cs;
-        if (first <= last) {
-          const int64_t snap =
-              (int64_t)floor(__dadd_rn(__ddiv_rn((double)pos, (double)cs), 0.5)) * cs;
-          {
-            int64_t q = snap < first ? (int64_t)first : snap;
-            pos = (int)(q > last ? (int64_t)last : q);
-          }
-        }
-        Box lreg = b, rreg = b, lb, rb;
-        lreg.hi[a] = pos;
-        rreg.lo[a] = pos;
-        const bool l = cells_reduce(B, i, b, a, lreg, cs, lane, lb);
-        const bool r = cells_reduce(B, i, b, a, rreg, cs, lane, rb);
-        d.axis = a; d.plane = pos;
-        if (l) { d.left = lb; d.nchild |= 1; }
-        if (r) { d.right = rb; d.nchild |= 2; }
-      } else {
-        const int k = pos - lo;
-        const RBox l = range_box(sp[a], 0, k, lane), r = range_box(sp[a], k, ext[a], lane);
-        d.axis = a; d.plane = pos;
-        if (l.hi0 >= 0) { d.left = to_global(b, a, l); d.nchild |= 1; }
-        if (r.hi0 >= 0) { d.right = to_global(b, a, r); d.nchild |= 2; }
+      const int cs = P.cs;
+      const int first = (lo / cs + 1) * cs, last = ((hi - 1) / cs) * cs;
+      if (first <= last) {
+        const int64_t snap =
+            (int64_t)floor(__dadd_rn(__ddiv_rn((double)pos, (double)cs), 0.5)) * cs;
+        const int64_t q = snap < first ? (int64_t)first : snap;
+        pos = (int)(q > last ? (int64_t)last : q);
       }
-      split = true;
+      Box lreg = b, rreg = b, lb, rb;
+      lreg.hi[a] = pos;
+      rreg.lo[a] = pos;
+      const bool l = cells_reduce(B, i, b, a, lreg, cs, lane, lb);
+      const bool r = cells_reduce(B, i, b, a, rreg, cs, lane, rb);
+      d.axis = a; d.plane = pos;
+      if (l) { d.left = lb; d.nchild |= 1; }
+      if (r) { d.right = rb; d.nchild |= 2; }
     }
   }
   if (lane == 0) {
@@ -615,26 +667,33 @@ __global__ void k_cell_boxes(const uint32_t* __restrict__ bits, int nx, int ny, 
   cells[i] = c;
 }
 
-// Cell-slab unions along axis A: warp per (node, cell slab c in the node's cell range).
-__global__ void k_cell_slabs(const CBox* __restrict__ cells, int ncx, int ncy, int ncz, int cs,
-                             int A, KdLevel L, int64_t items, CBox* __restrict__ out) {
+// Cell-slab unions along axis A: warp per (node, cell slab c in the node's cell range, chunk
+// of CELL_CHUNK cells of the slab); chunked slabs merge into initialised unions with atomics.
+__global__ void __launch_bounds__(256) k_cell_slabs(const CBox* __restrict__ cells, int ncx,
+                                                    int ncy, int ncz, int cs, int A, KdLevel L,
+                                                    int64_t items, CBox* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   const int nc[3] = {ncx, ncy, ncz};
   const int64_t* off = L.off[A_C0 + A];
+  const int64_t* ioff = L.off[A_IC0 + A];
   for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
        it += (int64_t)gridDim.x * wpb) {
-    const int i = find_node(off, L.n, it);
+    const int i = find_node(ioff, L.n, it);
     const Box b = L.box[i];
     int c0[3], c1[3];
     for (int k = 0; k < 3; ++k) node_cell_range(b, cs, nc, k, c0[k], c1[k]);
-    const int c = c0[A] + (int)(it - off[i]);
     int o1, o2;
     others(A, o1, o2);
     const int n1 = c1[o1] - c0[o1] + 1, n2 = c1[o2] - c0[o2] + 1;
+    const int nch = (n1 * n2 + CELL_CHUNK - 1) / CELL_CHUNK;
+    const int local = (int)(it - ioff[i]);
+    const int s = local / nch, ch = local - s * nch;
+    const int c = c0[A] + s;
+    const int q0 = ch * CELL_CHUNK, q1 = min(n1 * n2, q0 + CELL_CHUNK);
     CBox u;
     for (int k = 0; k < 3; ++k) { u.lo[k] = KD_FAR; u.hi[k] = -1; }
-    for (int q = lane; q < n1 * n2; q += 32) {
+    for (int q = q0 + lane; q < q1; q += 32) {
       int cc[3];
       cc[A] = c;
       cc[o1] = c0[o1] + q / n2;
@@ -648,8 +707,20 @@ __global__ void k_cell_slabs(const CBox* __restrict__ cells, int ncx, int ncy, i
         u.lo[k] = min(u.lo[k], __shfl_xor_sync(0xffffffffu, u.lo[k], o));
         u.hi[k] = max(u.hi[k], __shfl_xor_sync(0xffffffffu, u.hi[k], o));
       }
-    if (lane == 0) out[it] = u;
+    CBox* dst = out + off[i] + s;
+    if (nch == 1) {
+      if (lane == 0) *dst = u;
+    } else if (lane < 3 && u.lo[0] != KD_FAR) {
+      atomicMin(&dst->lo[lane], u.lo[lane]);
+      atomicMax(&dst->hi[lane], u.hi[lane]);
+    }
   }
+}
+
+__global__ void k_cbox_init(CBox* __restrict__ c, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
+    for (int k = 0; k < 3; ++k) { c[j].lo[k] = KD_FAR; c[j].hi[k] = -1; }
 }
 
 // ---- level bookkeeping ----------------------------------------------------------------------
@@ -684,12 +755,20 @@ __device__ __forceinline__ void prep_node(const PrepCtx& C, const Box& b, int64_
       v[A_SCR] = mx;
       v[A_IX] = (int64_t)ext[0] * ((ext[1] + SPAN_CHUNK - 1) / SPAN_CHUNK);
       v[A_IY] = (int64_t)ext[1] * ((ext[0] + SPAN_CHUNK - 1) / SPAN_CHUNK);
+      v[A_IZ] = (int64_t)wz * ((max(ext[0], ext[1]) + 31) >> 5);
     }
   } else {
+    int n[3];
     for (int a = 0; a < 3; ++a) {
       int c0, c1;
       node_cell_range(b, P.cs, C.nc, a, c0, c1);
-      v[A_C0 + a] = c1 - c0 + 1;
+      n[a] = c1 - c0 + 1;
+    }
+    for (int a = 0; a < 3; ++a) {
+      int o1, o2;
+      others(a, o1, o2);
+      v[A_C0 + a] = n[a];
+      v[A_IC0 + a] = (int64_t)n[a] * ((n[o1] * n[o2] + CELL_CHUNK - 1) / CELL_CHUNK);
     }
   }
   for (int k = 0; k < KA; ++k) C.arr[k][i] = v[k];
@@ -1094,7 +1173,7 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
     for (int k = 0; k < KA; ++k) C.arr[k] = arr(k);
     return C;
   };
-  const int nscan = binned ? 3 : 9;
+  const int nscan = binned ? 6 : A_IZ + 1;
   const int scan0 = binned ? A_C0 : 0;
   auto scan_level = [&](const int64_t* n_dev) -> int {
     ScanSet S;
@@ -1141,7 +1220,6 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
     VS_TRY(cnt.ensure((n + 1) * sizeof(int64_t), "counts"));
     BinnedCtx B;
     B.nc[0] = ncx; B.nc[1] = ncy; B.nc[2] = ncz;
-    const unsigned gw = (unsigned)cdiv(n, 4);  // warp per node, 128-thread blocks
     if (!binned) {
       VS_TRY(spx.ensure((tot[A_X] + 1) * sizeof(Span), "span_x"));
       VS_TRY(spy.ensure((tot[A_Y] + 1) * sizeof(Span), "span_y"));
@@ -1150,12 +1228,12 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
       VS_TRY(pyz.ensure((tot[A_PYZ] + 1) * 4, "pyz"));
       VS_TRY(scr.ensure((tot[A_SCR] + 1) * sizeof(RBox), "scratch"));
       if (tot[A_X] > 0) {
-        if (tot[A_IX] > tot[A_X] || tot[A_IY] > tot[A_Y]) {  // some slab is chunked
-          const int64_t mx = std::max(std::max(tot[A_X], tot[A_Y]),
+        if (tot[A_IX] > tot[A_X] || tot[A_IY] > tot[A_Y] || tot[A_IZ] > tot[A_ZW]) {  // chunked
+          const int64_t mx = std::max(std::max(std::max(tot[A_X], tot[A_Y]), tot[A_Z]),
                                       std::max(tot[A_PXZ], tot[A_PYZ]));
-          k_span_init<<<grid_for(mx, 256), 256, 0, st>>>(spx.as<Span>(), tot[A_X], spy.as<Span>(),
-                                                         tot[A_Y], pxz.as<uint32_t>(), tot[A_PXZ],
-                                                         pyz.as<uint32_t>(), tot[A_PYZ]);
+          k_span_init<<<grid_for(mx, 256), 256, 0, st>>>(
+              spx.as<Span>(), tot[A_X], spy.as<Span>(), tot[A_Y], spz.as<Span>(), tot[A_Z],
+              pxz.as<uint32_t>(), tot[A_PXZ], pyz.as<uint32_t>(), tot[A_PYZ]);
           VS_TRY(check_launch("k_span_init"));
         }
         k_spans_rows<0><<<grid_for(tot[A_IX], 8), 256, 0, st>>>(bits, ny, nzw, L, tot[A_IX],
@@ -1164,11 +1242,11 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
         k_spans_rows<1><<<grid_for(tot[A_IY], 8), 256, 0, st>>>(bits, ny, nzw, L, tot[A_IY],
                                                                 spy.as<Span>(), pyz.as<uint32_t>());
         VS_TRY(check_launch("k_spans_rows<y>"));
-        k_spans_z<<<grid_for(tot[A_ZW], 8), 256, 0, st>>>(L, tot[A_ZW], pxz.as<uint32_t>(),
+        k_spans_z<<<grid_for(tot[A_IZ], 8), 256, 0, st>>>(L, tot[A_IZ], pxz.as<uint32_t>(),
                                                           pyz.as<uint32_t>(), spz.as<Span>());
         VS_TRY(check_launch("k_spans_z"));
       }
-      k_decide<<<gw, 128, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(), spz.as<Span>(),
+      k_decide<<<(unsigned)n, DT, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(), spz.as<Span>(),
                                    scr.as<RBox>(), B, dec.as<KdDecision>(), cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
     } else {
@@ -1183,16 +1261,20 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
       VS_TRY(cslab.ensure((t0 + t1 + t2 + 3) * sizeof(CBox), "cell slabs"));
       CBox* cbase = cslab.as<CBox>();
       CBox* cs3[3] = {cbase, cbase + t0 + 1, cbase + t0 + t1 + 2};
-      const int64_t ta[3] = {t0, t1, t2};
+      if (tot[A_IC0] > t0 || tot[A_IC1] > t1 || tot[A_IC2] > t2) {  // some slab is chunked
+        k_cbox_init<<<grid_for(t0 + t1 + t2 + 3, 256), 256, 0, st>>>(cbase, t0 + t1 + t2 + 3);
+        VS_TRY(check_launch("k_cbox_init"));
+      }
       for (int a = 0; a < 3; ++a) {
-        k_cell_slabs<<<grid_for(ta[a], 8), 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
-                                                         ta[a], cs3[a]);
+        const int64_t items = tot[A_IC0 + a];
+        k_cell_slabs<<<grid_for(items, 8), 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
+                                                         items, cs3[a]);
         VS_TRY(check_launch("k_cell_slabs"));
         B.cslab[a] = cs3[a];
         B.coff[a] = L.off[A_C0 + a];
       }
-      k_decide<<<gw, 128, 0, st>>>(L, P, nullptr, nullptr, nullptr, nullptr, B,
-                                   dec.as<KdDecision>(), cnt.as<int64_t>());
+      k_decide_binned<<<(unsigned)cdiv(n, 4), 128, 0, st>>>(L, P, B, dec.as<KdDecision>(),
+                                                            cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
       // exact shrink for the binned leaves (kdtree.py:474)
       k_leaf_shrink<<<(unsigned)n, 128, 0, st>>>(bits, ny, nzw, L, dec.as<KdDecision>());
@@ -1304,17 +1386,20 @@ void vs_kd_result_free(void* handle) { delete static_cast<KdResultImpl*>(handle)
 //      kdtree.py:371-381): the level machinery on a one-node level ----------------------------
 namespace vs {
 
-__global__ void k_best_plane(KdLevel L, KdParams P, const Span* __restrict__ span_x,
-                             const Span* __restrict__ span_y, const Span* __restrict__ span_z,
-                             RBox* __restrict__ scratch, BinnedCtx B, long long* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x >= 32) return;
+__global__ void __launch_bounds__(DT) k_best_plane(KdLevel L, KdParams P,
+                                                   const Span* __restrict__ span_x,
+                                                   const Span* __restrict__ span_y,
+                                                   const Span* __restrict__ span_z,
+                                                   RBox* __restrict__ scratch, BinnedCtx B,
+                                                   long long* __restrict__ out) {
+  __shared__ DecideSmem sm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Box b = L.box[0];
   const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
   long long found = 0, axis = -1, pos = 0, cost = 0;
   if (!P.binned) {
     const Span* sp[3] = {span_x, span_y, span_z};
-    const RBox t = range_box(span_x, 0, ext[0], lane);
+    const RBox t = range_box(span_x, 0, ext[0], sm);
     if (t.hi0 >= 0) {
       const int64_t tv = rvol(t);  // _region_tight_volume
       int ba = -1, bk = 0;
@@ -1323,13 +1408,13 @@ __global__ void k_best_plane(KdLevel L, KdParams P, const Span* __restrict__ spa
         if (ext[a] < 2) continue;
         int k;
         int64_t c;
-        sweep_axis(sp[a], ext[a], scratch, lane, k, c);
+        sweep_axis(sp[a], ext[a], scratch, sm, k, c);
         if (ba >= 0 && c >= bc) continue;
         ba = a; bk = k; bc = c;
       }
       if (ba >= 0 && bc < tv) { found = 1; axis = ba; pos = b.lo[ba] + bk; cost = bc; }
     }
-  } else {
+  } else if (warp == 0) {
     Box target;
     if (cells_reduce(B, 0, b, 0, b, P.cs, lane, target)) {
       int ba = -1, bp = 0;
@@ -1350,7 +1435,7 @@ __global__ void k_best_plane(KdLevel L, KdParams P, const Span* __restrict__ spa
       if (ba >= 0 && bc < box_vol(target)) { found = 1; axis = ba; pos = bp; cost = bc; }
     }
   }
-  if (lane == 0) { out[0] = found; out[1] = axis; out[2] = pos; out[3] = cost; }
+  if (threadIdx.x == 0) { out[0] = found; out[1] = axis; out[2] = pos; out[3] = cost; }
 }
 
 // precompute_cell_boxes layout (kdtree.py:285-320): C-order lo/hi with the reference's
@@ -1429,17 +1514,23 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
   } h;
   memset(&h, 0, sizeof h);
   h.box = b;
-  const int64_t sizes[A_IY + 1] = {ext[0], ext[1], ext[2], (int64_t)ext[0] * wz,
+  const int64_t sizes[A_IZ + 1] = {ext[0], ext[1], ext[2], (int64_t)ext[0] * wz,
                                    (int64_t)ext[1] * wz, wz,
                                    std::max(ext[0], std::max(ext[1], ext[2])),
                                    (int64_t)ext[0] * cdiv(ext[1], SPAN_CHUNK),
-                                   (int64_t)ext[1] * cdiv(ext[0], SPAN_CHUNK)};
-  for (int k = 0; k <= A_IY; ++k) h.off[k][1] = sizes[k];
-  int64_t csz[3];
+                                   (int64_t)ext[1] * cdiv(ext[0], SPAN_CHUNK),
+                                   (int64_t)wz * cdiv(std::max(ext[0], ext[1]), 32)};
+  for (int k = 0; k <= A_IZ; ++k) h.off[k][1] = sizes[k];
+  int64_t csz[3], cit[3];
   for (int a = 0; a < 3; ++a) {
     int c0 = std::max(b.lo[a] / cs, 0), c1 = std::min((b.hi[a] - 1) / cs, nc[a] - 1);
     csz[a] = std::max(c1 - c0 + 1, 0);
     h.off[A_C0 + a][1] = csz[a];
+  }
+  for (int a = 0; a < 3; ++a) {
+    const int o1 = a == 0 ? 1 : 0, o2 = a == 2 ? 1 : 2;
+    cit[a] = csz[a] * cdiv(csz[o1] * csz[o2], CELL_CHUNK);
+    h.off[A_IC0 + a][1] = cit[a];
   }
   VS_TRY(lev.ensure(sizeof h, "level"));
   VS_CUDA(cudaMemcpyAsync(lev.p, &h, sizeof h, cudaMemcpyHostToDevice, st), "level copy");
@@ -1461,16 +1552,16 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
     VS_TRY(spz.ensure((ext[2] + 32) * sizeof(Span), "span_z"));
     VS_TRY(pxz.ensure((sizes[A_PXZ] + 1) * 4, "pxz"));
     VS_TRY(pyz.ensure((sizes[A_PYZ] + 1) * 4, "pyz"));
-    const int64_t mx = std::max(std::max(sizes[A_X], sizes[A_Y]),
+    const int64_t mx = std::max(std::max(std::max(sizes[A_X], sizes[A_Y]), sizes[A_Z]),
                                 std::max(sizes[A_PXZ], sizes[A_PYZ]));
-    k_span_init<<<grid_for(mx, 256), 256, 0, st>>>(spx.as<Span>(), sizes[A_X], spy.as<Span>(),
-                                                   sizes[A_Y], pxz.as<uint32_t>(), sizes[A_PXZ],
-                                                   pyz.as<uint32_t>(), sizes[A_PYZ]);
+    k_span_init<<<grid_for(mx, 256), 256, 0, st>>>(
+        spx.as<Span>(), sizes[A_X], spy.as<Span>(), sizes[A_Y], spz.as<Span>(), sizes[A_Z],
+        pxz.as<uint32_t>(), sizes[A_PXZ], pyz.as<uint32_t>(), sizes[A_PYZ]);
     k_spans_rows<0><<<grid_for(sizes[A_IX], 8), 256, 0, st>>>(bits, ny, nzw, L, sizes[A_IX],
                                                               spx.as<Span>(), pxz.as<uint32_t>());
     k_spans_rows<1><<<grid_for(sizes[A_IY], 8), 256, 0, st>>>(bits, ny, nzw, L, sizes[A_IY],
                                                               spy.as<Span>(), pyz.as<uint32_t>());
-    k_spans_z<<<grid_for(sizes[A_ZW], 8), 256, 0, st>>>(L, sizes[A_ZW], pxz.as<uint32_t>(),
+    k_spans_z<<<grid_for(sizes[A_IZ], 8), 256, 0, st>>>(L, sizes[A_IZ], pxz.as<uint32_t>(),
                                                         pyz.as<uint32_t>(), spz.as<Span>());
     VS_TRY(check_launch("spans"));
   } else {
@@ -1481,15 +1572,17 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
     VS_TRY(cslab.ensure((csz[0] + csz[1] + csz[2] + 3) * sizeof(CBox), "cell slabs"));
     CBox* cs3[3] = {cslab.as<CBox>(), cslab.as<CBox>() + csz[0] + 1,
                     cslab.as<CBox>() + csz[0] + csz[1] + 2};
+    k_cbox_init<<<grid_for(csz[0] + csz[1] + csz[2] + 3, 256), 256, 0, st>>>(
+        cslab.as<CBox>(), csz[0] + csz[1] + csz[2] + 3);
     for (int a = 0; a < 3; ++a) {
-      k_cell_slabs<<<grid_for(csz[a], 8), 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
-                                                        csz[a], cs3[a]);
+      k_cell_slabs<<<grid_for(cit[a], 8), 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
+                                                        cit[a], cs3[a]);
       B.cslab[a] = cs3[a];
       B.coff[a] = d->off[A_C0 + a];
     }
     VS_TRY(check_launch("cell slabs"));
   }
-  k_best_plane<<<1, 32, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(), spz.as<Span>(),
+  k_best_plane<<<1, DT, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(), spz.as<Span>(),
                                  scr.as<RBox>(), B, res.as<long long>());
   VS_TRY(check_launch("k_best_plane"));
   VS_TRY(d2h(out_host, res.p, 4 * sizeof(long long), st));

@@ -277,11 +277,12 @@ class BinaryVolume:
             dev = _lib.device()
             base = torch.empty(nx * ny * _nzw(nz), dtype=torch.int32, device=dev)
             cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-            call("vs_classify_bits", ptr(v.bins), nx, ny, nz, ptr(tf.params()), ptr(base),
-                 ptr(cnt), stream())
+            fused = dilate and nz % 32 == 0 and nz <= 1024 and v.bins.data_ptr() % 16 == 0
+            call("vs_classify_dilate_bits" if fused else "vs_classify_bits", ptr(v.bins), nx,
+                 ny, nz, ptr(tf.params()), ptr(base), ptr(cnt), stream())
             if self._count is None:
                 self._count = cnt
-            if dilate:
+            if dilate and not fused:
                 out = torch.empty_like(base)
                 call("vs_dilate_bits", ptr(base), nx, ny, nz, ptr(out), stream())
                 base = out

@@ -105,7 +105,8 @@ def _band_lut(lo, hi):
     return lut
 
 
-@pytest.mark.parametrize("dims", [(48, 40, 64), (64, 64, 32), (33, 17, 48), (24, 24, 528)])
+@pytest.mark.parametrize("dims", [(48, 40, 64), (64, 64, 32), (33, 17, 48), (24, 24, 528),
+                                  (40, 70, 96)])
 @pytest.mark.parametrize("tfkind", ["ramp", "ramp_lo", "band", "band_mid", "band_lo", "low", "lowhi",
                                     "twoband", "comb", "all", "none"])
 def test_random_volumes_vs_oracle(vs, rng, dims, tfkind):
@@ -155,6 +156,12 @@ def test_random_volumes_vs_oracle(vs, rng, dims, tfkind):
                                       O.macro_grid(ref, 16))
         np.testing.assert_array_equal(b.bits, ref)
     assert vs.classify(v, tf).base_count() == cnt
+    # packed dilated bits first (the fused classify+dilate pass when nz % 32 == 0): same bits,
+    # and the undilated count comes out of the same pass
+    b = vs.classify(v, tf, dilate=True)
+    b.packed()
+    np.testing.assert_array_equal(b.bits, ref_dil)
+    assert b.base_count() == cnt
 
 
 @pytest.mark.parametrize("bs", [1, 3, 8, 16])
