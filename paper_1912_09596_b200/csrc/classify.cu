@@ -370,13 +370,16 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
   } else {
     // y/z-dilated words of slabs x-1, x (ring), output row = warp
     uint32_t prev = 0, cur = 0;
+    // two slabs in flight ahead of the one being classified
+    uint4 fa = make_uint4(0, 0, 0, 0), fb = fa;
     load(x0 - 1, a, b);
+    load(x0, na, nb);
     for (int xs = x0 - 1; xs <= xe; ++xs) {
       // slab xs: classify, count, z-dilate, y-dilate
-      if (xs + 1 <= xe) {
-        na = make_uint4(0, 0, 0, 0);
-        nb = na;
-        load(xs + 1, na, nb);
+      if (xs + 2 <= xe) {
+        fa = make_uint4(0, 0, 0, 0);
+        fb = fa;
+        load(xs + 2, fa, fb);
       }
       uint32_t w = 0;
       if (rowok && xs >= 0 && xs < nx) w = classify_word<V>(ve, a, b);
@@ -397,6 +400,8 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
       cur = yd;
       a = na;
       b = nb;
+      na = fa;
+      nb = fb;
     }
   }
   if (count) {

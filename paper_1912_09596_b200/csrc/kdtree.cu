@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) k_spans_rows(const uint32_t* __restrict__
                                                     uint32_t* __restrict__ proj) {
   constexpr int AI = AX == 0 ? A_IX : A_IY, AS = AX == 0 ? A_X : A_Y,
                 AP = AX == 0 ? A_PXZ : A_PYZ;
-  constexpr int U = 4;
+  constexpr int U = 8;
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
@@ -141,17 +141,28 @@ __global__ void __launch_bounds__(256) k_spans_rows(const uint32_t* __restrict__
     const int slab = b.lo[AX] + s;
     uint32_t acc = 0;
     int rmin = KD_FAR, rmax = -1;
+    // branch-free loads (clamped addresses, masked after) so all 2U loads are in flight at once
+    const int wc = min(wl, wz - 1);
+    const int gz = b.lo[2] + 32 * wc, sh = gz & 31, rem = b.hi[2] - gz;
+    const int gw0 = gz >> 5, gw1 = min(gw0 + 1, nzw - 1);
+    const uint32_t zmask = rem < 32 ? (1u << rem) - 1u : 0xffffffffu;
     for (int rb = r0; rb < r1; rb += G * U) {
+      uint32_t lo[U], hi[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = min(rb + u * G + g, r1 - 1);
+        const int x = AX == 0 ? slab : b.lo[0] + r;
+        const int y = AX == 0 ? b.lo[1] + r : slab;
+        const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
+        lo[u] = __ldg(row + gw0);
+        hi[u] = __ldg(row + gw1);
+      }
       uint32_t v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int r = rb + u * G + g;
-        v[u] = 0;
-        if (r < r1 && wl < wz) {
-          const int x = AX == 0 ? slab : b.lo[0] + r;
-          const int y = AX == 0 ? b.lo[1] + r : slab;
-          v[u] = local_word(bits + ((int64_t)x * ny + y) * nzw, b.lo[2], b.hi[2], wl);
-        }
+        const bool ok = rb + u * G + g < r1 && wl < wz;
+        const uint32_t w = (lo[u] >> sh) | (sh ? hi[u] << (32 - sh) : 0u);
+        v[u] = ok ? (w & zmask) : 0u;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
