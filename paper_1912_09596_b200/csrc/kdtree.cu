@@ -422,13 +422,16 @@ __device__ __forceinline__ void others(int a, int& o1, int& o2) {
   o2 = a == 2 ? 1 : 2;
 }
 
+// (register-only: the axis selects components, no dynamically indexed arrays)
 __device__ __forceinline__ Box to_global(const Box& node, int a, const RBox& r) {
-  int o1, o2;
-  others(a, o1, o2);
+  const int lx = a == 0 ? r.lo0 : r.lo1, hx = a == 0 ? r.hi0 : r.hi1;
+  const int ly = a == 0 ? r.lo1 : (a == 1 ? r.lo0 : r.lo2);
+  const int hy = a == 0 ? r.hi1 : (a == 1 ? r.hi0 : r.hi2);
+  const int lz = a == 2 ? r.lo0 : r.lo2, hz = a == 2 ? r.hi0 : r.hi2;
   Box g;
-  g.lo[a] = node.lo[a] + r.lo0; g.hi[a] = node.lo[a] + r.hi0 + 1;
-  g.lo[o1] = node.lo[o1] + r.lo1; g.hi[o1] = node.lo[o1] + r.hi1 + 1;
-  g.lo[o2] = node.lo[o2] + r.lo2; g.hi[o2] = node.lo[o2] + r.hi2 + 1;
+  g.lo[0] = node.lo[0] + lx; g.hi[0] = node.lo[0] + hx + 1;
+  g.lo[1] = node.lo[1] + ly; g.hi[1] = node.lo[1] + hy + 1;
+  g.lo[2] = node.lo[2] + lz; g.hi[2] = node.lo[2] + hz + 1;
   return g;
 }
 
@@ -525,49 +528,54 @@ __global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
   const int i = blockIdx.x;
   if (i >= L.n) return;
   const Box b = L.box[i];
-  int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
+  const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
   const int64_t vol = box_vol(b);
   KdDecision d;
   d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.leaf = b;
   bool split = false;
-  {
-    const Span* sp[3] = {span_x + L.off[A_X][i], span_y + L.off[A_Y][i],
-                         span_z + L.off[A_Z][i]};
-    if (!halted(P, vol)) {
-      // _sweep_search + acceptance (kdtree.py:191-221, 431-439)
-      int ba = -1, bk = 0;
-      int64_t bc = 0;
-      for (int a = 0; a < 3; ++a) {
-        if (ext[a] < 2) continue;
-        int k;
-        int64_t c;
-        sweep_axis(sp[a], ext[a], scratch + L.off[A_SCR][i], sm, k, c);
-        if (ba >= 0 && c >= bc) continue;
-        ba = a; bk = k; bc = c;
-      }
-      if (ba >= 0 && bc < vol) {
-        const RBox l = range_box(sp[ba], 0, bk, sm);
-        const RBox r = range_box(sp[ba], bk, ext[ba], sm);
-        d.axis = ba; d.plane = b.lo[ba] + bk;
-        if (l.hi0 >= 0) { d.left = to_global(b, ba, l); d.nchild |= 1; }
-        if (r.hi0 >= 0) { d.right = to_global(b, ba, r); d.nchild |= 2; }
-        split = true;
-      }
+  const Span* spx = span_x + L.off[A_X][i];
+  const Span* spy = span_y + L.off[A_Y][i];
+  const Span* spz = span_z + L.off[A_Z][i];
+  // axis-selected operands without dynamically indexed (local-memory) arrays
+  auto axis_span = [&](int a) { return a == 0 ? spx : (a == 1 ? spy : spz); };
+  auto axis_ext = [&](int a) { return a == 0 ? ex : (a == 1 ? ey : ez); };
+  auto axis_lo = [&](int a) { return a == 0 ? b.lo[0] : (a == 1 ? b.lo[1] : b.lo[2]); };
+  auto split_at = [&](int a, int k) {
+    const Span* sp = axis_span(a);
+    const RBox l = range_box(sp, 0, k, sm);
+    const RBox r = range_box(sp, k, axis_ext(a), sm);
+    d.axis = a; d.plane = axis_lo(a) + k;
+    if (l.hi0 >= 0) { d.left = to_global(b, a, l); d.nchild |= 1; }
+    if (r.hi0 >= 0) { d.right = to_global(b, a, r); d.nchild |= 2; }
+  };
+  if (!halted(P, vol)) {
+    // _sweep_search + acceptance (kdtree.py:191-221, 431-439)
+    RBox* suf = scratch + L.off[A_SCR][i];
+    int ba = -1, bk = 0;
+    int64_t bc = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int e = a == 0 ? ex : (a == 1 ? ey : ez);
+      if (e < 2) continue;
+      int k;
+      int64_t c;
+      sweep_axis(a == 0 ? spx : (a == 1 ? spy : spz), e, suf, sm, k, c);
+      if (ba >= 0 && c >= bc) continue;
+      ba = a; bk = k; bc = c;
     }
-    if (!split && P.mls >= 0) {
-      // forced_split (kdtree.py:441-467): middle of the longest axis, exact children
-      int a = 0;
-      if (ext[1] > ext[a]) a = 1;
-      if (ext[2] > ext[a]) a = 2;
-      if (ext[a] > P.mls) {
-        const int k = ext[a] / 2;
-        const RBox l = range_box(sp[a], 0, k, sm);
-        const RBox r = range_box(sp[a], k, ext[a], sm);
-        d.axis = a; d.plane = b.lo[a] + k;
-        if (l.hi0 >= 0) { d.left = to_global(b, a, l); d.nchild |= 1; }
-        if (r.hi0 >= 0) { d.right = to_global(b, a, r); d.nchild |= 2; }
-        split = true;
-      }
+    if (ba >= 0 && bc < vol) {
+      split_at(ba, bk);
+      split = true;
+    }
+  }
+  if (!split && P.mls >= 0) {
+    // forced_split (kdtree.py:441-467): middle of the longest axis, exact children
+    int a = 0, e = ex;
+    if (ey > e) { a = 1; e = ey; }
+    if (ez > e) { a = 2; e = ez; }
+    if (e > P.mls) {
+      split_at(a, e / 2);
+      split = true;
     }
   }
   if (t == 0) {
@@ -1032,6 +1040,42 @@ __global__ void k_preorder(const NodeRec* __restrict__ rec, int64_t b0, int64_t 
   if (r.right >= 0 && size[r.right] > 0) pre[r.right] = nxt;
 }
 
+// Both passes for every level in one block (levels are few-thousand-node sets on deep trees,
+// so a block-wide barrier per level replaces two launches per level).
+__global__ void __launch_bounds__(1024) k_order_levels(const NodeRec* __restrict__ rec,
+                                                       const int64_t* __restrict__ level_base,
+                                                       int nlevels, int* __restrict__ size,
+                                                       int* __restrict__ pre) {
+  for (int l = nlevels - 1; l >= 0; --l) {
+    const int64_t b0 = level_base[l], b1 = level_base[l + 1];
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const NodeRec r = rec[i];
+      int s = 0;
+      if (!r.dropped) {
+        s = 1;
+        if (r.left >= 0) s += size[r.left];
+        if (r.right >= 0) s += size[r.right];
+      }
+      size[i] = s;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) pre[0] = 0;
+  __syncthreads();
+  for (int l = 0; l < nlevels; ++l) {
+    const int64_t b0 = level_base[l], b1 = level_base[l + 1];
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const NodeRec r = rec[i];
+      if (r.dropped) continue;
+      const int p = pre[i];
+      int nxt = p + 1;
+      if (r.left >= 0 && size[r.left] > 0) { pre[r.left] = nxt; nxt += size[r.left]; }
+      if (r.right >= 0 && size[r.right] > 0) pre[r.right] = nxt;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_scatter_rows(const NodeRec* __restrict__ rec, int64_t total,
                                const int* __restrict__ size, const int* __restrict__ pre,
                                int32_t* __restrict__ lo, int32_t* __restrict__ hi,
@@ -1330,23 +1374,35 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
   level_base.push_back(total);
   VS_TRY(sizes.ensure(total * sizeof(int), "sizes"));
   VS_TRY(pre.ensure(total * sizeof(int), "preorder"));
-  for (int l = (int)level_base.size() - 2; l >= 0; --l) {
-    const int64_t b0 = level_base[l], b1 = level_base[l + 1];
-    k_sizes<<<(unsigned)cdiv(b1 - b0, 128), 128, 0, st>>>(rec.as<NodeRec>(), b0, b1,
-                                                          sizes.as<int>());
-    VS_TRY(check_launch("k_sizes"));
+  const int nlev = (int)level_base.size() - 1;
+  if (total <= (1 << 16)) {
+    DBuf lb;
+    lb.st = st;
+    VS_TRY(lb.ensure(level_base.size() * sizeof(int64_t), "level bases"));
+    VS_CUDA(cudaMemcpyAsync(lb.p, level_base.data(), level_base.size() * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, st), "level bases");
+    k_order_levels<<<1, 1024, 0, st>>>(rec.as<NodeRec>(), lb.as<int64_t>(), nlev, sizes.as<int>(),
+                                       pre.as<int>());
+    VS_TRY(check_launch("k_order_levels"));
+  } else {
+    for (int l = nlev - 1; l >= 0; --l) {
+      const int64_t b0 = level_base[l], b1 = level_base[l + 1];
+      k_sizes<<<(unsigned)cdiv(b1 - b0, 128), 128, 0, st>>>(rec.as<NodeRec>(), b0, b1,
+                                                            sizes.as<int>());
+      VS_TRY(check_launch("k_sizes"));
+    }
+    VS_CUDA(cudaMemsetAsync(pre.p, 0, sizeof(int), st), "pre root");
+    for (int l = 0; l < nlev; ++l) {
+      const int64_t b0 = level_base[l], b1 = level_base[l + 1];
+      k_preorder<<<(unsigned)cdiv(b1 - b0, 128), 128, 0, st>>>(rec.as<NodeRec>(), b0, b1,
+                                                               sizes.as<int>(), pre.as<int>());
+      VS_TRY(check_launch("k_preorder"));
+    }
   }
   int m = 0;
   VS_TRY(d2h(&m, sizes.p, sizeof m, st));
   R->m = m;
   if (m == 0) return 0;
-  VS_CUDA(cudaMemsetAsync(pre.p, 0, sizeof(int), st), "pre root");
-  for (size_t l = 0; l + 1 < level_base.size(); ++l) {
-    const int64_t b0 = level_base[l], b1 = level_base[l + 1];
-    k_preorder<<<(unsigned)cdiv(b1 - b0, 128), 128, 0, st>>>(rec.as<NodeRec>(), b0, b1,
-                                                             sizes.as<int>(), pre.as<int>());
-    VS_TRY(check_launch("k_preorder"));
-  }
   VS_TRY(R->lo.ensure(3 * m * 4, "lo"));
   VS_TRY(R->hi.ensure(3 * m * 4, "hi"));
   VS_TRY(R->axis.ensure(m, "axis"));
