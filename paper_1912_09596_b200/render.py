@@ -226,7 +226,10 @@ def tf_device(tf: TransferFunction, dt: float):
 
 
 def _check_flags(flags: torch.Tensor):
-    f = int(flags.item())
+    _check_flag_bits(int(flags.item()))
+
+
+def _check_flag_bits(f: int):
     if f & RF_OVERFLOW:
         raise RuntimeError("traversal stack overflow (tree deeper than the device stack)")
     if f & RF_ORDER:

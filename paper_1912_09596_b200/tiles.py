@@ -10,12 +10,15 @@ process groups (gloo) for the host-side tests of the stripe bookkeeping.
 
 from __future__ import annotations
 
+import sys
+
 import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _lib
-from .render import (Camera, Frame, RenderTarget, RowsDesc, _check_flags, camera_desc,
+from .render import (Camera, Frame, RenderTarget, RowsDesc, _check_flag_bits, _check_flags,
+                     camera_desc,
                      index_desc, render_rows, volume_desc)
 
 DEFAULT_STRIPE = 8
@@ -116,14 +119,37 @@ class TileRenderer:
         return int(t.item())
 
     def frame(self, v, tf, index, cam: Camera, dt: float = 0.5) -> Frame:
-        """Public API: a full Frame (host pixels) rendered by the whole group; the pixels come
-        back through a pinned staging buffer."""
+        """Public API: a full Frame (host pixels) rendered by the whole group.
+
+        Pixels, the renderer's flags and the sample total come back in one asynchronous copy
+        into pinned host memory and one stream synchronisation.  The Frame's pixel array IS the
+        pinned buffer; it is recycled for a later frame only once the caller has dropped every
+        reference to it (otherwise a fresh pinned buffer is allocated)."""
         img = self.render(v, tf, index, cam, dt)
-        _check_flags(self.target.flags)
-        host = self.__dict__.get("_pinned")
-        if host is None:
-            host = torch.empty(img.shape, dtype=img.dtype).pin_memory()
-            self._pinned = host
-        host.copy_(img)
-        return Frame(width=self.width, height=self.height, pixels=host.numpy().copy(),
-                     sample_count=self.sample_total())
+        total = self._last_total
+        if self.world > 1:
+            if dist.get_backend(self.group) == "nccl":
+                dist.all_gather_into_tensor(self.totals, total, group=self.group)
+                total = self.totals.sum().reshape(1)
+            else:
+                total = torch.tensor([self.sample_total()], dtype=torch.int64, device=img.device)
+        ring = self.__dict__.setdefault("_pinned_ring", [])
+        slot = None
+        for s in ring:
+            # free when only the ring entry (and getrefcount's argument) refers to it
+            if sys.getrefcount(s["pixels"]) <= 2:
+                slot = s
+                break
+        if slot is None:
+            pix = torch.empty(img.shape, dtype=img.dtype).pin_memory()
+            slot = {"t": pix, "pixels": pix.numpy(),
+                    "meta": torch.empty(2, dtype=torch.int64).pin_memory()}
+            ring.append(slot)
+        slot["t"].copy_(img, non_blocking=True)
+        meta_dev = torch.cat([self.target.flags.to(torch.int64).reshape(1), total.reshape(1)])
+        slot["meta"].copy_(meta_dev, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        flags, samples = (int(x) for x in slot["meta"].tolist())
+        _check_flag_bits(flags)
+        return Frame(width=self.width, height=self.height, pixels=slot["pixels"],
+                     sample_count=samples)

@@ -325,3 +325,32 @@ def test_persistent_two_phase_equal(vs, blobs64, kind):
         np.testing.assert_array_equal(o[1], outs[0][1])
         np.testing.assert_array_equal(o[0], outs[0][0])
         assert o[2] == outs[0][2]
+
+
+def test_tile_frame_pinned_buffers(vs, blobs64):
+    """TileRenderer.frame hands out pinned pixel buffers: a held Frame is never overwritten,
+    a dropped one is recycled; pixels and sample counts equal render_frame's."""
+    from paper_1912_09596_b200.tiles import TileRenderer
+
+    v = vs.Volume(blobs64["u8"])
+    tfs = [vs.TransferFunction.ramp(0.3), vs.TransferFunction.ramp(0.6)]
+    cam = _cam_from(vs, blobs64, 80, 48)
+    tr = TileRenderer(cam.width, cam.height)
+    refs = []
+    for tf in tfs:
+        idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
+        refs.append(vs.render_frame(v, tf, idx, cam))
+    idx0 = vs.build_index("lbvh", vs.classify(v, tfs[0], dilate=True))
+    idx1 = vs.build_index("lbvh", vs.classify(v, tfs[1], dilate=True))
+    f0 = tr.frame(v, tfs[0], idx0, cam)
+    keep = f0.pixels.copy()
+    f1 = tr.frame(v, tfs[1], idx1, cam)
+    np.testing.assert_array_equal(f0.pixels, keep)          # still held: not overwritten
+    np.testing.assert_array_equal(f0.pixels, refs[0].pixels)
+    np.testing.assert_array_equal(f1.pixels, refs[1].pixels)
+    assert (f0.sample_count, f1.sample_count) == (refs[0].sample_count, refs[1].sample_count)
+    assert len(tr._pinned_ring) == 2
+    del f0
+    f2 = tr.frame(v, tfs[0], idx0, cam)                       # reuses the dropped buffer
+    assert len(tr._pinned_ring) == 2
+    np.testing.assert_array_equal(f2.pixels, refs[0].pixels)
