@@ -476,7 +476,7 @@ def run_multi(args, rank, ws, local):
 
     import paper_1912_09596_b200 as vs
     from paper_1912_09596_b200.engine import LbvhRebuilder
-    from paper_1912_09596_b200.multichannel import classify_multi
+    from paper_1912_09596_b200.multichannel import classify_multi, interleaved_quads
     from paper_1912_09596_b200.render import tf_device
     from paper_1912_09596_b200.synth import gen_blobs_u8
     from paper_1912_09596_b200.tiles import TileRenderer
@@ -485,8 +485,7 @@ def run_multi(args, rank, ws, local):
     nblobs = max(1, 25600 * n ** 3 // 1024 ** 3)
     u8s = [gen_blobs_u8((n, n, n), n=nblobs, seed=7 + c, sigma=3.0) for c in range(nch)]
     vols = [vs.Volume(u) for u in u8s]
-    for v in vols:
-        v.quads()
+    interleaved_quads(vols)  # channel-interleaved trilinear gather volume, built once
     tfs = channel_tfs(nch)
     cams = cameras(vols[0].dims)
     params = torch.stack([torch.stack([tf.params() for tf in tl]) for tl in tfs])

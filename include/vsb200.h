@@ -229,10 +229,16 @@ void vs_set_render_options(int opts);
 typedef struct vs_int2 { int32_t x, y; } int2_t;
 typedef struct vs_multi_desc {
   int nch, nx, ny, nz;              /* channels (<= 4) and dims                            */
-  const uint32_t* quads[4];         /* per channel trilinear gather volume (vs_build_quads) */
+  const uint32_t* quads[4];         /* per channel trilinear gather volume (unused)        */
   const float* lut[4];              /* per channel (256,4) float32 LUT                     */
   const double* corr[4];            /* per channel opacity correction table (libm pow)     */
+  const uint32_t* mquads;           /* channel-interleaved gather volume (vs_build_mquads) */
 } vs_multi_desc;
+/* Channel-interleaved trilinear gather volume: vs_mquads_words(nch) 32-bit words per voxel
+ * (1, 2 or 4), word c = channel c's vs_build_quads word.  bins: nch u8 channel volumes. */
+int vs_mquads_words(int nch);
+int vs_build_mquads(const uint8_t* const* bins, int nch, int nx, int ny, int nz, uint32_t* out,
+                    vs_stream_t stream);
 /* dst[i] |= src[i] (OR of per-channel brick summaries). */
 int vs_or_words(uint32_t* dst, const uint32_t* src, int64_t n, vs_stream_t stream);
 /* Integration of all channels over lattice ranges produced by vs_render_segments. */

@@ -8,7 +8,8 @@
 //                   the reference's update, w = (1 - A) * corr_c, C += w * rgb_c, A += w, for
 //                   every channel with alpha > 0 (render.py:750-757 per channel).
 // The renderer is the two-phase one: k_segments (shared with single channel) stores each ray's
-// lattice ranges; k_integrate_multi samples every channel per lattice point.
+// lattice ranges; k_integrate_multi<NCH> samples every channel per lattice point from the
+// channel-interleaved gather volume (two vector loads per sample for all channels).
 #include "common.cuh"
 
 namespace vs {
@@ -51,6 +52,83 @@ __device__ __forceinline__ bool mc_slab(double ox, double oy, double oz, double 
   return true;
 }
 
+// Interleaved trilinear gather volume of all channels: per voxel W words (W = 1, 2 or 4),
+// word c = channel c's packed (y,z) 2x2 quad (the vs_build_quads layout).  A multi-channel
+// sample then needs two vector loads (x0 and x1 planes) instead of 2 * nch scalar loads.
+template <int W>
+__global__ void k_build_mquads(const uint8_t* __restrict__ b0, const uint8_t* __restrict__ b1,
+                               const uint8_t* __restrict__ b2, const uint8_t* __restrict__ b3,
+                               int nch, int nx, int ny, int nz, uint32_t* __restrict__ q) {
+  const int64_t n = (int64_t)nx * ny * nz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int z = (int)(i % nz);
+  const int y = (int)((i / nz) % ny);
+  const int64_t dz = z + 1 < nz ? 1 : 0, dy = y + 1 < ny ? nz : 0;
+  const uint8_t* bs[4] = {b0, b1, b2, b3};
+  uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (c < nch) {
+      const uint8_t* b = bs[c];
+      w[c] = (uint32_t)b[i] | ((uint32_t)b[i + dz] << 8) | ((uint32_t)b[i + dy] << 16) |
+             ((uint32_t)b[i + dy + dz] << 24);
+    }
+  }
+  if (W == 4) reinterpret_cast<uint4*>(q)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  else if (W == 2) reinterpret_cast<uint2*>(q)[i] = make_uint2(w[0], w[1]);
+  else q[i] = w[0];
+}
+
+// One sample's gathered quads of every channel at the x0 and x1 planes.
+template <int NCH>
+struct McGather {
+  uint32_t w0[NCH], w1[NCH];
+  double fx, fy, fz;
+};
+
+template <int NCH>
+__device__ __forceinline__ void mc_gather(const vs_multi_desc& md, double ox, double oy, double oz,
+                                          double dx, double dy, double dz, double t,
+                                          McGather<NCH>& g) {
+  const int nx = md.nx, ny = md.ny, nz = md.nz;
+  const double px = __dadd_rn(ox, __dmul_rn(t, dx));
+  const double py = __dadd_rn(oy, __dmul_rn(t, dy));
+  const double pz = __dadd_rn(oz, __dmul_rn(t, dz));
+  const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
+  const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
+  g.fx = qx - flx; g.fy = qy - fly; g.fz = qz - flz;
+  const int x0r = (int)flx, y0r = (int)fly, z0r = (int)flz;
+  const int x0 = x0r < 0 ? 0 : (x0r > nx - 1 ? nx - 1 : x0r);
+  const int x1 = x0r + 1 < 0 ? 0 : (x0r + 1 > nx - 1 ? nx - 1 : x0r + 1);
+  const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
+  const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
+  const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
+  const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
+  const uint32_t o0 = (uint32_t)x0 * sxq + yz, o1 = (uint32_t)x1 * sxq + yz;
+  if constexpr (NCH >= 3) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(md.mquads) + o0);
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(md.mquads) + o1);
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) { g.w0[c] = aw[c]; g.w1[c] = bw[c]; }
+  } else if constexpr (NCH == 2) {
+    const uint2 a = __ldg(reinterpret_cast<const uint2*>(md.mquads) + o0);
+    const uint2 b = __ldg(reinterpret_cast<const uint2*>(md.mquads) + o1);
+    g.w0[0] = a.x; g.w0[1] = a.y; g.w1[0] = b.x; g.w1[1] = b.y;
+  } else {
+    g.w0[0] = __ldg(reinterpret_cast<const uint32_t*>(md.mquads) + o0);
+    g.w1[0] = __ldg(reinterpret_cast<const uint32_t*>(md.mquads) + o1);
+  }
+  // clamped low borders: the +1 neighbour is the voxel itself
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (y0r < 0) { g.w0[c] = __byte_perm(g.w0[c], 0, 0x1010); g.w1[c] = __byte_perm(g.w1[c], 0, 0x1010); }
+    if (z0r < 0) { g.w0[c] = __byte_perm(g.w0[c], 0, 0x2200); g.w1[c] = __byte_perm(g.w1[c], 0, 0x2200); }
+  }
+}
+
+template <int NCH>
 __global__ void __launch_bounds__(MC_TX* MC_TY)
     k_integrate_multi(vs_multi_desc md, vs_camera_desc cam, double dt, vs_rows_desc rows,
                       const int2* __restrict__ segs, const int* __restrict__ counts, int cap,
@@ -60,7 +138,8 @@ __global__ void __launch_bounds__(MC_TX* MC_TY)
   __shared__ McSmem sm;
   const int tid = threadIdx.y * MC_TX + threadIdx.x;
   for (int k = tid; k < 256; k += MC_TX * MC_TY) {
-    for (int c = 0; c < md.nch; ++c) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
       const float* L = md.lut[c];
       sm.lut[c][k] = make_float4(L[4 * k], L[4 * k + 1], L[4 * k + 2], L[4 * k + 3]);
       sm.corr[c][k] = md.corr[c][k];
@@ -84,62 +163,65 @@ __global__ void __launch_bounds__(MC_TX* MC_TY)
     const double dx = cam.dir[0], dy = cam.dir[1], dz = cam.dir[2];
     const bool zx = dx == 0.0, zy = dy == 0.0, zz = dz == 0.0;
     const double ix = zx ? 0.0 : 1.0 / dx, iy = zy ? 0.0 : 1.0 / dy, iz = zz ? 0.0 : 1.0 / dz;
-    const int nx = md.nx, ny = md.ny, nz = md.nz;
     double accr = 0.0, accg = 0.0, accb = 0.0, acca = 0.0;
     const int n = counts[pix];
     double entry, ex;
     if (n > cap) atomicOr(flags_out, 4);  // caller sizes cap from the counts (no fallback here)
     if (n > 0 && n <= cap &&
-        mc_slab(ox, oy, oz, ix, iy, iz, zx, zy, zz, (double)nx, (double)ny, (double)nz, entry, ex)) {
-      const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
-      for (int q = 0; q < n; ++q) {
-        const int2 kr = segs[(int64_t)q * npix + pix];
-        for (int k = kr.x; k < kr.y; ++k) {
-          const double t = __dadd_rn(entry, __dmul_rn((double)k, dt));
-          const double px = __dadd_rn(ox, __dmul_rn(t, dx));
-          const double py = __dadd_rn(oy, __dmul_rn(t, dy));
-          const double pz = __dadd_rn(oz, __dmul_rn(t, dz));
-          const double qx = px - 0.5, qy = py - 0.5, qz = pz - 0.5;
-          const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
-          const double fx = qx - flx, fy = qy - fly, fz = qz - flz;
-          const int x0r = (int)flx, y0r = (int)fly, z0r = (int)flz;
-          const int x0 = x0r < 0 ? 0 : (x0r > nx - 1 ? nx - 1 : x0r);
-          const int x1 = x0r + 1 < 0 ? 0 : (x0r + 1 > nx - 1 ? nx - 1 : x0r + 1);
-          const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
-          const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
-          const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
-          const uint32_t o0 = (uint32_t)x0 * sxq + yz, o1 = (uint32_t)x1 * sxq + yz;
-          for (int c = 0; c < md.nch; ++c) {
-            uint32_t w0 = __ldg(md.quads[c] + o0), w1 = __ldg(md.quads[c] + o1);
-            if (y0r < 0) { w0 = __byte_perm(w0, 0, 0x1010); w1 = __byte_perm(w1, 0, 0x1010); }
-            if (z0r < 0) { w0 = __byte_perm(w0, 0, 0x2200); w1 = __byte_perm(w1, 0, 0x2200); }
-            const float* tb = sm.u8f;
-            const float c000 = tb[w0 & 0xffu], c001 = tb[(w0 >> 8) & 0xffu];
-            const float c010 = tb[(w0 >> 16) & 0xffu], c011 = tb[w0 >> 24];
-            const float c100 = tb[w1 & 0xffu], c101 = tb[(w1 >> 8) & 0xffu];
-            const float c110 = tb[(w1 >> 16) & 0xffu], c111 = tb[w1 >> 24];
-            const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
-            const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
-            const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, fx));
-            const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, fx));
-            const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, fx));
-            const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, fx));
-            const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, fy));
-            const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, fy));
-            const double value = __dadd_rn(c0, __dmul_rn(c1 - c0, fz));
-            const int bi = __double2int_rd(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
-            const int bin = bi < 0 ? 0 : (bi > 255 ? 255 : bi);
-            const float4 col = sm.lut[c][bin];
-            if (col.w > 0.0f) {
-              const double wgt = __dmul_rn(1.0 - acca, sm.corr[c][bin]);
-              accr = __dadd_rn(accr, __dmul_rn(wgt, (double)col.x));
-              accg = __dadd_rn(accg, __dmul_rn(wgt, (double)col.y));
-              accb = __dadd_rn(accb, __dmul_rn(wgt, (double)col.z));
-              acca = __dadd_rn(acca, wgt);
-            }
-          }
-          ++taken;
+        mc_slab(ox, oy, oz, ix, iy, iz, zx, zy, zz, (double)md.nx, (double)md.ny, (double)md.nz,
+                entry, ex)) {
+      // flat sample loop over the lattice ranges, the next sample's loads issued before the
+      // current sample's interpolation and compositing
+      int q = 0;
+      int2 kr = segs[pix];
+      int k = kr.x;
+      McGather<NCH> g;
+      bool have = k < kr.y;
+      if (have) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)k, dt)), g);
+      while (true) {
+        if (!have) {
+          if (++q >= n) break;
+          kr = segs[(int64_t)q * npix + pix];
+          k = kr.x;
+          have = k < kr.y;
+          if (have) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)k, dt)), g);
+          continue;
         }
+        McGather<NCH> gn;
+        const bool hn = k + 1 < kr.y;
+        if (hn) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)(k + 1), dt)), gn);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const uint32_t w0 = g.w0[c], w1 = g.w1[c];
+          const float* tb = sm.u8f;
+          const float c000 = tb[w0 & 0xffu], c001 = tb[(w0 >> 8) & 0xffu];
+          const float c010 = tb[(w0 >> 16) & 0xffu], c011 = tb[w0 >> 24];
+          const float c100 = tb[w1 & 0xffu], c101 = tb[(w1 >> 8) & 0xffu];
+          const float c110 = tb[(w1 >> 16) & 0xffu], c111 = tb[w1 >> 24];
+          const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
+          const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
+          const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, g.fx));
+          const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, g.fx));
+          const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, g.fx));
+          const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, g.fx));
+          const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, g.fy));
+          const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, g.fy));
+          const double value = __dadd_rn(c0, __dmul_rn(c1 - c0, g.fz));
+          const int bi = __double2int_rd(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
+          const int bin = bi < 0 ? 0 : (bi > 255 ? 255 : bi);
+          const float4 col = sm.lut[c][bin];
+          if (col.w > 0.0f) {
+            const double wgt = __dmul_rn(1.0 - acca, sm.corr[c][bin]);
+            accr = __dadd_rn(accr, __dmul_rn(wgt, (double)col.x));
+            accg = __dadd_rn(accg, __dmul_rn(wgt, (double)col.y));
+            accb = __dadd_rn(accb, __dmul_rn(wgt, (double)col.z));
+            acca = __dadd_rn(acca, wgt);
+          }
+        }
+        ++taken;
+        ++k;
+        if (hn) g = gn;
+        have = hn;
       }
     }
     const double acc[4] = {accr, accg, accb, acca};
@@ -179,17 +261,49 @@ int vs_render_multi_integrate(const vs_multi_desc* md, const vs_camera_desc* cam
       md->nch > MC_MAX)
     return fail_arg("vs_render_multi_integrate");
   for (int c = 0; c < md->nch; ++c)
-    if (!md->quads[c] || !md->lut[c] || !md->corr[c]) return fail_arg("vs_render_multi: channel");
+    if (!md->lut[c] || !md->corr[c]) return fail_arg("vs_render_multi: channel");
+  if (!md->mquads) return fail_arg("vs_render_multi: interleaved gather volume (vs_build_mquads)");
   if ((int64_t)md->nx * md->ny * md->nz >= (1LL << 32)) return fail_arg("vs_render_multi: size");
   vs_rows_desc rows;
   if (rows_opt) rows = *rows_opt;
   else { rows.nrows = cam->height; rows.stripe = cam->height; rows.nparts = 1; rows.part = 0; }
   if (rows.nrows <= 0) return 0;
   dim3 grid((unsigned)cdiv(cam->width, MC_TX), (unsigned)cdiv(rows.nrows, MC_TY));
-  k_integrate_multi<<<grid, dim3(MC_TX, MC_TY), 0, S(stream)>>>(
-      *md, *cam, dt, rows, reinterpret_cast<const int2*>(segs), counts, cap, rgba8, rgba64_opt,
-      samples_opt, total_opt, flags);
+  const int2* sg = reinterpret_cast<const int2*>(segs);
+  switch (md->nch) {
+#define VS_MC_LAUNCH(K)                                                                  \
+  case K:                                                                                \
+    k_integrate_multi<K><<<grid, dim3(MC_TX, MC_TY), 0, S(stream)>>>(                    \
+        *md, *cam, dt, rows, sg, counts, cap, rgba8, rgba64_opt, samples_opt, total_opt, \
+        flags);                                                                          \
+    break;
+    VS_MC_LAUNCH(1)
+    VS_MC_LAUNCH(2)
+    VS_MC_LAUNCH(3)
+    VS_MC_LAUNCH(4)
+#undef VS_MC_LAUNCH
+  }
   return check_launch("k_integrate_multi");
+}
+
+int vs_mquads_words(int nch) { return nch <= 1 ? 1 : (nch == 2 ? 2 : 4); }
+
+int vs_build_mquads(const uint8_t* const* bins, int nch, int nx, int ny, int nz, uint32_t* out,
+                    vs_stream_t stream) {
+  if (!bins || !out || nch < 1 || nch > MC_MAX || nx < 1 || ny < 1 || nz < 1)
+    return fail_arg("vs_build_mquads");
+  for (int c = 0; c < nch; ++c)
+    if (!bins[c]) return fail_arg("vs_build_mquads: channel");
+  const uint8_t* b[4] = {bins[0], nch > 1 ? bins[1] : nullptr, nch > 2 ? bins[2] : nullptr,
+                         nch > 3 ? bins[3] : nullptr};
+  const int64_t n = (int64_t)nx * ny * nz;
+  const unsigned g = (unsigned)cdiv(n, 256);
+  switch (vs_mquads_words(nch)) {
+    case 1: k_build_mquads<1><<<g, 256, 0, S(stream)>>>(b[0], b[1], b[2], b[3], nch, nx, ny, nz, out); break;
+    case 2: k_build_mquads<2><<<g, 256, 0, S(stream)>>>(b[0], b[1], b[2], b[3], nch, nx, ny, nz, out); break;
+    default: k_build_mquads<4><<<g, 256, 0, S(stream)>>>(b[0], b[1], b[2], b[3], nch, nx, ny, nz, out); break;
+  }
+  return check_launch("k_build_mquads");
 }
 
 }  // extern "C"

@@ -93,7 +93,25 @@ def classify_multi(volumes, tfs, dilate: bool = False) -> MultiBinaryVolume:
 
 class MultiDesc(C.Structure):
     _fields_ = [("nch", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
-                ("quads", C.c_void_p * 4), ("lut", C.c_void_p * 4), ("corr", C.c_void_p * 4)]
+                ("quads", C.c_void_p * 4), ("lut", C.c_void_p * 4), ("corr", C.c_void_p * 4),
+                ("mquads", C.c_void_p)]
+
+
+def interleaved_quads(volumes) -> torch.Tensor:
+    """Channel-interleaved trilinear gather volume of the channels (vs_build_mquads), built once
+    per channel tuple and cached on the first channel."""
+    cache = volumes[0].__dict__.setdefault("_mquads", {})
+    key = tuple(id(v) for v in volumes)
+    hit = cache.get(key)
+    if hit is not None and all(a is b for a, b in zip(hit[0], volumes)):
+        return hit[1]
+    nx, ny, nz = volumes[0].dims
+    words = _lib.query("vs_mquads_words", len(volumes))
+    q = torch.empty((nx, ny, nz, words), dtype=torch.int32, device=volumes[0].bins.device)
+    bins = (C.c_void_p * 4)(*[ptr(v.bins) for v in volumes])
+    call("vs_build_mquads", C.addressof(bins), len(volumes), nx, ny, nz, ptr(q), stream())
+    cache[key] = (tuple(volumes), q)
+    return q
 
 
 class MultiTarget:
@@ -123,9 +141,9 @@ def render_multi_rows(volumes, tfs, index, cam: Camera, target: MultiTarget, dt:
     for c, (v, tf) in enumerate(zip(volumes, tfs)):
         lut, corr = tf_device(tf, dt)
         keep += [lut, corr]
-        md.quads[c] = ptr(v.quads())
         md.lut[c] = ptr(lut)
         md.corr[c] = ptr(corr)
+    md.mquads = ptr(interleaved_quads(volumes))
     vd = volume_desc(volumes[0], quads=False)
     idx = index_desc(index)
     cd = camera_desc(cam)

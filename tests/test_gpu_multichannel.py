@@ -78,3 +78,27 @@ def test_four_channels_vs_restatement(vs, blobs64, kind):
     np.testing.assert_array_equal(samples, osamples)
     assert float(np.max(np.abs(rgba - orgba))) <= 1e-3
     np.testing.assert_array_equal(rgba, orgba)
+
+
+@pytest.mark.parametrize("nch", [1, 2])
+def test_channel_counts_vs_restatement(vs, blobs64, nch):
+    """1 and 2 channels (the 1- and 2-word interleaved gather layouts) vs the restatement."""
+    from paper_1912_09596_b200.multichannel import classify_multi, render_float_multi
+
+    u8 = blobs64["u8"]
+    chans = [u8, np.ascontiguousarray(u8[::-1])][:nch]
+    luts = []
+    for c, t in enumerate((0.3, 0.45)[:nch]):
+        lut = vs.TransferFunction.ramp(t).lut.copy()
+        lut[:, c] = 0.8
+        luts.append(lut)
+    vols = [vs.Volume(c) for c in chans]
+    tfs = [vs.TransferFunction(l) for l in luts]
+    idx = vs.build_index("lbvh", classify_multi(vols, tfs, dilate=True))
+    cam = _cam(vs, blobs64, 80, 56)
+    rgba, samples = render_float_multi(vols, tfs, idx, cam)
+    oidx = {"lo": idx.lo, "hi": idx.hi, "left": idx.left, "right": idx.right,
+            "root": idx.root, "height": idx.height()}
+    orgba, osamples = O.render_multi("lbvh", chans, luts, oidx, cam)
+    np.testing.assert_array_equal(samples, osamples)
+    np.testing.assert_array_equal(rgba, orgba)
