@@ -569,6 +569,43 @@ __global__ void k_vote_cells(const uint32_t* __restrict__ bits, int nx, int ny, 
   flags[i] = f;
 }
 
+// 16^3 cell votes when every row is whole words (nz % 32 == 0, nz <= 1024 -> <= 64 cells in
+// z): block per (cx, cy) cell column, thread per row of the column's 16 x 16 footprint, the
+// row read with 16-byte loads (all in flight), a 64-bit z-cell mask per thread OR-reduced.
+__global__ void __launch_bounds__(256) k_vote_cells16(const uint32_t* __restrict__ bits, int nx,
+                                                      int ny, int nz, int ncy, int ncz,
+                                                      uint8_t* __restrict__ flags) {
+  __shared__ unsigned long long red[8];
+  const int cx = blockIdx.x / ncy, cy = blockIdx.x - (blockIdx.x / ncy) * ncy;
+  const int x = cx * 16 + (threadIdx.x >> 4), y = cy * 16 + (threadIdx.x & 15);
+  const int nzw = nz >> 5;
+  unsigned long long m = 0;
+  if (x < nx && y < ny) {
+    const uint4* row = reinterpret_cast<const uint4*>(bits + ((int64_t)x * ny + y) * nzw);
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = 4 * k < nzw ? __ldg(row + k) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int wi = 4 * k + j;  // word index: cells 2 wi (bits 0-15), 2 wi + 1 (bits 16-31)
+        m |= (unsigned long long)((w[j] & 0xffffu) != 0u) << (2 * wi);
+        m |= (unsigned long long)((w[j] >> 16) != 0u) << (2 * wi + 1);
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < ncz) {
+    unsigned long long t = 0;
+    for (int k = 0; k < 8; ++k) t |= red[k];
+    flags[((int64_t)cx * ncy + cy) * ncz + threadIdx.x] = (t >> threadIdx.x) & 1ull;
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // Summary -> Morton bitmap (+ tile counts, + 16^3 cells).  CTA = one 8^3 tile of bricks =
 // one aligned 512-code Morton range; the 10^3 summary halo is staged in shared memory.
@@ -825,6 +862,11 @@ int vs_vote_cells(const uint32_t* bits, int nx, int ny, int nz, int cs, uint8_t*
   if (!bits || !flags || nx < 1 || ny < 1 || nz < 1 || cs < 1) return fail_arg("vs_vote_cells");
   const int ncx = (int)cdiv(nx, cs), ncy = (int)cdiv(ny, cs), ncz = (int)cdiv(nz, cs);
   const int64_t n = (int64_t)ncx * ncy * ncz;
+  if (cs == 16 && nz % 32 == 0 && nz <= 1024 && (reinterpret_cast<uintptr_t>(bits) & 15) == 0 &&
+      (nz / 32) % 4 == 0) {
+    k_vote_cells16<<<(unsigned)(ncx * ncy), 256, 0, S(st)>>>(bits, nx, ny, nz, ncy, ncz, flags);
+    return check_launch("k_vote_cells16");
+  }
   k_vote_cells<<<(unsigned)cdiv(n, 128), 128, 0, S(st)>>>(bits, nx, ny, nz, cs, ncx, ncy, ncz,
                                                           flags);
   return check_launch("k_vote_cells");

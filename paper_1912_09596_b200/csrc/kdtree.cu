@@ -973,12 +973,18 @@ __global__ void __launch_bounds__(256) k_bits_bbox(const uint32_t* __restrict__ 
   const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int lo[2] = {KD_FAR, KD_FAR}, hi[2] = {-1, -1};
   uint32_t acc = 0;
+  const int wc = min(wl, nzw - 1);
   for (int64_t rb = wid * G; rb < nrows; rb += nwarps * G * 4) {
     uint32_t v[4];
 #pragma unroll
+    for (int u = 0; u < 4; ++u) {  // branch-free clamped loads: all four in flight
+      const int64_t r = rb + (int64_t)u * nwarps * G + g;
+      v[u] = __ldg(bits + min(r, nrows - 1) * nzw + wc);
+    }
+#pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t r = rb + (int64_t)u * nwarps * G + g;
-      v[u] = (r < nrows && wl < nzw) ? __ldg(bits + r * nzw + wl) : 0u;
+      v[u] = (r < nrows && wl < nzw) ? v[u] : 0u;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {

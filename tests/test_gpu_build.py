@@ -214,3 +214,16 @@ def test_float_volume_quantisation(vs, misc):
     edge = np.array([0.0, 1.0, 0.5, -0.25, 1.5, np.nan, 0.5 / 255, 1.5 / 255], np.float32)
     vv = vs.Volume(np.tile(edge, (2, 2, 1)))
     np.testing.assert_array_equal(vv.bins.cpu().numpy()[0, 0], vs.quantize_scalar(edge))
+
+
+@pytest.mark.parametrize("dims", [(40, 36, 128), (17, 33, 256), (32, 16, 1024)])
+def test_macro_grid_from_bits_vs_oracle(vs, rng, dims):
+    """16^3 cell votes over packed bits (whole-word rows: the vectorised vote kernel) and the
+    k-d root box from the same bits, against the oracle."""
+    bits = rng.random(dims) < 0.0007
+    b = vs.BinaryVolume(bits)
+    np.testing.assert_array_equal(vs.derive_macro_grid(b, 16).occupied, O.macro_grid(bits, 16))
+    kd = vs.build_kdtree(vs.build_svt_grid(b), vs.BuildParams(mode="shallow"))
+    ref = O.kd_build(bits, mode="shallow")
+    for f in ("lo", "hi", "axis", "plane", "left", "right"):
+        np.testing.assert_array_equal(getattr(kd, f), ref[f])
