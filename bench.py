@@ -413,8 +413,11 @@ def run_ours(args, rank, ws, local):
                "kind": "port", "sample": est["sample"], "rebuild_ms": est["rebuild_s"] * 1e3,
                "render_ms": est["render_s"] * 1e3}
     clocks = clk.summary()
-    launches_per_step = 5 + 1  # summary, summary_to_bitmap, leaves, karras, refit, brick grid
-    launches_per_step += 2     # k_segments (traversal), k_integrate_segments (sampling)
+    # per step (ncu launch list, profiles/r01_launches_interactive_frame.csv): k_brick_summary,
+    # k_summary_to_bitmap, 2 CUB scan kernels launched by vs_lbvh_from_bitmap (leaf ranks),
+    # k_leaves_from_bitmap, k_karras, k_refit_chunked, k_brick_grid | k_segments,
+    # k_integrate_segments
+    launches_per_step = 8 + 2
     line = {
         "metric": METRIC,
         "value": 1e3 / ms_per_step,
@@ -580,7 +583,7 @@ def run_multi(args, rank, ws, local):
         "e2e": {"value": 1e3 / e2e_ms, "unit": "frames/s",
                 "h2d_bytes_per_step": nch * (64 + 4096 + 2048),
                 "d2h_bytes_per_step": W * H * 4, "ms_per_step": e2e_ms},
-        "gpu_launches": (nch + (nch - 1) + 5 + 1 + 2) * args.steps,
+        "gpu_launches": (nch + (nch - 1) + 7 + 2) * args.steps,  # summaries, ORs, tree (as above), render
         "cpu_baseline": cpu, "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
