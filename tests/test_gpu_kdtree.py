@@ -181,3 +181,34 @@ def test_best_plane_apis_vs_reference_semantics(vs, rng):
             root = vs.Aabb(tuple(t.lo[0]), tuple(t.hi[0]))
             sp = vs.sweep_best_plane(gg, root)
             assert sp is not None and (sp.axis, sp.position) == (int(t.axis[0]), int(t.plane[0]))
+
+
+def _blobby(rng, dims, dens, nbox):
+    bits = rng.random(dims) < dens
+    for _ in range(nbox):
+        c = rng.integers(0, dims)
+        r = rng.integers(2, 9, size=3)
+        bits[tuple(slice(max(0, c[k] - r[k]), c[k] + r[k]) for k in range(3))] = True
+    return bits
+
+
+@pytest.mark.parametrize("name", ["kd-shallow", "kd-deep-mls32", "kd-binned-mls32", "kd-deep"])
+def test_large_chunked_vs_oracle(vs, name):
+    """Boxes wider than one 64-row span chunk / 1024-cell slab chunk (the atomic-merge paths of
+    the span and cell-slab passes) and unaligned z ranges, against the oracle."""
+    rng = np.random.default_rng(11)
+    bits = _blobby(rng, (96, 272, 272), 0.0004, 40)
+    t = vs.build_kdtree(vs.build_svt_grid(vs.BinaryVolume(bits)), vs.BuildParams(**KD_PARAMS[name]))
+    _check_tree(t, O.kd_build(bits, **KD_PARAMS[name]), name)
+
+
+@pytest.mark.parametrize("name", ["kd-deep-mls32", "kd-binned-mls32"])
+def test_wide_levels_vs_oracle(vs, name):
+    """Levels of thousands of nodes (multi-tile device scans) and > 64K rows (the per-level
+    subtree-size / preorder finalisation), against the oracle."""
+    rng = np.random.default_rng(7)
+    bits = rng.random((320, 288, 256)) < 0.008
+    t = vs.build_kdtree(vs.build_svt_grid(vs.BinaryVolume(bits)), vs.BuildParams(**KD_PARAMS[name]))
+    want = O.kd_build(bits, **KD_PARAMS[name])
+    assert len(want["axis"]) > 65536
+    _check_tree(t, want, name)
