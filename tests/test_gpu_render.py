@@ -354,3 +354,27 @@ def test_tile_frame_pinned_buffers(vs, blobs64):
     f2 = tr.frame(v, tfs[0], idx0, cam)                       # reuses the dropped buffer
     assert len(tr._pinned_ring) == 2
     np.testing.assert_array_equal(f2.pixels, refs[0].pixels)
+
+
+@pytest.mark.parametrize("kind", ["lbvh", "grid"])
+def test_configs1_row_band_vs_oracle(vs, kind):
+    """BASELINE configs[1] scale (256^3 blobs, 1024x1024): a 16-row band through the middle of
+    the GPU frame equals the oracle's render of the same rows, float RGBA and sample counts."""
+    from paper_1912_09596_b200.synth import gen_blobs_u8
+
+    u8_dev = gen_blobs_u8((256, 256, 256), 400, seed=7, sigma=3.0)
+    u8 = u8_dev.cpu().numpy()
+    v = vs.Volume(u8_dev)
+    tf = vs.TransferFunction.ramp(0.3)
+    idx = vs.build_index(kind, vs.classify(v, tf, dilate=True))
+    cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=1024, height=1024)
+    rgba, samples = vs.render_float(v, tf, idx, cam)
+    if kind == "lbvh":
+        oidx = {"lo": idx.lo, "hi": idx.hi, "left": idx.left, "right": idx.right,
+                "root": idx.root, "height": idx.height()}
+    else:
+        oidx = {"occupied": idx.occupied, "cell_size": 16}
+    r0, r1 = 504, 520
+    orgba, osamples = O.render(kind, u8, tf.lut, oidx, cam, rows=(r0, r1), nthreads=8)
+    np.testing.assert_array_equal(samples[r0:r1].reshape(-1), osamples.reshape(-1))
+    np.testing.assert_array_equal(rgba[r0:r1].reshape(-1, 4), orgba.reshape(-1, 4))
