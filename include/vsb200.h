@@ -222,6 +222,11 @@ size_t vs_render_workspace(int64_t npix, int seg_cap);
 
 /* Renderer turn sizes of the traversal / sampling interleave (<= 0: unbounded). */
 void vs_set_render_tuning(int trav_steps, int samples);
+/* Early ray termination for the calling thread's subsequent vs_render calls: a ray stops once
+ * its accumulated opacity reaches 1 - eps, so every RGBA channel is within eps of the full
+ * integral (LUT colours <= 1) and fewer samples are taken.  eps <= 0: off, the reference's
+ * integrator exactly (render.py:758 counts every lattice point; the default). */
+void vs_set_render_ert(double eps);
 /* Renderer code-path options (bit 0: u8 -> f32 via a shared-memory table); same results. */
 void vs_set_render_options(int opts);
 

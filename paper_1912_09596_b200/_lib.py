@@ -52,6 +52,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_kd_best_plane": (i32, [P, i32, i32, i32, P, i32, i32, i32, P, P]),
     "vs_set_render_tuning": (None, [i32, i32]),
     "vs_set_render_options": (None, [i32]),
+    "vs_set_render_ert": (None, [C.c_double]),
     "vs_build_quads": (i32, [P, i32, i32, i32, P, P]),
     "vs_mquads_words": (i32, [i32]),
     "vs_build_mquads": (i32, [P, i32, i32, i32, i32, P, P]),

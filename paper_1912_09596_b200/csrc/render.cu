@@ -119,6 +119,7 @@ struct Integrator {
   int nx, ny, nz;
   double entry, dt, inv_dt;
   bool nearest;
+  double ert_a;  // early ray termination: stop once acca >= ert_a (2.0 = never: parity mode)
   double accr, accg, accb, acca;
   int taken;  // per-ray lattice samples (< 2^31)
   // active segment
@@ -298,15 +299,16 @@ struct Integrator {
   }
 
   __device__ __forceinline__ void run(int smax) {
-    for (int q = 0; q < smax && t < t1; ++q) sample();
-    active = t < t1;
+    for (int q = 0; q < smax && t < t1 && acca < ert_a; ++q) sample();
+    active = t < t1 && acca < ert_a;
   }
 
   __device__ __forceinline__ void segment(double t0, double t1_) {  // whole segment at once
     begin(t0, t1_);
-    while (t < t1) sample();
+    while (t < t1 && acca < ert_a) sample();
     active = false;
   }
+  __device__ __forceinline__ bool terminated() const { return acca >= ert_a; }
 };
 
 // ---- interval generators -----------------------------------------------------------------
@@ -709,6 +711,8 @@ struct SegmentSource {
 
 // while-while turn sizes (vs_set_render_tuning): traversal steps / lattice samples per turn
 static int g_trav_budget = 1, g_sample_budget = 1;
+// early ray termination (vs_set_render_ert): opacity threshold, 2.0 = off (parity mode)
+static thread_local double g_ert_a = 2.0;
 // bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float conversion)
 static int g_render_opts = 1;
 
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
              const double* __restrict__ corr, double dt, int nearest, vs_rows_desc rows,
              uint8_t* __restrict__ rgba8, double* __restrict__ rgba64, int32_t* __restrict__ samples,
              unsigned long long* __restrict__ total, int* __restrict__ flags_out, int trav_budget,
-             int sample_budget, int render_opts) {
+             int sample_budget, int render_opts, double ert_a) {
   __shared__ RenderSmem sm;
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
   for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
@@ -748,6 +752,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
     I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
     I.use_tab = (render_opts & 1) != 0;
     I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
+    I.ert_a = ert_a;
     I.accr = I.accg = I.accb = I.acca = 0.0;
     I.taken = 0;
     I.active = false;
@@ -759,7 +764,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
       // while-while: each turn does a bounded amount of traversal (lanes without a segment)
       // and a bounded number of samples (lanes with one), so lanes in the same phase share
       // instructions instead of serialising whole traversals against whole sample loops.
-      while (true) {
+      while (!I.terminated()) {
         if (!I.active) {
           int budget = trav_budget;
           double a, b;
@@ -850,7 +855,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
   if (flags) atomicOr(flags_out, flags);
 }
 
-template <int KIND, bool IDX32>
+template <int KIND, bool IDX32, bool ERT>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
     k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
                          const float* __restrict__ lut, const double* __restrict__ corr, double dt,
@@ -858,7 +863,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
                          const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
                          double* __restrict__ rgba64, int32_t* __restrict__ samples,
                          unsigned long long* __restrict__ total, int* __restrict__ flags_out,
-                         int render_opts) {
+                         int render_opts, double ert_a) {
   __shared__ RenderSmem sm;
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
   for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
@@ -882,6 +887,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
     I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
     I.use_tab = (render_opts & 1) != 0;
     I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
+    I.ert_a = ERT ? ert_a : 2.0;
     I.accr = I.accg = I.accb = I.acca = 0.0;
     I.taken = 0;
     I.active = false;
@@ -904,6 +910,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
             const bool hn = k + 1 < kr.y;
             if (hn) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)(k + 1), dt)), gn);
             I.shade(I.use_tab ? I.interp_t<true>(g) : I.interp_t<false>(g));
+            if (ERT && I.terminated()) break;
             ++k;
             if (hn) g = gn;
             have = hn;
@@ -924,6 +931,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
           if (k < kr.y) {
             I.t = __dadd_rn(I.entry, __dmul_rn((double)k, dt));
             I.sample_at();
+            if (ERT && I.terminated()) break;
             ++k;
           } else {
             if (++q >= n) break;
@@ -934,7 +942,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
       } else {  // overflow: fused traversal + integration for this ray
         SegmentSource<KIND> src;
         src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
-        while (true) {
+        while (!I.terminated()) {
           int budget = 1 << 30;
           double a, b;
           const int g = src.next(r, ix, a, b, budget, &flags);
@@ -1037,6 +1045,7 @@ __global__ void k_integrate_rays(vs_volume_desc vol, const double* __restrict__ 
     I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
     I.use_tab = (render_opts & 1) != 0;
   I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
+  I.ert_a = 2.0;  // single-ray API: the reference integrator, no termination
   I.accr = I.accg = I.accb = I.acca = 0.0;
   I.taken = 0;
   const int m = counts[q];
@@ -1090,20 +1099,23 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                counts, g_seg_cap, flags,
                                                                g_trav_budget);
-    if ((int64_t)v.nx * v.ny * v.nz < (1LL << 32))
-      k_integrate_segments<K, true><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
-          total, flags, g_render_opts);
-    else
-      k_integrate_segments<K, false><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples,
-          total, flags, g_render_opts);
+    const bool idx32 = (int64_t)v.nx * v.ny * v.nz < (1LL << 32), ert = g_ert_a <= 1.0;
+#define VS_INTEGRATE(I32, E)                                                                  \
+  k_integrate_segments<K, I32, E><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(               \
+      v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples, \
+      total, flags, g_render_opts, g_ert_a)
+    if (idx32) {
+      if (ert) VS_INTEGRATE(true, true); else VS_INTEGRATE(true, false);
+    } else {
+      if (ert) VS_INTEGRATE(false, true); else VS_INTEGRATE(false, false);
+    }
+#undef VS_INTEGRATE
     return;
   }
   k_render<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
                                                           rgba8, rgba64, samples, total, flags,
                                                           g_trav_budget, g_sample_budget,
-                                                          g_render_opts);
+                                                          g_render_opts, g_ert_a);
 }
 
 }  // namespace vs
@@ -1196,6 +1208,8 @@ int vs_build_quads(const uint8_t* bins, int nx, int ny, int nz, uint32_t* quads,
 }
 
 void vs_set_render_options(int opts) { g_render_opts = opts; }
+
+void vs_set_render_ert(double eps) { g_ert_a = eps > 0.0 ? 1.0 - eps : 2.0; }
 
 void vs_set_render_tuning(int trav_steps, int samples) {
   g_trav_budget = trav_steps > 0 ? trav_steps : (1 << 30);

@@ -261,8 +261,11 @@ class RenderTarget:
 def render_rows(v: Volume, tf: TransferFunction, index, cam: Camera, target: RenderTarget,
                 dt: float = DEFAULT_DT, nearest: bool = False, rows: RowsDesc | None = None,
                 idx_desc: IndexDesc | None = None, vol_desc: VolumeDesc | None = None,
-                cam_desc: CameraDesc | None = None, zero: bool = True):
-    """Launch k_render for (a stripe set of) the frame into ``target`` (async)."""
+                cam_desc: CameraDesc | None = None, zero: bool = True, ert_eps: float = 0.0):
+    """Launch the renderer for (a stripe set of) the frame into ``target`` (async).
+
+    ``ert_eps`` > 0 enables early ray termination at accumulated opacity 1 - ert_eps (RGBA
+    within ert_eps of the full integral, fewer samples); 0 is the reference's integrator."""
     lut, corr = tf_device(tf, dt)
     if zero:
         target.total.zero_()
@@ -270,6 +273,7 @@ def render_rows(v: Volume, tf: TransferFunction, index, cam: Camera, target: Ren
     idx_desc = idx_desc or index_desc(index)
     vol_desc = vol_desc or volume_desc(v)
     cam_desc = cam_desc or camera_desc(cam)
+    _lib.lib().vs_set_render_ert(float(ert_eps))
     call("vs_render", C.addressof(vol_desc), C.addressof(idx_desc), C.addressof(cam_desc),
          ptr(lut), ptr(corr), float(dt), int(nearest),
          None if rows is None else C.addressof(rows), ptr(target.rgba8), ptr(target.rgba64),
@@ -293,11 +297,11 @@ def render_frame(v: Volume, tf: TransferFunction, index, cam: Camera, dt: float 
 
 
 def render_float(v: Volume, tf: TransferFunction, index, cam: Camera, dt: float = DEFAULT_DT,
-                 interp: str = "trilinear"):
+                 interp: str = "trilinear", ert_eps: float = 0.0):
     """(float64 premultiplied RGBA (h,w,4), per-pixel samples (h,w)) -- the float output the
     parity tests compare with the reference's _k_integrate accumulators."""
     tgt = RenderTarget(cam.width, cam.height, want_rgba64=True, want_samples=True)
-    render_rows(v, tf, index, cam, tgt, dt=dt, nearest=interp == "nearest")
+    render_rows(v, tf, index, cam, tgt, dt=dt, nearest=interp == "nearest", ert_eps=ert_eps)
     _check_flags(tgt.flags)
     return tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy().astype(np.int64)
 

@@ -378,3 +378,33 @@ def test_configs1_row_band_vs_oracle(vs, kind):
     orgba, osamples = O.render(kind, u8, tf.lut, oidx, cam, rows=(r0, r1), nthreads=8)
     np.testing.assert_array_equal(samples[r0:r1].reshape(-1), osamples.reshape(-1))
     np.testing.assert_array_equal(rgba[r0:r1].reshape(-1, 4), orgba.reshape(-1, 4))
+
+
+@pytest.mark.parametrize("kind", ["naive", "lbvh", "kd-deep-mls32"])
+@pytest.mark.parametrize("seg_cap", [0, 16])
+def test_early_ray_termination_bound(vs, blobs64, kind, seg_cap):
+    """ERT at eps: every float RGBA channel within eps of the full (reference) integral, never
+    more samples; eps = 0 is the reference integrator bit for bit."""
+    from paper_1912_09596_b200.render import RenderTarget, render_rows
+
+    v = vs.Volume(blobs64["u8"])
+    lut = vs.TransferFunction.ramp(0.05).lut.copy()
+    lut[:, 3] = np.minimum(1.0, lut[:, 3] * 4.0)   # dense, opaque: many rays saturate
+    tf = vs.TransferFunction(lut)
+    idx = vs.build_index(kind, vs.classify(v, tf, dilate=True))
+    cam = _cam_from(vs, blobs64, 96, 64)
+    outs = {}
+    for eps in (0.0, 1e-3, 1e-2):
+        tgt = RenderTarget(cam.width, cam.height, want_rgba64=True, want_samples=True,
+                           seg_cap=seg_cap)
+        render_rows(v, tf, idx, cam, tgt, ert_eps=eps)
+        outs[eps] = (tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy())
+    full, fs = outs[0.0]
+    orgba, osamples = vs.render_float(v, tf, idx, cam)
+    np.testing.assert_array_equal(full, orgba)
+    np.testing.assert_array_equal(fs, osamples)
+    assert float((full[..., 3] >= 1 - 1e-2).mean()) > 0.1  # the case exercises termination
+    for eps in (1e-3, 1e-2):
+        rgba, s = outs[eps]
+        assert float(np.max(np.abs(rgba - full))) <= eps
+        assert np.all(s <= fs) and int(s.sum()) < int(fs.sum())
