@@ -898,29 +898,34 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
       if (n <= cap && I.quads && !I.nearest) {
         // flat sample loop, software-pipelined: the next sample's gather loads are issued
         // before the current sample's interpolation and compositing
+        // the ray's lattice ranges as one sample stream (ranges are non-empty): every turn
+        // shades one sample, the next range is prefetched one range ahead, and the next
+        // sample's gather is issued before the current sample's arithmetic, across range ends
         int q = 0;
         int2 kr = segs[pix];
+        int2 krn = n > 1 ? segs[npix + pix] : make_int2(0, 0);
         int k = kr.x;
         Integrator::Gather g;
-        bool have = k < kr.y;
-        if (have) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
+        I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
         while (true) {
-          if (have) {
-            Integrator::Gather gn;
-            const bool hn = k + 1 < kr.y;
-            if (hn) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)(k + 1), dt)), gn);
-            I.shade(I.use_tab ? I.interp_t<true>(g) : I.interp_t<false>(g));
-            if (ERT && I.terminated()) break;
-            ++k;
-            if (hn) g = gn;
-            have = hn;
-          } else {
-            if (++q >= n) break;
-            kr = segs[(int64_t)q * npix + pix];
-            k = kr.x;
-            have = k < kr.y;
-            if (have) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
+          int kn = k + 1;
+          bool hn = true;
+          if (kn >= kr.y) {
+            if (q + 1 < n) {
+              ++q;
+              kr = krn;
+              kn = kr.x;
+              if (q + 1 < n) krn = segs[(int64_t)(q + 1) * npix + pix];
+            } else {
+              hn = false;
+            }
           }
+          Integrator::Gather gn;
+          if (hn) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)kn, dt)), gn);
+          I.shade(I.use_tab ? I.interp_t<true>(g) : I.interp_t<false>(g));
+          if (!hn || (ERT && I.terminated())) break;
+          k = kn;
+          g = gn;
         }
       } else if (n <= cap) {
         // flat sample loop: each turn either samples or switches to the next lattice range
