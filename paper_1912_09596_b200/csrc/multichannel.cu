@@ -172,24 +172,29 @@ __global__ void __launch_bounds__(MC_TX* MC_TY)
                 entry, ex)) {
       // flat sample loop over the lattice ranges, the next sample's loads issued before the
       // current sample's interpolation and compositing
+      // the ranges as one sample stream (see k_integrate_segments): next range prefetched,
+      // next sample's gather issued across range ends
       int q = 0;
       int2 kr = segs[pix];
+      int2 krn = n > 1 ? segs[npix + pix] : make_int2(0, 0);
       int k = kr.x;
       McGather<NCH> g;
-      bool have = k < kr.y;
-      if (have) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)k, dt)), g);
+      mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)k, dt)), g);
       while (true) {
-        if (!have) {
-          if (++q >= n) break;
-          kr = segs[(int64_t)q * npix + pix];
-          k = kr.x;
-          have = k < kr.y;
-          if (have) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)k, dt)), g);
-          continue;
+        int kn = k + 1;
+        bool hn = true;
+        if (kn >= kr.y) {
+          if (q + 1 < n) {
+            ++q;
+            kr = krn;
+            kn = kr.x;
+            if (q + 1 < n) krn = segs[(int64_t)(q + 1) * npix + pix];
+          } else {
+            hn = false;
+          }
         }
         McGather<NCH> gn;
-        const bool hn = k + 1 < kr.y;
-        if (hn) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)(k + 1), dt)), gn);
+        if (hn) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)kn, dt)), gn);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           const uint32_t w0 = g.w0[c], w1 = g.w1[c];
@@ -219,9 +224,9 @@ __global__ void __launch_bounds__(MC_TX* MC_TY)
           }
         }
         ++taken;
-        ++k;
-        if (hn) g = gn;
-        have = hn;
+        if (!hn) break;
+        k = kn;
+        g = gn;
       }
     }
     const double acc[4] = {accr, accg, accb, acca};
