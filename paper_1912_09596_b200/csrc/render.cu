@@ -714,6 +714,7 @@ static int g_trav_budget = 1, g_sample_budget = 1;
 // early ray termination (vs_set_render_ert): opacity threshold, 2.0 = off (parity mode)
 static thread_local double g_ert_a = 2.0;
 // bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float conversion)
+// bit2: generic k_segments for the LBVH brick DDA (else the specialised k_segments_brick)
 static int g_render_opts = 1;
 
 template <int KIND>
@@ -850,6 +851,94 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
       }
       kprev = k1;
     }
+  }
+  counts[pix] = n;
+  if (flags) atomicOr(flags_out, flags);
+}
+
+// k_segments specialised for the LBVH brick DDA: the same DDA steps (BrickDDA::init/next),
+// interval merge (_sort_merge via MergeState) and lattice-range emission as the generic
+// kernel, written as one flat loop of one DDA step per turn with 32-bit brick indices and no
+// generator/budget plumbing between the step and the merge.
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
+    k_segments_brick(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
+                     double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
+                     int* __restrict__ flags_out) {
+  const int i = blockIdx.x * RENDER_TX + threadIdx.x;
+  const int l = blockIdx.y * RENDER_TY + threadIdx.y;
+  if (i >= cam.width || l >= rows.nrows) return;
+  const int64_t pix = (int64_t)l * cam.width + i;
+  const int64_t npix = (int64_t)rows.nrows * cam.width;
+  Ray r;
+  pixel_ray(cam, rows, i, l, r);
+  int n = 0, flags = 0;
+  double tmin, tmax;
+  if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+    const int nb_bricks = ix.lbvh_info ? __ldg(ix.lbvh_info) : ix.root + 1;
+    BrickDDA D;
+    D.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax, nb_bricks > 0);
+    Integrator L;  // lattice only
+    L.entry = tmin;
+    L.dt = dt;
+    L.inv_dt = 1.0 / dt;
+    const int bs = D.bs, nby = D.nb[1], nbz = D.nb[2];
+    const uint32_t* __restrict__ bits = D.bits;
+    int steps = 0;
+    const int maxsteps = D.nb[0] + D.nb[1] + D.nb[2] + 3;
+    // merge state (MergeState): open interval [ma, mb)
+    bool open = false;
+    double ma = 0.0, mb = 0.0, last_t0 = -DBL_MAX;
+    int kprev = -1;
+    auto emit = [&](double a, double b) {
+      const int k0 = (int)L.first_k(a), k1 = (int)L.first_k(b);
+      if (k1 <= k0) return;
+      if (n > 0 && k0 == kprev && n <= cap) {
+        segs[(int64_t)(n - 1) * npix + pix].y = k1;
+      } else {
+        if (n < cap) segs[(int64_t)n * npix + pix] = make_int2(k0, k1);
+        ++n;
+      }
+      kprev = k1;
+    };
+    bool done = D.done;
+    while (!done) {
+      if (steps++ >= maxsteps) break;
+      const int lin = (D.c[0] * nby + D.c[1]) * nbz + D.c[2];
+      if ((__ldg(bits + (lin >> 5)) >> (lin & 31)) & 1u) {
+        double a, b;
+        const int l0 = D.c[0] * bs, l1 = D.c[1] * bs, l2 = D.c[2] * bs;
+        if (slab(r, (double)l0, (double)l1, (double)l2, (double)min(l0 + bs, D.dims[0]),
+                 (double)min(l1 + bs, D.dims[1]), (double)min(l2 + bs, D.dims[2]), a, b)) {
+          a = a > tmin ? a : tmin;
+          b = b < tmax ? b : tmax;
+          if (b > a) {
+            if (a < last_t0) flags |= RF_ORDER;
+            last_t0 = a;
+            if (open && a <= mb) {
+              if (b > mb) mb = b;
+            } else {
+              if (open) emit(ma, mb);
+              ma = a;
+              mb = b;
+              open = true;
+            }
+          }
+        }
+      }
+      double tt = D.tn[0];
+      if (D.tn[1] < tt) tt = D.tn[1];
+      if (D.tn[2] < tt) tt = D.tn[2];
+      if (tt >= tmax) break;
+#pragma unroll
+      for (int a2 = 0; a2 < 3; ++a2) {
+        if (D.tn[a2] == tt) {
+          D.c[a2] += D.s[a2];
+          if (D.c[a2] < 0 || D.c[a2] >= D.nb[a2]) done = true;
+          D.tn[a2] = D.plane_t(r, a2, D.c[a2] + (D.s[a2] > 0));
+        }
+      }
+    }
+    if (open) emit(ma, mb);
   }
   counts[pix] = n;
   if (flags) atomicOr(flags_out, flags);
@@ -1101,9 +1190,13 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     const int64_t npix = (int64_t)rows.nrows * c.width;
     int2* segs = static_cast<int2*>(g_seg_ws);
     int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
-    k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                               counts, g_seg_cap, flags,
-                                                               g_trav_budget);
+    if (K == KIND_LBVH_BRICK && !(g_render_opts & 4))
+      k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
+                                                                   counts, g_seg_cap, flags);
+    else
+      k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
+                                                                 counts, g_seg_cap, flags,
+                                                                 g_trav_budget);
     const bool idx32 = (int64_t)v.nx * v.ny * v.nz < (1LL << 32), ert = g_ert_a <= 1.0;
 #define VS_INTEGRATE(I32, E)                                                                  \
   k_integrate_segments<K, I32, E><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(               \
