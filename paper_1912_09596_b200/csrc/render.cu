@@ -714,7 +714,7 @@ static int g_trav_budget = 1, g_sample_budget = 1;
 // early ray termination (vs_set_render_ert): opacity threshold, 2.0 = off (parity mode)
 static thread_local double g_ert_a = 2.0;
 // bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float conversion)
-// bit2: generic k_segments for the LBVH brick DDA (else the specialised k_segments_brick)
+// bit2: generic k_segments for the LBVH brick DDA / grid (else k_segments_brick / _grid)
 static int g_render_opts = 1;
 
 template <int KIND>
@@ -938,6 +938,86 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
         }
       }
     }
+    if (open) emit(ma, mb);
+  }
+  counts[pix] = n;
+  if (flags) atomicOr(flags_out, flags);
+}
+
+// k_segments specialised for the macro-cell grid (_k_grid: _dda_runs then _sort_merge): the
+// same GridDDA steps, runs and merge as the generic kernel in one flat loop.
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
+    k_segments_grid(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
+                    double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
+                    int* __restrict__ flags_out) {
+  const int i = blockIdx.x * RENDER_TX + threadIdx.x;
+  const int l = blockIdx.y * RENDER_TY + threadIdx.y;
+  if (i >= cam.width || l >= rows.nrows) return;
+  const int64_t pix = (int64_t)l * cam.width + i;
+  const int64_t npix = (int64_t)rows.nrows * cam.width;
+  Ray r;
+  pixel_ray(cam, rows, i, l, r);
+  int n = 0, flags = 0;
+  double tmin, tmax;
+  if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+    GridDDA G;
+    G.init(r, ix, tmin, tmax);
+    Integrator L;  // lattice only
+    L.entry = tmin;
+    L.dt = dt;
+    L.inv_dt = 1.0 / dt;
+    bool open = false;
+    double ma = 0.0, mb = 0.0, last_t0 = -DBL_MAX;
+    int kprev = -1;
+    auto emit = [&](double a, double b) {
+      const int k0 = (int)L.first_k(a), k1 = (int)L.first_k(b);
+      if (k1 <= k0) return;
+      if (n > 0 && k0 == kprev && n <= cap) {
+        segs[(int64_t)(n - 1) * npix + pix].y = k1;
+      } else {
+        if (n < cap) segs[(int64_t)n * npix + pix] = make_int2(k0, k1);
+        ++n;
+      }
+      kprev = k1;
+    };
+    auto feed = [&](double a, double b) {  // MergeState::feed
+      if (a < last_t0) flags |= RF_ORDER;
+      last_t0 = a;
+      if (b <= a) return;
+      if (open && a <= mb) {
+        if (b > mb) mb = b;
+        return;
+      }
+      if (open) emit(ma, mb);
+      ma = a;
+      mb = b;
+      open = true;
+    };
+    const int ncy = G.ncy, ncz = G.ncz;
+    int cx = (int)G.cx, cy = (int)G.cy, cz = (int)G.cz;
+    int steps = 0;
+    const int max_steps = (int)G.max_steps;
+    bool run = false;
+    double run_t0 = 0.0, tcur = tmin;
+    while (steps < max_steps) {
+      double tn = G.tnx;
+      if (G.tny < tn) tn = G.tny;
+      if (G.tnz < tn) tn = G.tnz;
+      if (__ldg(G.occ + ((int64_t)cx * ncy + cy) * ncz + cz)) {
+        if (!run) { run = true; run_t0 = tcur; }
+      } else if (run) {
+        feed(run_t0, tcur);
+        run = false;
+      }
+      ++steps;
+      if (tn >= tmax) break;
+      if (G.tnx == tn) { cx += G.sx; G.tnx = G.cross(cx, G.sx, r.ox, r.ix); }
+      if (G.tny == tn) { cy += G.sy; G.tny = G.cross(cy, G.sy, r.oy, r.iy); }
+      if (G.tnz == tn) { cz += G.sz; G.tnz = G.cross(cz, G.sz, r.oz, r.iz); }
+      tcur = tn;
+      if (cx < 0 || cy < 0 || cz < 0 || cx >= G.ncx || cy >= ncy || cz >= ncz) break;
+    }
+    if (run) feed(run_t0, tmax);
     if (open) emit(ma, mb);
   }
   counts[pix] = n;
@@ -1193,6 +1273,9 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     if (K == KIND_LBVH_BRICK && !(g_render_opts & 4))
       k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                    counts, g_seg_cap, flags);
+    else if (K == VS_KIND_GRID && !(g_render_opts & 4))
+      k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
+                                                                  counts, g_seg_cap, flags);
     else
       k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                  counts, g_seg_cap, flags,
