@@ -370,17 +370,17 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
   } else {
     // y/z-dilated words of slabs x-1, x (ring), output row = warp
     uint32_t prev = 0, cur = 0;
-    // two slabs in flight ahead of the one being classified
-    uint4 fa = make_uint4(0, 0, 0, 0), fb = fa;
+    // three slabs in flight ahead of the one being classified; the y-dilation exchange is
+    // double-buffered so one barrier per slab suffices
+    uint4 fa = make_uint4(0, 0, 0, 0), fb = fa, ga = fa, gb = fa;
     load(x0 - 1, a, b);
     load(x0, na, nb);
+    load(x0 + 1, fa, fb);
     for (int xs = x0 - 1; xs <= xe; ++xs) {
       // slab xs: classify, count, z-dilate, y-dilate
-      if (xs + 2 <= xe) {
-        fa = make_uint4(0, 0, 0, 0);
-        fb = fa;
-        load(xs + 2, fa, fb);
-      }
+      ga = make_uint4(0, 0, 0, 0);
+      gb = ga;
+      if (xs + 3 <= xe) load(xs + 3, ga, gb);
       uint32_t w = 0;
       if (rowok && xs >= 0 && xs < nx) w = classify_word<V>(ve, a, b);
       if (outrow && xs >= x0 && xs < xe) cnt += __popc(w);
@@ -389,19 +389,18 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
       uint32_t zd = w | (w << 1) | (w >> 1);
       if (lane > 0) zd |= up >> 31;
       if (lane + 1 < nzw) zd |= dn << 31;
-      __syncthreads();
-      zs[warp * 32 + lane] = zd;
+      uint32_t* zb = zs + (xs & 1) * ((CP_TY + 2) * 32);
+      zb[warp * 32 + lane] = zd;
       __syncthreads();
       uint32_t yd = 0;
-      if (warp >= 1 && warp <= CP_TY) yd = zs[(warp - 1) * 32 + lane] | zd | zs[(warp + 1) * 32 + lane];
+      if (warp >= 1 && warp <= CP_TY) yd = zb[(warp - 1) * 32 + lane] | zd | zb[(warp + 1) * 32 + lane];
       // slab xs - 1 is complete: prev (xs-2) | cur (xs-1) | yd (xs)
       if (outrow && xs - 1 >= x0) out[((int64_t)(xs - 1) * ny + y) * nzw + lane] = prev | cur | yd;
       prev = cur;
       cur = yd;
-      a = na;
-      b = nb;
-      na = fa;
-      nb = fb;
+      a = na; b = nb;
+      na = fa; nb = fb;
+      fa = ga; fb = gb;
     }
   }
   if (count) {
@@ -425,7 +424,7 @@ __global__ void __launch_bounds__(1024) k_classify_pack(const uint8_t* __restric
                                                         uint32_t* __restrict__ out,
                                                         unsigned long long* __restrict__ count) {
   __shared__ uint8_t tab[256];
-  __shared__ uint32_t zs[(CP_TY + 2) * 32];
+  __shared__ uint32_t zs[2 * (CP_TY + 2) * 32];
   __shared__ uint32_t red[32];
   VisEval ve;
   const int v = load_vis(ve, tf, tab);
