@@ -6,18 +6,20 @@
 // the rows are renumbered to the reference's DFS preorder at the end (emit-before-recurse,
 // left subtree first; kdtree.py:412-419, 479-484).
 //
-// Per level:
+// Per level (one host synchronisation: the level's node count and work totals):
 //   sweep builder (kdtree.py:148-230): for every node that may split, per-slab spans along
-//     each axis (k_spans_x / k_spans_y own an x- or y-slab per warp and also OR the region's
-//     (x,z) / (y,z) projections; k_spans_z derives the z-slab spans from those projections),
-//     then one warp per node runs _axis_sweep's prefix/suffix min/max scans, the cost argmin
+//     each axis -- k_spans_rows<X>/<Y>: warp per (node, slab, 64-row chunk), a row's z words
+//     on one lane group, chunks merged with atomics, plus the (x,z) / (y,z) OR-projections;
+//     k_spans_z: z-slab spans from the projections by per-bit ballots -- then k_decide, one
+//     block per node: _axis_sweep's prefix/suffix tight boxes as block scans, the cost argmin
 //     (first minimum; strict < across axes), the acceptance test cost < box volume, the
 //     halting rule and the forced middle split; children are exact tight boxes.
 //   binned builder (kdtree.py:268-381): per-cell tight boxes once (precompute_cell_boxes),
-//     per level the same slab decomposition over cells with box unions (the coordinate
-//     filter that _cells_reduce's Morton range accelerates), _snapped_positions in IEEE
-//     double, first strict minimum; binned leaves get the exact shrink from k_spans_x.
-//   compaction of children into the next level (left then right), parent links.
+//     per level the cell-slab unions (k_cell_slabs; the coordinate filter that _cells_reduce's
+//     Morton range accelerates), k_decide_binned (warp per node: _snapped_positions in IEEE
+//     double, first strict minimum) and the exact leaf shrink from the bits (k_leaf_shrink).
+//   k_emit_level: rows of the level, the next level's boxes (left then right) and their work
+//     sizes (prep_node), scanned on the device (k_multi_scan).
 // Finalisation: subtree sizes bottom-up, preorder numbers top-down, scatter rows.
 #include <cub/cub.cuh>
 
