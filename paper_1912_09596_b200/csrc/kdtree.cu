@@ -517,7 +517,12 @@ __device__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a, 
                            lane, out);
 }
 
+// Slab spans of one axis staged in shared memory by k_decide (with the suffix boxes) when the
+// node's extent along the axis is at most this.
+constexpr int STAGE_SLABS = 1024;
+
 // ---- the decision kernel: one block of DT threads per node ----------------------------------
+template <bool STAGE>
 __global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
                                                const Span* __restrict__ span_x,
                                                const Span* __restrict__ span_y,
@@ -526,6 +531,8 @@ __global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
                                                KdDecision* __restrict__ out,
                                                int64_t* __restrict__ child_count) {
   __shared__ DecideSmem sm;
+  __shared__ Span stage_sp[STAGE ? STAGE_SLABS : 1];
+  __shared__ RBox stage_suf[STAGE ? STAGE_SLABS : 1];
   const int t = threadIdx.x;
   const int i = blockIdx.x;
   if (i >= L.n) return;
@@ -561,7 +568,16 @@ __global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
       if (e < 2) continue;
       int k;
       int64_t c;
-      sweep_axis(a == 0 ? spx : (a == 1 ? spy : spz), e, suf, sm, k, c);
+      const Span* sp = a == 0 ? spx : (a == 1 ? spy : spz);
+      if (STAGE && e <= STAGE_SLABS) {
+        // stage the axis' spans (coalesced) and keep the suffix boxes on chip
+        __syncthreads();
+        for (int s = t; s < e; s += DT) stage_sp[s] = sp[s];
+        __syncthreads();
+        sweep_axis(stage_sp, e, stage_suf, sm, k, c);
+      } else {
+        sweep_axis(sp, e, suf, sm, k, c);
+      }
       if (ba >= 0 && c >= bc) continue;
       ba = a; bk = k; bc = c;
     }
@@ -1309,8 +1325,15 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
                                                           pyz.as<uint32_t>(), spz.as<Span>());
         VS_TRY(check_launch("k_spans_z"));
       }
-      k_decide<<<(unsigned)n, DT, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(), spz.as<Span>(),
-                                   scr.as<RBox>(), B, dec.as<KdDecision>(), cnt.as<int64_t>());
+      // top levels (few, big nodes): spans staged in shared memory; wide levels: more blocks
+      if (n <= 512)
+        k_decide<true><<<(unsigned)n, DT, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(),
+                                                   spz.as<Span>(), scr.as<RBox>(), B,
+                                                   dec.as<KdDecision>(), cnt.as<int64_t>());
+      else
+        k_decide<false><<<(unsigned)n, DT, 0, st>>>(L, P, spx.as<Span>(), spy.as<Span>(),
+                                                    spz.as<Span>(), scr.as<RBox>(), B,
+                                                    dec.as<KdDecision>(), cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
     } else {
       if (level == 0) {
