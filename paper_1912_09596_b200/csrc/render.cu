@@ -714,7 +714,7 @@ static int g_trav_budget = 1, g_sample_budget = 1;
 // early ray termination (vs_set_render_ert): opacity threshold, 2.0 = off (parity mode)
 static thread_local double g_ert_a = 2.0;
 // bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float conversion)
-// bit2: generic k_segments for the LBVH brick DDA / grid (else k_segments_brick / _grid)
+// bit2: generic k_segments for the LBVH brick DDA / grid / hybrid (else the flat-loop kernels)
 static int g_render_opts = 1;
 
 template <int KIND>
@@ -1024,6 +1024,164 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
   if (flags) atomicOr(flags_out, flags);
 }
 
+// k_segments specialised for the hybrid (_k_hybrid: k-d leaf intervals -> _sort_merge -> for
+// each merged leaf interval _dda_runs over the macro grid -> _sort_merge), one flat loop whose
+// turn is either one k-d node visit or one grid DDA step; same steps and merges as the
+// generic generator stack (KdWalk, MergeState, GridDDA).
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
+    k_segments_hybrid(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
+                      double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
+                      int* __restrict__ flags_out) {
+  const int i = blockIdx.x * RENDER_TX + threadIdx.x;
+  const int l = blockIdx.y * RENDER_TY + threadIdx.y;
+  if (i >= cam.width || l >= rows.nrows) return;
+  const int64_t pix = (int64_t)l * cam.width + i;
+  const int64_t npix = (int64_t)rows.nrows * cam.width;
+  Ray r;
+  pixel_ray(cam, rows, i, l, r);
+  int n = 0, flags = 0;
+  double tmin, tmax;
+  if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+    KdWalk K;
+    K.init(ix, tmin, tmax);
+    Integrator L;  // lattice only
+    L.entry = tmin;
+    L.dt = dt;
+    L.inv_dt = 1.0 / dt;
+    // final merge + lattice-range emission
+    bool open = false;
+    double ma = 0.0, mb = 0.0, last_t0 = -DBL_MAX;
+    int kprev = -1;
+    auto emit = [&](double a, double b) {
+      const int k0 = (int)L.first_k(a), k1 = (int)L.first_k(b);
+      if (k1 <= k0) return;
+      if (n > 0 && k0 == kprev && n <= cap) {
+        segs[(int64_t)(n - 1) * npix + pix].y = k1;
+      } else {
+        if (n < cap) segs[(int64_t)n * npix + pix] = make_int2(k0, k1);
+        ++n;
+      }
+      kprev = k1;
+    };
+    auto feed = [&](double a, double b) {
+      if (a < last_t0) flags |= RF_ORDER;
+      last_t0 = a;
+      if (b <= a) return;
+      if (open && a <= mb) {
+        if (b > mb) mb = b;
+        return;
+      }
+      if (open) emit(ma, mb);
+      ma = a;
+      mb = b;
+      open = true;
+    };
+    // leaf-interval merge
+    bool lopen = false, kd_done = false;
+    double la = 0.0, lb = 0.0, llast = -DBL_MAX;
+    // grid walk over the current merged leaf interval [g_in, g_out)
+    bool gactive = false, run = false;
+    GridDDA G;
+    int gsteps = 0, gmax = 0;
+    double run_t0 = 0.0, tcur = 0.0, g_out = 0.0;
+    auto start_grid = [&](double a, double b) {
+      G.init(r, ix, a, b);
+      gactive = true;
+      run = false;
+      gsteps = 0;
+      gmax = (int)G.max_steps;
+      tcur = a;
+      g_out = b;
+    };
+    while (true) {
+      if (gactive) {
+        // one _dda_runs step (GridDDA::next)
+        bool fin = gsteps >= gmax;
+        if (!fin) {
+          double tn = G.tnx;
+          if (G.tny < tn) tn = G.tny;
+          if (G.tnz < tn) tn = G.tnz;
+          if (__ldg(G.occ + (G.cx * G.ncy + G.cy) * G.ncz + G.cz)) {
+            if (!run) { run = true; run_t0 = tcur; }
+          } else if (run) {
+            feed(run_t0, tcur);
+            run = false;
+          }
+          ++gsteps;
+          if (tn >= g_out) {
+            fin = true;
+          } else {
+            if (G.tnx == tn) { G.cx += G.sx; G.tnx = G.cross(G.cx, G.sx, r.ox, r.ix); }
+            if (G.tny == tn) { G.cy += G.sy; G.tny = G.cross(G.cy, G.sy, r.oy, r.iy); }
+            if (G.tnz == tn) { G.cz += G.sz; G.tnz = G.cross(G.cz, G.sz, r.oz, r.iz); }
+            tcur = tn;
+            if (G.cx < 0 || G.cy < 0 || G.cz < 0 || G.cx >= G.ncx || G.cy >= G.ncy ||
+                G.cz >= G.ncz)
+              fin = true;
+          }
+        }
+        if (fin) {
+          if (run) feed(run_t0, g_out);
+          gactive = false;
+        }
+        continue;
+      }
+      if (!kd_done) {
+        // one k-d node visit (KdWalk::next)
+        if (K.sp == 0) {
+          kd_done = true;
+          continue;
+        }
+        const int nd = K.stk[--K.sp];
+        double a, b;
+        if (!node_slab(r, K.lo, K.hi, nd, a, b)) continue;
+        a = a > tmin ? a : tmin;
+        b = b < tmax ? b : tmax;
+        if (b <= a) continue;
+        const int ax = __ldg(K.axis + nd);
+        if (ax < 0) {
+          // raw leaf interval -> leaf merge (MergeState::feed)
+          if (a < llast) flags |= RF_ORDER;
+          llast = a;
+          if (lopen && a <= lb) {
+            if (b > lb) lb = b;
+          } else {
+            const bool out = lopen;
+            const double oa = la, ob = lb;
+            la = a;
+            lb = b;
+            lopen = true;
+            if (out) start_grid(oa, ob);
+          }
+          continue;
+        }
+        const double pl = (double)__ldg(K.plane + nd);
+        bool front_left;
+        const bool zero = ax == 0 ? r.zx : (ax == 1 ? r.zy : r.zz);
+        if (zero)
+          front_left = (ax == 0 ? r.ox : (ax == 1 ? r.oy : r.oz)) < pl;
+        else
+          front_left = (ax == 0 ? r.ix : (ax == 1 ? r.iy : r.iz)) > 0.0;
+        const int lc = __ldg(K.left + nd), rc = __ldg(K.right + nd);
+        const int nr = front_left ? lc : rc, fr = front_left ? rc : lc;
+        if (K.sp + 2 > STACK_CAP) { flags |= RF_OVERFLOW; kd_done = true; continue; }
+        if (fr >= 0) K.stk[K.sp++] = fr;
+        if (nr >= 0) K.stk[K.sp++] = nr;
+        continue;
+      }
+      if (lopen) {  // drain the last merged leaf interval
+        lopen = false;
+        start_grid(la, lb);
+        continue;
+      }
+      break;
+    }
+    if (open) emit(ma, mb);
+  }
+  counts[pix] = n;
+  if (flags) atomicOr(flags_out, flags);
+}
+
 template <int KIND, bool IDX32, bool ERT>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
     k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
@@ -1276,6 +1434,9 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     else if (K == VS_KIND_GRID && !(g_render_opts & 4))
       k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                   counts, g_seg_cap, flags);
+    else if (K == VS_KIND_HYBRID && !(g_render_opts & 4))
+      k_segments_hybrid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
+                                                                    counts, g_seg_cap, flags);
     else
       k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                  counts, g_seg_cap, flags,
