@@ -1024,6 +1024,82 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
   if (flags) atomicOr(flags_out, flags);
 }
 
+// k_segments specialised for the k-d tree (_k_kd: _kd_leaves then _sort_merge): one node visit
+// per turn, the merge and lattice-range emission inline (same KdWalk / MergeState steps).
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
+    k_segments_kd(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
+                  double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
+                  int* __restrict__ flags_out) {
+  const int i = blockIdx.x * RENDER_TX + threadIdx.x;
+  const int l = blockIdx.y * RENDER_TY + threadIdx.y;
+  if (i >= cam.width || l >= rows.nrows) return;
+  const int64_t pix = (int64_t)l * cam.width + i;
+  const int64_t npix = (int64_t)rows.nrows * cam.width;
+  Ray r;
+  pixel_ray(cam, rows, i, l, r);
+  int n = 0, flags = 0;
+  double tmin, tmax;
+  if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+    KdWalk K;
+    K.init(ix, tmin, tmax);
+    Integrator L;  // lattice only
+    L.entry = tmin;
+    L.dt = dt;
+    L.inv_dt = 1.0 / dt;
+    bool open = false;
+    double ma = 0.0, mb = 0.0, last_t0 = -DBL_MAX;
+    int kprev = -1;
+    auto emit = [&](double a, double b) {
+      const int k0 = (int)L.first_k(a), k1 = (int)L.first_k(b);
+      if (k1 <= k0) return;
+      if (n > 0 && k0 == kprev && n <= cap) {
+        segs[(int64_t)(n - 1) * npix + pix].y = k1;
+      } else {
+        if (n < cap) segs[(int64_t)n * npix + pix] = make_int2(k0, k1);
+        ++n;
+      }
+      kprev = k1;
+    };
+    while (K.sp > 0) {
+      const int nd = K.stk[--K.sp];
+      double a, b;
+      if (!node_slab(r, K.lo, K.hi, nd, a, b)) continue;
+      a = a > tmin ? a : tmin;
+      b = b < tmax ? b : tmax;
+      if (b <= a) continue;
+      const int ax = __ldg(K.axis + nd);
+      if (ax < 0) {
+        if (a < last_t0) flags |= RF_ORDER;
+        last_t0 = a;
+        if (open && a <= mb) {
+          if (b > mb) mb = b;
+        } else {
+          if (open) emit(ma, mb);
+          ma = a;
+          mb = b;
+          open = true;
+        }
+        continue;
+      }
+      const double pl = (double)__ldg(K.plane + nd);
+      bool front_left;
+      const bool zero = ax == 0 ? r.zx : (ax == 1 ? r.zy : r.zz);
+      if (zero)
+        front_left = (ax == 0 ? r.ox : (ax == 1 ? r.oy : r.oz)) < pl;
+      else
+        front_left = (ax == 0 ? r.ix : (ax == 1 ? r.iy : r.iz)) > 0.0;
+      const int lc = __ldg(K.left + nd), rc = __ldg(K.right + nd);
+      const int nr = front_left ? lc : rc, fr = front_left ? rc : lc;
+      if (K.sp + 2 > STACK_CAP) { flags |= RF_OVERFLOW; break; }
+      if (fr >= 0) K.stk[K.sp++] = fr;
+      if (nr >= 0) K.stk[K.sp++] = nr;
+    }
+    if (open) emit(ma, mb);
+  }
+  counts[pix] = n;
+  if (flags) atomicOr(flags_out, flags);
+}
+
 // k_segments specialised for the hybrid (_k_hybrid: k-d leaf intervals -> _sort_merge -> for
 // each merged leaf interval _dda_runs over the macro grid -> _sort_merge), one flat loop whose
 // turn is either one k-d node visit or one grid DDA step; same steps and merges as the
@@ -1434,6 +1510,9 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     else if (K == VS_KIND_GRID && !(g_render_opts & 4))
       k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                   counts, g_seg_cap, flags);
+    else if (K == VS_KIND_KD && !(g_render_opts & 4))
+      k_segments_kd<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
+                                                                counts, g_seg_cap, flags);
     else if (K == VS_KIND_HYBRID && !(g_render_opts & 4))
       k_segments_hybrid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                     counts, g_seg_cap, flags);
