@@ -106,6 +106,29 @@ __device__ __forceinline__ int find_node(const int64_t* __restrict__ off, int n,
   return lo;
 }
 
+// A level's work items in one contiguous range per block; each warp walks its items in
+// increasing order (stride = warps per block) and finds an item's node by stepping forward
+// from the previous item's node, so only the first item pays the binary search.
+struct ItemWalker {
+  const int64_t* off;
+  int64_t it, end;
+  int node, step;
+  __device__ __forceinline__ ItemWalker(const int64_t* off_, int n, int64_t items) : off(off_) {
+    step = (int)(blockDim.x >> 5);
+    const int64_t chunk = (items + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = (int64_t)blockIdx.x * chunk;
+    end = min(items, b0 + chunk);
+    it = b0 + (threadIdx.x >> 5);
+    node = it < end ? find_node(off, n, it) : 0;
+  }
+  __device__ __forceinline__ bool valid() const { return it < end; }
+  __device__ __forceinline__ void advance() {
+    it += step;
+    if (it < end)
+      while (off[node + 1] <= it) ++node;
+  }
+};
+
 // Lanes per row: the smallest power of two >= the node's z word count.
 __device__ __forceinline__ int group_width(int wz) {
   return wz <= 1 ? 1 : 1 << (32 - __clz(wz - 1));
@@ -126,10 +149,9 @@ __global__ void __launch_bounds__(256) k_spans_rows(const uint32_t* __restrict__
                 AP = AX == 0 ? A_PXZ : A_PYZ;
   constexpr int U = 8;
   const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
-       it += (int64_t)gridDim.x * wpb) {
-    const int i = find_node(L.off[AI], L.n, it);
+  for (ItemWalker W(L.off[AI], L.n, items); W.valid(); W.advance()) {
+    const int64_t it = W.it;
+    const int i = W.node;
     const Box b = L.box[i];
     const int er = b.hi[1 - AX] - b.lo[1 - AX];
     const int nch = (er + SPAN_CHUNK - 1) / SPAN_CHUNK;
@@ -249,10 +271,9 @@ __global__ void __launch_bounds__(256) k_spans_z(KdLevel L, int64_t items,
                                                  const uint32_t* __restrict__ pyz,
                                                  Span* __restrict__ span_z) {
   const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
-       it += (int64_t)gridDim.x * wpb) {
-    const int i = find_node(L.off[A_IZ], L.n, it);
+  for (ItemWalker W(L.off[A_IZ], L.n, items); W.valid(); W.advance()) {
+    const int64_t it = W.it;
+    const int i = W.node;
     const Box b = L.box[i];
     const int wz = wz_of(b);
     const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
@@ -710,13 +731,12 @@ __global__ void __launch_bounds__(256) k_cell_slabs(const CBox* __restrict__ cel
                                                     int ncy, int ncz, int cs, int A, KdLevel L,
                                                     int64_t items, CBox* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
   const int nc[3] = {ncx, ncy, ncz};
   const int64_t* off = L.off[A_C0 + A];
   const int64_t* ioff = L.off[A_IC0 + A];
-  for (int64_t it = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); it < items;
-       it += (int64_t)gridDim.x * wpb) {
-    const int i = find_node(ioff, L.n, it);
+  for (ItemWalker W(ioff, L.n, items); W.valid(); W.advance()) {
+    const int64_t it = W.it;
+    const int i = W.node;
     const Box b = L.box[i];
     int c0[3], c1[3];
     for (int k = 0; k < 3; ++k) node_cell_range(b, cs, nc, k, c0[k], c1[k]);
