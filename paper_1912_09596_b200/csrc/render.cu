@@ -1258,22 +1258,93 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
   if (flags) atomicOr(flags_out, flags);
 }
 
-template <int KIND, bool IDX32, bool ERT>
-__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
-    k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
-                         const float* __restrict__ lut, const double* __restrict__ corr, double dt,
-                         int nearest, vs_rows_desc rows, const int2* __restrict__ segs,
-                         const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
-                         double* __restrict__ rgba64, int32_t* __restrict__ samples,
-                         unsigned long long* __restrict__ total, int* __restrict__ flags_out,
-                         int render_opts, double ert_a) {
-  __shared__ RenderSmem sm;
-  const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
-  for (int k = tid; k < 256; k += RENDER_TX * RENDER_TY) {
+// Output of one integrated ray (render_frame quantisation + optional float RGBA / samples).
+__device__ __forceinline__ void write_pixel(const Integrator& I, int64_t pix,
+                                            uint8_t* __restrict__ rgba8,
+                                            double* __restrict__ rgba64,
+                                            int32_t* __restrict__ samples) {
+  const double acc[4] = {I.accr, I.accg, I.accb, I.acca};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double q = floor(__dadd_rn(__dmul_rn(acc[c], 255.0), 0.5));
+    rgba8[4 * pix + c] = (uint8_t)(q < 0.0 ? 0 : (q > 255.0 ? 255 : (int)q));
+    if (rgba64) rgba64[4 * pix + c] = acc[c];
+  }
+  if (samples) samples[pix] = I.taken;
+}
+
+__device__ __forceinline__ void load_tables(RenderSmem& sm, const float* __restrict__ lut,
+                                            const double* __restrict__ corr, int tid, int nt) {
+  for (int k = tid; k < 256; k += nt) {
     sm.lut[k] = make_float4(lut[4 * k], lut[4 * k + 1], lut[4 * k + 2], lut[4 * k + 3]);
     sm.corr[k] = corr[k];
     sm.u8f[k] = (float)((double)k / 255.0);
   }
+}
+
+__device__ __forceinline__ void add_total(unsigned long long* total, int64_t taken, int tid) {
+  if (total) {
+    unsigned long long t = (unsigned long long)taken;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((tid & 31) == 0 && t) atomicAdd(total, t);
+  }
+}
+
+// A ray with more lattice ranges than the buffer holds: traversal and integration fused
+// (re-traverses the index).  Out of line, taking only values, so neither the sample loop's
+// register budget nor its locals depend on the traversal state.
+struct FusedOut {
+  double r, g, b, a;
+  int taken, flags;
+};
+
+template <int KIND, bool ERT>
+__device__ __noinline__ FusedOut integrate_fused(vs_volume_desc vol, vs_index_desc ix,
+                                                 vs_camera_desc cam, vs_rows_desc rows,
+                                                 const RenderSmem* sm, double dt, double ert_a,
+                                                 int i, int l) {
+  Ray r;
+  pixel_ray(cam, rows, i, l, r);
+  Integrator I;
+  I.r = &r; I.sm = sm; I.bins = vol.bins; I.field = nullptr; I.quads = vol.quads;
+  I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32); I.use_tab = true;
+  I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt;
+  I.nearest = false;
+  I.ert_a = ERT ? ert_a : 2.0;
+  I.accr = I.accg = I.accb = I.acca = 0.0;
+  I.taken = 0;
+  int flags = 0;
+  double tmin, tmax;
+  if (slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+    I.entry = tmin;
+    SegmentSource<KIND> src;
+    src.init(r, ix, vol.nx, vol.ny, vol.nz, tmin, tmax);
+    while (!I.terminated()) {
+      int budget = 1 << 30;
+      double a, b;
+      const int g = src.next(r, ix, a, b, budget, &flags);
+      if (g == 0) break;
+      I.segment(a, b);
+    }
+  }
+  return FusedOut{I.accr, I.accg, I.accb, I.acca, I.taken, flags};
+}
+
+// The hot integration kernel: u8 volumes through the quad gather volume, trilinear (float
+// fields and nearest sampling go to k_integrate_fallback).  Rays whose lattice ranges fit the
+// segment buffer run the sample-stream loop; the rare overflowing ray calls integrate_fused.
+template <int KIND, bool IDX32, bool ERT>
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
+    k_integrate_segments(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
+                         const float* __restrict__ lut, const double* __restrict__ corr,
+                         double dt, vs_rows_desc rows, const int2* __restrict__ segs,
+                         const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
+                         double* __restrict__ rgba64, int32_t* __restrict__ samples,
+                         unsigned long long* __restrict__ total, int* __restrict__ flags_out,
+                         double ert_a) {
+  __shared__ RenderSmem sm;
+  const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
+  load_tables(sm, lut, corr, tid, RENDER_TX * RENDER_TY);
   __syncthreads();
   const int i = blockIdx.x * RENDER_TX + threadIdx.x;
   const int l = blockIdx.y * RENDER_TY + threadIdx.y;
@@ -1282,25 +1353,25 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
   if (i < cam.width && l < rows.nrows) {
     const int64_t pix = (int64_t)l * cam.width + i;
     const int64_t npix = (int64_t)rows.nrows * cam.width;
-    Ray r;
-    pixel_ray(cam, rows, i, l, r);
-    Integrator I;
-    I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
-    I.quads = vol.field ? nullptr : vol.quads;
-    I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
-    I.use_tab = (render_opts & 1) != 0;
-    I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt; I.nearest = nearest != 0;
-    I.ert_a = ERT ? ert_a : 2.0;
-    I.accr = I.accg = I.accb = I.acca = 0.0;
-    I.taken = 0;
-    I.active = false;
     const int n = counts[pix];
-    double tmin, tmax;
-    if (n > 0 && slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
-      I.entry = tmin;
-      if (n <= cap && I.quads && !I.nearest) {
-        // flat sample loop, software-pipelined: the next sample's gather loads are issued
-        // before the current sample's interpolation and compositing
+    {
+      Ray r;
+      pixel_ray(cam, rows, i, l, r);
+      Integrator I;
+      I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = nullptr; I.quads = vol.quads;
+      I.idx32 = IDX32; I.use_tab = true;
+      I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt;
+      I.nearest = false;
+      I.ert_a = ERT ? ert_a : 2.0;
+      I.accr = I.accg = I.accb = I.acca = 0.0;
+      I.taken = 0;
+      double tmin, tmax;
+      if (n > cap) {
+        const FusedOut f = integrate_fused<KIND, ERT>(vol, ix, cam, rows, &sm, dt, ert_a, i, l);
+        I.accr = f.r; I.accg = f.g; I.accb = f.b; I.acca = f.a; I.taken = f.taken;
+        flags |= f.flags;
+      } else if (n > 0 && slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+        I.entry = tmin;
         // the ray's lattice ranges as one sample stream (ranges are non-empty): every turn
         // shades one sample, the next range is prefetched one range ahead, and the next
         // sample's gather is issued before the current sample's arithmetic, across range ends
@@ -1325,12 +1396,64 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
           }
           Integrator::Gather gn;
           if (hn) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)kn, dt)), gn);
-          I.shade(I.use_tab ? I.interp_t<true>(g) : I.interp_t<false>(g));
+          I.shade(I.interp_t<true>(g));
           if (!hn || (ERT && I.terminated())) break;
           k = kn;
           g = gn;
         }
-      } else if (n <= cap) {
+      }
+      taken = I.taken;
+      write_pixel(I, pix, rgba8, rgba64, samples);
+    }
+  }
+  if (flags) atomicOr(flags_out, flags);
+  add_total(total, taken, tid);
+}
+
+// Volumes k_integrate_segments does not take: float fields / no quad volume / nearest
+// sampling (generic sample path over the stored ranges, fused path for overflowing rays).
+template <int KIND, bool ERT>
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
+    k_integrate_fallback(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam,
+                         const float* __restrict__ lut, const double* __restrict__ corr, double dt,
+                         int nearest, vs_rows_desc rows, const int2* __restrict__ segs,
+                         const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
+                         double* __restrict__ rgba64, int32_t* __restrict__ samples,
+                         unsigned long long* __restrict__ total, int* __restrict__ flags_out,
+                         int render_opts, double ert_a) {
+  __shared__ RenderSmem sm;
+  const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
+  const bool generic = vol.field || !vol.quads || nearest;
+  const int i = blockIdx.x * RENDER_TX + threadIdx.x;
+  const int l = blockIdx.y * RENDER_TY + threadIdx.y;
+  const bool inside = i < cam.width && l < rows.nrows;
+  const int64_t pix = (int64_t)l * cam.width + i;
+  const int n = inside ? counts[pix] : 0;
+  const bool mine = inside && generic;
+  if (!__syncthreads_or(mine)) return;  // the common case: nothing to do in this tile
+  load_tables(sm, lut, corr, tid, RENDER_TX * RENDER_TY);
+  __syncthreads();
+  int64_t taken = 0;
+  int flags = 0;
+  if (mine) {
+    const int64_t npix = (int64_t)rows.nrows * cam.width;
+    Ray r;
+    pixel_ray(cam, rows, i, l, r);
+    Integrator I;
+    I.r = &r; I.sm = &sm; I.bins = vol.bins; I.field = vol.field;
+    I.quads = vol.field ? nullptr : vol.quads;
+    I.idx32 = (int64_t)vol.nx * vol.ny * vol.nz < (1LL << 32);
+    I.use_tab = (render_opts & 1) != 0;
+    I.nx = vol.nx; I.ny = vol.ny; I.nz = vol.nz; I.dt = dt; I.inv_dt = 1.0 / dt;
+    I.nearest = nearest != 0;
+    I.ert_a = ERT ? ert_a : 2.0;
+    I.accr = I.accg = I.accb = I.acca = 0.0;
+    I.taken = 0;
+    I.active = false;
+    double tmin, tmax;
+    if (n > 0 && slab(r, 0.0, 0.0, 0.0, (double)vol.nx, (double)vol.ny, (double)vol.nz, tmin, tmax)) {
+      I.entry = tmin;
+      if (n <= cap) {
         // flat sample loop: each turn either samples or switches to the next lattice range
         int q = 0;
         int2 kr = segs[pix];
@@ -1360,21 +1483,10 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
       }
     }
     taken = I.taken;
-    const double acc[4] = {I.accr, I.accg, I.accb, I.acca};
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double q = floor(__dadd_rn(__dmul_rn(acc[c], 255.0), 0.5));
-      rgba8[4 * pix + c] = (uint8_t)(q < 0.0 ? 0 : (q > 255.0 ? 255 : (int)q));
-      if (rgba64) rgba64[4 * pix + c] = acc[c];
-    }
-    if (samples) samples[pix] = (int32_t)taken;
+    write_pixel(I, pix, rgba8, rgba64, samples);
   }
   if (flags) atomicOr(flags_out, flags);
-  if (total) {
-    unsigned long long t = (unsigned long long)taken;
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if ((tid & 31) == 0 && t) atomicAdd(total, t);
-  }
+  add_total(total, taken, tid);
 }
 
 // Single-ray traversal (render.py:917-961): the merged interval list of each ray.
@@ -1521,16 +1633,27 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                                                                  counts, g_seg_cap, flags,
                                                                  g_trav_budget);
     const bool idx32 = (int64_t)v.nx * v.ny * v.nz < (1LL << 32), ert = g_ert_a <= 1.0;
+    const bool lean = !v.field && v.quads && !nearest;  // k_integrate_segments' rays exist
+    if (lean) {
 #define VS_INTEGRATE(I32, E)                                                                  \
   k_integrate_segments<K, I32, E><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(               \
-      v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples, \
-      total, flags, g_render_opts, g_ert_a)
-    if (idx32) {
-      if (ert) VS_INTEGRATE(true, true); else VS_INTEGRATE(true, false);
-    } else {
-      if (ert) VS_INTEGRATE(false, true); else VS_INTEGRATE(false, false);
-    }
+      v, ix, c, lut, corr, dt, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples, total,  \
+      flags, g_ert_a)
+      if (idx32) {
+        if (ert) VS_INTEGRATE(true, true); else VS_INTEGRATE(true, false);
+      } else {
+        if (ert) VS_INTEGRATE(false, true); else VS_INTEGRATE(false, false);
+      }
 #undef VS_INTEGRATE
+    }
+    else if (ert)
+      k_integrate_fallback<K, true><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64,
+          samples, total, flags, g_render_opts, g_ert_a);
+    else
+      k_integrate_fallback<K, false><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64,
+          samples, total, flags, g_render_opts, g_ert_a);
     return;
   }
   k_render<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
