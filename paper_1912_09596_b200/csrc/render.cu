@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
 // each merged leaf interval _dda_runs over the macro grid -> _sort_merge), one flat loop whose
 // turn is either one k-d node visit or one grid DDA step; same steps and merges as the
 // generic generator stack (KdWalk, MergeState, GridDDA).
-__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
+__global__ void __launch_bounds__(RENDER_TX* RENDER_TY, 6)
     k_segments_hybrid(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
                       double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
                       int* __restrict__ flags_out) {
