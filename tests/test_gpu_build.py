@@ -106,7 +106,7 @@ def _band_lut(lo, hi):
 
 
 @pytest.mark.parametrize("dims", [(48, 40, 64), (64, 64, 32), (33, 17, 48), (24, 24, 528),
-                                  (40, 70, 96)])
+                                  (40, 70, 96), (7, 33, 1024)])
 @pytest.mark.parametrize("tfkind", ["ramp", "ramp_lo", "band", "band_mid", "band_lo", "low", "lowhi",
                                     "twoband", "comb", "all", "none"])
 def test_random_volumes_vs_oracle(vs, rng, dims, tfkind):
