@@ -122,9 +122,14 @@ class TileRenderer:
         """Public API: a full Frame (host pixels) rendered by the whole group.
 
         Pixels, the renderer's flags and the sample total come back in one asynchronous copy
-        into pinned host memory and one stream synchronisation.  The Frame's pixel array IS the
-        pinned buffer; it is recycled for a later frame only once the caller has dropped every
-        reference to it (otherwise a fresh pinned buffer is allocated)."""
+        into pinned host memory.  The Frame's pixel array IS the pinned buffer; it is recycled
+        for a later frame only once the caller has dropped every reference to it (otherwise a
+        fresh pinned buffer is allocated)."""
+        return self.frame_async(v, tf, index, cam, dt).result()
+
+    def frame_async(self, v, tf, index, cam: Camera, dt: float = 0.5) -> "PendingFrame":
+        """Render now; the readback runs on a copy stream so the next frame's work can be
+        queued while this one travels to the host.  ``.result()`` waits and returns the Frame."""
         img = self.render(v, tf, index, cam, dt)
         total = self._last_total
         if self.world > 1:
@@ -133,23 +138,50 @@ class TileRenderer:
                 total = self.totals.sum().reshape(1)
             else:
                 total = torch.tensor([self.sample_total()], dtype=torch.int64, device=img.device)
+        slot = self._free_slot(img)
+        cur = torch.cuda.current_stream()
+        # device-side snapshot (the next render reuses frame_dev), then the D2H on the copy stream
+        slot["dev"].copy_(img)
+        slot["meta_dev"][0].copy_(self.target.flags.to(torch.int64).reshape(()))
+        slot["meta_dev"][1].copy_(total.reshape(()))
+        cs = self.__dict__.setdefault("_copy_stream", torch.cuda.Stream())
+        cs.wait_stream(cur)
+        with torch.cuda.stream(cs):
+            slot["t"].copy_(slot["dev"], non_blocking=True)
+            slot["meta"].copy_(slot["meta_dev"], non_blocking=True)
+            slot["done"].record(cs)
+        slot["busy"] = True
+        return PendingFrame(self, slot)
+
+    def _free_slot(self, img: torch.Tensor) -> dict:
         ring = self.__dict__.setdefault("_pinned_ring", [])
-        slot = None
         for s in ring:
-            # free when only the ring entry (and getrefcount's argument) refers to it
-            if sys.getrefcount(s["pixels"]) <= 2:
-                slot = s
-                break
-        if slot is None:
-            pix = torch.empty(img.shape, dtype=img.dtype).pin_memory()
-            slot = {"t": pix, "pixels": pix.numpy(),
-                    "meta": torch.empty(2, dtype=torch.int64).pin_memory()}
-            ring.append(slot)
-        slot["t"].copy_(img, non_blocking=True)
-        meta_dev = torch.cat([self.target.flags.to(torch.int64).reshape(1), total.reshape(1)])
-        slot["meta"].copy_(meta_dev, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        flags, samples = (int(x) for x in slot["meta"].tolist())
-        _check_flag_bits(flags)
-        return Frame(width=self.width, height=self.height, pixels=slot["pixels"],
-                     sample_count=samples)
+            # free when not pending and only the ring entry (and getrefcount's argument)
+            # refers to its pixel array
+            if not s["busy"] and sys.getrefcount(s["pixels"]) <= 2:
+                return s
+        pix = torch.empty(img.shape, dtype=img.dtype).pin_memory()
+        slot = {"t": pix, "pixels": pix.numpy(), "dev": torch.empty_like(img),
+                "meta": torch.empty(2, dtype=torch.int64).pin_memory(),
+                "meta_dev": torch.empty(2, dtype=torch.int64, device=img.device),
+                "done": torch.cuda.Event(), "busy": False}
+        ring.append(slot)
+        return slot
+
+
+class PendingFrame:
+    """A frame whose pixels are on their way to pinned host memory (TileRenderer.frame_async)."""
+
+    def __init__(self, tr: TileRenderer, slot: dict):
+        self._tr, self._slot, self._frame = tr, slot, None
+
+    def result(self) -> Frame:
+        if self._frame is None:
+            s = self._slot
+            s["done"].synchronize()
+            flags, samples = (int(x) for x in s["meta"].tolist())
+            s["busy"] = False
+            _check_flag_bits(flags)
+            self._frame = Frame(width=self._tr.width, height=self._tr.height,
+                                pixels=s["pixels"], sample_count=samples)
+        return self._frame

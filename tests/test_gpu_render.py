@@ -354,6 +354,13 @@ def test_tile_frame_pinned_buffers(vs, blobs64):
     f2 = tr.frame(v, tfs[0], idx0, cam)                       # reuses the dropped buffer
     assert len(tr._pinned_ring) == 2
     np.testing.assert_array_equal(f2.pixels, refs[0].pixels)
+    # pipelined readback: frame k+1 is queued before frame k is collected
+    p0 = tr.frame_async(v, tfs[1], idx1, cam)
+    p1 = tr.frame_async(v, tfs[0], idx0, cam)
+    g0, g1 = p0.result(), p1.result()
+    np.testing.assert_array_equal(g0.pixels, refs[1].pixels)
+    np.testing.assert_array_equal(g1.pixels, refs[0].pixels)
+    assert (g0.sample_count, g1.sample_count) == (refs[1].sample_count, refs[0].sample_count)
 
 
 @pytest.mark.parametrize("kind", ["lbvh", "grid"])
