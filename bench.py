@@ -520,15 +520,25 @@ def run_multi(args, rank, ws, local):
     for tl in tfs:
         for tf in tl:
             tf_device(tf, 0.5)
-    rb = LbvhRebuilder(vols).capture()
-    idx = rb.index()
+    # two index buffers: frame k+1's union rebuild (side stream) overlaps frame k's render
+    rbs = [LbvhRebuilder(vols).capture(), LbvhRebuilder(vols).capture()]
+    idxs = [r.index() for r in rbs]
     tiles = TileRenderer(W, H)
     st = torch.cuda.current_stream()
+    sb = torch.cuda.Stream()
+    built = [torch.cuda.Event(), torch.cuda.Event()]
+    rendered = [torch.cuda.Event(), torch.cuda.Event()]
 
     def step(k):
-        j = k % NSWEEP
-        rb.rebuild(params[j])
-        return tiles.render_multi(vols, tfs[j], idx, cams[j])
+        j, b = k % NSWEEP, k % 2
+        with torch.cuda.stream(sb):
+            sb.wait_event(rendered[b])
+            rbs[b].rebuild(params[j])
+            built[b].record(sb)
+        st.wait_event(built[b])
+        img = tiles.render_multi(vols, tfs[j], idxs[b], cams[j], checked=False)
+        rendered[b].record(st)
+        return img
 
     for k in range(args.warmup):
         step(k)
@@ -539,11 +549,16 @@ def run_multi(args, rank, ws, local):
         torch.cuda.synchronize()
         barrier(ws)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tiles.multi_flags()
         e0.record(st)
+        sb.wait_stream(st)
         for k in range(args.steps):
             step(k)
+        st.wait_stream(sb)
         e1.record(st)
         torch.cuda.synchronize()
+    if tiles.multi_flags() & 4:
+        raise RuntimeError("a timed frame exceeded the segment capacity (incomplete frame)")
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
     samples = tiles.sample_total()
     # e2e through the public API: per-step host LUTs -> classify_multi -> build_index -> frame

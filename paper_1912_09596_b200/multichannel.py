@@ -114,8 +114,11 @@ def interleaved_quads(volumes) -> torch.Tensor:
     return q
 
 
+RF_SEGCAP = 4  # a ray had more lattice ranges than the target's segment capacity
+
+
 class MultiTarget:
-    def __init__(self, width: int, nrows: int, cap: int = 32, want_rgba64=False,
+    def __init__(self, width: int, nrows: int, cap: int = 64, want_rgba64=False,
                  want_samples=False):
         dev = _lib.device()
         self.width, self.nrows, self.cap = width, nrows, cap
@@ -131,9 +134,13 @@ class MultiTarget:
 
 
 def render_multi_rows(volumes, tfs, index, cam: Camera, target: MultiTarget, dt: float = 0.5,
-                      rows: RowsDesc | None = None, grow: bool = True):
-    target.total.zero_()
-    target.flags.zero_()
+                      rows: RowsDesc | None = None, zero: bool = True):
+    """Launch the multi-channel render into ``target`` (async, no host synchronisation).  A ray
+    with more lattice ranges than ``target.cap`` sets RF_SEGCAP in ``target.flags`` and is left
+    unintegrated; render_multi_checked re-renders with a larger capacity."""
+    if zero:
+        target.total.zero_()
+        target.flags.zero_()
     md = MultiDesc()
     md.nch = len(volumes)
     md.nx, md.ny, md.nz = volumes[0].dims
@@ -150,19 +157,25 @@ def render_multi_rows(volumes, tfs, index, cam: Camera, target: MultiTarget, dt:
     rp = None if rows is None else C.addressof(rows)
     call("vs_render_segments", C.addressof(vd), C.addressof(idx), C.addressof(cd), float(dt), rp,
          ptr(target.segs), ptr(target.counts), target.cap, ptr(target.flags), stream())
-    need = int(target.counts.max().item()) if target.counts.numel() else 0
-    if need > target.cap:
-        if not grow:
-            raise RuntimeError("segment capacity exceeded")
-        fresh = MultiTarget(target.width, target.nrows, cap=need,
-                            want_rgba64=target.rgba64 is not None,
-                            want_samples=target.samples is not None)
-        target.__dict__.update(fresh.__dict__)
-        return render_multi_rows(volumes, tfs, index, cam, target, dt, rows, grow=False)
     call("vs_render_multi_integrate", C.addressof(md), C.addressof(cd), float(dt), rp,
          ptr(target.segs), ptr(target.counts), target.cap, ptr(target.rgba8), ptr(target.rgba64),
          ptr(target.samples), ptr(target.total), ptr(target.flags), stream())
     del keep
+
+
+def render_multi_checked(volumes, tfs, index, cam: Camera, target: MultiTarget, dt: float = 0.5,
+                         rows: RowsDesc | None = None) -> MultiTarget:
+    """render_multi_rows + the capacity check (one synchronisation); on overflow the target
+    grows to the frame's largest range count and the frame is rendered again."""
+    render_multi_rows(volumes, tfs, index, cam, target, dt, rows)
+    if int(target.flags.item()) & RF_SEGCAP:
+        need = int(target.counts.max().item())
+        fresh = MultiTarget(target.width, target.nrows, cap=need,
+                            want_rgba64=target.rgba64 is not None,
+                            want_samples=target.samples is not None)
+        target.__dict__.update(fresh.__dict__)
+        render_multi_rows(volumes, tfs, index, cam, target, dt, rows)
+    return target
 
 
 def render_frame_multi(volumes, tfs, index, cam: Camera, dt: float = 0.5) -> Frame:
@@ -170,7 +183,7 @@ def render_frame_multi(volumes, tfs, index, cam: Camera, dt: float = 0.5) -> Fra
     if dt <= 0:
         raise ValueError("dt must be positive")
     tgt = MultiTarget(cam.width, cam.height)
-    render_multi_rows(volumes, tfs, index, cam, tgt, dt)
+    render_multi_checked(volumes, tfs, index, cam, tgt, dt)
     _check_flags(tgt.flags)
     return Frame(width=cam.width, height=cam.height, pixels=tgt.rgba8.cpu().numpy(),
                  sample_count=int(tgt.total.item()))
@@ -178,6 +191,6 @@ def render_frame_multi(volumes, tfs, index, cam: Camera, dt: float = 0.5) -> Fra
 
 def render_float_multi(volumes, tfs, index, cam: Camera, dt: float = 0.5):
     tgt = MultiTarget(cam.width, cam.height, want_rgba64=True, want_samples=True)
-    render_multi_rows(volumes, tfs, index, cam, tgt, dt)
+    render_multi_checked(volumes, tfs, index, cam, tgt, dt)
     _check_flags(tgt.flags)
     return tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy().astype(np.int64)

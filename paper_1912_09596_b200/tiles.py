@@ -91,21 +91,37 @@ class TileRenderer:
             dist.all_gather_into_tensor(host, local.cpu(), group=self.group)
             self.gathered.copy_(host)
 
-    def render_multi(self, volumes, tfs, index, cam: Camera, dt: float = 0.5) -> torch.Tensor:
-        """Multi-channel frame (multichannel.py), same stripe split and gather."""
-        from .multichannel import MultiTarget, render_multi_rows
+    def render_multi(self, volumes, tfs, index, cam: Camera, dt: float = 0.5,
+                     checked: bool = True) -> torch.Tensor:
+        """Multi-channel frame (multichannel.py), same stripe split and gather.  ``checked``
+        verifies the segment capacity (one synchronisation, re-render on overflow); unchecked
+        frames queue without a host sync and accumulate RF_SEGCAP in ``multi_flags()``."""
+        from .multichannel import MultiTarget, render_multi_checked, render_multi_rows
 
         mt = self.__dict__.get("_multi_target")
         if mt is None:
             mt = MultiTarget(self.width, self.maxrows)
             self._multi_target = mt
-        render_multi_rows(volumes, tfs, index, cam, mt, dt, rows=self.rows_desc)
+        if checked:
+            render_multi_checked(volumes, tfs, index, cam, mt, dt, rows=self.rows_desc)
+        else:
+            mt.total.zero_()
+            render_multi_rows(volumes, tfs, index, cam, mt, dt, rows=self.rows_desc, zero=False)
         self._last_total = mt.total
         if self.world == 1:
             self.frame_dev.copy_(mt.rgba8[: self.height])
             return self.frame_dev
         self._gather(mt.rgba8)
         return assemble(self.gathered, self.perm, self.frame_dev)
+
+    def multi_flags(self) -> int:
+        """Renderer flags accumulated by unchecked multi-channel frames since the last read."""
+        mt = self.__dict__.get("_multi_target")
+        if mt is None:
+            return 0
+        f = int(mt.flags.item())
+        mt.flags.zero_()
+        return f
 
     def sample_total(self) -> int:
         t = self.__dict__.get("_last_total", self.target.total)
