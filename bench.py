@@ -414,6 +414,28 @@ def run_ours(args, rank, ws, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
     del fr, pending
 
+    # ---- the other hierarchies' TF-change rebuilds (north star: "the same rebuild is also
+    # reported for the SVT k-d tree, binned k-d tree and hybrid grid"): public API, classify +
+    # build_index, synchronised, median of 3 after one warm-up, sparse / medium / dense ramp
+    rebuilds = {}
+    for kind in ("lbvh", "grid", "hybrid", "kd-shallow", "kd-binned-mls32"):
+        per_t = []
+        for t in (0.6, 0.3, 0.0):
+            tfk = vs.TransferFunction.ramp(t)
+            times = []
+            for r in range(4):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ix = vs.build_index(kind, vs.classify(v, tfk, dilate=True))
+                vs.report_stats(ix)
+                torch.cuda.synchronize()
+                if r:
+                    times.append((time.perf_counter() - t0) * 1e3)
+            per_t.append(round(statistics.median(times), 3))
+        rebuilds[kind] = per_t
+        del ix
+    torch.cuda.empty_cache()
+
     # ---- roofline of the HBM-bound kernel -------------------------------------------------
     peak, peak_kind = hbm_peak()
     alg = rb.algorithmic_bytes(n_bricks)
@@ -472,6 +494,9 @@ def run_ours(args, rank, ws, local):
                      "alg_bytes_per_launch": alg["summary_kernel"],
                      "share_of_step": summ_ms / ms_per_step},
         "rebuild_roofline_frac": alg["rebuild"] / (build_ms * 1e-3) / 1e9 / peak,
+        "rebuild_ms_by_kind": {"ramp_t": [0.6, 0.3, 0.0], **rebuilds,
+                               "how": "public API classify+build_index, host-synchronised "
+                                      "wall time, median of 3"},
         "e2e": {"value": 1e3 / e2e_ms, "unit": "frames/s",
                 "h2d_bytes_per_step": 64 + 4096 + 2048, "d2h_bytes_per_step": W * H * 4 + 16,
                 "ms_per_step": e2e_ms,
