@@ -514,7 +514,12 @@ struct BinnedCtx {
   const CBox* cslab[3];      // per-level cell-slab unions, per axis
   const int64_t* coff[3];    // per-node offsets into cslab
   int nc[3];
+  const CBox* cells;         // per-cell tight boxes, C order (small nodes reduce these directly)
 };
+
+// Nodes with at most this many cells skip the per-level cell-slab unions: their region
+// unions are reduced straight from the cell boxes by the deciding warp.
+constexpr int SMALL_CELLS = 64;
 
 __device__ __forceinline__ void node_cell_range(const Box& b, int cs, const int* nc, int a,
                                                 int& c0, int& c1) {
@@ -533,6 +538,41 @@ __device__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a, 
   for (int k = 0; k < 3; ++k) {
     int r0 = max(region.lo[k] / cs, 0), r1 = min((region.hi[k] - 1) / cs, B.nc[k] - 1);
     if (r0 > r1) return false;
+  }
+  // the node's cell range per axis (scalars: no dynamically indexed local arrays)
+  int x0, x1, y0, y1, z0, z1;
+  node_cell_range(node, cs, B.nc, 0, x0, x1);
+  node_cell_range(node, cs, B.nc, 1, y0, y1);
+  node_cell_range(node, cs, B.nc, 2, z0, z1);
+  if ((x1 - x0 + 1) * (y1 - y0 + 1) * (z1 - z0 + 1) <= SMALL_CELLS) {
+    // direct: the node's cells with coordinate along a in [c0, c1] (other axes: the node's
+    // cell range, which is the region's), unioned, clipped to the region
+    const int s0 = max(c0, n0), s1 = min(c1, n1);
+    if (a == 0) { x0 = s0; x1 = s1; } else if (a == 1) { y0 = s0; y1 = s1; } else { z0 = s0; z1 = s1; }
+    int ulo0 = KD_FAR, ulo1 = KD_FAR, ulo2 = KD_FAR, uhi0 = -1, uhi1 = -1, uhi2 = -1;
+    const int e1 = y1 - y0 + 1, e2 = z1 - z0 + 1;
+    const int cnt = s1 < s0 ? 0 : (x1 - x0 + 1) * e1 * e2;
+    for (int q = lane; q < cnt; q += 32) {
+      const int cx = x0 + q / (e1 * e2), cy = y0 + (q / e2) % e1, cz = z0 + q % e2;
+      const CBox v = B.cells[((int64_t)cx * B.nc[1] + cy) * B.nc[2] + cz];
+      if (v.lo[0] != KD_FAR) {
+        ulo0 = min(ulo0, v.lo[0]); ulo1 = min(ulo1, v.lo[1]); ulo2 = min(ulo2, v.lo[2]);
+        uhi0 = max(uhi0, v.hi[0]); uhi1 = max(uhi1, v.hi[1]); uhi2 = max(uhi2, v.hi[2]);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      ulo0 = min(ulo0, __shfl_xor_sync(0xffffffffu, ulo0, o));
+      ulo1 = min(ulo1, __shfl_xor_sync(0xffffffffu, ulo1, o));
+      ulo2 = min(ulo2, __shfl_xor_sync(0xffffffffu, ulo2, o));
+      uhi0 = max(uhi0, __shfl_xor_sync(0xffffffffu, uhi0, o));
+      uhi1 = max(uhi1, __shfl_xor_sync(0xffffffffu, uhi1, o));
+      uhi2 = max(uhi2, __shfl_xor_sync(0xffffffffu, uhi2, o));
+    }
+    if (ulo0 == KD_FAR) return false;
+    out.lo[0] = max(ulo0, region.lo[0]); out.hi[0] = min(uhi0, region.hi[0]);
+    out.lo[1] = max(ulo1, region.lo[1]); out.hi[1] = min(uhi1, region.hi[1]);
+    out.lo[2] = max(ulo2, region.lo[2]); out.hi[2] = min(uhi2, region.hi[2]);
+    return out.lo[0] < out.hi[0] && out.lo[1] < out.hi[1] && out.lo[2] < out.hi[2];
   }
   return cells_reduce_axis(B.cslab[a] + B.coff[a][i], n0, max(c0, n0), min(c1, n1), region,
                            lane, out);
@@ -821,11 +861,13 @@ __device__ __forceinline__ void prep_node(const PrepCtx& C, const Box& b, int64_
       node_cell_range(b, P.cs, C.nc, a, c0, c1);
       n[a] = c1 - c0 + 1;
     }
-    for (int a = 0; a < 3; ++a) {
-      int o1, o2;
-      others(a, o1, o2);
-      v[A_C0 + a] = n[a];
-      v[A_IC0 + a] = (int64_t)n[a] * ((n[o1] * n[o2] + CELL_CHUNK - 1) / CELL_CHUNK);
+    if (n[0] * n[1] * n[2] > SMALL_CELLS) {  // small nodes reduce their cells directly
+      for (int a = 0; a < 3; ++a) {
+        int o1, o2;
+        others(a, o1, o2);
+        v[A_C0 + a] = n[a];
+        v[A_IC0 + a] = (int64_t)n[a] * ((n[o1] * n[o2] + CELL_CHUNK - 1) / CELL_CHUNK);
+      }
     }
   }
   for (int k = 0; k < KA; ++k) C.arr[k][i] = v[k];
@@ -1363,6 +1405,7 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
                                                                  ncz, cellb.as<CBox>());
         VS_TRY(check_launch("k_cell_boxes"));
       }
+      B.cells = cellb.as<CBox>();
       const int64_t t0 = tot[A_C0], t1 = tot[A_C1], t2 = tot[A_C2];
       VS_TRY(cslab.ensure((t0 + t1 + t2 + 3) * sizeof(CBox), "cell slabs"));
       CBox* cbase = cslab.as<CBox>();
@@ -1687,6 +1730,7 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
     VS_TRY(cellb.ensure(ncell * sizeof(CBox), "cells"));
     k_cell_boxes<<<(unsigned)cdiv(ncell, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy, ncz,
                                                              cellb.as<CBox>());
+    B.cells = cellb.as<CBox>();
     VS_TRY(cslab.ensure((csz[0] + csz[1] + csz[2] + 3) * sizeof(CBox), "cell slabs"));
     CBox* cs3[3] = {cslab.as<CBox>(), cslab.as<CBox>() + csz[0] + 1,
                     cslab.as<CBox>() + csz[0] + csz[1] + 2};
