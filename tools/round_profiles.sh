@@ -4,7 +4,10 @@
 #   launches_*.csv     ncu launch lists (gpu__time_duration.sum, cold + serialised)
 #   *.ncu-rep          ncu --set full captures of the kernels named in DESIGN.md
 set -x
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 python bench.py --channels 4 > gpurun_out/bench_mc4.json 2> gpurun_out/bench_mc4.err
 timeout 900 python tools/bench_configs.py > gpurun_out/configs.json 2> gpurun_out/configs.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
