@@ -317,7 +317,7 @@ __global__ void k_classify_bits(const uint8_t* __restrict__ vol, int nx, int ny,
 // with lane shuffles, y-dilate through shared memory, x-dilate with a 3-slab register ring.
 // The next slab's loads are issued before the current slab is processed.
 // ---------------------------------------------------------------------------------------
-constexpr int CP_TY = 30, CP_XC = 32;
+constexpr int CP_TY = 14, CP_XC = 64;
 
 template <int V>
 __device__ __forceinline__ uint32_t classify_word(const VisEval& ve, const uint4& a,
