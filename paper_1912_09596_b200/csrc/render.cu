@@ -715,6 +715,7 @@ static int g_trav_budget = 1, g_sample_budget = 1;
 static thread_local double g_ert_a = 2.0;
 // bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float conversion)
 // bit2: generic k_segments for the LBVH brick DDA / grid / hybrid (else the flat-loop kernels)
+// bit4: k_segments_brick evaluates every occupied brick's slab (no run shortcut)
 static int g_render_opts = 1;
 
 template <int KIND>
@@ -863,7 +864,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
     k_segments_brick(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
                      double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
-                     int* __restrict__ flags_out) {
+                     int* __restrict__ flags_out, int exact_runs) {
   const int i = blockIdx.x * RENDER_TX + threadIdx.x;
   const int l = blockIdx.y * RENDER_TY + threadIdx.y;
   if (i >= cam.width || l >= rows.nrows) return;
@@ -901,12 +902,20 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
       kprev = k1;
     };
     bool done = D.done;
+    // Run shortcut: inside a run of occupied interior bricks (box hi not clipped to dims) a
+    // brick's clipped slab interval is [previous crossing, next crossing] -- slab() evaluates
+    // the very plane expressions the DDA's crossings use -- so the merged run just extends to
+    // min(next crossing, tmax) and the brick's slab() is skipped (exact_runs: always slab()).
+    bool live = false;
     while (!done) {
       if (steps++ >= maxsteps) break;
       const int lin = (D.c[0] * nby + D.c[1]) * nbz + D.c[2];
-      if ((__ldg(bits + (lin >> 5)) >> (lin & 31)) & 1u) {
+      const bool occ = (__ldg(bits + (lin >> 5)) >> (lin & 31)) & 1u;
+      const int l0 = D.c[0] * bs, l1 = D.c[1] * bs, l2 = D.c[2] * bs;
+      const bool interior = l0 + bs <= D.dims[0] && l1 + bs <= D.dims[1] && l2 + bs <= D.dims[2];
+      const bool shortcut = occ && live && interior && !exact_runs;
+      if (occ && !shortcut) {
         double a, b;
-        const int l0 = D.c[0] * bs, l1 = D.c[1] * bs, l2 = D.c[2] * bs;
         if (slab(r, (double)l0, (double)l1, (double)l2, (double)min(l0 + bs, D.dims[0]),
                  (double)min(l1 + bs, D.dims[1]), (double)min(l2 + bs, D.dims[2]), a, b)) {
           a = a > tmin ? a : tmin;
@@ -928,6 +937,8 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
       double tt = D.tn[0];
       if (D.tn[1] < tt) tt = D.tn[1];
       if (D.tn[2] < tt) tt = D.tn[2];
+      if (shortcut) mb = tt < tmax ? tt : tmax;
+      live = occ && interior && open && mb == tt;
       if (tt >= tmax) break;
 #pragma unroll
       for (int a2 = 0; a2 < 3; ++a2) {
@@ -1617,8 +1628,8 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     int2* segs = static_cast<int2*>(g_seg_ws);
     int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
     if (K == KIND_LBVH_BRICK && !(g_render_opts & 4))
-      k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                   counts, g_seg_cap, flags);
+      k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+          v, ix, c, rows, dt, segs, counts, g_seg_cap, flags, (g_render_opts & 16) ? 1 : 0);
     else if (K == VS_KIND_GRID && !(g_render_opts & 4))
       k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                   counts, g_seg_cap, flags);

@@ -415,3 +415,31 @@ def test_early_ray_termination_bound(vs, blobs64, kind, seg_cap):
         rgba, s = outs[eps]
         assert float(np.max(np.abs(rgba - full))) <= eps
         assert np.all(s <= fs) and int(s.sum()) < int(fs.sum())
+
+
+@pytest.mark.parametrize("dims", [(100, 90, 70), (64, 64, 64)])
+def test_brick_run_shortcut_equals_per_brick_slab(vs, dims):
+    """k_segments_brick's run shortcut (occupied interior bricks extend the merged run to the
+    next crossing) == every brick through slab() == the generic generator kernel, at odd dims
+    (clipped border bricks) and several views."""
+    from paper_1912_09596_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    u8 = (rng.random(dims) * 255).astype(np.uint8)
+    u8[rng.random(dims) < 0.7] = 0
+    v = vs.Volume(u8)
+    tf = vs.TransferFunction.ramp(0.5)
+    idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
+    lib = _lib.lib()
+    try:
+        for az, el in ((30.0, 15.0), (0.0, 0.0), (90.0, 45.0), (211.0, -33.0)):
+            cam = vs.Camera.orbit(v.dims, az, el, width=120, height=96)
+            outs = []
+            for opts in (1, 1 | 16, 1 | 4):
+                lib.vs_set_render_options(opts)
+                outs.append(vs.render_float(v, tf, idx, cam))
+            for o in outs[1:]:
+                np.testing.assert_array_equal(o[1], outs[0][1])
+                np.testing.assert_array_equal(o[0], outs[0][0])
+    finally:
+        lib.vs_set_render_options(1)
