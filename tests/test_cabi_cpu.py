@@ -100,3 +100,32 @@ def test_morton_side(lib):
 def test_version(lib):
     lib.vs_version.restype = C.c_char_p
     assert b"sm_100a" in lib.vs_version()
+
+
+def _last_error(lib) -> str:
+    buf = C.create_string_buffer(512)
+    lib.vs_last_error(buf, C.c_size_t(512))
+    return buf.value.decode()
+
+
+def test_argument_errors_without_gpu(lib):
+    """The status convention (include/vsb200.h): argument errors return a negative status and
+    name the entry point in vs_last_error, before any device work (so they run on CPU)."""
+    dummy = C.c_void_p(0x1000)  # never dereferenced: validation fails first
+    i = C.c_int
+    cases = [
+        ("vs_classify_bits", lambda: lib.vs_classify_bits(None, i(8), i(8), i(8), None, None, None, None)),
+        ("vs_classify_dilate_bits", lambda: lib.vs_classify_dilate_bits(
+            dummy, i(8), i(8), i(33), dummy, dummy, None, None)),
+        ("vs_dilate_bits", lambda: lib.vs_dilate_bits(dummy, i(4), i(4), i(4), dummy, None)),
+        ("vs_kd_build", lambda: lib.vs_kd_build(None, i(8), i(8), i(8), i(0), i(-1), i(0), i(4),
+                                                i(8), None, None)),
+        ("vs_build_mquads", lambda: lib.vs_build_mquads(dummy, i(5), i(8), i(8), i(8), dummy, None)),
+        ("vs_render", lambda: lib.vs_render(None, None, None, None, None, C.c_double(0.5), i(0),
+                                            None, None, None, None, None, None, None,
+                                            C.c_size_t(0), i(0), None)),
+    ]
+    for name, fn in cases:
+        st = fn()
+        assert st < 0, (name, st)
+        assert name in _last_error(lib), (name, _last_error(lib))
