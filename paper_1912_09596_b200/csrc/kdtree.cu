@@ -1255,6 +1255,35 @@ int d2h(void* dst, const void* src, size_t n, cudaStream_t st) {
 
 constexpr int SPAN_BLOCKS = 148 * 8;
 
+// A non-blocking side stream per device for independent passes (created once).
+cudaStream_t side_stream(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  streams[dev] = s;
+  return s;
+}
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int create() {
+    VS_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+    VS_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
+    return 0;
+  }
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
 unsigned grid_for(int64_t items, int per_block, int cap = 148 * 64) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(items, per_block), cap));
 }
@@ -1288,6 +1317,14 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
   KdParams P;
   P.deep = deep; P.mls = mls; P.binned = binned; P.bins = bins; P.cs = cs; P.root_vol = 0;
   const int ncx = (int)cdiv(nx, cs), ncy = (int)cdiv(ny, cs), ncz = (int)cdiv(nz, cs);
+  // side stream (per device, cached) + fork/join events for the concurrent span passes
+  int dev = 0;
+  VS_CUDA(cudaGetDevice(&dev), "device");
+  cudaStream_t side = side_stream(dev);
+  if (!side) { set_error("vs_kd_build: side stream"); return VS_EINVAL; }
+  EventPair evs;
+  VS_TRY(evs.create());
+  cudaEvent_t ev_fork = evs.a, ev_join = evs.b;
 
   // header: [0] node count of the level being prepared, [1 + k] total of offset array k,
   // [KA + 1] child total (next level's node count), [KA + 2 ..] root bbox ints
@@ -1377,12 +1414,18 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
               pxz.as<uint32_t>(), tot[A_PXZ], pyz.as<uint32_t>(), tot[A_PYZ]);
           VS_TRY(check_launch("k_span_init"));
         }
+        // the x and y passes are independent: the y pass runs on a side stream concurrently
+        VS_CUDA(cudaEventRecord(ev_fork, st), "fork");
+        VS_CUDA(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
+        k_spans_rows<1><<<grid_for(tot[A_IY], 8), 256, 0, side>>>(bits, ny, nzw, L, tot[A_IY],
+                                                                  spy.as<Span>(),
+                                                                  pyz.as<uint32_t>());
+        VS_TRY(check_launch("k_spans_rows<y>"));
+        VS_CUDA(cudaEventRecord(ev_join, side), "join");
         k_spans_rows<0><<<grid_for(tot[A_IX], 8), 256, 0, st>>>(bits, ny, nzw, L, tot[A_IX],
                                                                 spx.as<Span>(), pxz.as<uint32_t>());
         VS_TRY(check_launch("k_spans_rows<x>"));
-        k_spans_rows<1><<<grid_for(tot[A_IY], 8), 256, 0, st>>>(bits, ny, nzw, L, tot[A_IY],
-                                                                spy.as<Span>(), pyz.as<uint32_t>());
-        VS_TRY(check_launch("k_spans_rows<y>"));
+        VS_CUDA(cudaStreamWaitEvent(st, ev_join, 0), "join wait");
         k_spans_z<<<grid_for(tot[A_IZ], 8), 256, 0, st>>>(L, tot[A_IZ], pxz.as<uint32_t>(),
                                                           pyz.as<uint32_t>(), spz.as<Span>());
         VS_TRY(check_launch("k_spans_z"));
@@ -1414,14 +1457,20 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
         k_cbox_init<<<grid_for(t0 + t1 + t2 + 3, 256), 256, 0, st>>>(cbase, t0 + t1 + t2 + 3);
         VS_TRY(check_launch("k_cbox_init"));
       }
+      // the three axes' cell-slab passes are independent: y and z on the side stream
+      VS_CUDA(cudaEventRecord(ev_fork, st), "fork");
+      VS_CUDA(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
       for (int a = 0; a < 3; ++a) {
         const int64_t items = tot[A_IC0 + a];
-        k_cell_slabs<<<grid_for(items, 8), 256, 0, st>>>(cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L,
-                                                         items, cs3[a]);
+        if (items > 0)
+          k_cell_slabs<<<grid_for(items, 8), 256, 0, a == 0 ? st : side>>>(
+              cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L, items, cs3[a]);
         VS_TRY(check_launch("k_cell_slabs"));
         B.cslab[a] = cs3[a];
         B.coff[a] = L.off[A_C0 + a];
       }
+      VS_CUDA(cudaEventRecord(ev_join, side), "join");
+      VS_CUDA(cudaStreamWaitEvent(st, ev_join, 0), "join wait");
       k_decide_binned<<<(unsigned)cdiv(n, 4), 128, 0, st>>>(L, P, B, dec.as<KdDecision>(),
                                                             cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
