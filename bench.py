@@ -592,16 +592,21 @@ def run_multi(args, rank, ws, local):
     torch.cuda.synchronize()
     barrier(ws)
     e0.record(st)
-    for k in range(e_steps):
+    pending = None
+    for k in range(e_steps):  # frame k's readback overlaps frame k+1's classify/build/render
         j = k % NSWEEP
         tl = [vs.TransferFunction(l) for l in luts[j]]
         b = classify_multi(vols, tl, dilate=True)
         index = vs.build_index("lbvh", b)
-        frame = tiles.render_multi(vols, tl, index, cams[j]).cpu()
+        nxt = tiles.frame_multi_async(vols, tl, index, cams[j])
+        if pending is not None:
+            frame = pending.result()
+        pending = nxt
+    frame = pending.result()
     e1.record(st)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
-    del frame
+    del frame, pending
     if rank != 0:
         return
     cpu = None

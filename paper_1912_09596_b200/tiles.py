@@ -147,6 +147,15 @@ class TileRenderer:
         """Render now; the readback runs on a copy stream so the next frame's work can be
         queued while this one travels to the host.  ``.result()`` waits and returns the Frame."""
         img = self.render(v, tf, index, cam, dt)
+        return self._readback(img, self.target.flags)
+
+    def frame_multi_async(self, volumes, tfs, index, cam: Camera,
+                          dt: float = 0.5) -> "PendingFrame":
+        """frame_async for a multi-channel volume (capacity-checked render_multi)."""
+        img = self.render_multi(volumes, tfs, index, cam, dt)
+        return self._readback(img, self._multi_target.flags)
+
+    def _readback(self, img: torch.Tensor, flags: torch.Tensor) -> "PendingFrame":
         total = self._last_total
         if self.world > 1:
             if dist.get_backend(self.group) == "nccl":
@@ -158,7 +167,7 @@ class TileRenderer:
         cur = torch.cuda.current_stream()
         # device-side snapshot (the next render reuses frame_dev), then the D2H on the copy stream
         slot["dev"].copy_(img)
-        slot["meta_dev"][0].copy_(self.target.flags.to(torch.int64).reshape(()))
+        slot["meta_dev"][0].copy_(flags.to(torch.int64).reshape(()))
         slot["meta_dev"][1].copy_(total.reshape(()))
         cs = self.__dict__.setdefault("_copy_stream", torch.cuda.Stream())
         cs.wait_stream(cur)

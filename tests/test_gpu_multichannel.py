@@ -102,3 +102,19 @@ def test_channel_counts_vs_restatement(vs, blobs64, nch):
     orgba, osamples = O.render_multi("lbvh", chans, luts, oidx, cam)
     np.testing.assert_array_equal(samples, osamples)
     np.testing.assert_array_equal(rgba, orgba)
+
+
+def test_tile_frame_multi_async(vs, blobs64):
+    """TileRenderer.frame_multi_async == render_frame_multi (pixels and sample count)."""
+    from paper_1912_09596_b200.multichannel import classify_multi, render_frame_multi
+    from paper_1912_09596_b200.tiles import TileRenderer
+
+    u8 = blobs64["u8"]
+    vols = [vs.Volume(u8), vs.Volume(np.ascontiguousarray(u8[::-1]))]
+    tfs = [vs.TransferFunction.ramp(0.3), vs.TransferFunction.ramp(0.5)]
+    idx = vs.build_index("lbvh", classify_multi(vols, tfs, dilate=True))
+    cam = _cam(vs, blobs64, 72, 40)
+    ref = render_frame_multi(vols, tfs, idx, cam)
+    fr = TileRenderer(cam.width, cam.height).frame_multi_async(vols, tfs, idx, cam).result()
+    np.testing.assert_array_equal(fr.pixels, ref.pixels)
+    assert fr.sample_count == ref.sample_count
