@@ -76,6 +76,15 @@ constexpr int CELL_CHUNK = 1024;
 // Rows one x/y-pass work item covers (a node's slab is split into chunks of this many rows so
 // the top levels of a big volume still spread over every SM; chunks merge with atomics).
 constexpr int SPAN_CHUNK = 64;
+// Slabs of at most one chunk are grouped SLAB_GROUP to a work item (per-item overhead dominates
+// the deep levels' small nodes).
+constexpr int SLAB_GROUP = 4;
+
+// Work items of one row pass over a node: es slabs of er rows each.
+__host__ __device__ __forceinline__ int64_t span_items(int es, int er) {
+  const int nch = (er + SPAN_CHUNK - 1) / SPAN_CHUNK;
+  return nch <= 1 ? (int64_t)((es + SLAB_GROUP - 1) / SLAB_GROUP) : (int64_t)es * nch;
+}
 
 struct KdLevel {
   int n;                      // nodes on this level
@@ -155,21 +164,25 @@ __global__ void __launch_bounds__(256) k_spans_rows(const uint32_t* __restrict__
     const Box b = L.box[i];
     const int er = b.hi[1 - AX] - b.lo[1 - AX];
     const int nch = (er + SPAN_CHUNK - 1) / SPAN_CHUNK;
+    const int es = b.hi[AX] - b.lo[AX];
     const int local = (int)(it - L.off[AI][i]);
-    const int s = local / nch, c = local - s * nch;
+    const int s0 = nch == 1 ? local * SLAB_GROUP : local / nch;
+    const int c = nch == 1 ? 0 : local - s0 * nch;
+    const int s1 = nch == 1 ? min(es, s0 + SLAB_GROUP) : s0 + 1;
     const int r0 = c * SPAN_CHUNK, r1 = min(er, r0 + SPAN_CHUNK);
     const int wz = wz_of(b);
     const int gw = group_width(wz), G = 32 / gw;
     const int g = lane / gw, wl = lane & (gw - 1);
     const uint32_t gmask = gw == 32 ? 0xffffffffu : ((1u << gw) - 1u);
-    const int slab = b.lo[AX] + s;
-    uint32_t acc = 0;
-    int rmin = KD_FAR, rmax = -1;
     // branch-free loads (clamped addresses, masked after) so all 2U loads are in flight at once
     const int wc = min(wl, wz - 1);
     const int gz = b.lo[2] + 32 * wc, sh = gz & 31, rem = b.hi[2] - gz;
     const int gw0 = gz >> 5, gw1 = min(gw0 + 1, nzw - 1);
     const uint32_t zmask = rem < 32 ? (1u << rem) - 1u : 0xffffffffu;
+    for (int s = s0; s < s1; ++s) {
+    const int slab = b.lo[AX] + s;
+    uint32_t acc = 0;
+    int rmin = KD_FAR, rmax = -1;
     for (int rb = r0; rb < r1; rb += G * U) {
       uint32_t lo[U], hi[U];
 #pragma unroll
@@ -226,6 +239,7 @@ __global__ void __launch_bounds__(256) k_spans_rows(const uint32_t* __restrict__
       }
       if (lane < wz && acc) atomicOr(pdst + lane, acc);
     }
+    }  // slabs of the item
   }
 }
 
@@ -850,8 +864,8 @@ __device__ __forceinline__ void prep_node(const PrepCtx& C, const Box& b, int64_
       v[A_PYZ] = (int64_t)ext[1] * wz;
       v[A_ZW] = wz;
       v[A_SCR] = mx;
-      v[A_IX] = (int64_t)ext[0] * ((ext[1] + SPAN_CHUNK - 1) / SPAN_CHUNK);
-      v[A_IY] = (int64_t)ext[1] * ((ext[0] + SPAN_CHUNK - 1) / SPAN_CHUNK);
+      v[A_IX] = span_items(ext[0], ext[1]);
+      v[A_IY] = span_items(ext[1], ext[0]);
       v[A_IZ] = (int64_t)wz * ((max(ext[0], ext[1]) + 31) >> 5);
     }
   } else {
@@ -1406,7 +1420,9 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
       VS_TRY(pyz.ensure((tot[A_PYZ] + 1) * 4, "pyz"));
       VS_TRY(scr.ensure((tot[A_SCR] + 1) * sizeof(RBox), "scratch"));
       if (tot[A_X] > 0) {
-        if (tot[A_IX] > tot[A_X] || tot[A_IY] > tot[A_Y] || tot[A_IZ] > tot[A_ZW]) {  // chunked
+        // some pass merges chunks with atomics: any x/y-chunked node (> 64 rows) is also
+        // z-chunked (> 32 projection rows), and per node A_IZ >= A_ZW with equality iff not
+        if (tot[A_IZ] > tot[A_ZW]) {
           const int64_t mx = std::max(std::max(std::max(tot[A_X], tot[A_Y]), tot[A_Z]),
                                       std::max(tot[A_PXZ], tot[A_PYZ]));
           k_span_init<<<grid_for(mx, 256), 256, 0, st>>>(
@@ -1727,8 +1743,8 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
   const int64_t sizes[A_IZ + 1] = {ext[0], ext[1], ext[2], (int64_t)ext[0] * wz,
                                    (int64_t)ext[1] * wz, wz,
                                    std::max(ext[0], std::max(ext[1], ext[2])),
-                                   (int64_t)ext[0] * cdiv(ext[1], SPAN_CHUNK),
-                                   (int64_t)ext[1] * cdiv(ext[0], SPAN_CHUNK),
+                                   span_items(ext[0], ext[1]),
+                                   span_items(ext[1], ext[0]),
                                    (int64_t)wz * cdiv(std::max(ext[0], ext[1]), 32)};
   for (int k = 0; k <= A_IZ; ++k) h.off[k][1] = sizes[k];
   int64_t csz[3], cit[3];
