@@ -209,12 +209,17 @@ def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # VSB200_DIST_BACKEND=gloo: test mode for the N > 1 code path on a single GPU (ranks share
+    # the device, frames gathered through host copies); the driver's runs use NCCL
+    backend = os.environ.get("VSB200_DIST_BACKEND", "nccl")
     if torch.cuda.is_available():
+        local = local % torch.cuda.device_count() if backend == "gloo" else local
         torch.cuda.set_device(local)
     if ws > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo",
-                                device_id=torch.device("cuda", local)
-                                if torch.cuda.is_available() else None)
+        if backend == "gloo" or not torch.cuda.is_available():
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, ws, local
 
 
@@ -224,7 +229,8 @@ def max_over_ranks(x: float, ws: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
