@@ -143,6 +143,45 @@ __device__ __forceinline__ int group_width(int wz) {
   return wz <= 1 ? 1 : 1 << (32 - __clz(wz - 1));
 }
 
+// One slab's rows [r0, r1) of a span pass: OR of the (masked) z words, first / last nonzero
+// row.  DIRECT: one stored word per lane; else two stored words shifted to a local word.
+template <int U, bool DIRECT>
+__device__ __forceinline__ void rows_or(const uint32_t* __restrict__ bits, int ny, int nzw, int ax,
+                                        int slab, int x0, int y0, int r0, int r1, int G, int g,
+                                        int gw, uint32_t gmask, int w0, int w1, int ssh,
+                                        uint32_t wmask, uint32_t& acc, int& rmin, int& rmax) {
+  for (int rb = r0; rb < r1; rb += G * U) {
+    uint32_t lo[U], hi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = min(rb + u * G + g, r1 - 1);
+      const int x = ax == 0 ? slab : x0 + r;
+      const int y = ax == 0 ? y0 + r : slab;
+      const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
+      lo[u] = __ldg(row + w0);
+      if (!DIRECT) hi[u] = __ldg(row + w1);
+    }
+    uint32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = rb + u * G + g < r1;
+      uint32_t w = lo[u];
+      if (!DIRECT && ssh) w = (lo[u] >> ssh) | (hi[u] << (32 - ssh));
+      v[u] = ok ? (w & wmask) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t m = __ballot_sync(0xffffffffu, v[u] != 0);
+      if ((m >> (g * gw)) & gmask) {
+        const int r = rb + u * G + g;
+        rmin = min(rmin, r);
+        rmax = max(rmax, r);
+      }
+      acc |= v[u];
+    }
+  }
+}
+
 // ---- slab spans along x (AX = 0, rows = y) or y (AX = 1, rows = x), and the matching
 //      (slab, z-word) OR projection ------------------------------------------------------
 // Warp per (node, slab, chunk of SPAN_CHUNK rows).  A row's z words are read by one group of
@@ -171,51 +210,51 @@ __global__ void __launch_bounds__(256) k_spans_rows(const uint32_t* __restrict__
     const int s1 = nch == 1 ? min(es, s0 + SLAB_GROUP) : s0 + 1;
     const int r0 = c * SPAN_CHUNK, r1 = min(er, r0 + SPAN_CHUNK);
     const int wz = wz_of(b);
-    const int gw = group_width(wz), G = 32 / gw;
+    // z words as stored (global alignment): one load per word, first / last word masked;
+    // the OR-projection is shifted to node-local words once per slab.  Nodes spanning more
+    // than 32 stored words (nz > 1024) read two words per local word instead.
+    const int gwa = b.lo[2] >> 5, sh = b.lo[2] & 31;
+    const int nwg = ((b.hi[2] - 1) >> 5) - gwa + 1;
+    const bool direct = nwg <= 32;
+    const int gw = group_width(direct ? nwg : wz), G = 32 / gw;
     const int g = lane / gw, wl = lane & (gw - 1);
     const uint32_t gmask = gw == 32 ? 0xffffffffu : ((1u << gw) - 1u);
-    // branch-free loads (clamped addresses, masked after) so all 2U loads are in flight at once
-    const int wc = min(wl, wz - 1);
-    const int gz = b.lo[2] + 32 * wc, sh = gz & 31, rem = b.hi[2] - gz;
-    const int gw0 = gz >> 5, gw1 = min(gw0 + 1, nzw - 1);
-    const uint32_t zmask = rem < 32 ? (1u << rem) - 1u : 0xffffffffu;
+    // branch-free loads (clamped addresses, masked after) so all loads are in flight at once
+    int w0, w1;
+    uint32_t wmask;
+    if (direct) {
+      w0 = w1 = gwa + min(wl, nwg - 1);
+      const int hb = b.hi[2] & 31;
+      wmask = wl < nwg ? 0xffffffffu : 0u;
+      if (wl == 0) wmask &= 0xffffffffu << sh;
+      if (wl == nwg - 1 && hb) wmask &= (1u << hb) - 1u;
+    } else {
+      const int wc = min(wl, wz - 1);
+      const int gz = b.lo[2] + 32 * wc, rem = b.hi[2] - gz;
+      w0 = gz >> 5;
+      w1 = min(w0 + 1, nzw - 1);
+      wmask = wl < wz ? (rem < 32 ? (1u << rem) - 1u : 0xffffffffu) : 0u;
+    }
+    const int ssh = direct ? 0 : sh;
     for (int s = s0; s < s1; ++s) {
     const int slab = b.lo[AX] + s;
     uint32_t acc = 0;
     int rmin = KD_FAR, rmax = -1;
-    for (int rb = r0; rb < r1; rb += G * U) {
-      uint32_t lo[U], hi[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int r = min(rb + u * G + g, r1 - 1);
-        const int x = AX == 0 ? slab : b.lo[0] + r;
-        const int y = AX == 0 ? b.lo[1] + r : slab;
-        const uint32_t* row = bits + ((int64_t)x * ny + y) * nzw;
-        lo[u] = __ldg(row + gw0);
-        hi[u] = __ldg(row + gw1);
-      }
-      uint32_t v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool ok = rb + u * G + g < r1 && wl < wz;
-        const uint32_t w = (lo[u] >> sh) | (sh ? hi[u] << (32 - sh) : 0u);
-        v[u] = ok ? (w & zmask) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t m = __ballot_sync(0xffffffffu, v[u] != 0);
-        if ((m >> (g * gw)) & gmask) {
-          const int r = rb + u * G + g;
-          rmin = min(rmin, r);
-          rmax = max(rmax, r);
-        }
-        acc |= v[u];
-      }
-    }
+    if (direct)
+      rows_or<U, true>(bits, ny, nzw, AX, slab, b.lo[0], b.lo[1], r0, r1, G, g, gw, gmask, w0, w1,
+                       0, wmask, acc, rmin, rmax);
+    else
+      rows_or<U, false>(bits, ny, nzw, AX, slab, b.lo[0], b.lo[1], r0, r1, G, g, gw, gmask, w0,
+                        w1, ssh, wmask, acc, rmin, rmax);
     for (int o = gw; o < 32; o <<= 1) {
       acc |= __shfl_xor_sync(0xffffffffu, acc, o);
       rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
       rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    }
+    if (direct) {  // stored words -> node-local words
+      const uint32_t nxt = __shfl_down_sync(0xffffffffu, acc, 1);
+      if (sh) acc = (acc >> sh) | (wl + 1 < nwg ? nxt << (32 - sh) : 0u);
+      if (wl >= wz) acc = 0u;
     }
     const uint32_t mz = __ballot_sync(0xffffffffu, acc != 0) & gmask;
     const int wf = mz ? __ffs(mz) - 1 : 0, wlst = mz ? 31 - __clz(mz) : 0;
@@ -366,6 +405,7 @@ struct DecideSmem {
   RBox wbox[DW];
   int64_t wcost[DW];
   int wk[DW];
+  RBox best_l, best_r;  // sweep_axis: tight boxes of [0, k) and [k, e) at the chosen cut
 };
 
 // Exclusive block scan (join) of one box per thread in thread order (rev = false) or in
@@ -430,13 +470,16 @@ __device__ void sweep_axis(const Span* __restrict__ sp, int e, RBox* __restrict_
   RBox pre = block_excl_scan(loc, false, sm);  // slabs before my run (syncs: suf visible)
   int64_t bc = INT64_MAX;
   int bk = 0;
+  RBox bpre = rb_empty();
   for (int s = s0; s < s1; ++s) {
     pre = rb_join(pre, slab_box(sp, s));
     if (s + 1 < e) {
       const int64_t c = rvol(pre) + rvol(suf[s + 1]);
-      if (c < bc) { bc = c; bk = s + 1; }
+      if (c < bc) { bc = c; bk = s + 1; bpre = pre; }
     }
   }
+  const int64_t my_c = bc;
+  const int my_k = bk;
   for (int o = 16; o; o >>= 1) {
     const int64_t c2 = __shfl_xor_sync(0xffffffffu, bc, o);
     const int k2 = __shfl_xor_sync(0xffffffffu, bk, o);
@@ -449,6 +492,9 @@ __device__ void sweep_axis(const Span* __restrict__ sp, int e, RBox* __restrict_
   bk = sm.wk[0];
   for (int w = 1; w < DW; ++w)
     if (sm.wcost[w] < bc || (sm.wcost[w] == bc && sm.wk[w] < bk)) { bc = sm.wcost[w]; bk = sm.wk[w]; }
+  // the winner's boxes: the cut is the first minimum of the thread owning slab k-1
+  if (my_c == bc && my_k == bk && bc != INT64_MAX) { sm.best_l = bpre; sm.best_r = suf[bk]; }
+  __syncthreads();
   best_k = bk;
   best_cost = bc;
 }
@@ -624,19 +670,23 @@ __global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
   auto axis_span = [&](int a) { return a == 0 ? spx : (a == 1 ? spy : spz); };
   auto axis_ext = [&](int a) { return a == 0 ? ex : (a == 1 ? ey : ez); };
   auto axis_lo = [&](int a) { return a == 0 ? b.lo[0] : (a == 1 ? b.lo[1] : b.lo[2]); };
+  auto split_boxes = [&](int a, int k, const RBox& l, const RBox& r) {
+    d.axis = a; d.plane = axis_lo(a) + k;
+    if (l.hi0 >= 0) { d.left = to_global(b, a, l); d.nchild |= 1; }
+    if (r.hi0 >= 0) { d.right = to_global(b, a, r); d.nchild |= 2; }
+  };
   auto split_at = [&](int a, int k) {
     const Span* sp = axis_span(a);
     const RBox l = range_box(sp, 0, k, sm);
     const RBox r = range_box(sp, k, axis_ext(a), sm);
-    d.axis = a; d.plane = axis_lo(a) + k;
-    if (l.hi0 >= 0) { d.left = to_global(b, a, l); d.nchild |= 1; }
-    if (r.hi0 >= 0) { d.right = to_global(b, a, r); d.nchild |= 2; }
+    split_boxes(a, k, l, r);
   };
   if (!halted(P, vol)) {
     // _sweep_search + acceptance (kdtree.py:191-221, 431-439)
     RBox* suf = scratch + L.off[A_SCR][i];
     int ba = -1, bk = 0;
     int64_t bc = 0;
+    RBox bl = rb_empty(), br = rb_empty();
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int e = a == 0 ? ex : (a == 1 ? ey : ez);
@@ -645,19 +695,26 @@ __global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
       int64_t c;
       const Span* sp = a == 0 ? spx : (a == 1 ? spy : spz);
       if (STAGE && e <= STAGE_SLABS) {
-        // stage the axis' spans (coalesced) and keep the suffix boxes on chip
+        // stage the axis' spans (coalesced, all loads in flight) and keep the suffix boxes
+        // on chip
         __syncthreads();
-        for (int s = t; s < e; s += DT) stage_sp[s] = sp[s];
+        Span v[STAGE_SLABS / DT];
+#pragma unroll
+        for (int j = 0; j < STAGE_SLABS / DT; ++j)
+          if (t + j * DT < e) v[j] = sp[t + j * DT];
+#pragma unroll
+        for (int j = 0; j < STAGE_SLABS / DT; ++j)
+          if (t + j * DT < e) stage_sp[t + j * DT] = v[j];
         __syncthreads();
         sweep_axis(stage_sp, e, stage_suf, sm, k, c);
       } else {
         sweep_axis(sp, e, suf, sm, k, c);
       }
       if (ba >= 0 && c >= bc) continue;
-      ba = a; bk = k; bc = c;
+      ba = a; bk = k; bc = c; bl = sm.best_l; br = sm.best_r;
     }
     if (ba >= 0 && bc < vol) {
-      split_at(ba, bk);
+      split_boxes(ba, bk, bl, br);
       split = true;
     }
   }
