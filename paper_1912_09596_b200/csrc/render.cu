@@ -1789,11 +1789,18 @@ int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
           *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
       break;
     case VS_KIND_GRID:
-      k_segments<VS_KIND_GRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      if (!(g_render_opts & 4))
+        k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(*vol, *ix, *cam, rows, dt, sg,
+                                                                counts, cap, flags);
+      else
+        k_segments<VS_KIND_GRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
       break;
     case VS_KIND_LBVH:
-      if (ix->brick_bits)
+      if (ix->brick_bits && !(g_render_opts & 4))
+        k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, (g_render_opts & 16) ? 1 : 0);
+      else if (ix->brick_bits)
         k_segments<KIND_LBVH_BRICK><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
             *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
       else
@@ -1801,12 +1808,20 @@ int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
             *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
       break;
     case VS_KIND_KD:
-      k_segments<VS_KIND_KD><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      if (!(g_render_opts & 4))
+        k_segments_kd<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(*vol, *ix, *cam, rows, dt, sg,
+                                                                counts, cap, flags);
+      else
+        k_segments<VS_KIND_KD><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
       break;
     case VS_KIND_HYBRID:
-      k_segments<VS_KIND_HYBRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+      if (!(g_render_opts & 4))
+        k_segments_hybrid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(*vol, *ix, *cam, rows, dt, sg,
+                                                                counts, cap, flags);
+      else
+        k_segments<VS_KIND_HYBRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
       break;
     default:
       return fail_arg("vs_render_segments: kind");
