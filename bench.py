@@ -396,15 +396,21 @@ def run_ours(args, rank, ws, local):
     e_steps = args.steps  # the same TF sweep / camera orbit as the device-timed loop
     pub = TileRenderer(W, H)
 
+    build_stream = torch.cuda.Stream()
+
     def e2e_step(k):
+        # TF change on a side stream: frame k+1's classify + build_index overlap frame k's
+        # render (fresh index tensors per frame, kept alive until that frame's result())
         j = k % NSWEEP
-        tf = vs.TransferFunction(luts[j])           # host LUT -> pinned -> device
-        b = vs.classify(v, tf, dilate=True)
-        index = vs.build_index("lbvh", b)
-        return pub.frame_async(v, tf, index, cams[j])  # pixels -> pinned host memory
+        with torch.cuda.stream(build_stream):
+            tf = vs.TransferFunction(luts[j])           # host LUT -> pinned -> device
+            b = vs.classify(v, tf, dilate=True)
+            index = vs.build_index("lbvh", b)
+        torch.cuda.current_stream().wait_stream(build_stream)
+        return pub.frame_async(v, tf, index, cams[j]), (tf, b, index)  # pixels -> pinned host
 
     for k in range(min(args.warmup, 3)):
-        e2e_step(k).result()
+        e2e_step(k)[0].result()
     torch.cuda.synchronize()
     barrier(ws)
     e0.record(st)
@@ -412,9 +418,9 @@ def run_ours(args, rank, ws, local):
     for k in range(e_steps):  # frame k's readback overlaps frame k+1's classify/build/render
         nxt = e2e_step(k)
         if pending is not None:
-            fr = pending.result()
+            fr = pending[0].result()
         pending = nxt
-    fr = pending.result()
+    fr = pending[0].result()
     e1.record(st)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
@@ -506,9 +512,9 @@ def run_ours(args, rank, ws, local):
         "e2e": {"value": 1e3 / e2e_ms, "unit": "frames/s",
                 "h2d_bytes_per_step": 64 + 4096 + 2048, "d2h_bytes_per_step": W * H * 4 + 16,
                 "ms_per_step": e2e_ms,
-                "path": "TransferFunction->classify->build_index('lbvh')->"
-                        "TileRenderer.frame_async(...).result(), readback of frame k "
-                        "overlapping frame k+1"},
+                "path": "TransferFunction->classify->build_index('lbvh') on a build stream->"
+                        "TileRenderer.frame_async(...).result(); frame k+1's TF change and "
+                        "frame k's readback overlap frame k's render"},
         "gpu_launches": launches_per_step * args.steps,
         "cpu_baseline": cpu,
         "clocks": clocks,
@@ -599,16 +605,19 @@ def run_multi(args, rank, ws, local):
     barrier(ws)
     e0.record(st)
     pending = None
+    build_stream = torch.cuda.Stream()
     for k in range(e_steps):  # frame k's readback overlaps frame k+1's classify/build/render
         j = k % NSWEEP
-        tl = [vs.TransferFunction(l) for l in luts[j]]
-        b = classify_multi(vols, tl, dilate=True)
-        index = vs.build_index("lbvh", b)
-        nxt = tiles.frame_multi_async(vols, tl, index, cams[j])
+        with torch.cuda.stream(build_stream):  # TF change overlapping the previous render
+            tl = [vs.TransferFunction(l) for l in luts[j]]
+            b = classify_multi(vols, tl, dilate=True)
+            index = vs.build_index("lbvh", b)
+        torch.cuda.current_stream().wait_stream(build_stream)
+        nxt = (tiles.frame_multi_async(vols, tl, index, cams[j]), (tl, b, index))
         if pending is not None:
-            frame = pending.result()
+            frame = pending[0].result()
         pending = nxt
-    frame = pending.result()
+    frame = pending[0].result()
     e1.record(st)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
@@ -658,7 +667,9 @@ def run_multi(args, rank, ws, local):
         "render": {"samples_per_frame": samples},
         "e2e": {"value": 1e3 / e2e_ms, "unit": "frames/s",
                 "h2d_bytes_per_step": nch * (64 + 4096 + 2048),
-                "d2h_bytes_per_step": W * H * 4, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": W * H * 4, "ms_per_step": e2e_ms,
+                "path": "TransferFunction x nch->classify_multi->build_index('lbvh') on a "
+                        "build stream->TileRenderer.frame_multi_async(...).result()"},
         "gpu_launches": (nch + (nch - 1) + 7 + 2) * args.steps,  # summaries, ORs, tree (as above), render
         "cpu_baseline": cpu, "clocks": clk.summary(),
     }

@@ -122,6 +122,15 @@ def ptr(t: torch.Tensor | None):
     return None if t is None else t.data_ptr()
 
 
+def upload(arr) -> torch.Tensor:
+    """Host array -> device without blocking the host: staged in pinned memory from torch's
+    caching host allocator (which keeps the block until the stream-ordered copy has run)."""
+    import numpy as np
+
+    host = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+    return host.to(device(), non_blocking=True)
+
+
 def workspace(nbytes: int) -> torch.Tensor:
     """Scratch from torch's caching allocator (stream-ordered on the current stream)."""
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device())

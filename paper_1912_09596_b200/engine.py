@@ -153,4 +153,4 @@ def tf_params_device(tfs: list[TransferFunction]) -> torch.Tensor:
     import numpy as np
 
     host = np.stack([tf.params_host() for tf in tfs])
-    return torch.from_numpy(host).to(_lib.device())
+    return _lib.upload(host)

@@ -220,8 +220,7 @@ def tf_device(tf: TransferFunction, dt: float):
     if key not in cache:
         corr = np.array([1.0 - math.pow(1.0 - float(a), float(dt)) for a in tf.lut[:, 3]],
                         dtype=np.float64)
-        cache[key] = (torch.from_numpy(np.ascontiguousarray(tf.lut)).to(dev),
-                      torch.from_numpy(corr).to(dev))
+        cache[key] = (_lib.upload(tf.lut), _lib.upload(corr))  # stream-ordered, no host wait
     return cache[key]
 
 

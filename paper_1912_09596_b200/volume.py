@@ -186,20 +186,8 @@ class TransferFunction:
         dev = _lib.device()
         key = ("params", dev.index)
         if key not in self._dev:
-            stage = _pinned_stage()
-            stage.copy_(torch.from_numpy(self.params_host()))
-            self._dev[key] = stage.to(dev)  # pinned -> device (synchronous, 64 bytes)
+            self._dev[key] = _lib.upload(self.params_host())  # 64 bytes, stream-ordered
         return self._dev[key]
-
-
-_STAGE = None
-
-
-def _pinned_stage() -> torch.Tensor:
-    global _STAGE
-    if _STAGE is None:
-        _STAGE = torch.empty(16, dtype=torch.int32).pin_memory()
-    return _STAGE
 
 
 def quantize_scalar(values) -> np.ndarray:
