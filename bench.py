@@ -430,7 +430,8 @@ def run_ours(args, rank, ws, local):
     # reported for the SVT k-d tree, binned k-d tree and hybrid grid"): public API, classify +
     # build_index, synchronised, median of 3 after one warm-up, sparse / medium / dense ramp
     rebuilds = {}
-    for kind in ("lbvh", "grid", "hybrid", "kd-shallow", "kd-binned-mls32"):
+    for kind in () if args.frame_only else ("lbvh", "grid", "hybrid", "kd-shallow",
+                                            "kd-binned-mls32"):
         per_t = []
         for t in (0.6, 0.3, 0.0):
             tfk = vs.TransferFunction.ramp(t)
@@ -685,6 +686,8 @@ def main():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--frame-only", action="store_true",
+                    help="skip the other hierarchies' rebuild timings (profiling runs)")
     ap.add_argument("--channels", type=int, default=1,
                     help="> 1: BASELINE configs[4] multi-channel frames")
     args = ap.parse_args()

@@ -11,7 +11,9 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.jso
 python bench.py --channels 4 > gpurun_out/bench_mc4.json 2> gpurun_out/bench_mc4.err
 timeout 900 python tools/bench_configs.py > gpurun_out/configs.json 2> gpurun_out/configs.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches_interactive_frame.csv python bench.py --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1
+  --log-file gpurun_out/launches_interactive_frame.csv python bench.py --steps 2 --warmup 3 --no-cpu --frame-only > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_mc4.csv python bench.py --channels 4 --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_hybrid_1024.csv python tools/prof_kd.py 1024 hybrid 0.3 > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
@@ -21,7 +23,7 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   python tools/prof_kd.py 1024 hybrid 0.6 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"k_brick_summary|k_segments|k_integrate_segments" -s 3 -c 3 -o gpurun_out/frame_1024 \
-  python bench.py --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1
+  python bench.py --steps 2 --warmup 3 --no-cpu --frame-only > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"k_integrate_multi" -c 1 -o gpurun_out/multi_1024 \
   python bench.py --channels 4 --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
