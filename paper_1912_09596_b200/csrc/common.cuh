@@ -89,4 +89,35 @@ __host__ __device__ inline uint32_t morton3(uint32_t x, uint32_t y, uint32_t z) 
 // (x*ny + y)*nzw + w, bit z & 31.
 __host__ __device__ inline int64_t nzw_of(int nz) { return (nz + 31) >> 5; }
 
+#ifdef __CUDACC__
+// A trilinear sample's classification bin floor(v*255 + 0.5) (render.py:694-748) from its
+// 2x2x2 u8 neighbourhood (quad words w0 = x0 plane, w1 = x1 plane; tb = f32(u/255) table) in
+// FP32, when that is provably the bin of the reference's evaluation (f32 first differences, FP64
+// lerps), else -1.  Error of v against the reference: < 9.0e-7 (fractions rounded to f32:
+// 2^-25; FMA and difference roundings: 2^-25 each on values in [0, 1]; three lerp levels), so
+// w = v*255 + 0.5 is within 2.4e-4 (+ its own rounding, 7.6e-6 at 255.5) of the reference's; a
+// fractional part of w at least BIN_EDGE from an integer fixes floor(w).  ~0.2% of samples
+// fall back to the FP64 evaluation.
+constexpr float BIN_EDGE = 1e-3f;
+__device__ __forceinline__ int bin_fast(const float* tb, uint32_t w0, uint32_t w1, float fx,
+                                        float fy, float fz) {
+  const float c000 = tb[w0 & 0xffu], c001 = tb[(w0 >> 8) & 0xffu];
+  const float c010 = tb[(w0 >> 16) & 0xffu], c011 = tb[w0 >> 24];
+  const float c100 = tb[w1 & 0xffu], c101 = tb[(w1 >> 8) & 0xffu];
+  const float c110 = tb[(w1 >> 16) & 0xffu], c111 = tb[w1 >> 24];
+  const float c00 = __fmaf_rn(__fsub_rn(c100, c000), fx, c000);
+  const float c10 = __fmaf_rn(__fsub_rn(c110, c010), fx, c010);
+  const float c01 = __fmaf_rn(__fsub_rn(c101, c001), fx, c001);
+  const float c11 = __fmaf_rn(__fsub_rn(c111, c011), fx, c011);
+  const float c0 = __fmaf_rn(__fsub_rn(c10, c00), fy, c00);
+  const float c1 = __fmaf_rn(__fsub_rn(c11, c01), fy, c01);
+  const float v = __fmaf_rn(__fsub_rn(c1, c0), fz, c0);
+  const float w = __fmaf_rn(v, 255.0f, 0.5f);
+  const float fl = floorf(w), fr = __fsub_rn(w, fl);
+  if (fr < BIN_EDGE || fr > 1.0f - BIN_EDGE) return -1;
+  const int bi = (int)fl;
+  return bi < 0 ? 0 : (bi > 255 ? 255 : bi);
+}
+#endif
+
 }  // namespace vs

@@ -235,11 +235,19 @@ struct Integrator {
     const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, g.fy));
     return __dadd_rn(c0, __dmul_rn(c1 - c0, g.fz));
   }
-  // classification + front-to-back compositing of one interpolated value (render.py:745-758)
-  __device__ __forceinline__ void shade(double value) {
-    // floor(v*255 + 0.5) clipped to [0, 255]: one floor-converting F2I + integer clamp
+  // the sample's bin by the FP32 filter (common.cuh bin_fast), -1: decide in FP64
+  __device__ __forceinline__ int bin_fast(const Gather& g) const {
+    return vs::bin_fast(sm->u8f, g.w0, g.w1, __double2float_rn(g.fx), __double2float_rn(g.fy),
+                        __double2float_rn(g.fz));
+  }
+  // floor(v*255 + 0.5) clipped to [0, 255] (render.py:745-748): one floor-converting F2I
+  __device__ __forceinline__ static int bin_of(double value) {
     const int bi = __double2int_rd(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
-    const int bin = bi < 0 ? 0 : (bi > 255 ? 255 : bi);
+    return bi < 0 ? 0 : (bi > 255 ? 255 : bi);
+  }
+  // classification + front-to-back compositing of one interpolated value (render.py:745-758)
+  __device__ __forceinline__ void shade(double value) { shade_bin(bin_of(value)); }
+  __device__ __forceinline__ void shade_bin(int bin) {
     const float4 c = sm->lut[bin];
     if (c.w > 0.0f) {
       const double w = __dmul_rn(1.0 - acca, sm->corr[bin]);
@@ -714,6 +722,7 @@ static int g_trav_budget = 1, g_sample_budget = 1;
 // early ray termination (vs_set_render_ert): opacity threshold, 2.0 = off (parity mode)
 static thread_local double g_ert_a = 2.0;
 // bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float conversion)
+// bit1: k_integrate_segments evaluates every sample's bin in FP64 (no FP32 bin filter)
 // bit2: generic k_segments for the LBVH brick DDA / grid / hybrid (else the flat-loop kernels)
 // bit4: k_segments_brick evaluates every occupied brick's slab (no run shortcut)
 static int g_render_opts = 1;
@@ -1352,7 +1361,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
                          const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
                          double* __restrict__ rgba64, int32_t* __restrict__ samples,
                          unsigned long long* __restrict__ total, int* __restrict__ flags_out,
-                         double ert_a) {
+                         double ert_a, int bin_filter) {
   __shared__ RenderSmem sm;
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
   load_tables(sm, lut, corr, tid, RENDER_TX * RENDER_TY);
@@ -1407,7 +1416,10 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
           }
           Integrator::Gather gn;
           if (hn) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)kn, dt)), gn);
-          I.shade(I.interp_t<true>(g));
+          // bin_filter 0: every sample through the FP64 path (tests the filter's exactness)
+          int bin = bin_filter ? I.bin_fast(g) : -1;
+          if (bin < 0) bin = Integrator::bin_of(I.interp_t<true>(g));
+          I.shade_bin(bin);
           if (!hn || (ERT && I.terminated())) break;
           k = kn;
           g = gn;
@@ -1649,7 +1661,7 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
 #define VS_INTEGRATE(I32, E)                                                                  \
   k_integrate_segments<K, I32, E><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(               \
       v, ix, c, lut, corr, dt, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples, total,  \
-      flags, g_ert_a)
+      flags, g_ert_a, (g_render_opts & 2) ? 0 : 1)
       if (idx32) {
         if (ert) VS_INTEGRATE(true, true); else VS_INTEGRATE(true, false);
       } else {
