@@ -436,7 +436,9 @@ __device__ RBox block_excl_scan(RBox x, bool rev, DecideSmem& sm) {
 
 __device__ RBox block_reduce(RBox r, DecideSmem& sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o; o >>= 1) r = rb_join(r, rb_shfl(r, lane ^ o));
+  r = RBox{__reduce_min_sync(0xffffffffu, r.lo0), __reduce_min_sync(0xffffffffu, r.lo1),
+           __reduce_min_sync(0xffffffffu, r.lo2), __reduce_max_sync(0xffffffffu, r.hi0),
+           __reduce_max_sync(0xffffffffu, r.hi1), __reduce_max_sync(0xffffffffu, r.hi2)};
   __syncthreads();
   if (lane == 0) sm.wbox[warp] = r;
   __syncthreads();
@@ -556,11 +558,10 @@ __device__ bool cells_reduce_axis(const CBox* __restrict__ cslab, int node_c0, i
       for (int k = 0; k < 3; ++k) { u.lo[k] = min(u.lo[k], v.lo[k]); u.hi[k] = max(u.hi[k], v.hi[k]); }
     }
   }
-  for (int o = 16; o; o >>= 1)
-    for (int k = 0; k < 3; ++k) {
-      u.lo[k] = min(u.lo[k], __shfl_xor_sync(0xffffffffu, u.lo[k], o));
-      u.hi[k] = max(u.hi[k], __shfl_xor_sync(0xffffffffu, u.hi[k], o));
-    }
+  for (int k = 0; k < 3; ++k) {  // warp reductions (redux.sync)
+    u.lo[k] = __reduce_min_sync(0xffffffffu, u.lo[k]);
+    u.hi[k] = __reduce_max_sync(0xffffffffu, u.hi[k]);
+  }
   if (u.lo[0] == KD_FAR) return false;
   for (int k = 0; k < 3; ++k) {
     out.lo[k] = max(u.lo[k], region.lo[k]);
@@ -620,14 +621,12 @@ __device__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a, 
         uhi0 = max(uhi0, v.hi[0]); uhi1 = max(uhi1, v.hi[1]); uhi2 = max(uhi2, v.hi[2]);
       }
     }
-    for (int o = 16; o; o >>= 1) {
-      ulo0 = min(ulo0, __shfl_xor_sync(0xffffffffu, ulo0, o));
-      ulo1 = min(ulo1, __shfl_xor_sync(0xffffffffu, ulo1, o));
-      ulo2 = min(ulo2, __shfl_xor_sync(0xffffffffu, ulo2, o));
-      uhi0 = max(uhi0, __shfl_xor_sync(0xffffffffu, uhi0, o));
-      uhi1 = max(uhi1, __shfl_xor_sync(0xffffffffu, uhi1, o));
-      uhi2 = max(uhi2, __shfl_xor_sync(0xffffffffu, uhi2, o));
-    }
+    ulo0 = __reduce_min_sync(0xffffffffu, ulo0);  // warp reductions (redux.sync)
+    ulo1 = __reduce_min_sync(0xffffffffu, ulo1);
+    ulo2 = __reduce_min_sync(0xffffffffu, ulo2);
+    uhi0 = __reduce_max_sync(0xffffffffu, uhi0);
+    uhi1 = __reduce_max_sync(0xffffffffu, uhi1);
+    uhi2 = __reduce_max_sync(0xffffffffu, uhi2);
     if (ulo0 == KD_FAR) return false;
     out.lo[0] = max(ulo0, region.lo[0]); out.hi[0] = min(uhi0, region.hi[0]);
     out.lo[1] = max(ulo1, region.lo[1]); out.hi[1] = min(uhi1, region.hi[1]);
@@ -870,11 +869,10 @@ __global__ void __launch_bounds__(256) k_cell_slabs(const CBox* __restrict__ cel
       if (v.lo[0] != KD_FAR)
         for (int k = 0; k < 3; ++k) { u.lo[k] = min(u.lo[k], v.lo[k]); u.hi[k] = max(u.hi[k], v.hi[k]); }
     }
-    for (int o = 16; o; o >>= 1)
-      for (int k = 0; k < 3; ++k) {
-        u.lo[k] = min(u.lo[k], __shfl_xor_sync(0xffffffffu, u.lo[k], o));
-        u.hi[k] = max(u.hi[k], __shfl_xor_sync(0xffffffffu, u.hi[k], o));
-      }
+    for (int k = 0; k < 3; ++k) {  // warp reductions (redux.sync)
+      u.lo[k] = __reduce_min_sync(0xffffffffu, u.lo[k]);
+      u.hi[k] = __reduce_max_sync(0xffffffffu, u.hi[k]);
+    }
     CBox* dst = out + off[i] + s;
     if (nch == 1) {
       if (lane == 0) *dst = u;
@@ -1032,11 +1030,10 @@ __global__ void __launch_bounds__(128) k_leaf_shrink(const uint32_t* __restrict_
     lo[2] = 32 * wf + __ffs(af) - 1;
     hi[2] = 32 * wlst + 31 - __clz(al);
   }
-  for (int o = 16; o; o >>= 1)
-    for (int k = 0; k < 3; ++k) {
-      lo[k] = min(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
-      hi[k] = max(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
-    }
+  for (int k = 0; k < 3; ++k) {  // warp reductions (redux.sync)
+    lo[k] = __reduce_min_sync(0xffffffffu, lo[k]);
+    hi[k] = __reduce_max_sync(0xffffffffu, hi[k]);
+  }
   if (lane == 0 && hi[0] >= 0)
     for (int k = 0; k < 3; ++k) { atomicMin(&red[k], lo[k]); atomicMax(&red[3 + k], hi[k]); }
   __syncthreads();
@@ -1158,11 +1155,10 @@ __global__ void __launch_bounds__(256) k_bits_bbox(const uint32_t* __restrict__ 
     zlo = 32 * wf + __ffs(af) - 1;
     zhi = 32 * wlst + 31 - __clz(al);
   }
-  for (int o = 16; o; o >>= 1)
-    for (int k = 0; k < 2; ++k) {
-      lo[k] = min(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
-      hi[k] = max(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
-    }
+  for (int k = 0; k < 2; ++k) {  // warp reductions (redux.sync)
+    lo[k] = __reduce_min_sync(0xffffffffu, lo[k]);
+    hi[k] = __reduce_max_sync(0xffffffffu, hi[k]);
+  }
   if (lane == 0 && hi[0] >= 0) {
     atomicMin(bb + 0, lo[0]); atomicMax(bb + 3, hi[0] + 1);
     atomicMin(bb + 1, lo[1]); atomicMax(bb + 4, hi[1] + 1);
