@@ -1056,54 +1056,107 @@ struct ScanSet {
   int k;
 };
 
+constexpr int SCAN_PER = 4, SCAN_TILE = 1024 * SCAN_PER;
+
+// Exclusive scan of a[base, min(base + SCAN_TILE, n)) in place, offset by carry (1024 threads);
+// returns carry + the tile's sum (every thread).
+__device__ int64_t scan_tile(int64_t* __restrict__ a, int64_t base, int64_t n, int64_t carry,
+                             int64_t* wsum, int64_t* total_s) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int64_t v[SCAN_PER], s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    const int64_t j = base + (int64_t)t * SCAN_PER + k;
+    v[k] = j < n ? a[j] : 0;
+    s += v[k];
+  }
+  int64_t incl = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = wsum[lane], wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    wsum[lane] = wi - w;  // exclusive warp offsets
+  }
+  __syncthreads();
+  int64_t run = carry + wsum[warp] + incl - s;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    const int64_t j = base + (int64_t)t * SCAN_PER + k;
+    if (j < n) a[j] = run;
+    run += v[k];
+  }
+  __syncthreads();
+  if (t == 1023) *total_s = run;
+  __syncthreads();
+  return *total_s;
+}
+
+// One block per array: the whole array in SCAN_TILE steps (narrow levels).
 __global__ void __launch_bounds__(1024) k_multi_scan(ScanSet S, const int64_t* __restrict__ n_ptr,
                                                     int64_t n_host) {
   __shared__ int64_t wsum[32];
-  __shared__ int64_t carry_s;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  __shared__ int64_t total_s;
   const int64_t n = n_ptr ? *n_ptr : n_host;
   int64_t* a = S.a[blockIdx.x];
-  if (t == 0) carry_s = 0;
-  __syncthreads();
-  constexpr int PER = 4, TILE = 1024 * PER;
-  for (int64_t base = 0; base < n; base += TILE) {
-    int64_t v[PER], s = 0;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int64_t j = base + (int64_t)t * PER + k;
-      v[k] = j < n ? a[j] : 0;
-      s += v[k];
-    }
-    int64_t incl = s;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += u;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      int64_t w = wsum[lane], wi = w;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t u = __shfl_up_sync(0xffffffffu, wi, o);
-        if (lane >= o) wi += u;
-      }
-      wsum[lane] = wi - w;  // exclusive warp offsets
-    }
-    __syncthreads();
-    int64_t run = carry_s + wsum[warp] + incl - s;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int64_t j = base + (int64_t)t * PER + k;
-      if (j < n) a[j] = run;
-      run += v[k];
-    }
-    __syncthreads();
-    if (t == 1023) carry_s = run;
-    __syncthreads();
+  int64_t carry = 0;
+  for (int64_t base = 0; base < n; base += SCAN_TILE) carry = scan_tile(a, base, n, carry, wsum, &total_s);
+  if (threadIdx.x == 0) {
+    a[n] = carry;
+    if (S.totals[blockIdx.x]) *S.totals[blockIdx.x] = carry;
   }
-  if (t == 0) {
-    a[n] = carry_s;
-    if (S.totals[blockIdx.x]) *S.totals[blockIdx.x] = carry_s;
+}
+
+// Wide levels: block (tile c, array j).  Pass 1: tile sums; pass 2: each tile's carry is the sum
+// of the earlier tiles' sums, then the tile scan; the tile holding element n-1 writes the total.
+__global__ void __launch_bounds__(256) k_scan_sums(ScanSet S, const int64_t* __restrict__ n_ptr,
+                                                   int64_t n_host, int64_t* __restrict__ part,
+                                                   int nch) {
+  __shared__ int64_t ws[8];
+  const int64_t n = n_ptr ? *n_ptr : n_host;
+  const int64_t* a = S.a[blockIdx.y];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  int64_t s = 0;
+  for (int64_t j = base + threadIdx.x; j < min(n, base + SCAN_TILE); j += 256) s += a[j];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < 8; ++w) t += ws[w];
+    part[(int64_t)blockIdx.y * nch + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_apply(ScanSet S, const int64_t* __restrict__ n_ptr,
+                                                     int64_t n_host,
+                                                     const int64_t* __restrict__ part, int nch) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t total_s;
+  const int64_t n = n_ptr ? *n_ptr : n_host;
+  int64_t* a = S.a[blockIdx.y];
+  const int c = blockIdx.x;
+  const int64_t base = (int64_t)c * SCAN_TILE;
+  if (base >= n && !(n == 0 && c == 0)) return;
+  int64_t s = 0;  // carry: the earlier tiles' sums
+  for (int q = threadIdx.x; q < c; q += 1024) s += part[(int64_t)blockIdx.y * nch + q];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+  __syncthreads();
+  int64_t carry = 0;
+  for (int w = 0; w < 32; ++w) carry += wsum[w];
+  __syncthreads();
+  const int64_t run = scan_tile(a, base, n, carry, wsum, &total_s);
+  if (threadIdx.x == 0 && base + SCAN_TILE >= n) {  // the last tile (or the empty array)
+    a[n] = run;
+    if (S.totals[blockIdx.y]) *S.totals[blockIdx.y] = run;
   }
 }
 
@@ -1420,15 +1473,32 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
   };
   const int nscan = binned ? 6 : A_IZ + 1;
   const int scan0 = binned ? A_C0 : 0;
-  auto scan_level = [&](const int64_t* n_dev) -> int {
+  DBuf part;
+  part.st = st;
+  // exclusive scans of S's arrays of n entries (n_dev on the device, else n_host); n_bound:
+  // the host's bound on n.  Narrow: one block per array; wide: tiles across blocks.
+  auto scan_arrays = [&](const ScanSet& S, const int64_t* n_dev, int64_t n_host,
+                         int64_t n_bound) -> int {
+    const int64_t nch = cdiv(std::max<int64_t>(n_bound, 1), SCAN_TILE);
+    if (nch <= 2) {
+      k_multi_scan<<<S.k, 1024, 0, st>>>(S, n_dev, n_host);
+      return check_launch("k_multi_scan");
+    }
+    VS_TRY(part.ensure((size_t)S.k * nch * sizeof(int64_t), "scan partials"));
+    const dim3 g((unsigned)nch, (unsigned)S.k);
+    k_scan_sums<<<g, 256, 0, st>>>(S, n_dev, n_host, part.as<int64_t>(), (int)nch);
+    VS_TRY(check_launch("k_scan_sums"));
+    k_scan_apply<<<g, 1024, 0, st>>>(S, n_dev, n_host, part.as<int64_t>(), (int)nch);
+    return check_launch("k_scan_apply");
+  };
+  auto scan_level = [&](const int64_t* n_dev, int64_t n_bound) -> int {
     ScanSet S;
     S.k = nscan;
     for (int j = 0; j < nscan; ++j) {
       S.a[j] = arr(scan0 + j);
       S.totals[j] = dh + 1 + scan0 + j;
     }
-    k_multi_scan<<<nscan, 1024, 0, st>>>(S, n_dev, 0);
-    return check_launch("k_multi_scan");
+    return scan_arrays(S, n_dev, 0, n_bound);
   };
 
   // root box (kdtree.py:398): tight box of every flag
@@ -1443,7 +1513,7 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
     // root_vol is needed by every level's halting rule: read the bbox with the header
     k_root_level<<<1, 32, 0, st>>>(dbb, cur.as<Box>(), prep_ctx(), dh);
     VS_TRY(check_launch("k_root_level"));
-    VS_TRY(scan_level(dh));
+    VS_TRY(scan_level(dh, 1));
     int rb[6];
     VS_CUDA(cudaMemcpyAsync(rb, dbb, sizeof rb, cudaMemcpyDeviceToHost, st), "bbox d2h");
     VS_TRY(d2h(hh, dh, sizeof hh, st));
@@ -1553,7 +1623,7 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
       S.k = 1;
       S.a[0] = cnt.as<int64_t>();
       S.totals[0] = dh + KA + 1;
-      k_multi_scan<<<1, 1024, 0, st>>>(S, nullptr, n);
+      VS_TRY(scan_arrays(S, nullptr, n, n));
       VS_TRY(check_launch("k_multi_scan"));
     }
     if ((size_t)(base + n) * sizeof(NodeRec) > rec.cap) {  // grow the records (copy-preserving)
@@ -1572,7 +1642,7 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
                                                          rec.as<NodeRec>(), nxt.as<Box>(),
                                                          prep_ctx());
     VS_TRY(check_launch("k_emit_level"));
-    VS_TRY(scan_level(dh + KA + 1));
+    VS_TRY(scan_level(dh + KA + 1, 2 * n));
     VS_CUDA(cudaMemcpyAsync(dh, dh + KA + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, st),
             "count");
     VS_TRY(d2h(hh, dh, sizeof hh, st));
