@@ -637,6 +637,69 @@ __device__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a, 
                            lane, out);
 }
 
+// A small node's cells (<= SMALL_CELLS = 64: two per lane) held in registers by the deciding
+// warp, so every candidate region's _cells_reduce is a masked fold plus warp reductions (the
+// same cell set as cells_reduce's direct path: the node's cells whose coordinate along the
+// split axis lies in the region's cell range).
+struct SmallCells {
+  CBox v[2];
+  int c[2][3];
+  int n0[3], n1[3];  // the node's cell range per axis
+  __device__ __forceinline__ void load(const BinnedCtx& B, const Box& b, int cs, int lane) {
+    for (int k = 0; k < 3; ++k) node_cell_range(b, cs, B.nc, k, n0[k], n1[k]);
+    const int e1 = n1[1] - n0[1] + 1, e2 = n1[2] - n0[2] + 1;
+    const int cnt = (n1[0] - n0[0] + 1) * e1 * e2;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int q = lane + 32 * j;
+      c[j][0] = n0[0] + q / (e1 * e2);
+      c[j][1] = n0[1] + (q / e2) % e1;
+      c[j][2] = n0[2] + q % e2;
+      if (q < cnt) {
+        v[j] = B.cells[((int64_t)c[j][0] * B.nc[1] + c[j][1]) * B.nc[2] + c[j][2]];
+      } else {
+        v[j].lo[0] = KD_FAR;
+      }
+    }
+  }
+  // _cells_reduce(region) for a region of the node cut along axis a
+  __device__ __forceinline__ bool reduce(const BinnedCtx& B, int a, const Box& region, int cs,
+                                         Box& out) const {
+    for (int k = 0; k < 3; ++k) {
+      const int r0 = max(region.lo[k] / cs, 0), r1 = min((region.hi[k] - 1) / cs, B.nc[k] - 1);
+      if (r0 > r1) return false;
+    }
+    // axis-a operands by selects (no dynamically indexed local arrays)
+    const int rlo = a == 0 ? region.lo[0] : (a == 1 ? region.lo[1] : region.lo[2]);
+    const int rhi = a == 0 ? region.hi[0] : (a == 1 ? region.hi[1] : region.hi[2]);
+    const int nca = a == 0 ? B.nc[0] : (a == 1 ? B.nc[1] : B.nc[2]);
+    const int na0 = a == 0 ? n0[0] : (a == 1 ? n0[1] : n0[2]);
+    const int na1 = a == 0 ? n1[0] : (a == 1 ? n1[1] : n1[2]);
+    const int c0 = max(rlo / cs, 0), c1 = min((rhi - 1) / cs, nca - 1);
+    const int s0 = max(c0, na0), s1 = min(c1, na1);
+    int ulo0 = KD_FAR, ulo1 = KD_FAR, ulo2 = KD_FAR, uhi0 = -1, uhi1 = -1, uhi2 = -1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int ca = a == 0 ? c[j][0] : (a == 1 ? c[j][1] : c[j][2]);
+      if (v[j].lo[0] != KD_FAR && ca >= s0 && ca <= s1) {
+        ulo0 = min(ulo0, v[j].lo[0]); ulo1 = min(ulo1, v[j].lo[1]); ulo2 = min(ulo2, v[j].lo[2]);
+        uhi0 = max(uhi0, v[j].hi[0]); uhi1 = max(uhi1, v[j].hi[1]); uhi2 = max(uhi2, v[j].hi[2]);
+      }
+    }
+    ulo0 = __reduce_min_sync(0xffffffffu, ulo0);
+    ulo1 = __reduce_min_sync(0xffffffffu, ulo1);
+    ulo2 = __reduce_min_sync(0xffffffffu, ulo2);
+    uhi0 = __reduce_max_sync(0xffffffffu, uhi0);
+    uhi1 = __reduce_max_sync(0xffffffffu, uhi1);
+    uhi2 = __reduce_max_sync(0xffffffffu, uhi2);
+    if (ulo0 == KD_FAR) return false;
+    out.lo[0] = max(ulo0, region.lo[0]); out.hi[0] = min(uhi0, region.hi[0]);
+    out.lo[1] = max(ulo1, region.lo[1]); out.hi[1] = min(uhi1, region.hi[1]);
+    out.lo[2] = max(ulo2, region.lo[2]); out.hi[2] = min(uhi2, region.hi[2]);
+    return out.lo[0] < out.hi[0] && out.lo[1] < out.hi[1] && out.lo[2] < out.hi[2];
+  }
+};
+
 // Slab spans of one axis staged in shared memory by k_decide (with the suffix boxes) when the
 // node's extent along the axis is at most this.
 constexpr int STAGE_SLABS = 1024;
@@ -746,6 +809,16 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
   KdDecision d;
   d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.leaf = b;
   bool split = false;
+  int nlo[3], nhi[3];
+  for (int k = 0; k < 3; ++k) node_cell_range(b, P.cs, B.nc, k, nlo[k], nhi[k]);
+  const bool small =
+      (nhi[0] - nlo[0] + 1) * (nhi[1] - nlo[1] + 1) * (nhi[2] - nlo[2] + 1) <= SMALL_CELLS;
+  SmallCells SC;
+  if (small) SC.load(B, b, P.cs, lane);
+  auto reduce = [&](int a, const Box& region, Box& o) {
+    return small ? SC.reduce(B, a, region, P.cs, o)
+                 : cells_reduce(B, i, b, a, region, P.cs, lane, o);
+  };
   if (!halted(P, vol)) {
     // first strict minimum over (axis, position)
     int ba = -1, bp = 0;
@@ -759,8 +832,8 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
         Box lreg = b, rreg = b, lb, rb;
         lreg.hi[a] = pos[q];
         rreg.lo[a] = pos[q];
-        const bool l = cells_reduce(B, i, b, a, lreg, P.cs, lane, lb);
-        const bool r = cells_reduce(B, i, b, a, rreg, P.cs, lane, rb);
+        const bool l = reduce(a, lreg, lb);
+        const bool r = reduce(a, rreg, rb);
         const int64_t c = (l ? box_vol(lb) : 0) + (r ? box_vol(rb) : 0);
         if (ba < 0 || c < bc) { ba = a; bp = pos[q]; bc = c; bl = lb; br = rb; hl = l; hr = r; }
       }
@@ -791,8 +864,8 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
       Box lreg = b, rreg = b, lb, rb;
       lreg.hi[a] = pos;
       rreg.lo[a] = pos;
-      const bool l = cells_reduce(B, i, b, a, lreg, cs, lane, lb);
-      const bool r = cells_reduce(B, i, b, a, rreg, cs, lane, rb);
+      const bool l = reduce(a, lreg, lb);
+      const bool r = reduce(a, rreg, rb);
       d.axis = a; d.plane = pos;
       if (l) { d.left = lb; d.nchild |= 1; }
       if (r) { d.right = rb; d.nchild |= 2; }
