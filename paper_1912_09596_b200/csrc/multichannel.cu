@@ -195,28 +195,45 @@ __global__ void __launch_bounds__(MC_TX* MC_TY)
         }
         McGather<NCH> gn;
         if (hn) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)kn, dt)), gn);
+        // every channel's bin by the FP32 filter (common.cuh bin_fast); the rare sample with a
+        // channel near a bin edge re-evaluates that channel's reference FP64 lerps
+        const float fx32 = __double2float_rn(g.fx), fy32 = __double2float_rn(g.fy),
+                    fz32 = __double2float_rn(g.fz);
+        int bins[NCH];
+        bool sure = true;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          const uint32_t w0 = g.w0[c], w1 = g.w1[c];
-          const float* tb = sm.u8f;
-          const float c000 = tb[w0 & 0xffu], c001 = tb[(w0 >> 8) & 0xffu];
-          const float c010 = tb[(w0 >> 16) & 0xffu], c011 = tb[w0 >> 24];
-          const float c100 = tb[w1 & 0xffu], c101 = tb[(w1 >> 8) & 0xffu];
-          const float c110 = tb[(w1 >> 16) & 0xffu], c111 = tb[w1 >> 24];
-          const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
-          const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
-          const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, g.fx));
-          const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, g.fx));
-          const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, g.fx));
-          const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, g.fx));
-          const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, g.fy));
-          const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, g.fy));
-          const double value = __dadd_rn(c0, __dmul_rn(c1 - c0, g.fz));
-          const int bi = __double2int_rd(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
-          const int bin = bi < 0 ? 0 : (bi > 255 ? 255 : bi);
-          const float4 col = sm.lut[c][bin];
+          bins[c] = bin_fast(sm.u8f, g.w0[c], g.w1[c], fx32, fy32, fz32);
+          sure &= bins[c] >= 0;
+        }
+        if (!sure) {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            if (bins[c] >= 0) continue;
+            const uint32_t w0 = g.w0[c], w1 = g.w1[c];
+            const float* tb = sm.u8f;
+            const float c000 = tb[w0 & 0xffu], c001 = tb[(w0 >> 8) & 0xffu];
+            const float c010 = tb[(w0 >> 16) & 0xffu], c011 = tb[w0 >> 24];
+            const float c100 = tb[w1 & 0xffu], c101 = tb[(w1 >> 8) & 0xffu];
+            const float c110 = tb[(w1 >> 16) & 0xffu], c111 = tb[w1 >> 24];
+            const float d00 = __fsub_rn(c100, c000), d10 = __fsub_rn(c110, c010);
+            const float d01 = __fsub_rn(c101, c001), d11 = __fsub_rn(c111, c011);
+            const double c00 = __dadd_rn((double)c000, __dmul_rn((double)d00, g.fx));
+            const double c10 = __dadd_rn((double)c010, __dmul_rn((double)d10, g.fx));
+            const double c01 = __dadd_rn((double)c001, __dmul_rn((double)d01, g.fx));
+            const double c11 = __dadd_rn((double)c011, __dmul_rn((double)d11, g.fx));
+            const double c0 = __dadd_rn(c00, __dmul_rn(c10 - c00, g.fy));
+            const double c1 = __dadd_rn(c01, __dmul_rn(c11 - c01, g.fy));
+            const double value = __dadd_rn(c0, __dmul_rn(c1 - c0, g.fz));
+            const int bi = __double2int_rd(__dadd_rn(__dmul_rn(value, 255.0), 0.5));
+            bins[c] = bi < 0 ? 0 : (bi > 255 ? 255 : bi);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const float4 col = sm.lut[c][bins[c]];
           if (col.w > 0.0f) {
-            const double wgt = __dmul_rn(1.0 - acca, sm.corr[c][bin]);
+            const double wgt = __dmul_rn(1.0 - acca, sm.corr[c][bins[c]]);
             accr = __dadd_rn(accr, __dmul_rn(wgt, (double)col.x));
             accg = __dadd_rn(accg, __dmul_rn(wgt, (double)col.y));
             accb = __dadd_rn(accb, __dmul_rn(wgt, (double)col.z));

@@ -118,3 +118,33 @@ def test_tile_frame_multi_async(vs, blobs64):
     fr = TileRenderer(cam.width, cam.height).frame_multi_async(vols, tfs, idx, cam).result()
     np.testing.assert_array_equal(fr.pixels, ref.pixels)
     assert fr.sample_count == ref.sample_count
+
+
+@pytest.mark.parametrize("nch", [2, 4])
+def test_smooth_channels_band_tfs_vs_restatement(vs, nch):
+    """Smooth fields (many interpolated values near bin edges: the FP32 bin filter's fallback
+    path) with narrow-band TFs, 2 and 4 channels, against the restatement bit for bit."""
+    from paper_1912_09596_b200.multichannel import classify_multi, render_float_multi
+
+    n = 36
+    g = np.mgrid[0:n, 0:n, 0:n].astype(np.float64)
+    chans, luts = [], []
+    for c in range(nch):
+        f = 0.5 + 0.5 * np.sin(g[0] / (4.0 + c)) * np.cos(g[1] / (6.0 - c * 0.5)) * \
+            np.sin(g[2] / 3.0 + c)
+        chans.append(np.clip(np.rint(f * 255.0), 0, 255).astype(np.uint8))
+        lut = np.zeros((256, 4), dtype=np.float32)
+        lut[:, c % 3] = 0.9
+        lut[90 + 30 * c:93 + 30 * c, 3] = 0.5   # narrow band per channel
+        lut[200:, 3] = 0.2
+        luts.append(lut)
+    vols = [vs.Volume(u) for u in chans]
+    tfs = [vs.TransferFunction(l) for l in luts]
+    idx = vs.build_index("lbvh", classify_multi(vols, tfs, dilate=True))
+    cam = vs.Camera.orbit((n, n, n), 41.0, 23.0, width=64, height=48)
+    rgba, samples = render_float_multi(vols, tfs, idx, cam)
+    oidx = {"lo": idx.lo, "hi": idx.hi, "left": idx.left, "right": idx.right,
+            "root": idx.root, "height": idx.height()}
+    orgba, osamples = O.render_multi("lbvh", chans, luts, oidx, cam)
+    np.testing.assert_array_equal(samples, osamples)
+    np.testing.assert_array_equal(rgba, orgba)
