@@ -99,10 +99,8 @@ __device__ __forceinline__ void mc_gather(const vs_multi_desc& md, double ox, do
   const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
   g.fx = qx - flx; g.fy = qy - fly; g.fz = qz - flz;
   const int x0r = (int)flx, y0r = (int)fly, z0r = (int)flz;
-  const int x0 = x0r < 0 ? 0 : (x0r > nx - 1 ? nx - 1 : x0r);
-  const int x1 = x0r + 1 < 0 ? 0 : (x0r + 1 > nx - 1 ? nx - 1 : x0r + 1);
-  const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
-  const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
+  const int x0 = min(max(x0r, 0), nx - 1), x1 = min(max(x0r + 1, 0), nx - 1);
+  const int y0 = min(max(y0r, 0), ny - 1), z0 = min(max(z0r, 0), nz - 1);
   const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
   const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
   const uint32_t o0 = (uint32_t)x0 * sxq + yz, o1 = (uint32_t)x1 * sxq + yz;

@@ -184,10 +184,8 @@ struct Integrator {
     const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
     g.fx = qx - flx; g.fy = qy - fly; g.fz = qz - flz;
     const int x0r = (int)flx, y0r = (int)fly, z0r = (int)flz;
-    const int x0 = x0r < 0 ? 0 : (x0r > nx - 1 ? nx - 1 : x0r);
-    const int x1 = x0r + 1 < 0 ? 0 : (x0r + 1 > nx - 1 ? nx - 1 : x0r + 1);
-    const int y0 = y0r < 0 ? 0 : (y0r > ny - 1 ? ny - 1 : y0r);
-    const int z0 = z0r < 0 ? 0 : (z0r > nz - 1 ? nz - 1 : z0r);
+    const int x0 = min(max(x0r, 0), nx - 1), x1 = min(max(x0r + 1, 0), nx - 1);
+    const int y0 = min(max(y0r, 0), ny - 1), z0 = min(max(z0r, 0), nz - 1);
     uint32_t w0, w1;
     if (IDX32) {  // < 2^32 voxels: 32-bit offsets
       const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
