@@ -15,7 +15,7 @@
 namespace vs {
 
 constexpr int MC_MAX = 4;
-constexpr int MC_TX = 16, MC_TY = 8;
+constexpr int MC_TX = 8, MC_TY = 16;  // warp = 8 x 4 pixels, as the single-channel tiles
 
 __global__ void k_or_words(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src,
                            int64_t n) {
