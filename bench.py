@@ -338,53 +338,51 @@ def run_ours(args, rank, ws, local):
         return img
 
     # ---- device-resident loop (value) ------------------------------------------------------
-    prio = torch.cuda.stream(st)
-    prio.__enter__()
-    for k in range(args.warmup):
-        step(k)
-    torch.cuda.synchronize()
-    barrier(ws)
-    with ClockSampler(local) as clk:
-        time.sleep(0.3)
+    with torch.cuda.stream(st):
+        for k in range(args.warmup):
+            step(k)
         torch.cuda.synchronize()
         barrier(ws)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        sb.wait_stream(st)
-        for k in range(args.steps):
-            step(k)
-        st.wait_stream(sb)
-        e1.record(st)
-        torch.cuda.synchronize()
-        total_ms = e0.elapsed_time(e1)
-        # component split (not the headline): rebuild alone, summary kernel alone, render alone
-        bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(3)]
-        reps = max(10, min(args.steps, 100))
-        bev[0][0].record(st)
-        for k in range(reps):
-            rb.rebuild(params[k % NSWEEP])
-        bev[0][1].record(st)
-        summ = []
-        for k in range(reps):
-            rb.set_tf(params[k % NSWEEP])
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(st)
-            rb.launch_summary(st.cuda_stream)
-            b.record(st)
-            rb.launch_tree(st.cuda_stream)
-            summ.append((a, b))
-        rb.rebuild(params[0])
-        rrep = max(3, min(args.steps, 10))
-        samples = 0
-        bev[1][0].record(st)
-        for k in range(rrep):
-            tiles.render(v, tfs[0], idx, cams[k % NSWEEP], idx_desc=index_desc(idx), vol_desc=vd,
-                         cam_desc=cds[k % NSWEEP])
-        bev[1][1].record(st)
-        torch.cuda.synchronize()
-        samples = tiles.sample_total()  # last frame's samples (all ranks)
-    prio.__exit__(None, None, None)
+        with ClockSampler(local) as clk:
+            time.sleep(0.3)
+            torch.cuda.synchronize()
+            barrier(ws)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            sb.wait_stream(st)
+            for k in range(args.steps):
+                step(k)
+            st.wait_stream(sb)
+            e1.record(st)
+            torch.cuda.synchronize()
+            total_ms = e0.elapsed_time(e1)
+            # component split (not the headline): rebuild alone, summary kernel alone, render alone
+            bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(3)]
+            reps = max(10, min(args.steps, 100))
+            bev[0][0].record(st)
+            for k in range(reps):
+                rb.rebuild(params[k % NSWEEP])
+            bev[0][1].record(st)
+            summ = []
+            for k in range(reps):
+                rb.set_tf(params[k % NSWEEP])
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                rb.launch_summary(st.cuda_stream)
+                b.record(st)
+                rb.launch_tree(st.cuda_stream)
+                summ.append((a, b))
+            rb.rebuild(params[0])
+            rrep = max(3, min(args.steps, 10))
+            samples = 0
+            bev[1][0].record(st)
+            for k in range(rrep):
+                tiles.render(v, tfs[0], idx, cams[k % NSWEEP], idx_desc=index_desc(idx),
+                             vol_desc=vd, cam_desc=cds[k % NSWEEP])
+            bev[1][1].record(st)
+            torch.cuda.synchronize()
+            samples = tiles.sample_total()  # last frame's samples (all ranks)
     total_ms = max_over_ranks(total_ms, ws)
     ms_per_step = total_ms / args.steps
     build_ms = max_over_ranks(bev[0][0].elapsed_time(bev[0][1]) / reps, ws)
@@ -417,26 +415,25 @@ def run_ours(args, rank, ws, local):
         torch.cuda.current_stream().wait_stream(build_stream)
         return pub.frame_async(v, tf, index, cams[j]), (tf, b, index)  # pixels -> pinned host
 
-    prio.__enter__()  # frames on the high-priority stream, TF changes on build_stream
-    for k in range(min(args.warmup, 3)):
-        e2e_step(k)[0].result()
-    e2e_runs = []
-    for _ in range(3):  # three passes over the sweep (host-side jitter): the median is reported
-        torch.cuda.synchronize()
-        barrier(ws)
-        e0.record(torch.cuda.current_stream())
-        pending = None
-        for k in range(e_steps):  # frame k's readback overlaps frame k+1's TF change / render
-            nxt = e2e_step(k)
-            if pending is not None:
-                fr = pending[0].result()
-            pending = nxt
-        fr = pending[0].result()
-        e1.record(torch.cuda.current_stream())
-        torch.cuda.synchronize()
-        e2e_runs.append(max_over_ranks(e0.elapsed_time(e1) / e_steps, ws))
-        del fr, pending
-    prio.__exit__(None, None, None)
+    with torch.cuda.stream(st):  # frames on the high-priority stream, TF changes on build_stream
+        for k in range(min(args.warmup, 3)):
+            e2e_step(k)[0].result()
+        e2e_runs = []
+        for _ in range(3):  # three passes over the sweep (host-side jitter): the median is reported
+            torch.cuda.synchronize()
+            barrier(ws)
+            e0.record(torch.cuda.current_stream())
+            pending = None
+            for k in range(e_steps):  # frame k's readback overlaps frame k+1's TF change / render
+                nxt = e2e_step(k)
+                if pending is not None:
+                    fr = pending[0].result()
+                pending = nxt
+            fr = pending[0].result()
+            e1.record(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            e2e_runs.append(max_over_ranks(e0.elapsed_time(e1) / e_steps, ws))
+            del fr, pending
     e2e_ms = statistics.median(e2e_runs)
 
     # ---- the other hierarchies' TF-change rebuilds (north star: "the same rebuild is also
@@ -580,71 +577,69 @@ def run_multi(args, rank, ws, local):
     st = torch.cuda.Stream(priority=-1) if os.environ.get("VSB200_PRIO", "1") == "1" \
         else torch.cuda.current_stream()
     st.wait_stream(torch.cuda.current_stream())
-    prio = torch.cuda.stream(st)
-    prio.__enter__()
-    sb = torch.cuda.Stream()
-    built = [torch.cuda.Event(), torch.cuda.Event()]
-    rendered = [torch.cuda.Event(), torch.cuda.Event()]
+    with torch.cuda.stream(st):
+        sb = torch.cuda.Stream()
+        built = [torch.cuda.Event(), torch.cuda.Event()]
+        rendered = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def step(k):
-        j, b = k % NSWEEP, k % 2
-        with torch.cuda.stream(sb):
-            sb.wait_event(rendered[b])
-            rbs[b].rebuild(params[j])
-            built[b].record(sb)
-        st.wait_event(built[b])
-        img = tiles.render_multi(vols, tfs[j], idxs[b], cams[j], checked=False)
-        rendered[b].record(st)
-        return img
+        def step(k):
+            j, b = k % NSWEEP, k % 2
+            with torch.cuda.stream(sb):
+                sb.wait_event(rendered[b])
+                rbs[b].rebuild(params[j])
+                built[b].record(sb)
+            st.wait_event(built[b])
+            img = tiles.render_multi(vols, tfs[j], idxs[b], cams[j], checked=False)
+            rendered[b].record(st)
+            return img
 
-    for k in range(args.warmup):
-        step(k)
-    torch.cuda.synchronize()
-    barrier(ws)
-    with ClockSampler(local) as clk:
-        time.sleep(0.3)
-        torch.cuda.synchronize()
-        barrier(ws)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        tiles.multi_flags()
-        e0.record(st)
-        sb.wait_stream(st)
-        for k in range(args.steps):
+        for k in range(args.warmup):
             step(k)
-        st.wait_stream(sb)
-        e1.record(st)
-        torch.cuda.synchronize()
-    if tiles.multi_flags() & 4:
-        raise RuntimeError("a timed frame exceeded the segment capacity (incomplete frame)")
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
-    samples = tiles.sample_total()
-    # e2e through the public API: per-step host LUTs -> classify_multi -> build_index -> frame
-    luts = [[tf.lut for tf in tl] for tl in tfs]
-    e_steps = args.steps
-    build_stream = torch.cuda.Stream()
-    e2e_runs = []
-    for _ in range(3):  # three passes over the sweep (host-side jitter): the median is reported
         torch.cuda.synchronize()
         barrier(ws)
-        e0.record(st)
-        pending = None
-        for k in range(e_steps):  # frame k's readback overlaps frame k+1's TF change / render
-            j = k % NSWEEP
-            with torch.cuda.stream(build_stream):  # TF change overlapping the previous render
-                tl = [vs.TransferFunction(l) for l in luts[j]]
-                b = classify_multi(vols, tl, dilate=True)
-                index = vs.build_index("lbvh", b)
-            torch.cuda.current_stream().wait_stream(build_stream)
-            nxt = (tiles.frame_multi_async(vols, tl, index, cams[j]), (tl, b, index))
-            if pending is not None:
-                frame = pending[0].result()
-            pending = nxt
-        frame = pending[0].result()
-        e1.record(st)
-        torch.cuda.synchronize()
-        e2e_runs.append(max_over_ranks(e0.elapsed_time(e1) / e_steps, ws))
-        del frame, pending
-    prio.__exit__(None, None, None)
+        with ClockSampler(local) as clk:
+            time.sleep(0.3)
+            torch.cuda.synchronize()
+            barrier(ws)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tiles.multi_flags()
+            e0.record(st)
+            sb.wait_stream(st)
+            for k in range(args.steps):
+                step(k)
+            st.wait_stream(sb)
+            e1.record(st)
+            torch.cuda.synchronize()
+        if tiles.multi_flags() & 4:
+            raise RuntimeError("a timed frame exceeded the segment capacity (incomplete frame)")
+        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+        samples = tiles.sample_total()
+        # e2e through the public API: per-step host LUTs -> classify_multi -> build_index -> frame
+        luts = [[tf.lut for tf in tl] for tl in tfs]
+        e_steps = args.steps
+        build_stream = torch.cuda.Stream()
+        e2e_runs = []
+        for _ in range(3):  # three passes over the sweep (host-side jitter): the median is reported
+            torch.cuda.synchronize()
+            barrier(ws)
+            e0.record(st)
+            pending = None
+            for k in range(e_steps):  # frame k's readback overlaps frame k+1's TF change / render
+                j = k % NSWEEP
+                with torch.cuda.stream(build_stream):  # TF change overlapping the previous render
+                    tl = [vs.TransferFunction(l) for l in luts[j]]
+                    b = classify_multi(vols, tl, dilate=True)
+                    index = vs.build_index("lbvh", b)
+                torch.cuda.current_stream().wait_stream(build_stream)
+                nxt = (tiles.frame_multi_async(vols, tl, index, cams[j]), (tl, b, index))
+                if pending is not None:
+                    frame = pending[0].result()
+                pending = nxt
+            frame = pending[0].result()
+            e1.record(st)
+            torch.cuda.synchronize()
+            e2e_runs.append(max_over_ranks(e0.elapsed_time(e1) / e_steps, ws))
+            del frame, pending
     e2e_ms = statistics.median(e2e_runs)
     if rank != 0:
         return
@@ -696,7 +691,8 @@ def run_multi(args, rank, ws, local):
                 "path": "TransferFunction x nch->classify_multi->build_index('lbvh') on a "
                         "build stream->TileRenderer.frame_multi_async(...).result(); median "
                         "of 3 passes"},
-        "gpu_launches": (nch + (nch - 1) + 7 + 2) * args.steps,  # summaries, ORs, tree (as above), render
+        # summaries, ORs, tree (as the single-channel step), render
+        "gpu_launches": (nch + (nch - 1) + 7 + 2) * args.steps,
         "cpu_baseline": cpu, "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
