@@ -300,7 +300,7 @@ def run_ours(args, rank, ws, local):
 
     n = args.size
     u8, nblobs = make_volume(n)
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tfs = sweep_tfs()
     cams = cameras(v.dims)
     params = tf_params_device(tfs)
@@ -561,7 +561,7 @@ def run_multi(args, rank, ws, local):
     n, nch = args.size, args.channels
     nblobs = max(1, 25600 * n ** 3 // 1024 ** 3)
     u8s = [gen_blobs_u8((n, n, n), n=nblobs, seed=7 + c, sigma=3.0) for c in range(nch)]
-    vols = [vs.Volume(u) for u in u8s]
+    vols = [vs.Volume.from_u8(u) for u in u8s]
     interleaved_quads(vols)  # channel-interleaved trilinear gather volume, built once
     tfs = channel_tfs(nch)
     cams = cameras(vols[0].dims)

@@ -205,6 +205,27 @@ typedef struct vs_rows_desc {
   int nrows, stripe, nparts, part;
 } vs_rows_desc;
 
+/* Per-call renderer options (SURVEY §8b threading row: no global mutable state -- every
+ * setting travels with the call).  opts == NULL means the defaults below (parity mode). */
+enum {
+  VS_RO_U8_TABLE = 1,          /* u8 -> f32 through a shared-memory table (same values)     */
+  VS_RO_FP64_BINS = 2,         /* every sample's bin in FP64 (no exact FP32 bin filter)      */
+  VS_RO_GENERIC_TRAVERSAL = 4, /* generic generator-stack traversal kernel (same intervals)  */
+  VS_RO_BRICK_NO_RUNS = 16,    /* brick DDA evaluates every occupied brick's slab            */
+  VS_RO_DEFAULT = VS_RO_U8_TABLE
+};
+typedef struct vs_render_opts {
+  /* Early ray termination: a ray stops once its accumulated opacity reaches 1 - ert_eps, so
+   * every RGBA channel is within ert_eps of the full integral (LUT colours <= 1) and fewer
+   * samples are taken.  <= 0: off, the reference integrator exactly (render.py:758 counts
+   * every lattice point; the default). */
+  double ert_eps;
+  int flags;        /* VS_RO_* code-path bits; all give identical results                */
+  int trav_steps;   /* generic kernels: traversal steps per turn (<= 0 unbounded; dflt 1) */
+  int sample_steps; /* fused kernel: lattice samples per turn (<= 0 unbounded; dflt 1)    */
+  int reserved;
+} vs_render_opts;
+
 /* Render rows of a frame.  lut: (256,4) float32 device; corr: 256 float64 device holding
  * 1 - (1 - lut[b,3])^dt computed with libm pow (render.py:752).  Outputs per local row-major
  * pixel: rgba8 (quantised), optional float64 premultiplied rgba, optional per-pixel sample
@@ -214,21 +235,13 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
               const float* lut, const double* corr, double dt, int nearest,
               const vs_rows_desc* rows_opt, uint8_t* rgba8, double* rgba64_opt,
               int32_t* samples_opt, unsigned long long* total_opt, int* flags, void* ws,
-              size_t ws_bytes, int seg_cap, vs_stream_t stream);
+              size_t ws_bytes, int seg_cap, const vs_render_opts* opts, vs_stream_t stream);
 /* Two-phase rendering (ws != NULL, seg_cap > 0): a traversal kernel stores each ray's merged
  * segments (up to seg_cap; rays with more are re-traversed inside the integration kernel),
  * then an integration kernel consumes them.  Workspace bytes for npix pixels: */
 size_t vs_render_workspace(int64_t npix, int seg_cap);
 
-/* Renderer turn sizes of the traversal / sampling interleave (<= 0: unbounded). */
-void vs_set_render_tuning(int trav_steps, int samples);
-/* Early ray termination for the calling thread's subsequent vs_render calls: a ray stops once
- * its accumulated opacity reaches 1 - eps, so every RGBA channel is within eps of the full
- * integral (LUT colours <= 1) and fewer samples are taken.  eps <= 0: off, the reference's
- * integrator exactly (render.py:758 counts every lattice point; the default). */
-void vs_set_render_ert(double eps);
-/* Renderer code-path options (bit 0: u8 -> f32 via a shared-memory table); same results. */
-void vs_set_render_options(int opts);
+
 
 /* ---- multi-channel volumes (configs[4]; no reference equivalent, see multichannel.cu) ---- */
 typedef struct vs_int2 { int32_t x, y; } int2_t;
@@ -255,7 +268,8 @@ int vs_render_multi_integrate(const vs_multi_desc* md, const vs_camera_desc* cam
  * int2, ray-minor) and counts (npix). */
 int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
                        const vs_camera_desc* cam, double dt, const vs_rows_desc* rows_opt,
-                       int2_t* segs, int* counts, int cap, int* flags, vs_stream_t stream);
+                       int2_t* segs, int* counts, int cap, int* flags,
+                       const vs_render_opts* opts, vs_stream_t stream);
 
 /* Leaf-brick bit grid of an LBVH from its brick_coords (n from n_dev, or cap if NULL). */
 int vs_lbvh_brick_grid(const int32_t* brick_coords, const int* n_dev, int64_t cap, int nbx,

@@ -12,9 +12,9 @@ from .kdtree import (BuildParams, CellBoxList, KdTree, SplitPlane, binned_best_p
                      empty_kdtree, precompute_cell_boxes, sweep_best_plane)
 from .lbvh import (BrickSet, Lbvh, MortonRangeError, build_lbvh, empty_lbvh, flag_bricks,
                    leaf_boxes, morton_decode, morton_encode)
-from .render import (DEFAULT_DT, Camera, Frame, Ray, RaySegmentList, integrate, render_float,
-                     render_frame, sample_count_of, traverse_grid, traverse_hybrid, traverse_kd,
-                     traverse_lbvh, traverse_naive)
+from .render import (DEFAULT_DT, Camera, Frame, Ray, RaySegmentList, SpatialIndex, integrate,
+                     render_float, render_frame, sample_count_of, traverse_grid, traverse_hybrid,
+                     traverse_kd, traverse_lbvh, traverse_naive)
 from .service import Reply, Session, handle_message
 from .svt import (MacroGrid, SvtGrid, box_count, build_svt_grid, derive_macro_grid,
                   shrink_to_occupied)

@@ -50,17 +50,14 @@ SIGNATURES: dict[str, tuple] = {
     "vs_kd_result_free": (None, [P]),
     "vs_cell_boxes": (i32, [P, i32, i32, i32, i32, P, P, P, P]),
     "vs_kd_best_plane": (i32, [P, i32, i32, i32, P, i32, i32, i32, P, P]),
-    "vs_set_render_tuning": (None, [i32, i32]),
-    "vs_set_render_options": (None, [i32]),
-    "vs_set_render_ert": (None, [C.c_double]),
     "vs_build_quads": (i32, [P, i32, i32, i32, P, P]),
     "vs_mquads_words": (i32, [i32]),
     "vs_build_mquads": (i32, [P, i32, i32, i32, i32, P, P]),
     "vs_or_words": (i32, [P, P, i64, P]),
     "vs_render_multi_integrate": (i32, [P, P, C.c_double, P, P, P, i32, P, P, P, P, P, P]),
-    "vs_render_segments": (i32, [P, P, P, C.c_double, P, P, P, i32, P, P]),
+    "vs_render_segments": (i32, [P, P, P, C.c_double, P, P, P, i32, P, P, P]),
     "vs_lbvh_brick_grid": (i32, [P, P, i64, i32, i32, i32, P, P]),
-    "vs_render": (i32, [P, P, P, P, P, C.c_double, i32, P, P, P, P, P, P, P, SZ, i32, P]),
+    "vs_render": (i32, [P, P, P, P, P, C.c_double, i32, P, P, P, P, P, P, P, SZ, i32, P, P]),
     "vs_render_workspace": (SZ, [i64, i32]),
     "vs_traverse_rays": (i32, [P, i32, i32, i32, P, P, i32, P, i32, P, P, P]),
     "vs_integrate_rays": (i32, [P, P, P, P, P, i32, i32, P, P, C.c_double, i32, P, P, P]),

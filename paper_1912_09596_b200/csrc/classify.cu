@@ -778,6 +778,7 @@ int vs_classify_summary(const uint8_t* bins, int nx, int ny, int nz, const vs_tf
   if (!bins || !tf || !summary || nx < 1 || ny < 1 || nz < 1)
     return fail_arg("vs_classify_summary");
   if (nz % 16 != 0) return fail_arg("vs_classify_summary needs nz % 16 == 0");
+  if ((uintptr_t)bins & 15) return fail_arg("vs_classify_summary needs 16-byte aligned bins");
   const int nbx = (int)cdiv(nx, 8), nby = (int)cdiv(ny, 8), nbz = (int)cdiv(nz, 8);
   const int nzc = (int)cdiv(nz, 512);
   const int64_t ntasks = (int64_t)nbx * nby * nzc;

@@ -720,15 +720,30 @@ struct SegmentSource {
   }
 };
 
-// while-while turn sizes (vs_set_render_tuning): traversal steps / lattice samples per turn
-static int g_trav_budget = 1, g_sample_budget = 1;
-// early ray termination (vs_set_render_ert): opacity threshold, 2.0 = off (parity mode)
-static thread_local double g_ert_a = 2.0;
-// bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float conversion)
-// bit1: k_integrate_segments evaluates every sample's bin in FP64 (no FP32 bin filter)
-// bit2: generic k_segments for the LBVH brick DDA / grid / hybrid (else the flat-loop kernels)
-// bit4: k_segments_brick evaluates every occupied brick's slab (no run shortcut)
-static int g_render_opts = 1;
+// Per-call renderer configuration, resolved from the caller's vs_render_opts (no global or
+// thread-local state: concurrent callers on other threads / streams never see each other's
+// settings).
+//   opts bit0: u8 -> f32 by shared-memory table (else the exact 64-bit integer-to-float path)
+//   opts bit1: k_integrate_segments evaluates every sample's bin in FP64 (no FP32 bin filter)
+//   opts bit2: generic k_segments for the LBVH brick DDA / grid / hybrid / k-d (else flat loops)
+//   opts bit4: k_segments_brick evaluates every occupied brick's slab (no run shortcut)
+struct RenderCfg {
+  int opts = VS_RO_DEFAULT;
+  int trav_budget = 1, sample_budget = 1;  // while-while turn sizes of the generic kernels
+  double ert_a = 2.0;                      // early ray termination threshold, 2.0 = off
+  void* seg_ws = nullptr;                  // two-phase workspace (segments + counts)
+  int seg_cap = 0;
+};
+
+static RenderCfg render_cfg(const vs_render_opts* o) {
+  RenderCfg c;
+  if (!o) return c;
+  c.opts = o->flags;
+  c.trav_budget = o->trav_steps > 0 ? o->trav_steps : (1 << 30);
+  c.sample_budget = o->sample_steps > 0 ? o->sample_steps : (1 << 30);
+  c.ert_a = o->ert_eps > 0.0 ? 1.0 - o->ert_eps : 2.0;
+  return c;
+}
 
 template <int KIND>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
@@ -1629,42 +1644,39 @@ __global__ void k_brick_grid(const int32_t* __restrict__ coords, const int* __re
   atomicOr(bits + (lin >> 5), 1u << (lin & 31));
 }
 
-static thread_local void* g_seg_ws = nullptr;  // set by vs_render for its own launches
-static thread_local int g_seg_cap = 0;
-
 template <int K>
 static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                           const vs_index_desc& ix, const vs_camera_desc& c, const float* lut,
                           const double* corr, double dt, int nearest, const vs_rows_desc& rows,
                           uint8_t* rgba8, double* rgba64, int32_t* samples,
-                          unsigned long long* total, int* flags) {
-  if (g_seg_ws && g_seg_cap > 0) {
+                          unsigned long long* total, int* flags, const RenderCfg& cfg) {
+  if (cfg.seg_ws && cfg.seg_cap > 0) {
     const int64_t npix = (int64_t)rows.nrows * c.width;
-    int2* segs = static_cast<int2*>(g_seg_ws);
-    int* counts = reinterpret_cast<int*>(segs + (int64_t)g_seg_cap * npix);
-    if (K == KIND_LBVH_BRICK && !(g_render_opts & 4))
+    int2* segs = static_cast<int2*>(cfg.seg_ws);
+    int* counts = reinterpret_cast<int*>(segs + (int64_t)cfg.seg_cap * npix);
+    if (K == KIND_LBVH_BRICK && !(cfg.opts & 4))
       k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          v, ix, c, rows, dt, segs, counts, g_seg_cap, flags, (g_render_opts & 16) ? 1 : 0);
-    else if (K == VS_KIND_GRID && !(g_render_opts & 4))
+          v, ix, c, rows, dt, segs, counts, cfg.seg_cap, flags, (cfg.opts & 16) ? 1 : 0);
+    else if (K == VS_KIND_GRID && !(cfg.opts & 4))
       k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                  counts, g_seg_cap, flags);
-    else if (K == VS_KIND_KD && !(g_render_opts & 4))
+                                                                  counts, cfg.seg_cap, flags);
+    else if (K == VS_KIND_KD && !(cfg.opts & 4))
       k_segments_kd<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                counts, g_seg_cap, flags);
-    else if (K == VS_KIND_HYBRID && !(g_render_opts & 4))
+                                                                counts, cfg.seg_cap, flags);
+    else if (K == VS_KIND_HYBRID && !(cfg.opts & 4))
       k_segments_hybrid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                    counts, g_seg_cap, flags);
+                                                                    counts, cfg.seg_cap, flags);
     else
       k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                 counts, g_seg_cap, flags,
-                                                                 g_trav_budget);
-    const bool idx32 = (int64_t)v.nx * v.ny * v.nz < (1LL << 32), ert = g_ert_a <= 1.0;
+                                                                 counts, cfg.seg_cap, flags,
+                                                                 cfg.trav_budget);
+    const bool idx32 = (int64_t)v.nx * v.ny * v.nz < (1LL << 32), ert = cfg.ert_a <= 1.0;
     const bool lean = !v.field && v.quads && !nearest;  // k_integrate_segments' rays exist
     if (lean) {
 #define VS_INTEGRATE(I32, E)                                                                  \
   k_integrate_segments<K, I32, E><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(               \
-      v, ix, c, lut, corr, dt, rows, segs, counts, g_seg_cap, rgba8, rgba64, samples, total,  \
-      flags, g_ert_a, (g_render_opts & 2) ? 0 : 1)
+      v, ix, c, lut, corr, dt, rows, segs, counts, cfg.seg_cap, rgba8, rgba64, samples, total,  \
+      flags, cfg.ert_a, (cfg.opts & 2) ? 0 : 1)
       if (idx32) {
         if (ert) VS_INTEGRATE(true, true); else VS_INTEGRATE(true, false);
       } else {
@@ -1674,18 +1686,18 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     }
     else if (ert)
       k_integrate_fallback<K, true><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64,
-          samples, total, flags, g_render_opts, g_ert_a);
+          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, cfg.seg_cap, rgba8, rgba64,
+          samples, total, flags, cfg.opts, cfg.ert_a);
     else
       k_integrate_fallback<K, false><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, g_seg_cap, rgba8, rgba64,
-          samples, total, flags, g_render_opts, g_ert_a);
+          v, ix, c, lut, corr, dt, nearest, rows, segs, counts, cfg.seg_cap, rgba8, rgba64,
+          samples, total, flags, cfg.opts, cfg.ert_a);
     return;
   }
   k_render<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, lut, corr, dt, nearest, rows,
                                                           rgba8, rgba64, samples, total, flags,
-                                                          g_trav_budget, g_sample_budget,
-                                                          g_render_opts, g_ert_a);
+                                                          cfg.trav_budget, cfg.sample_budget,
+                                                          cfg.opts, cfg.ert_a);
 }
 
 }  // namespace vs
@@ -1703,7 +1715,7 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
               const float* lut, const double* corr, double dt, int nearest,
               const vs_rows_desc* rows_opt, uint8_t* rgba8, double* rgba64_opt,
               int32_t* samples_opt, unsigned long long* total_opt, int* flags, void* ws,
-              size_t ws_bytes, int seg_cap, vs_stream_t stream) {
+              size_t ws_bytes, int seg_cap, const vs_render_opts* opts, vs_stream_t stream) {
   if (!vol || !ix || !cam || !lut || !corr || !rgba8 || !flags || !(dt > 0.0))
     return fail_arg("vs_render");
   if (!vol->bins || vol->nx < 1 || vol->ny < 1 || vol->nz < 1) return fail_arg("vs_render: volume");
@@ -1729,39 +1741,37 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
   dim3 grid((unsigned)cdiv(cam->width, RENDER_TX), (unsigned)cdiv(rows.nrows, RENDER_TY));
   cudaStream_t st = S(stream);
   const int64_t npix = (int64_t)rows.nrows * cam->width;
+  RenderCfg cfg = render_cfg(opts);
   if (ws && seg_cap > 0) {
     if (ws_bytes < vs_render_workspace(npix, seg_cap)) return VS_EWORKSPACE;
     if ((reinterpret_cast<uintptr_t>(ws) & 15) != 0) return fail_arg("vs_render: ws alignment");
-    g_seg_ws = ws;
-    g_seg_cap = seg_cap;
-  } else {
-    g_seg_ws = nullptr;
-    g_seg_cap = 0;
+    cfg.seg_ws = ws;
+    cfg.seg_cap = seg_cap;
   }
   switch (kind) {
     case VS_KIND_NAIVE:
       launch_render<VS_KIND_NAIVE>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
-                                   rgba64_opt, samples_opt, total_opt, flags);
+                                   rgba64_opt, samples_opt, total_opt, flags, cfg);
       break;
     case VS_KIND_GRID:
       launch_render<VS_KIND_GRID>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
-                                  rgba64_opt, samples_opt, total_opt, flags);
+                                  rgba64_opt, samples_opt, total_opt, flags, cfg);
       break;
     case VS_KIND_LBVH:
       if (ix->brick_bits)
         launch_render<KIND_LBVH_BRICK>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows,
-                                       rgba8, rgba64_opt, samples_opt, total_opt, flags);
+                                       rgba8, rgba64_opt, samples_opt, total_opt, flags, cfg);
       else
       launch_render<VS_KIND_LBVH>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
-                                  rgba64_opt, samples_opt, total_opt, flags);
+                                  rgba64_opt, samples_opt, total_opt, flags, cfg);
       break;
     case VS_KIND_KD:
       launch_render<VS_KIND_KD>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
-                                rgba64_opt, samples_opt, total_opt, flags);
+                                rgba64_opt, samples_opt, total_opt, flags, cfg);
       break;
     case VS_KIND_HYBRID:
       launch_render<VS_KIND_HYBRID>(grid, st, *vol, *ix, *cam, lut, corr, dt, nearest, rows, rgba8,
-                                    rgba64_opt, samples_opt, total_opt, flags);
+                                    rgba64_opt, samples_opt, total_opt, flags, cfg);
       break;
     default:
       return fail_arg("vs_render: kind");
@@ -1777,20 +1787,13 @@ int vs_build_quads(const uint8_t* bins, int nx, int ny, int nz, uint32_t* quads,
   return check_launch("k_build_quads");
 }
 
-void vs_set_render_options(int opts) { g_render_opts = opts; }
-
-void vs_set_render_ert(double eps) { g_ert_a = eps > 0.0 ? 1.0 - eps : 2.0; }
-
-void vs_set_render_tuning(int trav_steps, int samples) {
-  g_trav_budget = trav_steps > 0 ? trav_steps : (1 << 30);
-  g_sample_budget = samples > 0 ? samples : (1 << 30);
-}
-
 int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
                        const vs_camera_desc* cam, double dt, const vs_rows_desc* rows_opt,
-                       int2_t* segs, int* counts, int cap, int* flags, vs_stream_t stream) {
+                       int2_t* segs, int* counts, int cap, int* flags,
+                       const vs_render_opts* opts, vs_stream_t stream) {
   if (!vol || !ix || !cam || !segs || !counts || !flags || cap < 1 || !(dt > 0.0))
     return fail_arg("vs_render_segments");
+  const RenderCfg cfg = render_cfg(opts);
   vs_rows_desc rows;
   if (rows_opt) rows = *rows_opt;
   else { rows.nrows = cam->height; rows.stripe = cam->height; rows.nparts = 1; rows.part = 0; }
@@ -1801,42 +1804,42 @@ int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
   switch (ix->kind) {
     case VS_KIND_NAIVE:
       k_segments<VS_KIND_NAIVE><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+          *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
       break;
     case VS_KIND_GRID:
-      if (!(g_render_opts & 4))
+      if (!(cfg.opts & 4))
         k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(*vol, *ix, *cam, rows, dt, sg,
                                                                 counts, cap, flags);
       else
         k_segments<VS_KIND_GRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
       break;
     case VS_KIND_LBVH:
-      if (ix->brick_bits && !(g_render_opts & 4))
+      if (ix->brick_bits && !(cfg.opts & 4))
         k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, (g_render_opts & 16) ? 1 : 0);
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, (cfg.opts & 16) ? 1 : 0);
       else if (ix->brick_bits)
         k_segments<KIND_LBVH_BRICK><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
       else
         k_segments<VS_KIND_LBVH><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
       break;
     case VS_KIND_KD:
-      if (!(g_render_opts & 4))
+      if (!(cfg.opts & 4))
         k_segments_kd<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(*vol, *ix, *cam, rows, dt, sg,
                                                                 counts, cap, flags);
       else
         k_segments<VS_KIND_KD><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
       break;
     case VS_KIND_HYBRID:
-      if (!(g_render_opts & 4))
+      if (!(cfg.opts & 4))
         k_segments_hybrid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(*vol, *ix, *cam, rows, dt, sg,
                                                                 counts, cap, flags);
       else
         k_segments<VS_KIND_HYBRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, g_trav_budget);
+            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
       break;
     default:
       return fail_arg("vs_render_segments: kind");

@@ -18,6 +18,7 @@ from .volume import Aabb
 
 DEFAULT_CELL_SIZE = 8
 DEFAULT_BINS = 4
+MAX_NZ = 1024  # vs_kd_build / vs_kd_best_plane: a z row is at most one warp of 32-bit words
 
 
 @dataclass(frozen=True)
@@ -143,6 +144,10 @@ def build_kdtree(g, params: BuildParams | None = None) -> KdTree:
     params = params or BuildParams()
     b = g.binary
     nx, ny, nz = g.dims
+    if nz > MAX_NZ:
+        # the span passes give one z row to one warp (32 lanes x 32-bit words)
+        raise ValueError(f"build_kdtree supports nz <= {MAX_NZ} (got dims {g.dims}); "
+                         "store the longest axis first (x or y)")
     h = C.c_void_p()
     try:
         call("vs_kd_build", ptr(b.packed()), nx, ny, nz, int(params.mode == "deep"),

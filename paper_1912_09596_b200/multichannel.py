@@ -156,7 +156,7 @@ def render_multi_rows(volumes, tfs, index, cam: Camera, target: MultiTarget, dt:
     cd = camera_desc(cam)
     rp = None if rows is None else C.addressof(rows)
     call("vs_render_segments", C.addressof(vd), C.addressof(idx), C.addressof(cd), float(dt), rp,
-         ptr(target.segs), ptr(target.counts), target.cap, ptr(target.flags), stream())
+         ptr(target.segs), ptr(target.counts), target.cap, ptr(target.flags), None, stream())
     call("vs_render_multi_integrate", C.addressof(md), C.addressof(cd), float(dt), rp,
          ptr(target.segs), ptr(target.counts), target.cap, ptr(target.rgba8), ptr(target.rgba64),
          ptr(target.samples), ptr(target.total), ptr(target.flags), stream())

@@ -21,6 +21,8 @@ import torch
 from . import _lib
 from ._lib import call, ptr, stream
 from .bench import index_kind
+from .hybrid import HybridGrid
+from .kdtree import KdTree
 from .lbvh import Lbvh
 from .svt import MacroGrid
 from .volume import TransferFunction, Volume
@@ -28,6 +30,9 @@ from .volume import TransferFunction, Volume
 DEFAULT_DT = 0.5
 KIND_ID = {"naive": 0, "grid": 1, "lbvh": 2, "kd": 3, "hybrid": 4}
 RF_OVERFLOW, RF_ORDER = 1, 2
+
+# render.py:41 -- what render_frame / index_kind accept as an index
+SpatialIndex = None | MacroGrid | Lbvh | KdTree | HybridGrid
 
 
 def _normalize(v: np.ndarray) -> np.ndarray:
@@ -164,6 +169,23 @@ class RowsDesc(C.Structure):
     _fields_ = [("nrows", C.c_int), ("stripe", C.c_int), ("nparts", C.c_int), ("part", C.c_int)]
 
 
+# vs_render_opts code-path bits (include/vsb200.h); every combination gives the same frame
+RO_U8_TABLE, RO_FP64_BINS, RO_GENERIC_TRAVERSAL, RO_BRICK_NO_RUNS = 1, 2, 4, 16
+RO_DEFAULT = RO_U8_TABLE
+
+
+class RenderOpts(C.Structure):
+    """vs_render_opts: every renderer setting travels with the call (no library state)."""
+
+    _fields_ = [("ert_eps", C.c_double), ("flags", C.c_int), ("trav_steps", C.c_int),
+                ("sample_steps", C.c_int), ("reserved", C.c_int)]
+
+
+def render_opts(ert_eps: float = 0.0, flags: int = RO_DEFAULT, trav_steps: int = 1,
+                sample_steps: int = 1) -> RenderOpts:
+    return RenderOpts(float(ert_eps), int(flags), int(trav_steps), int(sample_steps), 0)
+
+
 def volume_desc(v: Volume, quads: bool = True) -> VolumeDesc:
     nx, ny, nz = v.dims
     q = v.quads() if (quads and v.field is None) else None
@@ -260,11 +282,13 @@ class RenderTarget:
 def render_rows(v: Volume, tf: TransferFunction, index, cam: Camera, target: RenderTarget,
                 dt: float = DEFAULT_DT, nearest: bool = False, rows: RowsDesc | None = None,
                 idx_desc: IndexDesc | None = None, vol_desc: VolumeDesc | None = None,
-                cam_desc: CameraDesc | None = None, zero: bool = True, ert_eps: float = 0.0):
+                cam_desc: CameraDesc | None = None, zero: bool = True, ert_eps: float = 0.0,
+                flags: int = RO_DEFAULT, opts: RenderOpts | None = None):
     """Launch the renderer for (a stripe set of) the frame into ``target`` (async).
 
     ``ert_eps`` > 0 enables early ray termination at accumulated opacity 1 - ert_eps (RGBA
-    within ert_eps of the full integral, fewer samples); 0 is the reference's integrator."""
+    within ert_eps of the full integral, fewer samples); 0 is the reference's integrator.
+    ``flags`` picks code paths (RO_*; identical results).  ``opts`` overrides both."""
     lut, corr = tf_device(tf, dt)
     if zero:
         target.total.zero_()
@@ -272,12 +296,13 @@ def render_rows(v: Volume, tf: TransferFunction, index, cam: Camera, target: Ren
     idx_desc = idx_desc or index_desc(index)
     vol_desc = vol_desc or volume_desc(v)
     cam_desc = cam_desc or camera_desc(cam)
-    _lib.lib().vs_set_render_ert(float(ert_eps))
+    opts = opts or render_opts(ert_eps, flags)
     call("vs_render", C.addressof(vol_desc), C.addressof(idx_desc), C.addressof(cam_desc),
          ptr(lut), ptr(corr), float(dt), int(nearest),
          None if rows is None else C.addressof(rows), ptr(target.rgba8), ptr(target.rgba64),
          ptr(target.samples), ptr(target.total), ptr(target.flags), ptr(target.ws),
-         0 if target.ws is None else target.ws.numel(), target.seg_cap, stream())
+         0 if target.ws is None else target.ws.numel(), target.seg_cap, C.addressof(opts),
+         stream())
 
 
 def render_frame(v: Volume, tf: TransferFunction, index, cam: Camera, dt: float = DEFAULT_DT,
@@ -296,11 +321,15 @@ def render_frame(v: Volume, tf: TransferFunction, index, cam: Camera, dt: float 
 
 
 def render_float(v: Volume, tf: TransferFunction, index, cam: Camera, dt: float = DEFAULT_DT,
-                 interp: str = "trilinear", ert_eps: float = 0.0):
+                 interp: str = "trilinear", ert_eps: float = 0.0, flags: int = RO_DEFAULT,
+                 rows: RowsDesc | None = None):
     """(float64 premultiplied RGBA (h,w,4), per-pixel samples (h,w)) -- the float output the
-    parity tests compare with the reference's _k_integrate accumulators."""
-    tgt = RenderTarget(cam.width, cam.height, want_rgba64=True, want_samples=True)
-    render_rows(v, tf, index, cam, tgt, dt=dt, nearest=interp == "nearest", ert_eps=ert_eps)
+    parity tests compare with the reference's _k_integrate accumulators.  ``rows`` renders a
+    row band / stripe set only (shape (rows.nrows, w, ...))."""
+    nrows = cam.height if rows is None else rows.nrows
+    tgt = RenderTarget(cam.width, nrows, want_rgba64=True, want_samples=True)
+    render_rows(v, tf, index, cam, tgt, dt=dt, nearest=interp == "nearest", rows=rows,
+                ert_eps=ert_eps, flags=flags)
     _check_flags(tgt.flags)
     return tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy().astype(np.int64)
 
@@ -386,7 +415,7 @@ def integrate(ray: Ray, segments: RaySegmentList, v: Volume, tf: TransferFunctio
 def sample_count_of(ray: Ray, segments: RaySegmentList, dims, dt: float = DEFAULT_DT) -> int:
     """Lattice points of the ray inside the segments."""
     dev = _lib.device()
-    v = Volume(torch.zeros(tuple(int(d) for d in dims), dtype=torch.uint8, device=dev))
+    v = Volume.from_u8(torch.zeros(tuple(int(d) for d in dims), dtype=torch.uint8, device=dev))
     lut = torch.zeros((256, 4), dtype=torch.float32, device=dev)
     corr = torch.zeros(256, dtype=torch.float64, device=dev)
     _, n = _integrate(ray, segments, v, lut, corr, dt, False)

@@ -76,17 +76,33 @@ U8_FIELD = (np.arange(256, dtype=np.float64) / 255.0).astype(np.float32)
 class Volume:
     """Dense scalar field normalised to [0, 1], shape (nx, ny, nz), C-order (volume.py:64-81).
 
-    ``data`` may be a float array (quantised on the device) or uint8 bins (taken as the field
-    ``f32(u/255)``, exactly what load_raw returns for 8-bit files).  numpy or torch input."""
+    ``Volume(data)`` follows the reference exactly: ``data`` (numpy or torch, any dtype) is
+    cast to float32 (volume.py:70-73) -- a uint8 array therefore holds raw values 0..255, which
+    quantise to bin 255 wherever they are nonzero, as in the reference.  8-bit LUT bins (the
+    field ``f32(u/255)``, what load_raw returns for 8-bit files) come in through
+    ``Volume.from_u8``, which uploads the bytes as they are."""
 
     def __init__(self, data, name: str = "volume"):
+        self._init(data, name, u8_bins=False)
+
+    @classmethod
+    def from_u8(cls, bins, name: str = "volume") -> "Volume":
+        """8-bit volume whose bytes are the LUT bins (field ``f32(u/255)``, volume.py:193-194).
+        ``bins`` must have dtype uint8 (numpy or torch, host or device)."""
+        v = cls.__new__(cls)
+        v._init(bins, name, u8_bins=True)
+        return v
+
+    def _init(self, data, name, u8_bins):
         self.name = name
         dev = _lib.device()
         t = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.asarray(data))
         if t.dim() != 3 or min(t.shape) < 1:
             raise ValueError("volume data must be a non-empty 3-d array")
         self._dims = tuple(int(d) for d in t.shape)
-        if t.dtype == torch.uint8:
+        if u8_bins:
+            if t.dtype != torch.uint8:
+                raise TypeError(f"Volume.from_u8 needs uint8 bins, got {t.dtype}")
             self.bins = t.to(dev).contiguous()
             self.field = None
         else:
@@ -134,12 +150,23 @@ class TransferFunction:
     """256-entry RGBA lookup table, all channels in [0, 1] (volume.py:84-140)."""
 
     def __init__(self, lut):
-        lut = np.ascontiguousarray(np.asarray(lut), dtype=np.float32)
+        self.lut = lut
+
+    @property
+    def lut(self) -> np.ndarray:
+        return self._lut
+
+    @lut.setter
+    def lut(self, lut) -> None:
+        """Validated private copy, read-only: the device caches below (params, opacity tables)
+        are derived from it, so assigning a new table is the one way to change a TF."""
+        lut = np.array(lut, dtype=np.float32, order="C", copy=True)
         if lut.shape != (LUT_SIZE, 4):
             raise ValueError(f"lut must be ({LUT_SIZE}, 4), got {lut.shape}")
         if lut.min() < 0.0 or lut.max() > 1.0:
             raise ValueError("lut channels must lie in [0, 1]")
-        self.lut = lut
+        lut.setflags(write=False)
+        self._lut = lut
         self._dev = {}
 
     @classmethod
@@ -238,7 +265,8 @@ class BinaryVolume:
 
     def summary_ok(self) -> bool:
         """The fused brick-summary kernel applies (8^3 bricks, rows of 16-byte multiples)."""
-        return self._source is not None and self._dims[2] % 16 == 0
+        return (self._source is not None and self._dims[2] % 16 == 0
+                and self._source[0].bins.data_ptr() % 16 == 0)
 
     def summary(self, count: bool = False) -> torch.Tensor:
         """27-bit halo summaries per 8^3 brick (vs_classify_summary); with ``count`` the
@@ -349,7 +377,7 @@ def load_raw(path, meta: dict | None = None) -> Volume:
         t = torch.from_numpy(flat.copy()).to(dev)
         # on disk x fastest: (nz, ny, nx) C-order == (nx, ny, nz) F-order -> permute on device
         vol = t.reshape(dims[2], dims[1], dims[0]).permute(2, 1, 0).contiguous()
-        return Volume(vol, name=path.stem)
+        return Volume.from_u8(vol, name=path.stem)
     t = torch.from_numpy(flat.astype(np.int32)).to(dev)
     f64 = t.reshape(dims[2], dims[1], dims[0]).permute(2, 1, 0).double() / float(2 ** bits - 1)
     return Volume(f64.float().contiguous(), name=path.stem)
@@ -388,7 +416,7 @@ def gen_menger(level: int) -> Volume:
         digit = (c // 3 ** d) % 3 == 1
         x, y, z = digit[:, None, None], digit[None, :, None], digit[None, None, :]
         solid &= ~((x & y) | (x & z) | (y & z))
-    return Volume(solid.to(torch.uint8) * 255, name=f"menger{level}")
+    return Volume.from_u8(solid.to(torch.uint8) * 255, name=f"menger{level}")
 
 
 def gen_shell(dims, center=None, radius: float = 0.0, thickness: float = 1.0) -> Volume:
@@ -403,7 +431,7 @@ def gen_shell(dims, center=None, radius: float = 0.0, thickness: float = 1.0) ->
     dist = torch.sqrt(ax[0][:, None, None] ** 2 + ax[1][None, :, None] ** 2 +
                       ax[2][None, None, :] ** 2)
     solid = torch.abs(dist - radius) <= thickness / 2.0
-    return Volume(solid.to(torch.uint8) * 255, name="shell")
+    return Volume.from_u8(solid.to(torch.uint8) * 255, name="shell")
 
 
 def gen_blobs(dims, n: int, seed: int, sigma: float = 1.5, centers=None) -> Volume:

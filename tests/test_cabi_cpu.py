@@ -123,7 +123,7 @@ def test_argument_errors_without_gpu(lib):
         ("vs_build_mquads", lambda: lib.vs_build_mquads(dummy, i(5), i(8), i(8), i(8), dummy, None)),
         ("vs_render", lambda: lib.vs_render(None, None, None, None, None, C.c_double(0.5), i(0),
                                             None, None, None, None, None, None, None,
-                                            C.c_size_t(0), i(0), None)),
+                                            C.c_size_t(0), i(0), None, None)),
     ]
     for name, fn in cases:
         st = fn()

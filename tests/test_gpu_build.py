@@ -45,7 +45,7 @@ def _check_lbvh_oracle(idx, ref):
 def test_blobs64_classify_bricks_lbvh_grid(vs, blobs64, tname):
     u8 = blobs64["u8"]
     tf = vs.TransferFunction(blobs64[f"{tname}_lut"])
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     plain = vs.classify(v, tf, dilate=False)
     np.testing.assert_array_equal(plain.bits, unpack_bits(blobs64[f"{tname}_plain_bits"], u8.shape))
     assert vs.occupancy(vs.classify(v, tf)) == float(blobs64[f"{tname}_occupancy"])
@@ -87,7 +87,7 @@ def test_bit_cases(vs, bitcases, case):
 def test_scenes(vs, scenes, scene, tname):
     p = f"{scene}_{tname}_"
     u8 = scenes[f"{scene}_u8"]
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction(scenes[p + "lut"])
     dil = vs.classify(v, tf, dilate=True)
     dims = u8.shape
@@ -141,7 +141,7 @@ def test_random_volumes_vs_oracle(vs, rng, dims, tfkind):
         lut = np.full((256, 4), 0.5, np.float32)
     else:
         lut = np.zeros((256, 4), np.float32)
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction(lut)
     ref_plain, cnt = O.classify(u8, lut, dilate=False)
     ref_dil, _ = O.classify(u8, lut, dilate=True)

@@ -40,7 +40,7 @@ def test_blobs_u8_matches_reference(vs, blobs64):
 
 
 def test_raw_round_trip(vs, tmp_path, blobs64):
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     vs.save_raw(v, tmp_path / "b.raw")
     meta = json.loads((tmp_path / "b.raw.json").read_text())
     assert meta == {"dims": [64, 64, 64], "bits": 8, "endian": "little"}

@@ -65,7 +65,7 @@ def _structures(vs, g, prefix, b):
 
 @pytest.mark.parametrize("tname", ["ramp03", "ramp06", "ramp00", "opaque", "band"])
 def test_blobs64(vs, blobs64, tname):
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     b = vs.classify(v, vs.TransferFunction(blobs64[f"{tname}_lut"]), dilate=True)
     _structures(vs, blobs64, f"{tname}_", b)
 
@@ -81,7 +81,7 @@ def test_bit_cases(vs, bitcases, case):
 @pytest.mark.parametrize("scene", ["shell", "menger"])
 @pytest.mark.parametrize("tname", ["opaque", "ramp"])
 def test_scenes(vs, scenes, scene, tname):
-    v = vs.Volume(scenes[f"{scene}_u8"])
+    v = vs.Volume.from_u8(scenes[f"{scene}_u8"])
     b = vs.classify(v, vs.TransferFunction(scenes[f"{scene}_{tname}_lut"]), dilate=True)
     _structures(vs, scenes, f"{scene}_{tname}_", b)
 
@@ -117,7 +117,7 @@ def test_box_queries(vs, rng):
 
 def test_index_kinds_and_render(vs, blobs64):
     """build_index for the table kinds == golden; frames through them == golden pixels."""
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tf = vs.TransferFunction(blobs64["ramp03_lut"])
     b = vs.classify(v, tf, dilate=True)
     cam = vs.Camera(eye=tuple(blobs64["cam_eye"]), direction=tuple(blobs64["cam_dir"]),

@@ -31,7 +31,7 @@ def test_reduces_to_single_channel(vs, blobs64):
     from paper_1912_09596_b200.multichannel import classify_multi, render_float_multi
 
     u8 = blobs64["u8"]
-    vols = [vs.Volume(u8), vs.Volume(u8[::-1].copy()), vs.Volume(u8.T.copy())]
+    vols = [vs.Volume.from_u8(u8), vs.Volume.from_u8(u8[::-1].copy()), vs.Volume.from_u8(u8.T.copy())]
     zero = vs.TransferFunction(np.zeros((256, 4), np.float32))
     tfs = [vs.TransferFunction(blobs64["ramp03_lut"]), zero, zero]
     b = classify_multi(vols, tfs, dilate=True)
@@ -56,7 +56,7 @@ def test_four_channels_vs_restatement(vs, blobs64, kind):
         lut = vs.TransferFunction.ramp(t).lut.copy()
         lut[:, c % 3] = 0.9
         luts.append(lut)
-    vols = [vs.Volume(c) for c in chans]
+    vols = [vs.Volume.from_u8(c) for c in chans]
     tfs = [vs.TransferFunction(l) for l in luts]
     b = classify_multi(vols, tfs, dilate=True)
     # union classification == OR of the per-channel oracle classifications, dilated
@@ -92,7 +92,7 @@ def test_channel_counts_vs_restatement(vs, blobs64, nch):
         lut = vs.TransferFunction.ramp(t).lut.copy()
         lut[:, c] = 0.8
         luts.append(lut)
-    vols = [vs.Volume(c) for c in chans]
+    vols = [vs.Volume.from_u8(c) for c in chans]
     tfs = [vs.TransferFunction(l) for l in luts]
     idx = vs.build_index("lbvh", classify_multi(vols, tfs, dilate=True))
     cam = _cam(vs, blobs64, 80, 56)
@@ -110,7 +110,7 @@ def test_tile_frame_multi_async(vs, blobs64):
     from paper_1912_09596_b200.tiles import TileRenderer
 
     u8 = blobs64["u8"]
-    vols = [vs.Volume(u8), vs.Volume(np.ascontiguousarray(u8[::-1]))]
+    vols = [vs.Volume.from_u8(u8), vs.Volume.from_u8(np.ascontiguousarray(u8[::-1]))]
     tfs = [vs.TransferFunction.ramp(0.3), vs.TransferFunction.ramp(0.5)]
     idx = vs.build_index("lbvh", classify_multi(vols, tfs, dilate=True))
     cam = _cam(vs, blobs64, 72, 40)
@@ -138,7 +138,7 @@ def test_smooth_channels_band_tfs_vs_restatement(vs, nch):
         lut[90 + 30 * c:93 + 30 * c, 3] = 0.5   # narrow band per channel
         lut[200:, 3] = 0.2
         luts.append(lut)
-    vols = [vs.Volume(u) for u in chans]
+    vols = [vs.Volume.from_u8(u) for u in chans]
     tfs = [vs.TransferFunction(l) for l in luts]
     idx = vs.build_index("lbvh", classify_multi(vols, tfs, dilate=True))
     cam = vs.Camera.orbit((n, n, n), 41.0, 23.0, width=64, height=48)

@@ -59,7 +59,7 @@ def _assert_rgba(got, want):
 @pytest.mark.parametrize("kind", ["naive", "grid", "lbvh", "kd-shallow", "kd-deep-mls32",
                                   "kd-binned-mls32", "hybrid"])
 def test_blobs64_render_exact(vs, blobs64, tname, kind):
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tf = vs.TransferFunction(blobs64[f"{tname}_lut"])
     idx = _index(vs, kind, blobs64, f"{tname}_", v, tf)
     cam = _cam_from(vs, blobs64, 96, 64)
@@ -75,7 +75,7 @@ def test_blobs64_render_exact(vs, blobs64, tname, kind):
 @pytest.mark.parametrize("tname", ["opaque", "ramp"])
 def test_scene_frames(vs, scenes, scene, tname):
     u8 = scenes[f"{scene}_u8"]
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction(scenes[f"{scene}_{tname}_lut"])
     cam = vs.Camera.orbit(u8.shape, 25.0, 20.0, width=64)
     for kind in ("naive", "grid", "lbvh", "kd-deep-mls32", "hybrid"):
@@ -107,7 +107,7 @@ def test_float_volume_render(vs, misc):
 
 
 def test_single_ray_api(vs, blobs64):
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tf = vs.TransferFunction(blobs64["ramp03_lut"])
     dims = v.dims
     idxs = {"naive": None, "grid": _index(vs, "grid", blobs64, "ramp03_", v, tf),
@@ -136,7 +136,7 @@ def test_axis_aligned_and_oblique_vs_oracle(vs, blobs64, az, el):
     """Zero direction components (containment slabs, R_FAR crossings) and steep views."""
     u8 = blobs64["u8"]
     lut = blobs64["ramp03_lut"]
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction(lut)
     cam = vs.Camera.orbit(u8.shape, az, el, width=48, height=40)
     b = vs.classify(v, tf, dilate=True)
@@ -159,7 +159,7 @@ def test_row_stripes_assemble(vs, blobs64):
 
     from paper_1912_09596_b200.render import RenderTarget, RowsDesc, render_rows
 
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tf = vs.TransferFunction(blobs64["ramp03_lut"])
     idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
     cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=40, height=37)
@@ -179,7 +179,7 @@ def test_row_stripes_assemble(vs, blobs64):
 
 
 def test_render_errors(vs, blobs64):
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tf = vs.TransferFunction(blobs64["ramp03_lut"])
     cam = vs.Camera.orbit(v.dims, 0.0, width=8)
     with pytest.raises(ValueError):
@@ -205,7 +205,7 @@ def test_lbvh_brick_dda_equals_tree_walk(vs, az, el):
     dims = (45, 38, 52)
     coarse = rng.integers(0, 256, size=(10, 10, 11), dtype=np.uint8)
     u8 = np.repeat(np.repeat(np.repeat(coarse, 5, 0), 4, 1), 5, 2)[:dims[0], :dims[1], :dims[2]].copy()
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction.ramp(0.7)
     idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
     cam = vs.Camera.orbit(dims, az, el, width=57, height=43)
@@ -232,7 +232,7 @@ def test_quad_gather_equals_byte_gather(vs, az, el):
 
     rng = np.random.default_rng(11)
     u8 = rng.integers(0, 256, size=(13, 17, 11), dtype=np.uint8)
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction.ramp(0.2)
     cam = vs.Camera.orbit(u8.shape, az, el, width=40, height=33, zoom=1.3)
     outs = []
@@ -251,7 +251,7 @@ def test_two_phase_equals_fused(vs, blobs64, kind):
     """Two-phase rendering (segment buffer, incl. overflow re-traversal at cap 1) == fused."""
     from paper_1912_09596_b200.render import RenderTarget, render_rows
 
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tf = vs.TransferFunction(blobs64["ramp03_lut"])
     idx = _index(vs, kind, blobs64, "ramp03_", v, tf)
     cam = _cam_from(vs, blobs64, 96, 64)
@@ -267,35 +267,10 @@ def test_two_phase_equals_fused(vs, blobs64, kind):
 
 
 def test_u8_table_option_equal(vs, blobs64):
-    from paper_1912_09596_b200 import _lib
-
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tf = vs.TransferFunction(blobs64["ramp03_lut"])
     cam = _cam_from(vs, blobs64, 96, 64)
-    outs = []
-    try:
-        for opts in (0, 1):
-            _lib.lib().vs_set_render_options(opts)
-            outs.append(vs.render_float(v, tf, None, cam))
-    finally:
-        _lib.lib().vs_set_render_options(0)
-    np.testing.assert_array_equal(outs[0][0], outs[1][0])
-    np.testing.assert_array_equal(outs[1][0], blobs64["ramp03_render_naive_rgba"])
-
-
-def test_u8_table_option_equal(vs, blobs64):
-    from paper_1912_09596_b200 import _lib
-
-    v = vs.Volume(blobs64["u8"])
-    tf = vs.TransferFunction(blobs64["ramp03_lut"])
-    cam = _cam_from(vs, blobs64, 96, 64)
-    outs = []
-    try:
-        for opts in (0, 1):
-            _lib.lib().vs_set_render_options(opts)
-            outs.append(vs.render_float(v, tf, None, cam))
-    finally:
-        _lib.lib().vs_set_render_options(0)
+    outs = [vs.render_float(v, tf, None, cam, flags=f) for f in (0, 1)]
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     np.testing.assert_array_equal(outs[1][0], blobs64["ramp03_render_naive_rgba"])
 
@@ -306,21 +281,17 @@ def test_persistent_two_phase_equal(vs, blobs64, kind):
     from paper_1912_09596_b200 import _lib
     from paper_1912_09596_b200.render import RenderTarget, render_rows
 
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tf = vs.TransferFunction(blobs64["ramp03_lut"])
     idx = _index(vs, kind, blobs64, "ramp03_", v, tf)
     cam = _cam_from(vs, blobs64, 96, 64)
     outs = []
-    try:
-        for opts, cap in ((1, 0), (3, 1), (3, 32), (5, 1), (5, 32)):
-            _lib.lib().vs_set_render_options(opts)
-            tgt = RenderTarget(cam.width, cam.height, want_rgba64=True, want_samples=True,
-                               seg_cap=cap)
-            render_rows(v, tf, idx, cam, tgt)
-            outs.append((tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy(),
-                         int(tgt.total.item())))
-    finally:
-        _lib.lib().vs_set_render_options(1)
+    for opts, cap in ((1, 0), (3, 1), (3, 32), (5, 1), (5, 32)):
+        tgt = RenderTarget(cam.width, cam.height, want_rgba64=True, want_samples=True,
+                           seg_cap=cap)
+        render_rows(v, tf, idx, cam, tgt, flags=opts)
+        outs.append((tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy(),
+                     int(tgt.total.item())))
     for o in outs[1:]:
         np.testing.assert_array_equal(o[1], outs[0][1])
         np.testing.assert_array_equal(o[0], outs[0][0])
@@ -332,7 +303,7 @@ def test_tile_frame_pinned_buffers(vs, blobs64):
     a dropped one is recycled; pixels and sample counts equal render_frame's."""
     from paper_1912_09596_b200.tiles import TileRenderer
 
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     tfs = [vs.TransferFunction.ramp(0.3), vs.TransferFunction.ramp(0.6)]
     cam = _cam_from(vs, blobs64, 80, 48)
     tr = TileRenderer(cam.width, cam.height)
@@ -371,7 +342,7 @@ def test_configs1_row_band_vs_oracle(vs, kind):
 
     u8_dev = gen_blobs_u8((256, 256, 256), 400, seed=7, sigma=3.0)
     u8 = u8_dev.cpu().numpy()
-    v = vs.Volume(u8_dev)
+    v = vs.Volume.from_u8(u8_dev)
     tf = vs.TransferFunction.ramp(0.3)
     idx = vs.build_index(kind, vs.classify(v, tf, dilate=True))
     cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=1024, height=1024)
@@ -394,7 +365,7 @@ def test_early_ray_termination_bound(vs, blobs64, kind, seg_cap):
     more samples; eps = 0 is the reference integrator bit for bit."""
     from paper_1912_09596_b200.render import RenderTarget, render_rows
 
-    v = vs.Volume(blobs64["u8"])
+    v = vs.Volume.from_u8(blobs64["u8"])
     lut = vs.TransferFunction.ramp(0.05).lut.copy()
     lut[:, 3] = np.minimum(1.0, lut[:, 3] * 4.0)   # dense, opaque: many rays saturate
     tf = vs.TransferFunction(lut)
@@ -427,22 +398,15 @@ def test_brick_run_shortcut_equals_per_brick_slab(vs, dims):
     rng = np.random.default_rng(3)
     u8 = (rng.random(dims) * 255).astype(np.uint8)
     u8[rng.random(dims) < 0.7] = 0
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction.ramp(0.5)
     idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
-    lib = _lib.lib()
-    try:
-        for az, el in ((30.0, 15.0), (0.0, 0.0), (90.0, 45.0), (211.0, -33.0)):
-            cam = vs.Camera.orbit(v.dims, az, el, width=120, height=96)
-            outs = []
-            for opts in (1, 1 | 16, 1 | 4):
-                lib.vs_set_render_options(opts)
-                outs.append(vs.render_float(v, tf, idx, cam))
-            for o in outs[1:]:
-                np.testing.assert_array_equal(o[1], outs[0][1])
-                np.testing.assert_array_equal(o[0], outs[0][0])
-    finally:
-        lib.vs_set_render_options(1)
+    for az, el in ((30.0, 15.0), (0.0, 0.0), (90.0, 45.0), (211.0, -33.0)):
+        cam = vs.Camera.orbit(v.dims, az, el, width=120, height=96)
+        outs = [vs.render_float(v, tf, idx, cam, flags=f) for f in (1, 1 | 16, 1 | 4)]
+        for o in outs[1:]:
+            np.testing.assert_array_equal(o[1], outs[0][1])
+            np.testing.assert_array_equal(o[0], outs[0][0])
 
 
 @pytest.mark.gpu
@@ -457,23 +421,17 @@ def test_fp32_bin_filter_equals_fp64_bins(vs, kind):
     g = np.mgrid[0:n, 0:n, 0:n].astype(np.float64)
     field = 0.5 + 0.5 * np.sin(g[0] / 5.0) * np.cos(g[1] / 7.0) * np.sin(g[2] / 3.0 + 1.0)
     u8 = np.clip(np.rint(field * 255.0), 0, 255).astype(np.uint8)
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     lut = np.zeros((256, 4), dtype=np.float32)
     lut[:, :3] = np.linspace(0, 1, 256)[:, None]
     lut[100:103, 3] = 0.6   # narrow band: bins decided right at the edges matter
     lut[180:, 3] = 0.3
     tfs = [vs.TransferFunction.ramp(0.45), vs.TransferFunction(lut)]
-    lib = _lib.lib()
-    try:
-        for tf in tfs:
-            idx = None if kind == "naive" else vs.build_index(kind, vs.classify(v, tf, dilate=True))
-            for az, el in ((30.0, 15.0), (123.0, -40.0)):
-                cam = vs.Camera.orbit(v.dims, az, el, width=96, height=80)
-                lib.vs_set_render_options(1)
-                fast = vs.render_float(v, tf, idx, cam)
-                lib.vs_set_render_options(1 | 2)
-                exact = vs.render_float(v, tf, idx, cam)
-                np.testing.assert_array_equal(fast[1], exact[1])
-                np.testing.assert_array_equal(fast[0], exact[0])
-    finally:
-        lib.vs_set_render_options(1)
+    for tf in tfs:
+        idx = None if kind == "naive" else vs.build_index(kind, vs.classify(v, tf, dilate=True))
+        for az, el in ((30.0, 15.0), (123.0, -40.0)):
+            cam = vs.Camera.orbit(v.dims, az, el, width=96, height=80)
+            fast = vs.render_float(v, tf, idx, cam, flags=1)
+            exact = vs.render_float(v, tf, idx, cam, flags=1 | 2)
+            np.testing.assert_array_equal(fast[1], exact[1])
+            np.testing.assert_array_equal(fast[0], exact[0])

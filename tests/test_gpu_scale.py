@@ -34,7 +34,7 @@ def test_config2_256_vs_oracle(vs):
 
     u8 = gen_blobs_u8((256, 256, 256), 400, seed=7, sigma=3.0)
     host = u8.cpu().numpy()
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction.ramp(0.3)
     b = vs.classify(v, tf, dilate=True)
     lb = vs.build_index("lbvh", b)
@@ -65,7 +65,7 @@ def test_config4_1024_properties(vs):
     from paper_1912_09596_b200.synth import gen_blobs_u8
 
     u8 = gen_blobs_u8((1024, 1024, 1024), 25600, seed=7, sigma=3.0)
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction.ramp(0.3)
     rb = LbvhRebuilder(v)
     rb.rebuild(tf.params())

@@ -34,7 +34,7 @@ def _worker(rank, world, port, u8, lut, q):
         import paper_1912_09596_b200 as vs
         from paper_1912_09596_b200.tiles import TileRenderer
 
-        v = vs.Volume(u8)
+        v = vs.Volume.from_u8(u8)
         tf = vs.TransferFunction(lut)
         idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
         cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=72, height=45)
@@ -65,7 +65,7 @@ def test_two_rank_tiles_equal_single_render(blobs64):
         res[rank] = (pix, n)
     for p in procs:
         p.join(timeout=60)
-    v = vs.Volume(u8)
+    v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction(lut)
     idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
     full = vs.render_frame(v, tf, idx, vs.Camera.orbit(v.dims, 30.0, 15.0, width=72, height=45))

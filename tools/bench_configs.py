@@ -62,7 +62,7 @@ def timed_render(v, tf, idx, w, h, reps=3):
 
 out = {"device": torch.cuda.get_device_name(0), "configs": []}
 for name, n, nb, ts, kinds, (w, h) in CONFIGS:
-    v = vs.Volume(gen_blobs_u8((n, n, n), nb, seed=7, sigma=3.0))
+    v = vs.Volume.from_u8(gen_blobs_u8((n, n, n), nb, seed=7, sigma=3.0))
     for t in ts:
         tf = vs.TransferFunction.ramp(t)
         occ = 100.0 * vs.occupancy(vs.classify(v, tf))

@@ -7,7 +7,7 @@ from paper_1912_09596_b200.synth import gen_blobs_u8
 from paper_1912_09596_b200.tiles import TileRenderer
 import bench as B
 n=1024
-vols=[vs.Volume(gen_blobs_u8((n,)*3, 25600, seed=7+c, sigma=3.0)) for c in range(4)]
+vols=[vs.Volume.from_u8(gen_blobs_u8((n,)*3, 25600, seed=7+c, sigma=3.0)) for c in range(4)]
 tfs=B.channel_tfs(4); cams=B.cameras(vols[0].dims)
 params = torch.stack([torch.stack([tf.params() for tf in tl]) for tl in tfs])
 rb=LbvhRebuilder(vols).capture(); idx=rb.index()

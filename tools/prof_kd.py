@@ -6,7 +6,7 @@ import paper_1912_09596_b200 as vs
 from paper_1912_09596_b200.synth import gen_blobs_u8
 
 n, kind, t = int(sys.argv[1]), sys.argv[2], float(sys.argv[3])
-v = vs.Volume(gen_blobs_u8((n, n, n), max(1, 25600 * n**3 // 1024**3), seed=7, sigma=3.0))
+v = vs.Volume.from_u8(gen_blobs_u8((n, n, n), max(1, 25600 * n**3 // 1024**3), seed=7, sigma=3.0))
 tf = vs.TransferFunction.ramp(t)
 b = vs.classify(v, tf, dilate=True)
 b.packed()

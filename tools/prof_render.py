@@ -12,7 +12,7 @@ kinds = sys.argv[2].split(",") if len(sys.argv) > 2 else ["lbvh", "naive"]
 t = float(sys.argv[3]) if len(sys.argv) > 3 else 0.3
 cap = int(sys.argv[4]) if len(sys.argv) > 4 else 16
 u8 = gen_blobs_u8((n, n, n), n=max(1, 25600 * n**3 // 1024**3), seed=7, sigma=3.0)
-v = vs.Volume(u8)
+v = vs.Volume.from_u8(u8)
 tf = vs.TransferFunction.ramp(t)
 b = vs.classify(v, tf, dilate=True)
 cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=1920, height=1080)

@@ -9,7 +9,7 @@ from paper_1912_09596_b200.synth import gen_blobs_u8
 from paper_1912_09596_b200.tiles import TileRenderer
 
 n = 1024
-v = vs.Volume(gen_blobs_u8((n, n, n), 25600, seed=7, sigma=3.0))
+v = vs.Volume.from_u8(gen_blobs_u8((n, n, n), 25600, seed=7, sigma=3.0))
 luts = [vs.TransferFunction.ramp(0.6 - 0.6 * k / 63).lut for k in range(64)]
 cams = [vs.Camera.orbit(v.dims, 360.0 * k / 64, 15.0, width=1920, height=1080) for k in range(64)]
 tr = TileRenderer(1920, 1080)

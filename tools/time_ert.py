@@ -6,7 +6,7 @@ import paper_1912_09596_b200 as vs
 from paper_1912_09596_b200.synth import gen_blobs_u8
 from paper_1912_09596_b200.render import RenderTarget, render_rows, index_desc, volume_desc, camera_desc
 
-v = vs.Volume(gen_blobs_u8((1024,) * 3, 25600, seed=7, sigma=3.0))
+v = vs.Volume.from_u8(gen_blobs_u8((1024,) * 3, 25600, seed=7, sigma=3.0))
 cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=1920, height=1080)
 for t in (0.6, 0.3, 0.0):
     tf = vs.TransferFunction.ramp(t)

@@ -13,7 +13,7 @@ kinds = sys.argv[2].split(",") if len(sys.argv) > 2 else ["lbvh", "grid", "naive
 ts = [float(t) for t in sys.argv[3].split(",")] if len(sys.argv) > 3 else [0.6, 0.3, 0.0]
 opts = [int(o) for o in sys.argv[4].split(",")] if len(sys.argv) > 4 else [1, 3]
 W, H = 1920, 1080
-v = vs.Volume(gen_blobs_u8((n, n, n), n=max(1, 25600 * n**3 // 1024**3), seed=7, sigma=3.0))
+v = vs.Volume.from_u8(gen_blobs_u8((n, n, n), n=max(1, 25600 * n**3 // 1024**3), seed=7, sigma=3.0))
 cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=W, height=H)
 for t in ts:
     tf = vs.TransferFunction.ramp(t)
@@ -24,19 +24,17 @@ for t in ts:
         tgt = RenderTarget(W, H, want_rgba64=True)
         d, vd, cd = index_desc(idx), volume_desc(v), camera_desc(cam)
         for o in opts:
-            _lib.lib().vs_set_render_options(o)
             for _ in range(2):
-                render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
+                render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd, flags=o)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             K = 5
             e0.record()
             for _ in range(K):
-                render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd)
+                render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd, flags=o)
             e1.record()
             torch.cuda.synchronize()
             res[o] = (e0.elapsed_time(e1) / K, int(tgt.total.item()), tgt.rgba64.clone())
-        _lib.lib().vs_set_render_options(1)
         same = all(torch.equal(res[o][2], res[opts[0]][2]) for o in opts)
         s = res[opts[0]][1]
         print(f"t={t} {kind:6s} samples {s:11d}  " +
