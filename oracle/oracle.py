@@ -80,9 +80,17 @@ def lib():
         L.or_integrate.restype = None
         L.or_integrate.argtypes = [P, P, P, i64, P, C.c_int, i64, i64, i64, P, C.c_double,
                                    C.c_int, P, P]
+        L.or_set_threads.restype = None
+        L.or_set_threads.argtypes = [C.c_int]
         L.or_corr_table.restype = None
         L.or_corr_table.argtypes = [P, C.c_double, P]
     return _LIB
+
+
+def set_threads(n: int) -> None:
+    """Host threads for classification / dilation / brick votes (0 = all cores).  Results
+    never depend on it (independent x slabs)."""
+    lib().or_set_threads(int(n))
 
 
 def _p(a: np.ndarray | None):
@@ -372,13 +380,15 @@ def math_pow_corr(lut, dt: float) -> np.ndarray:
     return np.array([1.0 - math.pow(1.0 - float(a), dt) for a in lut[:, 3]], np.float64)
 
 
-def render_multi(kind: str, fields, luts, index: dict | None, cam, dt: float = 0.5):
-    """Multi-channel frame (or_render_multi): u8 channels, one LUT each."""
+def render_multi(kind: str, fields, luts, index: dict | None, cam, dt: float = 0.5, rows=None,
+                 nthreads: int | None = None):
+    """Multi-channel frame rows [r0, r1) (or_render_multi_rows): u8 channels, one LUT each."""
     L = lib()
     if not hasattr(L, "_multi_bound"):
-        L.or_render_multi.restype = None
-        L.or_render_multi.argtypes = [C.c_int, P, C.c_int, i64, i64, i64, P, P, i64, i64, i64, i64,
-                                      P, P, P, P, P, P, i64, i64, P, P, i64, i64, C.c_double, P, P]
+        L.or_render_multi_rows.restype = None
+        L.or_render_multi_rows.argtypes = [C.c_int, P, C.c_int, i64, i64, i64, P, P, i64, i64,
+                                           i64, i64, P, P, P, P, P, P, i64, i64, P, P, i64, i64,
+                                           i64, i64, C.c_double, P, P, C.c_int]
         L._multi_bound = True
     fs = [np.ascontiguousarray(f, dtype=np.uint8) for f in fields]
     ls = [_lut(l) for l in luts]
@@ -386,11 +396,12 @@ def render_multi(kind: str, fields, luts, index: dict | None, cam, dt: float = 0
     lp = (C.c_void_p * len(ls))(*[l.ctypes.data for l in ls])
     packed, direction = camera_vectors(cam)
     w, h = cam.width, cam.height
-    rgba = np.zeros((w * h, 4), np.float64)
-    samples = np.zeros(w * h, np.int64)
+    r0, r1 = (0, h) if rows is None else rows
+    rgba = np.zeros(((r1 - r0) * w, 4), np.float64)
+    samples = np.zeros((r1 - r0) * w, np.int64)
     args, keep = _index_args(kind, index, fs[0].shape)
-    L.or_render_multi(_KIND[kind], C.cast(fp, C.c_void_p), len(fs), *fs[0].shape,
-                      C.cast(lp, C.c_void_p), *args, _p(packed), _p(direction), w, h, float(dt),
-                      _p(rgba), _p(samples))
+    L.or_render_multi_rows(_KIND[kind], C.cast(fp, C.c_void_p), len(fs), *fs[0].shape,
+                           C.cast(lp, C.c_void_p), *args, _p(packed), _p(direction), w, h, r0, r1,
+                           float(dt), _p(rgba), _p(samples), int(nthreads or os.cpu_count() or 1))
     del keep
-    return rgba.reshape(h, w, 4), samples.reshape(h, w)
+    return rgba.reshape(r1 - r0, w, 4), samples.reshape(r1 - r0, w)

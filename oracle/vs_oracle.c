@@ -30,6 +30,40 @@ static i64 imin64(i64 a, i64 b) { return a < b ? a : b; }
 static i64 imax64(i64 a, i64 b) { return a > b ? a : b; }
 static i64 floordiv(i64 a, i64 b) { i64 q = a / b; if ((a % b != 0) && ((a < 0) != (b < 0))) q--; return q; }
 
+/* Host threads for the data-parallel loops below (classification, dilation, brick votes).
+ * The split is over independent x slabs, so results never depend on the thread count. */
+#include <unistd.h>
+static int g_threads = 0;
+void or_set_threads(int n) { g_threads = n; }
+static int nthreads_for(i64 work) {
+    int t = g_threads > 0 ? g_threads : (int)sysconf(_SC_NPROCESSORS_ONLN);
+    if (t < 1) t = 1;
+    if (t > 64) t = 64;
+    if ((i64)t > work) t = (int)(work > 0 ? work : 1);
+    return t;
+}
+typedef void (*range_fn)(void* ctx, i64 lo, i64 hi, int tid);
+typedef struct { range_fn fn; void* ctx; i64 n; int nt, tid; } ParJob;
+static void* par_worker(void* a) {
+    ParJob* j = (ParJob*)a;
+    i64 lo = j->n * j->tid / j->nt, hi = j->n * (j->tid + 1) / j->nt;
+    j->fn(j->ctx, lo, hi, j->tid);
+    return NULL;
+}
+/* fn(ctx, lo, hi, tid) over contiguous chunks of [0, n); returns the thread count used. */
+static int par_for(i64 n, range_fn fn, void* ctx) {
+    int nt = nthreads_for(n);
+    ParJob jobs[64];
+    pthread_t th[64];
+    for (int t = 0; t < nt; ++t) {
+        jobs[t].fn = fn; jobs[t].ctx = ctx; jobs[t].n = n; jobs[t].nt = nt; jobs[t].tid = t;
+    }
+    for (int t = 1; t < nt; ++t) pthread_create(&th[t], NULL, par_worker, &jobs[t]);
+    par_worker(&jobs[0]);
+    for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+    return nt;
+}
+
 /* ------------------------------------------------------------------------------------ */
 /* classification: volume.py:231-234 (quantize_scalar), 361-376 (_dilate26),            */
 /* 379-391 (classify), 394-396 (occupancy)                                               */
@@ -54,25 +88,47 @@ static float field_value(const void* vol, int is_f32, i64 idx, const float* u8ta
 }
 
 /* volume.py:361-376: separable 3-tap OR per axis, borders clipped. */
+typedef struct { uint8_t* bits; const uint8_t* tmp; i64 nx, ny, nz; int axis; } DilJob;
+static void dilate_slabs(void* c, i64 lo, i64 hi, int tid) {
+    (void)tid;
+    DilJob* j = (DilJob*)c;
+    i64 dimsv[3] = {j->nx, j->ny, j->nz};
+    i64 stride[3] = {j->ny * j->nz, j->nz, 1};
+    for (i64 x = lo; x < hi; ++x)
+        for (i64 y = 0; y < j->ny; ++y)
+            for (i64 z = 0; z < j->nz; ++z) {
+                i64 cc[3] = {x, y, z};
+                i64 i = IDX3(x, y, z, j->ny, j->nz);
+                uint8_t v = j->tmp[i];
+                if (cc[j->axis] > 0) v |= j->tmp[i - stride[j->axis]];
+                if (cc[j->axis] < dimsv[j->axis] - 1) v |= j->tmp[i + stride[j->axis]];
+                j->bits[i] = v;
+            }
+}
 static void dilate26(uint8_t* bits, i64 nx, i64 ny, i64 nz) {
     i64 n = nx * ny * nz;
     uint8_t* tmp = (uint8_t*)malloc((size_t)n);
-    i64 dimsv[3] = {nx, ny, nz};
-    i64 stride[3] = {ny * nz, nz, 1};
     for (int axis = 0; axis < 3; ++axis) {
         memcpy(tmp, bits, (size_t)n);
-        for (i64 x = 0; x < nx; ++x)
-            for (i64 y = 0; y < ny; ++y)
-                for (i64 z = 0; z < nz; ++z) {
-                    i64 c[3] = {x, y, z};
-                    i64 i = IDX3(x, y, z, ny, nz);
-                    uint8_t v = tmp[i];
-                    if (c[axis] > 0) v |= tmp[i - stride[axis]];
-                    if (c[axis] < dimsv[axis] - 1) v |= tmp[i + stride[axis]];
-                    bits[i] = v;
-                }
+        DilJob j = {bits, tmp, nx, ny, nz, axis};
+        par_for(nx, dilate_slabs, &j);
     }
     free(tmp);
+}
+
+typedef struct {
+    const void* vol; int is_f32; i64 plane; const float* tab; const uint8_t* vis; uint8_t* out;
+    i64 counts[64];
+} ClsJob;
+static void classify_slabs(void* c, i64 lo, i64 hi, int tid) {
+    ClsJob* j = (ClsJob*)c;
+    i64 count = 0;
+    for (i64 i = lo * j->plane; i < hi * j->plane; ++i) {
+        uint8_t v = j->vis[quantize_f32(field_value(j->vol, j->is_f32, i, j->tab))];
+        j->out[i] = v;
+        count += v;
+    }
+    j->counts[tid] = count;
 }
 
 /* volume.py:379-391 + 394-396.  Returns the count of NON-dilated visible voxels. */
@@ -82,12 +138,12 @@ i64 or_classify(const void* vol, int is_f32, i64 nx, i64 ny, i64 nz, const float
     or_u8_field_table(tab);
     uint8_t vis[256];
     for (int b = 0; b < 256; ++b) vis[b] = lut[4 * b + 3] > 0.0f;
-    i64 n = nx * ny * nz, count = 0;
-    for (i64 i = 0; i < n; ++i) {
-        uint8_t v = vis[quantize_f32(field_value(vol, is_f32, i, tab))];
-        out[i] = v;
-        count += v;
-    }
+    ClsJob j;
+    memset(&j, 0, sizeof j);
+    j.vol = vol; j.is_f32 = is_f32; j.plane = ny * nz; j.tab = tab; j.vis = vis; j.out = out;
+    int nt = par_for(nx, classify_slabs, &j);
+    i64 count = 0;
+    for (int t = 0; t < nt; ++t) count += j.counts[t];
     if (dilate) dilate26(out, nx, ny, nz);
     return count;
 }
@@ -114,19 +170,33 @@ uint32_t or_morton_encode(i64 x, i64 y, i64 z) {
 /* [b*bs, (b+1)*bs) clipped to dims; output in np.argwhere (C) order.                    */
 /* Returns the count, or -count when cap is too small (nothing past cap written).        */
 /* ------------------------------------------------------------------------------------ */
+typedef struct { const uint8_t* bits; i64 nx, ny, nz, bs, nb[3]; uint8_t* vote; } VoteJob;
+static void vote_slabs(void* c, i64 lo, i64 hi, int tid) {
+    (void)tid;
+    VoteJob* j = (VoteJob*)c;
+    for (i64 bx = lo; bx < hi; ++bx)
+        for (i64 by = 0; by < j->nb[1]; ++by)
+            for (i64 bz = 0; bz < j->nb[2]; ++bz) {
+                int any = 0;
+                for (i64 x = bx * j->bs; x < imin64((bx + 1) * j->bs, j->nx) && !any; ++x)
+                    for (i64 y = by * j->bs; y < imin64((by + 1) * j->bs, j->ny) && !any; ++y)
+                        for (i64 z = bz * j->bs; z < imin64((bz + 1) * j->bs, j->nz); ++z)
+                            if (j->bits[IDX3(x, y, z, j->ny, j->nz)]) { any = 1; break; }
+                j->vote[IDX3(bx, by, bz, j->nb[1], j->nb[2])] = (uint8_t)any;
+            }
+}
 i64 or_flag_bricks(const uint8_t* bits, i64 nx, i64 ny, i64 nz, i64 bs, int32_t* coords,
                    uint32_t* codes, i64 cap) {
-    i64 nb[3] = {(nx + bs - 1) / bs, (ny + bs - 1) / bs, (nz + bs - 1) / bs};
+    VoteJob j = {bits, nx, ny, nz, bs, {(nx + bs - 1) / bs, (ny + bs - 1) / bs, (nz + bs - 1) / bs},
+                 NULL};
+    i64 nbt = j.nb[0] * j.nb[1] * j.nb[2];
+    j.vote = (uint8_t*)malloc((size_t)(nbt > 0 ? nbt : 1));
+    par_for(j.nb[0], vote_slabs, &j);
     i64 cnt = 0;
-    for (i64 bx = 0; bx < nb[0]; ++bx)
-        for (i64 by = 0; by < nb[1]; ++by)
-            for (i64 bz = 0; bz < nb[2]; ++bz) {
-                int any = 0;
-                for (i64 x = bx * bs; x < imin64((bx + 1) * bs, nx) && !any; ++x)
-                    for (i64 y = by * bs; y < imin64((by + 1) * bs, ny) && !any; ++y)
-                        for (i64 z = bz * bs; z < imin64((bz + 1) * bs, nz); ++z)
-                            if (bits[IDX3(x, y, z, ny, nz)]) { any = 1; break; }
-                if (!any) continue;
+    for (i64 bx = 0; bx < j.nb[0]; ++bx)
+        for (i64 by = 0; by < j.nb[1]; ++by)
+            for (i64 bz = 0; bz < j.nb[2]; ++bz) {
+                if (!j.vote[IDX3(bx, by, bz, j.nb[1], j.nb[2])]) continue;
                 if (cnt < cap) {
                     coords[3 * cnt] = (int32_t)bx;
                     coords[3 * cnt + 1] = (int32_t)by;
@@ -135,6 +205,7 @@ i64 or_flag_bricks(const uint8_t* bits, i64 nx, i64 ny, i64 nz, i64 bs, int32_t*
                 }
                 cnt++;
             }
+    free(j.vote);
     return cnt <= cap ? cnt : -cnt;
 }
 
@@ -1262,12 +1333,46 @@ static void integrate_ray_multi(const RaySt* r, const double* seg, i64 m, const 
 }
 
 /* Multi-channel frame (single thread per call; small test frames). */
-void or_render_multi(int kind, const uint8_t** fields, int nch, i64 nx, i64 ny, i64 nz,
-                     const float** luts, const uint8_t* occ, i64 ncx, i64 ncy, i64 ncz, i64 cs,
-                     const int32_t* lo, const int32_t* hi, const int32_t* left,
-                     const int32_t* right, const int8_t* axis, const int32_t* plane, i64 root,
-                     i64 stack_cap, const double* cam, const double* dir, i64 w, i64 h,
-                     double dt, double* rgba, i64* samples) {
+typedef struct {
+    const Index* ix; const uint8_t** fields; int nch; const float* tab; const float** luts;
+    const double** corrs; const double* cam; const double* dir; i64 w, h, row0, nrays, stack_cap;
+    double dt; double* rgba; i64* samples; atomic_llong next;
+} MultiJob;
+
+static void* render_multi_worker(void* arg) {
+    MultiJob* jb = (MultiJob*)arg;
+    SegBuf seg = {0, 0, 0}, tmp = {0, 0, 0};
+    i64* stk = (i64*)malloc(sizeof(i64) * (size_t)(jb->stack_cap + 4));
+    double* sa = (double*)malloc(sizeof(double) * (size_t)(jb->stack_cap + 4));
+    double* sb = (double*)malloc(sizeof(double) * (size_t)(jb->stack_cap + 4));
+    const Index* ix = jb->ix;
+    for (;;) {
+        i64 q0 = atomic_fetch_add(&jb->next, 256);
+        if (q0 >= jb->nrays) break;
+        i64 q1 = q0 + 256 < jb->nrays ? q0 + 256 : jb->nrays;
+        for (i64 q = q0; q < q1; ++q) {
+            double o[3];
+            pixel_origin(jb->cam, jb->w, jb->h, q % jb->w, jb->row0 + q / jb->w, o);
+            RaySt r;
+            ray_setup(&r, o, jb->dir);
+            i64 m = traverse_ray(ix, &r, &seg, &tmp, stk, sa, sb);
+            integrate_ray_multi(&r, seg.t, m, jb->fields, jb->nch, jb->tab, ix->nx, ix->ny, ix->nz,
+                                jb->luts, jb->corrs, jb->dt, jb->rgba + 4 * q, jb->samples + q);
+        }
+    }
+    free(seg.t); free(tmp.t); free(stk); free(sa); free(sb);
+    return NULL;
+}
+
+/* Rows [row0, row1) of a multi-channel frame, rays dealt to nthreads host threads in chunks
+ * of 256 (the split never changes a ray's result). */
+void or_render_multi_rows(int kind, const uint8_t** fields, int nch, i64 nx, i64 ny, i64 nz,
+                          const float** luts, const uint8_t* occ, i64 ncx, i64 ncy, i64 ncz,
+                          i64 cs, const int32_t* lo, const int32_t* hi, const int32_t* left,
+                          const int32_t* right, const int8_t* axis, const int32_t* plane,
+                          i64 root, i64 stack_cap, const double* cam, const double* dir, i64 w,
+                          i64 h, i64 row0, i64 row1, double dt, double* rgba, i64* samples,
+                          int nthreads) {
     Index ix = {kind, nx, ny, nz, occ, ncx, ncy, ncz, (double)cs, lo, hi, left, right, plane, axis, root};
     float tab[256];
     or_u8_field_table(tab);
@@ -1277,18 +1382,26 @@ void or_render_multi(int kind, const uint8_t** fields, int nch, i64 nx, i64 ny, 
         or_corr_table(luts[c], dt, corr_store[c]);
         corrs[c] = corr_store[c];
     }
-    SegBuf seg = {0, 0, 0}, tmp = {0, 0, 0};
-    i64* stk = (i64*)malloc(sizeof(i64) * (size_t)(stack_cap + 4));
-    double* sa = (double*)malloc(sizeof(double) * (size_t)(stack_cap + 4));
-    double* sb = (double*)malloc(sizeof(double) * (size_t)(stack_cap + 4));
-    for (i64 q = 0; q < w * h; ++q) {
-        double o[3];
-        pixel_origin(cam, w, h, q % w, q / w, o);
-        RaySt r;
-        ray_setup(&r, o, dir);
-        i64 m = traverse_ray(&ix, &r, &seg, &tmp, stk, sa, sb);
-        integrate_ray_multi(&r, seg.t, m, fields, nch, tab, nx, ny, nz, luts, corrs, dt,
-                            rgba + 4 * q, samples + q);
-    }
-    free(seg.t); free(tmp.t); free(stk); free(sa); free(sb);
+    MultiJob jb;
+    jb.ix = &ix; jb.fields = fields; jb.nch = nch; jb.tab = tab; jb.luts = luts; jb.corrs = corrs;
+    jb.cam = cam; jb.dir = dir; jb.w = w; jb.h = h; jb.row0 = row0; jb.nrays = (row1 - row0) * w;
+    jb.stack_cap = stack_cap; jb.dt = dt; jb.rgba = rgba; jb.samples = samples;
+    atomic_init(&jb.next, 0);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, render_multi_worker, &jb);
+    render_multi_worker(&jb);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+}
+
+void or_render_multi(int kind, const uint8_t** fields, int nch, i64 nx, i64 ny, i64 nz,
+                     const float** luts, const uint8_t* occ, i64 ncx, i64 ncy, i64 ncz, i64 cs,
+                     const int32_t* lo, const int32_t* hi, const int32_t* left,
+                     const int32_t* right, const int8_t* axis, const int32_t* plane, i64 root,
+                     i64 stack_cap, const double* cam, const double* dir, i64 w, i64 h,
+                     double dt, double* rgba, i64* samples) {
+    or_render_multi_rows(kind, fields, nch, nx, ny, nz, luts, occ, ncx, ncy, ncz, cs, lo, hi, left,
+                         right, axis, plane, root, stack_cap, cam, dir, w, h, 0, h, dt, rgba,
+                         samples, 1);
 }

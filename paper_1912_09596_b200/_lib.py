@@ -124,7 +124,10 @@ def upload(arr) -> torch.Tensor:
     caching host allocator (which keeps the block until the stream-ordered copy has run)."""
     import numpy as np
 
-    host = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+    a = np.ascontiguousarray(arr)
+    if not a.flags.writeable:
+        a = a.copy()  # torch.from_numpy wants a writable array (read-only LUTs)
+    host = torch.from_numpy(a).pin_memory()
     return host.to(device(), non_blocking=True)
 
 

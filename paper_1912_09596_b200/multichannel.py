@@ -189,8 +189,11 @@ def render_frame_multi(volumes, tfs, index, cam: Camera, dt: float = 0.5) -> Fra
                  sample_count=int(tgt.total.item()))
 
 
-def render_float_multi(volumes, tfs, index, cam: Camera, dt: float = 0.5):
-    tgt = MultiTarget(cam.width, cam.height, want_rgba64=True, want_samples=True)
-    render_multi_checked(volumes, tfs, index, cam, tgt, dt)
+def render_float_multi(volumes, tfs, index, cam: Camera, dt: float = 0.5,
+                       rows: RowsDesc | None = None):
+    """(float64 RGBA, per-pixel samples) of the frame, or of a row band / stripe set."""
+    nrows = cam.height if rows is None else rows.nrows
+    tgt = MultiTarget(cam.width, nrows, want_rgba64=True, want_samples=True)
+    render_multi_checked(volumes, tfs, index, cam, tgt, dt, rows)
     _check_flags(tgt.flags)
     return tgt.rgba64.cpu().numpy(), tgt.samples.cpu().numpy().astype(np.int64)

@@ -61,3 +61,50 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+
+@pytest.fixture(scope="session")
+def acceptance():
+    """The reference's acceptance datasets (test_acceptance.py:206-259) through the unmodified
+    reference: inputs, every index kind's arrays, 256x256 frames (make_golden.acceptance)."""
+    return _load("acceptance.npz")
+
+
+ACCEPT_DATASETS = ("menger3", "shell128", "blobs128")
+EQUIV_KINDS = ("grid", "lbvh", "kd-shallow", "kd-deep-mls32", "kd-deep-mls128",
+               "kd-binned-mls32", "hybrid")
+KD_ARGS = {
+    "kd-shallow": dict(mode="shallow"),
+    "kd-deep": dict(mode="deep"),
+    "kd-deep-mls8": dict(mode="deep", max_leaf_size=8),
+    "kd-deep-mls32": dict(mode="deep", max_leaf_size=32),
+    "kd-deep-mls128": dict(mode="deep", max_leaf_size=128),
+    "kd-binned-mls32": dict(mode="deep", max_leaf_size=32, builder="binned"),
+    "kd-binned": dict(mode="deep", builder="binned"),
+    "kd-binned-mls8": dict(mode="deep", max_leaf_size=8, builder="binned"),
+}
+
+
+def accept_field(gold, dname):
+    """(array the oracle takes, dims): u8 bins for u8-exact datasets, else the float field."""
+    a = gold[f"{dname}_u8"] if f"{dname}_u8" in gold else gold[f"{dname}_f32"]
+    return a, a.shape
+
+
+def oracle_index(O, kind, bits):
+    """The oracle's index of ``kind`` as the dict O.render takes."""
+    if kind == "naive":
+        return None
+    if kind == "grid":
+        return {"occupied": O.macro_grid(bits, 16), "cell_size": 16}
+    if kind == "lbvh":
+        coords, codes = O.flag_bricks(bits, 8)
+        return O.build_lbvh(coords, codes, 8, bits.shape)
+    if kind == "hybrid":
+        return {"occupied": O.macro_grid(bits, 16), "cell_size": 16,
+                "tree": O.kd_build(bits, **KD_ARGS["kd-shallow"])}
+    return O.kd_build(bits, **KD_ARGS[kind])
+
+
+def render_kind(kind):
+    return "kd" if kind.startswith("kd-") else kind

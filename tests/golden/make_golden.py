@@ -285,5 +285,63 @@ def main():
     print("misc.npz", (OUT / "misc.npz").stat().st_size)
 
 
+EQUIV_KINDS = ("grid", "lbvh", "kd-shallow", "kd-deep-mls32", "kd-deep-mls128",
+               "kd-binned-mls32", "hybrid")
+
+
+def acceptance():
+    """The reference's own acceptance datasets (pkg/tests/test_acceptance.py:206-234, criterion
+    6; criterion 7's thin shell :237-259): 3 volumes x 2 TFs, every index kind's arrays and
+    256x256 frames (pixels + sample counts) from the unmodified reference."""
+    vs, _ = _import_reference()
+    out = {}
+    datasets = {
+        "menger3": vs.gen_menger(3),
+        "shell128": vs.gen_shell((128, 128, 128), radius=48.0, thickness=2.0),
+        "blobs128": vs.gen_blobs((128, 128, 128), n=100, seed=7),
+        "thinshell128": vs.gen_shell((128, 128, 128), radius=48.0, thickness=1.0),
+    }
+    tfs = {"opaque": vs.TransferFunction.opaque(), "ramp": vs.TransferFunction.ramp()}
+    for dname, v in datasets.items():
+        q = np.rint(v.data.astype(np.float64) * 255.0)
+        if np.array_equal((q / 255.0).astype(np.float32), v.data):
+            out[f"{dname}_u8"] = q.astype(np.uint8)   # u8-exact field: store the bins
+        else:
+            out[f"{dname}_f32"] = v.data                # float field (blobs): store it as is
+        cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=256)
+        for tname, tf in tfs.items():
+            if dname == "thinshell128" and tname != "opaque":
+                continue
+            key = f"{dname}_{tname}"
+            out[f"{tname}_lut"] = tf.lut
+            out[f"{key}_plain_count"] = np.int64(np.count_nonzero(vs.classify(v, tf).bits))
+            bits = vs.classify(v, tf, dilate=True)
+            out[f"{key}_bits"] = np.packbits(bits.bits.reshape(-1))
+            naive = vs.render_frame(v, tf, None, cam)
+            out[f"{key}_naive_pixels"] = naive.pixels
+            out[f"{key}_naive_samples"] = np.int64(naive.sample_count)
+            kinds = ("kd-deep-mls32",) if dname == "thinshell128" else EQUIV_KINDS
+            for kind in kinds:
+                idx = vs.build_index(kind, bits)
+                k = f"{key}_{kind}"
+                if kind == "grid":
+                    out[f"{k}_occupied"] = idx.occupied
+                elif kind == "hybrid":
+                    tree_dict(k, idx.tree, out)
+                    out[f"{k}_occupied"] = idx.grid.occupied
+                else:
+                    tree_dict(k, idx, out)
+                fr = vs.render_frame(v, tf, idx, cam)
+                out[f"{k}_pixels"] = fr.pixels
+                out[f"{k}_samples"] = np.int64(fr.sample_count)
+            print(key, flush=True)
+    np.savez_compressed(OUT / "acceptance.npz", **out)
+    print("acceptance.npz", (OUT / "acceptance.npz").stat().st_size)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["acceptance"]:
+        acceptance()
+    else:
+        main()
+        acceptance()

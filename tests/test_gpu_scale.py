@@ -1,21 +1,33 @@
-"""Parity at the benchmark configs' sizes.
+"""Parity against the CPU oracle at the BASELINE configs' own sizes.
 
-256^3 (configs[1]): the GPU structures and a frame equal the C oracle's outright.  1024^3
-(configs[3]): the oracle is too slow for the full pipeline inside a test, so size-independent
-properties are checked on the device arrays: the LBVH leaves are exactly the dilated brick
-votes (checked against an independent torch max-pool dilation), leaves are in strictly
-increasing Morton order, every internal box is the union of its children's, heights agree,
-and a frame through the LBVH equals the naive frame wherever the TF is a ramp (skipping is
-exact for ramps)."""
+* configs[1] 256^3 (400 blobs): LBVH / grid / kd-shallow arrays and a frame.
+* configs[2] 512^3 (3,200 blobs) x ramp t = 0.6 / 0.3 / 0.0: kd-deep-mls32, kd-deep-mls128 and
+  kd-binned-mls32 arrays equal the oracle's; node counts and heights equal SURVEY App. B
+  (the unmodified reference's numbers).
+* configs[3] 1024^3 (25,600 blobs) x t = 0.6 / 0.3 / 0.0: LBVH, grid, kd-shallow and hybrid
+  arrays equal the oracle's full-size builds; full 1920x1080 LBVH and hybrid frames (float
+  RGBA and per-pixel samples) equal the oracle's at t = 0.3.
+* configs[4] 4-channel 1024^3: the union LBVH equals the oracle's, and a 1920-wide row band of
+  the 1080p frame equals the oracle's multi-channel restatement.
+
+The oracle runs multi-threaded (classification, dilation, brick votes, rendering); a 1024^3
+TF step takes seconds, so everything is compared outright -- bit-exact for bits, arrays and
+counts, exact float RGBA (the 1e-3 RGBA tolerance of the north star holds with margin 0).
+"""
 
 from __future__ import annotations
 
 import numpy as np
 import pytest
 
+from conftest import KD_ARGS
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
+
+TREE = ("lo", "hi", "left", "right")
+KD = TREE + ("axis", "plane")
+LBVH = TREE + ("leaf_brick", "brick_coords")
 
 
 @pytest.fixture(scope="module")
@@ -26,69 +38,192 @@ def vs():
         pytest.skip("no CUDA device")
     import paper_1912_09596_b200 as vs
 
+    O.set_threads(0)  # all host cores
     return vs
 
 
-def test_config2_256_vs_oracle(vs):
+def _same(got, want: dict, fields, what):
+    for f in fields:
+        np.testing.assert_array_equal(getattr(got, f), want[f], err_msg=f"{what}.{f}")
+    assert got.height() == want["height"], what
+
+
+def _oracle_lbvh(bits):
+    coords, codes = O.flag_bricks(bits, 8)
+    return O.build_lbvh(coords, codes, 8, bits.shape)
+
+
+def _blobs(n, nblobs, seed=7):
     from paper_1912_09596_b200.synth import gen_blobs_u8
 
-    u8 = gen_blobs_u8((256, 256, 256), 400, seed=7, sigma=3.0)
-    host = u8.cpu().numpy()
+    u8 = gen_blobs_u8((n, n, n), nblobs, seed=seed, sigma=3.0)
+    return u8, u8.cpu().numpy()
+
+
+# -- configs[1] ---------------------------------------------------------------------------------
+
+def test_config1_256_vs_oracle(vs):
+    u8, host = _blobs(256, 400)
     v = vs.Volume.from_u8(u8)
     tf = vs.TransferFunction.ramp(0.3)
     b = vs.classify(v, tf, dilate=True)
     lb = vs.build_index("lbvh", b)
     assert lb.n_bricks == 3716 and lb.node_count == 7431 and lb.height() == 16
     bits, _ = O.classify(host, tf.lut, dilate=True)
-    coords, codes = O.flag_bricks(bits, 8)
-    ref = O.build_lbvh(coords, codes, 8, host.shape)
-    for f in ("lo", "hi", "left", "right", "leaf_brick", "brick_coords"):
-        np.testing.assert_array_equal(getattr(lb, f), ref[f], err_msg=f)
-    grid = vs.build_index("grid", b)
-    np.testing.assert_array_equal(grid.occupied, O.macro_grid(bits, 16))
-    kd = vs.build_index("kd-shallow", b)
-    okd = O.kd_build(bits, mode="shallow")
-    for f in ("lo", "hi", "axis", "plane", "left", "right"):
-        np.testing.assert_array_equal(getattr(kd, f), okd[f], err_msg=f)
-    cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=128, height=96)
+    ref = _oracle_lbvh(bits)
+    _same(lb, ref, LBVH, "lbvh")
+    np.testing.assert_array_equal(vs.build_index("grid", b).occupied, O.macro_grid(bits, 16))
+    _same(vs.build_index("kd-shallow", b), O.kd_build(bits, mode="shallow"), KD, "kd-shallow")
+    cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=1024, height=1024)
     rgba, samples = vs.render_float(v, tf, lb, cam)
-    orgba, osamples = O.render("lbvh", host, tf.lut, dict(ref, root=0), cam)
+    orgba, osamples = O.render("lbvh", host, tf.lut, ref, cam)
+    assert int(samples.sum()) == 20328072  # the reference's frame sample count
     np.testing.assert_array_equal(samples, osamples)
     np.testing.assert_array_equal(rgba, orgba)
 
 
-def test_config4_1024_properties(vs):
+# -- configs[2] ---------------------------------------------------------------------------------
+
+# SURVEY App. B (unmodified reference, same volume): (nodes, height) per t
+APP_B_512 = {
+    0.6: {"kd-deep-mls32": (11127, 82), "kd-binned-mls32": (10697, 24)},
+    0.3: {"kd-deep-mls32": (41543, 62), "kd-deep-mls128": (41499, 62),
+          "kd-binned-mls32": (24397, 26)},
+    0.0: {"kd-deep-mls32": (149221, 63), "kd-deep-mls128": (62425, 53),
+          "kd-binned-mls32": (83457, 27)},
+}
+
+
+@pytest.fixture(scope="module")
+def vol512(vs):
+    return _blobs(512, 3200)
+
+
+@pytest.mark.parametrize("t", [0.6, 0.3, 0.0])
+def test_config2_512_kd_trees_vs_oracle(vs, vol512, t):
+    u8, host = vol512
+    v = vs.Volume.from_u8(u8)
+    tf = vs.TransferFunction.ramp(t)
+    b = vs.classify(v, tf, dilate=True)
+    bits, _ = O.classify(host, tf.lut, dilate=True)
+    np.testing.assert_array_equal(b.bits, bits)
+    for kind in ("kd-deep-mls32", "kd-deep-mls128", "kd-binned-mls32"):
+        kd = vs.build_index(kind, b)
+        _same(kd, O.kd_build(bits, **KD_ARGS[kind]), KD, f"{kind}@{t}")
+        if kind in APP_B_512[t]:
+            assert (kd.node_count, kd.height()) == APP_B_512[t][kind], (kind, t)
+
+
+# -- configs[3] ---------------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def vol1024(vs):
+    return _blobs(1024, 25600)
+
+
+_ORACLE_1024 = {}
+
+
+@pytest.mark.parametrize("t", [0.6, 0.3, 0.0])
+def test_config3_1024_indices_vs_oracle(vs, vol1024, t):
+    u8, host = vol1024
+    v = vs.Volume.from_u8(u8)
+    tf = vs.TransferFunction.ramp(t)
+    b = vs.classify(v, tf, dilate=True)
+    lb = vs.build_index("lbvh", b)
+    grid = vs.build_index("grid", b)
+    hyb = vs.build_index("hybrid", b)
+    bits, plain = O.classify(host, tf.lut, dilate=True)
+    assert vs.classify(v, tf).base_count() == plain
+    ref = _oracle_lbvh(bits)
+    _same(lb, ref, LBVH, f"lbvh@{t}")
+    occ = O.macro_grid(bits, 16)
+    np.testing.assert_array_equal(grid.occupied, occ)
+    shallow = O.kd_build(bits, mode="shallow")
+    _same(hyb.tree, shallow, KD, f"hybrid.tree@{t}")
+    np.testing.assert_array_equal(hyb.grid.occupied, occ)
+    _same(vs.build_index("kd-shallow", b), shallow, KD, f"kd-shallow@{t}")
+    if t == 0.3:  # SURVEY App. B (reference): n_b 243,434, 486,867 nodes, height 22; (11, 6)
+        assert (lb.n_bricks, lb.node_count, lb.height()) == (243434, 486867, 22)
+        assert (hyb.tree.node_count, hyb.tree.height()) == (11, 6)
+        _ORACLE_1024[t] = {"lbvh": ref, "hybrid": {"occupied": occ, "cell_size": 16,
+                                                   "tree": shallow}}
+
+
+@pytest.mark.parametrize("kind", ["lbvh", "hybrid"])
+def test_config3_1080p_frame_vs_oracle(vs, vol1024, kind):
+    u8, host = vol1024
+    t = 0.3
+    if t not in _ORACLE_1024:
+        pytest.skip("needs test_config3_1024_indices_vs_oracle[0.3] in the same session")
+    v = vs.Volume.from_u8(u8)
+    tf = vs.TransferFunction.ramp(t)
+    idx = vs.build_index(kind, vs.classify(v, tf, dilate=True))
+    cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=1920, height=1080)
+    rgba, samples = vs.render_float(v, tf, idx, cam)
+    orgba, osamples = O.render(kind, host, tf.lut, _ORACLE_1024[t][kind], cam)
+    np.testing.assert_array_equal(samples, osamples)
+    np.testing.assert_array_equal(rgba, orgba)
+    want = {"lbvh": 275332432, "hybrid": 773714751}[kind]  # SURVEY App. B frame samples
+    assert int(samples.sum()) == want
+
+
+# -- configs[4] ---------------------------------------------------------------------------------
+
+def test_config4_four_channel_1024_row_band_vs_oracle(vs, vol1024):
+    import sys
+    from pathlib import Path
+
+    from paper_1912_09596_b200.multichannel import classify_multi, render_float_multi
+    from paper_1912_09596_b200.render import RowsDesc
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench as B
+
+    chans = [vol1024] + [_blobs(1024, 25600, seed=7 + c) for c in range(1, 4)]
+    vols = [vs.Volume.from_u8(u) for u, _ in chans]
+    tfs = B.channel_tfs(4)[21]  # t = 0.4, the bench's sweep TFs
+    idx = vs.build_index("lbvh", classify_multi(vols, tfs, dilate=True))
+    # union classification: OR of the channels' visibility, then the 26-dilation
+    union = np.zeros(vols[0].dims, bool)
+    for (_, host), tf in zip(chans, tfs):
+        union |= O.classify(host, tf.lut, dilate=False)[0]
+    opaque = np.zeros((256, 4), np.float32)
+    opaque[1:, 3] = 1.0
+    bits, _ = O.classify(union.view(np.uint8), opaque, dilate=True)
+    ref = _oracle_lbvh(bits)
+    _same(idx, ref, LBVH, "4ch lbvh")
+    cam = B.cameras(vols[0].dims)[21]
+    band = 32  # image rows 512..543 (stripe 32, part 16)
+    rows = RowsDesc(band, band, -(-cam.height // band), 16)
+    rgba, samples = render_float_multi(vols, tfs, idx, cam, rows=rows)
+    orgba, osamples = O.render_multi("lbvh", [h for _, h in chans], [tf.lut for tf in tfs], ref,
+                                     cam, rows=(512, 512 + band))
+    np.testing.assert_array_equal(samples, osamples)
+    np.testing.assert_array_equal(rgba, orgba)
+    assert int(samples.sum()) > 0
+
+
+def test_lbvh_1024_device_properties(vs, vol1024):
+    """Size-independent properties on the rebuild engine's own arrays (the graph-captured
+    path the bench times): leaves in strictly increasing Morton order, internal boxes are the
+    unions of their children."""
     import torch
 
     from paper_1912_09596_b200.engine import LbvhRebuilder
     from paper_1912_09596_b200.lbvh import morton_encode
-    from paper_1912_09596_b200.synth import gen_blobs_u8
 
-    u8 = gen_blobs_u8((1024, 1024, 1024), 25600, seed=7, sigma=3.0)
+    u8, _ = vol1024
     v = vs.Volume.from_u8(u8)
-    tf = vs.TransferFunction.ramp(0.3)
     rb = LbvhRebuilder(v)
-    rb.rebuild(tf.params())
+    rb.rebuild(vs.TransferFunction.ramp(0.3).params())
     idx = rb.lbvh()
-    n, h = idx.n_bricks, idx.height()
-    assert n == 243434 and idx.node_count == 486867 and h == 22  # SURVEY App. B (reference run)
-    # leaves == dilated brick votes from an independent dilation (max-pool on the base mask)
-    lut_vis = torch.from_numpy(tf.lut[:, 3] > 0).to(u8.device)
-    base = lut_vis[u8.long()].float()[None, None]
-    dil = torch.nn.functional.max_pool3d(base, 3, stride=1, padding=1)[0, 0] > 0
-    votes = dil.reshape(128, 8, 128, 8, 128, 8).any(dim=5).any(dim=3).any(dim=1)
+    n = idx.n_bricks
+    assert n == 243434 and idx.node_count == 486867 and idx.height() == 22
     bc = idx.dev["brick_coords"][:n].long()
-    assert int(votes.sum()) == n
-    assert bool(votes[bc[:, 0], bc[:, 1], bc[:, 2]].all())
     codes = torch.from_numpy(morton_encode(*bc.cpu().numpy().T).astype(np.int64)).to(bc.device)
     assert bool((codes[1:] > codes[:-1]).all())
-    # internal boxes are the unions of their children
     lo, hi = idx.dev["lo"][:2 * n - 1], idx.dev["hi"][:2 * n - 1]
     left, right = idx.dev["left"][:n - 1].long(), idx.dev["right"][:n - 1].long()
     assert bool((lo[:n - 1] == torch.minimum(lo[left], lo[right])).all())
     assert bool((hi[:n - 1] == torch.maximum(hi[left], hi[right])).all())
-    # ramp TF: skipping is exact, so the LBVH frame equals the naive frame
-    cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=160, height=90)
-    a_rgba, _ = vs.render_float(v, tf, idx, cam)
-    n_rgba, _ = vs.render_float(v, tf, None, cam)
-    np.testing.assert_array_equal(a_rgba, n_rgba)
