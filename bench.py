@@ -127,77 +127,63 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
-# CPU reference (the oracle port of the reference path; test infrastructure)
+# CPU reference: the C oracle port of the reference path (oracle/vs_oracle.c; test
+# infrastructure -- executed only by --impl reference and the cpu_baseline leg, after the
+# GPU arm's timed regions)
 # ------------------------------------------------------------------------------------------
 
-def cpu_rebuild(u8_host: np.ndarray, lut: np.ndarray, slab: int):
-    """classify(dilate) + flag_bricks + build_lbvh on x-slab [0, slab) (1 core)."""
-    from oracle import oracle as O
+class OracleFrames:
+    """Full, unscaled interactive frames on the host: classify(dilate) + flag_bricks +
+    build_lbvh for the step's TF, then the 1920x1080 render through THAT tree -- the same
+    work as one GPU step, on every host core the box has."""
 
-    sub = np.ascontiguousarray(u8_host[:slab])
-    t0 = time.perf_counter()
-    bits, _ = O.classify(sub, lut, dilate=True)
-    coords, codes = O.flag_bricks(bits, 8)
-    O.build_lbvh(coords, codes, 8, sub.shape)
-    return time.perf_counter() - t0
+    def __init__(self, u8_host: np.ndarray, threads: int | None = None):
+        from oracle import oracle as O
 
-
-def oracle_lbvh(u8_host: np.ndarray, lut: np.ndarray):
-    """The oracle's full-size LBVH for `lut` (untimed setup of the render sample)."""
-    from oracle import oracle as O
-
-    bits, _ = O.classify(u8_host, lut, dilate=True)
-    coords, codes = O.flag_bricks(bits, 8)
-    return O.build_lbvh(coords, codes, 8, u8_host.shape)
-
-
-def cpu_render_rows(u8_host, lut, tree, cam, nrows: int, threads: int):
-    """Render `nrows` middle rows of the frame through the oracle LBVH (timed)."""
-    from oracle import oracle as O
-
-    r0 = cam.height // 2 - nrows // 2
-    t0 = time.perf_counter()
-    _, samples = O.render("lbvh", u8_host, lut, tree, cam, rows=(r0, r0 + nrows),
-                          nthreads=threads)
-    return time.perf_counter() - t0, int(samples.sum())
-
-
-class CpuFrame:
-    """Bounded CPU sample of one interactive frame: the rebuild on an x-slab (1 core, scaled by
-    n/slab) + the render of a middle row band (all cores, scaled by height/rows) through the
-    oracle LBVH of the first sweep TF.  Sizes are calibrated once to a time budget."""
-
-    def __init__(self, u8_host, lut0, cam, budget_s: float):
+        self.O = O
         self.u8 = u8_host
-        self.n = u8_host.shape[0]
-        self.threads = os.cpu_count() or 1
-        self.tree = oracle_lbvh(u8_host, lut0)
-        self.lut0 = lut0
-        t = cpu_rebuild(u8_host, lut0, 16)
-        self.slab = max(16, min(self.n, int(16 * (0.5 * budget_s) / max(t, 1e-3)) // 8 * 8))
-        tr, _ = cpu_render_rows(u8_host, lut0, self.tree, cam, 8, self.threads)
-        self.rows = max(8, min(cam.height, int(8 * (0.5 * budget_s) / max(tr, 1e-3)) // 8 * 8))
+        self.threads = threads or os.cpu_count() or 1
+        O.set_threads(self.threads)
 
-    def frame(self, lut, cam):
-        rb = cpu_rebuild(self.u8, lut, self.slab)
-        tr, _ = cpu_render_rows(self.u8, self.lut0, self.tree, cam, self.rows, self.threads)
-        rebuild_s = rb * self.n / self.slab
-        render_s = tr * cam.height / self.rows
-        return {"frame_s": rebuild_s + render_s, "rebuild_s": rebuild_s, "render_s": render_s}
-
-    def sample(self, cam):
-        return (f"oracle rebuild on x-slab [0,{self.slab}) of {self.n}^3 scaled "
-                f"x{self.n / self.slab:.1f} (1 core) + oracle LBVH render of {self.rows} middle "
-                f"rows of {cam.width}x{cam.height} scaled x{cam.height / self.rows:.1f} "
-                f"({self.threads} threads)")
+    def frame(self, lut, cam) -> dict:
+        O = self.O
+        t0 = time.perf_counter()
+        bits, _ = O.classify(self.u8, lut, dilate=True)
+        coords, codes = O.flag_bricks(bits, 8)
+        del bits
+        tree = O.build_lbvh(coords, codes, 8, self.u8.shape)
+        t1 = time.perf_counter()
+        _, samples = O.render("lbvh", self.u8, lut, tree, cam, nthreads=self.threads)
+        t2 = time.perf_counter()
+        return {"frame_s": t2 - t0, "rebuild_s": t1 - t0, "render_s": t2 - t1,
+                "samples": int(samples.sum()), "n_bricks": len(coords)}
 
 
-def cpu_frame_estimate(u8_host, lut, cam, budget_s: float):
-    cf = CpuFrame(u8_host, lut, cam, budget_s)
-    est = cf.frame(lut, cam)
-    est["threads"] = cf.threads
-    est["sample"] = cf.sample(cam)
-    return est
+def profile_value(name: str, key: str):
+    """(value, file) of ``key`` in the newest profiles/r??_<name> (ncu summaries committed
+    with the round), or (None, None)."""
+    for p in sorted((ROOT / "profiles").glob(f"r??_{name}"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+        except Exception:
+            continue
+        if d.get(key) is not None:
+            return d[key], f"profiles/{p.name}"
+    return None, None
+
+
+def sweep_j(k: int, steps: int) -> int:
+    """Sweep entry of timed step k: the K timed steps stride over the whole 64-TF sweep
+    (t = 0.6 -> 0) and the 360-degree orbit whatever K is."""
+    return (k * NSWEEP) // max(steps, 1) % NSWEEP
+
+
+def sweep_desc(steps: int) -> dict:
+    js = sorted({sweep_j(k, steps) for k in range(steps)})
+    t = [round(0.6 - 0.6 * j / 63, 4) for j in js]
+    return {"tfs_timed": len(js), "t_first": t[0], "t_last": t[-1],
+            "stride": "j = floor(64 k / steps): every timed step k uses sweep TF j and orbit "
+                      "view j"}
 
 
 # ------------------------------------------------------------------------------------------
@@ -250,44 +236,53 @@ def make_volume(n: int):
 
 
 def run_reference(args, rank, ws):
+    """--impl reference: the oracle port of the reference path on the box's host cores (the
+    reference is Python/numba; nothing of it compiles to an oracle/_ref).  Every step is one
+    full, unscaled frame of the same workload as the GPU arm: the step's sweep TF is
+    classified and its LBVH built at 1024^3, and the 1920x1080 frame is rendered through that
+    tree from the step's orbit view.  Rank 0 alone runs (no process group); others exit."""
     if rank != 0:
         return
-    import torch  # noqa: F401
-
     n = args.size
     u8d, nblobs = make_volume(n)
     u8 = u8d.cpu().numpy()
+    del u8d
     tfs = sweep_tfs()
     cams = cameras(u8.shape)
-    nsteps = args.steps + args.warmup
-    budget = max(0.5, min(20.0, 120.0 / max(nsteps, 1)))
-    cf = CpuFrame(u8, tfs[0].lut, cams[0], budget)
-    times = []
-    info = None
-    for k in range(nsteps):
-        est = cf.frame(tfs[k % NSWEEP].lut, cams[k % NSWEEP])
-        if k >= args.warmup:
-            times.append(est["frame_s"])
-            info = est
-    info["threads"] = cf.threads
-    info["sample"] = cf.sample(cams[0]) + "; per step: the sweep TF's rebuild, orbit camera"
-    frame_s = statistics.mean(times)
+    of = OracleFrames(u8)
+    for k in range(args.warmup):
+        of.frame(tfs[k % NSWEEP].lut, cams[k % NSWEEP])
+    t0 = time.perf_counter()
+    runs = [of.frame(tfs[sweep_j(k, args.steps)].lut, cams[sweep_j(k, args.steps)])
+            for k in range(args.steps)]
+    wall = time.perf_counter() - t0
+    frame_s = wall / args.steps
     value = 1.0 / frame_s
+    sample = (f"{args.steps} full {W}x{H} frames at {n}^3 (no scaling): per step the sweep "
+              f"TF's classify+flag_bricks+build_lbvh and the render through that tree, "
+              f"{of.threads} host threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": frame_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8+f64", "data": "synthetic",
-        "config": {"workload": f"interactive TF sweep on {n}^3 u8 blobs ({nblobs} blobs, sigma "
-                               f"3, seed 7): LBVH rebuild + {W}x{H} render per frame",
-                   "frame": "rebuild+render"},
-        "build_ms": info["rebuild_s"] * 1e3, "render_ms": info["render_s"] * 1e3,
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": info["threads"],
-                         "kind": "port", "sample": info["sample"]},
+        "config": workload_config(n, nblobs, args.steps),
+        "build_ms": 1e3 * statistics.mean(r["rebuild_s"] for r in runs),
+        "render_ms": 1e3 * statistics.mean(r["render_s"] for r in runs),
+        "timed_region_s": wall,
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": of.threads,
+                         "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(n, nblobs, steps):
+    return {"workload": f"interactive TF sweep on {n}^3 u8 blobs ({nblobs} blobs, sigma 3, "
+                        f"seed 7): LBVH rebuild + {W}x{H} render per frame, 64 ramp TFs "
+                        f"t=0.6..0, orbit camera el 15, dt 0.5",
+            "frame": "rebuild+render", "brick": 8, **sweep_desc(steps)}
 
 
 def run_ours(args, rank, ws, local):
@@ -324,8 +319,8 @@ def run_ours(args, rank, ws, local):
     built = [torch.cuda.Event(), torch.cuda.Event()]
     rendered = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def step(k):
-        j, b = k % NSWEEP, k % 2
+    def step(k, j):
+        b = k % 2
         with torch.cuda.stream(sb):
             sb.wait_event(rendered[b])        # buffer b free: frame k-2 rendered
             rbs[b].rebuild(params[j])
@@ -340,7 +335,7 @@ def run_ours(args, rank, ws, local):
     # ---- device-resident loop (value) ------------------------------------------------------
     with torch.cuda.stream(st):
         for k in range(args.warmup):
-            step(k)
+            step(k, k % NSWEEP)
         torch.cuda.synchronize()
         barrier(ws)
         with ClockSampler(local) as clk:
@@ -351,7 +346,7 @@ def run_ours(args, rank, ws, local):
             e0.record(st)
             sb.wait_stream(st)
             for k in range(args.steps):
-                step(k)
+                step(k, sweep_j(k, args.steps))
             st.wait_stream(sb)
             e1.record(st)
             torch.cuda.synchronize()
@@ -362,36 +357,47 @@ def run_ours(args, rank, ws, local):
             reps = max(10, min(args.steps, 100))
             bev[0][0].record(st)
             for k in range(reps):
-                rb.rebuild(params[k % NSWEEP])
+                rb.rebuild(params[sweep_j(k, reps)])
             bev[0][1].record(st)
             summ = []
             for k in range(reps):
-                rb.set_tf(params[k % NSWEEP])
+                rb.set_tf(params[sweep_j(k, reps)])
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(st)
                 rb.launch_summary(st.cuda_stream)
                 b.record(st)
                 rb.launch_tree(st.cuda_stream)
                 summ.append((a, b))
-            rb.rebuild(params[0])
-            rrep = max(3, min(args.steps, 10))
-            samples = 0
-            bev[1][0].record(st)
-            for k in range(rrep):
-                tiles.render(v, tfs[0], idx, cams[k % NSWEEP], idx_desc=index_desc(idx),
-                             vol_desc=vd, cam_desc=cds[k % NSWEEP])
-            bev[1][1].record(st)
+            # render alone at the sparse / medium / dense TF (the reference's App. B view)
+            render_by_t = {}
+            for t in (0.6, 0.3, 0.0):
+                tft = vs.TransferFunction.ramp(t)
+                ridx = vs.build_index("lbvh", vs.classify(v, tft, dilate=True))
+                rcam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=W, height=H)
+                rdesc, rcd = index_desc(ridx), camera_desc(rcam)
+                tiles.render(v, tft, ridx, rcam, idx_desc=rdesc, vol_desc=vd, cam_desc=rcd)
+                rrep = 5
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                for _ in range(rrep):
+                    tiles.render(v, tft, ridx, rcam, idx_desc=rdesc, vol_desc=vd, cam_desc=rcd)
+                b.record(st)
+                torch.cuda.synchronize()
+                render_by_t[t] = (a.elapsed_time(b) / rrep, tiles.sample_total())
+                del ridx
             torch.cuda.synchronize()
-            samples = tiles.sample_total()  # last frame's samples (all ranks)
     total_ms = max_over_ranks(total_ms, ws)
     ms_per_step = total_ms / args.steps
     build_ms = max_over_ranks(bev[0][0].elapsed_time(bev[0][1]) / reps, ws)
-    render_ms = max_over_ranks(bev[1][0].elapsed_time(bev[1][1]) / rrep, ws)
+    render_ms_t = {t: max_over_ranks(ms, ws) for t, (ms, _) in render_by_t.items()}
     summ_ms = statistics.median([a.elapsed_time(b) for a, b in summ])
     info = rb.info.cpu().tolist()
     n_bricks, height = int(info[0]), int(info[1])
 
     # ---- parity spot check: the timed path's index vs a fresh public-API build ----------------
+    with torch.cuda.stream(st):
+        rb.rebuild(params[0])
+    torch.cuda.synchronize()
     ref_idx = vs.build_lbvh(vs.flag_bricks(vs.classify(v, tfs[0], dilate=True)))
     parity = (n_bricks == ref_idx.n_bricks and height == ref_idx.height() and
               all(torch.equal(rb.tree[f][:ref_idx.node_count], ref_idx.dev[f][:ref_idx.node_count])
@@ -404,10 +410,9 @@ def run_ours(args, rank, ws, local):
 
     build_stream = torch.cuda.Stream()
 
-    def e2e_step(k):
+    def e2e_step(k, j):
         # TF change on a side stream: frame k+1's classify + build_index overlap frame k's
         # render (fresh index tensors per frame, kept alive until that frame's result())
-        j = k % NSWEEP
         with torch.cuda.stream(build_stream):
             tf = vs.TransferFunction(luts[j])           # host LUT -> pinned -> device
             b = vs.classify(v, tf, dilate=True)
@@ -417,7 +422,7 @@ def run_ours(args, rank, ws, local):
 
     with torch.cuda.stream(st):  # frames on the high-priority stream, TF changes on build_stream
         for k in range(min(args.warmup, 3)):
-            e2e_step(k)[0].result()
+            e2e_step(k, k % NSWEEP)[0].result()
         e2e_runs = []
         for _ in range(3):  # three passes over the sweep (host-side jitter): the median is reported
             torch.cuda.synchronize()
@@ -425,7 +430,7 @@ def run_ours(args, rank, ws, local):
             e0.record(torch.cuda.current_stream())
             pending = None
             for k in range(e_steps):  # frame k's readback overlaps frame k+1's TF change / render
-                nxt = e2e_step(k)
+                nxt = e2e_step(k, sweep_j(k, e_steps))
                 if pending is not None:
                     fr = pending[0].result()
                 pending = nxt
@@ -463,22 +468,30 @@ def run_ours(args, rank, ws, local):
     peak, peak_kind = hbm_peak()
     alg = rb.algorithmic_bytes(n_bricks)
     achieved = alg["summary_kernel"] / (summ_ms * 1e-3) / 1e9
-    traffic = None
-    prof = ROOT / "profiles" / "r01_summary_traffic.json"
-    if prof.exists():
-        try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    # dram bytes of this kernel per launch from the ncu --set full capture of the same
+    # command (bench.py --frame-only), or null when no capture is committed
+    traffic, traffic_src = profile_value("ncu_k_brick_summary.json", "dram_bytes_per_launch")
+    l1_by_t = {t: profile_value(f"ncu_render_t{int(t * 10):02d}.json", "l1_hit_pct")[0]
+               for t in render_by_t}
 
     if rank != 0:
         return
     cpu = None
     if ws == 1 and not args.no_cpu:
-        est = cpu_frame_estimate(u8.cpu().numpy(), tfs[0].lut, cams[0], args.cpu_budget)
-        cpu = {"value": 1.0 / est["frame_s"], "unit": "frames/s", "cores": est["threads"],
-               "kind": "port", "sample": est["sample"], "rebuild_ms": est["rebuild_s"] * 1e3,
-               "render_ms": est["render_s"] * 1e3}
+        # bounded CPU sample: args.cpu_frames full, unscaled frames of the same workload
+        of = OracleFrames(u8.cpu().numpy())
+        t0 = time.perf_counter()
+        runs = [of.frame(tfs[sweep_j(k, args.cpu_frames)].lut, cams[sweep_j(k, args.cpu_frames)])
+                for k in range(args.cpu_frames)]
+        wall = time.perf_counter() - t0
+        cpu = {"value": args.cpu_frames / wall, "unit": "frames/s", "cores": of.threads,
+               "kind": "port",
+               "sample": f"{args.cpu_frames} full {W}x{H} frames at {n}^3 (no scaling), sweep "
+                         f"TFs j={[sweep_j(k, args.cpu_frames) for k in range(args.cpu_frames)]}"
+                         f": classify+flag_bricks+build_lbvh + render through that tree",
+               "rebuild_ms": 1e3 * statistics.mean(r["rebuild_s"] for r in runs),
+               "render_ms": 1e3 * statistics.mean(r["render_s"] for r in runs)}
+        del of
     clocks = clk.summary()
     # per step (ncu launch list, profiles/r01_launches_interactive_frame.csv): k_brick_summary,
     # k_summary_to_bitmap, 2 CUB scan kernels launched by vs_lbvh_from_bitmap (leaf ranks),
@@ -496,24 +509,27 @@ def run_ours(args, rank, ws, local):
         "vs_baseline": None,
         "dtype": "u8+f64",
         "data": "synthetic",
-        "config": {"workload": f"interactive TF sweep on {n}^3 u8 blobs ({nblobs} blobs, sigma "
-                               f"3, seed 7): LBVH rebuild + {W}x{H} render per frame, 64 ramp "
-                               f"TFs t=0.6..0, orbit camera el 15, dt 0.5",
-                   "frame": "rebuild+render", "brick": 8,
+        "config": {**workload_config(n, nblobs, args.steps),
                    "l2": "input 1 GiB > 126 MB L2 (no flush needed)",
                    "parallelism": f"image row stripes x{ws} + NCCL all-gather; build replicated",
                    "pipeline": "rebuild k+1 on a side stream || render k (two index buffers); "
                                "renders on a high-priority stream"},
         "build_ms": build_ms,
-        "render_ms": render_ms,
-        "render": {"fps": 1e3 / render_ms, "samples_per_frame": samples,
-                   "Msamples_s": samples / render_ms / 1e3,
-                   "kernels": "k_segments<LBVH brick DDA> + k_integrate_segments"},
+        "render_ms": render_ms_t[0.3],
+        "render_by_t": {
+            f"{t:.1f}": {"ms": render_ms_t[t], "fps": 1e3 / render_ms_t[t],
+                         "samples_per_frame": smp, "Msamples_s": smp / render_ms_t[t] / 1e3,
+                         "l1_hit_pct_ncu": l1_by_t[t]}
+            for t, (_, smp) in render_by_t.items()},
+        "render": {"view": "Camera.orbit(dims, 30, 15, 1920, 1080) (SURVEY App. B), LBVH of "
+                           "ramp(t); render_ms = t 0.3; l1_hit_pct_ncu from profiles/"
+                           "<round>_ncu_render_tXX.json (ncu --set full, same view)",
+                   "kernels": "k_segments_brick (LBVH brick DDA) + k_integrate_segments"},
         "summary_kernel_ms": summ_ms,
         "n_bricks": n_bricks, "lbvh_nodes": max(2 * n_bricks - 1, 0), "lbvh_height": height,
         "parity_index_vs_public_api": bool(parity),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": "k_brick_summary", "peak_source": peak_kind,
                      "alg_bytes_per_launch": alg["summary_kernel"],
                      "share_of_step": summ_ms / ms_per_step},
@@ -582,8 +598,8 @@ def run_multi(args, rank, ws, local):
         built = [torch.cuda.Event(), torch.cuda.Event()]
         rendered = [torch.cuda.Event(), torch.cuda.Event()]
 
-        def step(k):
-            j, b = k % NSWEEP, k % 2
+        def step(k, j):
+            b = k % 2
             with torch.cuda.stream(sb):
                 sb.wait_event(rendered[b])
                 rbs[b].rebuild(params[j])
@@ -594,7 +610,7 @@ def run_multi(args, rank, ws, local):
             return img
 
         for k in range(args.warmup):
-            step(k)
+            step(k, k % NSWEEP)
         torch.cuda.synchronize()
         barrier(ws)
         with ClockSampler(local) as clk:
@@ -606,7 +622,7 @@ def run_multi(args, rank, ws, local):
             e0.record(st)
             sb.wait_stream(st)
             for k in range(args.steps):
-                step(k)
+                step(k, sweep_j(k, args.steps))
             st.wait_stream(sb)
             e1.record(st)
             torch.cuda.synchronize()
@@ -625,7 +641,7 @@ def run_multi(args, rank, ws, local):
             e0.record(st)
             pending = None
             for k in range(e_steps):  # frame k's readback overlaps frame k+1's TF change / render
-                j = k % NSWEEP
+                j = sweep_j(k, e_steps)
                 with torch.cuda.stream(build_stream):  # TF change overlapping the previous render
                     tl = [vs.TransferFunction(l) for l in luts[j]]
                     b = classify_multi(vols, tl, dilate=True)
@@ -647,33 +663,32 @@ def run_multi(args, rank, ws, local):
     if ws == 1 and not args.no_cpu:
         from oracle import oracle as O
 
+        # one full, unscaled 4-channel frame on every host core: per-channel classification,
+        # union + dilation, flag_bricks + build_lbvh, the multi-channel render through it
         hosts = [u.cpu().numpy() for u in u8s]
+        threads = os.cpu_count() or 1
+        O.set_threads(threads)
+        j0 = NSWEEP // 3
+        opaque = np.zeros((256, 4), np.float32)
+        opaque[1:, 3] = 1.0
         t0 = time.perf_counter()
-        slab = 64
-        for h_, tf in zip(hosts, tfs[0]):
-            O.classify(np.ascontiguousarray(h_[:slab]), tf.lut, dilate=True)
-        rebuild_s = (time.perf_counter() - t0) * n / slab
-        import types
-        cam = cams[0]
-        nrows = 4
-        sub = types.SimpleNamespace(eye=cam.eye, direction=cam.direction, up=cam.up,
-                                    extent=cam.extent, width=cam.width, height=nrows)
-        # a band of rows through the image centre: shift the eye down to row H/2
-        b = classify_multi(vols, tfs[0], dilate=True)
-        index = vs.build_index("lbvh", b)
-        eye, up, right, scale = cam.frame_vectors()
-        shift = (H / 2.0 - nrows / 2.0) * scale
-        sub.eye = tuple(np.asarray(eye) - shift * np.asarray(up))
-        oidx = {"lo": index.lo, "hi": index.hi, "left": index.left, "right": index.right,
-                "root": index.root, "height": index.height()}
-        t0 = time.perf_counter()
-        O.render_multi("lbvh", hosts, [tf.lut for tf in tfs[0]], oidx, sub)
-        render_s = (time.perf_counter() - t0) * H / nrows
-        cpu = {"value": 1.0 / (rebuild_s + render_s), "unit": "frames/s", "cores": 1,
-               "kind": "port", "sample": f"oracle: {nch}-channel classify on x-slab [0,{slab}) "
-               f"scaled x{n / slab:.0f} + multi-channel LBVH render of {nrows} centre rows "
-               f"scaled x{H / nrows:.0f} (1 thread)",
-               "rebuild_ms": rebuild_s * 1e3, "render_ms": render_s * 1e3}
+        union = np.zeros(hosts[0].shape, bool)
+        for h_, tf in zip(hosts, tfs[j0]):
+            union |= O.classify(h_, tf.lut, dilate=False)[0]
+        bits, _ = O.classify(union.view(np.uint8), opaque, dilate=True)
+        del union
+        coords, codes = O.flag_bricks(bits, 8)
+        del bits
+        tree = O.build_lbvh(coords, codes, 8, hosts[0].shape)
+        t1 = time.perf_counter()
+        O.render_multi("lbvh", hosts, [tf.lut for tf in tfs[j0]], tree, cams[j0],
+                       nthreads=threads)
+        t2 = time.perf_counter()
+        cpu = {"value": 1.0 / (t2 - t0), "unit": "frames/s", "cores": threads, "kind": "port",
+               "sample": f"1 full {W}x{H} {nch}-channel frame at {n}^3 (no scaling), sweep "
+                         f"TF j={j0}: per-channel classify, union dilation, flag_bricks + "
+                         f"build_lbvh, multi-channel render",
+               "rebuild_ms": (t1 - t0) * 1e3, "render_ms": (t2 - t1) * 1e3}
     line = {
         "metric": METRIC, "value": 1e3 / ms, "unit": "frames/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -681,7 +696,7 @@ def run_multi(args, rank, ws, local):
         "data": "synthetic",
         "config": {"workload": f"{nch}-channel {n}^3 u8 blobs (seeds 7..{6 + nch}), union "
                                f"LBVH rebuild + {W}x{H} render per frame, TF sweep",
-                   "frame": "rebuild+render", "channels": nch,
+                   "frame": "rebuild+render", "channels": nch, **sweep_desc(args.steps),
                    "parallelism": f"image row stripes x{ws} + NCCL all-gather"},
         "render": {"samples_per_frame": samples},
         "e2e": {"value": 1e3 / e2e_ms, "unit": "frames/s",
@@ -698,6 +713,20 @@ def run_multi(args, rank, ws, local):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(n: int) -> int:
+    """``bench.py --gpus N`` run bare: start N ranks (one per GPU) under torch.distributed.run
+    on 127.0.0.1 with this same command line; rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -705,7 +734,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=1024)
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-frames", type=int, default=2,
+                    help="full CPU oracle frames timed for cpu_baseline (rank 0, N=1)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--frame-only", action="store_true",
                     help="skip the other hierarchies' rebuild timings (profiling runs)")
@@ -713,10 +743,22 @@ def main():
                     help="> 1: BASELINE configs[4] multi-channel frames")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    rank, ws, local = dist_setup()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
-        run_reference(args, rank, ws)
-    elif args.channels > 1:
+        # CPU arm: rank 0 alone, no process group (the other ranks exit without work)
+        run_reference(args, int(os.environ.get("RANK", "0")),
+                      int(os.environ.get("WORLD_SIZE", "1")))
+        return
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # communicator init lines (rank / nranks / transport) in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    rank, ws, local = dist_setup()
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {ws}; reporting n_gpus = {ws}",
+              file=sys.stderr)
+    if args.channels > 1:
         run_multi(args, rank, ws, local)
     else:
         run_ours(args, rank, ws, local)

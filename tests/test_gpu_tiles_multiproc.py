@@ -1,7 +1,8 @@
-"""The tile-parallel render path end to end with 2 processes on one GPU (gloo group: NCCL
-refuses two ranks on the same device).  Each rank renders its interleaved row stripes with
-k_render; the gathered, re-permuted frame and the summed sample count equal a single-process
-render bit for bit."""
+"""The tile-parallel render path end to end with 2 processes.  Each rank renders its
+interleaved row stripes; the gathered, re-permuted frame and the summed sample count equal a
+single-process render bit for bit.  On one GPU the ranks share it over a gloo group (NCCL
+refuses two ranks on one device); with >= 2 GPUs the same check runs over NCCL, one rank per
+GPU (skipped on the 1-GPU boxes)."""
 
 from __future__ import annotations
 
@@ -22,15 +23,20 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, u8, lut, q):
+def _worker(rank, world, port, u8, lut, q, backend="gloo"):
     import torch
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
         import paper_1912_09596_b200 as vs
         from paper_1912_09596_b200.tiles import TileRenderer
 
@@ -44,19 +50,23 @@ def _worker(rank, world, port, u8, lut, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_tiles_equal_single_render(blobs64):
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_two_rank_tiles_equal_single_render(blobs64, backend):
     import torch
     import torch.multiprocessing as mp
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    if backend == "nccl" and torch.cuda.device_count() < 2:
+        pytest.skip("NCCL tile gather needs 2 GPUs (gpurun boxes have 1)")
     import paper_1912_09596_b200 as vs
 
     u8, lut = blobs64["u8"], blobs64["ramp03_lut"]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, u8, lut, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, u8, lut, q, backend))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = {}
