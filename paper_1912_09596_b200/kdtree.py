@@ -261,3 +261,39 @@ def binned_best_plane(cells: CellBoxList, box, bins: int = DEFAULT_BINS) -> Spli
     if cells.binary is None:
         raise ValueError("CellBoxList was not built by precompute_cell_boxes")
     return _best_plane(cells.binary, box, 1, bins, cells.cell_size)
+
+
+# -- host helpers the reference exposes at module level (its tests import them) -------------
+
+def _snapped_positions(lo: int, hi: int, bins: int, cell_size: int) -> list[int]:
+    """Candidate cuts of the binned search (kdtree.py:346-350): the bins-1 equal divisions of
+    [lo, hi) rounded half-up to the cell lattice in IEEE double, strictly inside the box,
+    deduplicated and ascending.  The device evaluates the same expression (k_decide_binned)."""
+    import math
+
+    step = (hi - lo) / bins
+    cuts = set()
+    for j in range(1, bins):
+        p = int(math.floor((lo + j * step) / cell_size + 0.5)) * cell_size
+        if lo < p < hi:
+            cuts.add(p)
+    return sorted(cuts)
+
+
+def _cells_reduce(cells: CellBoxList, region: Aabb) -> Aabb | None:
+    """Bounds of ``region`` from the per-cell tight boxes (kdtree.py:323-343): the union of the
+    occupied cells whose lattice footprint meets the region, clipped back to the region; None
+    when nothing remains.  Host mirror of the device's cell-slab reduction."""
+    cs = cells.cell_size
+    first = np.array([max(v // cs, 0) for v in region.lo])
+    last = np.array([min((v - 1) // cs, n - 1) for v, n in zip(region.hi, cells.cells_dims)])
+    if np.any(first > last):
+        return None
+    inside = cells.occupied & np.all((cells.coords >= first) & (cells.coords <= last), axis=1)
+    if not inside.any():
+        return None
+    lo = np.maximum(cells.lo[inside].min(axis=0), region.lo)
+    hi = np.minimum(cells.hi[inside].max(axis=0), region.hi)
+    if np.any(lo >= hi):
+        return None
+    return Aabb(tuple(int(v) for v in lo), tuple(int(v) for v in hi))

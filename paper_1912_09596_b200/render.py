@@ -203,6 +203,17 @@ def camera_desc(cam: Camera) -> CameraDesc:
     return c
 
 
+_EMPTY = {}
+
+
+def _placeholder() -> int:
+    """A valid device address for the arrays of an empty tree (root -1: never read)."""
+    dev = _lib.device()
+    if dev.index not in _EMPTY:
+        _EMPTY[dev.index] = torch.zeros(16, dtype=torch.int32, device=dev)
+    return ptr(_EMPTY[dev.index])
+
+
 def index_desc(index, use_brick_dda: bool = True) -> IndexDesc:
     """Descriptor + the tensors it points at (keep them alive for the launch)."""
     kind = index_kind(index)
@@ -230,6 +241,10 @@ def index_desc(index, use_brick_dda: bool = True) -> IndexDesc:
             ptr(dv["right"])
         d.plane, d.axis = ptr(dv["plane"]), ptr(dv["axis"])
         d.root = int(t.root)
+    if kind in ("lbvh", "kd", "hybrid"):
+        for f in ("lo", "hi", "left", "right", "plane", "axis"):
+            if not getattr(d, f):
+                setattr(d, f, _placeholder())  # empty tree: root -1 / 0 bricks
     return d
 
 

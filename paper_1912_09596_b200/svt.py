@@ -18,20 +18,36 @@ DEFAULT_BRICK_SIZE = 32
 
 
 class MacroGrid:
-    """Coarse occupancy grid (svt.py:29-37): ``occupied`` is (ncx, ncy, ncz) bool."""
+    """Coarse occupancy grid (svt.py:29-37): ``occupied`` is (ncx, ncy, ncz) bool.
 
-    def __init__(self, cell_size: int, cells_dims, dims, occupied_dev: torch.Tensor):
+    Same constructor as the reference dataclass -- ``MacroGrid(cell_size, cells_dims, dims,
+    occupied)`` -- where ``occupied`` may be a host bool array (uploaded on first render) or
+    the device uint8 tensor the builders produce (read back on first host access)."""
+
+    def __init__(self, cell_size: int, cells_dims, dims, occupied):
         self.cell_size = int(cell_size)
         self.cells_dims = tuple(int(c) for c in cells_dims)
         self.dims = tuple(int(d) for d in dims)
-        self.occupied_dev = occupied_dev  # uint8 (ncx, ncy, ncz) on the device
-        self._host = None
+        if isinstance(occupied, torch.Tensor):
+            self._dev, self._host = occupied, None
+        else:
+            host = np.ascontiguousarray(occupied, dtype=bool)
+            if host.shape != self.cells_dims:
+                raise ValueError(f"occupied has shape {host.shape}, cells_dims {self.cells_dims}")
+            self._dev, self._host = None, host
 
     @property
     def occupied(self) -> np.ndarray:
         if self._host is None:
-            self._host = self.occupied_dev.cpu().numpy().view(bool)
+            self._host = self._dev.cpu().numpy().view(bool)
         return self._host
+
+    @property
+    def occupied_dev(self) -> torch.Tensor:
+        """uint8 (ncx, ncy, ncz) on the device."""
+        if self._dev is None:
+            self._dev = torch.from_numpy(self._host.view(np.uint8).copy()).to(_lib.device())
+        return self._dev
 
     def storage_bytes(self) -> int:
         return (int(np.prod(self.cells_dims)) + 7) // 8  # packbits size, as svt.py:36-37
