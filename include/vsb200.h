@@ -83,6 +83,14 @@ int vs_classify_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_pa
 int vs_classify_dilate_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
                             uint32_t* bits, unsigned long long* count_opt, vs_stream_t stream);
 
+/* As vs_classify_dilate_bits, plus the tight box of the dilated flags (shrink_to_occupied of
+ * the whole volume, the k-d root box, kdtree.py:398) into device int[6] bbox_opt as
+ * {lo x, y, z, hi x, y, z} (hi x < 0: no flag), found in the same pass. */
+int vs_classify_dilate_bits_bbox(const uint8_t* bins, int nx, int ny, int nz,
+                                 const vs_tf_params* tf, uint32_t* bits,
+                                 unsigned long long* count_opt, int* bbox_opt,
+                                 vs_stream_t stream);
+
 /* _dilate26: 3x3x3 box OR, neighbourhood clipped at the borders.  in != out. */
 int vs_dilate_bits(const uint32_t* in, int nx, int ny, int nz, uint32_t* out,
                    vs_stream_t stream);
@@ -305,6 +313,10 @@ int vs_tight_box(const uint32_t* bits, int nx, int ny, int nz, const int32_t* bo
  * The result handle is read with vs_kd_result_info / _copy and released with _free. */
 int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, int binned,
                 int bins, int cs, void** handle, vs_stream_t stream);
+/* As vs_kd_build with the root box precomputed on the device (device int[6] from
+ * vs_classify_dilate_bits_bbox; NULL: computed from the bits). */
+int vs_kd_build_bbox(const uint32_t* bits, int nx, int ny, int nz, const int* bbox, int deep,
+                     int mls, int binned, int bins, int cs, void** handle, vs_stream_t stream);
 int vs_kd_result_info(void* handle, int64_t* m, int* root, int* height);
 int vs_kd_result_copy(void* handle, int32_t* lo, int32_t* hi, int8_t* axis, int32_t* plane,
                       int32_t* left, int32_t* right, vs_stream_t stream);

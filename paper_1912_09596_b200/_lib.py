@@ -27,6 +27,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_classify_summary": (i32, [P, i32, i32, i32, P, P, P, P, P]),
     "vs_classify_bits": (i32, [P, i32, i32, i32, P, P, P, P]),
     "vs_classify_dilate_bits": (i32, [P, i32, i32, i32, P, P, P, P]),
+    "vs_classify_dilate_bits_bbox": (i32, [P, i32, i32, i32, P, P, P, P, P]),
     "vs_dilate_bits": (i32, [P, i32, i32, i32, P, P]),
     "vs_pack_bits": (i32, [P, i32, i32, i32, P, P]),
     "vs_unpack_bits": (i32, [P, i32, i32, i32, P, P]),
@@ -45,6 +46,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_box_count": (i32, [P, i32, i32, i32, i32, P, i32, P, P]),
     "vs_tight_box": (i32, [P, i32, i32, i32, P, P, P]),
     "vs_kd_build": (i32, [P, i32, i32, i32, i32, i32, i32, i32, i32, P, P]),
+    "vs_kd_build_bbox": (i32, [P, i32, i32, i32, P, i32, i32, i32, i32, i32, P, P]),
     "vs_kd_result_info": (i32, [P, P, P, P]),
     "vs_kd_result_copy": (i32, [P, P, P, P, P, P, P, P]),
     "vs_kd_result_free": (None, [P]),

@@ -335,7 +335,8 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
                                                    uint32_t* red, const uint8_t* __restrict__ vol,
                                                    int nx, int ny, int nz,
                                                    uint32_t* __restrict__ out,
-                                                   unsigned long long* __restrict__ count) {
+                                                   unsigned long long* __restrict__ count,
+                                                   int* __restrict__ bbox) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nzw = nz >> 5;
   const int ty = DIL ? CP_TY : (int)(blockDim.x >> 5);
@@ -370,6 +371,9 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
   } else {
     // y/z-dilated words of slabs x-1, x (ring), output row = warp
     uint32_t prev = 0, cur = 0;
+    // tight box of the dilated flags (shrink_to_occupied of the whole volume, the k-d root,
+    // kdtree.py:398) as a by-product: x / z extremes of this thread's output words
+    int bx0 = 0x3fffffff, bx1 = -1, bz0 = 0x3fffffff, bz1 = -1;
     // three slabs in flight ahead of the one being classified; the y-dilation exchange is
     // double-buffered so one barrier per slab suffices
     uint4 fa = make_uint4(0, 0, 0, 0), fb = fa, ga = fa, gb = fa;
@@ -395,12 +399,32 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
       uint32_t yd = 0;
       if (warp >= 1 && warp <= CP_TY) yd = zb[(warp - 1) * 32 + lane] | zd | zb[(warp + 1) * 32 + lane];
       // slab xs - 1 is complete: prev (xs-2) | cur (xs-1) | yd (xs)
-      if (outrow && xs - 1 >= x0) out[((int64_t)(xs - 1) * ny + y) * nzw + lane] = prev | cur | yd;
+      if (outrow && xs - 1 >= x0) {
+        const uint32_t dw = prev | cur | yd;
+        out[((int64_t)(xs - 1) * ny + y) * nzw + lane] = dw;
+        if (dw) {
+          bx0 = min(bx0, xs - 1);
+          bx1 = xs - 1;
+          bz0 = min(bz0, 32 * lane + __ffs(dw) - 1);
+          bz1 = max(bz1, 32 * lane + 31 - __clz(dw));
+        }
+      }
       prev = cur;
       cur = yd;
       a = na; b = nb;
       na = fa; nb = fb;
       fa = ga; fb = gb;
+    }
+    if (bbox) {
+      bx0 = __reduce_min_sync(0xffffffffu, bx0);
+      bx1 = __reduce_max_sync(0xffffffffu, bx1);
+      bz0 = __reduce_min_sync(0xffffffffu, bz0);
+      bz1 = __reduce_max_sync(0xffffffffu, bz1);
+      if (lane == 0 && bx1 >= 0) {  // few warps see flags: global atomics per warp
+        atomicMin(bbox + 0, bx0); atomicMax(bbox + 3, bx1 + 1);
+        atomicMin(bbox + 1, y);   atomicMax(bbox + 4, y + 1);
+        atomicMin(bbox + 2, bz0); atomicMax(bbox + 5, bz1 + 1);
+      }
     }
   }
   if (count) {
@@ -415,14 +439,15 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
   }
 }
 
-#define VS_CP_ARGS ve, zs, red, vol, nx, ny, nz, out, count
+#define VS_CP_ARGS ve, zs, red, vol, nx, ny, nz, out, count, bbox
 
 template <bool DIL>
 __global__ void __launch_bounds__(1024) k_classify_pack(const uint8_t* __restrict__ vol, int nx,
                                                         int ny, int nz,
                                                         const vs_tf_params* __restrict__ tf,
                                                         uint32_t* __restrict__ out,
-                                                        unsigned long long* __restrict__ count) {
+                                                        unsigned long long* __restrict__ count,
+                                                        int* __restrict__ bbox) {
   __shared__ uint8_t tab[256];
   __shared__ uint32_t zs[2 * (CP_TY + 2) * 32];
   __shared__ uint32_t red[32];
@@ -445,6 +470,11 @@ __global__ void __launch_bounds__(1024) k_classify_pack(const uint8_t* __restric
     case V_CONST: classify_pack_body<V_CONST, DIL>(VS_CP_ARGS); break;
     default: classify_pack_body<V_TABLE, DIL>(VS_CP_ARGS); break;
   }
+}
+
+// Empty tight box {FAR, FAR, FAR, -1, -1, -1} for the atomic min / max of k_classify_pack.
+__global__ void k_bbox_init(int* __restrict__ bbox) {
+  if (threadIdx.x < 6) bbox[threadIdx.x] = threadIdx.x < 3 ? 0x3fffffff : -1;
 }
 
 __global__ void k_quantize(const float* __restrict__ f, int64_t n, uint8_t* __restrict__ out) {
@@ -803,7 +833,7 @@ int vs_classify_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_pa
   if (!bins || !tf || !bits || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_classify_bits");
   if (nz % 32 == 0 && nz <= 1024 && (reinterpret_cast<uintptr_t>(bins) & 15) == 0) {
     dim3 grid((unsigned)cdiv(ny, 32), (unsigned)cdiv(nx, CP_XC));
-    k_classify_pack<false><<<grid, 1024, 0, S(st)>>>(bins, nx, ny, nz, tf, bits, count);
+    k_classify_pack<false><<<grid, 1024, 0, S(st)>>>(bins, nx, ny, nz, tf, bits, count, nullptr);
     return check_launch("k_classify_pack");
   }
   const int64_t nwords = (int64_t)nx * ny * nzw_of(nz);
@@ -812,15 +842,26 @@ int vs_classify_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_pa
   return check_launch("k_classify_bits");
 }
 
-int vs_classify_dilate_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
-                            uint32_t* bits, unsigned long long* count, vs_stream_t st) {
+int vs_classify_dilate_bits_bbox(const uint8_t* bins, int nx, int ny, int nz,
+                                 const vs_tf_params* tf, uint32_t* bits,
+                                 unsigned long long* count, int* bbox, vs_stream_t st) {
   if (!bins || !tf || !bits || nx < 1 || ny < 1 || nz < 1)
     return fail_arg("vs_classify_dilate_bits");
   if (nz % 32 != 0 || nz > 1024 || (reinterpret_cast<uintptr_t>(bins) & 15) != 0)
     return fail_arg("vs_classify_dilate_bits: needs nz % 32 == 0, nz <= 1024, 16-byte aligned");
+  if (bbox) {
+    k_bbox_init<<<1, 32, 0, S(st)>>>(bbox);
+    VS_TRY(check_launch("k_bbox_init"));
+  }
   dim3 grid((unsigned)cdiv(ny, CP_TY), (unsigned)cdiv(nx, CP_XC));
-  k_classify_pack<true><<<grid, 32 * (CP_TY + 2), 0, S(st)>>>(bins, nx, ny, nz, tf, bits, count);
+  k_classify_pack<true><<<grid, 32 * (CP_TY + 2), 0, S(st)>>>(bins, nx, ny, nz, tf, bits, count,
+                                                             bbox);
   return check_launch("k_classify_pack<dilate>");
+}
+
+int vs_classify_dilate_bits(const uint8_t* bins, int nx, int ny, int nz, const vs_tf_params* tf,
+                            uint32_t* bits, unsigned long long* count, vs_stream_t st) {
+  return vs_classify_dilate_bits_bbox(bins, nx, ny, nz, tf, bits, count, nullptr, st);
 }
 
 int vs_dilate_bits(const uint32_t* in, int nx, int ny, int nz, uint32_t* out, vs_stream_t st) {

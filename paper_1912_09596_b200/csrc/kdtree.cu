@@ -21,10 +21,13 @@
 //   k_emit_level: rows of the level, the next level's boxes (left then right) and their work
 //     sizes (prep_node), scanned on the device (k_multi_scan).
 // Finalisation: subtree sizes bottom-up, preorder numbers top-down, scatter rows.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cfloat>
+#include <climits>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -32,6 +35,8 @@
 #include "common.cuh"
 
 namespace vs {
+
+namespace cg = cooperative_groups;
 
 constexpr int KD_FAR = 0x3fffffff;  // "no coordinate" sentinel for minima (kdtree.py:40 _FAR)
 
@@ -354,6 +359,7 @@ struct KdParams {
   int binned;
   int bins, cs;
   int64_t root_vol;
+  int subtrees;      // sweep builder: small nodes are finished by k_subtrees (1) or per level (0)
 };
 
 struct KdDecision {
@@ -361,12 +367,32 @@ struct KdDecision {
   int plane;
   int nchild;        // bit0 left present, bit1 right present
   int dropped;       // binned leaf whose shrink is empty (no row)
+  int sub;           // -1; SUB_DEFER: the node's subtree is built by k_subtrees
   Box left, right;   // global boxes
   Box leaf;          // leaf row box (binned: shrunk)
 };
 
 __device__ __forceinline__ bool halted(const KdParams& P, int64_t vol) {
   return P.deep ? vol <= 512 : vol * 10 <= P.root_vol;  // kdtree.py:421-424
+}
+
+// ---- subtree hand-off (sweep builder) -------------------------------------------------------
+// A node whose box fits one CTA's shared memory (extents <= SUB_EXT, packed bits <= SUB_WORDS
+// words) and that is not a leaf outright is built to completion -- its whole subtree, in the
+// reference's DFS preorder -- by one CTA of k_subtrees instead of level by level: the deep
+// levels of a tree are long chains of small nodes, where a level-synchronous pass costs a few
+// launches and a host round trip per level.
+constexpr int SUB_EXT = 128;
+constexpr int SUB_WORDS = 10240;
+constexpr int SUB_DEFER = -2;
+
+__device__ __forceinline__ bool defer_node(const KdParams& P, const Box& b) {
+  if (P.binned || !P.subtrees) return false;
+  const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
+  if (ex > SUB_EXT || ey > SUB_EXT || ez > SUB_EXT) return false;
+  if ((int64_t)ex * ey * ((ez + 31) >> 5) > SUB_WORDS) return false;
+  const int mx = max(ex, max(ey, ez));
+  return !halted(P, box_vol(b)) || (P.mls >= 0 && mx > P.mls);
 }
 
 // Row-order tight box (axis row, other1, other2) in local coordinates; empty if hi0 < 0.
@@ -723,7 +749,15 @@ __global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
   const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
   const int64_t vol = box_vol(b);
   KdDecision d;
-  d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.leaf = b;
+  d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.sub = -1; d.leaf = b;
+  if (defer_node(P, b)) {  // built by k_subtrees
+    if (t == 0) {
+      d.sub = SUB_DEFER;
+      out[i] = d;
+      child_count[i] = 0;
+    }
+    return;
+  }
   bool split = false;
   const Span* spx = span_x + L.off[A_X][i];
   const Span* spy = span_y + L.off[A_Y][i];
@@ -807,7 +841,7 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
   const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
   const int64_t vol = box_vol(b);
   KdDecision d;
-  d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.leaf = b;
+  d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.sub = -1; d.leaf = b;
   bool split = false;
   int nlo[3], nhi[3];
   for (int k = 0; k < 3; ++k) node_cell_range(b, P.cs, B.nc, k, nlo[k], nhi[k]);
@@ -966,6 +1000,7 @@ __global__ void k_cbox_init(CBox* __restrict__ c, int64_t n) {
 struct NodeRec {   // per node, global BFS id
   Box box;
   int axis, plane, left, right, dropped, level;
+  int sub;         // -1, SUB_DEFER (level loop), then the subtree id (k_collect_sub)
 };
 
 // Per-node work sizes of a level (written where the node's box is emitted).
@@ -983,7 +1018,7 @@ __device__ __forceinline__ void prep_node(const PrepCtx& C, const Box& b, int64_
   if (!P.binned) {
     const int mx = max(ext[0], max(ext[1], ext[2]));
     const bool need = !halted(P, box_vol(b)) || (P.mls >= 0 && mx > P.mls);
-    if (need) {
+    if (need && !defer_node(P, b)) {
       const int wz = (ext[2] + 31) >> 5;
       v[A_X] = ext[0];
       v[A_Y] = ext[1];
@@ -1044,6 +1079,7 @@ __global__ void k_emit_level(const KdDecision* __restrict__ dec, const int64_t* 
   r.left = r.right = -1;
   r.dropped = d.dropped;
   r.level = level;
+  r.sub = d.sub;
   int64_t o = coff[i];
   if (d.nchild & 1) {
     next_box[o] = d.left;
@@ -1293,18 +1329,23 @@ __global__ void __launch_bounds__(256) k_bits_bbox(const uint32_t* __restrict__ 
 }
 
 // Finalisation: subtree sizes (bottom-up per level), preorder (top-down per level), rows.
+// Rows under record r: its own row plus its children's subtrees; a deferred node's subtree
+// (k_subtrees) counts as built.
+__device__ __forceinline__ int rec_size(const NodeRec& r, const int* __restrict__ size,
+                                        const int* __restrict__ sub_count) {
+  if (r.dropped) return 0;
+  if (r.sub >= 0) return sub_count[r.sub];
+  int s = 1;
+  if (r.left >= 0) s += size[r.left];
+  if (r.right >= 0) s += size[r.right];
+  return s;
+}
+
 __global__ void k_sizes(const NodeRec* __restrict__ rec, int64_t b0, int64_t b1,
-                        int* __restrict__ size) {
+                        const int* __restrict__ sub_count, int* __restrict__ size) {
   const int64_t i = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b1) return;
-  const NodeRec r = rec[i];
-  int s = 0;
-  if (!r.dropped) {
-    s = 1;
-    if (r.left >= 0) s += size[r.left];
-    if (r.right >= 0) s += size[r.right];
-  }
-  size[i] = s;
+  size[i] = rec_size(rec[i], size, sub_count);
 }
 
 __global__ void k_preorder(const NodeRec* __restrict__ rec, int64_t b0, int64_t b1,
@@ -1323,20 +1364,14 @@ __global__ void k_preorder(const NodeRec* __restrict__ rec, int64_t b0, int64_t 
 // so a block-wide barrier per level replaces two launches per level).
 __global__ void __launch_bounds__(1024) k_order_levels(const NodeRec* __restrict__ rec,
                                                        const int64_t* __restrict__ level_base,
-                                                       int nlevels, int* __restrict__ size,
+                                                       int nlevels,
+                                                       const int* __restrict__ sub_count,
+                                                       int* __restrict__ size,
                                                        int* __restrict__ pre) {
   for (int l = nlevels - 1; l >= 0; --l) {
     const int64_t b0 = level_base[l], b1 = level_base[l + 1];
-    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const NodeRec r = rec[i];
-      int s = 0;
-      if (!r.dropped) {
-        s = 1;
-        if (r.left >= 0) s += size[r.left];
-        if (r.right >= 0) s += size[r.right];
-      }
-      size[i] = s;
-    }
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
+      size[i] = rec_size(rec[i], size, sub_count);
     __syncthreads();
   }
   if (threadIdx.x == 0) pre[0] = 0;
@@ -1364,7 +1399,7 @@ __global__ void k_scatter_rows(const NodeRec* __restrict__ rec, int64_t total,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   const NodeRec r = rec[i];
-  if (r.dropped) return;
+  if (r.dropped || r.sub >= 0) return;  // deferred nodes: k_scatter_sub
   const int p = pre[i];
   for (int k = 0; k < 3; ++k) { lo[3 * p + k] = r.box.lo[k]; hi[3 * p + k] = r.box.hi[k]; }
   axis[p] = (int8_t)r.axis;
@@ -1372,6 +1407,1264 @@ __global__ void k_scatter_rows(const NodeRec* __restrict__ rec, int64_t total,
   left[p] = (r.left >= 0 && size[r.left] > 0) ? pre[r.left] : -1;
   right[p] = (r.right >= 0 && size[r.right] > 0) ? pre[r.right] : -1;
   atomicMax(height, r.level + 1);
+}
+
+// ---- subtrees: one CTA builds a deferred node's whole subtree from shared memory ----------
+// The node's packed bits are staged once (R-local rows, z words from the box's first z); the
+// CTA then runs the reference recursion itself (kdtree.py:479-484: emit, then left subtree,
+// then right) with an explicit stack, so rows come out in local DFS preorder.  Per node:
+//   1. spans: warp per group of x slabs (lanes over y) -- x-slab spans and (x, z-word)
+//      projections by segment reductions, y-slab spans and (y, z-word) projections by shared
+//      atomics; z-slab spans from the projections (thread per z);
+//   2. warps 0..2 sweep axes x, y, z (first-minimum cut, prefix / suffix tight boxes by warp
+//      scans); warp 3 the forced middle split's exact boxes;
+//   3. thread 0 decides (strict < across axes, cost < volume, else forced, else leaf), writes
+//      the row and pushes right then left child.
+// Rows go to a global pool in 32-row chunks (chunk table in shared memory, copied out at the
+// end); k_scatter_sub places them once the global preorder is known.
+constexpr int SUB_T = 128;
+constexpr int SUB_STACK = 3 * SUB_EXT + 8;
+constexpr int SUB_CHUNK = 32;
+constexpr int SUB_MAXCH = 1024;  // 32768 rows per subtree
+
+struct SubRow {
+  int lo[3], hi[3];
+  int axis, plane, left, right;
+};
+
+struct SubEntry {
+  short lo[3], hi[3];
+  int parent;
+  short depth, right;
+};
+
+struct SubAxis {
+  long long cost;
+  int k, valid;
+  RBox l, r;
+};
+
+struct SubSmem {
+  Span spx[SUB_EXT], spy[SUB_EXT], spz[SUB_EXT];
+  uint32_t pxz[SUB_EXT * 4], pyz[SUB_EXT * 4];
+  SubEntry stack[SUB_STACK];
+  int chunk[SUB_MAXCH];
+  SubAxis ax[3], forced;
+  SubEntry cur;
+  int sp, count, maxdepth, status, choff;
+};
+
+struct SubCtx {
+  const NodeRec* rec;
+  const int* list;
+  SubRow* pool;
+  long long pool_chunks;              // capacity in chunks
+  unsigned long long* pool_used;      // chunks handed out
+  int* count;                         // rows per subtree
+  int* height;                        // local height per subtree
+  int* choff;                         // chunk-table offset per subtree
+  int* chunks;                        // chunk tables, concatenated
+  unsigned long long* chunks_used;
+  int* status;                        // bit 0: pool exhausted, bit 1: a subtree too large
+};
+
+__device__ __forceinline__ RBox rb_shfl_up(const RBox& r, int o) {
+  return RBox{__shfl_up_sync(0xffffffffu, r.lo0, o), __shfl_up_sync(0xffffffffu, r.lo1, o),
+              __shfl_up_sync(0xffffffffu, r.lo2, o), __shfl_up_sync(0xffffffffu, r.hi0, o),
+              __shfl_up_sync(0xffffffffu, r.hi1, o), __shfl_up_sync(0xffffffffu, r.hi2, o)};
+}
+__device__ __forceinline__ RBox rb_shfl_down(const RBox& r, int o) {
+  return RBox{__shfl_down_sync(0xffffffffu, r.lo0, o), __shfl_down_sync(0xffffffffu, r.lo1, o),
+              __shfl_down_sync(0xffffffffu, r.lo2, o), __shfl_down_sync(0xffffffffu, r.hi0, o),
+              __shfl_down_sync(0xffffffffu, r.hi1, o), __shfl_down_sync(0xffffffffu, r.hi2, o)};
+}
+__device__ __forceinline__ RBox rb_warp_reduce(RBox r) {
+  return RBox{__reduce_min_sync(0xffffffffu, r.lo0), __reduce_min_sync(0xffffffffu, r.lo1),
+              __reduce_min_sync(0xffffffffu, r.lo2), __reduce_max_sync(0xffffffffu, r.hi0),
+              __reduce_max_sync(0xffffffffu, r.hi1), __reduce_max_sync(0xffffffffu, r.hi2)};
+}
+
+// Slab spans of node b (R-local box) from the staged words: spx / spy / spz in node-local
+// coordinates, as k_spans_rows / k_spans_z produce them.
+__device__ void sub_spans(SubSmem& sm, const uint32_t* __restrict__ words, int eyR, int wzR,
+                          const Box& b) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
+  const int w0 = b.lo[2] >> 5, w1 = (b.hi[2] - 1) >> 5, nwz = w1 - w0 + 1;
+  uint32_t m[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t v = w < nwz ? 0xffffffffu : 0u;
+    if (w == 0) v &= 0xffffffffu << (b.lo[2] & 31);
+    if (w == nwz - 1 && (b.hi[2] & 31)) v &= (1u << (b.hi[2] & 31)) - 1u;
+    m[w] = v;
+  }
+  for (int i = t; i < ey; i += SUB_T) sm.spy[i] = Span{KD_FAR, -1, KD_FAR, -1};
+  for (int i = t; i < ey * nwz; i += SUB_T) sm.pyz[i] = 0u;
+  __syncthreads();
+  // x slabs: lane groups of gw lanes (pow2 >= ey, <= 32), G = 32 / gw slabs per warp step
+  const int gw = ey >= 32 ? 32 : group_width(ey), G = 32 / gw;
+  const int g = lane / gw, yl = lane & (gw - 1);
+  for (int xb = warp * G; xb < ex; xb += (SUB_T / 32) * G) {
+    const int x = xb + g;
+    int ymn = KD_FAR, ymx = -1, zmn = KD_FAR, zmx = -1;
+    uint32_t o[4] = {0u, 0u, 0u, 0u};
+    if (x < ex) {
+      for (int y = yl; y < ey; y += gw) {
+        const uint32_t* row = words + ((b.lo[0] + x) * eyR + b.lo[1] + y) * wzR + w0;
+        uint32_t v[4];
+        int zl = KD_FAR, zh = -1;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          v[w] = w < nwz ? row[w] & m[w] : 0u;
+          o[w] |= v[w];
+        }
+#pragma unroll
+        for (int w = 3; w >= 0; --w)
+          if (v[w]) zl = 32 * (w0 + w) + __ffs(v[w]) - 1;
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (v[w]) zh = 32 * (w0 + w) + 31 - __clz(v[w]);
+        if (zh >= 0) {
+          zl -= b.lo[2];
+          zh -= b.lo[2];
+          ymn = min(ymn, y);
+          ymx = max(ymx, y);
+          zmn = min(zmn, zl);
+          zmx = max(zmx, zh);
+          Span* d = &sm.spy[y];
+          atomicMin(&d->mn1, x);
+          atomicMax(&d->mx1, x);
+          atomicMin(&d->mn2, zl);
+          atomicMax(&d->mx2, zh);
+#pragma unroll
+          for (int w = 0; w < 4; ++w)
+            if (v[w]) atomicOr(&sm.pyz[y * nwz + w], v[w]);
+        }
+      }
+    }
+    for (int off = 1; off < gw; off <<= 1) {
+      ymn = min(ymn, __shfl_xor_sync(0xffffffffu, ymn, off));
+      ymx = max(ymx, __shfl_xor_sync(0xffffffffu, ymx, off));
+      zmn = min(zmn, __shfl_xor_sync(0xffffffffu, zmn, off));
+      zmx = max(zmx, __shfl_xor_sync(0xffffffffu, zmx, off));
+#pragma unroll
+      for (int w = 0; w < 4; ++w) o[w] |= __shfl_xor_sync(0xffffffffu, o[w], off);
+    }
+    if (yl == 0 && x < ex) {
+      sm.spx[x] = Span{ymn, ymx, zmn, zmx};
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (w < nwz) sm.pxz[x * nwz + w] = o[w];
+    }
+  }
+  __syncthreads();
+  // z slabs from the projections: first / last x (y) whose projection holds the z bit
+  for (int z = t; z < ez; z += SUB_T) {
+    const int zr = b.lo[2] + z, wi = (zr >> 5) - w0, bit = zr & 31;
+    Span sp{KD_FAR, -1, KD_FAR, -1};
+    int x = 0;
+    while (x < ex && !((sm.pxz[x * nwz + wi] >> bit) & 1u)) ++x;
+    if (x < ex) {
+      sp.mn1 = x;
+      x = ex - 1;
+      while (!((sm.pxz[x * nwz + wi] >> bit) & 1u)) --x;
+      sp.mx1 = x;
+      int y = 0;
+      while (!((sm.pyz[y * nwz + wi] >> bit) & 1u)) ++y;
+      sp.mn2 = y;
+      y = ey - 1;
+      while (!((sm.pyz[y * nwz + wi] >> bit) & 1u)) --y;
+      sp.mx2 = y;
+    }
+    sm.spz[z] = sp;
+  }
+  __syncthreads();
+}
+
+// _axis_sweep + first-minimum cut for one axis (one warp; e <= SUB_EXT: four slabs per lane).
+__device__ void sub_sweep_axis(const Span* __restrict__ sp, int e, SubAxis& out) {
+  const int lane = threadIdx.x & 31;
+  if (e < 2) {
+    if (lane == 0) out.valid = 0;
+    return;
+  }
+  const int per = (e + 31) >> 5;
+  const int s0 = min(e, lane * per), s1 = min(e, s0 + per);
+  RBox sb[4];
+  RBox loc = rb_empty();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    sb[j] = s0 + j < s1 ? slab_box(sp, s0 + j) : rb_empty();
+    loc = rb_join(loc, sb[j]);
+  }
+  // inclusive scans of the lane runs: prefix (up) and suffix (down)
+  RBox pin = loc, sin = loc;
+  for (int o = 1; o < 32; o <<= 1) {
+    const RBox u = rb_shfl_up(pin, o), d = rb_shfl_down(sin, o);
+    if (lane >= o) pin = rb_join(pin, u);
+    if (lane + o < 32) sin = rb_join(sin, d);
+  }
+  RBox before = rb_shfl_up(pin, 1), after = rb_shfl_down(sin, 1);
+  if (lane == 0) before = rb_empty();
+  if (lane == 31) after = rb_empty();
+  RBox suf[5];
+  suf[4] = after;
+#pragma unroll
+  for (int j = 3; j >= 0; --j) suf[j] = s0 + j < s1 ? rb_join(sb[j], suf[j + 1]) : suf[j + 1];
+  long long bc = LLONG_MAX;
+  int bk = 0, bj = -1;
+  RBox pre = before;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (s0 + j < s1) {
+      pre = rb_join(pre, sb[j]);
+      if (s0 + j + 1 < e) {
+        const long long c = rvol(pre) + rvol(suf[j + 1]);
+        if (c < bc) { bc = c; bk = s0 + j + 1; bj = j; }
+      }
+    }
+  }
+  long long wc = bc;
+  int wk = bk;
+  for (int o = 16; o; o >>= 1) {
+    const long long c2 = __shfl_xor_sync(0xffffffffu, wc, o);
+    const int k2 = __shfl_xor_sync(0xffffffffu, wk, o);
+    if (c2 < wc || (c2 == wc && k2 < wk)) { wc = c2; wk = k2; }
+  }
+  if (bj >= 0 && bc == wc && bk == wk) {  // the winner: prefix through k-1, suffix from k
+    RBox l = before;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j <= bj) l = rb_join(l, sb[j]);
+    RBox r = suf[4];
+#pragma unroll
+    for (int j = 3; j >= 0; --j)
+      if (j > bj && s0 + j < s1) r = rb_join(r, sb[j]);
+    out.cost = wc;
+    out.k = wk;
+    out.valid = 1;
+    out.l = l;
+    out.r = r;
+  }
+}
+
+// forced_split's exact children (kdtree.py:441-467): tight boxes of slabs [0, k) and [k, e).
+__device__ void sub_forced(const Span* __restrict__ sp, int e, int k, SubAxis& out) {
+  const int lane = threadIdx.x & 31;
+  RBox l = rb_empty(), r = rb_empty();
+  for (int s = lane; s < e; s += 32) {
+    if (s < k) l = rb_join(l, slab_box(sp, s));
+    else r = rb_join(r, slab_box(sp, s));
+  }
+  l = rb_warp_reduce(l);
+  r = rb_warp_reduce(r);
+  if (lane == 0) { out.k = k; out.valid = 1; out.l = l; out.r = r; }
+}
+
+__device__ __forceinline__ Box sub_box(const SubEntry& e) {
+  Box b;
+  for (int k = 0; k < 3; ++k) { b.lo[k] = e.lo[k]; b.hi[k] = e.hi[k]; }
+  return b;
+}
+
+__device__ __forceinline__ bool sub_push(SubSmem& sm, const Box& b, int parent, int depth,
+                                         int right) {
+  if (sm.sp >= SUB_STACK) return false;
+  SubEntry e;
+  for (int k = 0; k < 3; ++k) { e.lo[k] = (short)b.lo[k]; e.hi[k] = (short)b.hi[k]; }
+  e.parent = parent;
+  e.depth = (short)depth;
+  e.right = (short)right;
+  sm.stack[sm.sp++] = e;
+  return true;
+}
+
+__global__ void __launch_bounds__(SUB_T) k_subtrees(const uint32_t* __restrict__ bits, int ny,
+                                                    int nzw, KdParams P, SubCtx C) {
+  extern __shared__ __align__(16) unsigned char sub_smem[];
+  SubSmem& sm = *reinterpret_cast<SubSmem*>(sub_smem);
+  uint32_t* words = reinterpret_cast<uint32_t*>(sub_smem + ((sizeof(SubSmem) + 15) & ~size_t(15)));
+  const int t = threadIdx.x, warp = t >> 5;
+  const int s = blockIdx.x;
+  const Box RB = C.rec[C.list[s]].box;
+  const int exR = RB.hi[0] - RB.lo[0], eyR = RB.hi[1] - RB.lo[1], ezR = RB.hi[2] - RB.lo[2];
+  const int wzR = (ezR + 31) >> 5;
+  const int nw = exR * eyR * wzR;
+  for (int q = t; q < nw; q += SUB_T) {
+    const int w = q % wzR, rr = q / wzR, y = rr % eyR, x = rr / eyR;
+    words[q] = local_word(bits + ((int64_t)(RB.lo[0] + x) * ny + RB.lo[1] + y) * nzw, RB.lo[2],
+                          RB.hi[2], w);
+  }
+  if (t == 0) {
+    Box root;
+    for (int k = 0; k < 3; ++k) { root.lo[k] = 0; root.hi[k] = RB.hi[k] - RB.lo[k]; }
+    sm.sp = 0;
+    sub_push(sm, root, -1, 1, 0);
+    sm.count = 0;
+    sm.maxdepth = 0;
+    sm.status = 0;
+  }
+  for (;;) {
+    if (t == 0) {
+      if (sm.sp == 0 || sm.status) sm.cur.depth = -1;
+      else sm.cur = sm.stack[--sm.sp];
+    }
+    __syncthreads();
+    const SubEntry e = sm.cur;
+    if (e.depth < 0) break;
+    const Box b = sub_box(e);
+    const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
+    const int64_t vol = box_vol(b);
+    const bool sweep = !halted(P, vol);
+    int fa = 0, fe = ex;
+    if (ey > fe) { fa = 1; fe = ey; }
+    if (ez > fe) { fa = 2; fe = ez; }
+    const bool forced = P.mls >= 0 && fe > P.mls;
+    if (sweep || forced) {
+      sub_spans(sm, words, eyR, wzR, b);
+      if (warp < 3) {
+        const int a = warp;
+        if (sweep)
+          sub_sweep_axis(a == 0 ? sm.spx : (a == 1 ? sm.spy : sm.spz),
+                         a == 0 ? ex : (a == 1 ? ey : ez), sm.ax[a]);
+        else if ((t & 31) == 0)
+          sm.ax[a].valid = 0;
+      } else if (forced) {
+        sub_forced(fa == 0 ? sm.spx : (fa == 1 ? sm.spy : sm.spz), fe, fe / 2, sm.forced);
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      int a = -1, k = 0;
+      RBox l, r;
+      if (sweep) {
+        long long bc = 0;
+        for (int q = 0; q < 3; ++q) {
+          const SubAxis& A = sm.ax[q];
+          if (!A.valid || (a >= 0 && A.cost >= bc)) continue;
+          a = q; k = A.k; bc = A.cost; l = A.l; r = A.r;
+        }
+        if (a >= 0 && bc >= vol) a = -1;  // acceptance: cost < volume (kdtree.py:431, 436)
+      }
+      if (a < 0 && forced) { a = fa; k = sm.forced.k; l = sm.forced.l; r = sm.forced.r; }
+      const int p = sm.count;
+      bool ok = true;
+      if ((p & (SUB_CHUNK - 1)) == 0) {
+        const int ci = p / SUB_CHUNK;
+        if (ci >= SUB_MAXCH) {
+          sm.status |= 2;
+          ok = false;
+        } else {
+          const unsigned long long c = atomicAdd(C.pool_used, 1ull);
+          if ((long long)c >= C.pool_chunks) { sm.status |= 1; ok = false; }
+          else sm.chunk[ci] = (int)c;
+        }
+      }
+      if (ok) {
+        sm.count = p + 1;
+        sm.maxdepth = max(sm.maxdepth, (int)e.depth);
+        SubRow* row = C.pool + (int64_t)sm.chunk[p / SUB_CHUNK] * SUB_CHUNK + (p & (SUB_CHUNK - 1));
+        SubRow w;
+        for (int q = 0; q < 3; ++q) { w.lo[q] = RB.lo[q] + b.lo[q]; w.hi[q] = RB.lo[q] + b.hi[q]; }
+        w.axis = a;
+        w.plane = a < 0 ? -1 : RB.lo[a] + (a == 0 ? b.lo[0] : (a == 1 ? b.lo[1] : b.lo[2])) + k;
+        w.left = -1;
+        w.right = -1;
+        *row = w;
+        if (e.parent >= 0) {
+          SubRow* pr = C.pool + (int64_t)sm.chunk[e.parent / SUB_CHUNK] * SUB_CHUNK +
+                       (e.parent & (SUB_CHUNK - 1));
+          if (e.right) pr->right = p; else pr->left = p;
+        }
+        if (a >= 0) {  // right first: the left subtree is emitted next (DFS preorder)
+          if (r.hi0 >= 0 && !sub_push(sm, to_global(b, a, r), p, e.depth + 1, 1)) sm.status |= 2;
+          if (l.hi0 >= 0 && !sub_push(sm, to_global(b, a, l), p, e.depth + 1, 0)) sm.status |= 2;
+        }
+      }
+    }
+  }
+  if (t == 0) {
+    const int nch = (sm.count + SUB_CHUNK - 1) / SUB_CHUNK;
+    sm.choff = (int)atomicAdd(C.chunks_used, (unsigned long long)nch);
+    C.count[s] = sm.count;
+    C.height[s] = sm.maxdepth;
+    C.choff[s] = sm.choff;
+    if (sm.status) atomicOr(C.status, sm.status);
+  }
+  __syncthreads();
+  const int nch = (sm.count + SUB_CHUNK - 1) / SUB_CHUNK;
+  for (int i = t; i < nch; i += SUB_T) C.chunks[sm.choff + i] = sm.chunk[i];
+}
+
+// Deferred records -> subtree ids (order irrelevant: every subtree is independent).
+// Also sums a generous row-pool estimate (chunks: 1 + volume / 4096 per subtree).
+__global__ void k_collect_sub(NodeRec* __restrict__ rec, int64_t total, int* __restrict__ list,
+                              int64_t* __restrict__ nsub, int64_t* __restrict__ chunk_est) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total || rec[i].sub != SUB_DEFER) return;
+  const int id = (int)atomicAdd(reinterpret_cast<unsigned long long*>(nsub), 1ull);
+  rec[i].sub = id;
+  list[id] = (int)i;
+  atomicAdd(reinterpret_cast<unsigned long long*>(chunk_est),
+            (unsigned long long)(1 + box_vol(rec[i].box) / 4096));
+}
+
+// A subtree's rows at its global preorder p0 (the deferred record's), child links shifted.
+__global__ void k_scatter_sub(const NodeRec* __restrict__ rec, const int* __restrict__ list,
+                              SubCtx C, const int* __restrict__ pre, int32_t* __restrict__ lo,
+                              int32_t* __restrict__ hi, int8_t* __restrict__ axis,
+                              int32_t* __restrict__ plane, int32_t* __restrict__ left,
+                              int32_t* __restrict__ right, int* __restrict__ height) {
+  const int s = blockIdx.x;
+  const int ri = list[s];
+  const int p0 = pre[ri], cnt = C.count[s], off = C.choff[s];
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+    const SubRow w = C.pool[(int64_t)C.chunks[off + j / SUB_CHUNK] * SUB_CHUNK + (j & (SUB_CHUNK - 1))];
+    const int p = p0 + j;
+    for (int k = 0; k < 3; ++k) { lo[3 * p + k] = w.lo[k]; hi[3 * p + k] = w.hi[k]; }
+    axis[p] = (int8_t)w.axis;
+    plane[p] = w.plane;
+    left[p] = w.left >= 0 ? p0 + w.left : -1;
+    right[p] = w.right >= 0 ? p0 + w.right : -1;
+  }
+  if (threadIdx.x == 0) atomicMax(height, rec[ri].level + C.height[s]);
+}
+
+// ---- device-resident level loop (sweep builder) ---------------------------------------------
+// The sweep tree's top is a long spine of big nodes (a cut often peels a thin slab off a node,
+// so a 512^3 blob volume has ~75 levels of nodes too big for k_subtrees).  k_levels runs all
+// those levels in ONE cooperative launch, two grid barriers per level:
+//   phase A  every warp of the grid takes (node, slab, 64-row chunk) items of the level
+//            (rows_or, as k_spans_rows) and merges x / y slab spans and the [w][slab] z-word
+//            projections into the node's storage with atomics;
+//   phase B  CTA per node: z-slab spans from the projections (ballots), the three sweeps
+//            (block scans over a thread's run of slabs), acceptance / forced split, then the
+//            children: rows (BFS records, level-ordered, slots by atomics), work entries for
+//            the children that need a decision, their span / projection storage initialised.
+// Leaves and deferred children (k_subtrees) get their record and no work entry.  Anything
+// that does not fit the preallocated state (level width, records, storage, extents > 1024)
+// aborts the launch and the host reruns the level-by-level path.
+constexpr int LV_T = 256;
+constexpr int LV_W = LV_T / 32;
+constexpr int LV_NMAX = 1024;   // work nodes per level
+constexpr int LV_EMAX = 1024;   // node extent per axis
+
+struct LvNode {
+  Box box;
+  int rec;
+  int sx, sy, sz;    // x / y slab spans (phase A) and z slab spans (phase B) in the span arena
+  long long pz;      // [w][x] then [w][y] z-word projections in the level's word arena
+};
+
+struct LvCounters {
+  int nwork[2];
+  int nrec[2];       // records of the next level (by its parity)
+  int abort;
+  int nlevels;
+  unsigned long long span_used[2];
+  unsigned long long proj_used[2];
+  long long total;
+  long long root_vol;
+};
+
+struct LvCtx {
+  const uint32_t* bits;
+  int nx, ny, nz, nzw;
+  KdParams P;
+  const int* bbox;
+  LvCounters* C;
+  LvNode* work[2];
+  NodeRec* rec;
+  long long rec_cap;
+  long long* level_base;
+  int level_cap;
+  Span* span[2];
+  long long span_cap;
+  uint32_t* proj[2];
+  long long proj_cap;
+  long long* prof;   // optional: %globaltimer at each phase boundary (3 per level)
+  bool vec;          // packed rows 16-byte aligned (nzw % 4 == 0): phase A loads uint4
+  struct LvAxisRes* res;  // 3 per work node
+  int* arrive;            // per work node: axis CTAs done (reset by the deciding CTA)
+  int* zarrive;           // per work node: z-column groups done (reset by the last one)
+};
+
+__device__ __forceinline__ long long lv_now() {
+  long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+
+struct LvSmem {
+  int off[LV_NMAX + 1];        // phase A: item offsets of the level's nodes
+  Span stage[LV_EMAX];         // phase B: the axis' slab spans
+  RBox suf[LV_EMAX];           // phase B: suffix boxes
+  RBox wbox[LV_W];
+  long long wcost[LV_W];
+  int wk[LV_W];
+  int wsum[LV_W];
+  RBox best_l, best_r, ax_l[3], ax_r[3];
+  long long ax_cost[3];
+  int ax_k[3];
+  int cnew[2];                 // work slots of the new children (-1 none)
+  LvNode cnode[2];
+  int last;
+};
+
+// Phase-A row geometry of a node: lanes per row (a lane group; 16-byte vectors when the
+// packed rows allow it -- four z words per load) and rows per item (at most SPAN_CHUNK, two
+// 8-deep load rounds).
+struct LvGeom {
+  int gwa, nwg, sh, wz;
+  bool direct, vec;
+  int v0, nv;   // vector path: first vector, vectors covering the node's stored words
+  int gw, G, R;
+};
+__device__ __forceinline__ LvGeom lv_geom(const Box& b, bool vec_ok) {
+  LvGeom q;
+  q.gwa = b.lo[2] >> 5;
+  q.sh = b.lo[2] & 31;
+  q.nwg = ((b.hi[2] - 1) >> 5) - q.gwa + 1;
+  q.wz = wz_of(b);
+  q.direct = q.nwg <= 32;
+  q.vec = q.direct && vec_ok;
+  q.v0 = q.gwa >> 2;
+  q.nv = ((q.gwa + q.nwg - 1) >> 2) - q.v0 + 1;
+  q.gw = group_width(q.vec ? q.nv : (q.direct ? q.nwg : q.wz));
+  q.G = 32 / q.gw;
+  q.R = min(SPAN_CHUNK, 16 * q.G);
+  return q;
+}
+__device__ __forceinline__ int lv_items(const Box& b, bool vec_ok) {
+  const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], R = lv_geom(b, vec_ok).R;
+  return ex * ((ey + R - 1) / R) + ey * ((ex + R - 1) / R);
+}
+
+// One slab's rows [r0, r1) with 16-byte loads: lane group of gw lanes per row, each lane one
+// 4-word vector (masked to the node's stored words), U rows per lane in flight.
+template <int U>
+__device__ __forceinline__ void rows_or_v4(const uint32_t* __restrict__ bits, int ny, int nzw,
+                                           int ax, int slab, int x0, int y0, int r0, int r1,
+                                           int G, int g, int gw, uint32_t gmask, int vidx,
+                                           uint4 m, uint4& acc, int& rmin, int& rmax) {
+  for (int rb = r0; rb < r1; rb += G * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = min(rb + u * G + g, r1 - 1);
+      const int x = ax == 0 ? slab : x0 + r;
+      const int y = ax == 0 ? y0 + r : slab;
+      v[u] = __ldg(reinterpret_cast<const uint4*>(bits + ((int64_t)x * ny + y) * nzw) + vidx);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = rb + u * G + g < r1;
+      uint4 w;
+      w.x = ok ? v[u].x & m.x : 0u;
+      w.y = ok ? v[u].y & m.y : 0u;
+      w.z = ok ? v[u].z & m.z : 0u;
+      w.w = ok ? v[u].w & m.w : 0u;
+      const uint32_t bm = __ballot_sync(0xffffffffu, (w.x | w.y | w.z | w.w) != 0);
+      if ((bm >> (g * gw)) & gmask) {
+        const int r = rb + u * G + g;
+        rmin = min(rmin, r);
+        rmax = max(rmax, r);
+      }
+      acc.x |= w.x; acc.y |= w.y; acc.z |= w.z; acc.w |= w.w;
+    }
+  }
+}
+
+__device__ __forceinline__ LvNode lv_load(const LvNode* p) {
+  LvNode n;
+  const int* s = reinterpret_cast<const int*>(p);
+  int* d = reinterpret_cast<int*>(&n);
+#pragma unroll
+  for (int k = 0; k < (int)(sizeof(LvNode) / 4); ++k) d[k] = __ldcg(s + k);
+  return n;
+}
+__device__ __forceinline__ Span lv_span(const Span* p) {
+  const int4 v = __ldcg(reinterpret_cast<const int4*>(p));
+  return Span{v.x, v.y, v.z, v.w};
+}
+
+// Block-wide exclusive scan of one int per thread (LV_T threads).
+__device__ int lv_scan_int(int v, LvSmem& sm, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  __syncthreads();
+  if (lane == 31) sm.wsum[warp] = inc;
+  __syncthreads();
+  int before = 0;
+  total = 0;
+  for (int w = 0; w < LV_W; ++w) {
+    if (w < warp) before += sm.wsum[w];
+    total += sm.wsum[w];
+  }
+  return before + inc - v;
+}
+
+// ---- phase A: slab spans and projections of every node of the level ------------------------
+__device__ void lv_phase_a(const LvCtx& X, const LvNode* __restrict__ work, int n, Span* spans,
+                           uint32_t* proj, LvSmem& sm, long long* pf) {
+  const int t = threadIdx.x, lane = t & 31;
+  // item offsets (n <= LV_NMAX: NPT nodes per thread)
+  constexpr int NPT = LV_NMAX / LV_T;
+  int c[NPT], sum = 0;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const int i = NPT * t + j;
+    c[j] = i < n ? lv_items(lv_load(work + i).box, X.vec) : 0;
+    sum += c[j];
+  }
+  int total;
+  int run = lv_scan_int(sum, sm, total);
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const int i = NPT * t + j;
+    if (i <= n) sm.off[i] = run;
+    run += c[j];
+  }
+  if (t == 0) sm.off[n] = total;
+  __syncthreads();
+  if (pf) { pf[5] = lv_now(); pf[7] = total; }
+  // a contiguous range of items per CTA, its warps striding through it: a warp's node
+  // changes rarely (found by stepping forward, the node reloaded only then)
+  const int chunk = (total + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * chunk, b1 = min(total, b0 + chunk);
+  int node = -1;
+  LvNode nd;
+  for (int it = b0 + (t >> 5); it < b1; it += LV_W) {
+    if (node < 0 || it >= sm.off[node + 1]) {
+      if (node < 0) {
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.off[mid] <= it) lo = mid; else hi = mid - 1;
+        }
+        node = lo;
+      } else {
+        while (it >= sm.off[node + 1]) ++node;
+      }
+      nd = lv_load(work + node);
+    }
+    const Box b = nd.box;
+    const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1];
+    const LvGeom q = lv_geom(b, X.vec);
+    int local = it - sm.off[node];
+    const int chx = (ey + q.R - 1) / q.R, nxi = ex * chx;
+    const int AX = local < nxi ? 0 : 1;
+    if (AX) local -= nxi;
+    const int nch = AX == 0 ? chx : (ex + q.R - 1) / q.R;
+    const int s = local / nch, cc = local - s * nch;
+    const int er = AX == 0 ? ey : ex, es = AX == 0 ? ex : ey;
+    const int r0 = cc * q.R, r1 = min(er, r0 + q.R);
+    const int wz = q.wz, sh = q.sh, gw = q.gw, G = q.G;
+    const int g = lane / gw, wl = lane & (gw - 1);
+    const uint32_t gmask = gw == 32 ? 0xffffffffu : ((1u << gw) - 1u);
+    const int slab = b.lo[AX] + s;
+    const int hb = b.hi[2] & 31;
+    uint32_t acc = 0;
+    int rmin = KD_FAR, rmax = -1;
+    if (q.vec) {
+      // lane wl loads vector v0 + wl: words 4(v0 + wl) .. +3, masked to [gwa, gwa + nwg)
+      uint4 m;
+      uint32_t mk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int w = 4 * (q.v0 + wl) + j;
+        uint32_t mm = wl < q.nv && w >= q.gwa && w < q.gwa + q.nwg ? 0xffffffffu : 0u;
+        if (w == q.gwa) mm &= 0xffffffffu << sh;
+        if (w == q.gwa + q.nwg - 1 && hb) mm &= (1u << hb) - 1u;
+        mk[j] = mm;
+      }
+      m.x = mk[0]; m.y = mk[1]; m.z = mk[2]; m.w = mk[3];
+      uint4 a4 = make_uint4(0u, 0u, 0u, 0u);
+      rows_or_v4<8>(X.bits, X.ny, X.nzw, AX, slab, b.lo[0], b.lo[1], r0, r1, G, g, gw, gmask,
+                    q.v0 + min(wl, q.nv - 1), m, a4, rmin, rmax);
+      for (int o = gw; o < 32; o <<= 1) {
+        a4.x |= __shfl_xor_sync(0xffffffffu, a4.x, o);
+        a4.y |= __shfl_xor_sync(0xffffffffu, a4.y, o);
+        a4.z |= __shfl_xor_sync(0xffffffffu, a4.z, o);
+        a4.w |= __shfl_xor_sync(0xffffffffu, a4.w, o);
+        rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+        rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      }
+      // stored words -> node-local word `lane`: (S[gwa+lane] >> sh) | (S[gwa+lane+1] << 32-sh)
+      const int w1 = q.gwa + lane, w2 = w1 + 1;
+      const int l1 = min(31, (w1 >> 2) - q.v0), l2 = min(31, (w2 >> 2) - q.v0);
+      const uint32_t s1x = __shfl_sync(0xffffffffu, a4.x, l1), s1y = __shfl_sync(0xffffffffu, a4.y, l1);
+      const uint32_t s1z = __shfl_sync(0xffffffffu, a4.z, l1), s1w = __shfl_sync(0xffffffffu, a4.w, l1);
+      const uint32_t s2x = __shfl_sync(0xffffffffu, a4.x, l2), s2y = __shfl_sync(0xffffffffu, a4.y, l2);
+      const uint32_t s2z = __shfl_sync(0xffffffffu, a4.z, l2), s2w = __shfl_sync(0xffffffffu, a4.w, l2);
+      const int c1 = w1 & 3, c2 = w2 & 3;
+      const uint32_t S1 = c1 == 0 ? s1x : (c1 == 1 ? s1y : (c1 == 2 ? s1z : s1w));
+      const uint32_t S2 = c2 == 0 ? s2x : (c2 == 1 ? s2y : (c2 == 2 ? s2z : s2w));
+      acc = lane < wz ? ((S1 >> sh) | (sh ? S2 << (32 - sh) : 0u)) : 0u;
+    } else {
+      int w0, w1;
+      uint32_t wmask;
+      if (q.direct) {
+        w0 = w1 = q.gwa + min(wl, q.nwg - 1);
+        wmask = wl < q.nwg ? 0xffffffffu : 0u;
+        if (wl == 0) wmask &= 0xffffffffu << sh;
+        if (wl == q.nwg - 1 && hb) wmask &= (1u << hb) - 1u;
+      } else {
+        const int wc = min(wl, wz - 1);
+        const int gz = b.lo[2] + 32 * wc, rem = b.hi[2] - gz;
+        w0 = gz >> 5;
+        w1 = min(w0 + 1, X.nzw - 1);
+        wmask = wl < wz ? (rem < 32 ? (1u << rem) - 1u : 0xffffffffu) : 0u;
+      }
+      if (q.direct)
+        rows_or<8, true>(X.bits, X.ny, X.nzw, AX, slab, b.lo[0], b.lo[1], r0, r1, G, g, gw,
+                         gmask, w0, w1, 0, wmask, acc, rmin, rmax);
+      else
+        rows_or<8, false>(X.bits, X.ny, X.nzw, AX, slab, b.lo[0], b.lo[1], r0, r1, G, g, gw,
+                          gmask, w0, w1, sh, wmask, acc, rmin, rmax);
+      for (int o = gw; o < 32; o <<= 1) {
+        acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+        rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+        rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      }
+      if (q.direct) {  // stored words -> node-local words
+        const uint32_t nx2 = __shfl_down_sync(0xffffffffu, acc, 1);
+        if (sh) acc = (acc >> sh) | (wl + 1 < q.nwg ? nx2 << (32 - sh) : 0u);
+        if (wl >= wz) acc = 0u;
+      }
+      if (lane >= gw) acc = 0u;  // one copy of the node-local words: lanes 0 .. wz-1
+    }
+    const uint32_t mz = __ballot_sync(0xffffffffu, acc != 0);
+    if (rmax >= 0) {
+      const int wf = __ffs(mz) - 1, wlst = 31 - __clz(mz);
+      const uint32_t af = __shfl_sync(0xffffffffu, acc, wf), al = __shfl_sync(0xffffffffu, acc, wlst);
+      Span* dst = spans + (AX == 0 ? nd.sx : nd.sy) + s;
+      if (lane == 0) {
+        atomicMin(&dst->mn1, rmin);
+        atomicMax(&dst->mx1, rmax);
+        atomicMin(&dst->mn2, 32 * wf + __ffs(af) - 1);
+        atomicMax(&dst->mx2, 32 * wlst + 31 - __clz(al));
+      }
+      uint32_t* pdst = proj + nd.pz + (AX == 0 ? 0 : (long long)wz * ex) + s;
+      if (lane < wz && acc) atomicOr(pdst + (long long)lane * es, acc);
+    }
+  }
+  if (pf) {
+    __syncthreads();
+    if (t == 0) pf[6] = lv_now();
+  }
+}
+
+// Exclusive block scan (join) of one box per thread in thread order or reverse order.
+__device__ RBox lv_excl_scan(RBox x, bool rev, LvSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  RBox inc = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const RBox u = rev ? rb_shfl_down(inc, o) : rb_shfl_up(inc, o);
+    if (rev ? lane + o < 32 : lane >= o) inc = rb_join(inc, u);
+  }
+  RBox ex = rb_shfl(inc, rev ? min(lane + 1, 31) : max(lane - 1, 0));
+  if (rev ? lane == 31 : lane == 0) ex = rb_empty();
+  __syncthreads();
+  if (rev ? lane == 0 : lane == 31) sm.wbox[warp] = inc;
+  __syncthreads();
+  for (int w = 0; w < LV_W; ++w)
+    if (rev ? w > warp : w < warp) ex = rb_join(ex, sm.wbox[w]);
+  return ex;
+}
+
+__device__ RBox lv_reduce(RBox r, LvSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  r = rb_warp_reduce(r);
+  __syncthreads();
+  if (lane == 0) sm.wbox[warp] = r;
+  __syncthreads();
+  RBox t = rb_empty();
+  for (int w = 0; w < LV_W; ++w) t = rb_join(t, sm.wbox[w]);
+  return t;
+}
+
+// _axis_sweep over sm.stage[0, e): first-minimum cut, its cost and boxes (sm.best_l / _r).
+__device__ void lv_sweep(int e, LvSmem& sm, int& best_k, long long& best_cost) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int per = (e + LV_T - 1) / LV_T;
+  const int s0 = min(e, t * per), s1 = min(e, s0 + per);
+  RBox loc = rb_empty();
+  for (int s = s0; s < s1; ++s) loc = rb_join(loc, slab_box(sm.stage, s));
+  RBox r = lv_excl_scan(loc, true, sm);
+  for (int s = s1 - 1; s >= s0; --s) {
+    r = rb_join(r, slab_box(sm.stage, s));
+    sm.suf[s] = r;
+  }
+  RBox pre = lv_excl_scan(loc, false, sm);  // (its barriers publish suf)
+  long long bc = LLONG_MAX;
+  int bk = 0;
+  RBox bpre = rb_empty();
+  for (int s = s0; s < s1; ++s) {
+    pre = rb_join(pre, slab_box(sm.stage, s));
+    if (s + 1 < e) {
+      const long long c = rvol(pre) + rvol(sm.suf[s + 1]);
+      if (c < bc) { bc = c; bk = s + 1; bpre = pre; }
+    }
+  }
+  const long long my_c = bc;
+  const int my_k = bk;
+  for (int o = 16; o; o >>= 1) {
+    const long long c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+    const int k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+    if (c2 < bc || (c2 == bc && k2 < bk)) { bc = c2; bk = k2; }
+  }
+  __syncthreads();
+  if (lane == 0) { sm.wcost[warp] = bc; sm.wk[warp] = bk; }
+  __syncthreads();
+  bc = sm.wcost[0];
+  bk = sm.wk[0];
+  for (int w = 1; w < LV_W; ++w)
+    if (sm.wcost[w] < bc || (sm.wcost[w] == bc && sm.wk[w] < bk)) { bc = sm.wcost[w]; bk = sm.wk[w]; }
+  if (my_c == bc && my_k == bk && bc != LLONG_MAX) { sm.best_l = bpre; sm.best_r = sm.suf[bk]; }
+  __syncthreads();
+  best_k = bk;
+  best_cost = bc;
+}
+
+// Stage axis a's slab spans of node nd into sm.stage.
+__device__ void lv_stage(const LvCtx& X, const Span* spans, const LvNode& nd, int a, int e,
+                         LvSmem& sm) {
+  __syncthreads();
+  for (int s = threadIdx.x; s < e; s += LV_T)
+    sm.stage[s] = lv_span(spans + (a == 0 ? nd.sx : (a == 1 ? nd.sy : nd.sz)) + s);
+  __syncthreads();
+}
+
+// The children of a decided node (thread 0): records (level-ordered slots), and work entries
+// for those that need a decision.  The four counter atomics are issued together (one L2 round
+// trip), then consumed.
+__device__ void lv_children(const LvCtx& X, const Box* cb, const bool* has, int level,
+                            long long base_next, const KdParams& P, LvSmem& sm, int* rec_id) {
+  LvCounters* C = X.C;
+  const int nxt = (level + 1) & 1;
+  bool work[2] = {false, false}, deferred[2] = {false, false};
+  int nrec = 0, nwork = 0;
+  unsigned long long nspan = 0, nproj = 0;
+  for (int q = 0; q < 2; ++q) {
+    rec_id[q] = -1;
+    sm.cnew[q] = -1;
+    if (!has[q]) continue;
+    const Box& b = cb[q];
+    const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
+    const int mx = max(ex, max(ey, ez));
+    const bool need = !halted(P, box_vol(b)) || (P.mls >= 0 && mx > P.mls);
+    deferred[q] = need && defer_node(P, b);
+    work[q] = need && !deferred[q];
+    ++nrec;
+    if (work[q]) {
+      ++nwork;
+      nspan += ex + ey + ez;
+      nproj += ((unsigned long long)((ez + 31) >> 5) * (ex + ey) + 3) & ~3ull;
+      if (mx > LV_EMAX) atomicExch(&C->abort, 1);
+    }
+  }
+  if (!nrec) return;
+  const int r0 = atomicAdd(&C->nrec[nxt], nrec);
+  const int w0 = nwork ? atomicAdd(&C->nwork[nxt], nwork) : 0;
+  const unsigned long long s0 = nwork ? atomicAdd(&C->span_used[nxt], nspan) : 0;
+  const unsigned long long p0 = nwork ? atomicAdd(&C->proj_used[nxt], nproj) : 0;
+  if (base_next + r0 + nrec > X.rec_cap || w0 + nwork > LV_NMAX ||
+      (long long)(s0 + nspan) > X.span_cap || (long long)(p0 + nproj) > X.proj_cap) {
+    atomicExch(&C->abort, 1);
+    return;
+  }
+  int r = r0, w = w0;
+  unsigned long long so = s0, po = p0;
+  for (int q = 0; q < 2; ++q) {
+    if (!has[q]) continue;
+    const Box& b = cb[q];
+    const long long rid = base_next + r++;
+    rec_id[q] = (int)rid;
+    NodeRec rr;
+    rr.box = b;
+    rr.axis = -1; rr.plane = -1; rr.left = -1; rr.right = -1; rr.dropped = 0;
+    rr.level = level + 1;
+    rr.sub = deferred[q] ? SUB_DEFER : -1;
+    X.rec[rid] = rr;
+    if (!work[q]) continue;
+    const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
+    LvNode nd;
+    nd.box = b;
+    nd.rec = (int)rid;
+    nd.sx = (int)so;
+    nd.sy = (int)(so + ex);
+    nd.sz = (int)(so + ex + ey);
+    nd.pz = (long long)po;
+    so += ex + ey + ez;
+    po += ((unsigned long long)wz_of(b) * (ex + ey) + 3) & ~3ull;
+    X.work[nxt][w] = nd;
+    sm.cnew[q] = w++;
+    sm.cnode[q] = nd;
+  }
+}
+
+// Empty spans / zero projections for a new work node (the whole CTA).
+__device__ void lv_init_storage(const LvCtx& X, const LvNode& nd, int nxt) {
+  const Box& b = nd.box;
+  const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], wz = wz_of(b);
+  int4* sp = reinterpret_cast<int4*>(X.span[nxt] + nd.sx);
+  for (int i = threadIdx.x; i < ex + ey; i += LV_T) sp[i] = make_int4(KD_FAR, -1, KD_FAR, -1);
+  // projection blocks start 16-byte aligned (lv_children rounds them to 4 words)
+  uint4* pw = reinterpret_cast<uint4*>(X.proj[nxt] + nd.pz);
+  const long long nw = ((long long)wz * (ex + ey) + 3) >> 2;
+  for (long long i = threadIdx.x; i < nw; i += LV_T) pw[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+// ---- phase B: node decisions, one CTA per (node, axis) -------------------------------------
+// Each axis' sweep (and the forced split's boxes on the longest axis) runs on its own CTA and
+// is published to lv_res; the last of a node's three CTAs to arrive (arrival counter) decides
+// the node and creates its children -- the three sweeps run in parallel.
+struct LvAxisRes {
+  long long cost;
+  int k, valid, fvalid, pad;
+  RBox l, r, fl, fr;
+};
+
+// z-slab spans of node nd, columns [g*LV_W, g*LV_W + LV_W) of its 2*wz (axis, z word)
+// columns, one warp each: first / last x (y) whose projection word holds each z bit, into the
+// node's global z spans (x columns write mn1/mx1, y columns mn2/mx2; every field of every z
+// slab is written by exactly one column).  The [w][slab] column (<= 1024 slabs) is held in
+// registers, one word per lane per 32-slab chunk, and bit-transposed chunk by chunk.
+__device__ void lv_zcolumns(const uint32_t* __restrict__ proj, Span* __restrict__ zs,
+                            const LvNode& nd, int g, int kc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const Box& b = nd.box;
+  const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1], ez = b.hi[2] - b.lo[2];
+  const int wz = (ez + 31) >> 5;
+  for (int col = (g * LV_W + warp) * kc; col < min(2 * wz, (g * LV_W + warp + 1) * kc); ++col) {
+  const bool isx = col < wz;
+  const int w = isx ? col : col - wz;
+  const int e = isx ? ex : ey, nch = (e + 31) >> 5;
+  const uint32_t* p = proj + nd.pz + (isx ? 0 : (long long)wz * ex) + (long long)w * e;
+  uint32_t v[LV_EMAX / 32];
+#pragma unroll
+  for (int c = 0; c < LV_EMAX / 32; ++c) {
+    const int idx = c * 32 + lane;
+    v[c] = c < nch && idx < e ? __ldcg(p + idx) : 0u;
+  }
+  int first = KD_FAR, last = -1;
+#pragma unroll
+  for (int c = 0; c < LV_EMAX / 32; ++c) {
+    if (c < nch) {
+      uint32_t x = v[c];
+#pragma unroll
+      for (int j = 16; j >= 1; j >>= 1) {
+        const uint32_t m = j == 16 ? 0x0000ffffu : j == 8 ? 0x00ff00ffu : j == 4 ? 0x0f0f0f0fu
+                           : j == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+      }
+      if (x) {
+        if (first == KD_FAR) first = 32 * c + __ffs(x) - 1;
+        last = 32 * c + 31 - __clz(x);
+      }
+    }
+  }
+  const int z = 32 * w + lane;
+  if (z < ez) {
+    int* d = reinterpret_cast<int*>(zs + nd.sz + z) + (isx ? 0 : 2);
+    d[0] = first;
+    d[1] = last;
+  }
+  }  // columns of the warp
+}
+
+// z-column groups of a node (kc columns per warp, LV_W warps; one group even when z needs no
+// spans); kc is chosen per level so that the level's phase-B tasks fit the grid.
+__device__ __forceinline__ int lv_zgroups(const Box& b, int kc) {
+  const int wz = (b.hi[2] - b.lo[2] + 31) >> 5;
+  return (2 * wz + LV_W * kc - 1) / (LV_W * kc);
+}
+
+struct LvNodeInfo {
+  int ex, ey, ez, fa, fe;
+  bool sweep, forced;
+  int64_t vol;
+};
+__device__ __forceinline__ LvNodeInfo lv_info(const KdParams& P, const Box& b) {
+  LvNodeInfo f;
+  f.ex = b.hi[0] - b.lo[0]; f.ey = b.hi[1] - b.lo[1]; f.ez = b.hi[2] - b.lo[2];
+  f.fa = 0; f.fe = f.ex;
+  if (f.ey > f.fe) { f.fa = 1; f.fe = f.ey; }
+  if (f.ez > f.fe) { f.fa = 2; f.fe = f.ez; }
+  f.vol = box_vol(b);
+  f.sweep = !halted(P, f.vol);
+  f.forced = P.mls >= 0 && f.fe > P.mls;
+  return f;
+}
+
+__device__ void lv_finish(const LvCtx& X, const KdParams& P, const LvNode& nd, int i, int level,
+                          long long base_next, LvSmem& sm);
+__device__ void lv_axis(const LvCtx& X, const KdParams& P, const LvNode& nd, int i, int a,
+                        int level, long long base_next, LvSmem& sm);
+
+// Phase-B task q of node i: 0 / 1 the x / y sweep, 2.. the z-column groups; the last group
+// to finish runs the z sweep (lv_axis(2)) from the completed z spans.
+__device__ void lv_task(const LvCtx& X, const KdParams& P, const LvNode& nd, int i, int q,
+                        int kc, int level, long long base_next, LvSmem& sm) {
+  if (q < 2) {
+    lv_axis(X, P, nd, i, q, level, base_next, sm);
+    return;
+  }
+  const int cur = level & 1;
+  const LvNodeInfo f = lv_info(P, nd.box);
+  const bool need_z = (f.sweep && f.ez >= 2) || (f.forced && f.fa == 2);
+  if (need_z) lv_zcolumns(X.proj[cur], X.span[cur], nd, q - 2, kc);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int ng = lv_zgroups(nd.box, kc);
+    const int prev = atomicAdd(X.zarrive + i, 1);
+    sm.last = prev == ng - 1;
+    if (sm.last) X.zarrive[i] = 0;
+  }
+  __syncthreads();
+  if (sm.last) {
+    __threadfence();
+    lv_axis(X, P, nd, i, 2, level, base_next, sm);
+  }
+}
+
+// Axis a of node i (work-list index): its sweep and, on the longest axis, the forced boxes.
+__device__ void lv_axis(const LvCtx& X, const KdParams& P, const LvNode& nd, int i, int a,
+                        int level, long long base_next, LvSmem& sm) {
+  const int t = threadIdx.x;
+  const int cur = level & 1;
+  const LvNodeInfo f = lv_info(P, nd.box);
+  const int e = a == 0 ? f.ex : (a == 1 ? f.ey : f.ez);
+  const bool do_sweep = f.sweep && e >= 2, do_forced = f.forced && a == f.fa;
+  LvAxisRes* res = X.res + 3 * i + a;
+  if (do_sweep || do_forced) {
+    lv_stage(X, X.span[cur], nd, a, e, sm);
+    if (do_sweep) {
+      int k;
+      long long c;
+      lv_sweep(e, sm, k, c);
+      if (t == 0) { res->cost = c; res->k = k; res->l = sm.best_l; res->r = sm.best_r; }
+    }
+    if (do_forced) {
+      const int k = e / 2;
+      RBox lp = rb_empty(), rp = rb_empty();
+      for (int s = t; s < e; s += LV_T) {
+        if (s < k) lp = rb_join(lp, slab_box(sm.stage, s));
+        else rp = rb_join(rp, slab_box(sm.stage, s));
+      }
+      const RBox l = lv_reduce(lp, sm), r = lv_reduce(rp, sm);
+      if (t == 0) { res->fl = l; res->fr = r; }
+    }
+  }
+  if (t == 0) {
+    res->valid = do_sweep;
+    res->fvalid = do_forced;
+    if (X.prof && i == 0 && level < 1000) X.prof[16000 + 4 * level + a] = lv_now();
+    __threadfence();
+    sm.last = atomicAdd(X.arrive + i, 1) == 2;
+  }
+  __syncthreads();
+  if (sm.last) lv_finish(X, P, nd, i, level, base_next, sm);
+  __syncthreads();
+  if (sm.last && X.prof && i == 0 && t == 0 && level < 1000) X.prof[16000 + 4 * level + 3] = lv_now();
+}
+
+// The node's decision from its three axis results, its children and their storage.
+__device__ void lv_finish(const LvCtx& X, const KdParams& P, const LvNode& nd, int i, int level,
+                          long long base_next, LvSmem& sm) {
+  const int t = threadIdx.x;
+  const Box b = nd.box;
+  if (t == 0) {
+    __threadfence();
+    const LvNodeInfo f = lv_info(P, b);
+    // the three axis results in one round of independent L2 loads
+    constexpr int RW = sizeof(LvAxisRes) / 4;
+    int rw[3][RW];
+    const int* src = reinterpret_cast<const int*>(X.res + 3 * i);
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int j = 0; j < RW; ++j) rw[q][j] = __ldcg(src + q * RW + j);
+    const LvAxisRes* res = reinterpret_cast<const LvAxisRes*>(&rw[0][0]);
+    int a = -1, k = 0;
+    long long bc = 0;
+    RBox l, r;
+    if (f.sweep) {
+      for (int q = 0; q < 3; ++q) {
+        if (!res[q].valid || (a >= 0 && res[q].cost >= bc)) continue;
+        a = q; bc = res[q].cost; k = res[q].k; l = res[q].l; r = res[q].r;
+      }
+      if (a >= 0 && bc >= f.vol) a = -1;  // acceptance: cost < volume (kdtree.py:431, 436)
+    }
+    if (a < 0 && f.forced) {
+      a = f.fa;
+      k = f.fe / 2;
+      l = res[a].fl;
+      r = res[a].fr;
+    }
+    NodeRec me;
+    me.box = b;
+    me.axis = a;
+    me.plane = a < 0 ? -1 : (a == 0 ? b.lo[0] : (a == 1 ? b.lo[1] : b.lo[2])) + k;
+    me.left = me.right = -1;
+    me.dropped = 0;
+    me.level = level;
+    me.sub = -1;
+    sm.cnew[0] = sm.cnew[1] = -1;
+    if (a >= 0) {
+      Box cb[2];
+      bool has[2] = {l.hi0 >= 0, r.hi0 >= 0};
+      if (has[0]) cb[0] = to_global(b, a, l);
+      if (has[1]) cb[1] = to_global(b, a, r);
+      int rid[2];
+      lv_children(X, cb, has, level, base_next, P, sm, rid);
+      me.left = rid[0];
+      me.right = rid[1];
+    }
+    X.rec[nd.rec] = me;
+    X.arrive[i] = 0;
+  }
+  __syncthreads();
+  const int nxt = (level + 1) & 1;
+  for (int q = 0; q < 2; ++q)
+    if (sm.cnew[q] >= 0) lv_init_storage(X, sm.cnode[q], nxt);
+}
+
+__global__ void __launch_bounds__(LV_T, 2) k_levels(LvCtx X) {
+  extern __shared__ __align__(16) unsigned char lv_smem[];
+  LvSmem& sm = *reinterpret_cast<LvSmem*>(lv_smem);
+  cg::grid_group grid = cg::this_grid();
+  LvCounters* C = X.C;
+  const int t = threadIdx.x;
+  // root (kdtree.py:398): the bbox of every flag
+  Box root;
+  int bb[6];
+  for (int q = 0; q < 6; ++q) bb[q] = __ldcg(X.bbox + q);
+  for (int q = 0; q < 3; ++q) { root.lo[q] = bb[q]; root.hi[q] = bb[3 + q]; }
+  if (bb[3] < 0) {  // empty volume
+    if (blockIdx.x == 0 && t == 0) { C->nlevels = 0; C->total = 0; }
+    return;
+  }
+  KdParams P = X.P;
+  P.root_vol = box_vol(root);
+  {
+    const int ex = root.hi[0] - root.lo[0], ey = root.hi[1] - root.lo[1], ez = root.hi[2] - root.lo[2];
+    const int mx = max(ex, max(ey, ez));
+    const bool need = !halted(P, P.root_vol) || (P.mls >= 0 && mx > P.mls);
+    const bool deferred = need && defer_node(P, root);
+    const bool work = need && !deferred;
+    const int wz = (ez + 31) >> 5;
+    if (blockIdx.x == 0 && t == 0) {
+      NodeRec r;
+      r.box = root;
+      r.axis = r.plane = r.left = r.right = -1;
+      r.dropped = 0;
+      r.level = 0;
+      r.sub = deferred ? SUB_DEFER : -1;
+      X.rec[0] = r;
+      X.level_base[0] = 0;
+      C->nwork[0] = work ? 1 : 0;
+      if (work) {
+        if (mx > LV_EMAX) C->abort = 1;
+        LvNode nd;
+        nd.box = root; nd.rec = 0; nd.sx = 0; nd.sy = ex; nd.sz = ex + ey; nd.pz = 0;
+        X.work[0][0] = nd;
+      }
+    }
+    if (work) {  // root storage, grid-stride
+      const long long nspan = ex + ey + ez, nw = (long long)wz * (ex + ey);
+      const long long g0 = (long long)blockIdx.x * LV_T + t, gs = (long long)gridDim.x * LV_T;
+      for (long long i = g0; i < nspan; i += gs) X.span[0][i] = Span{KD_FAR, -1, KD_FAR, -1};
+      for (long long i = g0; i < nw; i += gs) X.proj[0][i] = 0u;
+    }
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && t == 0) C->root_vol = P.root_vol;
+  long long base = 0, nrec = 1;
+  int level = 0;
+  for (;;) {
+    if (X.prof && blockIdx.x == 0 && t == 0 && level < 1000) X.prof[3 * level] = lv_now();
+    const int cur = level & 1, nxt = cur ^ 1;
+    const int n = *(volatile int*)&C->nwork[cur];
+    if (n == 0 || *(volatile int*)&C->abort) break;
+    if (blockIdx.x == 0 && t == 0) {
+      C->nwork[nxt] = 0;
+      C->nrec[nxt] = 0;
+      C->span_used[nxt] = 0;
+      C->proj_used[nxt] = 0;
+    }
+    lv_phase_a(X, X.work[cur], n, X.span[cur], X.proj[cur], sm,
+               X.prof && blockIdx.x == 0 && level < 1000 ? X.prof + 3000 + 8 * level : nullptr);
+    grid.sync();
+    if (X.prof && blockIdx.x == 0 && t == 0 && level < 1000) X.prof[3 * level + 1] = lv_now();
+    {
+      // task offsets: 2 + z-column groups per node (every CTA scans them itself); columns per
+      // warp kc so that the tasks fit the grid
+      constexpr int NPT = LV_NMAX / LV_T;
+      int c[NPT], wzs[NPT], sum = 0;
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        const int i = NPT * t + j;
+        wzs[j] = 0;
+        if (i < n) {
+          const LvNode* w = X.work[cur] + i;
+          wzs[j] = (__ldcg(&w->box.hi[2]) - __ldcg(&w->box.lo[2]) + 31) >> 5;
+          sum += 2 * wzs[j];
+        }
+      }
+      int total;
+      lv_scan_int(sum, sm, total);  // total z columns of the level
+      const int spare = max((int)gridDim.x - 2 * n, n);
+      const int kc = max(1, (total + spare * LV_W - 1) / (spare * LV_W));
+      sum = 0;
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        const int i = NPT * t + j;
+        c[j] = i < n ? 2 + (2 * wzs[j] + LV_W * kc - 1) / (LV_W * kc) : 0;
+        sum += c[j];
+      }
+      int run = lv_scan_int(sum, sm, total);
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        const int i = NPT * t + j;
+        if (i <= n) sm.off[i] = run;
+        run += c[j];
+      }
+      __syncthreads();
+      int i = 0;
+      for (int task = blockIdx.x; task < total; task += gridDim.x) {
+        while (task >= sm.off[i + 1]) ++i;
+        const LvNode nd = lv_load(X.work[cur] + i);
+        lv_task(X, P, nd, i, task - sm.off[i], kc, level, base + nrec, sm);
+        __syncthreads();
+      }
+    }
+    grid.sync();
+    if (X.prof && blockIdx.x == 0 && t == 0 && level < 1000) X.prof[3 * level + 2] = lv_now();
+    const long long nn = *(volatile int*)&C->nrec[nxt];
+    base += nrec;
+    nrec = nn;
+    ++level;
+    if (level + 1 >= X.level_cap) {
+      if (blockIdx.x == 0 && t == 0) C->abort = 1;
+      break;
+    }
+    if (blockIdx.x == 0 && t == 0) X.level_base[level] = base;
+  }
+  if (blockIdx.x == 0 && t == 0 && !*(volatile int*)&C->abort) {
+    const int nl = nrec > 0 ? level + 1 : level;
+    C->nlevels = nl;
+    C->total = base + nrec;
+    X.level_base[nl] = base + nrec;
+  }
 }
 
 }  // namespace vs
@@ -1483,22 +2776,18 @@ unsigned grid_for(int64_t items, int per_block, int cap = 148 * 64) {
 
 }  // namespace
 
-extern "C" {
+namespace {
+
+constexpr int KD_RETRY_LEVELS = 1000;  // a subtree outgrew one CTA: rebuild level by level
 
 // Level-synchronous build with one host synchronisation per level: the level's work sizes
 // are computed where its boxes are emitted (prep_node) and scanned on the device; the host
 // reads {node count, totals} once, sizes the level's buffers and launches the span passes,
-// the decisions and the next level's emission.
-int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, int binned,
-                int bins, int cs, void** handle, vs_stream_t stream) {
-  if (!bits || !handle || nx < 1 || ny < 1 || nz < 1 || bins < 2 || cs < 1)
-    return fail_arg("vs_kd_build");
-  if (bins > 65) return fail_arg("vs_kd_build: bins > 65");
-  if (nz > 1024) return fail_arg("vs_kd_build: nz > 1024");
-  cudaStream_t st = S(stream);
-  auto* R = new KdResultImpl();
-  *handle = R;
-  for (DBuf* b : {&R->lo, &R->hi, &R->axis, &R->plane, &R->left, &R->right}) b->st = st;
+// the decisions and the next level's emission.  Nodes small enough for one CTA leave the
+// level loop (sweep builder) and are finished by k_subtrees.
+int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, int binned,
+             int bins, int cs, const int* bbox_in, int subtrees, int dev_levels,
+             KdResultImpl* R, cudaStream_t st) {
   const int nzw = (int)nzw_of(nz);
 
   DBuf bb, cur, nxt, offs, dec, cnt, spx, spy, spz, pxz, pyz, scr, rec, cellb, cslab, sizes, pre,
@@ -1509,6 +2798,7 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
 
   KdParams P;
   P.deep = deep; P.mls = mls; P.binned = binned; P.bins = bins; P.cs = cs; P.root_vol = 0;
+  P.subtrees = subtrees && !binned;
   const int ncx = (int)cdiv(nx, cs), ncy = (int)cdiv(ny, cs), ncz = (int)cdiv(nz, cs);
   // side stream (per device, cached) + fork/join events for the concurrent span passes
   int dev = 0;
@@ -1578,8 +2868,110 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
   const int init[8] = {KD_FAR, KD_FAR, KD_FAR, -1, -1, -1, 0, 0};
   VS_CUDA(cudaMemcpyAsync(dbb, init, sizeof init, cudaMemcpyHostToDevice, st), "bbox init");
   VS_CUDA(cudaMemsetAsync(dh, 0, H * sizeof(int64_t), st), "header init");
-  k_bits_bbox<<<SPAN_BLOCKS, 256, 0, st>>>(bits, nx, ny, nz, dbb);
-  VS_TRY(check_launch("k_bits_bbox"));
+  if (bbox_in) {  // the root box came with the bits (k_classify_pack)
+    VS_CUDA(cudaMemcpyAsync(dbb, bbox_in, 6 * sizeof(int), cudaMemcpyDeviceToDevice, st),
+            "bbox copy");
+  } else {
+    k_bits_bbox<<<SPAN_BLOCKS, 256, 0, st>>>(bits, nx, ny, nz, dbb);
+    VS_TRY(check_launch("k_bits_bbox"));
+  }
+  std::vector<int64_t> level_base;
+  int64_t total = -1;
+  DBuf lv_work, lv_ctr, lv_lb, lv_span, lv_proj, lv_res;
+  for (DBuf* b : {&lv_work, &lv_ctr, &lv_lb, &lv_span, &lv_proj, &lv_res}) b->st = st;
+  if (P.subtrees && dev_levels && nx <= LV_EMAX && ny <= LV_EMAX && nz <= LV_EMAX) {
+    // the whole big-node part of the tree in one cooperative launch (k_levels)
+    const long long rec_cap = 1 << 18, span_cap = 2LL * LV_NMAX * LV_EMAX;
+    const long long proj_cap = std::max<long long>(4LL << 20, (long long)nx * ny * nzw / 4);
+    const int level_cap = 4096;
+    VS_TRY(rec.ensure(rec_cap * sizeof(NodeRec), "records"));
+    VS_TRY(lv_work.ensure(2 * LV_NMAX * sizeof(LvNode), "level work"));
+    VS_TRY(lv_ctr.ensure(sizeof(LvCounters), "level counters"));
+    VS_TRY(lv_lb.ensure(level_cap * sizeof(long long), "level bases"));
+    VS_TRY(lv_span.ensure(2 * span_cap * sizeof(Span), "level spans"));
+    VS_TRY(lv_proj.ensure(2 * proj_cap * sizeof(uint32_t), "level projections"));
+    VS_CUDA(cudaMemsetAsync(lv_ctr.p, 0, sizeof(LvCounters), st), "level counters");
+    const size_t res_bytes = 3 * LV_NMAX * sizeof(LvAxisRes);
+    VS_TRY(lv_res.ensure(res_bytes + 2 * LV_NMAX * sizeof(int), "axis results"));
+    VS_CUDA(cudaMemsetAsync(static_cast<char*>(lv_res.p) + res_bytes, 0,
+                            2 * LV_NMAX * sizeof(int), st), "arrivals");
+    LvCtx X;
+    X.bits = bits; X.nx = nx; X.ny = ny; X.nz = nz; X.nzw = nzw;
+    X.P = P;
+    X.bbox = dbb;
+    X.C = lv_ctr.as<LvCounters>();
+    X.work[0] = lv_work.as<LvNode>();
+    X.work[1] = lv_work.as<LvNode>() + LV_NMAX;
+    X.rec = rec.as<NodeRec>();
+    X.rec_cap = rec_cap;
+    X.level_base = lv_lb.as<long long>();
+    X.level_cap = level_cap;
+    X.span[0] = lv_span.as<Span>();
+    X.span[1] = lv_span.as<Span>() + span_cap;
+    X.span_cap = span_cap;
+    X.proj[0] = lv_proj.as<uint32_t>();
+    X.proj[1] = lv_proj.as<uint32_t>() + proj_cap;
+    X.proj_cap = proj_cap;
+    X.prof = nullptr;
+    X.vec = (nzw & 3) == 0 && ((uintptr_t)bits & 15) == 0;
+    X.res = lv_res.as<LvAxisRes>();
+    X.arrive = reinterpret_cast<int*>(static_cast<char*>(lv_res.p) + res_bytes);
+    X.zarrive = X.arrive + LV_NMAX;
+    DBuf lv_prof;
+    lv_prof.st = st;
+    const char* penv = getenv("VSB200_KD_PROFILE");
+    if (penv && penv[0] == '1') {
+      VS_TRY(lv_prof.ensure(20000 * sizeof(long long), "profile"));
+      VS_CUDA(cudaMemsetAsync(lv_prof.p, 0, 20000 * sizeof(long long), st), "profile");
+      X.prof = lv_prof.as<long long>();
+    }
+    const size_t smem = sizeof(LvSmem);
+    VS_CUDA(cudaFuncSetAttribute(k_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "k_levels smem");
+    int per_sm = 0, nsm = 0;
+    VS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels, LV_T, smem),
+            "k_levels occupancy");
+    VS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SM count");
+    if (per_sm > 0) {
+      void* args[] = {&X};
+      VS_CUDA(cudaLaunchCooperativeKernel((void*)k_levels, dim3(nsm * per_sm), dim3(LV_T), args,
+                                          smem, st), "k_levels");
+      LvCounters hc;
+      VS_TRY(d2h(&hc, lv_ctr.p, sizeof hc, st));
+      if (X.prof) {  // dev profile: per-phase sums over the levels
+        std::vector<long long> pr(20000);
+        VS_TRY(d2h(pr.data(), X.prof, pr.size() * sizeof(long long), st));
+        for (int l = 0; l < std::min(hc.nlevels - 1, 12); ++l)
+          fprintf(stderr, "  level %d node 0 axis done x %.1f y %.1f z %.1f finish %.1f us\n", l,
+                  (pr[16000 + 4 * l] - pr[3 * l + 1]) * 1e-3, (pr[16001 + 4 * l] - pr[3 * l + 1]) * 1e-3,
+                  (pr[16002 + 4 * l] - pr[3 * l + 1]) * 1e-3, (pr[16003 + 4 * l] - pr[3 * l + 1]) * 1e-3);
+        for (int l = 0; l < std::min(hc.nlevels - 1, 12); ++l)
+          fprintf(stderr, "  level %d: A scan %.1f block0 %.1f all %.1f us (%lld items) | B %.1f us\n",
+                  l, (pr[3000 + 8 * l + 5] - pr[3 * l]) * 1e-3,
+                  (pr[3000 + 8 * l + 6] - pr[3 * l]) * 1e-3, (pr[3 * l + 1] - pr[3 * l]) * 1e-3,
+                  pr[3000 + 8 * l + 7], (pr[3 * l + 2] - pr[3 * l + 1]) * 1e-3);
+        const int nl = std::min(hc.nlevels, 999);
+        double a = 0, b = 0, c = 0;
+        for (int l = 0; l + 1 < nl; ++l) {
+          a += pr[3 * l + 1] - pr[3 * l];
+          b += pr[3 * l + 2] - pr[3 * l + 1];
+          c += pr[3 * l + 3] - pr[3 * l + 2];
+        }
+        fprintf(stderr, "k_levels: %d levels, grid %d x %d: phase A %.1f us, phase B %.1f us, "
+                "between %.1f us\n", hc.nlevels, nsm, per_sm, a * 1e-3, b * 1e-3, c * 1e-3);
+      }
+      if (!hc.abort) {
+        P.root_vol = hc.root_vol;
+        total = hc.total;
+        if (total == 0) return 0;  // empty tree
+        std::vector<long long> lb(hc.nlevels + 1);
+        VS_TRY(d2h(lb.data(), lv_lb.p, lb.size() * sizeof(long long), st));
+        level_base.assign(lb.begin(), lb.end());
+      }
+    }
+  }
+  if (total < 0) {
+  level_base.clear();
   VS_TRY(arrays(1));
   VS_TRY(cur.ensure(sizeof(Box), "level"));
   {
@@ -1595,7 +2987,6 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
   }
 
   int64_t n = hh[0], base = 0;
-  std::vector<int64_t> level_base;
   int level = 0;
   while (n > 0) {
     level_base.push_back(base);
@@ -1725,8 +3116,57 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
     n = hh[0];
     ++level;
   }
-  const int64_t total = base;
+  total = base;
   level_base.push_back(total);
+  }  // level-by-level path
+  // deferred nodes: one CTA per subtree
+  DBuf subl, subc, subh, subo, pool, chunks;
+  for (DBuf* b : {&subl, &subc, &subh, &subo, &pool, &chunks}) b->st = st;
+  SubCtx SC = {};
+  int64_t nsub = 0;
+  if (P.subtrees && total > 0) {
+    VS_TRY(subl.ensure(total * sizeof(int), "subtree list"));
+    VS_CUDA(cudaMemsetAsync(dh, 0, 2 * sizeof(int64_t), st), "subtree count");
+    k_collect_sub<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(rec.as<NodeRec>(), total,
+                                                            subl.as<int>(), dh, dh + 1);
+    VS_TRY(check_launch("k_collect_sub"));
+    int64_t cnt2[2];
+    VS_TRY(d2h(cnt2, dh, sizeof cnt2, st));
+    nsub = cnt2[0];
+    if (nsub > 0) {
+      VS_TRY(subc.ensure(nsub * sizeof(int), "subtree counts"));
+      VS_TRY(subh.ensure(nsub * sizeof(int), "subtree heights"));
+      VS_TRY(subo.ensure(nsub * sizeof(int), "subtree chunk offsets"));
+      const size_t smem = ((sizeof(SubSmem) + 15) & ~size_t(15)) + SUB_WORDS * sizeof(uint32_t);
+      VS_CUDA(cudaFuncSetAttribute(k_subtrees, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem), "k_subtrees smem");
+      int64_t pool_chunks = std::max<int64_t>(cnt2[1], 1024);  // k_collect_sub's estimate
+      for (;;) {
+        VS_TRY(pool.ensure(pool_chunks * SUB_CHUNK * sizeof(SubRow), "subtree rows"));
+        VS_TRY(chunks.ensure((pool_chunks + nsub) * sizeof(int), "subtree chunks"));
+        VS_CUDA(cudaMemsetAsync(dh + 1, 0, 3 * sizeof(int64_t), st), "subtree counters");
+        SC.rec = rec.as<NodeRec>();
+        SC.list = subl.as<int>();
+        SC.pool = pool.as<SubRow>();
+        SC.pool_chunks = pool_chunks;
+        SC.pool_used = reinterpret_cast<unsigned long long*>(dh + 1);
+        SC.chunks_used = reinterpret_cast<unsigned long long*>(dh + 2);
+        SC.status = reinterpret_cast<int*>(dh + 3);
+        SC.count = subc.as<int>();
+        SC.height = subh.as<int>();
+        SC.choff = subo.as<int>();
+        SC.chunks = chunks.as<int>();
+        k_subtrees<<<(unsigned)nsub, SUB_T, smem, st>>>(bits, ny, nzw, P, SC);
+        VS_TRY(check_launch("k_subtrees"));
+        int64_t res[3];
+        VS_TRY(d2h(res, dh + 1, sizeof res, st));
+        const int status = (int)(res[2] & 0xffffffff);
+        if (status & 2) return KD_RETRY_LEVELS;
+        if (!(status & 1)) break;
+        pool_chunks = std::max<int64_t>(2 * pool_chunks, res[0] + res[0] / 4);
+      }
+    }
+  }
   VS_TRY(sizes.ensure(total * sizeof(int), "sizes"));
   VS_TRY(pre.ensure(total * sizeof(int), "preorder"));
   const int nlev = (int)level_base.size() - 1;
@@ -1736,14 +3176,14 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
     VS_TRY(lb.ensure(level_base.size() * sizeof(int64_t), "level bases"));
     VS_CUDA(cudaMemcpyAsync(lb.p, level_base.data(), level_base.size() * sizeof(int64_t),
                             cudaMemcpyHostToDevice, st), "level bases");
-    k_order_levels<<<1, 1024, 0, st>>>(rec.as<NodeRec>(), lb.as<int64_t>(), nlev, sizes.as<int>(),
-                                       pre.as<int>());
+    k_order_levels<<<1, 1024, 0, st>>>(rec.as<NodeRec>(), lb.as<int64_t>(), nlev, subc.as<int>(),
+                                       sizes.as<int>(), pre.as<int>());
     VS_TRY(check_launch("k_order_levels"));
   } else {
     for (int l = nlev - 1; l >= 0; --l) {
       const int64_t b0 = level_base[l], b1 = level_base[l + 1];
       k_sizes<<<(unsigned)cdiv(b1 - b0, 128), 128, 0, st>>>(rec.as<NodeRec>(), b0, b1,
-                                                            sizes.as<int>());
+                                                            subc.as<int>(), sizes.as<int>());
       VS_TRY(check_launch("k_sizes"));
     }
     VS_CUDA(cudaMemsetAsync(pre.p, 0, sizeof(int), st), "pre root");
@@ -1770,9 +3210,48 @@ int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls,
       R->hi.as<int32_t>(), R->axis.as<int8_t>(), R->plane.as<int32_t>(), R->left.as<int32_t>(),
       R->right.as<int32_t>(), dbb);
   VS_TRY(check_launch("k_scatter_rows"));
+  if (nsub > 0) {
+    k_scatter_sub<<<(unsigned)nsub, 128, 0, st>>>(
+        rec.as<NodeRec>(), subl.as<int>(), SC, pre.as<int>(), R->lo.as<int32_t>(),
+        R->hi.as<int32_t>(), R->axis.as<int8_t>(), R->plane.as<int32_t>(), R->left.as<int32_t>(),
+        R->right.as<int32_t>(), dbb);
+    VS_TRY(check_launch("k_scatter_sub"));
+  }
   VS_TRY(d2h(&R->height, dbb, sizeof(int), st));
   R->root = 0;
   return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vs_kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, int binned,
+                int bins, int cs, void** handle, vs_stream_t stream) {
+  return vs_kd_build_bbox(bits, nx, ny, nz, nullptr, deep, mls, binned, bins, cs, handle, stream);
+}
+
+int vs_kd_build_bbox(const uint32_t* bits, int nx, int ny, int nz, const int* bbox, int deep,
+                     int mls, int binned, int bins, int cs, void** handle, vs_stream_t stream) {
+  if (!bits || !handle || nx < 1 || ny < 1 || nz < 1 || bins < 2 || cs < 1)
+    return fail_arg("vs_kd_build");
+  if (bins > 65) return fail_arg("vs_kd_build: bins > 65");
+  if (nz > 1024) return fail_arg("vs_kd_build: nz > 1024");
+  cudaStream_t st = S(stream);
+  auto* R = new KdResultImpl();
+  *handle = R;
+  for (DBuf* b : {&R->lo, &R->hi, &R->axis, &R->plane, &R->left, &R->right}) b->st = st;
+  // VSB200_KD_SUBTREES=0: every level through the level loop (A/B and tests)
+  const char* env = getenv("VSB200_KD_SUBTREES");
+  const int subtrees = !(env && env[0] == '0');
+  // VSB200_KD_DEVLEVELS=0: the big-node levels through the host loop instead of k_levels
+  const char* env2 = getenv("VSB200_KD_DEVLEVELS");
+  const int dev_levels = !(env2 && env2[0] == '0');
+  int rc = kd_build(bits, nx, ny, nz, deep, mls, binned, bins, cs, bbox, subtrees, dev_levels, R,
+                    st);
+  if (rc == KD_RETRY_LEVELS)
+    rc = kd_build(bits, nx, ny, nz, deep, mls, binned, bins, cs, bbox, 0, 0, R, st);
+  return rc;
 }
 
 int vs_kd_result_info(void* handle, int64_t* m, int* root, int* height) {

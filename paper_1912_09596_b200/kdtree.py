@@ -150,7 +150,10 @@ def build_kdtree(g, params: BuildParams | None = None) -> KdTree:
                          "store the longest axis first (x or y)")
     h = C.c_void_p()
     try:
-        call("vs_kd_build", ptr(b.packed()), nx, ny, nz, int(params.mode == "deep"),
+        packed = b.packed()
+        call("vs_kd_build_bbox", ptr(packed), nx, ny, nz,
+             ptr(b._bbox) if getattr(b, "_bbox", None) is not None else None,
+             int(params.mode == "deep"),
              -1 if params.max_leaf_size is None else int(params.max_leaf_size),
              int(params.builder == "binned"), int(params.bins), int(params.cell_size),
              C.byref(h), stream())

@@ -239,6 +239,7 @@ class BinaryVolume:
         self._source = _source
         self._summary = None
         self._count = None
+        self._bbox = None  # device int[6] tight box of the flags, when the pack produced it
         self._host = None
         if bits is not None:
             t = bits if isinstance(bits, torch.Tensor) else torch.from_numpy(
@@ -294,8 +295,13 @@ class BinaryVolume:
             base = torch.empty(nx * ny * _nzw(nz), dtype=torch.int32, device=dev)
             cnt = torch.zeros(1, dtype=torch.int64, device=dev)
             fused = dilate and nz % 32 == 0 and nz <= 1024 and v.bins.data_ptr() % 16 == 0
-            call("vs_classify_dilate_bits" if fused else "vs_classify_bits", ptr(v.bins), nx,
-                 ny, nz, ptr(tf.params()), ptr(base), ptr(cnt), stream())
+            if fused:  # the k-d root box comes out of the same pass
+                self._bbox = torch.empty(8, dtype=torch.int32, device=dev)
+                call("vs_classify_dilate_bits_bbox", ptr(v.bins), nx, ny, nz, ptr(tf.params()),
+                     ptr(base), ptr(cnt), ptr(self._bbox), stream())
+            else:
+                call("vs_classify_bits", ptr(v.bins), nx, ny, nz, ptr(tf.params()), ptr(base),
+                     ptr(cnt), stream())
             if self._count is None:
                 self._count = cnt
             if dilate and not fused:
