@@ -27,14 +27,16 @@ for t in ts:
             for _ in range(2):
                 render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd, flags=o)
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            K = 5
-            e0.record()
-            for _ in range(K):
-                render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd, flags=o)
-            e1.record()
-            torch.cuda.synchronize()
-            res[o] = (e0.elapsed_time(e1) / K, int(tgt.total.item()), tgt.rgba64.clone())
+            K, reps = 10, []
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(K):
+                    render_rows(v, tf, idx, cam, tgt, idx_desc=d, vol_desc=vd, cam_desc=cd, flags=o)
+                e1.record()
+                torch.cuda.synchronize()
+                reps.append(e0.elapsed_time(e1) / K)
+            res[o] = (sorted(reps)[2], int(tgt.total.item()), tgt.rgba64.clone())
         same = all(torch.equal(res[o][2], res[opts[0]][2]) for o in opts)
         s = res[opts[0]][1]
         print(f"t={t} {kind:6s} samples {s:11d}  " +
