@@ -122,7 +122,25 @@ int vs_morton_side(int nbx, int nby, int nbz);
  * cell16_opt != NULL: a 16-cell is exactly the OR of its 2x2x2 aligned 8-bricks. */
 int vs_summary_to_bitmap(const uint32_t* summary, int nx, int ny, int nz, int dilate, int P,
                          uint32_t* bitmap, uint32_t* tile_counts, uint8_t* cell16_opt,
-                         vs_stream_t stream);
+                         uint32_t* grid_opt, vs_stream_t stream);
+/* grid_opt: also the C-order leaf-brick bit grid ((nbx*nby*nbz+31)/32 words) the renderer's
+ * brick DDA reads (vs_index_desc.brick_bits), so no separate pass over the brick list. */
+
+/* ---- warm path: TF-independent per-volume brick presence (SURVEY.md §8d "cold / warm") ----
+ * presence (vs_presence_words u32): for every 8^3 brick, a 256-bit mask of the u8 bins that
+ * occur in the brick's 1-voxel halo (box-clipped).  flag_bricks(classify(v, tf, dilate=True),
+ * 8) (lbvh.py:83-102, volume.py:289-319) of any TF is then (presence & visible_bins) != 0 --
+ * exact, since the dilated vote of a brick is the OR of base visibility over its halo.  Needs
+ * nz % 16 == 0 and 16-byte aligned bins.  vs_presence_to_bitmap: nch channels (<= 4) voting
+ * as their union (multichannel semantics); presence_dev_ptrs = device array of the nch
+ * channels' presence pointers, tf_params = nch stacked device vs_tf_params blocks. */
+int64_t vs_presence_words(int nx, int ny, int nz);
+int vs_presence_build(const uint8_t* bins, int nx, int ny, int nz, uint32_t* presence,
+                      vs_stream_t stream);
+int vs_presence_to_bitmap(const uint32_t* const* presence_dev_ptrs, const int32_t* tf_params,
+                          int nch, int nx, int ny, int nz, int P, uint32_t* bitmap,
+                          uint32_t* tile_counts, uint8_t* cell16_opt, uint32_t* grid_opt,
+                          vs_stream_t stream);
 
 /* From C-order brick flag bytes (any brick size). */
 int vs_flags_to_bitmap(const uint8_t* flags, int nbx, int nby, int nbz, int P,
@@ -140,13 +158,21 @@ int vs_bricks_from_bitmap(const uint32_t* bitmap, int nbx, int nby, int nbz, int
  * rows n-1..2n-2 the leaves in Morton order; left/right = -1 on leaves; leaf_brick = -1 on
  * internal rows and 0..n-1 on leaves; brick_coords (n,3) Morton-sorted; root 0 (n>0).
  * Capacities: rows >= 2*cap-1, brick_coords >= cap, where cap >= number of bricks.
- * info (device int[2]) receives {n, height} (lbvh.py:128-144). */
+ * info (device int[2]) receives {n, height} (lbvh.py:128-144).
+ * Bitmap path: internal boxes are range reductions over the node's leaf run (no refit climb);
+ * info[1] is -1 when n >= 2 (height not computed: vs_lbvh_height fills it on demand, as the
+ * reference's Lbvh.height() is computed on call).  brick_grid_opt: the renderer's C-order
+ * leaf-brick bit grid ((nbx*nby*nbz+31)/32 words), written in the same launch sequence. */
 size_t vs_lbvh_workspace(int P, int64_t cap);
 int vs_lbvh_from_bitmap(const uint32_t* bitmap, const uint32_t* tile_counts, int P, int bs,
                         int nx, int ny, int nz, int64_t cap, int32_t* lo, int32_t* hi,
                         int32_t* left, int32_t* right, int32_t* leaf_brick,
-                        int32_t* brick_coords, int* info, void* ws, size_t ws_bytes,
-                        vs_stream_t stream);
+                        int32_t* brick_coords, uint32_t* brick_grid_opt, int* info, void* ws,
+                        size_t ws_bytes, vs_stream_t stream);
+/* Lbvh.height() (lbvh.py:128-144) of a built tree into info[1] (cap = brick capacity). */
+size_t vs_lbvh_height_workspace(int64_t cap);
+int vs_lbvh_height(const int32_t* left, const int32_t* right, int* info, int64_t cap, void* ws,
+                   size_t ws_bytes, vs_stream_t stream);
 
 /* Arbitrary BrickSet (codes may repeat): keys = code << 32 | index, stable radix sort, then
  * the same tree/refit.  n is known to the caller. */

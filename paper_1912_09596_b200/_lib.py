@@ -34,13 +34,18 @@ SIGNATURES: dict[str, tuple] = {
     "vs_count_bits": (i32, [P, i32, i32, i32, P, P]),
     "vs_vote_cells": (i32, [P, i32, i32, i32, i32, P, P]),
     "vs_morton_side": (i32, [i32, i32, i32]),
-    "vs_summary_to_bitmap": (i32, [P, i32, i32, i32, i32, i32, P, P, P, P]),
+    "vs_summary_to_bitmap": (i32, [P, i32, i32, i32, i32, i32, P, P, P, P, P]),
+    "vs_presence_words": (i64, [i32, i32, i32]),
+    "vs_presence_build": (i32, [P, i32, i32, i32, P, P]),
+    "vs_presence_to_bitmap": (i32, [P, P, i32, i32, i32, i32, i32, P, P, P, P, P]),
     "vs_flags_to_bitmap": (i32, [P, i32, i32, i32, i32, P, P, P]),
     "vs_bricks_workspace": (SZ, [i32, i32, i32]),
     "vs_bricks_from_bitmap": (i32, [P, i32, i32, i32, i32, P, P, P, P, SZ, P]),
     "vs_lbvh_workspace": (SZ, [i32, i64]),
     "vs_lbvh_from_bitmap": (i32, [P, P, i32, i32, i32, i32, i32, i64, P, P, P, P, P, P, P, P,
-                                  SZ, P]),
+                                  P, SZ, P]),
+    "vs_lbvh_height_workspace": (SZ, [i64]),
+    "vs_lbvh_height": (i32, [P, P, P, i64, P, SZ, P]),
     "vs_lbvh_bricks_workspace": (SZ, [i64]),
     "vs_svt_build": (i32, [P, i32, i32, i32, i32, P, P]),
     "vs_box_count": (i32, [P, i32, i32, i32, i32, P, i32, P, P]),

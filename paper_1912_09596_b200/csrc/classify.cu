@@ -705,6 +705,253 @@ __global__ void __launch_bounds__(512)
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Brick flags of one 512-code Morton tile (8^3 bricks) -> Morton bitmap words, tile count,
+// optional 16^3 cells and optional C-order leaf-brick bit grid.  Persistent CTAs; the next
+// tile's inputs are loaded into registers before the current tile is processed.
+//   FL_SUMMARY / FL_SUMMARY_DILATE: from the 27-bit summaries.  The dilated vote
+//     flag(b) = OR_e bit sbit(e) of S[b + e] is evaluated separably in shared memory:
+//     U = OR over ex (9 bits per brick), V = OR over ey (3 bits), flag = OR over ez.
+//   FL_PRESENCE: from the per-volume 256-bit halo presence masks (vs_presence_build):
+//     flag(b) = OR over channels of (presence_c[b] & vis_c) != 0 -- exact, because a brick's
+//     dilated vote is the OR of base visibility over its 1-voxel halo (volume.py:289-319,
+//     lbvh.py:93-96), and visibility depends on the bin alone.
+// ---------------------------------------------------------------------------------------
+enum { FL_SUMMARY = 0, FL_SUMMARY_DILATE = 1, FL_PRESENCE = 2 };
+constexpr int FL_T = 256;
+
+template <int MODE>
+__global__ void __launch_bounds__(FL_T)
+    k_flags_tiles(const uint32_t* __restrict__ src, const uint32_t* const* __restrict__ chans,
+                  const int32_t* __restrict__ tf_params,
+                  int nch, int nbx, int nby, int nbz, int64_t ntiles,
+                  uint32_t* __restrict__ bitmap, uint32_t* __restrict__ tile_counts,
+                  uint8_t* __restrict__ cell16, int ncx, int ncy, int ncz,
+                  uint32_t* __restrict__ grid) {
+  __shared__ uint32_t S[1000];
+  __shared__ uint32_t U[800];
+  __shared__ uint8_t V[640];
+  __shared__ uint8_t F[512];
+  __shared__ uint32_t s_vis[4][8];
+  __shared__ uint32_t s_wc[16];  // popcount of each of the tile's 16 bitmap words
+  const int t = threadIdx.x, lane = t & 31;
+  if (MODE == FL_PRESENCE && t < 32 && t < 8 * nch) s_vis[t >> 3][t & 7] = tf_params[16 * (t >> 3) + (t & 7)];
+  constexpr int NL = MODE == FL_SUMMARY_DILATE ? 4 : 2;  // halo words / bricks per thread
+  uint32_t reg[NL][MODE == FL_PRESENCE ? 8 : 1];
+  auto tile_origin = [](int64_t tile, int& tx, int& ty, int& tz) {
+    tx = (int)compact10((uint32_t)tile) * 8;
+    ty = (int)compact10((uint32_t)tile >> 1) * 8;
+    tz = (int)compact10((uint32_t)tile >> 2) * 8;
+  };
+  auto load = [&](int64_t tile) {
+    int tx, ty, tz;
+    tile_origin(tile, tx, ty, tz);
+    if (tx >= nbx || ty >= nby || tz >= nbz) return;
+#pragma unroll
+    for (int q = 0; q < NL; ++q) {
+      if (MODE == FL_SUMMARY_DILATE) {
+        const int k = t + q * FL_T;
+        uint32_t v = 0;
+        if (k < 1000) {
+          const int gx = tx + k / 100 - 1, gy = ty + (k / 10) % 10 - 1, gz = tz + k % 10 - 1;
+          if (gx >= 0 && gx < nbx && gy >= 0 && gy < nby && gz >= 0 && gz < nbz)
+            v = __ldg(src + ((int64_t)gx * nby + gy) * nbz + gz);
+        }
+        reg[q][0] = v;
+      } else {
+        const uint32_t m = (uint32_t)(t + q * FL_T);
+        const int bx = tx + (int)compact10(m), by = ty + (int)compact10(m >> 1),
+                  bz = tz + (int)compact10(m >> 2);
+        const bool in = bx < nbx && by < nby && bz < nbz;
+        const int64_t lin = ((int64_t)bx * nby + by) * nbz + bz;
+        if (MODE == FL_SUMMARY) {
+          reg[q][0] = in ? __ldg(src + lin) : 0u;
+        } else {
+          uint32_t f = 0;  // channels > 1: folded to the flag here (masks in shared memory)
+          for (int c = 0; c < nch; ++c) {
+            uint4 a = make_uint4(0, 0, 0, 0), b = a;
+            if (in) {
+              const uint4* pp = reinterpret_cast<const uint4*>(chans[c] + lin * 8);
+              a = __ldg(pp);
+              b = __ldg(pp + 1);
+            }
+            if (nch == 1) {
+              reg[q][0] = a.x; reg[q][1] = a.y; reg[q][2] = a.z; reg[q][3] = a.w;
+              reg[q][4] = b.x; reg[q][5] = b.y; reg[q][6] = b.z; reg[q][7] = b.w;
+            } else {
+              f |= (a.x & s_vis[c][0]) | (a.y & s_vis[c][1]) | (a.z & s_vis[c][2]) |
+                   (a.w & s_vis[c][3]) | (b.x & s_vis[c][4]) | (b.y & s_vis[c][5]) |
+                   (b.z & s_vis[c][6]) | (b.w & s_vis[c][7]);
+            }
+          }
+          if (nch > 1) reg[q][0] = f ? 1u : 0u;
+        }
+      }
+    }
+  };
+  __syncthreads();
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) load(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();  // the previous tile's shared-memory readers are done
+    int tx, ty, tz;
+    tile_origin(tile, tx, ty, tz);
+    const bool inside = tx < nbx && ty < nby && tz < nbz;  // CTA-uniform
+    uint32_t flag[2] = {0u, 0u};
+    if (inside) {
+      if (MODE == FL_SUMMARY_DILATE) {
+#pragma unroll
+        for (int q = 0; q < NL; ++q)
+          if (t + q * FL_T < 1000) S[t + q * FL_T] = reg[q][0];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (MODE == FL_SUMMARY) {
+            flag[q] = (reg[q][0] >> 13) & 1u;  // sbit(0,0,0): the brick itself
+          } else if (nch > 1) {
+            flag[q] = reg[q][0];
+          } else {
+            uint32_t any = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) any |= reg[q][w] & s_vis[0][w];
+            flag[q] = any != 0u;
+          }
+        }
+      }
+    }
+    const int64_t next = tile + gridDim.x;
+    if (next < ntiles) load(next);  // in flight while this tile is processed
+    if (!inside) {
+      if (t < 16) bitmap[tile * 16 + t] = 0;
+      if (t == 0) tile_counts[tile] = 0;
+      continue;
+    }
+    if (MODE == FL_SUMMARY_DILATE) {
+      __syncthreads();  // S stored
+      for (int k = t; k < 800; k += FL_T) {  // U[x][y][z], x in 0..7, y, z in halo 0..9
+        const int x = k / 100, yz = k - x * 100;
+        U[k] = (S[x * 100 + yz] | (S[(x + 1) * 100 + yz] >> 9) | (S[(x + 2) * 100 + yz] >> 18)) &
+               0x1FFu;
+      }
+      __syncthreads();
+      for (int k = t; k < 640; k += FL_T) {  // V[x][y][z], y in 0..7, z in halo 0..9
+        const int x = k / 80, r = k - x * 80, y = r / 10, z = r - y * 10;
+        const int u = x * 100 + y * 10 + z;
+        V[k] = (uint8_t)((U[u] | (U[u + 10] >> 3) | (U[u + 20] >> 6)) & 7u);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t m = (uint32_t)(t + q * FL_T);
+        const int lx = (int)compact10(m), ly = (int)compact10(m >> 1), lz = (int)compact10(m >> 2);
+        const int v = lx * 80 + ly * 10 + lz;
+        flag[q] = ((V[v] & 1u) | ((V[v + 1] >> 1) & 1u) | ((V[v + 2] >> 2) & 1u));
+      }
+    }
+    // bricks outside the grid (partial tiles) never vote
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t m = (uint32_t)(t + q * FL_T);
+      const int lx = (int)compact10(m), ly = (int)compact10(m >> 1), lz = (int)compact10(m >> 2);
+      const bool in = tx + lx < nbx && ty + ly < nby && tz + lz < nbz;
+      flag[q] = in ? flag[q] : 0u;
+      const uint32_t ball = __ballot_sync(0xffffffffu, flag[q] != 0u);
+      const int wd = (int)(m >> 5);
+      if (lane == 0) {
+        bitmap[tile * 16 + wd] = ball;
+        s_wc[wd] = (uint32_t)__popc(ball);
+      }
+      if (cell16 && (lane & 7) == 0) {
+        const int cx = (tx + lx) >> 1, cy = (ty + ly) >> 1, cz = (tz + lz) >> 1;
+        if (cx < ncx && cy < ncy && cz < ncz)
+          cell16[((int64_t)cx * ncy + cy) * ncz + cz] = ((ball >> lane) & 0xffu) ? 1 : 0;
+      }
+      if (grid) F[(lx * 8 + ly) * 8 + lz] = (uint8_t)(flag[q] != 0u);
+    }
+    __syncthreads();
+    if (t == 0) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) c += s_wc[k];
+      tile_counts[tile] = c;
+    }
+    if (grid && t < 64) {  // C-order leaf-brick bits: one byte per (x, y) row of 8 z-bricks
+      const int lx = t >> 3, ly = t & 7, bx = tx + lx, by = ty + ly;
+      if (bx < nbx && by < nby) {
+        uint32_t byte = 0;
+#pragma unroll
+        for (int z = 0; z < 8; ++z) byte |= (uint32_t)F[t * 8 + z] << z;
+        const int64_t lin = ((int64_t)bx * nby + by) * nbz + tz;
+        if ((nbz & 7) == 0) {
+          reinterpret_cast<uint8_t*>(grid)[lin >> 3] = (uint8_t)byte;
+        } else {
+          for (int z = 0; z < 8; ++z)
+            if ((byte >> z) & 1u) atomicOr(grid + ((lin + z) >> 5), 1u << ((lin + z) & 31));
+        }
+      }
+    }
+  }
+}
+
+// Per-volume 256-bit presence mask of every 8^3 brick's 1-voxel halo (the TF-independent warm
+// path of the brick vote: a TF change then reads 32 B per brick instead of the volume).  CTA
+// per (bx, by) brick column; each thread takes 16-byte z chunks of the column's 10 x 10 halo
+// rows; a byte sets its bit in the mask of its brick and, at a brick face, of the z neighbour
+// whose halo it is.  Bits are tested before the shared atomic, so repeated values are cheap.
+constexpr int PR_T = 256;
+__global__ void __launch_bounds__(PR_T)
+    k_presence(const uint8_t* __restrict__ vol, int nx, int ny, int nz, int nby, int nbz,
+               uint32_t* __restrict__ presence) {
+  extern __shared__ uint32_t pm[];  // nbz * 8 words
+  const int bx = blockIdx.x / nby, by = blockIdx.x - (blockIdx.x / nby) * nby;
+  for (int k = threadIdx.x; k < nbz * 8; k += PR_T) pm[k] = 0;
+  __syncthreads();
+  const int x0 = max(bx * 8 - 1, 0), x1 = min(bx * 8 + 9, nx);
+  const int y0 = max(by * 8 - 1, 0), y1 = min(by * 8 + 9, ny);
+  const int nyr = y1 - y0, nchunk = nz >> 4;
+  const int total = (x1 - x0) * nyr * nchunk;
+  auto set = [&](int brick, uint32_t v) {
+    uint32_t* w = pm + brick * 8 + (v >> 5);
+    const uint32_t bit = 1u << (v & 31);
+    if (!(*w & bit)) atomicOr(w, bit);
+  };
+  // k = r * nchunk + c walks the column's rows x chunks; (x, y, c) advance incrementally
+  const int step_r = PR_T / nchunk, step_c = PR_T % nchunk;
+  int c = threadIdx.x % nchunk, r = threadIdx.x / nchunk;
+  int x = x0 + r / nyr, y = y0 + r % nyr;
+  for (int k = threadIdx.x; k < total; k += PR_T) {
+    const uint4 q = __ldcs(reinterpret_cast<const uint4*>(vol + ((int64_t)x * ny + y) * nz) + c);
+    const int b0 = 2 * c;  // bricks b0 (bytes 0-7) and b0 + 1 (bytes 8-15)
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    if ((q.x | q.y) == 0u) {
+      set(b0, 0u);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) set(b0, (w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+    }
+    if ((q.z | q.w) == 0u) {
+      set(b0 + 1, 0u);
+    } else {
+#pragma unroll
+      for (int j = 8; j < 16; ++j) set(b0 + 1, (w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+    }
+    // z halo: byte 0 belongs to brick b0 - 1's halo, byte 7 to b0 + 1's, byte 8 to b0's,
+    // byte 15 to b0 + 2's
+    if (b0 > 0) set(b0 - 1, q.x & 0xffu);
+    set(b0 + 1, q.y >> 24);
+    set(b0, q.z & 0xffu);
+    if (b0 + 2 < nbz) set(b0 + 2, q.w >> 24);
+    c += step_c;
+    int dr = step_r;
+    if (c >= nchunk) { c -= nchunk; ++dr; }
+    y += dr;
+    while (y >= y1) { y -= nyr; ++x; }
+  }
+  __syncthreads();
+  uint32_t* out = presence + (((int64_t)bx * nby + by) * nbz) * 8;
+  for (int k = threadIdx.x; k < nbz * 8; k += PR_T) out[k] = pm[k];
+}
+
 __global__ void k_flags_scatter(const uint8_t* __restrict__ flags, int nbx, int nby, int nbz,
                                 uint32_t* __restrict__ bitmap) {
   const int64_t n = (int64_t)nbx * nby * nbz;
@@ -921,19 +1168,74 @@ int vs_morton_side(int nbx, int nby, int nbz) {
   return p;
 }
 
-int vs_summary_to_bitmap(const uint32_t* summary, int nx, int ny, int nz, int dilate, int P,
-                         uint32_t* bitmap, uint32_t* tile_counts, uint8_t* cell16,
-                         vs_stream_t st) {
-  if (!summary || !bitmap || !tile_counts || nx < 1 || ny < 1 || nz < 1)
-    return fail_arg("vs_summary_to_bitmap");
+static int flags_tiles(int mode, const uint32_t* src, const uint32_t* const* chans,
+                       const int32_t* tf_params, int nch,
+                       int nx, int ny, int nz, int P, uint32_t* bitmap, uint32_t* tile_counts,
+                       uint8_t* cell16, uint32_t* grid, cudaStream_t st) {
   const int nbx = (int)cdiv(nx, 8), nby = (int)cdiv(ny, 8), nbz = (int)cdiv(nz, 8);
-  if (P != vs_morton_side(nbx, nby, nbz)) return fail_arg("vs_summary_to_bitmap: P");
+  if (P != vs_morton_side(nbx, nby, nbz)) return fail_arg("flags to bitmap: P");
   const int64_t ntiles = (int64_t)P * P * P / 512;
   const int ncx = (int)cdiv(nx, 16), ncy = (int)cdiv(ny, 16), ncz = (int)cdiv(nz, 16);
-  k_summary_to_bitmap<<<(unsigned)ntiles, 512, 0, S(st)>>>(summary, nbx, nby, nbz, dilate,
-                                                           bitmap, tile_counts, cell16, ncx,
-                                                           ncy, ncz);
-  return check_launch("k_summary_to_bitmap");
+  const int64_t nb = (int64_t)nbx * nby * nbz;
+  if (grid && (nbz & 7) != 0)  // bits set by atomics
+    VS_CUDA(cudaMemsetAsync(grid, 0, ((nb + 31) / 32) * 4, st), "memset brick grid");
+  else if (grid && (nb & 31) != 0)  // padding bits of the last word (never stored by bytes)
+    VS_CUDA(cudaMemsetAsync(grid + nb / 32, 0, 4, st), "memset brick grid tail");
+  const unsigned g = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * 8);
+  if (mode == FL_SUMMARY_DILATE)
+    k_flags_tiles<FL_SUMMARY_DILATE><<<g, FL_T, 0, st>>>(src, chans, tf_params, nch, nbx, nby, nbz,
+                                                        ntiles, bitmap, tile_counts, cell16, ncx,
+                                                        ncy, ncz, grid);
+  else if (mode == FL_SUMMARY)
+    k_flags_tiles<FL_SUMMARY><<<g, FL_T, 0, st>>>(src, chans, tf_params, nch, nbx, nby, nbz, ntiles,
+                                                 bitmap, tile_counts, cell16, ncx, ncy, ncz,
+                                                 grid);
+  else
+    k_flags_tiles<FL_PRESENCE><<<g, FL_T, 0, st>>>(src, chans, tf_params, nch, nbx, nby, nbz, ntiles,
+                                                  bitmap, tile_counts, cell16, ncx, ncy, ncz,
+                                                  grid);
+  return check_launch("k_flags_tiles");
+}
+
+int vs_summary_to_bitmap(const uint32_t* summary, int nx, int ny, int nz, int dilate, int P,
+                         uint32_t* bitmap, uint32_t* tile_counts, uint8_t* cell16,
+                         uint32_t* grid, vs_stream_t st) {
+  if (!summary || !bitmap || !tile_counts || nx < 1 || ny < 1 || nz < 1)
+    return fail_arg("vs_summary_to_bitmap");
+  return flags_tiles(dilate ? FL_SUMMARY_DILATE : FL_SUMMARY, summary, nullptr, nullptr, 1, nx,
+                     ny, nz, P,
+                     bitmap, tile_counts, cell16, grid, S(st));
+}
+
+int64_t vs_presence_words(int nx, int ny, int nz) {
+  if (nx < 1 || ny < 1 || nz < 1) return -1;
+  return cdiv(nx, 8) * cdiv(ny, 8) * cdiv(nz, 8) * 8;
+}
+
+int vs_presence_build(const uint8_t* bins, int nx, int ny, int nz, uint32_t* presence,
+                      vs_stream_t st) {
+  if (!bins || !presence || nx < 1 || ny < 1 || nz < 1 || nz % 16 != 0 ||
+      ((uintptr_t)bins & 15) != 0)
+    return fail_arg("vs_presence_build (needs nz % 16 == 0, 16-byte aligned bins)");
+  const int nbx = (int)cdiv(nx, 8), nby = (int)cdiv(ny, 8), nbz = (int)cdiv(nz, 8);
+  const size_t smem = (size_t)nbz * 8 * 4;
+  if (smem > 48 * 1024)
+    VS_CUDA(cudaFuncSetAttribute(k_presence, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem), "presence smem");
+  k_presence<<<(unsigned)((int64_t)nbx * nby), PR_T, smem, S(st)>>>(bins, nx, ny, nz, nby, nbz,
+                                                                     presence);
+  return check_launch("k_presence");
+}
+
+int vs_presence_to_bitmap(const uint32_t* const* presence, const int32_t* tf_params, int nch,
+                          int nx, int ny, int nz, int P, uint32_t* bitmap,
+                          uint32_t* tile_counts, uint8_t* cell16, uint32_t* grid,
+                          vs_stream_t st) {
+  if (!presence || !tf_params || !bitmap || !tile_counts || nch < 1 || nch > 4 || nx < 1 ||
+      ny < 1 || nz < 1)
+    return fail_arg("vs_presence_to_bitmap");
+  return flags_tiles(FL_PRESENCE, nullptr, presence, tf_params, nch, nx, ny, nz, P, bitmap,
+                     tile_counts, cell16, grid, S(st));
 }
 
 int vs_flags_to_bitmap(const uint8_t* flags, int nbx, int nby, int nbz, int P, uint32_t* bitmap,

@@ -49,6 +49,15 @@ inline cudaStream_t S(vs_stream_t s) { return reinterpret_cast<cudaStream_t>(s);
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// SM count of the current device (a cheap attribute query; no cached global state).
+inline int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+    n = 148;
+  return n;
+}
+
 // Bump allocator over a caller-provided device workspace (CUB two-phase style: a null base
 // only measures).
 struct Bump {

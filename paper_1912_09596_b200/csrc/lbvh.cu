@@ -289,6 +289,333 @@ __global__ void __launch_bounds__(RC)
   }
 }
 
+// ---- bitmap path: sort-free leaves, Karras emission and range-reduction boxes ---------------
+// The leaves of the bitmap path are the set bits in code order, so every internal node's box is
+// the union of a CONTIGUOUS run of leaf boxes -- its Karras range [a, b] (lbvh.py:167-200; the
+// refit of lbvh.py:203-213 unions exactly the leaves of the subtree).  Boxes are therefore
+// computed as range reductions instead of a bottom-up climb: a CTA owns TC consecutive leaves
+// and the TC internal nodes with the same indices (node i always has i as one end of its range);
+// a node whose range lies inside the chunk reduces from shared-memory warp prefix / suffix boxes
+// and block totals, and the few nodes whose range crosses a chunk boundary are finished by a
+// second kernel from per-leaf chunk prefix / suffix boxes and the chunk totals.  Brick
+// coordinates are < 1024, so a box is kept as packed 16-bit (x | y << 16, z) minima / maxima.
+constexpr int TC = 512;
+
+__device__ __forceinline__ uint4 box_empty() { return make_uint4(~0u, ~0u, 0u, 0u); }
+__device__ __forceinline__ uint4 box_union(uint4 a, uint4 b) {
+  return make_uint4(__vminu2(a.x, b.x), min(a.y, b.y), __vmaxu2(a.z, b.z), max(a.w, b.w));
+}
+__device__ __forceinline__ uint4 shfl_box(uint4 v, int d, bool up) {
+  uint4 r;
+  if (up) {
+    r.x = __shfl_up_sync(0xffffffffu, v.x, d); r.y = __shfl_up_sync(0xffffffffu, v.y, d);
+    r.z = __shfl_up_sync(0xffffffffu, v.z, d); r.w = __shfl_up_sync(0xffffffffu, v.w, d);
+  } else {
+    r.x = __shfl_down_sync(0xffffffffu, v.x, d); r.y = __shfl_down_sync(0xffffffffu, v.y, d);
+    r.z = __shfl_down_sync(0xffffffffu, v.z, d); r.w = __shfl_down_sync(0xffffffffu, v.w, d);
+  }
+  return r;
+}
+// voxel box of a brick-coordinate box: lo = c*bs, hi = min(c*bs + bs, dims) (lbvh.py:231-232;
+// the union of clipped leaf boxes is the clipped box of the extreme bricks)
+__device__ __forceinline__ void store_box(uint4 b, int bs, int nx, int ny, int nz, int64_t row,
+                                          int32_t* __restrict__ lo, int32_t* __restrict__ hi) {
+  lo[3 * row] = (int)(b.x & 0xffffu) * bs;
+  lo[3 * row + 1] = (int)(b.x >> 16) * bs;
+  lo[3 * row + 2] = (int)b.y * bs;
+  hi[3 * row] = min((int)(b.z & 0xffffu) * bs + bs, nx);
+  hi[3 * row + 1] = min((int)(b.z >> 16) * bs + bs, ny);
+  hi[3 * row + 2] = min((int)b.w * bs + bs, nz);
+}
+
+// Exclusive scan of the tile popcounts in one CTA (off[ntiles] = n), for ntiles <= 1024 * 32:
+// all loads issued up front (coalesced, strided by the CTA width), then one block scan per
+// 1024-entry round with a running carry.
+constexpr int SCAN_T = 1024, SCAN_PER = 32;
+__global__ void __launch_bounds__(SCAN_T)
+    k_tile_scan(const uint32_t* __restrict__ cnt, int64_t ntiles, uint32_t* __restrict__ off) {
+  __shared__ uint32_t ws[2][32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int rounds = (int)((ntiles + SCAN_T - 1) / SCAN_T);
+  uint32_t v[SCAN_PER];
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    const int64_t i = (int64_t)k * SCAN_T + t;
+    v[k] = (k < rounds && i < ntiles) ? __ldg(cnt + i) : 0u;
+  }
+  uint32_t carry = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    if (k < rounds) {  // uniform
+      uint32_t incl = v[k];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (lane == 31) ws[k & 1][warp] = incl;
+      __syncthreads();
+      uint32_t w = ws[k & 1][lane], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += u;
+      }
+      const uint32_t before = __shfl_sync(0xffffffffu, wi - w, warp);
+      const uint32_t total = __shfl_sync(0xffffffffu, wi, 31);
+      const int64_t i = (int64_t)k * SCAN_T + t;
+      if (i < ntiles) off[i] = carry + before + incl - v[k];
+      carry += total;
+    }
+  }
+  if (t == 0) off[ntiles] = carry;
+}
+
+// Leaves: warp per two 512-code tiles (lane = bitmap word); the warp's leaves are one
+// contiguous run of ranks, staged in shared memory and written row-coalesced.  Also the
+// renderer's C-order leaf-brick bit grid (optional, pre-zeroed) and info {n, height sentinel}.
+constexpr int LV_WARPS = 8;
+__global__ void __launch_bounds__(LV_WARPS * 32)
+    k_leaves_coop(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ off, int bs,
+                  int nx, int ny, int nz, int nby, int nbz, int64_t ntiles,
+                  uint32_t* __restrict__ codes, int32_t* __restrict__ lo,
+                  int32_t* __restrict__ hi, int32_t* __restrict__ left,
+                  int32_t* __restrict__ right, int32_t* __restrict__ leaf_brick,
+                  int32_t* __restrict__ brick_coords, uint32_t* __restrict__ grid,
+                  int* __restrict__ info, int* __restrict__ cross_count) {
+  __shared__ uint32_t stage[LV_WARPS][1024];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = off[ntiles];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    info[0] = (int)n;
+    info[1] = n == 0 ? 0 : (n == 1 ? 1 : -1);  // -1: height computed on demand
+    *cross_count = 0;
+  }
+  const int64_t pair = (int64_t)blockIdx.x * LV_WARPS + warp;
+  const int64_t t0 = 2 * pair;
+  if (t0 >= ntiles) return;
+  const int64_t wi = t0 * 16 + lane;
+  const bool valid = t0 + (lane >> 4) < ntiles;
+  uint32_t word = valid ? __ldg(bitmap + wi) : 0u;
+  const uint32_t c = __popc(word);
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o, 16);
+    if ((lane & 15) >= o) incl += u;
+  }
+  const int64_t P0 = off[t0];
+  const int64_t P1 = off[(t0 + 2 < ntiles) ? t0 + 2 : ntiles];
+  int pos = (int)((int64_t)off[t0 + (lane >> 4)] - P0) + (int)(incl - c);
+  while (word) {
+    const int bit = __ffs(word) - 1;
+    word &= word - 1;
+    stage[warp][pos++] = (uint32_t)(wi * 32 + bit);
+  }
+  __syncwarp();
+  const int cnt = (int)(P1 - P0);
+  for (int k = lane; k < cnt; k += 32) {
+    const uint32_t code = stage[warp][k];
+    const int64_t p = P0 + k;
+    const int bx = (int)compact10(code), by = (int)compact10(code >> 1),
+              bz = (int)compact10(code >> 2);
+    codes[p] = code;
+    brick_coords[3 * p] = bx;
+    brick_coords[3 * p + 1] = by;
+    brick_coords[3 * p + 2] = bz;
+    const int64_t row = n - 1 + p;
+    lo[3 * row] = bx * bs;
+    lo[3 * row + 1] = by * bs;
+    lo[3 * row + 2] = bz * bs;
+    hi[3 * row] = min(bx * bs + bs, nx);
+    hi[3 * row + 1] = min(by * bs + bs, ny);
+    hi[3 * row + 2] = min(bz * bs + bs, nz);
+    left[row] = -1;
+    right[row] = -1;
+    leaf_brick[row] = (int32_t)p;
+    if (grid) {
+      const int64_t lin = ((int64_t)bx * nby + by) * nbz + bz;
+      atomicOr(grid + (lin >> 5), 1u << (lin & 31));
+    }
+  }
+}
+
+__device__ __forceinline__ int dlt32(const uint32_t* __restrict__ c, uint32_t ci, int64_t j,
+                                     int64_t n) {
+  if (j < 0 || j >= n) return -1;
+  return __clz(ci ^ __ldg(c + j));  // codes are distinct: never 64 (lbvh.py:153-164)
+}
+
+// Karras emission (lbvh.py:167-200) for the chunk's internal nodes + in-chunk range boxes.
+__global__ void __launch_bounds__(TC)
+    k_tree_chunk(const uint32_t* __restrict__ codes, const int* __restrict__ info, int bs,
+                 int nx, int ny, int nz, const int32_t* __restrict__ brick_coords,
+                 int32_t* __restrict__ lo, int32_t* __restrict__ hi, int32_t* __restrict__ left,
+                 int32_t* __restrict__ right, int32_t* __restrict__ leaf_brick,
+                 uint4* __restrict__ cpre, uint4* __restrict__ csuf, uint4* __restrict__ ctot,
+                 int4* __restrict__ cross, int* __restrict__ cross_count) {
+  __shared__ uint4 s_leaf[TC], s_pre[TC], s_suf[TC];
+  __shared__ uint4 s_tot[TC / 32], s_bp[TC / 32], s_bs[TC / 32];
+  const int64_t n = info[0];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  constexpr int NW = TC / 32;
+  const int64_t nchunks = (n + TC - 1) / TC;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t c0 = ch * TC, c1 = (c0 + TC < n) ? c0 + TC : n;
+    const int64_t p = c0 + t;
+    uint4 b = box_empty();
+    if (p < c1) {
+      const uint32_t x = (uint32_t)brick_coords[3 * p], y = (uint32_t)brick_coords[3 * p + 1],
+                     z = (uint32_t)brick_coords[3 * p + 2];
+      b = make_uint4(x | (y << 16), z, x | (y << 16), z);
+    }
+    uint4 pre = b, suf = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint4 u = shfl_box(pre, o, true);
+      if (lane >= o) pre = box_union(pre, u);
+      const uint4 d = shfl_box(suf, o, false);
+      if (lane + o < 32) suf = box_union(suf, d);
+    }
+    s_leaf[t] = b;
+    s_pre[t] = pre;
+    s_suf[t] = suf;
+    if (lane == 31) s_tot[warp] = pre;
+    __syncthreads();
+    if (warp == 0) {  // exclusive block prefix / suffix unions over the NW warp totals
+      const uint4 tv = lane < NW ? s_tot[lane] : box_empty();
+      uint4 bp = tv, bq = tv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint4 u = shfl_box(bp, o, true);
+        if (lane >= o) bp = box_union(bp, u);
+        const uint4 d = shfl_box(bq, o, false);
+        if (lane + o < 32) bq = box_union(bq, d);
+      }
+      uint4 ex = shfl_box(bp, 1, true), ey = shfl_box(bq, 1, false);
+      if (lane == 0) ex = box_empty();
+      if (lane == 31) ey = box_empty();
+      if (lane < NW) { s_bp[lane] = ex; s_bs[lane] = ey; }
+      if (lane == NW - 1) ctot[ch] = bp;  // the chunk's total
+    }
+    __syncthreads();
+    if (p < c1) {  // chunk-level prefix / suffix boxes of leaf p (for crossing ranges)
+      cpre[p] = box_union(s_bp[warp], pre);
+      csuf[p] = box_union(suf, s_bs[warp]);
+    }
+    // internal node i = p (lbvh.py:172-200)
+    if (p < n - 1) {
+      const int64_t i = p;
+      const uint32_t ci = __ldg(codes + i);
+      const int d = dlt32(codes, ci, i + 1, n) > dlt32(codes, ci, i - 1, n) ? 1 : -1;
+      const int dmin = dlt32(codes, ci, i - d, n);
+      int64_t lmax = 2;
+      while (dlt32(codes, ci, i + lmax * d, n) > dmin) lmax *= 2;
+      int64_t l = 0;
+      for (int64_t s = lmax / 2; s >= 1; s /= 2)
+        if (dlt32(codes, ci, i + (l + s) * d, n) > dmin) l += s;
+      const int64_t j = i + l * d;
+      const int dnode = dlt32(codes, ci, j, n);
+      int64_t s = 0, st = l;
+      while (true) {
+        st = (st + 1) / 2;
+        if (dlt32(codes, ci, i + (s + st) * d, n) > dnode) s += st;
+        if (st == 1) break;
+      }
+      const int64_t gamma = i + s * d + min(d, 0);
+      const int64_t a = min(i, j), e = max(i, j);
+      left[i] = (int32_t)(a == gamma ? (n - 1) + gamma : gamma);
+      right[i] = (int32_t)(e == gamma + 1 ? (n - 1) + gamma + 1 : gamma + 1);
+      leaf_brick[i] = -1;
+      if (a >= c0 && e < c1) {
+        const int la = (int)(a - c0), le = (int)(e - c0);
+        const int wa = la >> 5, we = le >> 5;
+        uint4 acc;
+        if (wa == we) {
+          acc = s_leaf[la];
+          for (int k = la + 1; k <= le; ++k) acc = box_union(acc, s_leaf[k]);
+        } else {
+          acc = box_union(s_suf[la], s_pre[le]);
+          for (int w = wa + 1; w < we; ++w) acc = box_union(acc, s_tot[w]);
+        }
+        store_box(acc, bs, nx, ny, nz, i, lo, hi);
+      } else {
+        const unsigned m = __activemask();
+        const int leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(cross_count, __popc(m));
+        base = __shfl_sync(m, base, leader);
+        cross[base + __popc(m & ((1u << lane) - 1u))] = make_int4((int)i, (int)a, (int)e, 0);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Internal nodes whose range crosses a chunk boundary: warp per node, box = chunk suffix of a
+// U totals of the chunks in between U chunk prefix of e.
+__global__ void __launch_bounds__(256)
+    k_tree_cross(const int4* __restrict__ cross, const int* __restrict__ cross_count, int bs,
+                 int nx, int ny, int nz, const uint4* __restrict__ cpre,
+                 const uint4* __restrict__ csuf, const uint4* __restrict__ ctot,
+                 int32_t* __restrict__ lo, int32_t* __restrict__ hi) {
+  const int cnt = *cross_count;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < cnt;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int4 c = cross[w];
+    const int64_t ca = c.y / TC, ce = c.z / TC;
+    uint4 acc = lane == 0 ? box_union(csuf[c.y], cpre[c.z]) : box_empty();
+    for (int64_t k = ca + 1 + lane; k < ce; k += 32) acc = box_union(acc, ctot[k]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      uint4 u;
+      u.x = __shfl_xor_sync(0xffffffffu, acc.x, o); u.y = __shfl_xor_sync(0xffffffffu, acc.y, o);
+      u.z = __shfl_xor_sync(0xffffffffu, acc.z, o); u.w = __shfl_xor_sync(0xffffffffu, acc.w, o);
+      acc = box_union(acc, u);
+    }
+    if (lane == 0) store_box(acc, bs, nx, ny, nz, c.x, lo, hi);
+  }
+}
+
+// height() (lbvh.py:128-144) on demand: parents from the child arrays, then a per-leaf climb
+// with arrival counters (the second arrival at a node knows both subtree heights).
+__global__ void k_parents(const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+                          const int* __restrict__ info, int32_t* __restrict__ parent,
+                          int32_t* __restrict__ visit) {
+  const int64_t n = info[0];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  parent[left[i]] = (int32_t)i;
+  parent[right[i]] = (int32_t)i;
+  visit[i] = 0;
+}
+
+__global__ void k_height_climb(const int32_t* __restrict__ left,
+                               const int32_t* __restrict__ right,
+                               const int32_t* __restrict__ parent, int32_t* __restrict__ visit,
+                               int32_t* __restrict__ hgt, int* __restrict__ info) {
+  const int64_t n = info[0];
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n < 2 || p >= n) return;
+  int64_t node = parent[n - 1 + p];
+  while (true) {
+    __threadfence();
+    if (atomicAdd(&visit[node], 1) == 0) return;
+    __threadfence();
+    const int32_t l = __ldcg(left + node), r = __ldcg(right + node);
+    const int hl = (l >= n - 1) ? 1 : __ldcg(hgt + l);
+    const int hr = (r >= n - 1) ? 1 : __ldcg(hgt + r);
+    const int h = 1 + max(hl, hr);
+    __stcg(hgt + node, h);
+    if (node == 0) {
+      info[1] = h;
+      return;
+    }
+    node = __ldcg(parent + node);
+  }
+}
+
 struct TreeWs {
   uint64_t* keys;
   int32_t* parent;
@@ -326,40 +653,98 @@ using namespace vs;
 
 extern "C" {
 
-size_t vs_lbvh_workspace(int P, int64_t cap) {
+static size_t bitmap_ws(int P, int64_t cap, uint32_t** off, uint32_t** codes, uint4** cpre,
+                        uint4** csuf, uint4** ctot, int4** cross, int** ccount, void* base) {
   const int64_t ntiles = (int64_t)P * P * P / 512;
-  Bump b(nullptr);
-  b.take<uint32_t>(ntiles + 1);
-  b.take<char>(scan_temp_bytes(ntiles + 1));
-  take_tree(b, cap);
+  Bump b(base);
+  uint32_t* o = b.take<uint32_t>(ntiles + 1);
+  const bool big = ntiles > (int64_t)SCAN_T * SCAN_PER;
+  if (big) b.take<char>(scan_temp_bytes(ntiles + 1));
+  uint32_t* c = b.take<uint32_t>(std::max<int64_t>(cap, 1));
+  uint4* pr = b.take<uint4>(std::max<int64_t>(cap, 1));
+  uint4* sf = b.take<uint4>(std::max<int64_t>(cap, 1));
+  uint4* tt = b.take<uint4>(cdiv(std::max<int64_t>(cap, 1), TC));
+  int4* cr = b.take<int4>(std::max<int64_t>(cap, 1));
+  int* cc = b.take<int>(1);
+  if (off) { *off = o; *codes = c; *cpre = pr; *csuf = sf; *ctot = tt; *cross = cr; *ccount = cc; }
   return b.off + 256;
+}
+
+size_t vs_lbvh_workspace(int P, int64_t cap) {
+  return bitmap_ws(P, cap, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                   nullptr);
 }
 
 int vs_lbvh_from_bitmap(const uint32_t* bitmap, const uint32_t* tile_counts, int P, int bs,
                         int nx, int ny, int nz, int64_t cap, int32_t* lo, int32_t* hi,
                         int32_t* left, int32_t* right, int32_t* leaf_brick,
-                        int32_t* brick_coords, int* info, void* ws, size_t ws_bytes,
-                        vs_stream_t stream) {
+                        int32_t* brick_coords, uint32_t* brick_grid, int* info, void* ws,
+                        size_t ws_bytes, vs_stream_t stream) {
   if (!bitmap || !tile_counts || !lo || !hi || !left || !right || !leaf_brick ||
       !brick_coords || !info || bs < 1 || P < 8 || cap < 1)
     return fail_arg("vs_lbvh_from_bitmap");
   if (ws_bytes < vs_lbvh_workspace(P, cap)) return VS_EWORKSPACE;
   cudaStream_t st = S(stream);
   const int64_t ntiles = (int64_t)P * P * P / 512;
+  uint32_t *off, *codes;
+  uint4 *cpre, *csuf, *ctot;
+  int4* cross;
+  int* ccount;
+  bitmap_ws(P, cap, &off, &codes, &cpre, &csuf, &ctot, &cross, &ccount, ws);
+  if (ntiles <= (int64_t)SCAN_T * SCAN_PER) {
+    k_tile_scan<<<1, SCAN_T, 0, st>>>(tile_counts, ntiles, off);
+    VS_TRY(check_launch("k_tile_scan"));
+  } else {  // exclusive scan over ntiles+1 entries; the extra (zero) entry yields the total n
+    size_t sb = scan_temp_bytes(ntiles + 1);
+    void* tmp = reinterpret_cast<char*>(off) + (((ntiles + 1) * 4 + 255) & ~int64_t(255));
+    VS_CUDA(cudaMemcpyAsync(off, tile_counts, ntiles * 4, cudaMemcpyDeviceToDevice, st), "copy");
+    VS_CUDA(cudaMemsetAsync(off + ntiles, 0, 4, st), "memset");
+    VS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, sb, off, off, (int)(ntiles + 1), st), "scan");
+  }
+  const int nby = (ny + bs - 1) / bs, nbz = (nz + bs - 1) / bs;
+  if (brick_grid) {
+    const int64_t nbx = (nx + bs - 1) / bs;
+    VS_CUDA(cudaMemsetAsync(brick_grid, 0, ((nbx * nby * nbz + 31) / 32) * 4, st),
+            "memset brick grid");
+  }
+  const int64_t pairs = cdiv(ntiles, 2);
+  k_leaves_coop<<<(unsigned)cdiv(pairs, LV_WARPS), LV_WARPS * 32, 0, st>>>(
+      bitmap, off, bs, nx, ny, nz, nby, nbz, ntiles, codes, lo, hi, left, right, leaf_brick,
+      brick_coords, brick_grid, info, ccount);
+  VS_TRY(check_launch("k_leaves_coop"));
+  const int nsm = sm_count();
+  const int64_t grid = std::min<int64_t>(cdiv(cap, TC), (int64_t)nsm * 4);
+  k_tree_chunk<<<(unsigned)std::max<int64_t>(grid, 1), TC, 0, st>>>(
+      codes, info, bs, nx, ny, nz, brick_coords, lo, hi, left, right, leaf_brick, cpre, csuf, ctot,
+      cross, ccount);
+  VS_TRY(check_launch("k_tree_chunk"));
+  k_tree_cross<<<(unsigned)nsm, 256, 0, st>>>(cross, ccount, bs, nx, ny, nz, cpre, csuf, ctot,
+                                               lo, hi);
+  return check_launch("k_tree_cross");
+}
+
+size_t vs_lbvh_height_workspace(int64_t cap) {
+  Bump b(nullptr);
+  b.take<int32_t>(std::max<int64_t>(2 * cap, 1));
+  b.take<int32_t>(std::max<int64_t>(cap, 1));
+  b.take<int32_t>(std::max<int64_t>(cap, 1));
+  return b.off + 256;
+}
+
+int vs_lbvh_height(const int32_t* left, const int32_t* right, int* info, int64_t cap, void* ws,
+                   size_t ws_bytes, vs_stream_t stream) {
+  if (!left || !right || !info || cap < 1) return fail_arg("vs_lbvh_height");
+  if (ws_bytes < vs_lbvh_height_workspace(cap)) return VS_EWORKSPACE;
+  cudaStream_t st = S(stream);
   Bump b(ws);
-  uint32_t* off = b.take<uint32_t>(ntiles + 1);
-  size_t sb = scan_temp_bytes(ntiles + 1);
-  void* tmp = b.take<char>(sb);
-  TreeWs w = take_tree(b, cap);
-  // exclusive scan over ntiles+1 entries; the extra (zero) entry yields the total n.
-  VS_CUDA(cudaMemcpyAsync(off, tile_counts, ntiles * 4, cudaMemcpyDeviceToDevice, st), "copy");
-  VS_CUDA(cudaMemsetAsync(off + ntiles, 0, 4, st), "memset");
-  VS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, sb, off, off, (int)(ntiles + 1), st), "scan");
-  k_leaves_from_bitmap<<<(unsigned)cdiv(ntiles * 16, 256), 256, 0, st>>>(
-      bitmap, off, bs, nx, ny, nz, ntiles, w.keys, lo, hi, left, right, leaf_brick, brick_coords,
-      info);
-  VS_TRY(check_launch("k_leaves_from_bitmap"));
-  return tree_and_refit(w, cap, lo, hi, left, right, leaf_brick, info, st);
+  int32_t* parent = b.take<int32_t>(std::max<int64_t>(2 * cap, 1));
+  int32_t* visit = b.take<int32_t>(std::max<int64_t>(cap, 1));
+  int32_t* hgt = b.take<int32_t>(std::max<int64_t>(cap, 1));
+  const unsigned g = (unsigned)cdiv(cap, 256);
+  k_parents<<<g, 256, 0, st>>>(left, right, info, parent, visit);
+  VS_TRY(check_launch("k_parents"));
+  k_height_climb<<<g, 256, 0, st>>>(left, right, parent, visit, hgt, info);
+  return check_launch("k_height_climb");
 }
 
 size_t vs_lbvh_bricks_workspace(int64_t n) {

@@ -3,7 +3,9 @@
 ``LbvhRebuilder`` owns every device buffer of one volume's LBVH rebuild (summary, Morton
 bitmap, tile counts, tree arrays, workspace) so a rebuild is a fixed launch sequence:
 
-    vs_classify_summary -> vs_summary_to_bitmap -> vs_lbvh_from_bitmap
+    cold: vs_classify_summary -> vs_summary_to_bitmap -> vs_lbvh_from_bitmap
+    warm: vs_presence_to_bitmap -> vs_lbvh_from_bitmap   (per-volume presence masks, built
+          once: a TF change reads 32 B per brick instead of the volume)
 
 reading the TF only through a 64-byte device parameter block.  The sequence is captured once
 into a CUDA graph; a TF change is then one 64-byte copy + one graph launch, with the index
@@ -19,7 +21,7 @@ from . import _lib
 from ._lib import call, ptr, query
 from .lbvh import Lbvh, _alloc_tree
 from .svt import MacroGrid
-from .volume import TransferFunction, Volume
+from .volume import TransferFunction, Volume, presence_table
 
 
 class LbvhRebuilder:
@@ -27,13 +29,17 @@ class LbvhRebuilder:
     hierarchy covers the union of the channels' visible voxels; one 64-byte TF block per
     channel, stacked)."""
 
-    def __init__(self, v, brick_size: int = 8, with_grid: bool = False, count: bool = False):
+    def __init__(self, v, brick_size: int = 8, with_grid: bool = False, count: bool = False,
+                 warm: bool = False):
         self.channels = list(v) if isinstance(v, (list, tuple)) else [v]
         v = self.channels[0]
         if brick_size != 8 or v.dims[2] % 16 != 0:
             raise ValueError("LbvhRebuilder needs 8^3 bricks and nz % 16 == 0")
         if len(self.channels) > 1 and count:
             raise ValueError("count is single-channel only")
+        if warm and count:
+            raise ValueError("the warm rebuild does not read the volume: no voxel count")
+        self.warm = bool(warm)
         self.v = v
         self.dims = v.dims
         nx, ny, nz = v.dims
@@ -58,12 +64,17 @@ class LbvhRebuilder:
         self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=dev)
         words = (self.cap + 31) // 32
         self.brick_bits = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
+        self.presence = None
+        if self.warm:  # the channels' per-volume halo presence masks (built once per volume)
+            self.presence = presence_table(self.channels)
         self.graph = None
         self._view = None
 
     # -- the launch sequence ------------------------------------------------------------
     def launch_summary(self, st: int):
         nx, ny, nz = self.dims
+        if self.warm:
+            return  # the presence masks replace the per-TF volume pass
         if self.count is not None:
             self.count.zero_()
         if self.summary_tmp is None:
@@ -79,16 +90,19 @@ class LbvhRebuilder:
 
     def launch_tree(self, st: int):
         nx, ny, nz = self.dims
-        call("vs_summary_to_bitmap", ptr(self.summary), nx, ny, nz, 1, self.P, ptr(self.bitmap),
-             ptr(self.tiles), ptr(self.grid), st)
+        # the vote also writes the leaf-brick grid for the renderer's brick DDA ("index ready")
+        if self.warm:
+            call("vs_presence_to_bitmap", ptr(self.presence), ptr(self.params),
+                 len(self.channels), nx, ny, nz, self.P, ptr(self.bitmap), ptr(self.tiles),
+                 ptr(self.grid), ptr(self.brick_bits), st)
+        else:
+            call("vs_summary_to_bitmap", ptr(self.summary), nx, ny, nz, 1, self.P,
+                 ptr(self.bitmap), ptr(self.tiles), ptr(self.grid), ptr(self.brick_bits), st)
         t = self.tree
         call("vs_lbvh_from_bitmap", ptr(self.bitmap), ptr(self.tiles), self.P, 8, nx, ny, nz,
              self.cap, ptr(t["lo"]), ptr(t["hi"]), ptr(t["left"]), ptr(t["right"]),
-             ptr(t["leaf_brick"]), ptr(t["brick_coords"]), ptr(self.info), ptr(self.ws),
+             ptr(t["leaf_brick"]), ptr(t["brick_coords"]), None, ptr(self.info), ptr(self.ws),
              self.wsb, st)
-        # leaf-brick grid for the renderer's brick DDA (part of "index ready")
-        call("vs_lbvh_brick_grid", ptr(t["brick_coords"]), ptr(self.info), self.cap, *self.nb,
-             ptr(self.brick_bits), st)
 
     def launch(self):
         st = torch.cuda.current_stream().cuda_stream
@@ -139,12 +153,15 @@ class LbvhRebuilder:
         return MacroGrid(16, nc, self.dims, self.grid.clone())
 
     def algorithmic_bytes(self, n_bricks: int) -> dict:
-        """SURVEY.md §8(d) B_lbvh terms for one rebuild (compulsory traffic only)."""
+        """SURVEY.md §8(d) B_lbvh terms for one rebuild (compulsory traffic only).  The warm
+        rebuild replaces the volume read by the presence masks (32 B per brick per channel)."""
         nx, ny, nz = self.dims
         vol = nx * ny * nz
+        tree = 16 * n_bricks + 36 * (2 * n_bricks - 1) + 12 * n_bricks
         return {
             "summary_kernel": vol + 4 * self.cap,           # u8 read + 27-bit summary write
-            "rebuild": vol + 16 * n_bricks + 36 * (2 * n_bricks - 1) + 12 * n_bricks,
+            "rebuild": vol + tree,                          # B_lbvh (cold)
+            "rebuild_warm": 32 * self.cap * len(self.channels) + tree,
         }
 
 

@@ -138,15 +138,18 @@ def flag_bricks(b: BinaryVolume, brick_size: int = DEFAULT_BRICK_SIZE) -> BrickS
     bitmap = torch.empty(P * P * P // 32, dtype=torch.int32, device=dev)
     tiles = torch.empty(P * P * P // 512, dtype=torch.int32, device=dev)
     nx, ny, nz = dims
+    grid = None
     if bs == 8 and b.lazy and b.summary_ok():
-        dilate = b._source[2]
-        call("vs_summary_to_bitmap", ptr(b.summary()), nx, ny, nz, int(dilate), P, ptr(bitmap),
-             ptr(tiles), None, stream())
+        words = (nb[0] * nb[1] * nb[2] + 31) // 32
+        grid = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
+        b.vote_bitmap(P, bitmap, tiles, grid=grid)
     else:
         flags = torch.empty(nb, dtype=torch.uint8, device=dev)
         call("vs_vote_cells", ptr(b.packed()), nx, ny, nz, bs, ptr(flags), stream())
         call("vs_flags_to_bitmap", ptr(flags), *nb, P, ptr(bitmap), ptr(tiles), stream())
-    return BrickSet(bs, dims, _bitmap=(bitmap, tiles, P, nb))
+    out = BrickSet(bs, dims, _bitmap=(bitmap, tiles, P, nb))
+    out._grid = grid  # C-order brick bits, when the vote produced them
+    return out
 
 
 class Lbvh:
@@ -183,8 +186,19 @@ class Lbvh:
         return 0 if self.n_bricks else -1
 
     def height(self) -> int:
-        """Nodes on the longest root-to-leaf path (computed during the device refit)."""
-        return self._ih()[1]
+        """Nodes on the longest root-to-leaf path (lbvh.py:128-144).  The bitmap builder does
+        not climb the tree, so, like the reference's DFS, the height is computed on the first
+        call (vs_lbvh_height) and kept in ``info``."""
+        h = self._ih()[1]
+        if h < 0:
+            cap = self.dev["brick_coords"].shape[0]
+            wsb = query("vs_lbvh_height_workspace", cap)
+            ws = _lib.workspace(wsb)
+            call("vs_lbvh_height", ptr(self.dev["left"]), ptr(self.dev["right"]), ptr(self.info),
+                 cap, ptr(ws), wsb, stream())
+            self._info_host = None
+            h = self._ih()[1]
+        return h
 
     def __getattr__(self, name):
         if name in Lbvh._FIELDS:
@@ -251,10 +265,17 @@ def build_lbvh(bricks: BrickSet) -> Lbvh:
         d = _alloc_tree(cap, dev)
         wsb = query("vs_lbvh_workspace", P, cap)
         ws = _lib.workspace(wsb)
+        grid = getattr(bricks, "_grid", None)
+        fill = grid is None  # the vote did not write the renderer's brick grid: leaves do
+        if fill:
+            grid = torch.empty(max((cap + 31) // 32, 1), dtype=torch.int32, device=dev)
         call("vs_lbvh_from_bitmap", ptr(bitmap), ptr(tiles), P, bs, nx, ny, nz, cap,
              ptr(d["lo"]), ptr(d["hi"]), ptr(d["left"]), ptr(d["right"]), ptr(d["leaf_brick"]),
-             ptr(d["brick_coords"]), ptr(info), ptr(ws), wsb, stream())
-        return Lbvh(d, info, bs, dims)
+             ptr(d["brick_coords"]), ptr(grid) if fill else None, ptr(info), ptr(ws), wsb,
+             stream())
+        out = Lbvh(d, info, bs, dims)
+        out.__dict__["_brick_grid"] = grid
+        return out
     n = bricks.count
     if n == 0:
         return empty_lbvh(bs, dims)

@@ -22,7 +22,10 @@ from . import _lib
 from ._lib import call, ptr, stream
 from .render import (Camera, Frame, RowsDesc, _check_flags, camera_desc, index_desc, tf_device,
                      volume_desc)
-from .volume import BinaryVolume, TransferFunction, Volume, _nzw
+from .volume import BinaryVolume, TransferFunction, Volume, _nzw, presence_table
+
+# channel pointer tables of the warm vote, per channel set (pointers re-checked on use)
+_TABLES: dict = {}
 
 
 class MultiBinaryVolume(BinaryVolume):
@@ -48,6 +51,26 @@ class MultiBinaryVolume(BinaryVolume):
                 call("vs_or_words", ptr(acc), ptr(tmp), acc.numel(), stream())
             self._summary = acc
         return self._summary
+
+    def vote_bitmap(self, P, bitmap, tiles, cell16=None, grid=None):
+        """Brick vote of the union: warm (channels seen before with another TF set) from the
+        channels' presence masks in one pass, else from the OR of the channels' summaries."""
+        vols, tfs, dilate = self._source
+        nx, ny, nz = self._dims
+        warm = dilate and self._summary is None and len(vols) <= 4 and \
+            all([v._warm_vote() for v in vols])
+        if warm:
+            key = tuple(id(v) for v in vols)
+            tab = _TABLES.get(key)
+            if tab is None or tab[0] != [v.presence().data_ptr() for v in vols]:
+                tab = ([v.presence().data_ptr() for v in vols], presence_table(vols))
+                _TABLES[key] = tab
+            params = torch.cat([tf.params() for tf in tfs])
+            call("vs_presence_to_bitmap", ptr(tab[1]), ptr(params), len(vols), nx, ny, nz, P,
+                 ptr(bitmap), ptr(tiles), ptr(cell16), ptr(grid), stream())
+        else:
+            call("vs_summary_to_bitmap", ptr(self.summary()), nx, ny, nz, int(dilate), P,
+                 ptr(bitmap), ptr(tiles), ptr(cell16), ptr(grid), stream())
 
     def packed(self) -> torch.Tensor:
         if self._packed is None:

@@ -71,8 +71,7 @@ def derive_macro_grid(source, cell_size: int) -> MacroGrid:
         P = query("vs_morton_side", *nb)
         bitmap = torch.empty(P * P * P // 32, dtype=torch.int32, device=dev)
         tiles = torch.empty(P * P * P // 512, dtype=torch.int32, device=dev)
-        call("vs_summary_to_bitmap", ptr(b.summary()), nx, ny, nz, int(b._source[2]), P,
-             ptr(bitmap), ptr(tiles), ptr(occ), stream())
+        b.vote_bitmap(P, bitmap, tiles, cell16=occ)
     else:
         call("vs_vote_cells", ptr(b.packed()), nx, ny, nz, cs, ptr(occ), stream())
     return MacroGrid(cs, nc, dims, occ)

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import call, ptr, stream
+from ._lib import call, ptr, query, stream
 
 LUT_SIZE = 256
 
@@ -145,6 +145,42 @@ class Volume:
     def bounds(self) -> Aabb:
         return Aabb((0, 0, 0), self.dims)
 
+    # -- warm path of the brick vote (TF-independent, SURVEY.md §8d cold / warm) -------------
+    def presence_ok(self) -> bool:
+        return self._dims[2] % 16 == 0 and self.bins.data_ptr() % 16 == 0
+
+    def presence(self) -> torch.Tensor:
+        """Per-8^3-brick 256-bit masks of the bins present in the brick's 1-voxel halo
+        (vs_presence_build, 32 B per brick), built once per volume.  A dilated brick vote of
+        any TF is then (presence & visible bins) != 0 (vs_presence_to_bitmap)."""
+        p = self.__dict__.get("_presence")
+        if p is None:
+            nx, ny, nz = self._dims
+            p = torch.empty(query("vs_presence_words", nx, ny, nz), dtype=torch.int32,
+                            device=self.bins.device)
+            call("vs_presence_build", ptr(self.bins), nx, ny, nz, ptr(p), stream())
+            self.__dict__["_presence"] = p
+        return p
+
+    def presence_table(self) -> torch.Tensor:
+        """Device array holding this volume's presence pointer (vs_presence_to_bitmap's
+        channel table for one channel)."""
+        t = self.__dict__.get("_presence_tab")
+        if t is None:
+            t = presence_table([self])
+            self.__dict__["_presence_tab"] = t
+        return t
+
+    def _warm_vote(self) -> bool:
+        """Policy: the first TF on a volume takes the one-pass summary (cold, no extra
+        memory); from the second TF on, the presence masks are built once and every later
+        dilated vote reads them instead of the volume."""
+        if "_presence" in self.__dict__:
+            return True
+        n = self.__dict__.get("_dilated_votes", 0) + 1
+        self.__dict__["_dilated_votes"] = n
+        return n >= 2 and self.presence_ok()
+
 
 class TransferFunction:
     """256-entry RGBA lookup table, all channels in [0, 1] (volume.py:84-140)."""
@@ -217,6 +253,12 @@ class TransferFunction:
         return self._dev[key]
 
 
+def presence_table(volumes) -> torch.Tensor:
+    """Device int64 array of the volumes' presence-mask pointers (built on demand)."""
+    ptrs = np.array([v.presence().data_ptr() for v in volumes], dtype=np.int64)
+    return _lib.upload(ptrs)
+
+
 def quantize_scalar(values) -> np.ndarray:
     """Host mirror of volume.py:159-162 (floor(v*255 + 0.5) clamped, float64).  The device
     path applies the same rounding in k_quantize."""
@@ -285,6 +327,21 @@ class BinaryVolume:
             if count:
                 self._count = cnt
         return self._summary
+
+    def vote_bitmap(self, P: int, bitmap: torch.Tensor, tiles: torch.Tensor,
+                    cell16: torch.Tensor | None = None, grid: torch.Tensor | None = None):
+        """8^3 brick vote (flag_bricks lbvh.py:83-102; dilated or not) into the Morton bitmap
+        + tile counts, optionally the 16^3 macro cells and the C-order leaf-brick bit grid.
+        Dilated votes on a volume seen with an earlier TF read its presence masks (warm);
+        otherwise the one-pass summary of this classification (cold).  Needs summary_ok()."""
+        v, tf, dilate = self._source
+        nx, ny, nz = self._dims
+        if dilate and self._summary is None and v._warm_vote():
+            call("vs_presence_to_bitmap", ptr(v.presence_table()), ptr(tf.params()), 1, nx, ny, nz, P,
+                 ptr(bitmap), ptr(tiles), ptr(cell16), ptr(grid), stream())
+        else:
+            call("vs_summary_to_bitmap", ptr(self.summary()), nx, ny, nz, int(dilate), P,
+                 ptr(bitmap), ptr(tiles), ptr(cell16), ptr(grid), stream())
 
     def packed(self) -> torch.Tensor:
         """Packed bits (int32 words, z-packed rows), materialised on first use."""

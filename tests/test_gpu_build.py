@@ -156,6 +156,22 @@ def test_random_volumes_vs_oracle(vs, rng, dims, tfkind):
                                       O.macro_grid(ref, 16))
         np.testing.assert_array_equal(b.bits, ref)
     assert vs.classify(v, tf).base_count() == cnt
+    # warm path: from its second dilated TF on, a volume votes from its per-brick halo presence
+    # masks (vs_presence_to_bitmap) instead of reading the voxels -- same bricks, tree, grid
+    assert "_presence" in v.__dict__
+    bw = vs.classify(v, tf, dilate=True)
+    bricks = vs.flag_bricks(bw, 8)
+    coords, codes = O.flag_bricks(ref_dil, 8)
+    np.testing.assert_array_equal(bricks.coords, coords)
+    np.testing.assert_array_equal(bricks.codes, codes)
+    idx = vs.build_lbvh(bricks)
+    _check_lbvh_oracle(idx, O.build_lbvh(coords, codes, 8, dims))
+    nb = [-(-d // 8) for d in dims]
+    grid_bits = np.unpackbits(idx.brick_grid().cpu().numpy().view(np.uint8), bitorder="little")
+    want = np.zeros(nb[0] * nb[1] * nb[2], np.uint8)
+    want[(coords[:, 0] * nb[1] + coords[:, 1]) * nb[2] + coords[:, 2]] = 1
+    np.testing.assert_array_equal(grid_bits[:want.size], want)
+    assert not grid_bits[want.size:].any()
     # packed dilated bits first (the fused classify+dilate pass when nz % 32 == 0): same bits,
     # and the undilated count comes out of the same pass
     b = vs.classify(v, tf, dilate=True)

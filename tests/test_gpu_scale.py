@@ -227,3 +227,44 @@ def test_lbvh_1024_device_properties(vs, vol1024):
     left, right = idx.dev["left"][:n - 1].long(), idx.dev["right"][:n - 1].long()
     assert bool((lo[:n - 1] == torch.minimum(lo[left], lo[right])).all())
     assert bool((hi[:n - 1] == torch.maximum(hi[left], hi[right])).all())
+
+
+def test_lbvh_1024_warm_rebuild_equals_cold(vs, vol1024):
+    """The warm rebuild (per-volume presence masks, no volume read per TF) produces the cold
+    rebuild's arrays and leaf-brick grid at every sweep TF, including non-monotone band TFs
+    (where a per-brick min/max range test would not be exact)."""
+    import torch
+
+    from paper_1912_09596_b200.engine import LbvhRebuilder
+
+    u8, _ = vol1024
+    v = vs.Volume.from_u8(u8)
+    cold, warm = LbvhRebuilder(v), LbvhRebuilder(v, warm=True)
+    tfs = [vs.TransferFunction.ramp(t) for t in (0.6, 0.45, 0.3, 0.1, 0.0)]
+    for lo_b, hi_b in ((180, 181), (90, 120), (3, 4)):
+        lut = np.zeros((256, 4), np.float32)
+        lut[lo_b:hi_b + 1] = 0.5
+        tfs.append(vs.TransferFunction(lut))
+    for tf in tfs:
+        cold.rebuild(tf.params())
+        warm.rebuild(tf.params())
+        torch.cuda.synchronize()
+        assert torch.equal(cold.info[:1], warm.info[:1])
+        n = int(cold.info[0])
+        m = max(2 * n - 1, 0)
+        for f in LBVH:
+            rows = n if f == "brick_coords" else m
+            assert torch.equal(cold.tree[f][:rows], warm.tree[f][:rows]), f
+        assert torch.equal(cold.brick_bits, warm.brick_bits)
+    # multi-channel union (configs[4] semantics): warm == cold
+    ch = [v, vs.Volume.from_u8(torch.flip(u8, dims=[0]).contiguous())]
+    cold2, warm2 = LbvhRebuilder(ch), LbvhRebuilder(ch, warm=True)
+    p = torch.cat([vs.TransferFunction.ramp(0.3).params(), vs.TransferFunction.ramp(0.5).params()])
+    cold2.rebuild(p)
+    warm2.rebuild(p)
+    torch.cuda.synchronize()
+    n = int(cold2.info[0])
+    assert n > 0 and torch.equal(cold2.info[:1], warm2.info[:1])
+    for f in LBVH:
+        rows = n if f == "brick_coords" else 2 * n - 1
+        assert torch.equal(cold2.tree[f][:rows], warm2.tree[f][:rows]), f
