@@ -50,6 +50,7 @@ METRIC = "hierarchy build ms and render frames/s (Msamples/s) vs CPU ref; % HBM 
 FALLBACK_HBM_GBS = 6650.0
 W, H = 1920, 1080
 NSWEEP = 64
+ERT_EPS = 5e-4  # opt-in early ray termination of the "ert" key (north-star RGBA tolerance 1e-3)
 
 
 def sweep_tfs(k: int = NSWEEP):
@@ -290,7 +291,8 @@ def run_ours(args, rank, ws, local):
 
     import paper_1912_09596_b200 as vs
     from paper_1912_09596_b200.engine import LbvhRebuilder, tf_params_device
-    from paper_1912_09596_b200.render import camera_desc, index_desc, tf_device, volume_desc
+    from paper_1912_09596_b200.render import (RenderTarget, camera_desc, index_desc, render_rows,
+                                              tf_device, volume_desc)
     from paper_1912_09596_b200.tiles import TileRenderer
 
     n = args.size
@@ -323,7 +325,7 @@ def run_ours(args, rank, ws, local):
     built = [torch.cuda.Event(), torch.cuda.Event()]
     rendered = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def step(k, j):
+    def step(k, j, ert=0.0):
         b = k % 2
         with torch.cuda.stream(sb):
             sb.wait_event(rendered[b])        # buffer b free: frame k-2 rendered
@@ -332,7 +334,7 @@ def run_ours(args, rank, ws, local):
         st.wait_event(built[b])
         with torch.cuda.stream(st):
             img = tiles.render(v, tfs[j], idxs[b], cams[j], idx_desc=ids[b], vol_desc=vd,
-                               cam_desc=cds[j])
+                               cam_desc=cds[j], ert_eps=ert)
         rendered[b].record(st)
         return img
 
@@ -355,6 +357,18 @@ def run_ours(args, rank, ws, local):
             e1.record(st)
             torch.cuda.synchronize()
             total_ms = e0.elapsed_time(e1)
+            # the same loop with the opt-in early ray termination (north star: "front-to-back
+            # compositing and early ray termination"; not the headline, which is the
+            # reference's integrator bit for bit)
+            torch.cuda.synchronize()
+            e0.record(st)
+            sb.wait_stream(st)
+            for k in range(args.steps):
+                step(k, sweep_j(k, args.steps), ert=ERT_EPS)
+            st.wait_stream(sb)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ert_total_ms = e0.elapsed_time(e1)
             # component split (not the headline): rebuild alone, summary kernel alone, render alone
             bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(3)]
@@ -374,7 +388,7 @@ def run_ours(args, rank, ws, local):
                 rbc.launch_tree(st.cuda_stream)
                 summ.append((a, b))
             # render alone at the sparse / medium / dense TF (the reference's App. B view)
-            render_by_t = {}
+            render_by_t, ert_by_t = {}, {}
             for t in (0.6, 0.3, 0.0):
                 tft = vs.TransferFunction.ramp(t)
                 ridx = vs.build_index("lbvh", vs.classify(v, tft, dilate=True))
@@ -389,13 +403,31 @@ def run_ours(args, rank, ws, local):
                 b.record(st)
                 torch.cuda.synchronize()
                 render_by_t[t] = (a.elapsed_time(b) / rrep, tiles.sample_total())
-                del ridx
+                a.record(st)
+                for _ in range(rrep):
+                    tiles.render(v, tft, ridx, rcam, idx_desc=rdesc, vol_desc=vd, cam_desc=rcd,
+                                 ert_eps=ERT_EPS)
+                b.record(st)
+                torch.cuda.synchronize()
+                ert_ms, ert_smp = a.elapsed_time(b) / rrep, tiles.sample_total()
+                # ERT frame vs the exact frame (float RGBA, this rank's rows)
+                outs = []
+                for eps in (0.0, ERT_EPS):
+                    tg = RenderTarget(W, H, want_rgba64=True)
+                    render_rows(v, tft, ridx, rcam, tg, idx_desc=rdesc, vol_desc=vd,
+                                cam_desc=rcd, ert_eps=eps)
+                    outs.append(tg.rgba64)
+                err = float((outs[0] - outs[1]).abs().max())
+                ert_by_t[t] = (ert_ms, ert_smp, err)
+                del ridx, outs, tg
             torch.cuda.synchronize()
     total_ms = max_over_ranks(total_ms, ws)
     ms_per_step = total_ms / args.steps
     build_ms = max_over_ranks(bev[0][0].elapsed_time(bev[0][1]) / reps, ws)
     build_cold_ms = max_over_ranks(bev[1][0].elapsed_time(bev[1][1]) / reps, ws)
     render_ms_t = {t: max_over_ranks(ms, ws) for t, (ms, _) in render_by_t.items()}
+    ert_ms_t = {t: max_over_ranks(ms, ws) for t, (ms, _, _) in ert_by_t.items()}
+    ert_step_ms = max_over_ranks(ert_total_ms, ws) / args.steps
     summ_ms = statistics.median([a.elapsed_time(b) for a, b in summ])
     with torch.cuda.stream(st):
         rb.rebuild(params[0])  # the t = 0.6 index: reported counts and the parity check below
@@ -544,6 +576,16 @@ def run_ours(args, rank, ws, local):
                            "ramp(t); render_ms = t 0.3; l1_hit_pct_ncu from profiles/"
                            "<round>_ncu_render_tXX.json (ncu --set full, same view)",
                    "kernels": "k_segments_brick (LBVH brick DDA) + k_integrate_segments"},
+        "ert": {"eps": ERT_EPS, "value": 1e3 / ert_step_ms, "unit": "frames/s",
+                "ms_per_step": ert_step_ms,
+                "render_by_t": {f"{t:.1f}": {"ms": ert_ms_t[t], "fps": 1e3 / ert_ms_t[t],
+                                             "samples_per_frame": smp,
+                                             "max_abs_rgba_vs_exact": err}
+                                for t, (_, smp, err) in ert_by_t.items()},
+                "what": "opt-in early ray termination at opacity 1 - eps (RGBA within eps of "
+                        "the reference integral; north star tolerance 1e-3): the same timed "
+                        "loop and per-t renders with ert_eps; samples_per_frame = samples "
+                        "actually taken"},
         "summary_kernel_ms": summ_ms,
         "n_bricks": n_bricks, "lbvh_nodes": max(2 * n_bricks - 1, 0), "lbvh_height": height,
         "parity_index_vs_public_api": bool(parity),

@@ -737,6 +737,15 @@ __global__ void __launch_bounds__(FL_T)
   const int t = threadIdx.x, lane = t & 31;
   if (MODE == FL_PRESENCE && t < 32 && t < 8 * nch) s_vis[t >> 3][t & 7] = tf_params[16 * (t >> 3) + (t & 7)];
   constexpr int NL = MODE == FL_SUMMARY_DILATE ? 4 : 2;  // halo words / bricks per thread
+  // the thread's two bricks of a tile (Morton ranks t and t + FL_T): tile-invariant offsets
+  int loc[2][3];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t m = (uint32_t)(t + q * FL_T);
+    loc[q][0] = (int)compact10(m);
+    loc[q][1] = (int)compact10(m >> 1);
+    loc[q][2] = (int)compact10(m >> 2);
+  }
   uint32_t reg[NL][MODE == FL_PRESENCE ? 8 : 1];
   auto tile_origin = [](int64_t tile, int& tx, int& ty, int& tz) {
     tx = (int)compact10((uint32_t)tile) * 8;
@@ -759,9 +768,7 @@ __global__ void __launch_bounds__(FL_T)
         }
         reg[q][0] = v;
       } else {
-        const uint32_t m = (uint32_t)(t + q * FL_T);
-        const int bx = tx + (int)compact10(m), by = ty + (int)compact10(m >> 1),
-                  bz = tz + (int)compact10(m >> 2);
+        const int bx = tx + loc[q][0], by = ty + loc[q][1], bz = tz + loc[q][2];
         const bool in = bx < nbx && by < nby && bz < nbz;
         const int64_t lin = ((int64_t)bx * nby + by) * nbz + bz;
         if (MODE == FL_SUMMARY) {
@@ -842,9 +849,7 @@ __global__ void __launch_bounds__(FL_T)
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const uint32_t m = (uint32_t)(t + q * FL_T);
-        const int lx = (int)compact10(m), ly = (int)compact10(m >> 1), lz = (int)compact10(m >> 2);
-        const int v = lx * 80 + ly * 10 + lz;
+        const int v = loc[q][0] * 80 + loc[q][1] * 10 + loc[q][2];
         flag[q] = ((V[v] & 1u) | ((V[v + 1] >> 1) & 1u) | ((V[v + 2] >> 2) & 1u));
       }
     }
@@ -852,7 +857,7 @@ __global__ void __launch_bounds__(FL_T)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const uint32_t m = (uint32_t)(t + q * FL_T);
-      const int lx = (int)compact10(m), ly = (int)compact10(m >> 1), lz = (int)compact10(m >> 2);
+      const int lx = loc[q][0], ly = loc[q][1], lz = loc[q][2];
       const bool in = tx + lx < nbx && ty + ly < nby && tz + lz < nbz;
       flag[q] = in ? flag[q] : 0u;
       const uint32_t ball = __ballot_sync(0xffffffffu, flag[q] != 0u);

@@ -445,6 +445,15 @@ __device__ __forceinline__ int dlt32(const uint32_t* __restrict__ c, uint32_t ci
   if (j < 0 || j >= n) return -1;
   return __clz(ci ^ __ldg(c + j));  // codes are distinct: never 64 (lbvh.py:153-164)
 }
+// the same with the codes of [base, base + 3 TC) staged in shared memory (most searches of
+// the chunk's nodes stay inside it)
+__device__ __forceinline__ int dlt32s(const uint32_t* __restrict__ c, const uint32_t* sc,
+                                      int64_t base, uint32_t ci, int64_t j, int64_t n) {
+  if (j < 0 || j >= n) return -1;
+  const int64_t r = j - base;
+  const uint32_t cj = (r >= 0 && r < 3 * TC) ? sc[r] : __ldg(c + j);
+  return __clz(ci ^ cj);
+}
 
 // Karras emission (lbvh.py:167-200) for the chunk's internal nodes + in-chunk range boxes.
 __global__ void __launch_bounds__(TC)
@@ -456,6 +465,7 @@ __global__ void __launch_bounds__(TC)
                  int4* __restrict__ cross, int* __restrict__ cross_count) {
   __shared__ uint4 s_leaf[TC], s_pre[TC], s_suf[TC];
   __shared__ uint4 s_tot[TC / 32], s_bp[TC / 32], s_bs[TC / 32];
+  __shared__ uint32_t s_code[3 * TC];
   const int64_t n = info[0];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   constexpr int NW = TC / 32;
@@ -463,6 +473,12 @@ __global__ void __launch_bounds__(TC)
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t c0 = ch * TC, c1 = (c0 + TC < n) ? c0 + TC : n;
     const int64_t p = c0 + t;
+    const int64_t cbase = c0 - TC;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int64_t j = cbase + q * TC + t;
+      s_code[q * TC + t] = (j >= 0 && j < n) ? __ldg(codes + j) : 0u;
+    }
     uint4 b = box_empty();
     if (p < c1) {
       const uint32_t x = (uint32_t)brick_coords[3 * p], y = (uint32_t)brick_coords[3 * p + 1],
@@ -506,20 +522,20 @@ __global__ void __launch_bounds__(TC)
     // internal node i = p (lbvh.py:172-200)
     if (p < n - 1) {
       const int64_t i = p;
-      const uint32_t ci = __ldg(codes + i);
-      const int d = dlt32(codes, ci, i + 1, n) > dlt32(codes, ci, i - 1, n) ? 1 : -1;
-      const int dmin = dlt32(codes, ci, i - d, n);
+      const uint32_t ci = s_code[TC + t];
+      const int d = dlt32s(codes, s_code, cbase, ci, i + 1, n) > dlt32s(codes, s_code, cbase, ci, i - 1, n) ? 1 : -1;
+      const int dmin = dlt32s(codes, s_code, cbase, ci, i - d, n);
       int64_t lmax = 2;
-      while (dlt32(codes, ci, i + lmax * d, n) > dmin) lmax *= 2;
+      while (dlt32s(codes, s_code, cbase, ci, i + lmax * d, n) > dmin) lmax *= 2;
       int64_t l = 0;
       for (int64_t s = lmax / 2; s >= 1; s /= 2)
-        if (dlt32(codes, ci, i + (l + s) * d, n) > dmin) l += s;
+        if (dlt32s(codes, s_code, cbase, ci, i + (l + s) * d, n) > dmin) l += s;
       const int64_t j = i + l * d;
-      const int dnode = dlt32(codes, ci, j, n);
+      const int dnode = dlt32s(codes, s_code, cbase, ci, j, n);
       int64_t s = 0, st = l;
       while (true) {
         st = (st + 1) / 2;
-        if (dlt32(codes, ci, i + (s + st) * d, n) > dnode) s += st;
+        if (dlt32s(codes, s_code, cbase, ci, i + (s + st) * d, n) > dnode) s += st;
         if (st == 1) break;
       }
       const int64_t gamma = i + s * d + min(d, 0);

@@ -69,12 +69,14 @@ class TileRenderer:
         self.frame_dev = torch.empty((self.height, self.width, 4), dtype=torch.uint8, device=dev)
 
     def render(self, v, tf, index, cam: Camera, dt: float = 0.5, idx_desc=None, vol_desc=None,
-               cam_desc=None) -> torch.Tensor:
-        """Render this rank's stripes and assemble the full frame on every rank (device)."""
+               cam_desc=None, ert_eps: float = 0.0) -> torch.Tensor:
+        """Render this rank's stripes and assemble the full frame on every rank (device).
+        ``ert_eps`` > 0: opt-in early ray termination (RGBA within ert_eps of the reference
+        integral, fewer samples); 0 is the reference's integrator."""
         self._last_total = self.target.total
         render_rows(v, tf, index, cam, self.target, dt=dt, rows=self.rows_desc,
                     idx_desc=idx_desc or index_desc(index), vol_desc=vol_desc or volume_desc(v),
-                    cam_desc=cam_desc or camera_desc(cam))
+                    cam_desc=cam_desc or camera_desc(cam), ert_eps=ert_eps)
         if self.world == 1:
             self.frame_dev.copy_(self.target.rgba8[: self.height])
             return self.frame_dev

@@ -168,6 +168,33 @@ def test_config3_1080p_frame_vs_oracle(vs, vol1024, kind):
     assert int(samples.sum()) == want
 
 
+@pytest.mark.parametrize("t", [0.3, 0.0])
+def test_config3_1080p_early_ray_termination_vs_oracle(vs, vol1024, t):
+    """Opt-in ERT (bench "ert" key, eps 5e-4) against the oracle's float RGBA at the north
+    star's tolerance: every channel within 1e-3 (and within eps) of the reference integral, never
+    more samples than the reference counts, on a 64-row band of the 1080p LBVH frame."""
+    from paper_1912_09596_b200.render import RenderTarget, render_rows
+
+    u8, host = vol1024
+    v = vs.Volume.from_u8(u8)
+    tf = vs.TransferFunction.ramp(t)
+    idx = vs.build_index("lbvh", vs.classify(v, tf, dilate=True))
+    cam = vs.Camera.orbit(v.dims, 30.0, 15.0, width=1920, height=1080)
+    r0, r1 = 480, 544
+    eps = 5e-4
+    tgt = RenderTarget(1920, 1080, want_rgba64=True, want_samples=True)
+    render_rows(v, tf, idx, cam, tgt, ert_eps=eps)
+    rgba = tgt.rgba64.cpu().numpy().reshape(1080, 1920, 4)[r0:r1]
+    samples = tgt.samples.cpu().numpy().reshape(1080, 1920)[r0:r1]
+    ref = _oracle_lbvh(O.classify(host, tf.lut, dilate=True)[0])
+    orgba, osamples = O.render("lbvh", host, tf.lut, ref, cam, rows=(r0, r1))
+    err = float(np.max(np.abs(rgba - orgba.reshape(rgba.shape))))
+    assert err <= eps <= 1e-3, err
+    assert np.all(samples <= osamples.reshape(samples.shape))
+    if t == 0.0:  # dense: saturating rays stop early (about a quarter fewer samples)
+        assert int(samples.sum()) < 0.9 * int(osamples.sum())
+
+
 # -- configs[4] ---------------------------------------------------------------------------------
 
 def test_config4_four_channel_1024_row_band_vs_oracle(vs, vol1024):

@@ -12,7 +12,8 @@ b = vs.classify(v, tf, dilate=True)
 b.packed()
 torch.cuda.synchronize()
 import time
-t0 = time.perf_counter()
-idx = vs.build_index(kind, b)
-torch.cuda.synchronize()
-print("build s", time.perf_counter() - t0, vs.report_stats(idx))
+for rep in range(int(sys.argv[4]) if len(sys.argv) > 4 else 2):  # first: warm-up
+    t0 = time.perf_counter()
+    idx = vs.build_index(kind, b)
+    torch.cuda.synchronize()
+    print("build ms", round((time.perf_counter() - t0) * 1e3, 3), vs.report_stats(idx), flush=True)
