@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(MC_TX* MC_TY)
         bool sure = true;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          bins[c] = bin_fast(sm.u8f, g.w0[c], g.w1[c], fx32, fy32, fz32);
+          bins[c] = bin_fast_table(sm.u8f, g.w0[c], g.w1[c], fx32, fy32, fz32);
           sure &= bins[c] >= 0;
         }
         if (!sure) {
