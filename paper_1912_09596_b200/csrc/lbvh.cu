@@ -445,13 +445,13 @@ __device__ __forceinline__ int dlt32(const uint32_t* __restrict__ c, uint32_t ci
   if (j < 0 || j >= n) return -1;
   return __clz(ci ^ __ldg(c + j));  // codes are distinct: never 64 (lbvh.py:153-164)
 }
-// the same with the codes of [base, base + 3 TC) staged in shared memory (most searches of
+// the same with the codes of [base, base + 2 TC) staged in shared memory (most searches of
 // the chunk's nodes stay inside it)
 __device__ __forceinline__ int dlt32s(const uint32_t* __restrict__ c, const uint32_t* sc,
                                       int64_t base, uint32_t ci, int64_t j, int64_t n) {
   if (j < 0 || j >= n) return -1;
   const int64_t r = j - base;
-  const uint32_t cj = (r >= 0 && r < 3 * TC) ? sc[r] : __ldg(c + j);
+  const uint32_t cj = (r >= 0 && r < 2 * TC) ? sc[r] : __ldg(c + j);
   return __clz(ci ^ cj);
 }
 
@@ -463,19 +463,27 @@ __global__ void __launch_bounds__(TC)
                  int32_t* __restrict__ right, int32_t* __restrict__ leaf_brick,
                  uint4* __restrict__ cpre, uint4* __restrict__ csuf, uint4* __restrict__ ctot,
                  int4* __restrict__ cross, int* __restrict__ cross_count) {
-  __shared__ uint4 s_leaf[TC], s_pre[TC], s_suf[TC];
-  __shared__ uint4 s_tot[TC / 32], s_bp[TC / 32], s_bs[TC / 32];
-  __shared__ uint32_t s_code[3 * TC];
+  // s_leaf: leaf boxes; s_sp[L-1][i]: union of leaves [i, i + 2^L) of i's warp block (clipped to
+  // the block), L = 1..4, so any in-block range is two lookups; s_tl[L][w]: the same over the
+  // warp-block totals (L = 0: the totals)
+  __shared__ uint4 s_leaf[TC], s_sp[4][TC];
+  __shared__ uint4 s_tl[4][TC / 32], s_bp[TC / 32], s_bs[TC / 32];
+  __shared__ uint32_t s_code[2 * TC];
   const int64_t n = info[0];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   constexpr int NW = TC / 32;
+  auto in_block = [&](int a, int e) -> uint4 {  // a <= e, same warp block (local indices)
+    if (a == e) return s_leaf[a];
+    const int L = min(31 - __clz(e - a + 1), 4);
+    return box_union(s_sp[L - 1][a], s_sp[L - 1][e - (1 << L) + 1]);
+  };
   const int64_t nchunks = (n + TC - 1) / TC;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t c0 = ch * TC, c1 = (c0 + TC < n) ? c0 + TC : n;
     const int64_t p = c0 + t;
-    const int64_t cbase = c0 - TC;
+    const int64_t cbase = c0 - TC / 2;
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < 2; ++q) {
       const int64_t j = cbase + q * TC + t;
       s_code[q * TC + t] = (j >= 0 && j < n) ? __ldg(codes + j) : 0u;
     }
@@ -494,19 +502,32 @@ __global__ void __launch_bounds__(TC)
       if (lane + o < 32) suf = box_union(suf, d);
     }
     s_leaf[t] = b;
-    s_pre[t] = pre;
-    s_suf[t] = suf;
-    if (lane == 31) s_tot[warp] = pre;
+    {
+      uint4 sp = b;
+#pragma unroll
+      for (int L = 1; L <= 4; ++L) {
+        const uint4 d = shfl_box(sp, 1 << (L - 1), false);
+        if (lane + (1 << (L - 1)) < 32) sp = box_union(sp, d);
+        s_sp[L - 1][t] = sp;
+      }
+    }
+    if (lane == 31) s_tl[0][warp] = pre;
     __syncthreads();
     if (warp == 0) {  // exclusive block prefix / suffix unions over the NW warp totals
-      const uint4 tv = lane < NW ? s_tot[lane] : box_empty();
-      uint4 bp = tv, bq = tv;
+      const uint4 tv = lane < NW ? s_tl[0][lane] : box_empty();
+      uint4 bp = tv, bq = tv, sp = tv;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint4 u = shfl_box(bp, o, true);
         if (lane >= o) bp = box_union(bp, u);
         const uint4 d = shfl_box(bq, o, false);
         if (lane + o < 32) bq = box_union(bq, d);
+      }
+#pragma unroll
+      for (int L = 1; L <= 3; ++L) {
+        const uint4 d = shfl_box(sp, 1 << (L - 1), false);
+        if (lane + (1 << (L - 1)) < NW) sp = box_union(sp, d);
+        if (lane < NW) s_tl[L][lane] = sp;
       }
       uint4 ex = shfl_box(bp, 1, true), ey = shfl_box(bq, 1, false);
       if (lane == 0) ex = box_empty();
@@ -522,7 +543,7 @@ __global__ void __launch_bounds__(TC)
     // internal node i = p (lbvh.py:172-200)
     if (p < n - 1) {
       const int64_t i = p;
-      const uint32_t ci = s_code[TC + t];
+      const uint32_t ci = s_code[TC / 2 + t];
       const int d = dlt32s(codes, s_code, cbase, ci, i + 1, n) > dlt32s(codes, s_code, cbase, ci, i - 1, n) ? 1 : -1;
       const int dmin = dlt32s(codes, s_code, cbase, ci, i - d, n);
       int64_t lmax = 2;
@@ -548,11 +569,13 @@ __global__ void __launch_bounds__(TC)
         const int wa = la >> 5, we = le >> 5;
         uint4 acc;
         if (wa == we) {
-          acc = s_leaf[la];
-          for (int k = la + 1; k <= le; ++k) acc = box_union(acc, s_leaf[k]);
+          acc = in_block(la, le);
         } else {
-          acc = box_union(s_suf[la], s_pre[le]);
-          for (int w = wa + 1; w < we; ++w) acc = box_union(acc, s_tot[w]);
+          acc = box_union(in_block(la, 32 * wa + 31), in_block(32 * we, le));
+          if (we - wa >= 2) {  // whole blocks wa+1 .. we-1
+            const int u = wa + 1, v = we - 1, L = 31 - __clz(v - u + 1);
+            acc = box_union(acc, box_union(s_tl[L][u], s_tl[L][v - (1 << L) + 1]));
+          }
         }
         store_box(acc, bs, nx, ny, nz, i, lo, hi);
       } else {
