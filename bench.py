@@ -488,9 +488,32 @@ def run_ours(args, rank, ws, local):
     # reported for the SVT k-d tree, binned k-d tree and hybrid grid"): public API, classify +
     # build_index, synchronised, median of 3 after one warm-up, sparse / medium / dense ramp
     rebuilds = {}
+    vox = v.dims[0] * v.dims[1] * v.dims[2]
+    nbricks = rb.cap
+    ncell16 = (-(-v.dims[0] // 16)) * (-(-v.dims[1] // 16)) * (-(-v.dims[2] // 16))
+
+    def kind_bytes(kind, st):
+        """Compulsory bytes of one TF-change rebuild (SVT-free builders: no summed-volume
+        tables are written, so SURVEY §8d's B_svt-kd term does not apply).  lbvh / grid take the
+        warm vote (the volume already has its presence masks): 32 B per brick; the k-d kinds
+        classify + dilate the volume to packed bits (N^3 read, N^3/8 written) and write 37 B
+        per row; hybrid adds its 16^3 grid, binned its 13 B per 8^3 cell box."""
+        m = st["node_count"]
+        if kind == "lbvh":
+            nb = (m + 1) // 2
+            return 32 * nbricks + 16 * nb + 36 * m + 12 * nb
+        if kind == "grid":
+            return 32 * nbricks + ncell16
+        b = vox + vox // 8 + 37 * m
+        if kind == "hybrid":
+            b += ncell16
+        if kind.startswith("kd-binned"):
+            b += 13 * nbricks
+        return b
+
     for kind in () if args.frame_only else ("lbvh", "grid", "hybrid", "kd-shallow",
                                             "kd-binned-mls32"):
-        per_t = []
+        per_t, fr_t, m_t = [], [], []
         for t in (0.6, 0.3, 0.0):
             tfk = vs.TransferFunction.ramp(t)
             times = []
@@ -498,12 +521,15 @@ def run_ours(args, rank, ws, local):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 ix = vs.build_index(kind, vs.classify(v, tfk, dilate=True))
-                vs.report_stats(ix)
+                stats = vs.report_stats(ix)
                 torch.cuda.synchronize()
                 if r:
                     times.append((time.perf_counter() - t0) * 1e3)
-            per_t.append(round(statistics.median(times), 3))
-        rebuilds[kind] = per_t
+            ms = statistics.median(times)
+            per_t.append(round(ms, 3))
+            m_t.append(stats["node_count"])
+            fr_t.append(round(kind_bytes(kind, stats) / (ms * 1e-3) / 1e9 / hbm_peak()[0], 3))
+        rebuilds[kind] = {"ms": per_t, "nodes": m_t, "roofline_frac": fr_t}
         del ix
     torch.cuda.empty_cache()
 
@@ -595,9 +621,10 @@ def run_ours(args, rank, ws, local):
                      "alg_bytes_per_launch": alg["summary_kernel"],
                      "share_of_step": summ_ms / ms_per_step},
         "rebuild_roofline_frac": alg["rebuild"] / (build_cold_ms * 1e-3) / 1e9 / peak,
-        "rebuild_ms_by_kind": {"ramp_t": [0.6, 0.3, 0.0], **rebuilds,
-                               "how": "public API classify+build_index, host-synchronised "
-                                      "wall time, median of 3"},
+        "rebuild_by_kind": {"ramp_t": [0.6, 0.3, 0.0], **rebuilds,
+                            "how": "public API classify+build_index, host-synchronised wall "
+                                   "time, median of 3; roofline_frac = compulsory bytes (see "
+                                   "kind_bytes in bench.py / DESIGN.md §3) / time / HBM peak"},
         "e2e": {"value": 1e3 / e2e_ms, "unit": "frames/s",
                 "h2d_bytes_per_step": 64 + 4096 + 2048, "d2h_bytes_per_step": W * H * 4 + 16,
                 "ms_per_step": e2e_ms, "passes_ms_per_step": [round(x, 4) for x in e2e_runs],
