@@ -29,7 +29,7 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   python bench.py --steps 2 --warmup 3 --no-cpu --frame-only > /dev/null 2>&1
 for t in 0.6 0.3 0.0; do
   timeout 600 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_segments_brick|k_integrate_segments" -s 2 -c 2 -o gpurun_out/render_t$t \
+    -k regex:"k_segments_brick|k_integrate_segments" -c 2 -o gpurun_out/render_t$t \
     python tools/prof_render.py 1024 lbvh $t 32 > /dev/null 2>&1
 done
 timeout 900 ncu --set full --clock-control none --import-source on \
