@@ -174,13 +174,17 @@ struct Integrator {
   // before the current sample's arithmetic (render.py:694-744) ----
   struct Gather {
     uint32_t w0, w1;
+    uint32_t fix;  // lazy border fix-ups (bit 0: y0 clamped below, bit 1: z0), see settle()
     double fx, fy, fz;
   };
   __device__ __forceinline__ void gather(double tt, Gather& g) const {
     if (idx32) gather_t<true>(tt, g);
     else gather_t<false>(tt, g);
   }
-  template <bool IDX32>
+  // LAZY: leave the clamped-border byte fix-ups to settle(), so the loads can complete while
+  // the previous sample is shaded (a fix-up right after the load waits on it even when its
+  // predicate is false)
+  template <bool IDX32, bool LAZY = false>
   __device__ __forceinline__ void gather_t(double tt, Gather& g) const {
     const double px = __dadd_rn(r->ox, __dmul_rn(tt, r->dx));
     const double py = __dadd_rn(r->oy, __dmul_rn(tt, r->dy));
@@ -202,11 +206,15 @@ struct Integrator {
       w0 = __ldg(quads + (int64_t)x0 * sxq + yz);
       w1 = __ldg(quads + (int64_t)x1 * sxq + yz);
     }
-    // clamped low borders: the +1 neighbour is the voxel itself
-    if (y0r < 0) { w0 = __byte_perm(w0, 0, 0x1010); w1 = __byte_perm(w1, 0, 0x1010); }
-    if (z0r < 0) { w0 = __byte_perm(w0, 0, 0x2200); w1 = __byte_perm(w1, 0, 0x2200); }
     g.w0 = w0;
     g.w1 = w1;
+    g.fix = (y0r < 0 ? 1u : 0u) | (z0r < 0 ? 2u : 0u);
+    if (!LAZY) settle(g);
+  }
+  // clamped low borders: the +1 neighbour is the voxel itself
+  __device__ __forceinline__ static void settle(Gather& g) {
+    if (g.fix & 1u) { g.w0 = __byte_perm(g.w0, 0, 0x1010); g.w1 = __byte_perm(g.w1, 0, 0x1010); }
+    if (g.fix & 2u) { g.w0 = __byte_perm(g.w0, 0, 0x2200); g.w1 = __byte_perm(g.w1, 0, 0x2200); }
   }
   __device__ __forceinline__ double interp(const Gather& g) const {
     if (use_tab) return interp_t<true>(g);
@@ -1417,8 +1425,10 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
         int2 kr = segs[pix];
         int2 krn = n > 1 ? segs[npix + pix] : make_int2(0, 0);
         int k = kr.x;
+        const uint32_t lut_s = (uint32_t)__cvta_generic_to_shared(sm.lut);
+        const uint32_t corr_s = (uint32_t)__cvta_generic_to_shared(sm.corr);
         Integrator::Gather g;
-        I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
+        I.gather_t<IDX32, true>(__dadd_rn(I.entry, __dmul_rn((double)k, dt)), g);
         while (true) {
           int kn = k + 1;
           bool hn = true;
@@ -1433,11 +1443,28 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
             }
           }
           Integrator::Gather gn;
-          if (hn) I.gather_t<IDX32>(__dadd_rn(I.entry, __dmul_rn((double)kn, dt)), gn);
+          if (hn) I.gather_t<IDX32, true>(__dadd_rn(I.entry, __dmul_rn((double)kn, dt)), gn);
+          Integrator::settle(g);
           // bin_filter 0: every sample through the FP64 path (tests the filter's exactness)
           int bin = bin_filter ? I.bin_fast(g) : -1;
           if (bin < 0) bin = Integrator::bin_of(I.interp_t<true>(g));
-          I.shade_bin(bin);
+          {  // I.shade_bin(bin) on the kernel's shared tables, addressed from 32-bit shared
+             // offsets taken once (the generic path re-derives the CTA's window every sample)
+            float4 c;
+            asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w)
+                         : "r"(lut_s + 16u * (uint32_t)bin));
+            if (c.w > 0.0f) {
+              double cr;
+              asm("ld.shared.f64 %0, [%1];" : "=d"(cr) : "r"(corr_s + 8u * (uint32_t)bin));
+              const double w = __dmul_rn(1.0 - I.acca, cr);
+              I.accr = __dadd_rn(I.accr, __dmul_rn(w, (double)c.x));
+              I.accg = __dadd_rn(I.accg, __dmul_rn(w, (double)c.y));
+              I.accb = __dadd_rn(I.accb, __dmul_rn(w, (double)c.z));
+              I.acca = __dadd_rn(I.acca, w);
+            }
+            ++I.taken;
+          }
           if (!hn || (ERT && I.terminated())) break;
           k = kn;
           g = gn;

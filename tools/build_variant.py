@@ -14,7 +14,10 @@ out.mkdir(exist_ok=True)
 objdir = out / f"obj_{name}"
 objdir.mkdir(exist_ok=True)
 procs, objs = [], []
-for src in _build.sources():
+import os  # noqa: E402
+srcdir = os.environ.get("VARIANT_SRC")  # optional: another csrc tree (e.g. a git checkout)
+sources = sorted(Path(srcdir).glob("*.cu")) if srcdir else _build.sources()
+for src in sources:
     obj = objdir / (src.stem + ".o")
     cmd = [_build._nvcc(), *_build.NVCC_FLAGS, *extra, "-I", str(_build.ROOT / "include"), "-c",
            str(src), "-o", str(obj)]
