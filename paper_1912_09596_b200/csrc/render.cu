@@ -1476,20 +1476,26 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
         };
         constexpr int PF = KIND == VS_KIND_GRID ? VS_PREFETCH_GRID : VS_PREFETCH;
         if constexpr (PF >= 2) {
-        // gathers issued two samples ahead: two loads per warp in flight across the shading
-        Integrator::Gather g0, g1;
+        // gathers issued two samples ahead; the loop is unrolled three times so the three
+        // gather slots rotate by role, never by copying (a copy of a loaded register waits on
+        // the load like any other use)
+        Integrator::Gather g0, g1, g2;
         issue(g0);
-        bool h1 = advance();
+        bool h0 = true, h1 = advance(), h2 = false;
         if (h1) issue(g1);
         while (true) {
-          const bool h2 = h1 && advance();
-          Integrator::Gather g2;
+          h2 = h1 && advance();
           if (h2) issue(g2);
           shade(g0);
           if (!h1 || (ERT && I.terminated())) break;
-          g0 = g1;
-          g1 = g2;
-          h1 = h2;
+          h0 = h2 && advance();
+          if (h0) issue(g0);
+          shade(g1);
+          if (!h2 || (ERT && I.terminated())) break;
+          h1 = h0 && advance();
+          if (h1) issue(g1);
+          shade(g2);
+          if (!h0 || (ERT && I.terminated())) break;
         }
         } else {
         Integrator::Gather g;
