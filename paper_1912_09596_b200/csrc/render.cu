@@ -31,14 +31,11 @@
 #ifndef VS_SEGMENTS_MINB
 #define VS_SEGMENTS_MINB 8
 #endif
-// Samples the integration loop's gathers run ahead of the shading (1 or 2), per index kind:
-// two loads in flight per warp take 7-10% off LBVH / hybrid / naive frames and 3% off binned
-// k-d frames, but cost the macro grid's frames 3-4% -- measured on the B200.
+// Samples the integration loop's gathers run ahead of the shading (1 or 2): two loads in
+// flight per warp (rotating slots) take 2-15% off every index kind's frames on the B200; three
+// (four slots) spill at the 80-register cap and lose 2-3%.
 #ifndef VS_PREFETCH
 #define VS_PREFETCH 2
-#endif
-#ifndef VS_PREFETCH_GRID
-#define VS_PREFETCH_GRID 1
 #endif
 
 namespace vs {
@@ -1474,7 +1471,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
         auto issue = [&](Integrator::Gather& g) {
           I.gather_t<IDX32, true>(__dadd_rn(I.entry, __dmul_rn((double)kc, dt)), g);
         };
-        constexpr int PF = KIND == VS_KIND_GRID ? VS_PREFETCH_GRID : VS_PREFETCH;
+        constexpr int PF = VS_PREFETCH;
         if constexpr (PF >= 2) {
         // gathers issued two samples ahead; the loop is unrolled three times so the three
         // gather slots rotate by role, never by copying (a copy of a loaded register waits on
