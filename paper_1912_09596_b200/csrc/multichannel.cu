@@ -84,6 +84,7 @@ __global__ void k_build_mquads(const uint8_t* __restrict__ b0, const uint8_t* __
 template <int NCH>
 struct McGather {
   uint32_t w0[NCH], w1[NCH];
+  uint32_t fix;  // lazy border fix-ups (bit 0: y0 clamped below, bit 1: z0): mc_settle
   double fx, fy, fz;
 };
 
@@ -118,11 +119,17 @@ __device__ __forceinline__ void mc_gather(const vs_multi_desc& md, double ox, do
     g.w0[0] = __ldg(reinterpret_cast<const uint32_t*>(md.mquads) + o0);
     g.w1[0] = __ldg(reinterpret_cast<const uint32_t*>(md.mquads) + o1);
   }
-  // clamped low borders: the +1 neighbour is the voxel itself
+  g.fix = (y0r < 0 ? 1u : 0u) | (z0r < 0 ? 2u : 0u);
+}
+
+// clamped low borders: the +1 neighbour is the voxel itself (applied when the sample is
+// consumed, so the gather's loads complete under the previous sample's shading)
+template <int NCH>
+__device__ __forceinline__ void mc_settle(McGather<NCH>& g) {
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
-    if (y0r < 0) { g.w0[c] = __byte_perm(g.w0[c], 0, 0x1010); g.w1[c] = __byte_perm(g.w1[c], 0, 0x1010); }
-    if (z0r < 0) { g.w0[c] = __byte_perm(g.w0[c], 0, 0x2200); g.w1[c] = __byte_perm(g.w1[c], 0, 0x2200); }
+    if (g.fix & 1u) { g.w0[c] = __byte_perm(g.w0[c], 0, 0x1010); g.w1[c] = __byte_perm(g.w1[c], 0, 0x1010); }
+    if (g.fix & 2u) { g.w0[c] = __byte_perm(g.w0[c], 0, 0x2200); g.w1[c] = __byte_perm(g.w1[c], 0, 0x2200); }
   }
 }
 
@@ -175,24 +182,25 @@ __global__ void __launch_bounds__(MC_TX* MC_TY)
       int q = 0;
       int2 kr = segs[pix];
       int2 krn = n > 1 ? segs[npix + pix] : make_int2(0, 0);
-      int k = kr.x;
-      McGather<NCH> g;
-      mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)k, dt)), g);
-      while (true) {
-        int kn = k + 1;
-        bool hn = true;
+      // the stream cursor: kc = the last lattice index whose gather was issued
+      int kc = kr.x;
+      auto advance = [&]() -> bool {
+        int kn = kc + 1;
         if (kn >= kr.y) {
-          if (q + 1 < n) {
-            ++q;
-            kr = krn;
-            kn = kr.x;
-            if (q + 1 < n) krn = segs[(int64_t)(q + 1) * npix + pix];
-          } else {
-            hn = false;
-          }
+          if (q + 1 >= n) return false;
+          ++q;
+          kr = krn;
+          kn = kr.x;
+          if (q + 1 < n) krn = segs[(int64_t)(q + 1) * npix + pix];
         }
-        McGather<NCH> gn;
-        if (hn) mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)kn, dt)), gn);
+        kc = kn;
+        return true;
+      };
+      auto issue = [&](McGather<NCH>& g) {
+        mc_gather<NCH>(md, ox, oy, oz, dx, dy, dz, __dadd_rn(entry, __dmul_rn((double)kc, dt)), g);
+      };
+      auto shade = [&](McGather<NCH>& g) {
+        mc_settle<NCH>(g);
         // every channel's bin by the FP32 filter (common.cuh bin_fast); the rare sample with a
         // channel near a bin edge re-evaluates that channel's reference FP64 lerps
         const float fx32 = __double2float_rn(g.fx), fy32 = __double2float_rn(g.fy),
@@ -239,9 +247,19 @@ __global__ void __launch_bounds__(MC_TX* MC_TY)
           }
         }
         ++taken;
-        if (!hn) break;
-        k = kn;
-        g = gn;
+      };
+      // one sample ahead in two rotating slots (no copies of loaded registers)
+      McGather<NCH> g0, g1;
+      issue(g0);
+      while (true) {
+        const bool h1 = advance();
+        if (h1) issue(g1);
+        shade(g0);
+        if (!h1) break;
+        const bool h0 = advance();
+        if (h0) issue(g0);
+        shade(g1);
+        if (!h0) break;
       }
     }
     const double acc[4] = {accr, accg, accb, acca};

@@ -89,8 +89,13 @@ class LbvhRebuilder:
                 call("vs_or_words", ptr(self.summary), ptr(out), self.cap, st)
 
     def launch_tree(self, st: int):
+        self.launch_vote(st)
+        self.launch_build(st)
+
+    def launch_vote(self, st: int):
+        """The dilated brick vote into the Morton bitmap (warm: presence masks; cold: summary);
+        it also writes the leaf-brick grid for the renderer's brick DDA ("index ready")."""
         nx, ny, nz = self.dims
-        # the vote also writes the leaf-brick grid for the renderer's brick DDA ("index ready")
         if self.warm:
             call("vs_presence_to_bitmap", ptr(self.presence), ptr(self.params),
                  len(self.channels), nx, ny, nz, self.P, ptr(self.bitmap), ptr(self.tiles),
@@ -98,6 +103,9 @@ class LbvhRebuilder:
         else:
             call("vs_summary_to_bitmap", ptr(self.summary), nx, ny, nz, 1, self.P,
                  ptr(self.bitmap), ptr(self.tiles), ptr(self.grid), ptr(self.brick_bits), st)
+
+    def launch_build(self, st: int):
+        nx, ny, nz = self.dims
         t = self.tree
         call("vs_lbvh_from_bitmap", ptr(self.bitmap), ptr(self.tiles), self.P, 8, nx, ny, nz,
              self.cap, ptr(t["lo"]), ptr(t["hi"]), ptr(t["left"]), ptr(t["right"]),
