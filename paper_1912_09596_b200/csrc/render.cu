@@ -101,6 +101,25 @@ __device__ __forceinline__ bool slab(const Ray& r, double lx, double ly, double 
   return true;
 }
 
+// slab() for a ray with no zero direction component (the branches on r.zx/zy/zz dropped).
+__device__ __forceinline__ bool slab_nz(const Ray& r, double lx, double ly, double lz, double hx,
+                                        double hy, double hz, double& t0, double& t1) {
+  double tmin = -R_FAR, tmax = R_FAR;
+  const double o[3] = {r.ox, r.oy, r.oz}, inv[3] = {r.ix, r.iy, r.iz};
+  const double l[3] = {lx, ly, lz}, h[3] = {hx, hy, hz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double ta = __dmul_rn(l[a] - o[a], inv[a]), tb = __dmul_rn(h[a] - o[a], inv[a]);
+    if (ta > tb) { double t = ta; ta = tb; tb = t; }
+    if (ta > tmin) tmin = ta;
+    if (tb < tmax) tmax = tb;
+  }
+  if (tmax <= tmin) return false;
+  t0 = tmin;
+  t1 = tmax;
+  return true;
+}
+
 __device__ __forceinline__ bool node_slab(const Ray& r, const int32_t* __restrict__ lo,
                                           const int32_t* __restrict__ hi, int i, double& a,
                                           double& b) {
@@ -901,7 +920,11 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
 // k_segments specialised for the LBVH brick DDA: the same DDA steps (BrickDDA::init/next),
 // interval merge (_sort_merge via MergeState) and lattice-range emission as the generic
 // kernel, written as one flat loop of one DDA step per turn with 32-bit brick indices and no
-// generator/budget plumbing between the step and the merge.
+// generator/budget plumbing between the step and the merge.  SGN >= 0: the (frame-uniform,
+// orthographic) ray direction has no zero component and bit a of SGN is the sign of axis a, so
+// the per-step sign bookkeeping and slab()'s zero-direction branches compile away; SGN = -1 is
+// the general kernel.
+template <int SGN>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
     k_segments_brick(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
                      double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
@@ -957,8 +980,10 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
       const bool shortcut = occ && live && interior && !exact_runs;
       if (occ && !shortcut) {
         double a, b;
-        if (slab(r, (double)l0, (double)l1, (double)l2, (double)min(l0 + bs, D.dims[0]),
-                 (double)min(l1 + bs, D.dims[1]), (double)min(l2 + bs, D.dims[2]), a, b)) {
+        const double h0 = (double)min(l0 + bs, D.dims[0]), h1 = (double)min(l1 + bs, D.dims[1]),
+                     h2 = (double)min(l2 + bs, D.dims[2]);
+        if (SGN >= 0 ? slab_nz(r, (double)l0, (double)l1, (double)l2, h0, h1, h2, a, b)
+                     : slab(r, (double)l0, (double)l1, (double)l2, h0, h1, h2, a, b)) {
           a = a > tmin ? a : tmin;
           b = b < tmax ? b : tmax;
           if (b > a) {
@@ -984,9 +1009,16 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
 #pragma unroll
       for (int a2 = 0; a2 < 3; ++a2) {
         if (D.tn[a2] == tt) {
-          D.c[a2] += D.s[a2];
-          if (D.c[a2] < 0 || D.c[a2] >= D.nb[a2]) done = true;
-          D.tn[a2] = D.plane_t(r, a2, D.c[a2] + (D.s[a2] > 0));
+          if constexpr (SGN >= 0) {
+            const int sg = ((SGN >> a2) & 1) ? 1 : -1;
+            D.c[a2] += sg;
+            if (sg > 0 ? D.c[a2] >= D.nb[a2] : D.c[a2] < 0) done = true;
+            D.tn[a2] = D.plane_t(r, a2, D.c[a2] + (sg > 0 ? 1 : 0));
+          } else {
+            D.c[a2] += D.s[a2];
+            if (D.c[a2] < 0 || D.c[a2] >= D.nb[a2]) done = true;
+            D.tn[a2] = D.plane_t(r, a2, D.c[a2] + (D.s[a2] > 0));
+          }
         }
       }
     }
@@ -1708,6 +1740,29 @@ __global__ void k_brick_grid(const int32_t* __restrict__ coords, const int* __re
   atomicOr(bits + (lin >> 5), 1u << (lin & 31));
 }
 
+// k_segments_brick instantiation for the camera: sign bits when no direction component is 0.
+static void launch_segments_brick(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
+                                  const vs_index_desc& ix, const vs_camera_desc& c,
+                                  const vs_rows_desc& rows, double dt, int2* segs, int* counts,
+                                  int cap, int* flags, int exact_runs) {
+  const dim3 blk(RENDER_TX, RENDER_TY);
+  int sgn = 0;
+  for (int a = 0; a < 3; ++a) {
+    if (c.dir[a] == 0.0) { sgn = -1; break; }
+    if (c.dir[a] > 0.0) sgn |= 1 << a;
+  }
+  switch (sgn) {
+#define VS_SEG_BRICK(S) \
+  case S: k_segments_brick<S><<<grid, blk, 0, st>>>(v, ix, c, rows, dt, segs, counts, cap, flags, exact_runs); break;
+    VS_SEG_BRICK(0) VS_SEG_BRICK(1) VS_SEG_BRICK(2) VS_SEG_BRICK(3)
+    VS_SEG_BRICK(4) VS_SEG_BRICK(5) VS_SEG_BRICK(6) VS_SEG_BRICK(7)
+#undef VS_SEG_BRICK
+    default:
+      k_segments_brick<-1><<<grid, blk, 0, st>>>(v, ix, c, rows, dt, segs, counts, cap, flags,
+                                                  exact_runs);
+  }
+}
+
 template <int K>
 static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                           const vs_index_desc& ix, const vs_camera_desc& c, const float* lut,
@@ -1719,8 +1774,8 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
     int2* segs = static_cast<int2*>(cfg.seg_ws);
     int* counts = reinterpret_cast<int*>(segs + (int64_t)cfg.seg_cap * npix);
     if (K == KIND_LBVH_BRICK && !(cfg.opts & 4))
-      k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-          v, ix, c, rows, dt, segs, counts, cfg.seg_cap, flags, (cfg.opts & 16) ? 1 : 0);
+      launch_segments_brick(grid, st, v, ix, c, rows, dt, segs, counts, cfg.seg_cap, flags,
+                            (cfg.opts & 16) ? 1 : 0);
     else if (K == VS_KIND_GRID && !(cfg.opts & 4))
       k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                   counts, cfg.seg_cap, flags);
@@ -1880,8 +1935,8 @@ int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
       break;
     case VS_KIND_LBVH:
       if (ix->brick_bits && !(cfg.opts & 4))
-        k_segments_brick<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
-            *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, (cfg.opts & 16) ? 1 : 0);
+        launch_segments_brick(grid, st, *vol, *ix, *cam, rows, dt, sg, counts, cap, flags,
+                              (cfg.opts & 16) ? 1 : 0);
       else if (ix->brick_bits)
         k_segments<KIND_LBVH_BRICK><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
             *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
