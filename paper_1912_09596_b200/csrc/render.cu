@@ -1029,7 +1029,9 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
 }
 
 // k_segments specialised for the macro-cell grid (_k_grid: _dda_runs then _sort_merge): the
-// same GridDDA steps, runs and merge as the generic kernel in one flat loop.
+// same GridDDA steps, runs and merge as the generic kernel in one flat loop.  SGN as for
+// k_segments_brick (direction sign bits; -1: general).
+template <int SGN>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
     k_segments_grid(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
                     double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
@@ -1095,11 +1097,22 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
       }
       ++steps;
       if (tn >= tmax) break;
-      if (G.tnx == tn) { cx += G.sx; G.tnx = G.cross(cx, G.sx, r.ox, r.ix); }
-      if (G.tny == tn) { cy += G.sy; G.tny = G.cross(cy, G.sy, r.oy, r.iy); }
-      if (G.tnz == tn) { cz += G.sz; G.tnz = G.cross(cz, G.sz, r.oz, r.iz); }
-      tcur = tn;
-      if (cx < 0 || cy < 0 || cz < 0 || cx >= G.ncx || cy >= ncy || cz >= ncz) break;
+      if constexpr (SGN >= 0) {
+        constexpr int SX = (SGN & 1) ? 1 : -1, SY = (SGN & 2) ? 1 : -1, SZ = (SGN & 4) ? 1 : -1;
+        if (G.tnx == tn) { cx += SX; G.tnx = G.cross(cx, SX, r.ox, r.ix); }
+        if (G.tny == tn) { cy += SY; G.tny = G.cross(cy, SY, r.oy, r.iy); }
+        if (G.tnz == tn) { cz += SZ; G.tnz = G.cross(cz, SZ, r.oz, r.iz); }
+        tcur = tn;
+        if ((SX < 0 ? cx < 0 : cx >= G.ncx) || (SY < 0 ? cy < 0 : cy >= ncy) ||
+            (SZ < 0 ? cz < 0 : cz >= ncz))
+          break;
+      } else {
+        if (G.tnx == tn) { cx += G.sx; G.tnx = G.cross(cx, G.sx, r.ox, r.ix); }
+        if (G.tny == tn) { cy += G.sy; G.tny = G.cross(cy, G.sy, r.oy, r.iy); }
+        if (G.tnz == tn) { cz += G.sz; G.tnz = G.cross(cz, G.sz, r.oz, r.iz); }
+        tcur = tn;
+        if (cx < 0 || cy < 0 || cz < 0 || cx >= G.ncx || cy >= ncy || cz >= ncz) break;
+      }
     }
     if (run) feed(run_t0, tmax);
     if (open) emit(ma, mb);
@@ -1740,18 +1753,39 @@ __global__ void k_brick_grid(const int32_t* __restrict__ coords, const int* __re
   atomicOr(bits + (lin >> 5), 1u << (lin & 31));
 }
 
+// Direction sign bits of the (orthographic, frame-uniform) camera, -1 if a component is 0.
+static int dir_signs(const vs_camera_desc& c) {
+  int sgn = 0;
+  for (int a = 0; a < 3; ++a) {
+    if (c.dir[a] == 0.0) return -1;
+    if (c.dir[a] > 0.0) sgn |= 1 << a;
+  }
+  return sgn;
+}
+
+static void launch_segments_grid(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
+                                 const vs_index_desc& ix, const vs_camera_desc& c,
+                                 const vs_rows_desc& rows, double dt, int2* segs, int* counts,
+                                 int cap, int* flags) {
+  const dim3 blk(RENDER_TX, RENDER_TY);
+  switch (dir_signs(c)) {
+#define VS_SEG_GRID(S) \
+  case S: k_segments_grid<S><<<grid, blk, 0, st>>>(v, ix, c, rows, dt, segs, counts, cap, flags); break;
+    VS_SEG_GRID(0) VS_SEG_GRID(1) VS_SEG_GRID(2) VS_SEG_GRID(3)
+    VS_SEG_GRID(4) VS_SEG_GRID(5) VS_SEG_GRID(6) VS_SEG_GRID(7)
+#undef VS_SEG_GRID
+    default:
+      k_segments_grid<-1><<<grid, blk, 0, st>>>(v, ix, c, rows, dt, segs, counts, cap, flags);
+  }
+}
+
 // k_segments_brick instantiation for the camera: sign bits when no direction component is 0.
 static void launch_segments_brick(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                                   const vs_index_desc& ix, const vs_camera_desc& c,
                                   const vs_rows_desc& rows, double dt, int2* segs, int* counts,
                                   int cap, int* flags, int exact_runs) {
   const dim3 blk(RENDER_TX, RENDER_TY);
-  int sgn = 0;
-  for (int a = 0; a < 3; ++a) {
-    if (c.dir[a] == 0.0) { sgn = -1; break; }
-    if (c.dir[a] > 0.0) sgn |= 1 << a;
-  }
-  switch (sgn) {
+  switch (dir_signs(c)) {
 #define VS_SEG_BRICK(S) \
   case S: k_segments_brick<S><<<grid, blk, 0, st>>>(v, ix, c, rows, dt, segs, counts, cap, flags, exact_runs); break;
     VS_SEG_BRICK(0) VS_SEG_BRICK(1) VS_SEG_BRICK(2) VS_SEG_BRICK(3)
@@ -1777,8 +1811,7 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
       launch_segments_brick(grid, st, v, ix, c, rows, dt, segs, counts, cfg.seg_cap, flags,
                             (cfg.opts & 16) ? 1 : 0);
     else if (K == VS_KIND_GRID && !(cfg.opts & 4))
-      k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                  counts, cfg.seg_cap, flags);
+      launch_segments_grid(grid, st, v, ix, c, rows, dt, segs, counts, cfg.seg_cap, flags);
     else if (K == VS_KIND_KD && !(cfg.opts & 4))
       k_segments_kd<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                 counts, cfg.seg_cap, flags);
@@ -1927,8 +1960,7 @@ int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
       break;
     case VS_KIND_GRID:
       if (!(cfg.opts & 4))
-        k_segments_grid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(*vol, *ix, *cam, rows, dt, sg,
-                                                                counts, cap, flags);
+        launch_segments_grid(grid, st, *vol, *ix, *cam, rows, dt, sg, counts, cap, flags);
       else
         k_segments<VS_KIND_GRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
             *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
