@@ -1201,6 +1201,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
 // each merged leaf interval _dda_runs over the macro grid -> _sort_merge), one flat loop whose
 // turn is either one k-d node visit or one grid DDA step; same steps and merges as the
 // generic generator stack (KdWalk, MergeState, GridDDA).
+template <int SGN>
 __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, 6)
     k_segments_hybrid(vs_volume_desc vol, vs_index_desc ix, vs_camera_desc cam, vs_rows_desc rows,
                       double dt, int2* __restrict__ segs, int* __restrict__ counts, int cap,
@@ -1283,6 +1284,16 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, 6)
           ++gsteps;
           if (tn >= g_out) {
             fin = true;
+          } else if constexpr (SGN >= 0) {  // direction signs known (k_segments_brick)
+            constexpr int SX = (SGN & 1) ? 1 : -1, SY = (SGN & 2) ? 1 : -1,
+                          SZ = (SGN & 4) ? 1 : -1;
+            if (G.tnx == tn) { G.cx += SX; G.tnx = G.cross(G.cx, SX, r.ox, r.ix); }
+            if (G.tny == tn) { G.cy += SY; G.tny = G.cross(G.cy, SY, r.oy, r.iy); }
+            if (G.tnz == tn) { G.cz += SZ; G.tnz = G.cross(G.cz, SZ, r.oz, r.iz); }
+            tcur = tn;
+            if ((SX < 0 ? G.cx < 0 : G.cx >= G.ncx) || (SY < 0 ? G.cy < 0 : G.cy >= G.ncy) ||
+                (SZ < 0 ? G.cz < 0 : G.cz >= G.ncz))
+              fin = true;
           } else {
             if (G.tnx == tn) { G.cx += G.sx; G.tnx = G.cross(G.cx, G.sx, r.ox, r.ix); }
             if (G.tny == tn) { G.cy += G.sy; G.tny = G.cross(G.cy, G.sy, r.oy, r.iy); }
@@ -1779,6 +1790,22 @@ static void launch_segments_grid(dim3 grid, cudaStream_t st, const vs_volume_des
   }
 }
 
+static void launch_segments_hybrid(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
+                                   const vs_index_desc& ix, const vs_camera_desc& c,
+                                   const vs_rows_desc& rows, double dt, int2* segs, int* counts,
+                                   int cap, int* flags) {
+  const dim3 blk(RENDER_TX, RENDER_TY);
+  switch (dir_signs(c)) {
+#define VS_SEG_HYB(S) \
+  case S: k_segments_hybrid<S><<<grid, blk, 0, st>>>(v, ix, c, rows, dt, segs, counts, cap, flags); break;
+    VS_SEG_HYB(0) VS_SEG_HYB(1) VS_SEG_HYB(2) VS_SEG_HYB(3)
+    VS_SEG_HYB(4) VS_SEG_HYB(5) VS_SEG_HYB(6) VS_SEG_HYB(7)
+#undef VS_SEG_HYB
+    default:
+      k_segments_hybrid<-1><<<grid, blk, 0, st>>>(v, ix, c, rows, dt, segs, counts, cap, flags);
+  }
+}
+
 // k_segments_brick instantiation for the camera: sign bits when no direction component is 0.
 static void launch_segments_brick(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                                   const vs_index_desc& ix, const vs_camera_desc& c,
@@ -1816,8 +1843,7 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
       k_segments_kd<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                 counts, cfg.seg_cap, flags);
     else if (K == VS_KIND_HYBRID && !(cfg.opts & 4))
-      k_segments_hybrid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
-                                                                    counts, cfg.seg_cap, flags);
+      launch_segments_hybrid(grid, st, v, ix, c, rows, dt, segs, counts, cfg.seg_cap, flags);
     else
       k_segments<K><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(v, ix, c, rows, dt, segs,
                                                                  counts, cfg.seg_cap, flags,
@@ -1986,8 +2012,7 @@ int vs_render_segments(const vs_volume_desc* vol, const vs_index_desc* ix,
       break;
     case VS_KIND_HYBRID:
       if (!(cfg.opts & 4))
-        k_segments_hybrid<<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(*vol, *ix, *cam, rows, dt, sg,
-                                                                counts, cap, flags);
+        launch_segments_hybrid(grid, st, *vol, *ix, *cam, rows, dt, sg, counts, cap, flags);
       else
         k_segments<VS_KIND_HYBRID><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(
             *vol, *ix, *cam, rows, dt, sg, counts, cap, flags, cfg.trav_budget);
