@@ -137,8 +137,9 @@ __device__ __forceinline__ int bin_fast_bytes(uint32_t w0, uint32_t w1, float fx
   const int bi = (int)fl;
   return bi < 0 ? 0 : (bi > 255 ? 255 : bi);
 }
-// Table variant (f32(u/255) from a shared-memory table): the multi-channel integrator keeps
-// it -- with four channels' filters inlined the byte variant measured 16% slower there.
+// Table variant (f32(u/255) from a shared-memory table; build with VS_BIN_TABLE for A/B).  The
+// byte variant is faster in both integrators once their gathers are software-pipelined (the
+// table's 8 LDS per channel per sample compete with the gathers for L1TEX).
 __device__ __forceinline__ int bin_fast_table(const float* tb, uint32_t w0, uint32_t w1, float fx,
                                               float fy, float fz) {
   const float c000 = tb[w0 & 0xffu], c001 = tb[(w0 >> 8) & 0xffu];
