@@ -110,25 +110,28 @@ __host__ __device__ inline int64_t nzw_of(int nz) { return (nz + 31) >> 5; }
 constexpr float BIN_EDGE = 1e-3f;
 // Byte-domain variant (default): the same test on 255·v evaluated from the raw bytes, so no
 // shared-memory table reads (8 LDS per sample) compete with the gathers for L1TEX.  A byte u
-// becomes the float u by one PRMT into the mantissa of 2^23 (0x4B0000uu) and one FADD of -2^23,
-// both exact; first differences of bytes are exact.  Error of w' = lerp(bytes) + 0.5 against
+// becomes the float 2^23 + u by one PRMT into the mantissa of 2^23 (0x4B0000uu), exact; the
+// first differences of those are the exact byte differences, and one FADD of -2^23 (exact)
+// unbiases each lerp base.  Error of w' = lerp(bytes) + 0.5 against
 // the reference's v*255 + 0.5: table values f32(u/255)*255 vs u <= 1.6e-5, the reference's f32
 // difference roundings x255 <= 7.6e-6 per difference, our three FMA levels on values <= 255.5
 // at 2^-24 relative (1.6e-5 each) and the f32 fractions (<= 255 * 2^-25 = 7.6e-6 per level):
 // < 1.4e-4 in total, well inside BIN_EDGE.
-__device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) {
-  return __fadd_rn(__int_as_float((int)__byte_perm(w, 0x4B000000u, sel)), -8388608.0f);
+__device__ __forceinline__ float byte_b(uint32_t w, uint32_t sel) {  // 2^23 + byte, exact
+  return __int_as_float((int)__byte_perm(w, 0x4B000000u, sel));
 }
 __device__ __forceinline__ int bin_fast_bytes(uint32_t w0, uint32_t w1, float fx, float fy,
                                               float fz) {
-  const float c000 = byte_f(w0, 0x7440), c001 = byte_f(w0, 0x7441);
-  const float c010 = byte_f(w0, 0x7442), c011 = byte_f(w0, 0x7443);
-  const float c100 = byte_f(w1, 0x7440), c101 = byte_f(w1, 0x7441);
-  const float c110 = byte_f(w1, 0x7442), c111 = byte_f(w1, 0x7443);
-  const float c00 = __fmaf_rn(__fsub_rn(c100, c000), fx, c000);
-  const float c10 = __fmaf_rn(__fsub_rn(c110, c010), fx, c010);
-  const float c01 = __fmaf_rn(__fsub_rn(c101, c001), fx, c001);
-  const float c11 = __fmaf_rn(__fsub_rn(c111, c011), fx, c011);
+  // biased corners 2^23 + u: their differences are the exact byte differences, and only the
+  // four x0 corners need the bias removed
+  const float b000 = byte_b(w0, 0x7440), b001 = byte_b(w0, 0x7441);
+  const float b010 = byte_b(w0, 0x7442), b011 = byte_b(w0, 0x7443);
+  const float b100 = byte_b(w1, 0x7440), b101 = byte_b(w1, 0x7441);
+  const float b110 = byte_b(w1, 0x7442), b111 = byte_b(w1, 0x7443);
+  const float c00 = __fmaf_rn(__fsub_rn(b100, b000), fx, __fadd_rn(b000, -8388608.0f));
+  const float c10 = __fmaf_rn(__fsub_rn(b110, b010), fx, __fadd_rn(b010, -8388608.0f));
+  const float c01 = __fmaf_rn(__fsub_rn(b101, b001), fx, __fadd_rn(b001, -8388608.0f));
+  const float c11 = __fmaf_rn(__fsub_rn(b111, b011), fx, __fadd_rn(b011, -8388608.0f));
   const float c0 = __fmaf_rn(__fsub_rn(c10, c00), fy, c00);
   const float c1 = __fmaf_rn(__fsub_rn(c11, c01), fy, c01);
   const float w = __fadd_rn(__fmaf_rn(__fsub_rn(c1, c0), fz, c0), 0.5f);
