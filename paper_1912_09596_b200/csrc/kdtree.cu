@@ -2538,7 +2538,10 @@ __device__ void lv_finish(const LvCtx& X, const KdParams& P, const LvNode& nd, i
     if (sm.cnew[q] >= 0) lv_init_storage(X, sm.cnode[q], nxt);
 }
 
-__global__ void __launch_bounds__(LV_T, 2) k_levels(LvCtx X) {
+#ifndef VS_LV_MINB
+#define VS_LV_MINB 2
+#endif
+__global__ void __launch_bounds__(LV_T, VS_LV_MINB) k_levels(LvCtx X) {
   extern __shared__ __align__(16) unsigned char lv_smem[];
   LvSmem& sm = *reinterpret_cast<LvSmem*>(lv_smem);
   cg::grid_group grid = cg::this_grid();

@@ -409,6 +409,27 @@ def test_brick_run_shortcut_equals_per_brick_slab(vs, dims):
             np.testing.assert_array_equal(o[0], outs[0][0])
 
 
+@pytest.mark.parametrize("kind", ["lbvh", "grid", "hybrid"])
+def test_sign_specialised_traversal_all_octants(vs, kind):
+    """The traversal kernels instantiated per sign pattern of the (frame-uniform) ray direction
+    == the generic generator kernel, for all eight octants and an axis-aligned view (the
+    general instantiation), at odd dims."""
+    rng = np.random.default_rng(5)
+    dims = (70, 53, 96)
+    u8 = (rng.random(dims) * 255).astype(np.uint8)
+    u8[rng.random(dims) < 0.8] = 0
+    v = vs.Volume.from_u8(u8)
+    tf = vs.TransferFunction.ramp(0.5)
+    idx = vs.build_index(kind, vs.classify(v, tf, dilate=True))
+    views = [(az, el) for az in (45.0, 135.0, 225.0, 315.0) for el in (30.0, -30.0)]
+    for az, el in views + [(90.0, 0.0)]:
+        cam = vs.Camera.orbit(v.dims, az, el, width=72, height=60)
+        fast = vs.render_float(v, tf, idx, cam, flags=1)
+        generic = vs.render_float(v, tf, idx, cam, flags=1 | 4)
+        np.testing.assert_array_equal(fast[1], generic[1], err_msg=f"{kind} {az} {el}")
+        np.testing.assert_array_equal(fast[0], generic[0], err_msg=f"{kind} {az} {el}")
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("kind", ["naive", "lbvh", "grid", "hybrid"])
 def test_fp32_bin_filter_equals_fp64_bins(vs, kind):

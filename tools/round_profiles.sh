@@ -38,4 +38,8 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"k_integrate_multi" -c 1 -o gpurun_out/multi_1024 \
   python bench.py --channels 4 --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
-ls -la gpurun_out
+# summaries on the box (the .ncu-rep files exceed what gpurun copies back)
+python tools/round_summaries.py ${ROUND:-r02} gpurun_out/summaries > gpurun_out/summaries.log 2>&1
+mkdir -p gpurun_out/keep; mv gpurun_out/summary_1024.ncu-rep gpurun_out/keep/ 2>/dev/null
+rm -f gpurun_out/*.ncu-rep
+ls -la gpurun_out gpurun_out/summaries

@@ -10,7 +10,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent))
 from ncu_summary import summarise  # noqa: E402
 
 rnd = sys.argv[1]
-G, P = Path("gpurun_out"), Path("profiles")
+G, P = Path("gpurun_out"), Path(sys.argv[2] if len(sys.argv) > 2 else "profiles")
+P.mkdir(parents=True, exist_ok=True)
 
 
 def val(k, name):
