@@ -197,7 +197,9 @@ typedef struct vs_volume_desc {
   const uint32_t* quads;
 } vs_volume_desc;
 
-/* Trilinear gather volume for vs_volume_desc.quads: quads[(x*ny + y)*nz + z] (4 B / voxel). */
+/* Trilinear gather volume for vs_volume_desc.quads: one word per voxel in 4x4x4-voxel tiles
+ * (layout internal to the renderer; size vs_quads_words words, < 2^32). */
+int64_t vs_quads_words(int nx, int ny, int nz);
 int vs_build_quads(const uint8_t* bins, int nx, int ny, int nz, uint32_t* quads,
                    vs_stream_t stream);
 

@@ -58,6 +58,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_cell_boxes": (i32, [P, i32, i32, i32, i32, P, P, P, P]),
     "vs_kd_best_plane": (i32, [P, i32, i32, i32, P, i32, i32, i32, P, P]),
     "vs_build_quads": (i32, [P, i32, i32, i32, P, P]),
+    "vs_quads_words": (i64, [i32, i32, i32]),
     "vs_mquads_words": (i32, [i32]),
     "vs_build_mquads": (i32, [P, i32, i32, i32, i32, P, P]),
     "vs_or_words": (i32, [P, P, i64, P]),

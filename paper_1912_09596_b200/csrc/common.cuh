@@ -94,6 +94,57 @@ __host__ __device__ inline uint32_t morton3(uint32_t x, uint32_t y, uint32_t z) 
   return spread10(x) | (spread10(y) << 1) | (spread10(z) << 2);
 }
 
+// ---- the renderer's trilinear gather ("quad") volume ---------------------------------------
+// One 32-bit word per voxel: its 2x2 (y, z) neighbourhood.  Stored in 4x4x4-voxel tiles (64
+// words = two 128-byte lines of 2x4x4 voxels each, tiles in C order, words in C order inside a
+// tile), so the 32 samples a warp takes at one lattice index -- a small patch of the plane
+// normal to the rays, at any orientation -- touch a few lines instead of one line per (x, y)
+// row, and a ray's next samples stay in the same tiles.  VS_QUAD_LINEAR: plain C order.
+#ifndef VS_QUAD_LINEAR
+#ifndef VS_QT_X
+#define VS_QT_X 2  // log2 tile edge along x, y, z
+#endif
+#ifndef VS_QT_Y
+#define VS_QT_Y 2
+#endif
+#ifndef VS_QT_Z
+#define VS_QT_Z 2
+#endif
+struct QuadGeom {
+  static constexpr uint32_t LX = VS_QT_X, LY = VS_QT_Y, LZ = VS_QT_Z, T = 1u << (LX + LY + LZ);
+  uint32_t ntz, tsx;  // tiles along z; words per x row of tiles
+  __host__ __device__ QuadGeom(int nx, int ny, int nz)
+      : ntz(((uint32_t)nz + (1u << LZ) - 1) >> LZ),
+        tsx((((uint32_t)ny + (1u << LY) - 1) >> LY) * (((uint32_t)nz + (1u << LZ) - 1) >> LZ) * T) {
+    (void)nx;
+  }
+  __host__ __device__ static int64_t words(int nx, int ny, int nz) {
+    return (int64_t)((nx + (1 << LX) - 1) >> LX) * ((ny + (1 << LY) - 1) >> LY) *
+           ((nz + (1 << LZ) - 1) >> LZ) * T;
+  }
+  // word index of voxel (x, y, z): tile part + in-tile part
+  __host__ __device__ uint32_t yz(int y, int z) const {
+    return (((uint32_t)y >> LY) * ntz + ((uint32_t)z >> LZ)) * T +
+           (((uint32_t)y & ((1u << LY) - 1)) << LZ) + ((uint32_t)z & ((1u << LZ) - 1));
+  }
+  __host__ __device__ uint32_t at(int x, uint32_t yzw) const {
+    return ((uint32_t)x >> LX) * tsx + (((uint32_t)x & ((1u << LX) - 1)) << (LY + LZ)) + yzw;
+  }
+};
+#else
+struct QuadGeom {
+  uint32_t ny, nz;
+  __host__ __device__ QuadGeom(int nx, int ny_, int nz_) : ny((uint32_t)ny_), nz((uint32_t)nz_) {
+    (void)nx;
+  }
+  __host__ __device__ static int64_t words(int nx, int ny, int nz) {
+    return (int64_t)nx * ny * nz;
+  }
+  __host__ __device__ uint32_t yz(int y, int z) const { return (uint32_t)y * nz + (uint32_t)z; }
+  __host__ __device__ uint32_t at(int x, uint32_t yzw) const { return (uint32_t)x * ny * nz + yzw; }
+};
+#endif
+
 // Packed bit volume: one 32-bit word per 32 voxels along z; word (x, y, w) at
 // (x*ny + y)*nzw + w, bit z & 31.
 __host__ __device__ inline int64_t nzw_of(int nz) { return (nz + 31) >> 5; }

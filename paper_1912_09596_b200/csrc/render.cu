@@ -221,15 +221,11 @@ struct Integrator {
     const int x0 = min(max(x0r, 0), nx - 1), x1 = min(max(x0r + 1, 0), nx - 1);
     const int y0 = min(max(y0r, 0), ny - 1), z0 = min(max(z0r, 0), nz - 1);
     uint32_t w0, w1;
-    if (IDX32) {  // < 2^32 voxels: 32-bit offsets
-      const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
-      const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
-      w0 = __ldg(quads + ((uint32_t)x0 * sxq + yz));
-      w1 = __ldg(quads + ((uint32_t)x1 * sxq + yz));
-    } else {
-      const int64_t yz = (int64_t)y0 * nz + z0, sxq = (int64_t)ny * nz;
-      w0 = __ldg(quads + (int64_t)x0 * sxq + yz);
-      w1 = __ldg(quads + (int64_t)x1 * sxq + yz);
+    {  // the quad volume has < 2^32 words (vs_render rejects larger volumes for it)
+      const QuadGeom qg(nx, ny, nz);
+      const uint32_t yzw = qg.yz(y0, z0);
+      w0 = __ldg(quads + qg.at(x0, yzw));
+      w1 = __ldg(quads + qg.at(x1, yzw));
     }
     g.w0 = w0;
     g.w1 = w1;
@@ -1750,9 +1746,11 @@ __global__ void k_build_quads(const uint8_t* __restrict__ b, int nx, int ny, int
   if (i >= n) return;
   const int z = (int)(i % nz);
   const int y = (int)((i / nz) % ny);
+  const int x = (int)(i / ((int64_t)ny * nz));
   const int64_t dz = z + 1 < nz ? 1 : 0, dy = y + 1 < ny ? nz : 0;
   const uint32_t v0 = b[i], v1 = b[i + dz], v2 = b[i + dy], v3 = b[i + dy + dz];
-  q[i] = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
+  const QuadGeom qg(nx, ny, nz);
+  q[qg.at(x, qg.yz(y, z))] = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
 }
 
 __global__ void k_brick_grid(const int32_t* __restrict__ coords, const int* __restrict__ n_dev,
@@ -1957,9 +1955,15 @@ int vs_render(const vs_volume_desc* vol, const vs_index_desc* ix, const vs_camer
   return check_launch("k_render");
 }
 
+int64_t vs_quads_words(int nx, int ny, int nz) {
+  if (nx < 1 || ny < 1 || nz < 1) return -1;
+  return QuadGeom::words(nx, ny, nz);
+}
+
 int vs_build_quads(const uint8_t* bins, int nx, int ny, int nz, uint32_t* quads,
                    vs_stream_t stream) {
   if (!bins || !quads || nx < 1 || ny < 1 || nz < 1) return fail_arg("vs_build_quads");
+  if (QuadGeom::words(nx, ny, nz) >= (1LL << 32)) return fail_arg("vs_build_quads: size");
   const int64_t n = (int64_t)nx * ny * nz;
   k_build_quads<<<(unsigned)cdiv(n, 256), 256, 0, S(stream)>>>(bins, nx, ny, nz, quads);
   return check_launch("k_build_quads");

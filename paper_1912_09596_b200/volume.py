@@ -132,12 +132,16 @@ class Volume:
     def is_u8(self) -> bool:
         return self.field is None
 
-    def quads(self) -> torch.Tensor:
-        """Trilinear gather volume (4 B/voxel, TF-independent; vs_build_quads), built once."""
+    def quads(self) -> torch.Tensor | None:
+        """Trilinear gather volume (4 B/voxel in 4^3 tiles, TF-independent; vs_build_quads),
+        built once; None past 2^32 words (the renderer then samples the bins directly)."""
         q = self.__dict__.get("_quads")
         if q is None:
             nx, ny, nz = self._dims
-            q = torch.empty(self._dims, dtype=torch.int32, device=self.bins.device)
+            words = query("vs_quads_words", nx, ny, nz)
+            if words >= 1 << 32:
+                return None
+            q = torch.empty(words, dtype=torch.int32, device=self.bins.device)
             call("vs_build_quads", ptr(self.bins), nx, ny, nz, ptr(q), stream())
             self.__dict__["_quads"] = q
         return q
