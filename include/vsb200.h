@@ -289,8 +289,10 @@ typedef struct vs_multi_desc {
   const uint32_t* mquads;           /* channel-interleaved gather volume (vs_build_mquads) */
 } vs_multi_desc;
 /* Channel-interleaved trilinear gather volume: vs_mquads_words(nch) 32-bit words per voxel
- * (1, 2 or 4), word c = channel c's vs_build_quads word.  bins: nch u8 channel volumes. */
+ * (1, 2 or 4), word c = channel c's vs_build_quads word, voxels in vs_build_quads' tile order
+ * (vs_mquads_size words in all).  bins: nch u8 channel volumes. */
 int vs_mquads_words(int nch);
+int64_t vs_mquads_size(int nch, int nx, int ny, int nz);
 int vs_build_mquads(const uint8_t* const* bins, int nch, int nx, int ny, int nz, uint32_t* out,
                     vs_stream_t stream);
 /* dst[i] |= src[i] (OR of per-channel brick summaries). */

@@ -60,6 +60,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_build_quads": (i32, [P, i32, i32, i32, P, P]),
     "vs_quads_words": (i64, [i32, i32, i32]),
     "vs_mquads_words": (i32, [i32]),
+    "vs_mquads_size": (i64, [i32, i32, i32, i32]),
     "vs_build_mquads": (i32, [P, i32, i32, i32, i32, P, P]),
     "vs_or_words": (i32, [P, P, i64, P]),
     "vs_render_multi_integrate": (i32, [P, P, C.c_double, P, P, P, i32, P, P, P, P, P, P]),

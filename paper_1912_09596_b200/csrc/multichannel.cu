@@ -68,8 +68,11 @@ __global__ void k_build_mquads(const uint8_t* __restrict__ b0, const uint8_t* __
   if (i >= n) return;
   const int z = (int)(i % nz);
   const int y = (int)((i / nz) % ny);
+  const int x = (int)(i / ((int64_t)ny * nz));
   const int64_t dz = z + 1 < nz ? 1 : 0, dy = y + 1 < ny ? nz : 0;
   const uint8_t* bs[4] = {b0, b1, b2, b3};
+  const QuadGeom qg(nx, ny, nz);  // the single-channel gather volume's tiling (common.cuh)
+  const int64_t o = qg.at(x, qg.yz(y, z));
   uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -79,9 +82,9 @@ __global__ void k_build_mquads(const uint8_t* __restrict__ b0, const uint8_t* __
              ((uint32_t)b[i + dy + dz] << 24);
     }
   }
-  if (W == 4) reinterpret_cast<uint4*>(q)[i] = make_uint4(w[0], w[1], w[2], w[3]);
-  else if (W == 2) reinterpret_cast<uint2*>(q)[i] = make_uint2(w[0], w[1]);
-  else q[i] = w[0];
+  if (W == 4) reinterpret_cast<uint4*>(q)[o] = make_uint4(w[0], w[1], w[2], w[3]);
+  else if (W == 2) reinterpret_cast<uint2*>(q)[o] = make_uint2(w[0], w[1]);
+  else q[o] = w[0];
 }
 
 // One sample's gathered quads of every channel at the x0 and x1 planes.
@@ -106,9 +109,9 @@ __device__ __forceinline__ void mc_gather(const vs_multi_desc& md, double ox, do
   const int x0r = (int)flx, y0r = (int)fly, z0r = (int)flz;
   const int x0 = min(max(x0r, 0), nx - 1), x1 = min(max(x0r + 1, 0), nx - 1);
   const int y0 = min(max(y0r, 0), ny - 1), z0 = min(max(z0r, 0), nz - 1);
-  const uint32_t yz = (uint32_t)y0 * (uint32_t)nz + (uint32_t)z0;
-  const uint32_t sxq = (uint32_t)ny * (uint32_t)nz;
-  const uint32_t o0 = (uint32_t)x0 * sxq + yz, o1 = (uint32_t)x1 * sxq + yz;
+  const QuadGeom qg(nx, ny, nz);
+  const uint32_t yzw = qg.yz(y0, z0);
+  const uint32_t o0 = qg.at(x0, yzw), o1 = qg.at(x1, yzw);
   if constexpr (NCH >= 3) {
     const uint4 a = __ldg(reinterpret_cast<const uint4*>(md.mquads) + o0);
     const uint4 b = __ldg(reinterpret_cast<const uint4*>(md.mquads) + o1);
@@ -352,10 +355,16 @@ int vs_render_multi_integrate(const vs_multi_desc* md, const vs_camera_desc* cam
 
 int vs_mquads_words(int nch) { return nch <= 1 ? 1 : (nch == 2 ? 2 : 4); }
 
+int64_t vs_mquads_size(int nch, int nx, int ny, int nz) {
+  if (nch < 1 || nch > MC_MAX || nx < 1 || ny < 1 || nz < 1) return -1;
+  return QuadGeom::words(nx, ny, nz) * vs_mquads_words(nch);
+}
+
 int vs_build_mquads(const uint8_t* const* bins, int nch, int nx, int ny, int nz, uint32_t* out,
                     vs_stream_t stream) {
   if (!bins || !out || nch < 1 || nch > MC_MAX || nx < 1 || ny < 1 || nz < 1)
     return fail_arg("vs_build_mquads");
+  if (QuadGeom::words(nx, ny, nz) >= (1LL << 32)) return fail_arg("vs_build_mquads: size");
   for (int c = 0; c < nch; ++c)
     if (!bins[c]) return fail_arg("vs_build_mquads: channel");
   const uint8_t* b[4] = {bins[0], nch > 1 ? bins[1] : nullptr, nch > 2 ? bins[2] : nullptr,

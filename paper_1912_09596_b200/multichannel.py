@@ -129,8 +129,8 @@ def interleaved_quads(volumes) -> torch.Tensor:
     if hit is not None and all(a is b for a, b in zip(hit[0], volumes)):
         return hit[1]
     nx, ny, nz = volumes[0].dims
-    words = _lib.query("vs_mquads_words", len(volumes))
-    q = torch.empty((nx, ny, nz, words), dtype=torch.int32, device=volumes[0].bins.device)
+    size = _lib.query("vs_mquads_size", len(volumes), nx, ny, nz)
+    q = torch.empty(size, dtype=torch.int32, device=volumes[0].bins.device)
     bins = (C.c_void_p * 4)(*[ptr(v.bins) for v in volumes])
     call("vs_build_mquads", C.addressof(bins), len(volumes), nx, ny, nz, ptr(q), stream())
     cache[key] = (tuple(volumes), q)
