@@ -694,28 +694,20 @@ def run_multi(args, rank, ws, local):
         for tf in tl:
             tf_device(tf, 0.5)
     # two index buffers: frame k+1's union rebuild (side stream) overlaps frame k's render
-    rbs = [LbvhRebuilder(vols, warm=True).capture(), LbvhRebuilder(vols, warm=True).capture()]
+    rbs = [LbvhRebuilder(vols, warm=True).capture()]
     idxs = [r.index() for r in rbs]
     tiles = TileRenderer(W, H)
-    # frames on a high-priority stream, rebuilds / TF changes on default-priority streams
     st = torch.cuda.Stream(priority=-1) if os.environ.get("VSB200_PRIO", "1") == "1" \
         else torch.cuda.current_stream()
     st.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(st):
-        sb = torch.cuda.Stream()
-        built = [torch.cuda.Event(), torch.cuda.Event()]
-        rendered = [torch.cuda.Event(), torch.cuda.Event()]
 
         def step(k, j):
-            b = k % 2
-            with torch.cuda.stream(sb):
-                sb.wait_event(rendered[b])
-                rbs[b].rebuild(params[j])
-                built[b].record(sb)
-            st.wait_event(built[b])
-            img = tiles.render_multi(vols, tfs[j], idxs[b], cams[j], checked=False)
-            rendered[b].record(st)
-            return img
+            # rebuild then render on one stream: a rebuild overlapped on a side stream takes
+            # SM slots from the 118-register 4-channel integrator while it runs and costs the
+            # frame 15% (tools/mc_loop_probe.py; the single-channel frame is indifferent)
+            rbs[0].rebuild(params[j])
+            return tiles.render_multi(vols, tfs[j], idxs[0], cams[j], checked=False)
 
         for k in range(args.warmup):
             step(k, k % NSWEEP)
@@ -728,10 +720,8 @@ def run_multi(args, rank, ws, local):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             tiles.multi_flags()
             e0.record(st)
-            sb.wait_stream(st)
             for k in range(args.steps):
                 step(k, sweep_j(k, args.steps))
-            st.wait_stream(sb)
             e1.record(st)
             torch.cuda.synchronize()
         if tiles.multi_flags() & 4:
