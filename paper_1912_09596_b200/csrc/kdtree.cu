@@ -1846,6 +1846,9 @@ __global__ void k_scatter_sub(const NodeRec* __restrict__ rec, const int* __rest
 // that does not fit the preallocated state (level width, records, storage, extents > 1024)
 // aborts the launch and the host reruns the level-by-level path.
 constexpr int LV_T = 256;
+#ifndef VS_LV_U
+#define VS_LV_U 8  // rows per lane in flight in phase A's vector loads
+#endif
 constexpr int LV_W = LV_T / 32;
 constexpr int LV_NMAX = 1024;   // work nodes per level
 constexpr int LV_EMAX = 1024;   // node extent per axis
@@ -2085,7 +2088,7 @@ __device__ void lv_phase_a(const LvCtx& X, const LvNode* __restrict__ work, int 
       }
       m.x = mk[0]; m.y = mk[1]; m.z = mk[2]; m.w = mk[3];
       uint4 a4 = make_uint4(0u, 0u, 0u, 0u);
-      rows_or_v4<8>(X.bits, X.ny, X.nzw, AX, slab, b.lo[0], b.lo[1], r0, r1, G, g, gw, gmask,
+      rows_or_v4<VS_LV_U>(X.bits, X.ny, X.nzw, AX, slab, b.lo[0], b.lo[1], r0, r1, G, g, gw, gmask,
                     q.v0 + min(wl, q.nv - 1), m, a4, rmin, rmax);
       for (int o = gw; o < 32; o <<= 1) {
         a4.x |= __shfl_xor_sync(0xffffffffu, a4.x, o);
