@@ -371,6 +371,15 @@ __global__ void __launch_bounds__(SCAN_T)
   if (t == 0) off[ntiles] = carry;
 }
 
+// Sampled codes for the Karras searches: every S-th sorted code (S = 2^slog >= 64 so that at most
+// NSAMP samples exist), written by k_leaves_coop and staged in shared memory by k_tree_chunk.
+constexpr int NSAMP = 4096;
+__device__ __forceinline__ int samp_log(int64_t n) {
+  int lg = 6;
+  while (((n + (1LL << lg) - 1) >> lg) > NSAMP) ++lg;
+  return lg;
+}
+
 // Leaves: warp per two 512-code tiles (lane = bitmap word); the warp's leaves are one
 // contiguous run of ranks, staged in shared memory and written row-coalesced.  Also the
 // renderer's C-order leaf-brick bit grid (optional, pre-zeroed) and info {n, height sentinel}.
@@ -382,7 +391,8 @@ __global__ void __launch_bounds__(LV_WARPS * 32)
                   int32_t* __restrict__ hi, int32_t* __restrict__ left,
                   int32_t* __restrict__ right, int32_t* __restrict__ leaf_brick,
                   int32_t* __restrict__ brick_coords, uint32_t* __restrict__ grid,
-                  int* __restrict__ info, int* __restrict__ cross_count) {
+                  int* __restrict__ info, int* __restrict__ cross_count,
+                  uint32_t* __restrict__ samp) {
   __shared__ uint32_t stage[LV_WARPS][1024];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = off[ntiles];
@@ -414,12 +424,14 @@ __global__ void __launch_bounds__(LV_WARPS * 32)
   }
   __syncwarp();
   const int cnt = (int)(P1 - P0);
+  const int slog = samp_log(n);
   for (int k = lane; k < cnt; k += 32) {
     const uint32_t code = stage[warp][k];
     const int64_t p = P0 + k;
     const int bx = (int)compact10(code), by = (int)compact10(code >> 1),
               bz = (int)compact10(code >> 2);
     codes[p] = code;
+    if ((p & ((1LL << slog) - 1)) == 0) samp[p >> slog] = code;
     brick_coords[3 * p] = bx;
     brick_coords[3 * p + 1] = by;
     brick_coords[3 * p + 2] = bz;
@@ -455,6 +467,59 @@ __device__ __forceinline__ int dlt32s(const uint32_t* __restrict__ c, const uint
   return __clz(ci ^ cj);
 }
 
+// The furthest m in [0, M] with clz(ci ^ code[i + m d]) > thr.  The predicate is monotone in m
+// (sorted distinct codes share a shorter prefix with code i the further they are), so this is
+// the index _build_radix_tree's doubling + bisection searches find (lbvh.py:178-196): here a
+// bisection over the shared-memory samples, then one inside an S-wide block (global codes,
+// or the chunk's staged window).
+__device__ __forceinline__ int64_t furthest(const uint32_t* __restrict__ codes,
+                                            const uint32_t* samp, int slog,
+                                            const uint32_t* sc, int64_t cbase, uint32_t ci,
+                                            int64_t i, int d, int64_t M, int thr) {
+  auto code_at = [&](int64_t j) -> uint32_t {
+    const int64_t r = j - cbase;
+    return (r >= 0 && r < 2 * TC) ? sc[r] : __ldg(codes + j);
+  };
+  auto P = [&](uint32_t c) { return (int)__clz(ci ^ c) > thr; };
+  if (M <= 0) return 0;
+  if (d > 0) {
+    const int64_t hi = i + M;
+    // samples strictly after i and <= hi: largest one with P (P holds on a prefix)
+    int64_t k0 = (i >> slog) + 1, k1 = hi >> slog, base = i;
+    if (k0 <= k1 && P(samp[k0])) {
+      while (k0 < k1) {
+        const int64_t mid = (k0 + k1 + 1) >> 1;
+        if (P(samp[mid])) k0 = mid; else k1 = mid - 1;
+      }
+      base = k0 << slog;
+    }
+    const int64_t bend = base + (1LL << slog) - 1;
+    int64_t lo = base, h = hi < bend ? hi : bend;  // P(lo) holds
+    while (lo < h) {
+      const int64_t mid = (lo + h + 1) >> 1;
+      if (P(code_at(mid))) lo = mid; else h = mid - 1;
+    }
+    return lo - i;
+  }
+  const int64_t lo_pos = i - M;
+  // samples strictly before i and >= lo_pos: smallest one with P (P holds on a suffix)
+  int64_t k1 = (i - 1) >> slog, k0 = (lo_pos + (1LL << slog) - 1) >> slog, base = i;
+  if (i > 0 && k0 <= k1 && P(samp[k1])) {
+    while (k0 < k1) {
+      const int64_t mid = (k0 + k1) >> 1;
+      if (P(samp[mid])) k1 = mid; else k0 = mid + 1;
+    }
+    base = k1 << slog;
+  }
+  const int64_t bbeg = base - (1LL << slog) + 1;
+  int64_t lo = lo_pos > bbeg ? lo_pos : bbeg, h = base;  // P(h) holds
+  while (lo < h) {
+    const int64_t mid = (lo + h) >> 1;
+    if (P(code_at(mid))) h = mid; else lo = mid + 1;
+  }
+  return i - h;
+}
+
 // Karras emission (lbvh.py:167-200) for the chunk's internal nodes + in-chunk range boxes.
 __global__ void __launch_bounds__(TC)
     k_tree_chunk(const uint32_t* __restrict__ codes, const int* __restrict__ info, int bs,
@@ -462,7 +527,9 @@ __global__ void __launch_bounds__(TC)
                  int32_t* __restrict__ lo, int32_t* __restrict__ hi, int32_t* __restrict__ left,
                  int32_t* __restrict__ right, int32_t* __restrict__ leaf_brick,
                  uint4* __restrict__ cpre, uint4* __restrict__ csuf, uint4* __restrict__ ctot,
-                 int4* __restrict__ cross, int* __restrict__ cross_count) {
+                 int4* __restrict__ cross, int* __restrict__ cross_count,
+                 const uint32_t* __restrict__ samp_g) {
+  extern __shared__ uint32_t s_samp[];  // NSAMP sampled codes (dynamic shared memory)
   // s_leaf: leaf boxes; s_sp[L-1][i]: union of leaves [i, i + 2^L) of i's warp block (clipped to
   // the block), L = 1..4, so any in-block range is two lookups; s_tl[L][w]: the same over the
   // warp-block totals (L = 0: the totals)
@@ -478,6 +545,10 @@ __global__ void __launch_bounds__(TC)
     return box_union(s_sp[L - 1][a], s_sp[L - 1][e - (1 << L) + 1]);
   };
   const int64_t nchunks = (n + TC - 1) / TC;
+  const int slog = samp_log(n);
+  const int64_t nsamp = (n + (1LL << slog) - 1) >> slog;
+  if (blockIdx.x < nchunks)
+    for (int k = t; k < nsamp; k += TC) s_samp[k] = __ldg(samp_g + k);
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t c0 = ch * TC, c1 = (c0 + TC < n) ? c0 + TC : n;
     const int64_t p = c0 + t;
@@ -546,19 +617,13 @@ __global__ void __launch_bounds__(TC)
       const uint32_t ci = s_code[TC / 2 + t];
       const int d = dlt32s(codes, s_code, cbase, ci, i + 1, n) > dlt32s(codes, s_code, cbase, ci, i - 1, n) ? 1 : -1;
       const int dmin = dlt32s(codes, s_code, cbase, ci, i - d, n);
-      int64_t lmax = 2;
-      while (dlt32s(codes, s_code, cbase, ci, i + lmax * d, n) > dmin) lmax *= 2;
-      int64_t l = 0;
-      for (int64_t s = lmax / 2; s >= 1; s /= 2)
-        if (dlt32s(codes, s_code, cbase, ci, i + (l + s) * d, n) > dmin) l += s;
+      // the far end j (furthest index with delta > dmin) and the split s (furthest with
+      // delta > delta(i, j)): the same indices as the doubling / bisection of lbvh.py:178-196
+      const int64_t l = furthest(codes, s_samp, slog, s_code, cbase, ci, i, d,
+                                 d > 0 ? n - 1 - i : i, dmin);
       const int64_t j = i + l * d;
       const int dnode = dlt32s(codes, s_code, cbase, ci, j, n);
-      int64_t s = 0, st = l;
-      while (true) {
-        st = (st + 1) / 2;
-        if (dlt32s(codes, s_code, cbase, ci, i + (s + st) * d, n) > dnode) s += st;
-        if (st == 1) break;
-      }
+      const int64_t s = furthest(codes, s_samp, slog, s_code, cbase, ci, i, d, l, dnode);
       const int64_t gamma = i + s * d + min(d, 0);
       const int64_t a = min(i, j), e = max(i, j);
       left[i] = (int32_t)(a == gamma ? (n - 1) + gamma : gamma);
@@ -693,7 +758,8 @@ using namespace vs;
 extern "C" {
 
 static size_t bitmap_ws(int P, int64_t cap, uint32_t** off, uint32_t** codes, uint4** cpre,
-                        uint4** csuf, uint4** ctot, int4** cross, int** ccount, void* base) {
+                        uint4** csuf, uint4** ctot, int4** cross, int** ccount, uint32_t** samp,
+                        void* base) {
   const int64_t ntiles = (int64_t)P * P * P / 512;
   Bump b(base);
   uint32_t* o = b.take<uint32_t>(ntiles + 1);
@@ -705,13 +771,17 @@ static size_t bitmap_ws(int P, int64_t cap, uint32_t** off, uint32_t** codes, ui
   uint4* tt = b.take<uint4>(cdiv(std::max<int64_t>(cap, 1), TC));
   int4* cr = b.take<int4>(std::max<int64_t>(cap, 1));
   int* cc = b.take<int>(1);
-  if (off) { *off = o; *codes = c; *cpre = pr; *csuf = sf; *ctot = tt; *cross = cr; *ccount = cc; }
+  uint32_t* sp = b.take<uint32_t>(NSAMP);
+  if (off) {
+    *off = o; *codes = c; *cpre = pr; *csuf = sf; *ctot = tt; *cross = cr; *ccount = cc;
+    *samp = sp;
+  }
   return b.off + 256;
 }
 
 size_t vs_lbvh_workspace(int P, int64_t cap) {
   return bitmap_ws(P, cap, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                   nullptr);
+                   nullptr, nullptr);
 }
 
 int vs_lbvh_from_bitmap(const uint32_t* bitmap, const uint32_t* tile_counts, int P, int bs,
@@ -729,7 +799,8 @@ int vs_lbvh_from_bitmap(const uint32_t* bitmap, const uint32_t* tile_counts, int
   uint4 *cpre, *csuf, *ctot;
   int4* cross;
   int* ccount;
-  bitmap_ws(P, cap, &off, &codes, &cpre, &csuf, &ctot, &cross, &ccount, ws);
+  uint32_t* samp;
+  bitmap_ws(P, cap, &off, &codes, &cpre, &csuf, &ctot, &cross, &ccount, &samp, ws);
   if (ntiles <= (int64_t)SCAN_T * SCAN_PER) {
     k_tile_scan<<<1, SCAN_T, 0, st>>>(tile_counts, ntiles, off);
     VS_TRY(check_launch("k_tile_scan"));
@@ -749,13 +820,16 @@ int vs_lbvh_from_bitmap(const uint32_t* bitmap, const uint32_t* tile_counts, int
   const int64_t pairs = cdiv(ntiles, 2);
   k_leaves_coop<<<(unsigned)cdiv(pairs, LV_WARPS), LV_WARPS * 32, 0, st>>>(
       bitmap, off, bs, nx, ny, nz, nby, nbz, ntiles, codes, lo, hi, left, right, leaf_brick,
-      brick_coords, brick_grid, info, ccount);
+      brick_coords, brick_grid, info, ccount, samp);
   VS_TRY(check_launch("k_leaves_coop"));
   const int nsm = sm_count();
   const int64_t grid = std::min<int64_t>(cdiv(cap, TC), (int64_t)nsm * 4);
-  k_tree_chunk<<<(unsigned)std::max<int64_t>(grid, 1), TC, 0, st>>>(
+  const int samp_bytes = NSAMP * 4;
+  VS_CUDA(cudaFuncSetAttribute(k_tree_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               samp_bytes), "k_tree_chunk smem");
+  k_tree_chunk<<<(unsigned)std::max<int64_t>(grid, 1), TC, samp_bytes, st>>>(
       codes, info, bs, nx, ny, nz, brick_coords, lo, hi, left, right, leaf_brick, cpre, csuf, ctot,
-      cross, ccount);
+      cross, ccount, samp);
   VS_TRY(check_launch("k_tree_chunk"));
   k_tree_cross<<<(unsigned)nsm, 256, 0, st>>>(cross, ccount, bs, nx, ny, nz, cpre, csuf, ctot,
                                                lo, hi);
