@@ -898,6 +898,42 @@ __global__ void __launch_bounds__(FL_T)
   }
 }
 
+// The warm vote straight from the presence masks in C order (no cells requested, nbz % 32 == 0):
+// CTA per brick row (bx, by), thread per bz.  Loads are one 32-byte mask per thread, row-
+// contiguous; the renderer's C-order brick bits are the warps' ballots; the Morton bitmap and its
+// tile counts (pre-zeroed) take one atomicOr / atomicAdd per flagged brick (~10% of them).
+__global__ void __launch_bounds__(256)
+    k_presence_vote(const uint32_t* const* __restrict__ chans,
+                    const int32_t* __restrict__ tf_params, int nch, int nby, int nbz,
+                    uint32_t* __restrict__ bitmap, uint32_t* __restrict__ tile_counts,
+                    uint32_t* __restrict__ grid) {
+  __shared__ uint32_t s_vis[4][8];
+  const int t = threadIdx.x;
+  if (t < 8 * nch) s_vis[t >> 3][t & 7] = tf_params[16 * (t >> 3) + (t & 7)];
+  __syncthreads();
+  const int row = blockIdx.y, bx = row / nby, by = row - (row / nby) * nby;
+  const int bz = blockIdx.x * blockDim.x + t;
+  uint32_t f = 0;
+  const int64_t lin = (int64_t)row * nbz + bz;
+  if (bz < nbz) {
+    for (int c = 0; c < nch; ++c) {
+      const uint4* pp = reinterpret_cast<const uint4*>(chans[c] + lin * 8);
+      const uint4 a = __ldcs(pp), b = __ldcs(pp + 1);
+      f |= (a.x & s_vis[c][0]) | (a.y & s_vis[c][1]) | (a.z & s_vis[c][2]) |
+           (a.w & s_vis[c][3]) | (b.x & s_vis[c][4]) | (b.y & s_vis[c][5]) |
+           (b.z & s_vis[c][6]) | (b.w & s_vis[c][7]);
+    }
+  }
+  const uint32_t ball = __ballot_sync(0xffffffffu, f != 0u);
+  if (grid && (t & 31) == 0 && bz < nbz) grid[lin >> 5] = ball;
+  if (f) {
+    const uint32_t code = spread10((uint32_t)bx) | (spread10((uint32_t)by) << 1) |
+                          (spread10((uint32_t)bz) << 2);
+    atomicOr(bitmap + (code >> 5), 1u << (code & 31));
+    atomicAdd(tile_counts + (code >> 9), 1u);
+  }
+}
+
 // Per-volume 256-bit presence mask of every 8^3 brick's 1-voxel halo (the TF-independent warm
 // path of the brick vote: a TF change then reads 32 B per brick instead of the volume).  CTA
 // per (bx, by) brick column; each thread takes 16-byte z chunks of the column's 10 x 10 halo
@@ -1186,6 +1222,14 @@ static int flags_tiles(int mode, const uint32_t* src, const uint32_t* const* cha
     VS_CUDA(cudaMemsetAsync(grid, 0, ((nb + 31) / 32) * 4, st), "memset brick grid");
   else if (grid && (nb & 31) != 0)  // padding bits of the last word (never stored by bytes)
     VS_CUDA(cudaMemsetAsync(grid + nb / 32, 0, 4, st), "memset brick grid tail");
+  if (mode == FL_PRESENCE && !cell16 && (nbz & 31) == 0 && (int64_t)nbx * nby <= 65535) {
+    VS_CUDA(cudaMemsetAsync(bitmap, 0, ntiles * 16 * 4, st), "memset bitmap");
+    VS_CUDA(cudaMemsetAsync(tile_counts, 0, ntiles * 4, st), "memset tile counts");
+    const int bt = nbz >= 256 ? 256 : nbz;
+    k_presence_vote<<<dim3((unsigned)cdiv(nbz, bt), (unsigned)(nbx * nby)), bt, 0, st>>>(
+        chans, tf_params, nch, nby, nbz, bitmap, tile_counts, grid);
+    return check_launch("k_presence_vote");
+  }
   const unsigned g = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * 8);
   if (mode == FL_SUMMARY_DILATE)
     k_flags_tiles<FL_SUMMARY_DILATE><<<g, FL_T, 0, st>>>(src, chans, tf_params, nch, nbx, nby, nbz,
