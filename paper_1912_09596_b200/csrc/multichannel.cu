@@ -140,8 +140,11 @@ __device__ __forceinline__ void mc_settle(McGather<NCH>& g) {
   }
 }
 
+#ifndef VS_MC_MINB
+#define VS_MC_MINB 1
+#endif
 template <int NCH>
-__global__ void __launch_bounds__(MC_TX* MC_TY)
+__global__ void __launch_bounds__(MC_TX* MC_TY, VS_MC_MINB)
     k_integrate_multi(vs_multi_desc md, vs_camera_desc cam, double dt, vs_rows_desc rows,
                       const int2* __restrict__ segs, const int* __restrict__ counts, int cap,
                       uint8_t* __restrict__ rgba8, double* __restrict__ rgba64,

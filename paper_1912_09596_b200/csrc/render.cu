@@ -26,7 +26,7 @@
 
 // Minimum resident blocks per SM for the two render kernels (register caps; tuned on B200).
 #ifndef VS_INTEGRATE_MINB
-#define VS_INTEGRATE_MINB 6
+#define VS_INTEGRATE_MINB 7
 #endif
 #ifndef VS_SEGMENTS_MINB
 #define VS_SEGMENTS_MINB 8
