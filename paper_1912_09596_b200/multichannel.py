@@ -24,9 +24,6 @@ from .render import (Camera, Frame, RowsDesc, _check_flags, camera_desc, index_d
                      volume_desc)
 from .volume import BinaryVolume, TransferFunction, Volume, _nzw, presence_table
 
-# channel pointer tables of the warm vote, per channel set (pointers re-checked on use)
-_TABLES: dict = {}
-
 
 class MultiBinaryVolume(BinaryVolume):
     """Lazy union classification of several channels."""
@@ -60,13 +57,16 @@ class MultiBinaryVolume(BinaryVolume):
         warm = dilate and self._summary is None and len(vols) <= 4 and \
             all([v._warm_vote() for v in vols])
         if warm:
+            # the channel pointer table, cached on the first channel per channel tuple (as
+            # interleaved_quads caches its volume)
+            cache = vols[0].__dict__.setdefault("_presence_tabs", {})
             key = tuple(id(v) for v in vols)
-            tab = _TABLES.get(key)
-            if tab is None or tab[0] != [v.presence().data_ptr() for v in vols]:
-                tab = ([v.presence().data_ptr() for v in vols], presence_table(vols))
-                _TABLES[key] = tab
+            hit = cache.get(key)
+            if hit is None or not all(a is b for a, b in zip(hit[0], vols)):
+                hit = (tuple(vols), presence_table(vols))
+                cache[key] = hit
             params = torch.cat([tf.params() for tf in tfs])
-            call("vs_presence_to_bitmap", ptr(tab[1]), ptr(params), len(vols), nx, ny, nz, P,
+            call("vs_presence_to_bitmap", ptr(hit[1]), ptr(params), len(vols), nx, ny, nz, P,
                  ptr(bitmap), ptr(tiles), ptr(cell16), ptr(grid), stream())
         else:
             call("vs_summary_to_bitmap", ptr(self.summary()), nx, ny, nz, int(dilate), P,
