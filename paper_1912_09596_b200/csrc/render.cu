@@ -1445,7 +1445,7 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
                          const int* __restrict__ counts, int cap, uint8_t* __restrict__ rgba8,
                          double* __restrict__ rgba64, int32_t* __restrict__ samples,
                          unsigned long long* __restrict__ total, int* __restrict__ flags_out,
-                         double ert_a, int bin_filter) {
+                         double ert_a) {
   __shared__ RenderSmem sm;
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
   load_tables(sm, lut, corr, tid, RENDER_TX * RENDER_TY);
@@ -1500,8 +1500,9 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_INTEGRATE_MINB)
         };
         auto shade = [&](Integrator::Gather& g) {
           Integrator::settle(g);
-          // bin_filter 0: every sample through the FP64 path (tests the filter's exactness)
-          int bin = bin_filter ? I.bin_fast(g) : -1;
+          // (render option RO_FP64_BINS sends every ray to k_integrate_fallback instead: all
+          // samples through the FP64 path, the check of this filter's exactness)
+          int bin = I.bin_fast(g);
           if (bin < 0) bin = Integrator::bin_of(I.interp_t<true>(g));
           // I.shade_bin(bin) on the kernel's shared tables, addressed from 32-bit shared
           // offsets taken once (the generic path re-derives the CTA's window every sample)
@@ -1580,7 +1581,8 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY)
                          int render_opts, double ert_a) {
   __shared__ RenderSmem sm;
   const int tid = threadIdx.y * RENDER_TX + threadIdx.x;
-  const bool generic = vol.field || !vol.quads || nearest;
+  // RO_FP64_BINS (render_opts & 2): every ray here, sampled with the FP64 arithmetic only
+  const bool generic = vol.field || !vol.quads || nearest || (render_opts & 2);
   const int i = blockIdx.x * RENDER_TX + threadIdx.x;
   const int l = blockIdx.y * RENDER_TY + threadIdx.y;
   const bool inside = i < cam.width && l < rows.nrows;
@@ -1847,12 +1849,13 @@ static void launch_render(dim3 grid, cudaStream_t st, const vs_volume_desc& v,
                                                                  counts, cfg.seg_cap, flags,
                                                                  cfg.trav_budget);
     const bool idx32 = (int64_t)v.nx * v.ny * v.nz < (1LL << 32), ert = cfg.ert_a <= 1.0;
-    const bool lean = !v.field && v.quads && !nearest;  // k_integrate_segments' rays exist
+    // k_integrate_segments' rays exist (RO_FP64_BINS: all rays to the fallback kernel)
+    const bool lean = !v.field && v.quads && !nearest && !(cfg.opts & 2);
     if (lean) {
 #define VS_INTEGRATE(I32, E)                                                                  \
   k_integrate_segments<K, I32, E><<<grid, dim3(RENDER_TX, RENDER_TY), 0, st>>>(               \
       v, ix, c, lut, corr, dt, rows, segs, counts, cfg.seg_cap, rgba8, rgba64, samples, total,  \
-      flags, cfg.ert_a, (cfg.opts & 2) ? 0 : 1)
+      flags, cfg.ert_a)
       if (idx32) {
         if (ert) VS_INTEGRATE(true, true); else VS_INTEGRATE(true, false);
       } else {
