@@ -967,15 +967,18 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
     // the very plane expressions the DDA's crossings use -- so the merged run just extends to
     // min(next crossing, tmax) and the brick's slab() is skipped (exact_runs: always slab()).
     bool live = false;
+    // "interior" (box not clipped to dims) <=> c <= dims / bs - 1 per axis: limits from the
+    // kernel parameters (uniform), so no per-step multiplies
+    const int ci0 = vol.nx / ix.bs - 1, ci1 = vol.ny / ix.bs - 1, ci2 = vol.nz / ix.bs - 1;
     while (!done) {
       if (steps++ >= maxsteps) break;
       const int lin = (D.c[0] * nby + D.c[1]) * nbz + D.c[2];
       const bool occ = (__ldg(bits + (lin >> 5)) >> (lin & 31)) & 1u;
-      const int l0 = D.c[0] * bs, l1 = D.c[1] * bs, l2 = D.c[2] * bs;
-      const bool interior = l0 + bs <= D.dims[0] && l1 + bs <= D.dims[1] && l2 + bs <= D.dims[2];
+      const bool interior = D.c[0] <= ci0 && D.c[1] <= ci1 && D.c[2] <= ci2;
       const bool shortcut = occ && live && interior && !exact_runs;
       if (occ && !shortcut) {
         double a, b;
+        const int l0 = D.c[0] * bs, l1 = D.c[1] * bs, l2 = D.c[2] * bs;
         const double h0 = (double)min(l0 + bs, D.dims[0]), h1 = (double)min(l1 + bs, D.dims[1]),
                      h2 = (double)min(l2 + bs, D.dims[2]);
         if (SGN >= 0 ? slab_nz(r, (double)l0, (double)l1, (double)l2, h0, h1, h2, a, b)
