@@ -971,7 +971,11 @@ __global__ void __launch_bounds__(RENDER_TX* RENDER_TY, VS_SEGMENTS_MINB)
     // kernel parameters (uniform), so no per-step multiplies
     const int ci0 = vol.nx / ix.bs - 1, ci1 = vol.ny / ix.bs - 1, ci2 = vol.nz / ix.bs - 1;
     while (!done) {
-      if (steps++ >= maxsteps) break;
+      // (a step advances at least one axis by one brick, so with every direction component
+      // nonzero the walk leaves the grid within sum(nb) steps: the guard is for SGN = -1)
+      if constexpr (SGN < 0) {
+        if (steps++ >= maxsteps) break;
+      }
       const int lin = (D.c[0] * nby + D.c[1]) * nbz + D.c[2];
       const bool occ = (__ldg(bits + (lin >> 5)) >> (lin & 31)) & 1u;
       const bool interior = D.c[0] <= ci0 && D.c[1] <= ci1 && D.c[2] <= ci2;
