@@ -942,6 +942,73 @@ __global__ void k_cell_boxes(const uint32_t* __restrict__ bits, int nx, int ny, 
   cells[i] = c;
 }
 
+// 8^3 cells (the binned builder's default): warp per (cell column cx, cy; 32 z words), lane
+// = one z word = four cells.  The 64 rows of the column stream through coalesced loads; the
+// cells' x / y / z occupancy comes out of per-byte "any" masks (SWAR), no per-voxel work.
+__device__ __forceinline__ uint32_t bytes_any(uint32_t v) {  // 0x80 per nonzero byte
+  return (((v & 0x7f7f7f7fu) + 0x7f7f7f7fu) | v) & 0x80808080u;
+}
+__global__ void __launch_bounds__(256) k_cell_boxes8(const uint32_t* __restrict__ bits, int nx,
+                                                     int ny, int nz, int ncx, int ncy, int ncz,
+                                                     CBox* __restrict__ cells) {
+  const int nzw = (int)nzw_of(nz), nch = (nzw + 31) >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= (int64_t)ncx * ncy * nch) return;
+  const int lane = threadIdx.x & 31;
+  const int ch = (int)(warp % nch);
+  const int cy = (int)((warp / nch) % ncy), cx = (int)(warp / ((int64_t)nch * ncy));
+  const int w = 32 * ch + lane;
+  if (w >= nzw) return;
+  const uint32_t zm = nz - 32 * w >= 32 ? 0xffffffffu : (1u << (nz - 32 * w)) - 1u;
+  const int x0 = 8 * cx, y0 = 8 * cy;
+  const int lxn = min(8, nx - x0), lyn = min(8, ny - y0);
+  uint32_t oy[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t xm = 0;
+  for (int lx = 0; lx < lxn; ++lx) {
+    const uint32_t* row = bits + ((int64_t)(x0 + lx) * ny + y0) * nzw + w;
+    uint32_t v[8];
+#pragma unroll
+    for (int ly = 0; ly < 8; ++ly) v[ly] = ly < lyn ? __ldg(row + (int64_t)ly * nzw) & zm : 0u;
+    uint32_t ox = 0;
+#pragma unroll
+    for (int ly = 0; ly < 8; ++ly) { ox |= v[ly]; oy[ly] |= v[ly]; }
+    xm |= (bytes_any(ox) >> 7) << lx;
+  }
+  uint32_t ym = 0, zo = 0;
+#pragma unroll
+  for (int ly = 0; ly < 8; ++ly) { ym |= (bytes_any(oy[ly]) >> 7) << ly; zo |= oy[ly]; }
+  CBox* out = cells + ((int64_t)cx * ncy + cy) * ncz;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int cz = 4 * w + k;
+    if (cz >= ncz) break;
+    const uint32_t zb = (zo >> (8 * k)) & 0xffu;
+    CBox c;
+    if (zb) {
+      const uint32_t xb = (xm >> (8 * k)) & 0xffu, yb = (ym >> (8 * k)) & 0xffu;
+      c.lo[0] = x0 + __ffs(xb) - 1; c.hi[0] = x0 + 32 - __clz(xb);
+      c.lo[1] = y0 + __ffs(yb) - 1; c.hi[1] = y0 + 32 - __clz(yb);
+      c.lo[2] = 8 * cz + __ffs(zb) - 1; c.hi[2] = 8 * cz + 32 - __clz(zb);
+    } else {
+      for (int j = 0; j < 3; ++j) { c.lo[j] = KD_FAR; c.hi[j] = -1; }
+    }
+    out[cz] = c;
+  }
+}
+
+int launch_cell_boxes(const uint32_t* bits, int nx, int ny, int nz, int cs, int ncx, int ncy,
+                      int ncz, CBox* cells, cudaStream_t st) {
+  if (cs == 8) {
+    const int64_t warps = (int64_t)ncx * ncy * ((nzw_of(nz) + 31) >> 5);
+    k_cell_boxes8<<<(unsigned)cdiv(warps * 32, 256), 256, 0, st>>>(bits, nx, ny, nz, ncx, ncy,
+                                                                    ncz, cells);
+  } else {
+    k_cell_boxes<<<(unsigned)cdiv((int64_t)ncx * ncy * ncz, 128), 128, 0, st>>>(
+        bits, nx, ny, nz, cs, ncx, ncy, ncz, cells);
+  }
+  return check_launch("k_cell_boxes");
+}
+
 // Cell-slab unions along axis A: warp per (node, cell slab c in the node's cell range, chunk
 // of CELL_CHUNK cells of the slab); chunked slabs merge into initialised unions with atomics.
 __global__ void __launch_bounds__(256) k_cell_slabs(const CBox* __restrict__ cells, int ncx,
@@ -3053,9 +3120,7 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
       if (level == 0) {
         const int64_t ncell = (int64_t)ncx * ncy * ncz;
         VS_TRY(cellb.ensure(ncell * sizeof(CBox), "cells"));
-        k_cell_boxes<<<(unsigned)cdiv(ncell, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy,
-                                                                 ncz, cellb.as<CBox>());
-        VS_TRY(check_launch("k_cell_boxes"));
+        VS_TRY(launch_cell_boxes(bits, nx, ny, nz, cs, ncx, ncy, ncz, cellb.as<CBox>(), st));
       }
       B.cells = cellb.as<CBox>();
       const int64_t t0 = tot[A_C0], t1 = tot[A_C1], t2 = tot[A_C2];
@@ -3378,9 +3443,7 @@ int vs_cell_boxes(const uint32_t* bits, int nx, int ny, int nz, int cs, int32_t*
   DBuf cells;
   cells.st = st;
   VS_TRY(cells.ensure(n * sizeof(CBox), "cells"));
-  k_cell_boxes<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy, ncz,
-                                                       cells.as<CBox>());
-  VS_TRY(check_launch("k_cell_boxes"));
+  VS_TRY(launch_cell_boxes(bits, nx, ny, nz, cs, ncx, ncy, ncz, cells.as<CBox>(), st));
   k_cell_box_rows<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(cells.as<CBox>(), ncx, ncy, ncz, cs, lo,
                                                           hi, occupied);
   VS_TRY(check_launch("k_cell_box_rows"));
@@ -3474,8 +3537,7 @@ int vs_kd_best_plane(const uint32_t* bits, int nx, int ny, int nz, const int* bo
   } else {
     const int64_t ncell = (int64_t)ncx * ncy * ncz;
     VS_TRY(cellb.ensure(ncell * sizeof(CBox), "cells"));
-    k_cell_boxes<<<(unsigned)cdiv(ncell, 128), 128, 0, st>>>(bits, nx, ny, nz, cs, ncx, ncy, ncz,
-                                                             cellb.as<CBox>());
+    VS_TRY(launch_cell_boxes(bits, nx, ny, nz, cs, ncx, ncy, ncz, cellb.as<CBox>(), st));
     B.cells = cellb.as<CBox>();
     VS_TRY(cslab.ensure((csz[0] + csz[1] + csz[2] + 3) * sizeof(CBox), "cell slabs"));
     CBox* cs3[3] = {cslab.as<CBox>(), cslab.as<CBox>() + csz[0] + 1,

@@ -152,6 +152,19 @@ def test_precompute_cell_boxes(vs, bitcases, case):
         np.testing.assert_array_equal(getattr(cells, f), bitcases[f"{case}_cells8_{f}"], err_msg=f)
 
 
+@pytest.mark.parametrize("dims,cs", [((37, 29, 45), 8), ((16, 8, 96), 8), ((70, 9, 1030), 8),
+                                     ((33, 20, 41), 5), ((40, 40, 40), 16)])
+def test_cell_boxes_ragged_vs_oracle(vs, rng, dims, cs):
+    """k_cell_boxes8 (cs 8: warp per cell column, byte masks) and the generic per-cell kernel
+    on ragged dims (partial cells on every axis, nz past one 32-word chunk) vs the oracle."""
+    bits = rng.random(dims) < 0.004
+    bits[:, :, -1] |= rng.random(dims[:2]) < 0.05  # flags in the last (partial) z word
+    cells = vs.precompute_cell_boxes(vs.BinaryVolume(bits), cs)
+    want = O.cell_boxes(bits, cs)
+    for f in ("codes", "coords", "lo", "hi", "occupied"):
+        np.testing.assert_array_equal(getattr(cells, f), want[f], err_msg=f)
+
+
 def test_best_plane_apis_vs_reference_semantics(vs, rng):
     """sweep_best_plane / binned_best_plane on random boxes: the split the k-d builder takes
     at a root equals the single-box search, and the two-cluster known answer
