@@ -77,6 +77,9 @@ enum {
 
 // Cells one cell-slab work item reduces (chunks of a big slab merge with atomics).
 constexpr int CELL_CHUNK = 1024;
+#ifndef VS_CS_CU
+#define VS_CS_CU 1  // k_cell_slabs: cells in flight per lane
+#endif
 
 // Rows one x/y-pass work item covers (a node's slab is split into chunks of this many rows so
 // the top levels of a big volume still spread over every SM; chunks merge with atomics).
@@ -615,8 +618,8 @@ __device__ __forceinline__ void node_cell_range(const Box& b, int cs, const int*
 }
 
 // _cells_reduce(region) for a region inside node box b (uses the axis-a slab unions).
-__device__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a, const Box& region,
-                             int cs, int lane, Box& out) {
+__device__ __forceinline__ bool cells_reduce(const BinnedCtx& B, int i, const Box& node, int a,
+                                             const Box& region, int cs, int lane, Box& out) {
   int n0, n1;
   node_cell_range(node, cs, B.nc, a, n0, n1);
   // region's cell range along a (kdtree.py:329-331), clamped like the reference
@@ -831,6 +834,16 @@ __global__ void __launch_bounds__(DT) k_decide(KdLevel L, KdParams P,
 }
 
 // ---- binned decisions: one warp per node (kdtree.py:353-368, 441-467) ----------------------
+// CS = 8: the default 8^3 cells as a compile-time constant (the cell-coordinate divisions
+// become shifts) and, for bins <= 8, the candidate cuts generated in registers in ascending
+// order (the snapped raster is monotone in j, so the reference's sort is the identity and its
+// de-duplication is "differs from the previous accepted cut"); divisions by powers of two in
+// _snapped_positions are exact multiplications.  CS = 0: any cell size / bin count.
+__device__ __forceinline__ double div_exact(double x, int d) {
+  return (d & (d - 1)) == 0 ? __dmul_rn(x, 1.0 / (double)d) : __ddiv_rn(x, (double)d);
+}
+
+template <int CS>
 __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, BinnedCtx B,
                                                        KdDecision* __restrict__ out,
                                                        int64_t* __restrict__ child_count) {
@@ -843,15 +856,16 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
   KdDecision d;
   d.axis = -1; d.plane = -1; d.nchild = 0; d.dropped = 0; d.sub = -1; d.leaf = b;
   bool split = false;
+  const int cs = CS ? CS : P.cs;
   int nlo[3], nhi[3];
-  for (int k = 0; k < 3; ++k) node_cell_range(b, P.cs, B.nc, k, nlo[k], nhi[k]);
+  for (int k = 0; k < 3; ++k) node_cell_range(b, cs, B.nc, k, nlo[k], nhi[k]);
   const bool small =
       (nhi[0] - nlo[0] + 1) * (nhi[1] - nlo[1] + 1) * (nhi[2] - nlo[2] + 1) <= SMALL_CELLS;
   SmallCells SC;
-  if (small) SC.load(B, b, P.cs, lane);
+  if (small) SC.load(B, b, cs, lane);
   auto reduce = [&](int a, const Box& region, Box& o) {
-    return small ? SC.reduce(B, a, region, P.cs, o)
-                 : cells_reduce(B, i, b, a, region, P.cs, lane, o);
+    return small ? SC.reduce(B, a, region, cs, o)
+                 : cells_reduce(B, i, b, a, region, cs, lane, o);
   };
   if (!halted(P, vol)) {
     // first strict minimum over (axis, position)
@@ -859,17 +873,37 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
     int64_t bc = 0;
     Box bl, br;
     bool hl = false, hr = false;
-    for (int a = 0; a < 3; ++a) {
-      int pos[64];
-      const int np = snapped_positions(b.lo[a], b.hi[a], P.bins, P.cs, pos);
-      for (int q = 0; q < np; ++q) {
-        Box lreg = b, rreg = b, lb, rb;
-        lreg.hi[a] = pos[q];
-        rreg.lo[a] = pos[q];
-        const bool l = reduce(a, lreg, lb);
-        const bool r = reduce(a, rreg, rb);
-        const int64_t c = (l ? box_vol(lb) : 0) + (r ? box_vol(rb) : 0);
-        if (ba < 0 || c < bc) { ba = a; bp = pos[q]; bc = c; bl = lb; br = rb; hl = l; hr = r; }
+    auto candidate = [&](int a, int p) {
+      Box lreg = b, rreg = b, lb, rb;
+      if (a == 0) { lreg.hi[0] = p; rreg.lo[0] = p; }
+      else if (a == 1) { lreg.hi[1] = p; rreg.lo[1] = p; }
+      else { lreg.hi[2] = p; rreg.lo[2] = p; }
+      const bool l = reduce(a, lreg, lb);
+      const bool r = reduce(a, rreg, rb);
+      const int64_t c = (l ? box_vol(lb) : 0) + (r ? box_vol(rb) : 0);
+      if (ba < 0 || c < bc) { ba = a; bp = p; bc = c; bl = lb; br = rb; hl = l; hr = r; }
+    };
+    if (CS && P.bins <= 8) {
+      for (int a = 0; a < 3; ++a) {
+        const int lo = a == 0 ? b.lo[0] : (a == 1 ? b.lo[1] : b.lo[2]);
+        const int hi = a == 0 ? b.hi[0] : (a == 1 ? b.hi[1] : b.hi[2]);
+        const double step = div_exact((double)(hi - lo), P.bins);
+        int last = INT_MIN;
+#pragma unroll 1
+        for (int j = 1; j < P.bins; ++j) {
+          const double raw = __dadd_rn((double)lo, __dmul_rn((double)j, step));
+          const int64_t p = (int64_t)floor(__dadd_rn(div_exact(raw, cs), 0.5)) * cs;
+          if (lo < p && p < hi && (int)p != last) {
+            last = (int)p;
+            candidate(a, (int)p);
+          }
+        }
+      }
+    } else {
+      for (int a = 0; a < 3; ++a) {
+        int pos[64];
+        const int np = snapped_positions(b.lo[a], b.hi[a], P.bins, cs, pos);
+        for (int q = 0; q < np; ++q) candidate(a, pos[q]);
       }
     }
     if (ba >= 0 && bc < vol) {
@@ -887,11 +921,10 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
     if (ext[a] > P.mls) {
       const int lo = b.lo[a], hi = b.hi[a];
       int pos = lo + ext[a] / 2;
-      const int cs = P.cs;
       const int first = (lo / cs + 1) * cs, last = ((hi - 1) / cs) * cs;
       if (first <= last) {
         const int64_t snap =
-            (int64_t)floor(__dadd_rn(__ddiv_rn((double)pos, (double)cs), 0.5)) * cs;
+            (int64_t)floor(__dadd_rn(div_exact((double)pos, cs), 0.5)) * cs;
         const int64_t q = snap < first ? (int64_t)first : snap;
         pos = (int)(q > last ? (int64_t)last : q);
       }
@@ -1034,14 +1067,32 @@ __global__ void __launch_bounds__(256) k_cell_slabs(const CBox* __restrict__ cel
     const int q0 = ch * CELL_CHUNK, q1 = min(n1 * n2, q0 + CELL_CHUNK);
     CBox u;
     for (int k = 0; k < 3; ++k) { u.lo[k] = KD_FAR; u.hi[k] = -1; }
-    for (int q = q0 + lane; q < q1; q += 32) {
-      int cc[3];
-      cc[A] = c;
-      cc[o1] = c0[o1] + q / n2;
-      cc[o2] = c0[o2] + q % n2;
-      const CBox v = cells[((int64_t)cc[0] * ncy + cc[1]) * ncz + cc[2]];
-      if (v.lo[0] != KD_FAR)
-        for (int k = 0; k < 3; ++k) { u.lo[k] = min(u.lo[k], v.lo[k]); u.hi[k] = max(u.hi[k], v.hi[k]); }
+    // cell index = c * stride(A) + (c0[o1] + q / n2) * stride(o1) + (c0[o2] + q % n2) * stride(o2)
+    const int64_t sxz = (int64_t)ncy * ncz;
+    auto stride = [&](int k) { return k == 0 ? sxz : (k == 1 ? (int64_t)ncz : (int64_t)1); };
+    const int b1 = o1 == 0 ? c0[0] : (o1 == 1 ? c0[1] : c0[2]);
+    const int b2 = o2 == 0 ? c0[0] : (o2 == 1 ? c0[1] : c0[2]);
+    const int64_t st1 = stride(o1), st2 = stride(o2);
+    const int64_t cbase = (int64_t)c * stride(A) + b1 * st1 + b2 * st2;
+    constexpr int CU = VS_CS_CU;  // cells in flight per lane
+    for (int qb = q0 + lane; qb < q1; qb += 32 * CU) {
+      CBox v[CU];
+#pragma unroll
+      for (int j = 0; j < CU; ++j) {
+        const int q = qb + 32 * j;
+        if (q < q1) {
+          v[j] = cells[cbase + (int64_t)(q / n2) * st1 + (int64_t)(q % n2) * st2];
+        } else {
+          v[j].lo[0] = KD_FAR;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CU; ++j)
+        if (v[j].lo[0] != KD_FAR)
+          for (int k = 0; k < 3; ++k) {
+            u.lo[k] = min(u.lo[k], v[j].lo[k]);
+            u.hi[k] = max(u.hi[k], v[j].hi[k]);
+          }
     }
     for (int k = 0; k < 3; ++k) {  // warp reductions (redux.sync)
       u.lo[k] = __reduce_min_sync(0xffffffffu, u.lo[k]);
@@ -1163,13 +1214,14 @@ __global__ void k_emit_level(const KdDecision* __restrict__ dec, const int64_t* 
 }
 
 // Binned leaves: exact shrink_to_occupied(box) (kdtree.py:474) read straight from the bits;
-// empty -> dropped (no row).  Block per node; non-leaves exit at once.
+// empty -> dropped (no row).  Block per leaf, blocks striding over the level's nodes (most are
+// not leaves: a block per node would be mostly launch cost).
 __global__ void __launch_bounds__(128) k_leaf_shrink(const uint32_t* __restrict__ bits, int ny,
                                                      int nzw, KdLevel L,
                                                      KdDecision* __restrict__ dec) {
-  const int i = blockIdx.x;
-  if (i >= L.n || dec[i].axis >= 0) return;
   __shared__ int red[6];
+  for (int i = blockIdx.x; i < L.n; i += gridDim.x) {
+  if (dec[i].axis >= 0) continue;
   const Box b = L.box[i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x < 6) red[threadIdx.x] = threadIdx.x < 3 ? KD_FAR : -1;
@@ -1221,6 +1273,8 @@ __global__ void __launch_bounds__(128) k_leaf_shrink(const uint32_t* __restrict_
       for (int k = 0; k < 3; ++k) { t.lo[k] = b.lo[k] + red[k]; t.hi[k] = b.lo[k] + red[3 + k] + 1; }
       dec[i].leaf = t;
     }
+  }
+  __syncthreads();  // red[] is reused by the block's next leaf
   }
 }
 
@@ -3145,11 +3199,13 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
       }
       VS_CUDA(cudaEventRecord(ev_join, side), "join");
       VS_CUDA(cudaStreamWaitEvent(st, ev_join, 0), "join wait");
-      k_decide_binned<<<(unsigned)cdiv(n, 4), 128, 0, st>>>(L, P, B, dec.as<KdDecision>(),
+      (cs == 8 ? k_decide_binned<8> : k_decide_binned<0>)<<<(unsigned)cdiv(n, 4), 128, 0, st>>>(
+          L, P, B, dec.as<KdDecision>(),
                                                             cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
       // exact shrink for the binned leaves (kdtree.py:474)
-      k_leaf_shrink<<<(unsigned)n, 128, 0, st>>>(bits, ny, nzw, L, dec.as<KdDecision>());
+      k_leaf_shrink<<<(unsigned)std::min<int64_t>(n, 148 * 16), 128, 0, st>>>(
+          bits, ny, nzw, L, dec.as<KdDecision>());
       VS_TRY(check_launch("k_leaf_shrink"));
     }
     // next level: child offsets, rows of this level, next boxes and their work sizes
