@@ -843,12 +843,25 @@ __device__ __forceinline__ double div_exact(double x, int d) {
   return (d & (d - 1)) == 0 ? __dmul_rn(x, 1.0 / (double)d) : __ddiv_rn(x, (double)d);
 }
 
-template <int CS>
-__global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, BinnedCtx B,
-                                                       KdDecision* __restrict__ out,
-                                                       int64_t* __restrict__ child_count) {
+// WPN = 1: four nodes per 128-thread CTA (wide levels).  WPN > 1: one node per CTA of WPN
+// warps (narrow levels: a few big nodes), the candidates dealt round-robin over the warps and
+// the winner taken as (least cost, then first candidate) -- the reference's first strict
+// minimum of the sequential scan.
+template <int WPN>
+struct BinnedBest {
+  long long cost[WPN];
+  int idx[WPN], axis[WPN], plane[WPN], has[WPN];
+  Box lb[WPN], rb[WPN];
+};
+template <int CS, int WPN>
+__global__ void __launch_bounds__(WPN == 1 ? 128 : 32 * WPN)
+    k_decide_binned(KdLevel L, KdParams P, BinnedCtx B, KdDecision* __restrict__ out,
+                    int64_t* __restrict__ child_count) {
+  __shared__ BinnedBest<WPN> sbest;
   const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int wid = WPN == 1 ? 0 : (int)(threadIdx.x >> 5);
+  const int i = WPN == 1 ? (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5))
+                         : (int)blockIdx.x;
   if (i >= L.n) return;
   const Box b = L.box[i];
   const int ext[3] = {b.hi[0] - b.lo[0], b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]};
@@ -869,11 +882,13 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
   };
   if (!halted(P, vol)) {
     // first strict minimum over (axis, position)
-    int ba = -1, bp = 0;
+    int ba = -1, bp = 0, bi = 0, ncand = 0;
     int64_t bc = 0;
     Box bl, br;
     bool hl = false, hr = false;
     auto candidate = [&](int a, int p) {
+      const int ci = ncand++;
+      if (WPN > 1 && ci % WPN != wid) return;
       Box lreg = b, rreg = b, lb, rb;
       if (a == 0) { lreg.hi[0] = p; rreg.lo[0] = p; }
       else if (a == 1) { lreg.hi[1] = p; rreg.lo[1] = p; }
@@ -881,7 +896,7 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
       const bool l = reduce(a, lreg, lb);
       const bool r = reduce(a, rreg, rb);
       const int64_t c = (l ? box_vol(lb) : 0) + (r ? box_vol(rb) : 0);
-      if (ba < 0 || c < bc) { ba = a; bp = p; bc = c; bl = lb; br = rb; hl = l; hr = r; }
+      if (ba < 0 || c < bc) { ba = a; bp = p; bc = c; bi = ci; bl = lb; br = rb; hl = l; hr = r; }
     };
     if (CS && P.bins <= 8) {
       for (int a = 0; a < 3; ++a) {
@@ -906,6 +921,27 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
         for (int q = 0; q < np; ++q) candidate(a, pos[q]);
       }
     }
+    if (WPN > 1) {  // combine the warps' bests: least cost, then first candidate
+      if (lane == 0) {
+        sbest.cost[wid] = bc; sbest.idx[wid] = bi; sbest.axis[wid] = ba; sbest.plane[wid] = bp;
+        sbest.has[wid] = (hl ? 1 : 0) | (hr ? 2 : 0);
+        sbest.lb[wid] = bl; sbest.rb[wid] = br;
+      }
+      __syncthreads();
+      int w = -1;
+      for (int k = 0; k < WPN; ++k)
+        if (sbest.axis[k] >= 0 &&
+            (w < 0 || sbest.cost[k] < sbest.cost[w] ||
+             (sbest.cost[k] == sbest.cost[w] && sbest.idx[k] < sbest.idx[w])))
+          w = k;
+      if (wid != 0) return;
+      ba = -1;
+      if (w >= 0) {
+        ba = sbest.axis[w]; bp = sbest.plane[w]; bc = sbest.cost[w];
+        hl = sbest.has[w] & 1; hr = (sbest.has[w] >> 1) & 1;
+        bl = sbest.lb[w]; br = sbest.rb[w];
+      }
+    }
     if (ba >= 0 && bc < vol) {
       d.axis = ba; d.plane = bp;
       if (hl) { d.left = bl; d.nchild |= 1; }
@@ -913,6 +949,7 @@ __global__ void __launch_bounds__(128) k_decide_binned(KdLevel L, KdParams P, Bi
       split = true;
     }
   }
+  if (WPN > 1 && wid != 0) return;
   if (!split && P.mls >= 0) {
     // forced_split snapped to the interior raster
     int a = 0;
@@ -1106,6 +1143,133 @@ __global__ void __launch_bounds__(256) k_cell_slabs(const CBox* __restrict__ cel
       atomicMax(&dst->hi[lane], u.hi[lane]);
     }
   }
+}
+
+// Packed cell boxes for cells of at most 16 voxels per axis: one 32-bit word per cell, the
+// box as offsets from the cell's corner (4 bits each: lo x/y/z, then hi-1 x/y/z); empty =
+// ~0.  Two copies: [x][y][z] (the x- and y-slab passes read runs along z) and [z][x][y] (the
+// z-slab pass reads runs along y), so every cell-slab pass streams 4 contiguous bytes per
+// cell instead of a strided 24-byte CBox.
+#ifndef VS_CELL_PK
+#define VS_CELL_PK 1  // 0: the cell-slab passes read the 24-byte CBoxes (A/B builds)
+#endif
+constexpr uint32_t CPK_EMPTY = 0xffffffffu;
+constexpr int CPK_MAX_CS = VS_CELL_PK ? 16 : 0;
+__global__ void k_cell_pack(const CBox* __restrict__ cells, int ncx, int ncy, int ncz, int cs,
+                            uint32_t* __restrict__ pxyz, uint32_t* __restrict__ pzxy) {
+  const int64_t n = (int64_t)ncx * ncy * ncz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cz = (int)(i % ncz), cy = (int)((i / ncz) % ncy), cx = (int)(i / ((int64_t)ncz * ncy));
+  const CBox c = cells[i];
+  uint32_t v = CPK_EMPTY;
+  if (c.lo[0] != KD_FAR) {
+    const int b[3] = {cx * cs, cy * cs, cz * cs};
+    v = 0;
+    for (int k = 0; k < 3; ++k)
+      v |= (uint32_t)(c.lo[k] - b[k]) << (4 * k) | (uint32_t)(c.hi[k] - 1 - b[k]) << (12 + 4 * k);
+  }
+  pxyz[i] = v;
+  pzxy[((int64_t)cz * ncx + cx) * ncy + cy] = v;
+}
+
+// k_cell_slabs over the packed cells: the same items, the same unions (so the same
+// decisions), 4 coalesced bytes per cell.  The slab's cross-section (o1, o2) is walked as
+// rows of o2-contiguous cells; lane positions advance by a precomputed (rows, cols) step.
+template <int A>
+__device__ __forceinline__ void cell_slabs_pk(const uint32_t* __restrict__ pxyz,
+                                              const uint32_t* __restrict__ pzxy, int ncx, int ncy,
+                                              int ncz, int cs, const KdLevel& L, int64_t items,
+                                              CBox* __restrict__ out) {
+  constexpr int o1 = A == 0 ? 1 : 0, o2 = A == 2 ? 1 : 2;
+  constexpr int CU = 4;  // cells in flight per lane
+  const int lane = threadIdx.x & 31;
+  const int nc[3] = {ncx, ncy, ncz};
+  const int64_t* off = L.off[A_C0 + A];
+  const int64_t* ioff = L.off[A_IC0 + A];
+  const uint32_t* __restrict__ pk = A == 2 ? pzxy : pxyz;
+  for (ItemWalker W(ioff, L.n, items); W.valid(); W.advance()) {
+    const int i = W.node;
+    const Box b = L.box[i];
+    int c0[3], c1[3];
+    for (int k = 0; k < 3; ++k) node_cell_range(b, cs, nc, k, c0[k], c1[k]);
+    const int n1 = c1[o1] - c0[o1] + 1, n2 = c1[o2] - c0[o2] + 1;
+    const int nch = (n1 * n2 + CELL_CHUNK - 1) / CELL_CHUNK;
+    const int local = (int)(W.it - ioff[i]);
+    const int s = local / nch, ch = local - s * nch;
+    const int c = c0[A] + s;
+    const int q0 = ch * CELL_CHUNK, q1 = min(n1 * n2, q0 + CELL_CHUNK);
+    // row stride of the layout along o1 (o2 is contiguous) and the slab's base cell
+    int64_t st1, base;
+    if (A == 0) {
+      st1 = ncz; base = ((int64_t)c * ncy + c0[1]) * ncz + c0[2];
+    } else if (A == 1) {
+      st1 = (int64_t)ncy * ncz; base = ((int64_t)c0[0] * ncy + c) * ncz + c0[2];
+    } else {
+      st1 = ncy; base = ((int64_t)c * ncx + c0[0]) * ncy + c0[1];
+    }
+    int r = (q0 + lane) / n2, col = (q0 + lane) - r * n2;  // lane's first cell
+    const int dr = 32 / n2, dc = 32 - dr * n2;              // one 32-cell step
+    int ma_lo = 64, ma_hi = -1;                             // local offsets along A
+    int m1_lo = KD_FAR, m1_hi = -1, m2_lo = KD_FAR, m2_hi = -1;
+    for (int qb = q0 + lane; qb < q1; qb += 32 * CU) {
+      uint32_t v[CU];
+      int rr[CU], cc[CU];
+#pragma unroll
+      for (int j = 0; j < CU; ++j) {
+        rr[j] = r; cc[j] = col;
+        v[j] = qb + 32 * j < q1 ? __ldg(pk + base + (int64_t)r * st1 + col) : CPK_EMPTY;
+        col += dc; r += dr;
+        if (col >= n2) { col -= n2; ++r; }
+      }
+#pragma unroll
+      for (int j = 0; j < CU; ++j)
+        if (v[j] != CPK_EMPTY) {
+          const int e1 = (c0[o1] + rr[j]) * cs, e2 = (c0[o2] + cc[j]) * cs;
+          ma_lo = min(ma_lo, (int)(v[j] >> (4 * A)) & 15);
+          ma_hi = max(ma_hi, (int)(v[j] >> (12 + 4 * A)) & 15);
+          m1_lo = min(m1_lo, e1 + (int)((v[j] >> (4 * o1)) & 15));
+          m1_hi = max(m1_hi, e1 + (int)((v[j] >> (12 + 4 * o1)) & 15));
+          m2_lo = min(m2_lo, e2 + (int)((v[j] >> (4 * o2)) & 15));
+          m2_hi = max(m2_hi, e2 + (int)((v[j] >> (12 + 4 * o2)) & 15));
+        }
+    }
+    ma_lo = __reduce_min_sync(0xffffffffu, ma_lo);
+    ma_hi = __reduce_max_sync(0xffffffffu, ma_hi);
+    m1_lo = __reduce_min_sync(0xffffffffu, m1_lo);
+    m1_hi = __reduce_max_sync(0xffffffffu, m1_hi);
+    m2_lo = __reduce_min_sync(0xffffffffu, m2_lo);
+    m2_hi = __reduce_max_sync(0xffffffffu, m2_hi);
+    CBox u;
+    if (ma_hi < 0) {
+      for (int k = 0; k < 3; ++k) { u.lo[k] = KD_FAR; u.hi[k] = -1; }
+    } else {
+      u.lo[A] = c * cs + ma_lo; u.hi[A] = c * cs + ma_hi + 1;
+      u.lo[o1] = m1_lo; u.hi[o1] = m1_hi + 1;
+      u.lo[o2] = m2_lo; u.hi[o2] = m2_hi + 1;
+    }
+    CBox* dst = out + off[i] + s;
+    if (nch == 1) {
+      if (lane == 0) *dst = u;
+    } else if (lane < 3 && ma_hi >= 0) {
+      atomicMin(&dst->lo[lane], u.lo[lane]);
+      atomicMax(&dst->hi[lane], u.hi[lane]);
+    }
+  }
+}
+
+// The three axes' passes in one launch (blockIdx.y = axis; they are independent).
+__global__ void __launch_bounds__(256) k_cell_slabs_pk3(const uint32_t* __restrict__ pxyz,
+                                                        const uint32_t* __restrict__ pzxy,
+                                                        int ncx, int ncy, int ncz, int cs,
+                                                        KdLevel L, int64_t i0, int64_t i1,
+                                                        int64_t i2, CBox* o0, CBox* o1, CBox* o2) {
+  if (blockIdx.y == 0)
+    cell_slabs_pk<0>(pxyz, pzxy, ncx, ncy, ncz, cs, L, i0, o0);
+  else if (blockIdx.y == 1)
+    cell_slabs_pk<1>(pxyz, pzxy, ncx, ncy, ncz, cs, L, i1, o1);
+  else
+    cell_slabs_pk<2>(pxyz, pzxy, ncx, ncy, ncz, cs, L, i2, o2);
 }
 
 __global__ void k_cbox_init(CBox* __restrict__ c, int64_t n) {
@@ -2860,13 +3024,27 @@ struct KdResultImpl {
   DBuf lo, hi, axis, plane, left, right;
 };
 
+// Small device -> host reads (the level loop's per-level header) go through a per-thread
+// pinned staging buffer: a pageable copy is staged by the driver and costs a few us more.
 int d2h(void* dst, const void* src, size_t n, cudaStream_t st) {
-  VS_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st), "d2h");
+  constexpr size_t STAGE = 64 << 10;
+  thread_local void* stage = nullptr;
+  if (n <= STAGE && !stage && cudaMallocHost(&stage, STAGE) != cudaSuccess) {
+    cudaGetLastError();
+    stage = nullptr;
+  }
+  const bool pinned = n <= STAGE && stage;
+  VS_CUDA(cudaMemcpyAsync(pinned ? stage : dst, src, n, cudaMemcpyDeviceToHost, st), "d2h");
   VS_CUDA(cudaStreamSynchronize(st), "sync");
+  if (pinned) memcpy(dst, stage, n);
   return 0;
 }
 
 constexpr int SPAN_BLOCKS = 148 * 8;
+#ifndef VS_BINNED_NARROW
+#define VS_BINNED_NARROW 1024  // levels of at most this many nodes: 8 warps per node decision
+#endif
+constexpr int BINNED_NARROW = VS_BINNED_NARROW;
 
 // A non-blocking side stream per device for independent passes (created once).
 cudaStream_t side_stream(int dev) {
@@ -2917,10 +3095,10 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
              KdResultImpl* R, cudaStream_t st) {
   const int nzw = (int)nzw_of(nz);
 
-  DBuf bb, cur, nxt, offs, dec, cnt, spx, spy, spz, pxz, pyz, scr, rec, cellb, cslab, sizes, pre,
-      hdr;
+  DBuf bb, cur, nxt, offs, dec, cnt, spx, spy, spz, pxz, pyz, scr, rec, cellb, cpk, cslab, sizes,
+      pre, hdr;
   for (DBuf* b : {&bb, &cur, &nxt, &offs, &dec, &cnt, &spx, &spy, &spz, &pxz, &pyz, &scr, &rec,
-                  &cellb, &cslab, &sizes, &pre, &hdr})
+                  &cellb, &cpk, &cslab, &sizes, &pre, &hdr})
     b->st = st;
 
   KdParams P;
@@ -3175,7 +3353,14 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
         const int64_t ncell = (int64_t)ncx * ncy * ncz;
         VS_TRY(cellb.ensure(ncell * sizeof(CBox), "cells"));
         VS_TRY(launch_cell_boxes(bits, nx, ny, nz, cs, ncx, ncy, ncz, cellb.as<CBox>(), st));
+        if (cs <= CPK_MAX_CS) {  // packed copies for the cell-slab passes
+          VS_TRY(cpk.ensure(2 * ncell * sizeof(uint32_t), "packed cells"));
+          k_cell_pack<<<(unsigned)cdiv(ncell, 256), 256, 0, st>>>(
+              cellb.as<CBox>(), ncx, ncy, ncz, cs, cpk.as<uint32_t>(), cpk.as<uint32_t>() + ncell);
+          VS_TRY(check_launch("k_cell_pack"));
+        }
       }
+      const int64_t ncell_all = (int64_t)ncx * ncy * ncz;
       B.cells = cellb.as<CBox>();
       const int64_t t0 = tot[A_C0], t1 = tot[A_C1], t2 = tot[A_C2];
       VS_TRY(cslab.ensure((t0 + t1 + t2 + 3) * sizeof(CBox), "cell slabs"));
@@ -3185,23 +3370,40 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
         k_cbox_init<<<grid_for(t0 + t1 + t2 + 3, 256), 256, 0, st>>>(cbase, t0 + t1 + t2 + 3);
         VS_TRY(check_launch("k_cbox_init"));
       }
-      // the three axes' cell-slab passes are independent: y and z on the side stream
-      VS_CUDA(cudaEventRecord(ev_fork, st), "fork");
-      VS_CUDA(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
       for (int a = 0; a < 3; ++a) {
-        const int64_t items = tot[A_IC0 + a];
-        if (items > 0)
-          k_cell_slabs<<<grid_for(items, 8), 256, 0, a == 0 ? st : side>>>(
-              cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L, items, cs3[a]);
-        VS_TRY(check_launch("k_cell_slabs"));
         B.cslab[a] = cs3[a];
         B.coff[a] = L.off[A_C0 + a];
       }
-      VS_CUDA(cudaEventRecord(ev_join, side), "join");
-      VS_CUDA(cudaStreamWaitEvent(st, ev_join, 0), "join wait");
-      (cs == 8 ? k_decide_binned<8> : k_decide_binned<0>)<<<(unsigned)cdiv(n, 4), 128, 0, st>>>(
-          L, P, B, dec.as<KdDecision>(),
-                                                            cnt.as<int64_t>());
+      if (cs <= CPK_MAX_CS) {  // packed cells: the three axes in one launch
+        const int64_t mi = std::max(std::max(tot[A_IC0], tot[A_IC1]), tot[A_IC2]);
+        if (mi > 0) {
+          const uint32_t* p0 = cpk.as<uint32_t>();
+          k_cell_slabs_pk3<<<dim3(grid_for(mi, 8), 3), 256, 0, st>>>(
+              p0, p0 + ncell_all, ncx, ncy, ncz, cs, L, tot[A_IC0], tot[A_IC1], tot[A_IC2],
+              cs3[0], cs3[1], cs3[2]);
+          VS_TRY(check_launch("k_cell_slabs_pk3"));
+        }
+      } else {
+        // the three axes' cell-slab passes are independent: y and z on the side stream
+        VS_CUDA(cudaEventRecord(ev_fork, st), "fork");
+        VS_CUDA(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
+        for (int a = 0; a < 3; ++a) {
+          const int64_t items = tot[A_IC0 + a];
+          if (items > 0)
+            k_cell_slabs<<<grid_for(items, 8), 256, 0, a == 0 ? st : side>>>(
+                cellb.as<CBox>(), ncx, ncy, ncz, cs, a, L, items, cs3[a]);
+          VS_TRY(check_launch("k_cell_slabs"));
+        }
+        VS_CUDA(cudaEventRecord(ev_join, side), "join");
+        VS_CUDA(cudaStreamWaitEvent(st, ev_join, 0), "join wait");
+      }
+      if (n <= BINNED_NARROW)  // a few big nodes: one CTA of 8 warps per node
+        (cs == 8 ? k_decide_binned<8, 8> : k_decide_binned<0, 8>)<<<(unsigned)n, 256, 0, st>>>(
+            L, P, B, dec.as<KdDecision>(), cnt.as<int64_t>());
+      else
+        (cs == 8 ? k_decide_binned<8, 1> : k_decide_binned<0, 1>)<<<(unsigned)cdiv(n, 4), 128, 0,
+                                                                   st>>>(
+            L, P, B, dec.as<KdDecision>(), cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
       // exact shrink for the binned leaves (kdtree.py:474)
       k_leaf_shrink<<<(unsigned)std::min<int64_t>(n, 148 * 16), 128, 0, st>>>(

@@ -11,7 +11,9 @@ import paper_1912_09596_b200 as vs
 from paper_1912_09596_b200.synth import gen_blobs_u8
 
 sizes = [int(a) for a in sys.argv[1:]] or [512, 1024]
-KINDS = ["kd-shallow", "kd-deep-mls32", "kd-deep-mls128", "kd-binned-mls32", "hybrid"]
+import os
+
+KINDS = os.environ.get("KINDS", "kd-shallow kd-deep-mls32 kd-deep-mls128 kd-binned-mls32 hybrid").split()
 for n in sizes:
     v = vs.Volume.from_u8(gen_blobs_u8((n, n, n), max(1, 25600 * n**3 // 1024**3), seed=7, sigma=3.0))
     for t in (0.6, 0.3, 0.0):
