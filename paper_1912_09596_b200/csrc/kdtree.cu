@@ -2134,6 +2134,9 @@ constexpr int LV_T = 256;
 #ifndef VS_LV_U
 #define VS_LV_U 8  // rows per lane in flight in phase A's vector loads
 #endif
+#ifndef VS_LV_TILED
+#define VS_LV_TILED 0  // 1: phase A items in x/y band tiles (measured 2-3% slower; kept for A/B)
+#endif
 constexpr int LV_W = LV_T / 32;
 constexpr int LV_NMAX = 1024;   // work nodes per level
 constexpr int LV_EMAX = 1024;   // node extent per axis
@@ -2344,12 +2347,36 @@ __device__ void lv_phase_a(const LvCtx& X, const LvNode* __restrict__ work, int 
     const Box b = nd.box;
     const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1];
     const LvGeom q = lv_geom(b, X.vec);
+#if VS_LV_TILED
+    // Items in (x band, y band) tiles of R x R rows: the tile's x-slab items (slabs of the x
+    // band, rows = the y band) and its y-slab items (slabs of the y band, rows = the x band)
+    // alternate, so the second read of a row is an L2 hit instead of a second DRAM pass.
+    const int local = it - sm.off[node];
+    const int R = q.R;
+    const int chx = (ey + R - 1) / R, chy = (ex + R - 1) / R;
+    const int rowfull = R * chx + ey;  // items of a full x band
+    const int bx = min(local / rowfull, chy - 1);
+    const int rem = local - bx * rowfull;
+    const int nxb = min(R, ex - bx * R);
+    const int by = min(rem / (nxb + R), chx - 1);
+    const int j = rem - by * (nxb + R);
+    const int nyb = min(R, ey - by * R), mxy = min(nxb, nyb);
+    int AX, idx;
+    if (j < 2 * mxy) {
+      AX = j & 1; idx = j >> 1;
+    } else {
+      AX = nxb > nyb ? 0 : 1; idx = j - mxy;
+    }
+    const int s = AX == 0 ? bx * R + idx : by * R + idx;
+    const int cc = AX == 0 ? by : bx;
+#else
     int local = it - sm.off[node];
     const int chx = (ey + q.R - 1) / q.R, nxi = ex * chx;
     const int AX = local < nxi ? 0 : 1;
     if (AX) local -= nxi;
     const int nch = AX == 0 ? chx : (ex + q.R - 1) / q.R;
     const int s = local / nch, cc = local - s * nch;
+#endif
     const int er = AX == 0 ? ey : ex, es = AX == 0 ? ex : ey;
     const int r0 = cc * q.R, r1 = min(er, r0 + q.R);
     const int wz = q.wz, sh = q.sh, gw = q.gw, G = q.G;
