@@ -293,11 +293,13 @@ def run_ours(args, rank, ws, local):
     from paper_1912_09596_b200.engine import LbvhRebuilder, tf_params_device
     from paper_1912_09596_b200.render import (RenderTarget, camera_desc, index_desc, render_rows,
                                               tf_device, volume_desc)
-    from paper_1912_09596_b200.tiles import TileRenderer
+    from paper_1912_09596_b200.tiles import TileRenderer, shard_presence
 
     n = args.size
     u8, nblobs = make_volume(n)
     v = vs.Volume.from_u8(u8)
+    if ws > 1:
+        shard_presence(v)  # the once-per-volume presence pass split by brick x-slabs + all-gather
     tfs = sweep_tfs()
     cams = cameras(v.dims)
     params = tf_params_device(tfs)

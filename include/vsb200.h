@@ -137,6 +137,11 @@ int vs_summary_to_bitmap(const uint32_t* summary, int nx, int ny, int nz, int di
 int64_t vs_presence_words(int nx, int ny, int nz);
 int vs_presence_build(const uint8_t* bins, int nx, int ny, int nz, uint32_t* presence,
                       vs_stream_t stream);
+/* The masks of brick x-slabs [bx0, bx1) only (their words: offset bx0 * nby * nbz * 8 of the
+ * full array), so N ranks each build a slab range of a replicated volume and one all-gather
+ * assembles the array (render.py:16-18's ray-chunk sharding applied to the per-volume pass). */
+int vs_presence_build_slab(const uint8_t* bins, int nx, int ny, int nz, int bx0, int bx1,
+                           uint32_t* presence, vs_stream_t stream);
 int vs_presence_to_bitmap(const uint32_t* const* presence_dev_ptrs, const int32_t* tf_params,
                           int nch, int nx, int ny, int nz, int P, uint32_t* bitmap,
                           uint32_t* tile_counts, uint8_t* cell16_opt, uint32_t* grid_opt,

@@ -37,6 +37,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_summary_to_bitmap": (i32, [P, i32, i32, i32, i32, i32, P, P, P, P, P]),
     "vs_presence_words": (i64, [i32, i32, i32]),
     "vs_presence_build": (i32, [P, i32, i32, i32, P, P]),
+    "vs_presence_build_slab": (i32, [P, i32, i32, i32, i32, i32, P, P]),
     "vs_presence_to_bitmap": (i32, [P, P, i32, i32, i32, i32, i32, P, P, P, P, P]),
     "vs_flags_to_bitmap": (i32, [P, i32, i32, i32, i32, P, P, P]),
     "vs_bricks_workspace": (SZ, [i32, i32, i32]),

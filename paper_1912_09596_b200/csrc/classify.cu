@@ -942,9 +942,9 @@ __global__ void __launch_bounds__(256)
 constexpr int PR_T = 256;
 __global__ void __launch_bounds__(PR_T)
     k_presence(const uint8_t* __restrict__ vol, int nx, int ny, int nz, int nby, int nbz,
-               uint32_t* __restrict__ presence) {
+               int bx0, uint32_t* __restrict__ presence) {
   extern __shared__ uint32_t pm[];  // nbz * 8 words
-  const int bx = blockIdx.x / nby, by = blockIdx.x - (blockIdx.x / nby) * nby;
+  const int bx = bx0 + (int)(blockIdx.x / nby), by = blockIdx.x - (blockIdx.x / nby) * nby;
   for (int k = threadIdx.x; k < nbz * 8; k += PR_T) pm[k] = 0;
   __syncthreads();
   const int x0 = max(bx * 8 - 1, 0), x1 = min(bx * 8 + 9, nx);
@@ -1261,19 +1261,28 @@ int64_t vs_presence_words(int nx, int ny, int nz) {
   return cdiv(nx, 8) * cdiv(ny, 8) * cdiv(nz, 8) * 8;
 }
 
-int vs_presence_build(const uint8_t* bins, int nx, int ny, int nz, uint32_t* presence,
-                      vs_stream_t st) {
+int vs_presence_build_slab(const uint8_t* bins, int nx, int ny, int nz, int bx0, int bx1,
+                           uint32_t* presence, vs_stream_t st) {
   if (!bins || !presence || nx < 1 || ny < 1 || nz < 1 || nz % 16 != 0 ||
       ((uintptr_t)bins & 15) != 0)
     return fail_arg("vs_presence_build (needs nz % 16 == 0, 16-byte aligned bins)");
   const int nbx = (int)cdiv(nx, 8), nby = (int)cdiv(ny, 8), nbz = (int)cdiv(nz, 8);
+  if (bx0 < 0 || bx1 > nbx || bx0 > bx1)
+    return fail_arg("vs_presence_build_slab: brick slab range outside [0, nbx]");
+  if (bx0 == bx1) return 0;
   const size_t smem = (size_t)nbz * 8 * 4;
   if (smem > 48 * 1024)
     VS_CUDA(cudaFuncSetAttribute(k_presence, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem), "presence smem");
-  k_presence<<<(unsigned)((int64_t)nbx * nby), PR_T, smem, S(st)>>>(bins, nx, ny, nz, nby, nbz,
-                                                                     presence);
+  k_presence<<<(unsigned)((int64_t)(bx1 - bx0) * nby), PR_T, smem, S(st)>>>(
+      bins, nx, ny, nz, nby, nbz, bx0, presence);
   return check_launch("k_presence");
+}
+
+int vs_presence_build(const uint8_t* bins, int nx, int ny, int nz, uint32_t* presence,
+                      vs_stream_t st) {
+  return vs_presence_build_slab(bins, nx, ny, nz, 0, nx < 1 ? 0 : (int)cdiv(nx, 8), presence,
+                                st);
 }
 
 int vs_presence_to_bitmap(const uint32_t* const* presence, const int32_t* tf_params, int nch,

@@ -45,6 +45,57 @@ def assemble(gathered: torch.Tensor, perm: torch.Tensor, out: torch.Tensor) -> t
     return torch.index_select(gathered, 0, perm, out=out)
 
 
+def presence_slabs(nbx: int, nparts: int) -> list[tuple[int, int]]:
+    """Brick x-slab range [bx0, bx1) of each part for the sharded presence build: equal
+    ceil(nbx / nparts) slabs per part (the last ones short or empty), so every rank's slice
+    of the all-gather has the same size."""
+    per = -(-nbx // nparts)
+    return [(min(nbx, p * per), min(nbx, (p + 1) * per)) for p in range(nparts)]
+
+
+def shard_presence(v, group=None, builder=None) -> torch.Tensor:
+    """The volume's per-brick halo presence masks (Volume.presence, vs_presence_build) built
+    sharded over a process group: rank r builds its brick x-slabs of the replicated volume
+    (vs_presence_build_slab) and one all-gather (NCCL over NVLink on device buffers; host
+    copies for a gloo group) assembles the array on every rank.  Bit-identical to the
+    single-GPU build (the slabs are independent: each brick reads only its own halo).
+    World size 1 is the plain build.  ``builder(bx0, bx1, out)`` overrides the slab build
+    (CPU-side tests of the split)."""
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    nx, ny, nz = v.dims if hasattr(v, "dims") else v._dims
+    nbx, nby, nbz = -(-nx // 8), -(-ny // 8), -(-nz // 8)
+    slab_words = nby * nbz * 8
+    if world == 1 and builder is None:
+        return v.presence()
+    rank = dist.get_rank(group) if world > 1 else 0
+    per = -(-nbx // world)
+    dev = v.bins.device if builder is None else torch.device("cpu")
+    full = torch.zeros(world * per * slab_words, dtype=torch.int32, device=dev)
+    bx0, bx1 = presence_slabs(nbx, world)[rank]
+    mine = full[rank * per * slab_words: (rank + 1) * per * slab_words]
+    if builder is not None:
+        builder(bx0, bx1, mine)
+    elif bx1 > bx0:
+        # the slab kernel writes at the slab's offset of a full-size array: point it at
+        # ``mine`` shifted back by bx0 slabs (only words of [bx0, bx1) are written)
+        base = mine.data_ptr() - bx0 * slab_words * 4
+        _lib.call("vs_presence_build_slab", _lib.ptr(v.bins), nx, ny, nz, bx0, bx1, base,
+                  _lib.stream())
+    if world > 1:
+        local = mine.clone()
+        if dev.type == "cuda" and dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(full, local, group=group)
+        else:
+            host = torch.empty(full.shape, dtype=full.dtype)
+            dist.all_gather_into_tensor(host, local.cpu(), group=group)
+            full.copy_(host)
+    p = full[: nbx * slab_words]
+    if builder is None:
+        v.__dict__["_presence"] = p  # Volume.presence() returns the assembled array
+        v.__dict__.pop("_presence_tab", None)
+    return p
+
+
 class TileRenderer:
     """Renders frames of one (volume, index) with the rows split over a process group."""
 

@@ -243,3 +243,32 @@ def test_macro_grid_from_bits_vs_oracle(vs, rng, dims):
     ref = O.kd_build(bits, mode="shallow")
     for f in ("lo", "hi", "axis", "plane", "left", "right"):
         np.testing.assert_array_equal(getattr(kd, f), ref[f])
+
+
+@pytest.mark.parametrize("dims,world", [((64, 48, 32), 2), ((72, 40, 48), 3), ((40, 24, 16), 8)])
+def test_presence_slab_shards_equal_full_build(vs, dims, world):
+    """vs_presence_build_slab over each rank's brick x-slabs (tiles.presence_slabs, uneven and
+    empty ranges included) writes exactly the words of the full build; with no process group
+    tiles.shard_presence is the plain Volume.presence()."""
+    import torch
+
+    from paper_1912_09596_b200 import _lib
+    from paper_1912_09596_b200.tiles import presence_slabs, shard_presence
+
+    rng = np.random.default_rng(sum(dims) + world)
+    u8 = rng.integers(0, 256, dims, dtype=np.uint8)
+    u8[rng.random(dims) < 0.7] = 0
+    v = vs.Volume.from_u8(u8)
+    full = v.presence().clone()
+    nx, ny, nz = dims
+    nbx = -(-nx // 8)
+    parts = torch.full_like(full, -7)
+    for bx0, bx1 in presence_slabs(nbx, world):
+        _lib.call("vs_presence_build_slab", _lib.ptr(v.bins), nx, ny, nz, bx0, bx1,
+                  _lib.ptr(parts), _lib.stream())
+    torch.cuda.synchronize()
+    assert torch.equal(parts, full)
+    with pytest.raises(_lib.VsError):
+        _lib.call("vs_presence_build_slab", _lib.ptr(v.bins), nx, ny, nz, 0, nbx + 1,
+                  _lib.ptr(parts), _lib.stream())
+    assert torch.equal(shard_presence(v), full)

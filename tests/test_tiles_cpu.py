@@ -68,3 +68,58 @@ def test_gloo_world2_gather_assembles_frame(height, stripe):
         p.join(timeout=120)
     res = dict(q.get(timeout=5) for _ in range(2))
     assert res == {0: True, 1: True}
+
+
+@pytest.mark.parametrize("nbx,world", [(128, 1), (128, 2), (128, 8), (5, 3), (3, 4), (1, 2)])
+def test_presence_slabs_partition(nbx, world):
+    from paper_1912_09596_b200.tiles import presence_slabs
+
+    sl = presence_slabs(nbx, world)
+    assert len(sl) == world
+    per = -(-nbx // world)
+    covered = []
+    for bx0, bx1 in sl:
+        assert 0 <= bx0 <= bx1 <= nbx and bx1 - bx0 <= per
+        covered += list(range(bx0, bx1))
+    assert covered == list(range(nbx))
+
+
+class _FakeVolume:  # what shard_presence reads of a Volume (dims; bins only on the GPU path)
+    def __init__(self, dims):
+        self.dims = dims
+
+
+def _presence_worker(rank, world, port, dims, q):
+    from paper_1912_09596_b200.tiles import shard_presence
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nbx, nby, nbz = (-(-d // 8) for d in dims)
+        sw = nby * nbz * 8
+
+        def builder(bx0, bx1, out):  # "build" this rank's slabs: word w of the array -> w % 9973
+            out[: (bx1 - bx0) * sw] = torch.arange(bx0 * sw, bx1 * sw, dtype=torch.int32) % 9973
+
+        p = shard_presence(_FakeVolume(dims), builder=builder)
+        ref = torch.arange(nbx * sw, dtype=torch.int32) % 9973
+        q.put((rank, bool(torch.equal(p, ref))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims", [(64, 40, 32), (72, 16, 16)])
+def test_gloo_world2_sharded_presence_assembles(dims):
+    """Sharded per-volume presence build (tiles.shard_presence): each rank's brick x-slabs,
+    one all-gather, the full array in order on every rank (9 slabs over 2 ranks: uneven)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_presence_worker, args=(r, 2, port, dims, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=5) for _ in range(2))
+    assert res == {0: True, 1: True}
