@@ -1751,6 +1751,7 @@ struct SubCtx {
   int* chunks;                        // chunk tables, concatenated
   unsigned long long* chunks_used;
   int* status;                        // bit 0: pool exhausted, bit 1: a subtree too large
+  const int* order;                   // launch order of the subtrees (nullptr: by id)
 };
 
 __device__ __forceinline__ RBox rb_shfl_up(const RBox& r, int o) {
@@ -1971,7 +1972,7 @@ __global__ void __launch_bounds__(SUB_T) k_subtrees(const uint32_t* __restrict__
   SubSmem& sm = *reinterpret_cast<SubSmem*>(sub_smem);
   uint32_t* words = reinterpret_cast<uint32_t*>(sub_smem + ((sizeof(SubSmem) + 15) & ~size_t(15)));
   const int t = threadIdx.x, warp = t >> 5;
-  const int s = blockIdx.x;
+  const int s = C.order ? C.order[blockIdx.x] : (int)blockIdx.x;
   const Box RB = C.rec[C.list[s]].box;
   const int exR = RB.hi[0] - RB.lo[0], eyR = RB.hi[1] - RB.lo[1], ezR = RB.hi[2] - RB.lo[2];
   const int wzR = (ezR + 31) >> 5;
@@ -2093,6 +2094,35 @@ __global__ void k_collect_sub(NodeRec* __restrict__ rec, int64_t total, int* __r
   list[id] = (int)i;
   atomicAdd(reinterpret_cast<unsigned long long*>(chunk_est),
             (unsigned long long)(1 + box_vol(rec[i].box) / 4096));
+}
+
+// The subtrees' launch order: by box volume (the work estimate) in power-of-two classes,
+// biggest class first, so the big subtrees start first and the small ones fill in behind
+// them (LPT-like order).  k_sub_class: class histogram; k_sub_order: each subtree's slot =
+// its class offset (exclusive scan of the classes above, per block) + a slot counter.
+constexpr int SUB_CLASSES = 32;
+__device__ __forceinline__ int sub_class(const NodeRec* rec, const int* list, int64_t s) {
+  const int64_t v = box_vol(rec[list[s]].box);
+  return v > 0 ? 63 - __clzll(v) : 0;
+}
+__global__ void k_sub_class(const NodeRec* __restrict__ rec, const int* __restrict__ list,
+                            int64_t nsub, int* __restrict__ hist) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nsub) atomicAdd(hist + sub_class(rec, list, s), 1);
+}
+__global__ void k_sub_order(const NodeRec* __restrict__ rec, const int* __restrict__ list,
+                            int64_t nsub, const int* __restrict__ hist, int* __restrict__ cursor,
+                            int* __restrict__ order) {
+  __shared__ int off[SUB_CLASSES];
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int c = SUB_CLASSES - 1; c >= 0; --c) { off[c] = run; run += hist[c]; }
+  }
+  __syncthreads();
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsub) return;
+  const int c = sub_class(rec, list, s);
+  order[off[c] + atomicAdd(cursor + c, 1)] = (int)s;
 }
 
 // A subtree's rows at its global preorder p0 (the deferred record's), child links shifted.
@@ -3068,6 +3098,9 @@ int d2h(void* dst, const void* src, size_t n, cudaStream_t st) {
 }
 
 constexpr int SPAN_BLOCKS = 148 * 8;
+#ifndef VS_SUB_LPT
+#define VS_SUB_LPT 1  // k_subtrees launched biggest subtree first (0: in collection order)
+#endif
 #ifndef VS_BINNED_NARROW
 #define VS_BINNED_NARROW 1024  // levels of at most this many nodes: 8 warps per node decision
 #endif
@@ -3497,6 +3530,21 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
       VS_CUDA(cudaFuncSetAttribute(k_subtrees, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem), "k_subtrees smem");
       int64_t pool_chunks = std::max<int64_t>(cnt2[1], 1024);  // k_collect_sub's estimate
+      const int* order = nullptr;
+      DBuf sord;
+      sord.st = st;
+      if (VS_SUB_LPT && nsub > 1) {  // biggest subtrees first
+        VS_TRY(sord.ensure((2 * SUB_CLASSES + nsub) * sizeof(int), "subtree order"));
+        int* hist = sord.as<int>();
+        VS_CUDA(cudaMemsetAsync(hist, 0, 2 * SUB_CLASSES * sizeof(int), st), "subtree classes");
+        const unsigned g = (unsigned)cdiv(nsub, 256);
+        k_sub_class<<<g, 256, 0, st>>>(rec.as<NodeRec>(), subl.as<int>(), nsub, hist);
+        VS_TRY(check_launch("k_sub_class"));
+        k_sub_order<<<g, 256, 0, st>>>(rec.as<NodeRec>(), subl.as<int>(), nsub, hist,
+                                       hist + SUB_CLASSES, hist + 2 * SUB_CLASSES);
+        VS_TRY(check_launch("k_sub_order"));
+        order = hist + 2 * SUB_CLASSES;
+      }
       for (;;) {
         VS_TRY(pool.ensure(pool_chunks * SUB_CHUNK * sizeof(SubRow), "subtree rows"));
         VS_TRY(chunks.ensure((pool_chunks + nsub) * sizeof(int), "subtree chunks"));
@@ -3512,10 +3560,21 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
         SC.height = subh.as<int>();
         SC.choff = subo.as<int>();
         SC.chunks = chunks.as<int>();
+        SC.order = order;
         k_subtrees<<<(unsigned)nsub, SUB_T, smem, st>>>(bits, ny, nzw, P, SC);
         VS_TRY(check_launch("k_subtrees"));
         int64_t res[3];
         VS_TRY(d2h(res, dh + 1, sizeof res, st));
+        const char* penv2 = getenv("VSB200_KD_PROFILE");
+        if (penv2 && penv2[0] == '1') {  // dev profile: the subtrees' row counts
+          std::vector<int> cnts(nsub);
+          VS_TRY(d2h(cnts.data(), subc.p, nsub * sizeof(int), st));
+          long long sum = 0;
+          int mx = 0;
+          for (int c : cnts) { sum += c; mx = std::max(mx, c); }
+          fprintf(stderr, "k_subtrees: %lld subtrees, %lld rows, largest %d rows\n",
+                  (long long)nsub, sum, mx);
+        }
         const int status = (int)(res[2] & 0xffffffff);
         if (status & 2) return KD_RETRY_LEVELS;
         if (!(status & 1)) break;
