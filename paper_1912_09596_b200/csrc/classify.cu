@@ -330,6 +330,48 @@ __device__ __forceinline__ uint32_t classify_word(const VisEval& ve, const uint4
   return w;
 }
 
+// Bulk-async (TMA, 1-D) staging of the dilating pass: a block's 16 rows of one x slab are
+// CP_TY + 2 consecutive y rows = one contiguous (rows x nz)-byte run, fetched by one
+// cp.async.bulk into a CP_NS-deep ring of shared-memory stages completed on mbarriers, so
+// CP_NS slabs are in flight per block without holding them in registers.
+#ifndef VS_CP_BULK
+#define VS_CP_BULK 1
+#endif
+#ifndef VS_CP_NS
+#define VS_CP_NS 4
+#endif
+constexpr int CP_NS = VS_CP_NS;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <int V, bool DIL>
 __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* zs,
                                                    uint32_t* red, const uint8_t* __restrict__ vol,
@@ -374,6 +416,43 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
     // tight box of the dilated flags (shrink_to_occupied of the whole volume, the k-d root,
     // kdtree.py:398) as a by-product: x / z extremes of this thread's output words
     int bx0 = 0x3fffffff, bx1 = -1, bz0 = 0x3fffffff, bz1 = -1;
+#if VS_CP_BULK
+    // slab xs = x0 - 1 + j lives in stage j % CP_NS; the block's rows [ylo, yhi) are one
+    // contiguous run per slab.  Slabs outside [0, nx) complete their phase by a plain arrive.
+    extern __shared__ __align__(128) uint8_t cp_stage[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(cp_stage);
+    uint8_t* stage0 = cp_stage + 128;
+    const int ylo = max(y0 - 1, 0), yhi = min(y0 + CP_TY + 1, ny);
+    const uint32_t run = (uint32_t)(yhi - ylo) * (uint32_t)nz;
+    const size_t stage_bytes = (size_t)(CP_TY + 2) * nz;
+    const int nj = xe - x0 + 2;  // slabs x0 - 1 .. xe
+    auto issue = [&](int j) {
+      const int xsj = x0 - 1 + j;
+      uint64_t* bar = full + (j % CP_NS);
+      if (xsj >= 0 && xsj < nx)
+        bulk_load(stage0 + (size_t)(j % CP_NS) * stage_bytes,
+                  vol + ((int64_t)xsj * ny + ylo) * nz, run, bar);
+      else
+        mbar_arrive(bar);
+    };
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < CP_NS; ++k) mbar_init(full + k, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int j = 0; j < min(CP_NS, nj); ++j) issue(j);
+    const uint8_t* srow = stage0 + (size_t)(y - ylo) * nz + lane * 32;
+    for (int xs = x0 - 1; xs <= xe; ++xs) {
+      const int j = xs - (x0 - 1);
+      mbar_wait(full + (j % CP_NS), (uint32_t)(j / CP_NS) & 1u);
+      uint32_t w = 0;
+      if (rowok && xs >= 0 && xs < nx) {
+        const uint4* q = reinterpret_cast<const uint4*>(srow + (size_t)(j % CP_NS) * stage_bytes);
+        w = classify_word<V>(ve, q[0], q[1]);
+      }
+#else
     // three slabs in flight ahead of the one being classified; the y-dilation exchange is
     // double-buffered so one barrier per slab suffices
     uint4 fa = make_uint4(0, 0, 0, 0), fb = fa, ga = fa, gb = fa;
@@ -387,6 +466,7 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
       if (xs + 3 <= xe) load(xs + 3, ga, gb);
       uint32_t w = 0;
       if (rowok && xs >= 0 && xs < nx) w = classify_word<V>(ve, a, b);
+#endif
       if (outrow && xs >= x0 && xs < xe) cnt += __popc(w);
       const uint32_t up = __shfl_up_sync(0xffffffffu, w, 1);
       const uint32_t dn = __shfl_down_sync(0xffffffffu, w, 1);
@@ -396,6 +476,10 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
       uint32_t* zb = zs + (xs & 1) * ((CP_TY + 2) * 32);
       zb[warp * 32 + lane] = zd;
       __syncthreads();
+#if VS_CP_BULK
+      // every thread is done with stage j: refill it with slab j + CP_NS
+      if (threadIdx.x == 0 && j + CP_NS < nj) issue(j + CP_NS);
+#endif
       uint32_t yd = 0;
       if (warp >= 1 && warp <= CP_TY) yd = zb[(warp - 1) * 32 + lane] | zd | zb[(warp + 1) * 32 + lane];
       // slab xs - 1 is complete: prev (xs-2) | cur (xs-1) | yd (xs)
@@ -411,9 +495,11 @@ __device__ __forceinline__ void classify_pack_body(const VisEval& ve, uint32_t* 
       }
       prev = cur;
       cur = yd;
+#if !VS_CP_BULK
       a = na; b = nb;
       na = fa; nb = fb;
       fa = ga; fb = gb;
+#endif
     }
     if (bbox) {
       bx0 = __reduce_min_sync(0xffffffffu, bx0);
@@ -1142,8 +1228,13 @@ int vs_classify_dilate_bits_bbox(const uint8_t* bins, int nx, int ny, int nz,
     VS_TRY(check_launch("k_bbox_init"));
   }
   dim3 grid((unsigned)cdiv(ny, CP_TY), (unsigned)cdiv(nx, CP_XC));
-  k_classify_pack<true><<<grid, 32 * (CP_TY + 2), 0, S(st)>>>(bins, nx, ny, nz, tf, bits, count,
-                                                             bbox);
+  const size_t smem = VS_CP_BULK ? 128 + (size_t)CP_NS * (CP_TY + 2) * nz : 0;
+  if (smem > 48 * 1024)
+    VS_CUDA(cudaFuncSetAttribute(k_classify_pack<true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "k_classify_pack smem");
+  k_classify_pack<true><<<grid, 32 * (CP_TY + 2), smem, S(st)>>>(bins, nx, ny, nz, tf, bits,
+                                                                count, bbox);
   return check_launch("k_classify_pack<dilate>");
 }
 
