@@ -3496,13 +3496,11 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
                                                          prep_ctx());
     VS_TRY(check_launch("k_emit_level"));
     VS_TRY(scan_level(dh + KA + 1, 2 * n));
-    VS_CUDA(cudaMemcpyAsync(dh, dh + KA + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, st),
-            "count");
-    VS_TRY(d2h(hh, dh, sizeof hh, st));
+    VS_TRY(d2h(hh, dh, sizeof hh, st));  // the next level's totals and (KA + 1) its node count
     std::swap(cur.p, nxt.p);
     std::swap(cur.cap, nxt.cap);
     base += n;
-    n = hh[0];
+    n = hh[KA + 1];
     ++level;
   }
   total = base;
