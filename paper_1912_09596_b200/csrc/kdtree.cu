@@ -386,7 +386,10 @@ __device__ __forceinline__ bool halted(const KdParams& P, int64_t vol) {
 // levels of a tree are long chains of small nodes, where a level-synchronous pass costs a few
 // launches and a host round trip per level.
 constexpr int SUB_EXT = 128;
-constexpr int SUB_WORDS = 10240;
+#ifndef VS_SUB_WORDS
+#define VS_SUB_WORDS 10240
+#endif
+constexpr int SUB_WORDS = VS_SUB_WORDS;
 constexpr int SUB_DEFER = -2;
 
 __device__ __forceinline__ bool defer_node(const KdParams& P, const Box& b) {
