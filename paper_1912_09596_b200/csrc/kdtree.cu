@@ -387,7 +387,7 @@ __device__ __forceinline__ bool halted(const KdParams& P, int64_t vol) {
 // launches and a host round trip per level.
 constexpr int SUB_EXT = 128;
 #ifndef VS_SUB_WORDS
-#define VS_SUB_WORDS 10240
+#define VS_SUB_WORDS 2560  // hand-off bound (measured: 10240 / 5120 / 2560 / 1280; 2560 fastest)
 #endif
 constexpr int SUB_WORDS = VS_SUB_WORDS;
 constexpr int SUB_DEFER = -2;
