@@ -76,7 +76,10 @@ enum {
 };
 
 // Cells one cell-slab work item reduces (chunks of a big slab merge with atomics).
-constexpr int CELL_CHUNK = 1024;
+#ifndef VS_CELL_CHUNK
+#define VS_CELL_CHUNK 1024
+#endif
+constexpr int CELL_CHUNK = VS_CELL_CHUNK;
 #ifndef VS_CS_CU
 #define VS_CS_CU 1  // k_cell_slabs: cells in flight per lane
 #endif
@@ -1156,6 +1159,9 @@ __global__ void __launch_bounds__(256) k_cell_slabs(const CBox* __restrict__ cel
 #ifndef VS_CELL_PK
 #define VS_CELL_PK 1  // 0: the cell-slab passes read the 24-byte CBoxes (A/B builds)
 #endif
+#ifndef VS_CPK_CU
+#define VS_CPK_CU 4
+#endif
 constexpr uint32_t CPK_EMPTY = 0xffffffffu;
 constexpr int CPK_MAX_CS = VS_CELL_PK ? 16 : 0;
 __global__ void k_cell_pack(const CBox* __restrict__ cells, int ncx, int ncy, int ncz, int cs,
@@ -1185,7 +1191,7 @@ __device__ __forceinline__ void cell_slabs_pk(const uint32_t* __restrict__ pxyz,
                                               int ncz, int cs, const KdLevel& L, int64_t items,
                                               CBox* __restrict__ out) {
   constexpr int o1 = A == 0 ? 1 : 0, o2 = A == 2 ? 1 : 2;
-  constexpr int CU = 4;  // cells in flight per lane
+  constexpr int CU = VS_CPK_CU;  // cells in flight per lane
   const int lane = threadIdx.x & 31;
   const int nc[3] = {ncx, ncy, ncz};
   const int64_t* off = L.off[A_C0 + A];
@@ -1675,6 +1681,39 @@ __global__ void __launch_bounds__(1024) k_order_levels(const NodeRec* __restrict
       if (r.right >= 0 && size[r.right] > 0) pre[r.right] = nxt;
     }
     __syncthreads();
+  }
+}
+
+// The same two passes for big trees over a co-resident grid (cooperative launch), one grid
+// barrier per level instead of two launches per level (the binned trees: 85K-680K rows over
+// 24-32 levels at 1024^3).
+__global__ void __launch_bounds__(1024) k_order_levels_grid(const NodeRec* __restrict__ rec,
+                                                            const int64_t* __restrict__ level_base,
+                                                            int nlevels,
+                                                            const int* __restrict__ sub_count,
+                                                            int* __restrict__ size,
+                                                            int* __restrict__ pre) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int l = nlevels - 1; l >= 0; --l) {
+    const int64_t b0 = level_base[l], b1 = level_base[l + 1];
+    for (int64_t i = b0 + tid; i < b1; i += nth) size[i] = rec_size(rec[i], size, sub_count);
+    grid.sync();
+  }
+  if (tid == 0) pre[0] = 0;
+  grid.sync();
+  for (int l = 0; l < nlevels; ++l) {
+    const int64_t b0 = level_base[l], b1 = level_base[l + 1];
+    for (int64_t i = b0 + tid; i < b1; i += nth) {
+      const NodeRec r = rec[i];
+      if (r.dropped) continue;
+      const int p = pre[i];
+      int nxt = p + 1;
+      if (r.left >= 0 && size[r.left] > 0) { pre[r.left] = nxt; nxt += size[r.left]; }
+      if (r.right >= 0 && size[r.right] > 0) pre[r.right] = nxt;
+    }
+    grid.sync();
   }
 }
 
@@ -3101,6 +3140,9 @@ int d2h(void* dst, const void* src, size_t n, cudaStream_t st) {
 }
 
 constexpr int SPAN_BLOCKS = 148 * 8;
+#ifndef VS_ORDER_GRID
+#define VS_ORDER_GRID 1  // trees > 64K rows: preorder passes over a cooperative grid
+#endif
 #ifndef VS_SUB_LPT
 #define VS_SUB_LPT 1  // k_subtrees launched biggest subtree first (0: in collection order)
 #endif
@@ -3586,15 +3628,35 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
   VS_TRY(sizes.ensure(total * sizeof(int), "sizes"));
   VS_TRY(pre.ensure(total * sizeof(int), "preorder"));
   const int nlev = (int)level_base.size() - 1;
-  if (total <= (1 << 16)) {
+  int order_grid = 0;  // co-resident blocks for k_order_levels_grid (0: not used)
+  if (VS_ORDER_GRID && total > (1 << 16)) {
+    int per_sm = 0, nsm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_order_levels_grid, 1024, 0) ==
+            cudaSuccess &&
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      order_grid = per_sm * nsm;
+    cudaGetLastError();
+  }
+  if (total <= (1 << 16) || order_grid > 0) {
     DBuf lb;
     lb.st = st;
     VS_TRY(lb.ensure(level_base.size() * sizeof(int64_t), "level bases"));
     VS_CUDA(cudaMemcpyAsync(lb.p, level_base.data(), level_base.size() * sizeof(int64_t),
                             cudaMemcpyHostToDevice, st), "level bases");
-    k_order_levels<<<1, 1024, 0, st>>>(rec.as<NodeRec>(), lb.as<int64_t>(), nlev, subc.as<int>(),
-                                       sizes.as<int>(), pre.as<int>());
-    VS_TRY(check_launch("k_order_levels"));
+    if (order_grid > 0) {
+      const NodeRec* rp = rec.as<NodeRec>();
+      const int64_t* lbp = lb.as<int64_t>();
+      const int* scp = subc.as<int>();
+      int* szp = sizes.as<int>();
+      int* prp = pre.as<int>();
+      void* args[] = {&rp, &lbp, (void*)&nlev, &scp, &szp, &prp};
+      VS_CUDA(cudaLaunchCooperativeKernel((void*)k_order_levels_grid, dim3(order_grid),
+                                          dim3(1024), args, 0, st), "k_order_levels_grid");
+    } else {
+      k_order_levels<<<1, 1024, 0, st>>>(rec.as<NodeRec>(), lb.as<int64_t>(), nlev,
+                                         subc.as<int>(), sizes.as<int>(), pre.as<int>());
+      VS_TRY(check_launch("k_order_levels"));
+    }
   } else {
     for (int l = nlev - 1; l >= 0; --l) {
       const int64_t b0 = level_base[l], b1 = level_base[l + 1];
