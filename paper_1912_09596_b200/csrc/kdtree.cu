@@ -3141,7 +3141,10 @@ int d2h(void* dst, const void* src, size_t n, cudaStream_t st) {
 
 constexpr int SPAN_BLOCKS = 148 * 8;
 #ifndef VS_ORDER_GRID
-#define VS_ORDER_GRID 1  // trees > 64K rows: preorder passes over a cooperative grid
+#define VS_ORDER_GRID 1  // trees > VS_ORDER_GRID_MIN rows: preorder passes over a cooperative grid
+#endif
+#ifndef VS_ORDER_GRID_MIN
+#define VS_ORDER_GRID_MIN 65536
 #endif
 #ifndef VS_SUB_LPT
 #define VS_SUB_LPT 1  // k_subtrees launched biggest subtree first (0: in collection order)
@@ -3629,7 +3632,7 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
   VS_TRY(pre.ensure(total * sizeof(int), "preorder"));
   const int nlev = (int)level_base.size() - 1;
   int order_grid = 0;  // co-resident blocks for k_order_levels_grid (0: not used)
-  if (VS_ORDER_GRID && total > (1 << 16)) {
+  if (VS_ORDER_GRID && total > VS_ORDER_GRID_MIN) {
     int per_sm = 0, nsm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_order_levels_grid, 1024, 0) ==
             cudaSuccess &&

@@ -1,8 +1,8 @@
 # Preorder pass A/B on one B200 (dev tool): k-d parity tests (default build), per-variant timings.
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_kdtree.py tests/ref_suite/test_ref_kdtree.py tests/test_gpu_build.py -q -x -m gpu -p no:cacheprovider 2>&1 | tail -3 > gpurun_out/og_tests.log
-timeout 900 python -m pytest tests/test_gpu_scale.py -q -x -m gpu -p no:cacheprovider -k "config2 or config3" 2>&1 | tail -3 >> gpurun_out/og_tests.log
+timeout 900 python -m pytest tests/test_gpu_kdtree.py tests/ref_suite/test_ref_kdtree.py tests/test_gpu_build.py -q -x -m gpu -p no:cacheprovider 2>&1 | tail -3 > gpurun_out/og2_tests.log
+timeout 900 python -m pytest tests/test_gpu_scale.py -q -x -m gpu -p no:cacheprovider -k "config2 or config3" 2>&1 | tail -3 >> gpurun_out/og2_tests.log
 for f in variants/lib_*.so; do
-  echo "== $f" >> gpurun_out/og_time.txt
-  VSB200_LIB=$PWD/$f timeout 300 python tools/time_kd.py 512 1024 >> gpurun_out/og_time.txt 2>&1
+  echo "== $f" >> gpurun_out/og2_time.txt
+  VSB200_LIB=$PWD/$f timeout 300 python tools/time_kd.py 512 1024 >> gpurun_out/og2_time.txt 2>&1
 done
