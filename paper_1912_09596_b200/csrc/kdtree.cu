@@ -80,6 +80,9 @@ enum {
 #define VS_CELL_CHUNK 1024
 #endif
 constexpr int CELL_CHUNK = VS_CELL_CHUNK;
+#ifndef VS_SHRINK_WARP
+#define VS_SHRINK_WARP 1  // binned leaves of bounded size: warp-per-leaf exact shrink
+#endif
 #ifndef VS_CS_CU
 #define VS_CS_CU 1  // k_cell_slabs: cells in flight per lane
 #endif
@@ -1448,6 +1451,74 @@ __global__ void __launch_bounds__(128) k_leaf_shrink(const uint32_t* __restrict_
     }
   }
   __syncthreads();  // red[] is reused by the block's next leaf
+  }
+}
+
+// The same shrink with a warp per leaf (four leaves per 128-thread block, no block barriers)
+// for leaves bounded by a small max-leaf-size (every leaf extent <= mls <= 64: at most 4096
+// rows), four rows per lane group in flight.
+__global__ void __launch_bounds__(128) k_leaf_shrink_warp(const uint32_t* __restrict__ bits,
+                                                          int ny, int nzw, KdLevel L,
+                                                          KdDecision* __restrict__ dec) {
+  const int lane = threadIdx.x & 31;
+  const int nwt = (int)((gridDim.x * blockDim.x) >> 5);
+  for (int i = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < L.n; i += nwt) {
+    if (dec[i].axis >= 0) continue;
+    const Box b = L.box[i];
+    const int ex = b.hi[0] - b.lo[0], ey = b.hi[1] - b.lo[1];
+    const int wz = wz_of(b), gw = group_width(wz), G = 32 / gw;
+    const int g = lane / gw, wl = lane & (gw - 1);
+    const uint32_t gmask = gw == 32 ? 0xffffffffu : ((1u << gw) - 1u);
+    const int rows = ex * ey;
+    int lo0 = KD_FAR, lo1 = KD_FAR, hi0 = -1, hi1 = -1;
+    uint32_t acc = 0;
+    constexpr int U = 4;
+    for (int rb = 0; rb < rows; rb += G * U) {
+      uint32_t v[U];
+      int xs[U], ys[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = rb + u * G + g;
+        v[u] = 0;
+        xs[u] = 0;
+        ys[u] = 0;
+        if (q < rows && wl < wz) {
+          xs[u] = q / ey;
+          ys[u] = q - xs[u] * ey;
+          v[u] = local_word(bits + ((int64_t)(b.lo[0] + xs[u]) * ny + b.lo[1] + ys[u]) * nzw,
+                            b.lo[2], b.hi[2], wl);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t m = __ballot_sync(0xffffffffu, v[u] != 0);
+        if (wl == 0 && ((m >> (g * gw)) & gmask)) {
+          lo0 = min(lo0, xs[u]); hi0 = max(hi0, xs[u]);
+          lo1 = min(lo1, ys[u]); hi1 = max(hi1, ys[u]);
+        }
+        acc |= v[u];
+      }
+    }
+    for (int o = gw; o < 32; o <<= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+    const uint32_t mz = __ballot_sync(0xffffffffu, acc != 0) & gmask;
+    lo0 = __reduce_min_sync(0xffffffffu, lo0);
+    lo1 = __reduce_min_sync(0xffffffffu, lo1);
+    hi0 = __reduce_max_sync(0xffffffffu, hi0);
+    hi1 = __reduce_max_sync(0xffffffffu, hi1);
+    const int wf = mz ? __ffs(mz) - 1 : 0, wlst = mz ? 31 - __clz(mz) : 0;
+    const uint32_t af = __shfl_sync(0xffffffffu, acc, wf), al = __shfl_sync(0xffffffffu, acc, wlst);
+    if (lane == 0) {
+      if (hi0 < 0) {
+        dec[i].dropped = 1;
+      } else {
+        Box t;
+        t.lo[0] = b.lo[0] + lo0; t.hi[0] = b.lo[0] + hi0 + 1;
+        t.lo[1] = b.lo[1] + lo1; t.hi[1] = b.lo[1] + hi1 + 1;
+        t.lo[2] = b.lo[2] + 32 * wf + __ffs(af) - 1;
+        t.hi[2] = b.lo[2] + 32 * wlst + 31 - __clz(al) + 1;
+        dec[i].leaf = t;
+      }
+    }
   }
 }
 
@@ -3514,8 +3585,12 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
             L, P, B, dec.as<KdDecision>(), cnt.as<int64_t>());
       VS_TRY(check_launch("k_decide"));
       // exact shrink for the binned leaves (kdtree.py:474)
-      k_leaf_shrink<<<(unsigned)std::min<int64_t>(n, 148 * 16), 128, 0, st>>>(
-          bits, ny, nzw, L, dec.as<KdDecision>());
+      if (VS_SHRINK_WARP && P.mls >= 0 && P.mls <= 64)  // leaf extents <= mls
+        k_leaf_shrink_warp<<<(unsigned)std::min<int64_t>(cdiv(n, 4), 148 * 16), 128, 0, st>>>(
+            bits, ny, nzw, L, dec.as<KdDecision>());
+      else
+        k_leaf_shrink<<<(unsigned)std::min<int64_t>(n, 148 * 16), 128, 0, st>>>(
+            bits, ny, nzw, L, dec.as<KdDecision>());
       VS_TRY(check_launch("k_leaf_shrink"));
     }
     // next level: child offsets, rows of this level, next boxes and their work sizes
