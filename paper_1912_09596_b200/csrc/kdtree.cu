@@ -3220,6 +3220,9 @@ constexpr int SPAN_BLOCKS = 148 * 8;
 #ifndef VS_SUB_LPT
 #define VS_SUB_LPT 1  // k_subtrees launched biggest subtree first (0: in collection order)
 #endif
+#ifndef VS_BINNED_WPN
+#define VS_BINNED_WPN 8  // warps per node on narrow levels
+#endif
 #ifndef VS_BINNED_NARROW
 #define VS_BINNED_NARROW 1024  // levels of at most this many nodes: 8 warps per node decision
 #endif
@@ -3577,7 +3580,8 @@ int kd_build(const uint32_t* bits, int nx, int ny, int nz, int deep, int mls, in
         VS_CUDA(cudaStreamWaitEvent(st, ev_join, 0), "join wait");
       }
       if (n <= BINNED_NARROW)  // a few big nodes: one CTA of 8 warps per node
-        (cs == 8 ? k_decide_binned<8, 8> : k_decide_binned<0, 8>)<<<(unsigned)n, 256, 0, st>>>(
+        (cs == 8 ? k_decide_binned<8, VS_BINNED_WPN> : k_decide_binned<0, VS_BINNED_WPN>)
+            <<<(unsigned)n, 32 * VS_BINNED_WPN, 0, st>>>(
             L, P, B, dec.as<KdDecision>(), cnt.as<int64_t>());
       else
         (cs == 8 ? k_decide_binned<8, 1> : k_decide_binned<0, 1>)<<<(unsigned)cdiv(n, 4), 128, 0,
