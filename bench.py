@@ -591,7 +591,10 @@ def run_ours(args, rank, ws, local):
         "data": "synthetic",
         "config": {**workload_config(n, nblobs, args.steps),
                    "l2": "input 1 GiB > 126 MB L2 (no flush needed)",
-                   "parallelism": f"image row stripes x{ws} + NCCL all-gather; build replicated",
+                   "parallelism": (f"image row stripes x{ws} + NCCL all-gather; "
+                                   "per-TF build replicated"
+                                   + ("; per-volume presence pass sharded by brick x-slabs"
+                                      if ws > 1 else "")),
                    "pipeline": "rebuild k+1 on a side stream || render k (two index buffers); "
                                "renders on a high-priority stream"},
         "build_ms": build_ms,
